@@ -1,0 +1,208 @@
+"""ctypes binding of the CPU oracle (oracle/bnn_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: importable from tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py. The product package never imports it.
+The oracle shares no code with the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+MLP, RESNET18 = 0, 1
+CE, MSE = 0, 1
+RELU, TANH = 0, 1
+AUG_NONE, AUG_PER_SAMPLE = 0, 1
+
+
+class OrcModel(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n_widths", C.c_int), ("widths", C.c_int * 16),
+                ("in_h", C.c_int), ("in_w", C.c_int), ("in_c", C.c_int),
+                ("n_classes", C.c_int), ("base_width", C.c_int), ("loss", C.c_int),
+                ("act", C.c_int)]
+
+
+def build():
+    subprocess.check_call([os.path.join(_HERE, "build.sh")])
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        src = os.path.join(_HERE, "bnn_oracle.c")
+        if not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+            build()
+        _lib = C.CDLL(_LIB)
+        _lib.orc_log24.restype = C.c_float
+        _lib.orc_log24.argtypes = [C.c_float]
+        _lib.orc_eps.restype = C.c_float
+        _lib.orc_eps.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.c_uint32]
+        _lib.orc_n_params.restype = C.c_long
+        _lib.orc_eps_fill.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]
+        _lib.orc_aug_params.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_philox_fill.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_void_p]
+        _lib.orc_elbo_partial.argtypes = [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int] * 6 + [
+            C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_finalize.argtypes = [C.c_void_p] * 4 + [C.c_double] + [C.c_void_p] * 4
+        _lib.orc_forward.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32,
+                                                                         C.c_int, C.c_void_p]
+        _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
+                                                                         C.c_void_p, C.c_void_p]
+    return _lib
+
+
+def model_struct(model: dict, act: str = "relu") -> OrcModel:
+    m = OrcModel()
+    m.kind = MLP if model["kind"] == "mlp" else RESNET18
+    if model["kind"] == "mlp":
+        w = model["widths"]
+        m.n_widths = len(w)
+        for i, v in enumerate(w):
+            m.widths[i] = v
+    else:
+        m.in_h, m.in_w, m.in_c = model["in_h"], model["in_w"], model["in_c"]
+        m.n_classes = model["n_classes"]
+        m.base_width = model.get("base_width", 64)
+    m.loss = CE if model["loss"] == "ce" else MSE
+    m.act = RELU if act == "relu" else TANH
+    return m
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _d(a):
+    return None if a is None else np.ascontiguousarray(a, np.float64)
+
+
+# ---------------------------------------------------------------- EPS-v1 (docs/EPS.md)
+def philox(ctr, key):
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox_fill(c.ctypes.data, k.ctypes.data, 1, out.ctypes.data)
+    return out
+
+
+def philox_fill(ctr, key, n):
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    out = np.zeros((n, 4), np.uint32)
+    lib().orc_philox_fill(c.ctypes.data, k.ctypes.data, n, out.ctypes.data)
+    return out
+
+
+def log24_all():
+    out = np.empty(1 << 24, np.float32)
+    lib().orc_log24_all(out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def sincos2pi24_all():
+    c = np.empty(1 << 24, np.float32)
+    s = np.empty(1 << 24, np.float32)
+    lib().orc_sincos2pi24_all(c.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p))
+    return c, s
+
+
+def eps(seed, step, s, t, r, c) -> float:
+    return lib().orc_eps(seed, step, s, t, r, c)
+
+
+def eps_fill(seed, step, s, t, r0, nr, c0, nc) -> np.ndarray:
+    out = np.empty((nr, nc), np.float32)
+    lib().orc_eps_fill(seed, step, s, t, r0, nr, c0, nc, out.ctypes.data)
+    return out
+
+
+def aug_params(seed, step, s, b):
+    dx, dy, fl = C.c_int(), C.c_int(), C.c_int()
+    lib().orc_aug_params(seed, step, s, b, C.byref(dx), C.byref(dy), C.byref(fl))
+    return dx.value, dy.value, fl.value
+
+
+# ---------------------------------------------------------------- model
+def n_params(model, act="relu"):
+    m = model_struct(model, act)
+    return lib().orc_n_params(C.byref(m))
+
+
+def tensor_infos(model):
+    m = model_struct(model)
+    n = lib().orc_n_tensors(C.byref(m))
+    out = []
+    info = (C.c_long * 7)()
+    for t in range(n):
+        assert lib().orc_tensor_info(C.byref(m), t, info) == 0
+        out.append(dict(t=t, offset=info[0], rows=info[1], cols=info[2]))
+    return out
+
+
+def elbo_partial(model, mu, rho, x, y_cls, y_reg, B_glob, b_offset, S_glob, s0, s1, seed, step,
+                 aug=AUG_NONE, nthreads=0, act="relu"):
+    m = model_struct(model, act)
+    P = lib().orc_n_params(C.byref(m))
+    mu, rho, x, yr = _d(mu), _d(rho), _d(x), _d(y_reg)
+    yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
+    B_loc = x.shape[0]
+    acc = np.zeros(2 * P + 1, np.float64)
+    rc = lib().orc_elbo_partial(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), B_loc,
+                                b_offset, B_glob, S_glob, s0, s1, seed, step, aug, _p(acc),
+                                nthreads)
+    assert rc == 0, rc
+    return acc
+
+
+def finalize(model, mu, rho, acc, D, act="relu"):
+    m = model_struct(model, act)
+    P = lib().orc_n_params(C.byref(m))
+    mu, rho, acc = _d(mu), _d(rho), _d(acc)
+    gmu = np.zeros(P)
+    grho = np.zeros(P)
+    loss, kl = C.c_double(), C.c_double()
+    rc = lib().orc_finalize(C.byref(m), _p(mu), _p(rho), _p(acc), D, C.byref(loss), C.byref(kl),
+                            _p(gmu), _p(grho))
+    assert rc == 0
+    return dict(loss=loss.value, kl=kl.value, grad_mu=gmu, grad_rho=grho, L_data=acc[2 * P])
+
+
+def elbo_step(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=AUG_NONE, nthreads=0,
+              act="relu"):
+    B = np.asarray(x).shape[0]
+    acc = elbo_partial(model, mu, rho, x, y_cls, y_reg, B, 0, S, 0, S, seed, step, aug, nthreads,
+                       act)
+    return finalize(model, mu, rho, acc, D, act)
+
+
+def forward(model, mu, rho, x, s0, s1, seed, step, aug=AUG_NONE, act="relu"):
+    m = model_struct(model, act)
+    mu, rho, x = _d(mu), _d(rho), _d(x)
+    B = x.shape[0]
+    O = model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]
+    z = np.zeros((s1 - s0, B, O))
+    assert lib().orc_forward(C.byref(m), _p(mu), _p(rho), _p(x), B, s0, s1, seed, step, aug,
+                             _p(z)) == 0
+    return z
+
+
+def predict(model, mu, rho, x, S, seed, step):
+    m = model_struct(model)
+    mu, rho, x = _d(mu), _d(rho), _d(x)
+    B = x.shape[0]
+    O = model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]
+    mean = np.zeros((B, O))
+    var = np.zeros((B, O))
+    assert lib().orc_predict(C.byref(m), _p(mu), _p(rho), _p(x), B, S, seed, step, _p(mean),
+                             _p(var)) == 0
+    return mean, var

@@ -1,0 +1,77 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds none of the method's arithmetic: it only draws μ, ρ, x and y with
+numpy so that the oracle and the CUDA path see the same numbers. The recipe follows
+SURVEY.md §8(d) and is restated in DESIGN.md §5:
+
+* μ ~ N(0, 2/fan_in) (Kaiming), weights and biases alike ("initialized in the
+  same fashion as for a non-Bayesian network"; biases are variational).
+* ρ = softplus⁻¹(c/fan_in) with c = 1 ("constant value that depends on the layer size",
+  PAPER.md:148; "scaled inversely with the layer width"), or, for the
+  finite-difference and gradient-checking tests, ρ ~ U(-3, 0) so σ ∈ [0.05, 0.69].
+* MLP regression (C1): x ~ N(0,1)^8; y = a fixed random 8-16-1 ReLU teacher + N(0, 0.1²).
+* MLP classification (C2): x ~ U[0,1]^784 (MNIST-like intensities); labels uniform.
+* CNN (C3-C5): x ~ N(0,1) NHWC 32×32×3 (post-normalisation CIFAR-like); labels uniform.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .configs import input_shape, layout, n_outputs, n_params
+
+
+def _softplus_inv(s: np.ndarray) -> np.ndarray:
+    # ρ such that log(1 + e^ρ) = s; expm1 keeps small s accurate
+    return np.log(np.expm1(s))
+
+
+def init_params(model: dict, seed: int = 2, rho_mode: str = "init", sigma_c: float = 1.0):
+    """Return (mu, rho) as float32 arrays of length n_params(model)."""
+    rng = np.random.default_rng(seed)
+    P = n_params(model)
+    mu = np.empty(P, np.float64)
+    rho = np.empty(P, np.float64)
+    for ti in layout(model):
+        n = ti["rows"] * ti["cols"]
+        sl = slice(ti["offset"], ti["offset"] + n)
+        mu[sl] = rng.normal(0.0, math.sqrt(2.0 / ti["fan_in"]), n)
+        if rho_mode == "init":
+            rho[sl] = _softplus_inv(np.full(n, sigma_c / ti["fan_in"]))
+        elif rho_mode == "wide":
+            rho[sl] = rng.uniform(-3.0, 0.0, n)
+        elif rho_mode == "tiny":
+            rho[sl] = -40.0
+        else:
+            raise ValueError(rho_mode)
+    return mu.astype(np.float32), rho.astype(np.float32)
+
+
+def make_batch(model: dict, B: int, seed: int = 1):
+    """Return (x, y_cls, y_reg): x float32 [B, *input_shape]; exactly one of y_* is set."""
+    rng = np.random.default_rng(seed)
+    shp = input_shape(model)
+    O = n_outputs(model)
+    if model["kind"] == "mlp" and model["loss"] == "mse":
+        x = rng.normal(0.0, 1.0, (B,) + shp)
+        # fixed teacher network: widths of the model, ReLU hidden layers
+        w = model["widths"]
+        trng = np.random.default_rng(12345)
+        h = x
+        for i in range(1, len(w)):
+            W = trng.normal(0.0, math.sqrt(2.0 / w[i - 1]), (w[i], w[i - 1]))
+            h = h @ W.T
+            if i < len(w) - 1:
+                h = np.maximum(h, 0.0)
+        y = h + rng.normal(0.0, 0.1, h.shape)
+        return x.astype(np.float32), None, y.astype(np.float32)
+    if model["kind"] == "mlp":
+        x = rng.uniform(0.0, 1.0, (B,) + shp)
+    else:
+        x = rng.normal(0.0, 1.0, (B,) + shp)
+    if model["loss"] == "ce":
+        y = rng.integers(0, O, B).astype(np.int32)
+        return x.astype(np.float32), y, None
+    y = rng.normal(0.0, 1.0, (B, O))
+    return x.astype(np.float32), None, y.astype(np.float32)

@@ -1,0 +1,117 @@
+"""An independent fp64 PyTorch-CPU formulation of the ELBO step, used only to pin the oracle.
+
+Forward uses library routines (F.linear, F.conv2d, F.cross_entropy, F.softplus); the
+backward is torch autograd. It shares no code with oracle/bnn_oracle.c: only the ε values
+(oracle.eps_fill, itself pinned in test_eps_oracle.py) and the augmentation offsets
+(oracle.aug_params) are taken from the oracle, so that both evaluate the same draw.
+"""
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+import oracle as O
+from paper_2604_04736_b200.configs import layout
+
+
+def _augment(x, seed, step, s, b_global):
+    """docs/EPS.md §4: zero-pad by 4, crop at (dy, dx), then optional horizontal flip."""
+    dx, dy, fl = O.aug_params(seed, step, s, b_global)
+    H, W, C = x.shape
+    p = torch.zeros(H + 8, W + 8, C, dtype=x.dtype)
+    p[4:4 + H, 4:4 + W] = x
+    out = p[dy:dy + H, dx:dx + W]
+    if fl:
+        out = torch.flip(out, dims=[1])
+    return out
+
+
+def _forward(model, ws, x, act):
+    """x: [B, features] (MLP) or [B, H, W, C] (CNN); ws: list of tensors in layout order."""
+    a = torch.relu if act == "relu" else torch.tanh
+    if model["kind"] == "mlp":
+        h = x
+        n = len(ws) // 2
+        for l in range(n):
+            W, b = ws[2 * l], ws[2 * l + 1].reshape(-1)
+            h = F.linear(h, W, b)
+            if l < n - 1:
+                h = a(h)
+        return h
+    # ResNet-18 (reading R12), NCHW for torch
+    cin = model["in_c"]
+    it = iter(range(len(ws) // 2))
+
+    def conv(h, stride, pad, k):
+        l = next(it)
+        W = ws[2 * l]
+        cout = W.shape[0]
+        W4 = W.reshape(cout, k, k, -1).permute(0, 3, 1, 2)
+        return F.conv2d(h, W4, ws[2 * l + 1].reshape(-1), stride=stride, padding=pad)
+
+    h = x.permute(0, 3, 1, 2)
+    h = a(conv(h, 1, 1, 3))
+    bw = model.get("base_width", 64)
+    width = bw
+    for stage in range(4):
+        cout = bw << stage
+        for blk in range(2):
+            stride = 2 if (stage > 0 and blk == 0) else 1
+            y = a(conv(h, stride, 1, 3))
+            y = conv(y, 1, 1, 3)
+            if stride != 1 or width != cout:
+                sc = conv(h, stride, 0, 1)
+            else:
+                sc = h
+            h = a(y + sc)
+            width = cout
+    h = h.mean(dim=(2, 3))
+    l = next(it)
+    return F.linear(h, ws[2 * l], ws[2 * l + 1].reshape(-1))
+
+
+def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu"):
+    """Return loss, L_data, KL, grad_mu, grad_rho (numpy fp64) via autograd."""
+    lay = layout(model)
+    mu_t = torch.tensor(np.asarray(mu, np.float64), requires_grad=True)
+    rho_t = torch.tensor(np.asarray(rho, np.float64), requires_grad=True)
+    sigma = F.softplus(rho_t)
+    X = torch.tensor(np.asarray(x, np.float64))
+    B = X.shape[0]
+    L_data = 0.0
+    for s in range(S):
+        ws = []
+        for ti in lay:
+            n = ti["rows"] * ti["cols"]
+            sl = slice(ti["offset"], ti["offset"] + n)
+            e = torch.tensor(O.eps_fill(seed, step, s, ti["t"], 0, ti["rows"], 0, ti["cols"])
+                             .astype(np.float64)).reshape(-1)
+            ws.append((mu_t[sl] + sigma[sl] * e).reshape(ti["rows"], ti["cols"]))
+        Xs = X
+        if aug:
+            Xs = torch.stack([_augment(X[b], seed, step, s, b) for b in range(B)])
+        z = _forward(model, ws, Xs, act)
+        if model["loss"] == "ce":
+            l = F.cross_entropy(z, torch.tensor(np.asarray(y_cls, np.int64)), reduction="mean")
+        else:
+            l = F.mse_loss(z, torch.tensor(np.asarray(y_reg, np.float64)), reduction="mean")
+        L_data = L_data + l / S
+    kl = 0.5 * torch.sum(sigma ** 2 + mu_t ** 2 - 1.0 - torch.log(sigma ** 2))
+    loss = L_data + kl / D
+    loss.backward()
+    return dict(loss=loss.item(), L_data=float(L_data.detach()), kl=kl.item(),
+                grad_mu=mu_t.grad.numpy().copy(), grad_rho=rho_t.grad.numpy().copy())
+
+
+def deterministic(model, mu, x, y_cls, y_reg):
+    """σ = 0 exactly: the plain network with weights μ; returns (data loss, d loss / d μ)."""
+    lay = layout(model)
+    mu_t = torch.tensor(np.asarray(mu, np.float64), requires_grad=True)
+    ws = [mu_t[t["offset"]:t["offset"] + t["rows"] * t["cols"]].reshape(t["rows"], t["cols"])
+          for t in lay]
+    z = _forward(model, ws, torch.tensor(np.asarray(x, np.float64)), "relu")
+    if model["loss"] == "ce":
+        l = F.cross_entropy(z, torch.tensor(np.asarray(y_cls, np.int64)))
+    else:
+        l = F.mse_loss(z, torch.tensor(np.asarray(y_reg, np.float64)))
+    l.backward()
+    return l.item(), mu_t.grad.numpy().copy()
