@@ -1,0 +1,209 @@
+/*
+ * bnn.h — C ABI of libbnn.so, the B200-native Bayes-by-backprop ELBO step with sampling
+ * parallelism (arXiv 2604.04736, "Sampling Parallelism for Fast and Efficient Bayesian
+ * Learning").
+ *
+ * The library computes, for a mean-field Gaussian BNN with variational parameters (μ, ρ),
+ * σ = softplus(ρ), one minibatch (x, y), S Monte-Carlo samples, a 64-bit seed and a step
+ * counter:
+ *     w_s    = μ + σ ⊙ ε_s,  ε_s from EPS-v1 (docs/EPS.md)       PAPER.md:158-159 (Alg. 1 l.5-6)
+ *     ŷ_s    = ForwardPass(x, w_s)                               PAPER.md:160 (Alg. 1 l.7)
+ *     L_data = (1/S) Σ_s Loss(ŷ_s, y)                            PAPER.md:162 (Alg. 1 l.9)
+ *     KL     = ½ Σ_i (σ_i² + μ_i² − 1 − log σ_i²)                PAPER.md:163 (Alg. 1 l.10)
+ *     loss   = L_data + KL / |D|                                 PAPER.md:164 (Alg. 1 l.11)
+ *     grad_μ = ∂loss/∂μ,  grad_ρ = ∂loss/∂ρ                      PAPER.md:165 (Alg. 1 l.12)
+ * with the S samples (and optionally the batch) sharded over the ranks of one node and a
+ * single SUM-allreduce of the gradient partials (§4.1, Alg. 2
+ * PAPER.md:250-264; hybrid sample×data grid PAPER.md:283-295, §4.2). The optimizer step
+ * (Alg. 1 l.13) is the caller's. Readings of points the paper leaves open are DESIGN.md §2.
+ *
+ * Conventions for every entry point:
+ *  - Return value: BNN_OK (0) or a bnn_status code; bnn_last_error() names the violated
+ *    invariant. Entry points never abort the process.
+ *  - Pointers named *_dev are CUDA device pointers on cfg.device; *_host are host pointers.
+ *    Unless stated, tensors are dense, row-major, 16-byte aligned (256-byte preferred).
+ *  - The caller owns every tensor passed in. The library owns its workspace (allocated in
+ *    bnn_init, never inside a step), its NCCL communicator and its CUDA streams/events.
+ *  - All device work is enqueued on cfg.stream (NULL: a stream the library creates); calls
+ *    return after enqueue unless a *_host output is requested, which synchronises.
+ *  - A bnn_ctx is used by one host thread at a time.
+ *  - There is no CPU fallback: without a usable sm_100 device bnn_init fails with
+ *    BNN_ERR_CUDA.
+ *
+ * Parameter layout: a flat fp32 vector of n_params entries; for each layer
+ * l in model order, weight tensor t = 2l viewed as [rows = c_out, cols = kh·kw·c_in]
+ * (OHWI, c_in fastest; a linear layer is kh = kw = 1), then bias tensor t = 2l+1 viewed as
+ * [1, c_out]. μ, ρ, grad_μ and grad_ρ all use this layout.
+ */
+#ifndef BNN_H_
+#define BNN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BNN_ABI_VERSION 1
+
+typedef enum {
+    BNN_OK = 0,
+    BNN_ERR_CONFIG = 2,  /* invalid model/config/shape/alignment (SPEC.md:426-428 invariants) */
+    BNN_ERR_COMM = 3,    /* NCCL error or timeout */
+    BNN_ERR_NUMERIC = 4, /* non-finite loss (only checked when the loss is read on the host) */
+    BNN_ERR_CUDA = 5     /* CUDA runtime/driver error, or no sm_100 device */
+} bnn_status;
+
+enum { BNN_MODEL_MLP = 0, BNN_MODEL_RESNET18 = 1 };
+enum { BNN_LOSS_CE = 0, BNN_LOSS_MSE = 1 };
+enum { BNN_PREC_FP32 = 0, BNN_PREC_BF16 = 1 };
+enum { BNN_MODE_SAMPLE_SHARDED = 0, BNN_MODE_DATA_SHARDED = 1, BNN_MODE_HYBRID = 2 };
+enum { BNN_AUG_NONE = 0, BNN_AUG_PER_SAMPLE = 1 };
+
+/* Model description.
+ *  MLP:      widths[0] = input features, widths[n_widths-1] = outputs; ReLU between layers.
+ *  RESNET18: CIFAR ResNet-18 topology without BatchNorm (reading R12): 3×3 stem,
+ *            4 stages × 2 BasicBlocks of widths base_width·{1,2,4,8}, stride-2 1×1
+ *            projections, global average pool, linear head to n_classes. Input NHWC fp32. */
+typedef struct bnn_model_desc {
+    int32_t kind;
+    int32_t n_widths;
+    int32_t widths[16];
+    int32_t in_h, in_w, in_c;
+    int32_t n_classes;
+    int32_t base_width;
+    int32_t loss; /* BNN_LOSS_CE (labels int32) | BNN_LOSS_MSE (targets fp32 [B, outputs]) */
+} bnn_model_desc;
+
+/* Run configuration. Rank r of world P = K·G is sample group k = r / G, data group
+ * g = r % G; it owns global samples [k·S/K, (k+1)·S/K) and global examples
+ * [g·B/G, (g+1)·B/G). SAMPLE_SHARDED forces K = world, G = 1;
+ * DATA_SHARDED forces K = 1, G = world; HYBRID takes K, G as given. */
+typedef struct bnn_config {
+    int32_t precision;        /* BNN_PREC_FP32 (SIMT fp32, parity mode) | BNN_PREC_BF16 (tcgen05) */
+    int32_t mode;             /* BNN_MODE_* */
+    int32_t K, G;             /* HYBRID grid; ignored otherwise */
+    int32_t rank, world;
+    const uint8_t* nccl_uid;  /* 128-byte id from bnn_get_unique_id on rank 0 (broadcast by the
+                                 caller), or NULL: no communicator. With NULL and world > 1 the
+                                 context is a "virtual rank": use bnn_elbo_partial/bnn_finalize. */
+    int32_t max_B_loc;        /* largest per-rank batch a step will pass */
+    int32_t max_S_loc;        /* largest per-rank sample count a step will use */
+    int32_t sample_chunk;     /* samples processed together (0 = all local samples) */
+    int32_t aug;              /* BNN_AUG_NONE | BNN_AUG_PER_SAMPLE (images only; docs/EPS.md §4) */
+    double dataset_size;      /* |D| of PAPER.md:164, > 0 */
+    int32_t device;           /* CUDA device ordinal */
+    void* stream;             /* cudaStream_t or NULL */
+} bnn_config;
+
+typedef struct bnn_tensor_info {
+    int64_t offset;  /* element offset in the flat parameter vector */
+    int32_t rows;    /* c_out (weights) or 1 (biases) */
+    int32_t cols;    /* kh·kw·c_in (weights) or c_out (biases) */
+    int32_t t;       /* tensor index used by EPS-v1 keys */
+    int32_t is_bias;
+} bnn_tensor_info;
+
+typedef struct bnn_ctx bnn_ctx;
+
+/* NCCL unique id for a new communicator; call on rank 0 and broadcast the 128 bytes. */
+int bnn_get_unique_id(uint8_t out[128]);
+
+/* Validate model and config, select the device, build the layer graph and parameter
+ * layout, allocate all workspace, create the NCCL communicator (if nccl_uid != NULL).
+ * Errors: BNN_ERR_CONFIG (e.g. "world == K*G", "S mod K == 0" is checked per step),
+ * BNN_ERR_CUDA (no sm_100 device / out of memory), BNN_ERR_COMM. */
+int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out);
+
+/* Parameter layout: *n_params total entries; up to max_infos tensor records written to
+ * infos (may be NULL); *n_tensors receives the tensor count. */
+int bnn_param_layout(bnn_ctx* ctx, int64_t* n_params, int32_t* n_tensors,
+                     bnn_tensor_info* infos, int32_t max_infos);
+
+/* One full ELBO step on this rank: σ prologue, (augmentation), per local
+ * sample chunk: sampled forward, loss head, sampled backward with the sample-accumulating
+ * wgrad epilogue; SUM-allreduce of [acc_μ | acc_ρ | L_data] over all ranks; finalize + KL.
+ *   mu_dev, rho_dev        [n_params] fp32, identical on all ranks
+ *   x_dev                  this rank's examples [B_loc, features] (MLP) or [B_loc, H, W, C]
+ *                          NHWC (ResNet) fp32
+ *   ycls_dev / yreg_dev    int32 [B_loc] labels (CE) or fp32 [B_loc, outputs] (MSE); the
+ *                          other is NULL
+ *   B_loc, B_global        per-rank and global batch (B_global == G·B_loc)
+ *   S_global               global sample count (S_global mod K == 0, S_global/K ≤ max_S_loc)
+ *   seed, step             EPS-v1 key and counter word (docs/EPS.md §1)
+ *   loss_dev               device fp32 scalar (may be NULL)
+ *   loss_host              if non-NULL, the loss is copied back (synchronises) and checked
+ *                          for finiteness (BNN_ERR_NUMERIC)
+ *   grad_mu_dev, grad_rho_dev  [n_params] fp32 outputs, identical on all ranks on return */
+int bnn_elbo_step(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* x_dev,
+                  const int32_t* ycls_dev, const float* yreg_dev, int32_t B_loc,
+                  int32_t B_global, int32_t S_global, uint64_t seed, uint32_t step,
+                  float* loss_dev, double* loss_host, float* grad_mu_dev, float* grad_rho_dev);
+
+/* Same step with the minibatch in HOST memory (pinned recommended): x/y are copied into
+ * library-owned device buffers on the ctx stream inside the call, and the loss is read
+ * back into *loss_host (synchronises). The end-to-end path of bench.py. */
+int bnn_elbo_step_host(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev,
+                       const float* x_host, const int32_t* ycls_host, const float* yreg_host,
+                       int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                       uint32_t step, double* loss_host, float* grad_mu_dev,
+                       float* grad_rho_dev);
+
+/* Layout of the gradient-partial ("acc") buffer exchanged by the allreduce: acc_μ at 0,
+ * acc_ρ at *rho_offset (n_params rounded up to 64 so every segment is 256-byte aligned),
+ * the L_data partial at *loss_offset; *total floats in all. */
+int bnn_acc_layout(bnn_ctx* ctx, int64_t* rho_offset, int64_t* loss_offset, int64_t* total);
+
+/* This rank's shard only, no collective and no finalize: writes acc_dev (bnn_acc_layout) =
+ * [Σ_s dW_s | Σ_s dW_s ⊙ ε_s | L_data partial], each pre-scaled by the global 1/(S·B)
+ * (reading R8). Summing the acc of every rank of a K×G grid and calling
+ * bnn_finalize equals bnn_elbo_step. */
+int bnn_elbo_partial(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev,
+                     const float* x_dev, const int32_t* ycls_dev, const float* yreg_dev,
+                     int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                     uint32_t step, float* acc_dev);
+
+/* Finalize + KL (Alg. 1 l.10-12) from a summed acc buffer:
+ *   grad_μ = acc_μ + μ/|D|;  grad_ρ = sigmoid(ρ)·(acc_ρ + (σ − 1/σ)/|D|);
+ *   loss = acc[2P] + ½Σ(σ² + μ² − 1 − 2 ln σ)/|D|. */
+int bnn_finalize(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* acc_dev,
+                 float* loss_dev, float* grad_mu_dev, float* grad_rho_dev);
+
+/* Posterior predictive over S_global samples: per output element
+ * the mean and the population variance (÷S) of softmax probabilities (CE) or outputs
+ * (MSE). x_dev holds all B examples (predict is sample-sharded only); every rank returns
+ * the full [B, outputs] mean_dev/var_dev after an allgather of per-rank (mean, M2, n). */
+int bnn_predict(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* x_dev,
+                int32_t B, int32_t S_global, uint64_t seed, uint32_t step, float* mean_dev,
+                float* var_dev);
+
+/* EPS-v1 ε (docs/EPS.md) for tensor t, sample s, rows [r0, r0+nr), cols [c0, c0+nc):
+ * out_dev[i·nc + j] = ε(seed, step, s, t, r0+i, c0+j). Stand-alone K1 kernel, used by the
+ * bit-exactness tests. stream may be NULL (legacy default stream). */
+int bnn_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
+                 uint32_t nr, uint32_t c0, uint32_t nc, float* out_dev, void* stream);
+
+/* ε-throughput microbenchmark (the ALU roofline of DESIGN.md §4): generates n4·4 normals
+ * with the same code as the fused kernels and reduces them into sink_dev[grid] instead of
+ * storing them. */
+int bnn_eps_bench(uint64_t n4, uint64_t seed, float* sink_dev, int32_t grid, void* stream);
+
+/* Per-kernel-class device timing, measured with CUDA events on the ctx stream around each
+ * launch while enabled (bench.py's roofline). names: comma-separated classes. */
+int bnn_profile_enable(bnn_ctx* ctx, int32_t on);
+int bnn_profile_read(bnn_ctx* ctx, char* names, int32_t names_cap, double* ms, int64_t* launches,
+                     int32_t max_entries, int32_t* n_entries);
+
+/* Number of kernels the library launched since bnn_init (bench.py's gpu_launches). */
+int64_t bnn_launch_count(bnn_ctx* ctx);
+
+/* Message for the last error on ctx (or the last context-free error if ctx is NULL). */
+const char* bnn_last_error(bnn_ctx* ctx);
+
+void bnn_destroy(bnn_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNN_H_ */

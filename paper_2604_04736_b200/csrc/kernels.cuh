@@ -1,0 +1,72 @@
+// kernels.cuh — launcher declarations of libbnn's CUDA kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "eps.cuh"
+
+namespace bnn {
+
+// One sampled layer: W_s = μ + σ ⊙ ε_s over tensor t_w ([N, K]) and bias t_b ([1, N]).
+struct SampledLayer {
+    const float* mu;     // full μ vector
+    const float* sigma;  // full σ = softplus(ρ) vector (written once per step by K7)
+    int64_t off_w, off_b;
+    int N, K;            // rows (outputs), cols (fan-in)
+    uint32_t t_w, t_b;
+};
+
+struct SampleKeys {
+    EpsKey key;
+    uint32_t step;
+    uint32_t s0;  // global index of the first sample of the chunk
+};
+
+// ---------------------------------------------------------------- K7 / K8 / K6 / K10 / K1
+void launch_sigma(const float* rho, float* sigma, int64_t n, cudaStream_t st);
+// grad_μ, grad_ρ, KL block partials (double), then loss = acc[2P] + KL/D
+// loss[0] = L_data + KL/D, loss[1] = KL
+void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
+                     const float* acc_rho, const float* Ldata, int64_t P, double D,
+                     float* grad_mu, float* grad_rho, double* kl_partials, int n_part,
+                     float* loss, cudaStream_t st);
+int finalize_partials_count(int64_t P);
+// loss head on logits [S][B][O] fp32: writes dZ (unscaled gradient seed) as fp32 or bf16 with
+// row stride ldg, and per-(s,b) loss values.
+void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,
+                      const int32_t* ycls, const float* yreg, void* dz, int ldg, bool dz_bf16,
+                      float* lossrow, cudaStream_t st);
+// acc[2P] += scale · Σ lossrow[0..n) in fixed order
+void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slot,
+                        cudaStream_t st);
+void launch_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
+                     uint32_t nr, uint32_t c0, uint32_t nc, float* out, cudaStream_t st);
+void launch_eps_bench(uint64_t n4, uint64_t seed, float* sink, int grid, cudaStream_t st);
+// predict: probabilities/outputs [S][B][O] → local mean and M2 (two-pass)
+void launch_predict_stats(const float* logits, int S, int B, int O, int loss_kind, float* mean,
+                          float* m2, cudaStream_t st);
+// ordered Chan merge of per-rank (mean, M2, n) [R][BO] → mean, var (÷ total n)
+void launch_predict_merge(const float* means, const float* m2s, const float* counts, int R,
+                          int BO, float* mean, float* var, cudaStream_t st);
+// x fp32 [B][K] → bf16 [B][ldx] (zero padding of columns K..ldx)
+void launch_to_bf16(const float* x, int B, int K, int ldx, void* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- K11: FP32 SIMT sampled GEMMs
+// Z[s][b][n] = act(Σ_k A[s][b][k]·W_s[n][k] + b_s[n]) for s in [0, S), b in [0, B).
+void launch_fwd_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* A,
+                     int64_t strideA, float* Z, int64_t strideZ, bool relu, cudaStream_t st);
+// dA[s][b][k] = (Σ_n G[s][b][n]·W_s[n][k]) · 1[A[s][b][k] > 0]
+void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
+                       int64_t strideG, const float* Aprev, int64_t strideA, float* dA,
+                       int64_t strideD, cudaStream_t st);
+// acc_μ[n][k] += scale·Σ_s dW_s[n][k]; acc_ρ[n][k] += scale·Σ_s dW_s[n][k]·ε_s[n][k] with
+// dW_s = Σ_b G[s][b][n]·A[s][b][k]; plus the bias: db_s[n] = Σ_b G[s][b][n].
+void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
+                       int64_t strideG, const float* A, int64_t strideA, float scale,
+                       float* acc_mu, float* acc_rho, cudaStream_t st);
+// bias part of the above for bf16 or fp32 G with row stride ldg
+void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, int B, const void* G,
+                      int64_t strideG, int ldg, bool g_bf16, float scale, float* acc_mu,
+                      float* acc_rho, cudaStream_t st);
+
+}  // namespace bnn

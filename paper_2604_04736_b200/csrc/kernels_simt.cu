@@ -1,0 +1,567 @@
+// kernels_simt.cu — HBM-bound elementwise/reduction kernels (K1, K6, K7, K8, K10) and the
+// FP32 SIMT sampled-GEMM kernels of the FP32 parity mode (K11).
+//
+// Equations (DESIGN.md §1 cites each to PAPER.md):
+//   σ = softplus(ρ)                                          K7, R1
+//   W_s[n][k] = fma(σ, ε_s, μ) rounded once in fp32           PAPER.md:159 (Alg. 1 l.6)
+//   CE: ℓ = logsumexp(z) − z_y, dℓ/dz = softmax(z) − onehot    PAPER.md:162, R5/R6
+//   MSE: ℓ = Σ_o (z−y)², dℓ/dz = 2(z−y)                        PAPER.md:162, :320, R7
+//   grad_μ = acc_μ + μ/|D|; grad_ρ = sigmoid(ρ)(acc_ρ + (σ − 1/σ)/|D|)
+//   KL = ½ Σ (σ² + μ² − 1 − 2 ln σ)
+#include <algorithm>
+
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace bnn {
+
+// ====================================================================== K7: σ prologue
+__global__ void sigma_kernel(const float* __restrict__ rho, float* __restrict__ sigma,
+                             int64_t n) {
+    const int64_t n4 = n / 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 r = reinterpret_cast<const float4*>(rho)[i];
+        reinterpret_cast<float4*>(sigma)[i] =
+            make_float4(softplus_f(r.x), softplus_f(r.y), softplus_f(r.z), softplus_f(r.w));
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        sigma[i] = softplus_f(rho[i]);
+}
+
+void launch_sigma(const float* rho, float* sigma, int64_t n, cudaStream_t st) {
+    int grid = (int)std::min<int64_t>((n / 4 + 255) / 256 + 1, kNumSMs * 8);
+    sigma_kernel<<<grid, 256, 0, st>>>(rho, sigma, n);
+}
+
+// ====================================================================== K8: finalize + KL
+__device__ __forceinline__ double fin_one(float mu, float rho, float am, float ar, float invD,
+                                          float& gm, float& gr) {
+    const float sg = softplus_f(rho);
+    gm = am + mu * invD;
+    gr = sigmoid_f(rho) * (ar + (sg - 1.0f / sg) * invD);
+    const float ls = log_sigma_f(rho, sg);
+    return 0.5 * ((double)sg * sg + (double)mu * mu - 1.0 - 2.0 * (double)ls);
+}
+
+__global__ void __launch_bounds__(256) finalize_kernel(
+    const float* __restrict__ mu, const float* __restrict__ rho, const float* __restrict__ acc_mu,
+    const float* __restrict__ acc_rho, int64_t P, float invD, float* __restrict__ grad_mu,
+    float* __restrict__ grad_rho, double* __restrict__ kl_partials) {
+    double kl = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t P4 = P / 4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
+        const float4 m = reinterpret_cast<const float4*>(mu)[i];
+        const float4 r = reinterpret_cast<const float4*>(rho)[i];
+        const float4 a = reinterpret_cast<const float4*>(acc_mu)[i];
+        const float4 b = reinterpret_cast<const float4*>(acc_rho)[i];
+        float4 gm, gr;
+        kl += fin_one(m.x, r.x, a.x, b.x, invD, gm.x, gr.x);
+        kl += fin_one(m.y, r.y, a.y, b.y, invD, gm.y, gr.y);
+        kl += fin_one(m.z, r.z, a.z, b.z, invD, gm.z, gr.z);
+        kl += fin_one(m.w, r.w, a.w, b.w, invD, gm.w, gr.w);
+        reinterpret_cast<float4*>(grad_mu)[i] = gm;
+        reinterpret_cast<float4*>(grad_rho)[i] = gr;
+    }
+    for (int64_t i = 4 * P4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
+        float gm, gr;
+        kl += fin_one(mu[i], rho[i], acc_mu[i], acc_rho[i], invD, gm, gr);
+        grad_mu[i] = gm;
+        grad_rho[i] = gr;
+    }
+    __shared__ double red[8];
+    kl = warp_sum(kl);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = kl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        kl_partials[blockIdx.x] = t;
+    }
+}
+
+__global__ void finalize_loss_kernel(const double* __restrict__ kl_partials, int n,
+                                     const float* __restrict__ Ldata, double invD,
+                                     float* __restrict__ loss) {
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += kl_partials[i];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double kl = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) kl += red[w];
+        loss[0] = (float)((double)Ldata[0] + kl * invD);
+        loss[1] = (float)kl;
+    }
+}
+
+int finalize_partials_count(int64_t P) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((P / 4 + 255) / 256, kNumSMs * 8));
+}
+
+void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
+                      const float* acc_rho, const float* Ldata, int64_t P, double D,
+                      float* grad_mu, float* grad_rho, double* kl_partials, int n_part,
+                      float* loss, cudaStream_t st) {
+    finalize_kernel<<<n_part, 256, 0, st>>>(mu, rho, acc_mu, acc_rho, P, (float)(1.0 / D),
+                                            grad_mu, grad_rho, kl_partials);
+    finalize_loss_kernel<<<1, 1024, 0, st>>>(kl_partials, n_part, Ldata, 1.0 / D, loss);
+}
+
+// ====================================================================== K6: loss head
+__global__ void loss_head_kernel(const float* __restrict__ logits, int rows, int B, int O,
+                                 int loss_kind, const int32_t* __restrict__ ycls,
+                                 const float* __restrict__ yreg, void* __restrict__ dz, int ldg,
+                                 int dz_bf16, float* __restrict__ lossrow) {
+    const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (warp >= rows) return;
+    const int b = warp % B;
+    const float* z = logits + (int64_t)warp * O;
+    float loss = 0.0f;
+    auto put = [&](int k, float v) {
+        if (dz_bf16)
+            reinterpret_cast<__nv_bfloat16*>(dz)[(int64_t)warp * ldg + k] = __float2bfloat16_rn(v);
+        else
+            reinterpret_cast<float*>(dz)[(int64_t)warp * ldg + k] = v;
+    };
+    if (loss_kind == 0) {  // CE
+        float m = -INFINITY;
+        for (int k = lane; k < O; k += 32) m = fmaxf(m, z[k]);
+        m = warp_max(m);
+        float se = 0.0f;
+        for (int k = lane; k < O; k += 32) se += expf(z[k] - m);
+        se = warp_sum(se);
+        const float lse = m + logf(se);
+        const int y = ycls[b];
+        for (int k = lane; k < O; k += 32) put(k, expf(z[k] - lse) - (k == y ? 1.0f : 0.0f));
+        loss = lse - z[y];
+    } else {  // MSE
+        float l = 0.0f;
+        for (int k = lane; k < O; k += 32) {
+            const float d = z[k] - yreg[(int64_t)b * O + k];
+            l += d * d;
+            put(k, 2.0f * d);
+        }
+        loss = warp_sum(l);
+    }
+    for (int k = O + lane; k < ldg; k += 32) put(k, 0.0f);
+    if (lane == 0) lossrow[warp] = loss;
+}
+
+void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,
+                      const int32_t* ycls, const float* yreg, void* dz, int ldg, bool dz_bf16,
+                      float* lossrow, cudaStream_t st) {
+    const int rows = S * B;
+    loss_head_kernel<<<(rows + 7) / 8, 256, 0, st>>>(logits, rows, B, O, loss_kind, ycls, yreg,
+                                                     dz, ldg, dz_bf16 ? 1 : 0, lossrow);
+}
+
+__global__ void loss_reduce_kernel(const float* __restrict__ lossrow, int n, float scale,
+                                   float* __restrict__ acc_slot) {
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += (double)lossrow[i];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        acc_slot[0] = (float)((double)acc_slot[0] + s * (double)scale);
+    }
+}
+
+void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slot,
+                        cudaStream_t st) {
+    loss_reduce_kernel<<<1, 1024, 0, st>>>(lossrow, n, scale, acc_slot);
+}
+
+// ====================================================================== K1: ε fill / bench
+__global__ void eps_fill_kernel(EpsKey key, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
+                                uint32_t nr, uint32_t c0, uint32_t nc, float* __restrict__ out) {
+    const uint64_t n = (uint64_t)nr * nc;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = (uint32_t)(i / nc), c = (uint32_t)(i % nc);
+        out[i] = eps1(key, step, s, t, r0 + r, c0 + c);
+    }
+}
+
+void launch_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
+                     uint32_t nr, uint32_t c0, uint32_t nc, float* out, cudaStream_t st) {
+    const uint64_t n = (uint64_t)nr * nc;
+    const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)kNumSMs * 16);
+    eps_fill_kernel<<<std::max(grid, 1), 256, 0, st>>>(make_key(seed), step, s, t, r0, nr, c0,
+                                                       nc, out);
+}
+
+__global__ void __launch_bounds__(256) eps_bench_kernel(uint64_t n4, EpsKey key,
+                                                        float* __restrict__ sink) {
+    float acc = 0.0f;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const float4 e = eps4(key, 0u, 0u, 0u, (uint32_t)(i >> 32), (uint32_t)i);
+        acc += (e.x + e.y) + (e.z + e.w);
+    }
+    acc = warp_sum(acc);
+    __shared__ float red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.0f;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        sink[blockIdx.x] = t;
+    }
+}
+
+void launch_eps_bench(uint64_t n4, uint64_t seed, float* sink, int grid, cudaStream_t st) {
+    eps_bench_kernel<<<grid, 256, 0, st>>>(n4, make_key(seed), sink);
+}
+
+// ====================================================================== K10: predict stats
+__global__ void predict_stats_kernel(const float* __restrict__ logits, int S, int B, int O,
+                                     int loss_kind, float* __restrict__ mean,
+                                     float* __restrict__ m2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (b, o)
+    if (i >= B * O) return;
+    const int b = i / O, o = i % O;
+    auto prob = [&](int s) -> float {
+        const float* z = logits + ((int64_t)s * B + b) * O;
+        if (loss_kind != 0) return z[o];
+        float m = z[0];
+        for (int k = 1; k < O; ++k) m = fmaxf(m, z[k]);
+        float se = 0.0f;
+        for (int k = 0; k < O; ++k) se += expf(z[k] - m);
+        return expf(z[o] - m) / se;
+    };
+    double acc = 0.0;
+    for (int s = 0; s < S; ++s) acc += prob(s);
+    const double mu = acc / S;
+    double v = 0.0;
+    for (int s = 0; s < S; ++s) {
+        const double d = prob(s) - mu;
+        v += d * d;
+    }
+    mean[i] = (float)mu;
+    m2[i] = (float)v;
+}
+
+void launch_predict_stats(const float* logits, int S, int B, int O, int loss_kind, float* mean,
+                          float* m2, cudaStream_t st) {
+    predict_stats_kernel<<<(B * O + 255) / 256, 256, 0, st>>>(logits, S, B, O, loss_kind, mean,
+                                                              m2);
+}
+
+__global__ void predict_merge_kernel(const float* __restrict__ means, const float* __restrict__ m2s,
+                                     const float* __restrict__ counts, int R, int BO,
+                                     float* __restrict__ mean, float* __restrict__ var) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= BO) return;
+    double n = 0.0, mu = 0.0, M2 = 0.0;
+    for (int r = 0; r < R; ++r) {  // Chan et al. pairwise update, fixed rank order
+        const double nr = counts[r];
+        const double mr = means[(int64_t)r * BO + i];
+        const double n_new = n + nr;
+        const double d = mr - mu;
+        mu += d * nr / n_new;
+        M2 += (double)m2s[(int64_t)r * BO + i] + d * d * n * nr / n_new;
+        n = n_new;
+    }
+    mean[i] = (float)mu;
+    var[i] = (float)(M2 / n);
+}
+
+void launch_predict_merge(const float* means, const float* m2s, const float* counts, int R,
+                          int BO, float* mean, float* var, cudaStream_t st) {
+    predict_merge_kernel<<<(BO + 255) / 256, 256, 0, st>>>(means, m2s, counts, R, BO, mean, var);
+}
+
+// ====================================================================== input cast
+__global__ void to_bf16_kernel(const float* __restrict__ x, int B, int K, int ldx,
+                               __nv_bfloat16* __restrict__ out) {
+    const int64_t n = (int64_t)B * ldx;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int b = (int)(i / ldx), k = (int)(i % ldx);
+        out[i] = __float2bfloat16_rn(k < K ? x[(int64_t)b * K + k] : 0.0f);
+    }
+}
+
+void launch_to_bf16(const float* x, int B, int K, int ldx, void* out, cudaStream_t st) {
+    const int64_t n = (int64_t)B * ldx;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+    to_bf16_kernel<<<grid, 256, 0, st>>>(x, B, K, ldx, reinterpret_cast<__nv_bfloat16*>(out));
+}
+
+// ====================================================================== K11: FP32 SIMT GEMMs
+constexpr int TB = 64, TK = 16;
+
+__global__ void __launch_bounds__(256) fwd_fp32_kernel(SampledLayer L, SampleKeys kk, int B,
+                                                       const float* __restrict__ A,
+                                                       int64_t strideA, float* __restrict__ Z,
+                                                       int64_t strideZ, int relu) {
+    __shared__ float As[TK][TB + 4];  // [k][b]
+    __shared__ float Ws[TK][TB + 4];  // [k][n]
+    __shared__ float bias[TB];
+    const int n0 = blockIdx.x * TB, b0 = blockIdx.y * TB, s = blockIdx.z;
+    const uint32_t sg = kk.s0 + s;
+    const float* Ag = A + s * strideA;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int N = L.N, K = L.K;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += TK) {
+        {
+            const int bb = tid >> 2, kq = (tid & 3) * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = k0 + kq + j;
+                As[kq + j][bb] = (b0 + bb < B && k < K) ? Ag[(int64_t)(b0 + bb) * K + k] : 0.0f;
+            }
+        }
+        {
+            const int nn = tid >> 2, kq = tid & 3, n = n0 + nn, kb = k0 + 4 * kq;
+            float w[4] = {0.f, 0.f, 0.f, 0.f};
+            if (n < N && kb < K) {
+                const float4 e = eps4(kk.key, kk.step, sg, L.t_w, n, kb >> 2);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (kb + j < K) {
+                        const int64_t i = L.off_w + (int64_t)n * K + kb + j;
+                        w[j] = __fmaf_rn(L.sigma[i], eps_get(e, j), L.mu[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) Ws[4 * kq + j][nn] = w[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < TK; ++q) {
+            float a[4], w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[q][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = Ws[q][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    if (tid < TB) {
+        const int n = n0 + tid;
+        bias[tid] = n < N ? __fmaf_rn(L.sigma[L.off_b + n], eps1(kk.key, kk.step, sg, L.t_b, 0, n),
+                                      L.mu[L.off_b + n])
+                          : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int b = b0 + ty * 4 + i;
+        if (b >= B) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n >= N) continue;
+            float v = acc[i][j] + bias[tx * 4 + j];
+            if (relu) v = fmaxf(v, 0.0f);
+            Z[s * strideZ + (int64_t)b * N + n] = v;
+        }
+    }
+}
+
+void launch_fwd_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* A,
+                     int64_t strideA, float* Z, int64_t strideZ, bool relu, cudaStream_t st) {
+    dim3 grid((L.N + TB - 1) / TB, (B + TB - 1) / TB, S);
+    fwd_fp32_kernel<<<grid, 256, 0, st>>>(L, k, B, A, strideA, Z, strideZ, relu ? 1 : 0);
+}
+
+__global__ void __launch_bounds__(256) dgrad_fp32_kernel(SampledLayer L, SampleKeys kk, int B,
+                                                         const float* __restrict__ G,
+                                                         int64_t strideG,
+                                                         const float* __restrict__ Ap,
+                                                         int64_t strideA, float* __restrict__ dA,
+                                                         int64_t strideD) {
+    __shared__ float Gs[TK][TB + 4];  // [n][b]
+    __shared__ float Ws[TK][TB + 4];  // [n][k]
+    const int kt0 = blockIdx.x * TB, b0 = blockIdx.y * TB, s = blockIdx.z;
+    const uint32_t sg = kk.s0 + s;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int N = L.N, K = L.K;
+    const float* Gg = G + s * strideG;
+    float acc[4][4] = {};
+    for (int n0 = 0; n0 < N; n0 += TK) {
+        {
+            const int bb = tid >> 2, nq = (tid & 3) * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = n0 + nq + j;
+                Gs[nq + j][bb] = (b0 + bb < B && n < N) ? Gg[(int64_t)(b0 + bb) * N + n] : 0.0f;
+            }
+        }
+        {
+            const int nn = tid >> 4, kq = tid & 15, n = n0 + nn, kb = kt0 + 4 * kq;
+            float w[4] = {0.f, 0.f, 0.f, 0.f};
+            if (n < N && kb < K) {
+                const float4 e = eps4(kk.key, kk.step, sg, L.t_w, n, kb >> 2);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (kb + j < K) {
+                        const int64_t i = L.off_w + (int64_t)n * K + kb + j;
+                        w[j] = __fmaf_rn(L.sigma[i], eps_get(e, j), L.mu[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) Ws[nn][4 * kq + j] = w[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < TK; ++q) {
+            float a[4], w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = Gs[q][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = Ws[q][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], w[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int b = b0 + ty * 4 + i;
+        if (b >= B) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = kt0 + tx * 4 + j;
+            if (k >= K) continue;
+            const float m = Ap[s * strideA + (int64_t)b * K + k] > 0.0f ? 1.0f : 0.0f;
+            dA[s * strideD + (int64_t)b * K + k] = acc[i][j] * m;
+        }
+    }
+}
+
+void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
+                       int64_t strideG, const float* Aprev, int64_t strideA, float* dA,
+                       int64_t strideD, cudaStream_t st) {
+    dim3 grid((L.K + TB - 1) / TB, (B + TB - 1) / TB, S);
+    dgrad_fp32_kernel<<<grid, 256, 0, st>>>(L, k, B, G, strideG, Aprev, strideA, dA, strideD);
+}
+
+__global__ void __launch_bounds__(256) wgrad_fp32_kernel(SampledLayer L, SampleKeys kk, int S,
+                                                         int B, const float* __restrict__ G,
+                                                         int64_t strideG,
+                                                         const float* __restrict__ A,
+                                                         int64_t strideA, float scale,
+                                                         float* __restrict__ acc_mu,
+                                                         float* __restrict__ acc_rho) {
+    __shared__ float Gs[TK][TB + 4];  // [b][n]
+    __shared__ float As[TK][TB + 4];  // [b][k]
+    const int kt0 = blockIdx.x * TB, n0 = blockIdx.y * TB;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int N = L.N, K = L.K;
+    float am[4][4] = {}, ar[4][4] = {};
+    for (int s = 0; s < S; ++s) {
+        const float* Gg = G + s * strideG;
+        const float* Ag = A + s * strideA;
+        float d[4][4] = {};
+        for (int b0 = 0; b0 < B; b0 += TK) {
+            {
+                const int bb = tid >> 4, q = (tid & 15) * 4;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int n = n0 + q + j, k = kt0 + q + j, b = b0 + bb;
+                    Gs[bb][q + j] = (b < B && n < N) ? Gg[(int64_t)b * N + n] : 0.0f;
+                    As[bb][q + j] = (b < B && k < K) ? Ag[(int64_t)b * K + k] : 0.0f;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < TK; ++q) {
+                float g[4], a[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) g[i] = Gs[q][ty * 4 + i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[j] = As[q][tx * 4 + j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) d[i][j] = fmaf(g[i], a[j], d[i][j]);
+            }
+            __syncthreads();
+        }
+        const int kb = kt0 + tx * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int n = n0 + ty * 4 + i;
+            if (n >= N || kb >= K) continue;
+            const float4 e = eps4(kk.key, kk.step, kk.s0 + s, L.t_w, n, kb >> 2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                am[i][j] += d[i][j];
+                ar[i][j] = fmaf(d[i][j], eps_get(e, j), ar[i][j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int n = n0 + ty * 4 + i;
+        if (n >= N) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = kt0 + tx * 4 + j;
+            if (k >= K) continue;
+            const int64_t o = L.off_w + (int64_t)n * K + k;
+            acc_mu[o] += scale * am[i][j];
+            acc_rho[o] += scale * ar[i][j];
+        }
+    }
+}
+
+void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
+                       int64_t strideG, const float* A, int64_t strideA, float scale,
+                       float* acc_mu, float* acc_rho, cudaStream_t st) {
+    dim3 grid((L.K + TB - 1) / TB, (L.N + TB - 1) / TB);
+    wgrad_fp32_kernel<<<grid, 256, 0, st>>>(L, k, S, B, G, strideG, A, strideA, scale, acc_mu,
+                                            acc_rho);
+}
+
+__global__ void bias_grad_kernel(SampledLayer L, SampleKeys kk, int S, int B,
+                                 const void* __restrict__ G, int64_t strideG, int ldg, int g_bf16,
+                                 float scale, float* __restrict__ acc_mu,
+                                 float* __restrict__ acc_rho) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= L.N) return;
+    float am = 0.0f, ar = 0.0f;
+    for (int s = 0; s < S; ++s) {
+        float db = 0.0f;
+        for (int b = 0; b < B; ++b) {
+            const int64_t o = s * strideG + (int64_t)b * ldg + n;
+            db += g_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(G)[o])
+                         : reinterpret_cast<const float*>(G)[o];
+        }
+        am += db;
+        ar = fmaf(db, eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n), ar);
+    }
+    acc_mu[L.off_b + n] += scale * am;
+    acc_rho[L.off_b + n] += scale * ar;
+}
+
+void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, int B, const void* G,
+                      int64_t strideG, int ldg, bool g_bf16, float scale, float* acc_mu,
+                      float* acc_rho, cudaStream_t st) {
+    bias_grad_kernel<<<(L.N + 127) / 128, 128, 0, st>>>(L, k, S, B, G, strideG, ldg,
+                                                        g_bf16 ? 1 : 0, scale, acc_mu, acc_rho);
+}
+
+}  // namespace bnn

@@ -1,0 +1,427 @@
+// kernels_tc.cu — BF16 tensor-core sampled-layer kernels for sm_100a.
+//
+// K2 (fwd):   Z_s = X_s · W_sᵀ + b_s, ReLU                       PAPER.md:160 (Alg. 1 l.7)
+// K4 (dgrad): dX_s = (G_s · W_s) ⊙ 1[X_s > 0]                    PAPER.md:165 (Alg. 1 l.12)
+// K5 (wgrad): dW_s = G_sᵀ · X_s;  acc_μ += dW_s,  acc_ρ += dW_s ⊙ ε_s over the CTA's samples
+//             (north_star subsystem (3); reading R20: sigmoid(ρ) is applied once in K8)
+//
+// The sampled weight tile W_s = RN_bf16(fma(σ, ε_s, μ)) is produced on chip by eight
+// generator warps straight into the UMMA canonical SWIZZLE_128B layout in shared memory
+// (north_star subsystem (2)); it is never written to global memory. Activations and
+// gradients are TMA-loaded; one elected thread issues tcgen05.mma (M=128, K=16 steps) with
+// the fp32 accumulator in TMEM; the epilogue reads TMEM with tcgen05.ld.
+//
+// Operand orientation (tcgen05 computes D[M×N] = A[M×K]·B[N×K]ᵀ):
+//   fwd   : M = output feature n, N = batch b, K = fan-in k. A = W_s tile, K-major (as
+//           generated); B = X_s [b][k], K-major (TMA box 64 k × 256 b).
+//   dgrad : M = input feature k, N = batch b, K = output feature n. A = W_sᵀ: the same
+//           generated rows of W_s, stored MN-major (k contiguous); B = G_s [b][n], K-major.
+//   wgrad : M = n, N = k (64-wide tiles), K = batch b. A = G_sᵀ, MN-major; B = X_s, MN-major.
+#include <algorithm>
+
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels_tc.cuh"
+#include "tc_ptx.cuh"
+
+namespace bnn {
+
+using namespace ptx;
+
+// ============================================================================ K2 / K4
+namespace gen {
+constexpr int kGenWarps = 8;
+constexpr int kThreads = (kGenWarps + 1) * 32;  // + one control warp (TMEM alloc, MMA issue)
+constexpr int kStages = 2;
+constexpr int kAStage = 128 * 64 * 2;           // 16 KB generated W tile
+constexpr int kBStage = 256 * 64 * 2;           // 32 KB activation/gradient tile
+constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256 + 128 * 4;
+}  // namespace gen
+
+__device__ __forceinline__ void load_mu_sigma4(const SampledLayer& L, int64_t i, int kvalid,
+                                               bool vec, float4& m, float4& sg) {
+    if (vec && kvalid >= 4) {
+        m = __ldg(reinterpret_cast<const float4*>(L.mu + i));
+        sg = __ldg(reinterpret_cast<const float4*>(L.sigma + i));
+    } else {
+        float mm[4] = {0.f, 0.f, 0.f, 0.f}, ss[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < 4 && j < kvalid; ++j) {
+            mm[j] = __ldg(L.mu + i + j);
+            ss[j] = __ldg(L.sigma + i + j);
+        }
+        m = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        sg = make_float4(ss[0], ss[1], ss[2], ss[3]);
+    }
+}
+
+// W_s[n][k .. k+3] as two packed bf16x2 words (zero outside the tensor).
+__device__ __forceinline__ uint2 gen_w4(const SampledLayer& L, const SampleKeys& kk, uint32_t sg,
+                                        int n, int k, bool vec) {
+    if (n >= L.N || k >= L.K) return make_uint2(0u, 0u);
+    const int kvalid = L.K - k;
+    const int64_t i = L.off_w + (int64_t)n * L.K + k;
+    float4 m, s;
+    load_mu_sigma4(L, i, kvalid, vec, m, s);
+    const float4 e = eps4(kk.key, kk.step, sg, L.t_w, (uint32_t)n, (uint32_t)(k >> 2));
+    float w0 = __fmaf_rn(s.x, e.x, m.x), w1 = __fmaf_rn(s.y, e.y, m.y);
+    float w2 = __fmaf_rn(s.z, e.z, m.z), w3 = __fmaf_rn(s.w, e.w, m.w);
+    if (kvalid < 4) {
+        w1 = kvalid > 1 ? w1 : 0.f;
+        w2 = kvalid > 2 ? w2 : 0.f;
+        w3 = 0.f;
+    }
+    return make_uint2(pack_bf16x2(w0, w1), pack_bf16x2(w2, w3));
+}
+
+__global__ void __launch_bounds__(gen::kThreads, 2)
+    gen_gemm_kernel(const __grid_constant__ CUtensorMap tmB, const TcGenArgs a) {
+    using namespace gen;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kAStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+    uint64_t* full_gen = bars;
+    uint64_t* full_tma = bars + kStages;
+    uint64_t* empty = bars + 2 * kStages;
+    uint64_t* tfull = bars + 3 * kStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 1);
+    float* sbias = reinterpret_cast<float*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int m0 = blockIdx.x * 128, s = blockIdx.y, b0 = blockIdx.z * 256;
+    const uint32_t sg = a.kk.s0 + s;
+    const SampledLayer& L = a.L;
+
+    if (tid == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full_gen[i], kGenWarps);
+            mbar_init(&full_tma[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == kGenWarps) tmem_alloc(tslot, 256);
+    if (a.mode == 0 && tid < 128) {
+        const int n = m0 + tid;
+        sbias[tid] = n < L.N ? __fmaf_rn(L.sigma[L.off_b + n],
+                                         eps1(a.kk.key, a.kk.step, sg, L.t_b, 0u, (uint32_t)n),
+                                         L.mu[L.off_b + n])
+                             : 0.0f;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int nkb = (a.R + 63) / 64;
+    const bool vec = a.vec_ok != 0;
+
+    if (warp == kGenWarps) {
+        // ------------------------------------------------ MMA issuer (one thread)
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, a.nb, a.mode == 1 ? 1 : 0, 0);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int st = kb % kStages;
+                const uint32_t ph = (kb / kStages) & 1;
+                mbar_wait(&full_gen[st], ph);
+                mbar_wait(&full_tma[st], ph);
+                tc_fence_after();
+                const uint32_t aBase = smem_u32(sA + st * kAStage);
+                const uint32_t bBase = smem_u32(sB + st * kBStage);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint64_t ad = a.mode == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
+                                                    : sdesc_sw128(aBase + 2048 * q, 8192, 1024);
+                    const uint64_t bd = sdesc_sw128(bBase + 32 * q, 16, 1024);
+                    mma_bf16(tmem, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
+                }
+                mma_commit(&empty[st]);
+            }
+            mma_commit(tfull);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ generator warps
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % kStages;
+            const uint32_t ph = (kb / kStages) & 1;
+            mbar_wait(&empty[st], ph ^ 1);
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&full_tma[st], kBStage);
+                tma_load_3d(&tmB, &full_tma[st], sB + st * kBStage, kb * 64, b0,
+                            a.b_shared ? 0 : s);
+            }
+            uint8_t* tileA = sA + st * kAStage;
+#pragma unroll 2
+            for (int it = 0; it < 8; ++it) {
+                const int item = it * 256 + tid;
+                uint32_t off;
+                int n, k;
+                if (a.mode == 0) {  // rows = n (128), 16 quads of k per row; K-major SW128
+                    const int row = item >> 4, kq = item & 15;
+                    n = m0 + row;
+                    k = kb * 64 + 4 * kq;
+                    off = row * 128 + ((((kq >> 1) ^ (row & 7))) << 4) + ((kq & 1) << 3);
+                } else {  // rows = n (64, the MMA K dim), 32 quads of k (M) per row; MN-major
+                    const int r = item >> 5, mq = item & 31;
+                    n = kb * 64 + r;
+                    k = m0 + 4 * mq;
+                    const int blk = mq >> 4, c = mq & 15;
+                    off = blk * 8192 + r * 128 + ((((c >> 1) ^ (r & 7))) << 4) + ((c & 1) << 3);
+                }
+                const uint2 w = gen_w4(L, a.kk, sg, n, k, vec);
+                asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(smem_u32(tileA + off)),
+                             "r"(w.x), "r"(w.y)
+                             : "memory");
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_gen[st]);
+        }
+        // ------------------------------------------------ epilogue
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const int q = warp & 3, h = warp >> 2;
+        const int row = 32 * q + lane, m = m0 + row;
+        const int nchunks = (a.nb + 31) / 32;
+        const float bias = a.mode == 0 ? sbias[row] : 0.0f;
+        for (int c = h; c < nchunks; c += 2) {
+            float v[32];
+            __syncwarp();
+            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + c * 32, v);
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+                const int b = b0 + c * 32 + j;
+                if (b >= a.B || m >= a.M) break;
+                if (a.mode == 0) {
+                    float z = v[j] + bias;
+                    if (a.out_f32) {
+                        reinterpret_cast<float*>(a.out)[s * a.out_stride_s + (int64_t)b * a.ldo + m] = z;
+                    } else {
+                        if (a.relu) z = fmaxf(z, 0.0f);
+                        reinterpret_cast<__nv_bfloat16*>(a.out)[s * a.out_stride_s +
+                                                                (int64_t)b * a.ldo + m] =
+                            __float2bfloat16_rn(z);
+                    }
+                } else {
+                    const int64_t o = s * a.out_stride_s + (int64_t)b * a.ldo + m;
+                    const float mk = __bfloat162float(a.mask[s * a.mask_stride_s + (int64_t)b * a.ldm + m]);
+                    reinterpret_cast<__nv_bfloat16*>(a.out)[o] =
+                        __float2bfloat16_rn(mk > 0.0f ? v[j] : 0.0f);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kGenWarps) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gen_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             gen::kSmem);
+        attr = true;
+    }
+    dim3 grid((a.M + 127) / 128, S, (a.B + 255) / 256);
+    gen_gemm_kernel<<<grid, gen::kThreads, gen::kSmem, st>>>(tmB, a);
+}
+
+// ============================================================================ K5
+namespace wg {
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
+constexpr int kStages = 4;
+constexpr int kAStage = 64 * 128 * 2;  // G_sᵀ: 64 b × 128 n (two 64-wide MN blocks)
+constexpr int kBStage = 64 * 64 * 2;   // X_s : 64 b × 64 k
+constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
+}  // namespace wg
+
+__global__ void __launch_bounds__(wg::kThreads, 2)
+    wgrad_tc_kernel(const __grid_constant__ TcWgradMaps maps, const TcWgradArgs a) {
+    using namespace wg;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kAStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = bars + 2 * kStages + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // which layer / tile
+    int li = 0;
+#pragma unroll 1
+    while (li + 1 < a.nlayers && (int)blockIdx.x >= a.lay[li + 1].tile_base) ++li;
+    const WgradLayer& W = a.lay[li];
+    const SampledLayer& L = W.L;
+    const int tile = blockIdx.x - W.tile_base;
+    const int n0 = (tile / W.ktiles) * 128, k0 = (tile % W.ktiles) * 64;
+    const CUtensorMap* mapG = &maps.g[li];
+    const CUtensorMap* mapX = &maps.x[li];
+    const int nbb = (a.B + 63) / 64;
+    const int S = a.S;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kEpiWarps);
+        }
+        mbar_fence_init();
+    }
+    if (warp == kEpiWarps + 1) tmem_alloc(tslot, 128);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == kEpiWarps) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(mapG);
+            tma_prefetch_desc(mapX);
+            int it = 0;
+            for (int s = 0; s < S; ++s)
+                for (int bb = 0; bb < nbb; ++bb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait(&empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[st], kAStage + kBStage);
+                    uint8_t* a_st = sA + st * kAStage;
+                    tma_load_3d(mapG, &full[st], a_st, n0, 64 * bb, s);
+                    tma_load_3d(mapG, &full[st], a_st + 8192, n0 + 64, 64 * bb, s);
+                    tma_load_3d(mapX, &full[st], sB + st * kBStage, k0, 64 * bb,
+                                W.b_shared ? 0 : s);
+                }
+        }
+        __syncwarp();
+    } else if (warp == kEpiWarps + 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+            int it = 0;
+            for (int s = 0; s < S; ++s) {
+                const int buf = s & 1;
+                mbar_wait(&tempty[buf], ((s >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int bb = 0; bb < nbb; ++bb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait(&full[st], ph);
+                    tc_fence_after();
+                    const uint32_t aBase = smem_u32(sA + st * kAStage);
+                    const uint32_t bBase = smem_u32(sB + st * kBStage);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t ad = sdesc_sw128(aBase + 2048 * q, 8192, 1024);
+                        const uint64_t bd = sdesc_sw128(bBase + 2048 * q, 8192, 1024);
+                        mma_bf16(tmem + buf * 64, ad, bd, idesc, (bb | q) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ epilogue: ε regeneration + accumulation
+        const int q = warp & 3, h = warp >> 2;
+        const int n = n0 + 32 * q + lane;
+        const int k = k0 + 32 * h;
+        float am[32], ar[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) am[j] = ar[j] = 0.0f;
+        for (int s = 0; s < S; ++s) {
+            const int buf = s & 1;
+            mbar_wait(&tfull[buf], (s >> 1) & 1);
+            tc_fence_after();
+            float d[32];
+            __syncwarp();
+            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 64 + 32 * h, d);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (n < L.N) {
+                const uint32_t sg = a.kk.s0 + s;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    if (k + 4 * g < L.K) {
+                        const float4 e = eps4(a.kk.key, a.kk.step, sg, L.t_w, (uint32_t)n,
+                                              (uint32_t)((k >> 2) + g));
+                        am[4 * g + 0] += d[4 * g + 0];
+                        am[4 * g + 1] += d[4 * g + 1];
+                        am[4 * g + 2] += d[4 * g + 2];
+                        am[4 * g + 3] += d[4 * g + 3];
+                        ar[4 * g + 0] = fmaf(d[4 * g + 0], e.x, ar[4 * g + 0]);
+                        ar[4 * g + 1] = fmaf(d[4 * g + 1], e.y, ar[4 * g + 1]);
+                        ar[4 * g + 2] = fmaf(d[4 * g + 2], e.z, ar[4 * g + 2]);
+                        ar[4 * g + 3] = fmaf(d[4 * g + 3], e.w, ar[4 * g + 3]);
+                    }
+                }
+            }
+        }
+        if (n < L.N) {
+            const int64_t base = L.off_w + (int64_t)n * L.K + k;
+            float* pm = a.acc_mu + base;
+            float* pr = a.acc_rho + base;
+            const bool v4 = ((base & 3) == 0) && (k + 32 <= L.K);
+            if (v4) {
+#pragma unroll
+                for (int g = 0; g < 8; ++g) {
+                    float4 x = reinterpret_cast<float4*>(pm)[g];
+                    float4 y = reinterpret_cast<float4*>(pr)[g];
+                    x.x += a.scale * am[4 * g + 0]; x.y += a.scale * am[4 * g + 1];
+                    x.z += a.scale * am[4 * g + 2]; x.w += a.scale * am[4 * g + 3];
+                    y.x += a.scale * ar[4 * g + 0]; y.y += a.scale * ar[4 * g + 1];
+                    y.z += a.scale * ar[4 * g + 2]; y.w += a.scale * ar[4 * g + 3];
+                    reinterpret_cast<float4*>(pm)[g] = x;
+                    reinterpret_cast<float4*>(pr)[g] = y;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (k + j < L.K) {
+                        pm[j] += a.scale * am[j];
+                        pr[j] += a.scale * ar[j];
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kEpiWarps + 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 128);
+    }
+}
+
+void launch_wgrad_tc(const TcWgradMaps& maps, const TcWgradArgs& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             wg::kSmem);
+        attr = true;
+    }
+    const WgradLayer& last = a.lay[a.nlayers - 1];
+    const int ntiles = last.tile_base + last.mtiles * last.ktiles;
+    wgrad_tc_kernel<<<ntiles, wg::kThreads, wg::kSmem, st>>>(maps, a);
+}
+
+}  // namespace bnn

@@ -1,0 +1,55 @@
+// kernels_tc.cuh — BF16 tcgen05 sampled-layer kernels (K2 fwd, K4 dgrad, K5 wgrad).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "kernels.cuh"
+
+namespace bnn {
+
+// K2 (mode 0) / K4 (mode 1): one CTA = 128 rows of the output feature dim (M) × up to 256
+// batch rows (N) of one sample; A = W_s generated on chip, B = TMA (tmB: 3-D map
+// [depth = sample][rows = batch][inner = reduction dim], box 64 × 256 × 1, SWIZZLE_128B).
+struct TcGenArgs {
+    SampledLayer L;
+    SampleKeys kk;
+    int mode;            // 0 fwd (M = L.N, R = L.K), 1 dgrad (M = L.K, R = L.N)
+    int B;               // batch rows of a sample
+    int b_shared;        // B operand is shared by all samples (layer-0 input)
+    int M, R;
+    int nb;              // MMA N: round_up(min(B, 256), 16)
+    void* out;           // fwd: bf16 activations or fp32 logits; dgrad: bf16 gradients
+    int64_t out_stride_s;
+    int ldo;
+    int out_f32, relu;
+    const __nv_bfloat16* mask;  // dgrad: input activations of the layer (ReLU mask source)
+    int64_t mask_stride_s;
+    int ldm;
+    int vec_ok;          // μ/σ rows are 16-byte aligned (float4 loads)
+};
+void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
+
+// K5: grouped over up to 4 layers; CTA = 128 n × 64 k tile, loops over all S samples.
+constexpr int kMaxWgradLayers = 4;
+struct WgradLayer {
+    SampledLayer L;
+    int mtiles, ktiles, tile_base;
+    int b_shared;
+};
+struct TcWgradArgs {
+    SampleKeys kk;
+    int S, B;
+    float scale;
+    float* acc_mu;
+    float* acc_rho;
+    int nlayers;
+    WgradLayer lay[kMaxWgradLayers];
+};
+struct TcWgradMaps {
+    CUtensorMap g[kMaxWgradLayers];  // G_l: [S][B][N_l], box 64 × 64 × 1
+    CUtensorMap x[kMaxWgradLayers];  // X_l: [S or 1][B][K_l], box 64 × 64 × 1
+};
+void launch_wgrad_tc(const TcWgradMaps& maps, const TcWgradArgs& a, cudaStream_t st);
+
+}  // namespace bnn

@@ -1,0 +1,833 @@
+// runtime.cu — the step orchestrator and the C ABI (L4) of libbnn.so.
+//
+// One bnn_ctx per rank/GPU. bnn_init builds the layer graph and parameter layout, allocates
+// every workspace buffer, encodes the TMA descriptors of the BF16 path and creates the NCCL
+// communicator. bnn_elbo_step then only enqueues kernels on the context stream (no
+// allocation, no host synchronisation unless the loss is requested on the host):
+//   K7 σ prologue → per sample chunk: sampled forward (K2 / K11), loss head (K6), sampled
+//   dgrad (K4 / K11), wgrad with sample accumulation (K5 / K11), bias grads → one NCCL
+//   SUM-allreduce of [acc_μ | acc_ρ | L_data] → K8 finalize + KL.
+// Sample sharding, data sharding and the K×G hybrid grid only
+// change which global samples (EPS-v1 keys) and which examples a rank processes; the
+// global 1/(S·B) pre-scaling makes the flat allreduce sum compose over both axes
+// (reading R8).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/bnn.h"
+#include "kernels.cuh"
+#include "kernels_tc.cuh"
+
+using namespace bnn;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct LayerDesc {
+    int cin, cout, k, stride, pad;
+    int64_t off_w, off_b;
+    uint32_t t_w, t_b;
+};
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D bf16 view [depth][rows][inner] with row pitch ld elements, box (64, box_rows, 1),
+// 128-byte swizzle, zero fill out of bounds.
+bool make_map(CUtensorMap* m, const void* base, int inner, int rows, int depth, int ld,
+              int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)depth};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * rows};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct bnn_ctx {
+    bnn_model_desc model{};
+    bnn_config cfg{};
+    std::vector<LayerDesc> layers;
+    std::vector<int> widths;  // MLP widths
+    int64_t P = 0, P_pad = 0, acc_total = 0;
+    int O = 0;
+    int K = 1, G = 1, kidx = 0, gidx = 0;
+    int S_loc_max = 0, B_max = 0, chunk = 0;
+    bool bf16 = false;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    // workspace
+    float* sigma = nullptr;
+    float* acc = nullptr;
+    double* kl_part = nullptr;
+    int n_part = 0;
+    float* lossbuf = nullptr;  // [0] loss, [1] KL
+    float* lossrow = nullptr;
+    float* logits = nullptr;
+    std::vector<void*> act;    // act[l]: input of layer l (l ≥ 1)
+    std::vector<int> ld;       // padded row pitch of width l
+    std::vector<void*> grad;   // grad[l]: dℓ/dz of layer l output
+    void* xb = nullptr;        // bf16 copy of the layer-0 input
+    float* x_stage = nullptr;  // device copy of a host batch
+    int32_t* ycls_stage = nullptr;
+    float* yreg_stage = nullptr;
+    float* p_mean = nullptr;
+    float* p_m2 = nullptr;
+    float* g_means = nullptr;
+    float* g_m2s = nullptr;
+    float* g_counts = nullptr;
+    float* acc_scratch = nullptr;  // for bnn_elbo_step_host / predict helpers
+    // TMA descriptors (BF16)
+    std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;
+    // bookkeeping
+    std::string err;
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_next = 0;
+    std::vector<std::string> prof_names;
+    std::vector<double> prof_ms;
+    std::vector<int64_t> prof_n;
+    std::vector<void*> allocs;
+
+    int set_err(int code, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        g_last_error = buf;
+        return code;
+    }
+    template <class T>
+    bool alloc(T** p, size_t n) {
+        void* q = nullptr;
+        if (cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return false;
+        cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(T));
+        allocs.push_back(q);
+        *p = reinterpret_cast<T*>(q);
+        return true;
+    }
+    int prof_class(const char* name) {
+        for (size_t i = 0; i < prof_names.size(); ++i)
+            if (prof_names[i] == name) return (int)i;
+        prof_names.push_back(name);
+        prof_ms.push_back(0.0);
+        prof_n.push_back(0);
+        return (int)prof_names.size() - 1;
+    }
+    void prof_flush() {
+        if (pending.empty()) return;
+        cudaStreamSynchronize(st);
+        for (auto& p : pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+            prof_ms[p.first] += ms;
+            prof_n[p.first] += 1;
+        }
+        pending.clear();
+        ev_next = 0;
+    }
+    template <class F>
+    void launch(const char* cls, F&& f) {
+        int c = -1;
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (prof) {
+            c = prof_class(cls);
+            if (ev_next + 2 > ev_pool.size()) prof_flush();
+            if (ev_next + 2 > ev_pool.size()) {
+                for (int i = 0; i < 256; ++i) {
+                    cudaEvent_t e;
+                    cudaEventCreate(&e);
+                    ev_pool.push_back(e);
+                }
+            }
+            a = ev_pool[ev_next++];
+            b = ev_pool[ev_next++];
+            cudaEventRecord(a, st);
+        }
+        f();
+        ++launches;
+        if (prof) {
+            cudaEventRecord(b, st);
+            pending.push_back({c, {a, b}});
+        }
+    }
+};
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return (ctx)->set_err(BNN_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));    \
+    } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                  \
+    do {                                                                                     \
+        ncclResult_t r_ = (expr);                                                            \
+        if (r_ != ncclSuccess)                                                               \
+            return (ctx)->set_err(BNN_ERR_COMM, "%s: %s", #expr, ncclGetErrorString(r_));    \
+    } while (0)
+
+namespace {
+
+int build_layers(bnn_ctx* c) {
+    const bnn_model_desc& m = c->model;
+    int64_t off = 0;
+    auto add = [&](int cin, int cout, int k, int stride, int pad) {
+        LayerDesc L{cin, cout, k, stride, pad, 0, 0, 0, 0};
+        L.t_w = (uint32_t)(2 * c->layers.size());
+        L.t_b = L.t_w + 1;
+        L.off_w = off;
+        off += (int64_t)cout * k * k * cin;
+        L.off_b = off;
+        off += cout;
+        c->layers.push_back(L);
+    };
+    if (m.kind == BNN_MODEL_MLP) {
+        if (m.n_widths < 2 || m.n_widths > 16)
+            return c->set_err(BNN_ERR_CONFIG, "MLP needs 2 <= n_widths <= 16");
+        for (int i = 0; i < m.n_widths; ++i) {
+            if (m.widths[i] <= 0) return c->set_err(BNN_ERR_CONFIG, "MLP widths must be > 0");
+            c->widths.push_back(m.widths[i]);
+        }
+        for (int i = 1; i < m.n_widths; ++i) add(m.widths[i - 1], m.widths[i], 1, 1, 0);
+        c->O = m.widths[m.n_widths - 1];
+    } else {
+        return c->set_err(BNN_ERR_CONFIG,
+                          "model kind %d: only BNN_MODEL_MLP is implemented in this build", m.kind);
+    }
+    c->P = off;
+    c->P_pad = round_up(off, 64);
+    c->acc_total = 2 * c->P_pad + 64;
+    if (2 * c->layers.size() >= 4095) return c->set_err(BNN_ERR_CONFIG, "too many tensors (t < 4095)");
+    return BNN_OK;
+}
+
+SampledLayer sampled(const bnn_ctx* c, int l, const float* mu) {
+    const LayerDesc& L = c->layers[l];
+    SampledLayer s;
+    s.mu = mu;
+    s.sigma = c->sigma;
+    s.off_w = L.off_w;
+    s.off_b = L.off_b;
+    s.N = L.cout;
+    s.K = L.cin * L.k * L.k;
+    s.t_w = L.t_w;
+    s.t_b = L.t_b;
+    return s;
+}
+
+int alloc_mlp(bnn_ctx* c) {
+    const int L = (int)c->layers.size();
+    const int B = c->B_max, Sc = c->chunk;
+    const size_t es = c->bf16 ? 2 : 4;
+    c->ld.resize(L + 1);
+    for (int l = 0; l <= L; ++l) c->ld[l] = c->bf16 ? (int)round_up(c->widths[l], 8) : c->widths[l];
+    c->act.assign(L, nullptr);
+    for (int l = 1; l < L; ++l) {
+        void* p;
+        if (cudaMalloc(&p, (size_t)Sc * B * c->ld[l] * es) != cudaSuccess)
+            return c->set_err(BNN_ERR_CUDA, "out of memory (activations)");
+        cudaMemset(p, 0, (size_t)Sc * B * c->ld[l] * es);
+        c->allocs.push_back(p);
+        c->act[l] = p;
+    }
+    c->grad.assign(L, nullptr);
+    for (int l = 0; l < L; ++l) {
+        void* p;
+        const size_t n = (size_t)Sc * B * c->ld[l + 1] * es;
+        if (cudaMalloc(&p, n) != cudaSuccess) return c->set_err(BNN_ERR_CUDA, "out of memory (grads)");
+        cudaMemset(p, 0, n);
+        c->allocs.push_back(p);
+        c->grad[l] = p;
+    }
+    if (!c->alloc(&c->logits, (size_t)Sc * B * c->O) || !c->alloc(&c->lossrow, (size_t)Sc * B))
+        return c->set_err(BNN_ERR_CUDA, "out of memory (logits)");
+    if (c->bf16) {
+        __nv_bfloat16* xb;
+        if (!c->alloc(&xb, (size_t)B * c->ld[0])) return c->set_err(BNN_ERR_CUDA, "out of memory");
+        c->xb = xb;
+        // TMA descriptors
+        c->map_fwdB.resize(L);
+        c->map_dgradB.resize(L);
+        c->map_wgG.resize(L);
+        c->map_wgX.resize(L);
+        for (int l = 0; l < L; ++l) {
+            const void* in = l == 0 ? c->xb : c->act[l];
+            const int depth = l == 0 ? 1 : Sc;
+            if (!make_map(&c->map_fwdB[l], in, c->widths[l], B, depth, c->ld[l], 256) ||
+                !make_map(&c->map_wgX[l], in, c->widths[l], B, depth, c->ld[l], 64) ||
+                !make_map(&c->map_dgradB[l], c->grad[l], c->widths[l + 1], B, Sc, c->ld[l + 1], 256) ||
+                !make_map(&c->map_wgG[l], c->grad[l], c->widths[l + 1], B, Sc, c->ld[l + 1], 64))
+                return c->set_err(BNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l);
+        }
+    }
+    return BNN_OK;
+}
+
+// ------------------------------------------------------------------ one chunk of samples
+int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
+              const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
+              uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+    const int L = (int)c->layers.size();
+    cudaStream_t st = c->st;
+    SampleKeys kk{make_key(seed), step, s0};
+    const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
+                                                     : 1.0f / ((float)S_glob * B_glob * c->O);
+    if (!c->bf16) {
+        // ---------------- FP32 SIMT path (parity mode)
+        for (int l = 0; l < L; ++l) {
+            SampledLayer sl = sampled(c, l, mu);
+            const float* A = l == 0 ? x : (const float*)c->act[l];
+            const int64_t sA = l == 0 ? 0 : (int64_t)B * c->ld[l];
+            float* Z = l == L - 1 ? c->logits : (float*)c->act[l + 1];
+            const int64_t sZ = (int64_t)B * (l == L - 1 ? c->O : c->ld[l + 1]);
+            c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, Sc, B, A, sA, Z, sZ, l < L - 1, st); });
+        }
+        c->launch("loss", [&] {
+            launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1], c->O,
+                             false, c->lossrow, st);
+        });
+        for (int l = L - 1; l >= 0; --l) {
+            SampledLayer sl = sampled(c, l, mu);
+            const float* Gl = (const float*)c->grad[l];
+            const int64_t sG = (int64_t)B * c->ld[l + 1];
+            const float* A = l == 0 ? x : (const float*)c->act[l];
+            const int64_t sA = l == 0 ? 0 : (int64_t)B * c->ld[l];
+            c->launch("wgrad", [&] {
+                launch_wgrad_fp32(sl, kk, Sc, B, Gl, sG, A, sA, scale, acc_mu, acc_rho, st);
+            });
+            c->launch("bias", [&] {
+                launch_bias_grad(sl, kk, Sc, B, Gl, sG, c->ld[l + 1], false, scale, acc_mu, acc_rho, st);
+            });
+            if (l > 0)
+                c->launch("dgrad", [&] {
+                    launch_dgrad_fp32(sl, kk, Sc, B, Gl, sG, (const float*)c->act[l], sA,
+                                      (float*)c->grad[l - 1], (int64_t)B * c->ld[l], st);
+                });
+        }
+    } else {
+        // ---------------- BF16 tcgen05 path
+        if (B > 256 * 64) return c->set_err(BNN_ERR_CONFIG, "B_loc too large");
+        const int nb = (int)round_up(std::min(B, 256), 16);
+        for (int l = 0; l < L; ++l) {
+            TcGenArgs a{};
+            a.L = sampled(c, l, mu);
+            a.kk = kk;
+            a.mode = 0;
+            a.B = B;
+            a.b_shared = l == 0 ? 1 : 0;
+            a.M = a.L.N;
+            a.R = a.L.K;
+            a.nb = nb;
+            a.out_f32 = l == L - 1;
+            a.relu = l < L - 1;
+            a.out = l == L - 1 ? (void*)c->logits : c->act[l + 1];
+            a.ldo = l == L - 1 ? c->O : c->ld[l + 1];
+            a.out_stride_s = (int64_t)B * a.ldo;
+            a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
+            c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, Sc, st); });
+        }
+        c->launch("loss", [&] {
+            launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1],
+                             c->ld[L], true, c->lossrow, st);
+        });
+        for (int l = L - 1; l >= 1; --l) {
+            TcGenArgs a{};
+            a.L = sampled(c, l, mu);
+            a.kk = kk;
+            a.mode = 1;
+            a.B = B;
+            a.b_shared = 0;
+            a.M = a.L.K;
+            a.R = a.L.N;
+            a.nb = nb;
+            a.out = c->grad[l - 1];
+            a.ldo = c->ld[l];
+            a.out_stride_s = (int64_t)B * c->ld[l];
+            a.mask = (const __nv_bfloat16*)c->act[l];
+            a.ldm = c->ld[l];
+            a.mask_stride_s = (int64_t)B * c->ld[l];
+            a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
+            c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[l], a, Sc, st); });
+        }
+        for (int l0 = 0; l0 < L; l0 += kMaxWgradLayers) {
+            TcWgradMaps maps;
+            TcWgradArgs w{};
+            w.kk = kk;
+            w.S = Sc;
+            w.B = B;
+            w.scale = scale;
+            w.acc_mu = acc_mu;
+            w.acc_rho = acc_rho;
+            int base = 0;
+            for (int l = l0; l < std::min(L, l0 + kMaxWgradLayers); ++l) {
+                WgradLayer& wl = w.lay[w.nlayers];
+                wl.L = sampled(c, l, mu);
+                wl.mtiles = (wl.L.N + 127) / 128;
+                wl.ktiles = (wl.L.K + 63) / 64;
+                wl.tile_base = base;
+                wl.b_shared = l == 0 ? 1 : 0;
+                base += wl.mtiles * wl.ktiles;
+                maps.g[w.nlayers] = c->map_wgG[l];
+                maps.x[w.nlayers] = c->map_wgX[l];
+                ++w.nlayers;
+            }
+            c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, st); });
+        }
+        for (int l = 0; l < L; ++l) {
+            SampledLayer sl = sampled(c, l, mu);
+            c->launch("bias", [&] {
+                launch_bias_grad(sl, kk, Sc, B, c->grad[l], (int64_t)B * c->ld[l + 1], c->ld[l + 1],
+                                 true, scale, acc_mu, acc_rho, st);
+            });
+        }
+    }
+    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    return BNN_OK;
+}
+
+int check_step_args(bnn_ctx* c, int B_loc, int B_glob, int S_glob) {
+    if (B_loc <= 0 || B_loc > c->B_max)
+        return c->set_err(BNN_ERR_CONFIG, "0 < B_loc <= max_B_loc (%d) violated: B_loc=%d", c->B_max, B_loc);
+    if (B_glob != B_loc * c->G)
+        return c->set_err(BNN_ERR_CONFIG, "B_global == G * B_loc violated (%d != %d * %d)", B_glob, c->G, B_loc);
+    if (S_glob <= 0 || S_glob % c->K != 0)
+        return c->set_err(BNN_ERR_CONFIG, "S mod K == 0 violated (S=%d, K=%d)", S_glob, c->K);
+    if (S_glob / c->K > c->S_loc_max)
+        return c->set_err(BNN_ERR_CONFIG, "S/K <= max_S_loc violated (%d > %d)", S_glob / c->K, c->S_loc_max);
+    if (S_glob >= (1 << 20)) return c->set_err(BNN_ERR_CONFIG, "S < 2^20 (EPS-v1 counter) violated");
+    return BNN_OK;
+}
+
+// local partial sums into acc (zeroed first)
+int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
+                const float* yreg, int B_loc, int B_glob, int S_glob, uint64_t seed, uint32_t step,
+                float* acc) {
+    int rc = check_step_args(c, B_loc, B_glob, S_glob);
+    if (rc) return rc;
+    if (c->model.loss == BNN_LOSS_CE && !ycls) return c->set_err(BNN_ERR_CONFIG, "CE loss needs int32 labels");
+    if (c->model.loss == BNN_LOSS_MSE && !yreg) return c->set_err(BNN_ERR_CONFIG, "MSE loss needs fp32 targets");
+    cudaStream_t st = c->st;
+    CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(float) * c->acc_total, st));
+    c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
+    if (c->bf16) {
+        const int K0 = c->widths[0];
+        c->launch("cast", [&] { launch_to_bf16(x, B_loc, K0, c->ld[0], c->xb, st); });
+    }
+    const int S_loc = S_glob / c->K;
+    for (int s = 0; s < S_loc; s += c->chunk) {
+        const int Sc = std::min(c->chunk, S_loc - s);
+        const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
+        rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
+                       acc + c->P_pad, acc + 2 * c->P_pad);
+        if (rc) return rc;
+    }
+    CUDA_TRY(c, cudaGetLastError());
+    return BNN_OK;
+}
+
+int run_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc, float* loss_dev,
+                 float* gmu, float* grho) {
+    cudaStream_t st = c->st;
+    c->launch("finalize", [&] {
+        launch_finalize(mu, rho, acc, acc + c->P_pad, acc + 2 * c->P_pad, c->P, c->cfg.dataset_size,
+                        gmu, grho, c->kl_part, c->n_part, c->lossbuf, st);
+    });
+    if (loss_dev) CUDA_TRY(c, cudaMemcpyAsync(loss_dev, c->lossbuf, sizeof(float), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaGetLastError());
+    return BNN_OK;
+}
+
+int read_loss(bnn_ctx* c, double* loss_host) {
+    float h = 0.f;
+    CUDA_TRY(c, cudaMemcpyAsync(&h, c->lossbuf, sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    *loss_host = h;
+    if (!std::isfinite(h)) return c->set_err(BNN_ERR_NUMERIC, "non-finite loss %f", (double)h);
+    return BNN_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int bnn_get_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        g_last_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+        return BNN_ERR_COMM;
+    }
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return BNN_OK;
+}
+
+int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) {
+    if (!model || !cfg || !out) {
+        g_last_error = "null argument";
+        return BNN_ERR_CONFIG;
+    }
+    *out = nullptr;
+    bnn_ctx* c = new bnn_ctx();
+    c->model = *model;
+    c->cfg = *cfg;
+    auto fail = [&](int rc) {
+        bnn_destroy(c);
+        return rc;
+    };
+    // ---- config invariants
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+        return fail(c->set_err(BNN_ERR_CONFIG, "0 <= rank < world violated"));
+    if (cfg->mode == BNN_MODE_SAMPLE_SHARDED) {
+        c->K = cfg->world;
+        c->G = 1;
+    } else if (cfg->mode == BNN_MODE_DATA_SHARDED) {
+        c->K = 1;
+        c->G = cfg->world;
+    } else if (cfg->mode == BNN_MODE_HYBRID) {
+        c->K = cfg->K;
+        c->G = cfg->G;
+        if (c->K < 1 || c->G < 1 || c->K * c->G != cfg->world)
+            return fail(c->set_err(BNN_ERR_CONFIG, "world == K*G violated (%d != %d*%d)", cfg->world, cfg->K, cfg->G));
+    } else {
+        return fail(c->set_err(BNN_ERR_CONFIG, "unknown mode %d", cfg->mode));
+    }
+    c->kidx = cfg->rank / c->G;
+    c->gidx = cfg->rank % c->G;
+    if (cfg->max_B_loc <= 0 || cfg->max_S_loc <= 0)
+        return fail(c->set_err(BNN_ERR_CONFIG, "max_B_loc > 0 and max_S_loc > 0 required"));
+    if (!(cfg->dataset_size > 0)) return fail(c->set_err(BNN_ERR_CONFIG, "dataset_size > 0 required"));
+    if (cfg->precision != BNN_PREC_FP32 && cfg->precision != BNN_PREC_BF16)
+        return fail(c->set_err(BNN_ERR_CONFIG, "unknown precision"));
+    if (cfg->aug != BNN_AUG_NONE && cfg->aug != BNN_AUG_PER_SAMPLE)
+        return fail(c->set_err(BNN_ERR_CONFIG, "unknown aug mode"));
+    if (model->loss != BNN_LOSS_CE && model->loss != BNN_LOSS_MSE)
+        return fail(c->set_err(BNN_ERR_CONFIG, "unknown loss"));
+    c->bf16 = cfg->precision == BNN_PREC_BF16;
+    c->B_max = cfg->max_B_loc;
+    c->S_loc_max = cfg->max_S_loc;
+    c->chunk = cfg->sample_chunk > 0 ? std::min(cfg->sample_chunk, cfg->max_S_loc) : cfg->max_S_loc;
+    int rc = build_layers(c);
+    if (rc) return fail(rc);
+    if (model->kind == BNN_MODEL_MLP && cfg->aug != BNN_AUG_NONE)
+        return fail(c->set_err(BNN_ERR_CONFIG, "augmentation applies to image models only"));
+    // ---- device
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(c->set_err(BNN_ERR_CUDA, "no CUDA device (there is no CPU fallback)"));
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(c->set_err(BNN_ERR_CONFIG, "bad device ordinal"));
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(c->set_err(BNN_ERR_CUDA, "cudaSetDevice failed"));
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, cfg->device);
+    if (prop.major != 10)
+        return fail(c->set_err(BNN_ERR_CUDA, "device is sm_%d%d; libbnn is built for sm_100a only", prop.major, prop.minor));
+    if (cfg->stream) {
+        c->st = reinterpret_cast<cudaStream_t>(cfg->stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess)
+            return fail(c->set_err(BNN_ERR_CUDA, "stream creation failed"));
+        c->own_stream = true;
+    }
+    // ---- workspace
+    c->n_part = finalize_partials_count(c->P);
+    if (!c->alloc(&c->sigma, c->P) || !c->alloc(&c->acc, c->acc_total) ||
+        !c->alloc(&c->kl_part, c->n_part) || !c->alloc(&c->lossbuf, 4) ||
+        !c->alloc(&c->x_stage, (size_t)c->B_max * std::max(1, c->widths.empty() ? 1 : c->widths[0])) ||
+        !c->alloc(&c->ycls_stage, c->B_max) || !c->alloc(&c->yreg_stage, (size_t)c->B_max * c->O) ||
+        !c->alloc(&c->p_mean, (size_t)c->B_max * c->G * c->O) || !c->alloc(&c->p_m2, (size_t)c->B_max * c->G * c->O) ||
+        !c->alloc(&c->g_means, (size_t)c->B_max * c->G * c->O * cfg->world) ||
+        !c->alloc(&c->g_m2s, (size_t)c->B_max * c->G * c->O * cfg->world) ||
+        !c->alloc(&c->g_counts, cfg->world))
+        return fail(c->set_err(BNN_ERR_CUDA, "out of device memory"));
+    rc = alloc_mlp(c);
+    if (rc) return fail(rc);
+    // ---- communicator
+    if (cfg->nccl_uid && cfg->world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_uid, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, cfg->world, id, cfg->rank);
+        if (r != ncclSuccess) return fail(c->set_err(BNN_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail(c->set_err(BNN_ERR_CUDA, "init sync failed"));
+    *out = c;
+    return BNN_OK;
+}
+
+int bnn_param_layout(bnn_ctx* c, int64_t* n_params, int32_t* n_tensors, bnn_tensor_info* infos,
+                     int32_t max_infos) {
+    if (!c) return BNN_ERR_CONFIG;
+    if (n_params) *n_params = c->P;
+    const int nt = (int)c->layers.size() * 2;
+    if (n_tensors) *n_tensors = nt;
+    if (infos) {
+        for (int t = 0; t < nt && t < max_infos; ++t) {
+            const LayerDesc& L = c->layers[t / 2];
+            bnn_tensor_info& I = infos[t];
+            I.t = t;
+            I.is_bias = t % 2;
+            if (t % 2 == 0) {
+                I.offset = L.off_w;
+                I.rows = L.cout;
+                I.cols = L.k * L.k * L.cin;
+            } else {
+                I.offset = L.off_b;
+                I.rows = 1;
+                I.cols = L.cout;
+            }
+        }
+    }
+    return BNN_OK;
+}
+
+int bnn_acc_layout(bnn_ctx* c, int64_t* rho_offset, int64_t* loss_offset, int64_t* total) {
+    if (!c) return BNN_ERR_CONFIG;
+    if (rho_offset) *rho_offset = c->P_pad;
+    if (loss_offset) *loss_offset = 2 * c->P_pad;
+    if (total) *total = c->acc_total;
+    return BNN_OK;
+}
+
+int bnn_elbo_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
+                     const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                     uint32_t step, float* acc_dev) {
+    if (!c || !mu || !rho || !x || !acc_dev) return BNN_ERR_CONFIG;
+    return run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, acc_dev);
+}
+
+int bnn_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc_dev, float* loss_dev,
+                 float* gmu, float* grho) {
+    if (!c || !mu || !rho || !acc_dev || !gmu || !grho) return BNN_ERR_CONFIG;
+    return run_finalize(c, mu, rho, acc_dev, loss_dev, gmu, grho);
+}
+
+int bnn_elbo_step(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
+                  const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                  uint32_t step, float* loss_dev, double* loss_host, float* gmu, float* grho) {
+    if (!c || !mu || !rho || !x || !gmu || !grho) {
+        if (c) return c->set_err(BNN_ERR_CONFIG, "null tensor argument");
+        return BNN_ERR_CONFIG;
+    }
+    if (c->cfg.world > 1 && !c->comm)
+        return c->set_err(BNN_ERR_CONFIG, "world > 1 without a communicator: use bnn_elbo_partial + bnn_finalize");
+    int rc = run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, c->acc);
+    if (rc) return rc;
+    if (c->comm) {
+        const int64_t t0 = c->launches;
+        (void)t0;
+        int cls = -1;
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (c->prof) {
+            cls = c->prof_class("allreduce");
+            if (c->ev_next + 2 > c->ev_pool.size()) c->prof_flush();
+            if (c->ev_next + 2 > c->ev_pool.size())
+                for (int i = 0; i < 64; ++i) {
+                    cudaEvent_t e;
+                    cudaEventCreate(&e);
+                    c->ev_pool.push_back(e);
+                }
+            a = c->ev_pool[c->ev_next++];
+            b = c->ev_pool[c->ev_next++];
+            cudaEventRecord(a, c->st);
+        }
+        NCCL_TRY(c, ncclAllReduce(c->acc, c->acc, (size_t)(2 * c->P_pad + 1), ncclFloat32, ncclSum, c->comm, c->st));
+        if (c->prof) {
+            cudaEventRecord(b, c->st);
+            c->pending.push_back({cls, {a, b}});
+        }
+    }
+    rc = run_finalize(c, mu, rho, c->acc, loss_dev, gmu, grho);
+    if (rc) return rc;
+    if (loss_host) return read_loss(c, loss_host);
+    return BNN_OK;
+}
+
+int bnn_elbo_step_host(bnn_ctx* c, const float* mu, const float* rho, const float* x_host,
+                       const int32_t* ycls_host, const float* yreg_host, int32_t B_loc, int32_t B_global,
+                       int32_t S_global, uint64_t seed, uint32_t step, double* loss_host, float* gmu,
+                       float* grho) {
+    if (!c || !x_host || !loss_host) return BNN_ERR_CONFIG;
+    if (B_loc <= 0 || B_loc > c->B_max) return c->set_err(BNN_ERR_CONFIG, "0 < B_loc <= max_B_loc violated");
+    const size_t in = (size_t)c->widths[0];
+    CUDA_TRY(c, cudaMemcpyAsync(c->x_stage, x_host, sizeof(float) * in * B_loc, cudaMemcpyHostToDevice, c->st));
+    if (ycls_host)
+        CUDA_TRY(c, cudaMemcpyAsync(c->ycls_stage, ycls_host, sizeof(int32_t) * B_loc, cudaMemcpyHostToDevice, c->st));
+    if (yreg_host)
+        CUDA_TRY(c, cudaMemcpyAsync(c->yreg_stage, yreg_host, sizeof(float) * B_loc * c->O, cudaMemcpyHostToDevice, c->st));
+    return bnn_elbo_step(c, mu, rho, c->x_stage, ycls_host ? c->ycls_stage : nullptr,
+                         yreg_host ? c->yreg_stage : nullptr, B_loc, B_global, S_global, seed, step, nullptr,
+                         loss_host, gmu, grho);
+}
+
+int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, int32_t B, int32_t S_global,
+                uint64_t seed, uint32_t step, float* mean, float* var) {
+    if (!c || !mu || !rho || !x || !mean || !var) return BNN_ERR_CONFIG;
+    if (c->G != 1) return c->set_err(BNN_ERR_CONFIG, "predict is sample-sharded only (G == 1)");
+    int rc = check_step_args(c, B, B * c->G, S_global);
+    if (rc) return rc;
+    cudaStream_t st = c->st;
+    const int L = (int)c->layers.size();
+    const int S_loc = S_global / c->K;
+    const int BO = B * c->O;
+    c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
+    if (c->bf16) c->launch("cast", [&] { launch_to_bf16(x, B, c->widths[0], c->ld[0], c->xb, st); });
+    // per chunk forward; stats over all local samples need all logits, so chunk == S_loc here
+    if (S_loc > c->chunk) return c->set_err(BNN_ERR_CONFIG, "predict needs S/K <= sample_chunk");
+    SampleKeys kk{make_key(seed), step, (uint32_t)(c->kidx * S_loc)};
+    const int nb = (int)round_up(std::min(B, 256), 16);
+    for (int l = 0; l < L; ++l) {
+        if (!c->bf16) {
+            SampledLayer sl = sampled(c, l, mu);
+            const float* A = l == 0 ? x : (const float*)c->act[l];
+            const int64_t sA = l == 0 ? 0 : (int64_t)B * c->ld[l];
+            float* Z = l == L - 1 ? c->logits : (float*)c->act[l + 1];
+            const int64_t sZ = (int64_t)B * (l == L - 1 ? c->O : c->ld[l + 1]);
+            c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, S_loc, B, A, sA, Z, sZ, l < L - 1, st); });
+        } else {
+            TcGenArgs a{};
+            a.L = sampled(c, l, mu);
+            a.kk = kk;
+            a.mode = 0;
+            a.B = B;
+            a.b_shared = l == 0 ? 1 : 0;
+            a.M = a.L.N;
+            a.R = a.L.K;
+            a.nb = nb;
+            a.out_f32 = l == L - 1;
+            a.relu = l < L - 1;
+            a.out = l == L - 1 ? (void*)c->logits : c->act[l + 1];
+            a.ldo = l == L - 1 ? c->O : c->ld[l + 1];
+            a.out_stride_s = (int64_t)B * a.ldo;
+            a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
+            c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, S_loc, st); });
+        }
+    }
+    c->launch("predict", [&] { launch_predict_stats(c->logits, S_loc, B, c->O, c->model.loss, c->p_mean, c->p_m2, st); });
+    const int R = c->cfg.world;
+    if (c->comm && R > 1) {
+        NCCL_TRY(c, ncclGroupStart());
+        NCCL_TRY(c, ncclAllGather(c->p_mean, c->g_means, BO, ncclFloat32, c->comm, st));
+        NCCL_TRY(c, ncclAllGather(c->p_m2, c->g_m2s, BO, ncclFloat32, c->comm, st));
+        NCCL_TRY(c, ncclGroupEnd());
+    } else if (R > 1) {
+        return c->set_err(BNN_ERR_CONFIG, "predict with world > 1 needs a communicator");
+    } else {
+        CUDA_TRY(c, cudaMemcpyAsync(c->g_means, c->p_mean, sizeof(float) * BO, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(c, cudaMemcpyAsync(c->g_m2s, c->p_m2, sizeof(float) * BO, cudaMemcpyDeviceToDevice, st));
+    }
+    std::vector<float> counts(R, (float)S_loc);
+    CUDA_TRY(c, cudaMemcpyAsync(c->g_counts, counts.data(), sizeof(float) * R, cudaMemcpyHostToDevice, st));
+    c->launch("predict", [&] { launch_predict_merge(c->g_means, c->g_m2s, c->g_counts, R, BO, mean, var, st); });
+    CUDA_TRY(c, cudaStreamSynchronize(st));  // counts host buffer lifetime
+    CUDA_TRY(c, cudaGetLastError());
+    return BNN_OK;
+}
+
+int bnn_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t r0, uint32_t nr,
+                 uint32_t c0, uint32_t nc, float* out, void* stream) {
+    if (!out) return BNN_ERR_CONFIG;
+    launch_eps_fill(seed, step, s, t, r0, nr, c0, nc, out, reinterpret_cast<cudaStream_t>(stream));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_last_error = cudaGetErrorString(e);
+        return BNN_ERR_CUDA;
+    }
+    return BNN_OK;
+}
+
+int bnn_eps_bench(uint64_t n4, uint64_t seed, float* sink, int32_t grid, void* stream) {
+    if (!sink || grid <= 0) return BNN_ERR_CONFIG;
+    launch_eps_bench(n4, seed, sink, grid, reinterpret_cast<cudaStream_t>(stream));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_last_error = cudaGetErrorString(e);
+        return BNN_ERR_CUDA;
+    }
+    return BNN_OK;
+}
+
+int bnn_profile_enable(bnn_ctx* c, int32_t on) {
+    if (!c) return BNN_ERR_CONFIG;
+    if (!on) c->prof_flush();
+    c->prof = on != 0;
+    if (on) {
+        for (size_t i = 0; i < c->prof_ms.size(); ++i) {
+            c->prof_ms[i] = 0.0;
+            c->prof_n[i] = 0;
+        }
+    }
+    return BNN_OK;
+}
+
+int bnn_profile_read(bnn_ctx* c, char* names, int32_t cap, double* ms, int64_t* launches, int32_t max_entries,
+                     int32_t* n_entries) {
+    if (!c) return BNN_ERR_CONFIG;
+    c->prof_flush();
+    std::string all;
+    const int n = (int)std::min<size_t>(c->prof_names.size(), (size_t)max_entries);
+    for (int i = 0; i < n; ++i) {
+        if (i) all += ",";
+        all += c->prof_names[i];
+        if (ms) ms[i] = c->prof_ms[i];
+        if (launches) launches[i] = c->prof_n[i];
+    }
+    if (names && cap > 0) {
+        strncpy(names, all.c_str(), cap - 1);
+        names[cap - 1] = 0;
+    }
+    if (n_entries) *n_entries = n;
+    return BNN_OK;
+}
+
+int64_t bnn_launch_count(bnn_ctx* c) { return c ? c->launches : -1; }
+
+const char* bnn_last_error(bnn_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
+
+void bnn_destroy(bnn_ctx* c) {
+    if (!c) return;
+    if (c->st) cudaStreamSynchronize(c->st);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (void* p : c->allocs) cudaFree(p);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,205 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * ε bit-exact (EPS-v1, docs/EPS.md);
+  * FP32 mode: loss and every gradient tensor within 1e-4 relative (‖Δ‖₂/‖ref‖₂ per tensor);
+  * BF16 tensor-core mode: within 2e-2 relative;
+  * sharded (virtual ranks, K×G grids) vs single rank: within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2604_04736_b200 import synth
+from paper_2604_04736_b200.configs import CONFIGS, MODELS
+
+pytestmark = pytest.mark.gpu
+
+C1 = MODELS["mlp_8_16_1"]
+C2 = MODELS["mlp_784_1024_1024_10"]
+RAGGED = dict(kind="mlp", widths=[100, 200, 130, 10], loss="ce")
+RAGGED_MSE = dict(kind="mlp", widths=[36, 72, 3], loss="mse")
+
+
+def _native():
+    from paper_2604_04736_b200 import native
+    return native
+
+
+def _dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _per_tensor_rel(ctx, g, ref):
+    out = []
+    for t in ctx.tensors:
+        sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
+        out.append(_rel(g[sl], ref[sl]))
+    return out
+
+
+def _inputs(model, B, rho_mode="init", seed=1):
+    mu, rho = synth.init_params(model, seed=seed + 1, rho_mode=rho_mode)
+    x, yc, yr = synth.make_batch(model, B, seed=seed)
+    return mu, rho, x, yc, yr
+
+
+def _run_gpu(model, precision, mu, rho, x, yc, yr, S, seed, step, D, **kw):
+    native = _native()
+    B = x.shape[0]
+    ctx = native.Context(model, precision=precision, max_B_loc=B, max_S_loc=S, dataset_size=D, **kw)
+    y = _dev(yc) if yc is not None else _dev(yr)
+    loss, gmu, grho = ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), y, B, S, seed, step)
+    torch.cuda.synchronize()
+    return ctx, loss, gmu.cpu().numpy(), grho.cpu().numpy()
+
+
+# ------------------------------------------------------------------ ε
+@pytest.mark.parametrize("args", [(0x5EED, 0, 0, 0, 0, 64, 0, 1024),
+                                  (0xFFFFFFFFFFFFFFFF, 7, 1048575, 4094, 123456, 3, 784, 261),
+                                  (42, 123456789, 31, 5, 0, 1, 0, 4 * 4096 + 3)])
+def test_eps_bit_exact(args):
+    native = _native()
+    g = native.eps_fill(*args).cpu().numpy()
+    o = O.eps_fill(*args)
+    assert g.dtype == o.dtype == np.float32
+    assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+def test_eps_bench_kernel_runs():
+    native = _native()
+    sink = torch.zeros(148 * 4, device="cuda")
+    native.eps_bench(1 << 20, 9, sink, 148 * 4)
+    torch.cuda.synchronize()
+    tot = float(sink.double().sum())
+    # mean of 4M normals: |Σ| ≲ 5·sqrt(4M)
+    assert abs(tot) < 5 * (4 << 20) ** 0.5
+
+
+# ------------------------------------------------------------------ full steps
+CASES = [
+    ("C1", C1, 32, 4, "wide"),
+    ("ragged_ce", RAGGED, 77, 3, "wide"),
+    ("ragged_mse", RAGGED_MSE, 40, 5, "init"),
+    ("C2_S4", C2, 256, 4, "init"),
+]
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 2e-2)])
+@pytest.mark.parametrize("name,model,B,S,rho_mode", CASES)
+def test_elbo_step_matches_oracle(name, model, B, S, rho_mode, precision, tol):
+    mu, rho, x, yc, yr = _inputs(model, B, rho_mode)
+    D = 1000.0
+    ctx, loss, gmu, grho = _run_gpu(model, precision, mu, rho, x, yc, yr, S, 0xC0FFEE, 3, D)
+    ref = O.elbo_step(model, mu, rho, x, yc, yr, S, 0xC0FFEE, 3, D)
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    rm = _per_tensor_rel(ctx, gmu, ref["grad_mu"])
+    rr = _per_tensor_rel(ctx, grho, ref["grad_rho"])
+    assert max(rm) <= tol, rm
+    assert max(rr) <= tol, rr
+
+
+def test_sigma_to_zero_limit_gpu():
+    """ρ = −40: the step is the deterministic network with weights μ (plus the KL terms)."""
+    mu, rho, x, yc, yr = _inputs(RAGGED, 33, "tiny")
+    ctx, loss, gmu, grho = _run_gpu(RAGGED, "fp32", mu, rho, x, yc, yr, 2, 1, 0, 500.0)
+    ref = O.elbo_step(RAGGED, mu, rho, x, yc, yr, 2, 1, 0, 500.0)
+    assert _rel(gmu, ref["grad_mu"]) < 1e-4
+    assert _rel(grho, ref["grad_rho"]) < 1e-4
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_sample_chunking_equals_single_chunk(precision):
+    mu, rho, x, yc, yr = _inputs(RAGGED, 64, "wide")
+    _, l1, g1, r1 = _run_gpu(RAGGED, precision, mu, rho, x, yc, yr, 6, 5, 1, 100.0)
+    _, l2, g2, r2 = _run_gpu(RAGGED, precision, mu, rho, x, yc, yr, 6, 5, 1, 100.0, sample_chunk=4)
+    assert _rel(g2, g1) < 1e-5 and _rel(r2, r1) < 1e-5
+    assert abs(l2 - l1) <= 1e-5 * abs(l1)
+
+
+def test_deterministic_bitwise():
+    mu, rho, x, yc, yr = _inputs(C2, 128, "init")
+    _, l1, g1, r1 = _run_gpu(C2, "bf16", mu, rho, x, yc, yr, 4, 5, 1, 100.0)
+    _, l2, g2, r2 = _run_gpu(C2, "bf16", mu, rho, x, yc, yr, 4, 5, 1, 100.0)
+    assert l1 == l2 and np.array_equal(g1, g2) and np.array_equal(r1, r2)
+
+
+# ------------------------------------------------------------------ sharding (virtual ranks)
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("mode,K,G", [("sample", 4, 1), ("data", 1, 2), ("hybrid", 2, 2)])
+def test_virtual_rank_sharding_equals_single_rank(mode, K, G, precision):
+    native = _native()
+    model, B, S, D = RAGGED, 64, 8, 321.0
+    mu, rho, x, yc, yr = _inputs(model, B, "wide")
+    mu_d, rho_d = _dev(mu), _dev(rho)
+    single = native.Context(model, precision=precision, max_B_loc=B, max_S_loc=S, dataset_size=D)
+    acc1 = single.elbo_partial(mu_d, rho_d, _dev(x), _dev(yc), B, S, 77, 9)
+    l1, g1, r1 = single.finalize(mu_d, rho_d, acc1)
+    total = None
+    world = K * G
+    for rank in range(world):
+        ctx = native.Context(model, precision=precision, mode=mode, K=K, G=G, rank=rank,
+                             world=world, max_B_loc=B // G, max_S_loc=S // K, dataset_size=D)
+        g = rank % G
+        xs, ys = x[g * (B // G):(g + 1) * (B // G)], yc[g * (B // G):(g + 1) * (B // G)]
+        acc = ctx.elbo_partial(mu_d, rho_d, _dev(xs), _dev(ys), B, S, 77, 9)
+        total = acc if total is None else total + acc  # fixed rank order
+    l2, g2, r2 = single.finalize(mu_d, rho_d, total)
+    torch.cuda.synchronize()
+    if precision == "fp32" or mode == "sample":
+        tol = 1e-5
+    else:
+        tol = 2e-2  # data sharding changes the bf16 rounding of nothing but summation order
+    assert _rel(g2.cpu().numpy(), g1.cpu().numpy()) < tol
+    assert _rel(r2.cpu().numpy(), r1.cpu().numpy()) < tol
+    assert abs(float(l2) - float(l1)) <= tol * abs(float(l1))
+
+
+# ------------------------------------------------------------------ predict
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 3e-2)])
+def test_predict_matches_oracle(precision, tol):
+    native = _native()
+    model, B, S = RAGGED, 50, 8
+    mu, rho, x, _, _ = _inputs(model, B, "wide")
+    ctx = native.Context(model, precision=precision, max_B_loc=B, max_S_loc=S, dataset_size=1.0)
+    mean, var = ctx.predict(_dev(mu), _dev(rho), _dev(x), S, 3, 0)
+    rm, rv = O.predict(model, mu, rho, x, S, 3, 0)
+    assert _rel(mean.cpu().numpy(), rm) < tol
+    assert _rel(var.cpu().numpy(), rv) < 5 * tol
+
+
+# ------------------------------------------------------------------ full BASELINE size (C2)
+def test_c2_full_size_bf16_loss_and_logits():
+    """BASELINE.json configs[1] at full size (B=256, S=64), bench launch configuration:
+    the loss needs every sample's forward pass (the oracle's forward only, ≈30 GFLOP fp64);
+    gradients at full size are checked in test_c2_full_size_bf16_gradients."""
+    cfg = CONFIGS["C2"]
+    mu, rho, x, yc, _ = _inputs(C2, cfg["B"], "init")
+    ctx, loss, gmu, grho = _run_gpu(C2, "bf16", mu, rho, x, yc, None, cfg["S"], 0x5EED, 0, cfg["D"])
+    z = O.forward(C2, mu, rho, x, 0, cfg["S"], 0x5EED, 0)
+    lse = np.log(np.exp(z - z.max(-1, keepdims=True)).sum(-1)) + z.max(-1)
+    L_data = float((lse - np.take_along_axis(z, yc[None, :, None].astype(np.int64), -1)[..., 0]).mean())
+    kl = O.finalize(C2, mu, rho, np.zeros(2 * ctx.n_params + 1), cfg["D"])["kl"]
+    ref = L_data + kl / cfg["D"]
+    assert abs(loss - ref) <= 2e-2 * abs(ref)
+    assert np.all(np.isfinite(gmu)) and np.all(np.isfinite(grho))
+
+
+@pytest.mark.slow
+def test_c2_full_size_bf16_gradients():
+    cfg = CONFIGS["C2"]
+    mu, rho, x, yc, _ = _inputs(C2, cfg["B"], "init")
+    ctx, loss, gmu, grho = _run_gpu(C2, "bf16", mu, rho, x, yc, None, cfg["S"], 0x5EED, 0, cfg["D"])
+    ref = O.elbo_step(C2, mu, rho, x, yc, None, cfg["S"], 0x5EED, 0, cfg["D"])
+    assert max(_per_tensor_rel(ctx, gmu, ref["grad_mu"])) <= 2e-2
+    assert max(_per_tensor_rel(ctx, grho, ref["grad_rho"])) <= 2e-2
