@@ -24,7 +24,7 @@
  *    Unless stated, tensors are dense, row-major, 16-byte aligned (256-byte preferred).
  *  - The caller owns every tensor passed in. The library owns its workspace (allocated in
  *    bnn_init, never inside a step), its NCCL communicator and its CUDA streams/events.
- *  - All device work is enqueued on cfg.stream (NULL: a stream the library creates); calls
+ *  - All device work is enqueued on cfg.stream (NULL: the legacy default stream); calls
  *    return after enqueue unless a *_host output is requested, which synchronises.
  *  - A bnn_ctx is used by one host thread at a time.
  *  - There is no CPU fallback: without a usable sm_100 device bnn_init fails with
@@ -94,7 +94,7 @@ typedef struct bnn_config {
     int32_t aug;              /* BNN_AUG_NONE | BNN_AUG_PER_SAMPLE (images only; docs/EPS.md §4) */
     double dataset_size;      /* |D| of PAPER.md:164, > 0 */
     int32_t device;           /* CUDA device ordinal */
-    void* stream;             /* cudaStream_t or NULL */
+    void* stream;             /* cudaStream_t; NULL = the legacy default stream */
 } bnn_config;
 
 typedef struct bnn_tensor_info {

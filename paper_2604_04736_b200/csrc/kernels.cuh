@@ -35,7 +35,7 @@ int finalize_partials_count(int64_t P);
 // row stride ldg, and per-(s,b) loss values.
 void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,
                       const int32_t* ycls, const float* yreg, void* dz, int ldg, bool dz_bf16,
-                      float* lossrow, cudaStream_t st);
+                      float* lossrow, float* dz_f32, cudaStream_t st);
 // acc[2P] += scale · Σ lossrow[0..n) in fixed order
 void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slot,
                         cudaStream_t st);
@@ -64,9 +64,9 @@ void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B,
 void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
                        int64_t strideG, const float* A, int64_t strideA, float scale,
                        float* acc_mu, float* acc_rho, cudaStream_t st);
-// bias part of the above for bf16 or fp32 G with row stride ldg
-void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, int B, const void* G,
-                      int64_t strideG, int ldg, bool g_bf16, float scale, float* acc_mu,
-                      float* acc_rho, cudaStream_t st);
+// bias gradient from fp32 partial column sums parts[s][p][n] (p < nparts, row pitch ldp)
+void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
+                      int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
+                      float* acc_mu, float* acc_rho, cudaStream_t st);
 
 }  // namespace bnn

@@ -117,7 +117,8 @@ void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
 __global__ void loss_head_kernel(const float* __restrict__ logits, int rows, int B, int O,
                                  int loss_kind, const int32_t* __restrict__ ycls,
                                  const float* __restrict__ yreg, void* __restrict__ dz, int ldg,
-                                 int dz_bf16, float* __restrict__ lossrow) {
+                                 int dz_bf16, float* __restrict__ lossrow,
+                                 float* __restrict__ dz_f32) {
     const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (warp >= rows) return;
@@ -125,6 +126,7 @@ __global__ void loss_head_kernel(const float* __restrict__ logits, int rows, int
     const float* z = logits + (int64_t)warp * O;
     float loss = 0.0f;
     auto put = [&](int k, float v) {
+        if (dz_f32 && k < O) dz_f32[(int64_t)warp * O + k] = v;
         if (dz_bf16)
             reinterpret_cast<__nv_bfloat16*>(dz)[(int64_t)warp * ldg + k] = __float2bfloat16_rn(v);
         else
@@ -156,10 +158,10 @@ __global__ void loss_head_kernel(const float* __restrict__ logits, int rows, int
 
 void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,
                       const int32_t* ycls, const float* yreg, void* dz, int ldg, bool dz_bf16,
-                      float* lossrow, cudaStream_t st) {
+                      float* lossrow, float* dz_f32, cudaStream_t st) {
     const int rows = S * B;
     loss_head_kernel<<<(rows + 7) / 8, 256, 0, st>>>(logits, rows, B, O, loss_kind, ycls, yreg,
-                                                     dz, ldg, dz_bf16 ? 1 : 0, lossrow);
+                                                     dz, ldg, dz_bf16 ? 1 : 0, lossrow, dz_f32);
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ lossrow, int n, float scale,
@@ -536,32 +538,42 @@ void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B,
                                             acc_rho);
 }
 
-__global__ void bias_grad_kernel(SampledLayer L, SampleKeys kk, int S, int B,
-                                 const void* __restrict__ G, int64_t strideG, int ldg, int g_bf16,
-                                 float scale, float* __restrict__ acc_mu,
-                                 float* __restrict__ acc_rho) {
+// Bias gradient in two deterministic phases. parts[s][p][n] are fp32 partial column sums
+// of the layer's output gradient (B rows in FP32 mode; 32-row chunks written by the BF16
+// dgrad epilogue; the loss head's fp32 seed for the last layer).
+//   phase A: db[s][n] = Σ_p parts[s][p][n]
+//   phase B: acc_μ[b_n] += scale·Σ_s db[s][n];  acc_ρ[b_n] += scale·Σ_s db[s][n]·ε_s(t_b, 0, n)
+__global__ void bias_reduce_kernel(const float* __restrict__ parts, int nparts, int ldp,
+                                   int64_t strideS, int N, float* __restrict__ db) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, s = blockIdx.y;
+    if (n >= N) return;
+    const float* p = parts + s * strideS + n;
+    float acc = 0.0f;
+    for (int i = 0; i < nparts; ++i) acc += p[(int64_t)i * ldp];
+    db[(int64_t)s * N + n] = acc;
+}
+
+__global__ void bias_acc_kernel(SampledLayer L, SampleKeys kk, int S,
+                                const float* __restrict__ db, float scale,
+                                float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= L.N) return;
     float am = 0.0f, ar = 0.0f;
     for (int s = 0; s < S; ++s) {
-        float db = 0.0f;
-        for (int b = 0; b < B; ++b) {
-            const int64_t o = s * strideG + (int64_t)b * ldg + n;
-            db += g_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(G)[o])
-                         : reinterpret_cast<const float*>(G)[o];
-        }
-        am += db;
-        ar = fmaf(db, eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n), ar);
+        const float d = db[(int64_t)s * L.N + n];
+        am += d;
+        ar = fmaf(d, eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n), ar);
     }
     acc_mu[L.off_b + n] += scale * am;
     acc_rho[L.off_b + n] += scale * ar;
 }
 
-void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, int B, const void* G,
-                      int64_t strideG, int ldg, bool g_bf16, float scale, float* acc_mu,
-                      float* acc_rho, cudaStream_t st) {
-    bias_grad_kernel<<<(L.N + 127) / 128, 128, 0, st>>>(L, k, S, B, G, strideG, ldg,
-                                                        g_bf16 ? 1 : 0, scale, acc_mu, acc_rho);
+void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
+                      int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
+                      float* acc_mu, float* acc_rho, cudaStream_t st) {
+    dim3 grid((L.N + 127) / 128, S);
+    bias_reduce_kernel<<<grid, 128, 0, st>>>(parts, nparts, ldp, strideS, L.N, db_scratch);
+    bias_acc_kernel<<<(L.N + 127) / 128, 128, 0, st>>>(L, k, S, db_scratch, scale, acc_mu, acc_rho);
 }
 
 }  // namespace bnn

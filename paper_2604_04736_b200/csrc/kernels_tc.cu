@@ -193,26 +193,38 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
             float v[32];
             __syncwarp();
             tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + c * 32, v);
+            if (m >= a.M) continue;
+            const int bc0 = b0 + c * 32;
+            if (bc0 >= a.B) continue;
+            const int nvalid = min(32, a.B - bc0);
+            if (a.mode == 0) {
+                if (a.out_f32) {
+                    float* o = reinterpret_cast<float*>(a.out) + s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
 #pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-                const int b = b0 + c * 32 + j;
-                if (b >= a.B || m >= a.M) break;
-                if (a.mode == 0) {
-                    float z = v[j] + bias;
-                    if (a.out_f32) {
-                        reinterpret_cast<float*>(a.out)[s * a.out_stride_s + (int64_t)b * a.ldo + m] = z;
-                    } else {
-                        if (a.relu) z = fmaxf(z, 0.0f);
-                        reinterpret_cast<__nv_bfloat16*>(a.out)[s * a.out_stride_s +
-                                                                (int64_t)b * a.ldo + m] =
-                            __float2bfloat16_rn(z);
-                    }
+                    for (int j = 0; j < nvalid; ++j) o[(int64_t)j * a.ldo] = v[j] + bias;
                 } else {
-                    const int64_t o = s * a.out_stride_s + (int64_t)b * a.ldo + m;
-                    const float mk = __bfloat162float(a.mask[s * a.mask_stride_s + (int64_t)b * a.ldm + m]);
-                    reinterpret_cast<__nv_bfloat16*>(a.out)[o] =
-                        __float2bfloat16_rn(mk > 0.0f ? v[j] : 0.0f);
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + s * a.out_stride_s +
+                                       (int64_t)bc0 * a.ldo + m;
+#pragma unroll 4
+                    for (int j = 0; j < nvalid; ++j) {
+                        float z = v[j] + bias;
+                        if (a.relu) z = fmaxf(z, 0.0f);
+                        o[(int64_t)j * a.ldo] = __float2bfloat16_rn(z);
+                    }
                 }
+            } else {
+                const __nv_bfloat16* mk = a.mask + s * a.mask_stride_s + (int64_t)bc0 * a.ldm + m;
+                __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + s * a.out_stride_s +
+                                   (int64_t)bc0 * a.ldo + m;
+                float part = 0.0f;
+#pragma unroll 4
+                for (int j = 0; j < nvalid; ++j) {
+                    const float g = __bfloat162float(mk[(int64_t)j * a.ldm]) > 0.0f ? v[j] : 0.0f;
+                    part += g;
+                    o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
+                }
+                // fp32 partial column sum over this 32-row chunk: the bias gradient source
+                a.dbpart[s * a.dbpart_stride_s + (int64_t)(bc0 >> 5) * a.M + m] = part;
             }
         }
     }

@@ -99,6 +99,9 @@ struct bnn_ctx {
     std::vector<void*> act;    // act[l]: input of layer l (l ≥ 1)
     std::vector<int> ld;       // padded row pitch of width l
     std::vector<void*> grad;   // grad[l]: dℓ/dz of layer l output
+    std::vector<float*> dbpart;  // BF16: fp32 32-row column sums of grad[l] (l < L-1)
+    float* dz_f32 = nullptr;     // BF16: fp32 copy of the loss-head seed [S][B][O]
+    float* db_scratch = nullptr; // [S][max N] per-sample bias gradients
     void* xb = nullptr;        // bf16 copy of the layer-0 input
     float* x_stage = nullptr;  // device copy of a host batch
     int32_t* ycls_stage = nullptr;
@@ -163,7 +166,7 @@ struct bnn_ctx {
         ev_next = 0;
     }
     template <class F>
-    void launch(const char* cls, F&& f) {
+    void launch(const char* cls, F&& f, int kernels = 1) {
         int c = -1;
         cudaEvent_t a = nullptr, b = nullptr;
         if (prof) {
@@ -181,7 +184,7 @@ struct bnn_ctx {
             cudaEventRecord(a, st);
         }
         f();
-        ++launches;
+        launches += kernels;
         if (prof) {
             cudaEventRecord(b, st);
             pending.push_back({c, {a, b}});
@@ -278,6 +281,17 @@ int alloc_mlp(bnn_ctx* c) {
     }
     if (!c->alloc(&c->logits, (size_t)Sc * B * c->O) || !c->alloc(&c->lossrow, (size_t)Sc * B))
         return c->set_err(BNN_ERR_CUDA, "out of memory (logits)");
+    int maxN = 0;
+    for (int l = 0; l < L; ++l) maxN = std::max(maxN, c->widths[l + 1]);
+    if (!c->alloc(&c->db_scratch, (size_t)Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+    if (c->bf16) {
+        if (!c->alloc(&c->dz_f32, (size_t)Sc * B * c->O)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+        c->dbpart.assign(L, nullptr);
+        const int nbc = (B + 31) / 32;
+        for (int l = 0; l + 1 < L; ++l)
+            if (!c->alloc(&c->dbpart[l], (size_t)Sc * nbc * c->widths[l + 1]))
+                return c->set_err(BNN_ERR_CUDA, "out of memory");
+    }
     if (c->bf16) {
         __nv_bfloat16* xb;
         if (!c->alloc(&xb, (size_t)B * c->ld[0])) return c->set_err(BNN_ERR_CUDA, "out of memory");
@@ -321,7 +335,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
         }
         c->launch("loss", [&] {
             launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1], c->O,
-                             false, c->lossrow, st);
+                             false, c->lossrow, nullptr, st);
         });
         for (int l = L - 1; l >= 0; --l) {
             SampledLayer sl = sampled(c, l, mu);
@@ -333,8 +347,9 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                 launch_wgrad_fp32(sl, kk, Sc, B, Gl, sG, A, sA, scale, acc_mu, acc_rho, st);
             });
             c->launch("bias", [&] {
-                launch_bias_grad(sl, kk, Sc, B, Gl, sG, c->ld[l + 1], false, scale, acc_mu, acc_rho, st);
-            });
+                launch_bias_grad(sl, kk, Sc, Gl, B, c->ld[l + 1], sG, scale, c->db_scratch, acc_mu,
+                                 acc_rho, st);
+            }, 2);
             if (l > 0)
                 c->launch("dgrad", [&] {
                     launch_dgrad_fp32(sl, kk, Sc, B, Gl, sG, (const float*)c->act[l], sA,
@@ -365,7 +380,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
         }
         c->launch("loss", [&] {
             launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1],
-                             c->ld[L], true, c->lossrow, st);
+                             c->ld[L], true, c->lossrow, c->dz_f32, st);
         });
         for (int l = L - 1; l >= 1; --l) {
             TcGenArgs a{};
@@ -384,6 +399,8 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.ldm = c->ld[l];
             a.mask_stride_s = (int64_t)B * c->ld[l];
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
+            a.dbpart = c->dbpart[l - 1];
+            a.dbpart_stride_s = (int64_t)((B + 31) / 32) * a.L.K;
             c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[l], a, Sc, st); });
         }
         for (int l0 = 0; l0 < L; l0 += kMaxWgradLayers) {
@@ -412,10 +429,15 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
         }
         for (int l = 0; l < L; ++l) {
             SampledLayer sl = sampled(c, l, mu);
+            const bool last = l == L - 1;
+            const int nbc = (B + 31) / 32;
+            const float* parts = last ? c->dz_f32 : c->dbpart[l];
+            const int nparts = last ? B : nbc;
+            const int ldp = last ? c->O : sl.N;
             c->launch("bias", [&] {
-                launch_bias_grad(sl, kk, Sc, B, c->grad[l], (int64_t)B * c->ld[l + 1], c->ld[l + 1],
-                                 true, scale, acc_mu, acc_rho, st);
-            });
+                launch_bias_grad(sl, kk, Sc, parts, nparts, ldp, (int64_t)nparts * ldp, scale,
+                                 c->db_scratch, acc_mu, acc_rho, st);
+            }, 2);
         }
     }
     c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
@@ -468,7 +490,7 @@ int run_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc
     c->launch("finalize", [&] {
         launch_finalize(mu, rho, acc, acc + c->P_pad, acc + 2 * c->P_pad, c->P, c->cfg.dataset_size,
                         gmu, grho, c->kl_part, c->n_part, c->lossbuf, st);
-    });
+    }, 2);
     if (loss_dev) CUDA_TRY(c, cudaMemcpyAsync(loss_dev, c->lossbuf, sizeof(float), cudaMemcpyDeviceToDevice, st));
     CUDA_TRY(c, cudaGetLastError());
     return BNN_OK;
@@ -559,13 +581,7 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     cudaGetDeviceProperties(&prop, cfg->device);
     if (prop.major != 10)
         return fail(c->set_err(BNN_ERR_CUDA, "device is sm_%d%d; libbnn is built for sm_100a only", prop.major, prop.minor));
-    if (cfg->stream) {
-        c->st = reinterpret_cast<cudaStream_t>(cfg->stream);
-    } else {
-        if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess)
-            return fail(c->set_err(BNN_ERR_CUDA, "stream creation failed"));
-        c->own_stream = true;
-    }
+    c->st = reinterpret_cast<cudaStream_t>(cfg->stream);  // NULL = legacy default stream
     // ---- workspace
     c->n_part = finalize_partials_count(c->P);
     if (!c->alloc(&c->sigma, c->P) || !c->alloc(&c->acc, c->acc_total) ||
@@ -822,7 +838,7 @@ const char* bnn_last_error(bnn_ctx* c) { return c ? c->err.c_str() : g_last_erro
 
 void bnn_destroy(bnn_ctx* c) {
     if (!c) return;
-    if (c->st) cudaStreamSynchronize(c->st);
+    if (!c->allocs.empty()) cudaStreamSynchronize(c->st);
     if (c->comm) ncclCommDestroy(c->comm);
     for (void* p : c->allocs) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
