@@ -184,6 +184,12 @@ int bnn_predict(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const f
 int bnn_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
                  uint32_t nr, uint32_t c0, uint32_t nc, float* out_dev, void* stream);
 
+/* Every value of the EPS-v1 transform pieces (docs/EPS.md §3), for the exhaustive
+ * bit-exactness test: which = 0 → out[k-1] = R = sqrt_rn(-2·LOG24(k·2^-24)), k = 1..2^24;
+ * which = 1 / 2 → out[v] = cos / sin part of SINCOS2PI24(v), v = 0..2^24-1.
+ * out_dev holds 2^24 floats. */
+int bnn_eps_transform_table(int32_t which, float* out_dev, void* stream);
+
 /* ε-throughput microbenchmark (the ALU roofline of DESIGN.md §4): generates n4·4 normals
  * with the same code as the fused kernels and reduces them into sink_dev[grid] instead of
  * storing them. */

@@ -41,6 +41,7 @@ void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slo
                         cudaStream_t st);
 void launch_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
                      uint32_t nr, uint32_t c0, uint32_t nc, float* out, cudaStream_t st);
+void launch_eps_table(int which, float* out, cudaStream_t st);
 void launch_eps_bench(uint64_t n4, uint64_t seed, float* sink, int grid, cudaStream_t st);
 // predict: probabilities/outputs [S][B][O] → local mean and M2 (two-pass)
 void launch_predict_stats(const float* logits, int S, int B, int O, int loss_kind, float* mean,

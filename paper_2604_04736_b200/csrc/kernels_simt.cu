@@ -226,6 +226,23 @@ void launch_eps_bench(uint64_t n4, uint64_t seed, float* sink, int grid, cudaStr
     eps_bench_kernel<<<grid, 256, 0, st>>>(n4, make_key(seed), sink);
 }
 
+// every EPS-v1 transform input: which 0 → R(k) for k = 1..2^24 (u = k·2^-24),
+// which 1/2 → cos/sin(2π v/2^24) for v = 0..2^24-1
+__global__ void eps_table_kernel(int which, float* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (1u << 24)) return;
+    if (which == 0) {
+        out[i] = bm_radius(i << 8);  // (a >> 8) + 1 = i + 1
+    } else {
+        const float2 cs = bm_sincos(i << 8);
+        out[i] = which == 1 ? cs.x : cs.y;
+    }
+}
+
+void launch_eps_table(int which, float* out, cudaStream_t st) {
+    eps_table_kernel<<<(1 << 24) / 256, 256, 0, st>>>(which, out);
+}
+
 // ====================================================================== K10: predict stats
 __global__ void predict_stats_kernel(const float* __restrict__ logits, int S, int B, int O,
                                      int loss_kind, float* __restrict__ mean,
@@ -543,26 +560,26 @@ void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B,
 // dgrad epilogue; the loss head's fp32 seed for the last layer).
 //   phase A: db[s][n] = Σ_p parts[s][p][n]
 //   phase B: acc_μ[b_n] += scale·Σ_s db[s][n];  acc_ρ[b_n] += scale·Σ_s db[s][n]·ε_s(t_b, 0, n)
-__global__ void bias_reduce_kernel(const float* __restrict__ parts, int nparts, int ldp,
-                                   int64_t strideS, int N, float* __restrict__ db) {
+__global__ void bias_reduce_kernel(SampledLayer L, SampleKeys kk, const float* __restrict__ parts,
+                                   int nparts, int ldp, int64_t strideS, int S,
+                                   float* __restrict__ db) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x, s = blockIdx.y;
-    if (n >= N) return;
+    if (n >= L.N) return;
     const float* p = parts + s * strideS + n;
     float acc = 0.0f;
     for (int i = 0; i < nparts; ++i) acc += p[(int64_t)i * ldp];
-    db[(int64_t)s * N + n] = acc;
+    db[(int64_t)s * L.N + n] = acc;
+    db[(int64_t)(S + s) * L.N + n] = acc * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n);
 }
 
-__global__ void bias_acc_kernel(SampledLayer L, SampleKeys kk, int S,
-                                const float* __restrict__ db, float scale,
+__global__ void bias_acc_kernel(SampledLayer L, int S, const float* __restrict__ db, float scale,
                                 float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= L.N) return;
     float am = 0.0f, ar = 0.0f;
     for (int s = 0; s < S; ++s) {
-        const float d = db[(int64_t)s * L.N + n];
-        am += d;
-        ar = fmaf(d, eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n), ar);
+        am += db[(int64_t)s * L.N + n];
+        ar += db[(int64_t)(S + s) * L.N + n];
     }
     acc_mu[L.off_b + n] += scale * am;
     acc_rho[L.off_b + n] += scale * ar;
@@ -572,8 +589,8 @@ void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const f
                       int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
                       float* acc_mu, float* acc_rho, cudaStream_t st) {
     dim3 grid((L.N + 127) / 128, S);
-    bias_reduce_kernel<<<grid, 128, 0, st>>>(parts, nparts, ldp, strideS, L.N, db_scratch);
-    bias_acc_kernel<<<(L.N + 127) / 128, 128, 0, st>>>(L, k, S, db_scratch, scale, acc_mu, acc_rho);
+    bias_reduce_kernel<<<grid, 128, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
+    bias_acc_kernel<<<(L.N + 127) / 128, 128, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
 }
 
 }  // namespace bnn

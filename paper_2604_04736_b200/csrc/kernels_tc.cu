@@ -55,7 +55,8 @@ __device__ __forceinline__ void load_mu_sigma4(const SampledLayer& L, int64_t i,
     }
 }
 
-// W_s[n][k .. k+3] as two packed bf16x2 words (zero outside the tensor).
+// W_s[n][k .. k+3] as two packed bf16x2 words (zero outside the tensor). Checked path,
+// used only for edge tiles.
 __device__ __forceinline__ uint2 gen_w4(const SampledLayer& L, const SampleKeys& kk, uint32_t sg,
                                         int n, int k, bool vec) {
     if (n >= L.N || k >= L.K) return make_uint2(0u, 0u);
@@ -74,6 +75,29 @@ __device__ __forceinline__ uint2 gen_w4(const SampledLayer& L, const SampleKeys&
     return make_uint2(pack_bf16x2(w0, w1), pack_bf16x2(w2, w3));
 }
 
+// Fast path: interior tile, 16-byte aligned μ/σ rows, no bounds checks.
+__device__ __forceinline__ uint2 gen_w4_fast(const float* __restrict__ mu,
+                                             const float* __restrict__ sigma, EpsKey key,
+                                             uint32_t step, uint32_t w3, uint32_t n, uint32_t cq) {
+    const float4 m = __ldg(reinterpret_cast<const float4*>(mu));
+    const float4 s = __ldg(reinterpret_cast<const float4*>(sigma));
+    const uint4 y = philox10(make_uint4(cq, n, w3, step), key);
+    const float R0 = bm_radius(y.x);
+    const float2 cs0 = bm_sincos(y.y);
+    const float R1 = bm_radius(y.z);
+    const float2 cs1 = bm_sincos(y.w);
+    const float w0 = __fmaf_rn(s.x, __fmul_rn(R0, cs0.x), m.x);
+    const float w1 = __fmaf_rn(s.y, __fmul_rn(R0, cs0.y), m.y);
+    const float w2 = __fmaf_rn(s.z, __fmul_rn(R1, cs1.x), m.z);
+    const float w3v = __fmaf_rn(s.w, __fmul_rn(R1, cs1.y), m.w);
+    return make_uint2(pack_bf16x2(w0, w1), pack_bf16x2(w2, w3v));
+}
+
+__device__ __forceinline__ void sts64(uint32_t addr, uint2 v) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(gen::kThreads, 2)
     gen_gemm_kernel(const __grid_constant__ CUtensorMap tmB, const TcGenArgs a) {
     using namespace gen;
@@ -106,7 +130,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
         tma_prefetch_desc(&tmB);
     }
     if (warp == kGenWarps) tmem_alloc(tslot, 256);
-    if (a.mode == 0 && tid < 128) {
+    if (MODE == 0 && tid < 128) {
         const int n = m0 + tid;
         sbias[tid] = n < L.N ? __fmaf_rn(L.sigma[L.off_b + n],
                                          eps1(a.kk.key, a.kk.step, sg, L.t_b, 0u, (uint32_t)n),
@@ -118,24 +142,23 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const int nkb = (a.R + 63) / 64;
-    const bool vec = a.vec_ok != 0;
 
     if (warp == kGenWarps) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
-            const uint32_t idesc = idesc_bf16(128, a.nb, a.mode == 1 ? 1 : 0, 0);
+            const uint32_t idesc = idesc_bf16(128, a.nb, MODE == 1 ? 1 : 0, 0);
             for (int kb = 0; kb < nkb; ++kb) {
                 const int st = kb % kStages;
                 const uint32_t ph = (kb / kStages) & 1;
-                mbar_wait(&full_gen[st], ph);
-                mbar_wait(&full_tma[st], ph);
+                mbar_wait_sleep(&full_gen[st], ph);
+                mbar_wait_sleep(&full_tma[st], ph);
                 tc_fence_after();
                 const uint32_t aBase = smem_u32(sA + st * kAStage);
                 const uint32_t bBase = smem_u32(sB + st * kBStage);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const uint64_t ad = a.mode == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
-                                                    : sdesc_sw128(aBase + 2048 * q, 8192, 1024);
+                    const uint64_t ad = MODE == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
+                                                  : sdesc_sw128(aBase + 2048 * q, 8192, 1024);
                     const uint64_t bd = sdesc_sw128(bBase + 32 * q, 16, 1024);
                     mma_bf16(tmem, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
                 }
@@ -146,6 +169,22 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
         __syncwarp();
     } else {
         // ------------------------------------------------ generator warps
+        // Thread → item mapping (constant per thread; `it` advances the row):
+        //   fwd  : row = it*16 + (tid>>4) (output feature n), quad kq = tid&15 of the 64 k
+        //   dgrad: row = it*8 + (tid>>5) (output feature n = the MMA K dim), quad mq = tid&31
+        //          of the 128 k of this M tile (two 64-wide MN blocks)
+        // The 128B-swizzle chunk depends on row&7, which is constant per thread.
+        const int rsub = MODE == 0 ? (tid >> 4) : (tid >> 5);
+        const int qd = MODE == 0 ? (tid & 15) : (tid & 31);
+        const int rstep = MODE == 0 ? 16 : 8;
+        const uint32_t soff0 =
+            MODE == 0 ? rsub * 128 + ((((qd >> 1) ^ (rsub & 7))) << 4) + ((qd & 1) << 3)
+                      : (qd >> 4) * 8192 + rsub * 128 + (((((qd & 15) >> 1) ^ (rsub & 7))) << 4) +
+                            ((qd & 1) << 3);
+        const uint32_t sstep = MODE == 0 ? 2048 : 1024;
+        const bool vec = a.vec_ok != 0;
+        const uint32_t w3 = (L.t_w << 20) | sg;
+        const bool m_full = MODE == 0 ? (m0 + 128 <= L.N) : (m0 + 128 <= L.K);
         for (int kb = 0; kb < nkb; ++kb) {
             const int st = kb % kStages;
             const uint32_t ph = (kb / kStages) & 1;
@@ -155,76 +194,91 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                 tma_load_3d(&tmB, &full_tma[st], sB + st * kBStage, kb * 64, b0,
                             a.b_shared ? 0 : s);
             }
-            uint8_t* tileA = sA + st * kAStage;
-#pragma unroll 2
-            for (int it = 0; it < 8; ++it) {
-                const int item = it * 256 + tid;
-                uint32_t off;
-                int n, k;
-                if (a.mode == 0) {  // rows = n (128), 16 quads of k per row; K-major SW128
-                    const int row = item >> 4, kq = item & 15;
-                    n = m0 + row;
-                    k = kb * 64 + 4 * kq;
-                    off = row * 128 + ((((kq >> 1) ^ (row & 7))) << 4) + ((kq & 1) << 3);
-                } else {  // rows = n (64, the MMA K dim), 32 quads of k (M) per row; MN-major
-                    const int r = item >> 5, mq = item & 31;
-                    n = kb * 64 + r;
-                    k = m0 + 4 * mq;
-                    const int blk = mq >> 4, c = mq & 15;
-                    off = blk * 8192 + r * 128 + ((((c >> 1) ^ (r & 7))) << 4) + ((c & 1) << 3);
+            const uint32_t tileA = smem_u32(sA + st * kAStage) + soff0;
+            const bool full = vec && m_full &&
+                              (MODE == 0 ? (kb * 64 + 64 <= L.K) : (kb * 64 + 64 <= L.N));
+            if (full) {
+                // n, k of item 0; item `it` adds rstep rows
+                const int n0 = MODE == 0 ? m0 + rsub : kb * 64 + rsub;
+                const int k0 = MODE == 0 ? kb * 64 + 4 * qd : m0 + 4 * qd;
+                const int64_t e0 = L.off_w + (int64_t)n0 * L.K + k0;
+                const float* mup = L.mu + e0;
+                const float* sgp = L.sigma + e0;
+                const int64_t estep = (int64_t)rstep * L.K;
+#pragma unroll 4
+                for (int it = 0; it < 8; ++it) {
+                    const uint2 w = gen_w4_fast(mup + it * estep, sgp + it * estep, a.kk.key,
+                                                a.kk.step, w3, (uint32_t)(n0 + it * rstep),
+                                                (uint32_t)(k0 >> 2));
+                    sts64(tileA + it * sstep, w);
                 }
-                const uint2 w = gen_w4(L, a.kk, sg, n, k, vec);
-                asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(smem_u32(tileA + off)),
-                             "r"(w.x), "r"(w.y)
-                             : "memory");
+            } else {
+#pragma unroll 1
+                for (int it = 0; it < 8; ++it) {
+                    const int n = MODE == 0 ? m0 + rsub + it * rstep : kb * 64 + rsub + it * rstep;
+                    const int k = MODE == 0 ? kb * 64 + 4 * qd : m0 + 4 * qd;
+                    sts64(tileA + it * sstep, gen_w4(L, a.kk, sg, n, k, vec));
+                }
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full_gen[st]);
         }
         // ------------------------------------------------ epilogue
-        mbar_wait(tfull, 0);
+        mbar_wait_sleep(tfull, 0);
         tc_fence_after();
         const int q = warp & 3, h = warp >> 2;
         const int row = 32 * q + lane, m = m0 + row;
-        const int nchunks = (a.nb + 31) / 32;
-        const float bias = a.mode == 0 ? sbias[row] : 0.0f;
+        const int nchunks = (a.nb + 15) / 16;
+        const float bias = MODE == 0 ? sbias[row] : 0.0f;
         for (int c = h; c < nchunks; c += 2) {
-            float v[32];
+            const int bc0 = b0 + c * 16;
+            const int nvalid = min(16, a.B - bc0);
+            const bool live = m < a.M && nvalid > 0;
+            uint16_t mraw[16];
+            if (MODE == 1 && live) {
+                const uint16_t* mk = reinterpret_cast<const uint16_t*>(a.mask) + s * a.mask_stride_s +
+                                     (int64_t)bc0 * a.ldm + m;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) mraw[j] = j < nvalid ? __ldg(mk + (int64_t)j * a.ldm) : 0;
+            }
+            float v[16];
             __syncwarp();
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + c * 32, v);
-            if (m >= a.M) continue;
-            const int bc0 = b0 + c * 32;
-            if (bc0 >= a.B) continue;
-            const int nvalid = min(32, a.B - bc0);
-            if (a.mode == 0) {
+            tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + c * 16, v);
+            if (!live) continue;
+            if (MODE == 0) {
                 if (a.out_f32) {
                     float* o = reinterpret_cast<float*>(a.out) + s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
-#pragma unroll 4
-                    for (int j = 0; j < nvalid; ++j) o[(int64_t)j * a.ldo] = v[j] + bias;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < nvalid) o[(int64_t)j * a.ldo] = v[j] + bias;
                 } else {
                     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + s * a.out_stride_s +
                                        (int64_t)bc0 * a.ldo + m;
-#pragma unroll 4
-                    for (int j = 0; j < nvalid; ++j) {
-                        float z = v[j] + bias;
-                        if (a.relu) z = fmaxf(z, 0.0f);
-                        o[(int64_t)j * a.ldo] = __float2bfloat16_rn(z);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        if (j < nvalid) {
+                            float z = v[j] + bias;
+                            if (a.relu) z = fmaxf(z, 0.0f);
+                            o[(int64_t)j * a.ldo] = __float2bfloat16_rn(z);
+                        }
                     }
                 }
             } else {
-                const __nv_bfloat16* mk = a.mask + s * a.mask_stride_s + (int64_t)bc0 * a.ldm + m;
                 __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + s * a.out_stride_s +
                                    (int64_t)bc0 * a.ldo + m;
                 float part = 0.0f;
-#pragma unroll 4
-                for (int j = 0; j < nvalid; ++j) {
-                    const float g = __bfloat162float(mk[(int64_t)j * a.ldm]) > 0.0f ? v[j] : 0.0f;
-                    part += g;
-                    o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if (j < nvalid) {
+                        // ReLU mask of the layer input: bf16 > 0 ⟺ sign bit clear and ≠ 0
+                        const float g = (mraw[j] != 0 && (mraw[j] & 0x8000u) == 0) ? v[j] : 0.0f;
+                        part += g;
+                        o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
+                    }
                 }
-                // fp32 partial column sum over this 32-row chunk: the bias gradient source
-                a.dbpart[s * a.dbpart_stride_s + (int64_t)(bc0 >> 5) * a.M + m] = part;
+                // fp32 partial column sum over this 16-row chunk: the bias gradient source
+                a.dbpart[s * a.dbpart_stride_s + (int64_t)(bc0 >> 4) * a.M + m] = part;
             }
         }
     }
@@ -239,12 +293,17 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gen_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gen_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             gen::kSmem);
+        cudaFuncSetAttribute(gen_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              gen::kSmem);
         attr = true;
     }
     dim3 grid((a.M + 127) / 128, S, (a.B + 255) / 256);
-    gen_gemm_kernel<<<grid, gen::kThreads, gen::kSmem, st>>>(tmB, a);
+    if (a.mode == 0)
+        gen_gemm_kernel<0><<<grid, gen::kThreads, gen::kSmem, st>>>(tmB, a);
+    else
+        gen_gemm_kernel<1><<<grid, gen::kThreads, gen::kSmem, st>>>(tmB, a);
 }
 
 // ============================================================================ K5
@@ -297,7 +356,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
         }
         mbar_fence_init();
     }
-    if (warp == kEpiWarps + 1) tmem_alloc(tslot, 128);
+    if (warp == kEpiWarps + 1) tmem_alloc(tslot, 256);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -313,7 +372,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
                 for (int bb = 0; bb < nbb; ++bb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait(&empty[st], ph ^ 1);
+                    mbar_wait_sleep(&empty[st], ph ^ 1);
                     mbar_arrive_expect_tx(&full[st], kAStage + kBStage);
                     uint8_t* a_st = sA + st * kAStage;
                     tma_load_3d(mapG, &full[st], a_st, n0, 64 * bb, s);
@@ -330,12 +389,12 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
             int it = 0;
             for (int s = 0; s < S; ++s) {
                 const int buf = s & 1;
-                mbar_wait(&tempty[buf], ((s >> 1) & 1) ^ 1);
+                mbar_wait_sleep(&tempty[buf], ((s >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int bb = 0; bb < nbb; ++bb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait(&full[st], ph);
+                    mbar_wait_sleep(&full[st], ph);
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
                     const uint32_t bBase = smem_u32(sB + st * kBStage);
@@ -343,7 +402,10 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t ad = sdesc_sw128(aBase + 2048 * q, 8192, 1024);
                         const uint64_t bd = sdesc_sw128(bBase + 2048 * q, 8192, 1024);
+                        // per-sample dW_s (double-buffered) for the ε-weighted acc_ρ ...
                         mma_bf16(tmem + buf * 64, ad, bd, idesc, (bb | q) != 0 ? 1u : 0u);
+                        // ... and acc_μ = Σ_s dW_s accumulated by the tensor core itself
+                        mma_bf16(tmem + 128, ad, bd, idesc, (s | bb | q) != 0 ? 1u : 0u);
                     }
                     mma_commit(&empty[st]);
                 }
@@ -356,9 +418,10 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
         const int q = warp & 3, h = warp >> 2;
         const int n = n0 + 32 * q + lane;
         const int k = k0 + 32 * h;
-        float am[32], ar[32];
+        const bool kfull = k + 32 <= L.K;
+        float ar[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) am[j] = ar[j] = 0.0f;
+        for (int j = 0; j < 32; ++j) ar[j] = 0.0f;
         for (int s = 0; s < S; ++s) {
             const int buf = s & 1;
             mbar_wait(&tfull[buf], (s >> 1) & 1);
@@ -370,29 +433,49 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
             if (n < L.N) {
-                const uint32_t sg = a.kk.s0 + s;
+                const uint32_t sgw = ((L.t_w << 20) | (a.kk.s0 + s));
+                if (kfull) {
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    if (k + 4 * g < L.K) {
-                        const float4 e = eps4(a.kk.key, a.kk.step, sg, L.t_w, (uint32_t)n,
-                                              (uint32_t)((k >> 2) + g));
-                        am[4 * g + 0] += d[4 * g + 0];
-                        am[4 * g + 1] += d[4 * g + 1];
-                        am[4 * g + 2] += d[4 * g + 2];
-                        am[4 * g + 3] += d[4 * g + 3];
-                        ar[4 * g + 0] = fmaf(d[4 * g + 0], e.x, ar[4 * g + 0]);
-                        ar[4 * g + 1] = fmaf(d[4 * g + 1], e.y, ar[4 * g + 1]);
-                        ar[4 * g + 2] = fmaf(d[4 * g + 2], e.z, ar[4 * g + 2]);
-                        ar[4 * g + 3] = fmaf(d[4 * g + 3], e.w, ar[4 * g + 3]);
+                    for (int g = 0; g < 8; ++g) {
+                        const uint4 y = philox10(make_uint4((uint32_t)((k >> 2) + g), (uint32_t)n, sgw,
+                                                            a.kk.step), a.kk.key);
+                        const float R0 = bm_radius(y.x);
+                        const float2 cs0 = bm_sincos(y.y);
+                        const float R1 = bm_radius(y.z);
+                        const float2 cs1 = bm_sincos(y.w);
+                        ar[4 * g + 0] = fmaf(d[4 * g + 0], __fmul_rn(R0, cs0.x), ar[4 * g + 0]);
+                        ar[4 * g + 1] = fmaf(d[4 * g + 1], __fmul_rn(R0, cs0.y), ar[4 * g + 1]);
+                        ar[4 * g + 2] = fmaf(d[4 * g + 2], __fmul_rn(R1, cs1.x), ar[4 * g + 2]);
+                        ar[4 * g + 3] = fmaf(d[4 * g + 3], __fmul_rn(R1, cs1.y), ar[4 * g + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        if (k + 4 * g < L.K) {
+                            const float4 e = eps4(a.kk.key, a.kk.step, a.kk.s0 + s, L.t_w, (uint32_t)n,
+                                                  (uint32_t)((k >> 2) + g));
+                            float dd[4] = {d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]};
+                            float ee[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) ar[4 * g + j] = fmaf(dd[j], ee[j], ar[4 * g + j]);
+                        }
                     }
                 }
             }
+        }
+        // acc_μ from TMEM (complete once the last sample's commit has landed)
+        float am[32];
+        __syncwarp();
+        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 128 + 32 * h, am);
+        if (S == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) am[j] = 0.0f;
         }
         if (n < L.N) {
             const int64_t base = L.off_w + (int64_t)n * L.K + k;
             float* pm = a.acc_mu + base;
             float* pr = a.acc_rho + base;
-            const bool v4 = ((base & 3) == 0) && (k + 32 <= L.K);
+            const bool v4 = ((base & 3) == 0) && kfull;
             if (v4) {
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
@@ -420,7 +503,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
     __syncthreads();
     if (warp == kEpiWarps + 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 128);
+        tmem_dealloc(tmem, 256);
     }
 }
 

@@ -27,7 +27,7 @@ struct TcGenArgs {
     int64_t mask_stride_s;
     int ldm;
     int vec_ok;          // μ/σ rows are 16-byte aligned (float4 loads)
-    float* dbpart;       // dgrad: fp32 column sums per 32-row chunk, [s][B/32][M]
+    float* dbpart;       // dgrad: fp32 column sums per 16-row chunk, [s][B/16][M]
     int64_t dbpart_stride_s;
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);

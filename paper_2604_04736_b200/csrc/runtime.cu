@@ -283,11 +283,11 @@ int alloc_mlp(bnn_ctx* c) {
         return c->set_err(BNN_ERR_CUDA, "out of memory (logits)");
     int maxN = 0;
     for (int l = 0; l < L; ++l) maxN = std::max(maxN, c->widths[l + 1]);
-    if (!c->alloc(&c->db_scratch, (size_t)Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+    if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
     if (c->bf16) {
         if (!c->alloc(&c->dz_f32, (size_t)Sc * B * c->O)) return c->set_err(BNN_ERR_CUDA, "out of memory");
         c->dbpart.assign(L, nullptr);
-        const int nbc = (B + 31) / 32;
+        const int nbc = (B + 15) / 16;
         for (int l = 0; l + 1 < L; ++l)
             if (!c->alloc(&c->dbpart[l], (size_t)Sc * nbc * c->widths[l + 1]))
                 return c->set_err(BNN_ERR_CUDA, "out of memory");
@@ -400,7 +400,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.mask_stride_s = (int64_t)B * c->ld[l];
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
             a.dbpart = c->dbpart[l - 1];
-            a.dbpart_stride_s = (int64_t)((B + 31) / 32) * a.L.K;
+            a.dbpart_stride_s = (int64_t)((B + 15) / 16) * a.L.K;
             c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[l], a, Sc, st); });
         }
         for (int l0 = 0; l0 < L; l0 += kMaxWgradLayers) {
@@ -430,7 +430,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
         for (int l = 0; l < L; ++l) {
             SampledLayer sl = sampled(c, l, mu);
             const bool last = l == L - 1;
-            const int nbc = (B + 31) / 32;
+            const int nbc = (B + 15) / 16;
             const float* parts = last ? c->dz_f32 : c->dbpart[l];
             const int nparts = last ? B : nbc;
             const int ldp = last ? c->O : sl.N;
@@ -780,6 +780,17 @@ int bnn_eps_fill(uint64_t seed, uint32_t step, uint32_t s, uint32_t t, uint32_t 
                  uint32_t c0, uint32_t nc, float* out, void* stream) {
     if (!out) return BNN_ERR_CONFIG;
     launch_eps_fill(seed, step, s, t, r0, nr, c0, nc, out, reinterpret_cast<cudaStream_t>(stream));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_last_error = cudaGetErrorString(e);
+        return BNN_ERR_CUDA;
+    }
+    return BNN_OK;
+}
+
+int bnn_eps_transform_table(int32_t which, float* out, void* stream) {
+    if (!out || which < 0 || which > 2) return BNN_ERR_CONFIG;
+    launch_eps_table(which, out, reinterpret_cast<cudaStream_t>(stream));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         g_last_error = cudaGetErrorString(e);

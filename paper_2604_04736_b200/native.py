@@ -69,6 +69,7 @@ def lib():
     L.bnn_predict.argtypes = [vp, vp, vp, vp, i32, i32, u64, u32, vp, vp]
     L.bnn_eps_fill.argtypes = [u64, u32, u32, u32, u32, u32, u32, u32, vp, vp]
     L.bnn_eps_bench.argtypes = [u64, u64, vp, i32, vp]
+    L.bnn_eps_transform_table.argtypes = [i32, vp, vp]
     L.bnn_profile_enable.argtypes = [vp, i32]
     L.bnn_profile_read.argtypes = [vp, vp, i32, vp, vp, i32, vp]
     L.bnn_launch_count.argtypes = [vp]
@@ -248,6 +249,13 @@ def eps_fill(seed, step, s, t, r0, nr, c0, nc, device=0) -> torch.Tensor:
     out = torch.empty(nr, nc, dtype=torch.float32, device=torch.device("cuda", device))
     _check(lib().bnn_eps_fill(seed, step, s, t, r0, nr, c0, nc, _p(out),
                               torch.cuda.current_stream(device).cuda_stream))
+    return out
+
+
+def eps_transform_table(which: int, device=0) -> torch.Tensor:
+    out = torch.empty(1 << 24, dtype=torch.float32, device=torch.device("cuda", device))
+    _check(lib().bnn_eps_transform_table(which, _p(out),
+                                         torch.cuda.current_stream(device).cuda_stream))
     return out
 
 
