@@ -28,6 +28,7 @@
 
 #include "../../include/bnn.h"
 #include "kernels.cuh"
+#include "kernels_conv.cuh"
 #include "kernels_tc.cuh"
 
 using namespace bnn;
@@ -75,6 +76,17 @@ bool make_map(CUtensorMap* m, const void* base, int inner, int rows, int depth, 
 
 }  // namespace
 
+// ResNet graph (the CNN of C3–C5): every op is a fused conv (+bias, +residual, ReLU) or GAP.
+struct RBuf {
+    int H, W, C;
+    float* val;
+    float* grad;
+};
+struct ROp {
+    int type;  // 0 conv, 1 global average pool
+    int layer, src, dst, res, relu;
+};
+
 struct bnn_ctx {
     bnn_model_desc model{};
     bnn_config cfg{};
@@ -112,6 +124,10 @@ struct bnn_ctx {
     float* g_m2s = nullptr;
     float* g_counts = nullptr;
     float* acc_scratch = nullptr;  // for bnn_elbo_step_host / predict helpers
+    std::vector<RBuf> rbufs;       // ResNet activations / gradients, [S_chunk][B][H][W][C]
+    std::vector<ROp> rops;
+    int rlogits = -1;
+    int64_t in_elems = 0;          // per-example input elements
     // TMA descriptors (BF16)
     std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;
     // bookkeeping
@@ -230,9 +246,28 @@ int build_layers(bnn_ctx* c) {
         }
         for (int i = 1; i < m.n_widths; ++i) add(m.widths[i - 1], m.widths[i], 1, 1, 0);
         c->O = m.widths[m.n_widths - 1];
+    } else if (m.kind == BNN_MODEL_RESNET18) {
+        // CIFAR ResNet-18 without BatchNorm (R12); tensor order: stem, then per block
+        // conv1, conv2, [1×1 projection], then the linear head.
+        if (m.in_h < 4 || m.in_w < 4 || m.in_c < 1 || m.n_classes < 1)
+            return c->set_err(BNN_ERR_CONFIG, "ResNet needs in_h, in_w >= 4, in_c, n_classes >= 1");
+        const int bw = m.base_width > 0 ? m.base_width : 64;
+        add(m.in_c, bw, 3, 1, 1);
+        int width = bw;
+        for (int stage = 0; stage < 4; ++stage) {
+            const int cout = bw << stage;
+            for (int blk = 0; blk < 2; ++blk) {
+                const int stride = (stage > 0 && blk == 0) ? 2 : 1;
+                add(width, cout, 3, stride, 1);
+                add(cout, cout, 3, 1, 1);
+                if (stride != 1 || width != cout) add(width, cout, 1, stride, 0);
+                width = cout;
+            }
+        }
+        add(width, m.n_classes, 1, 1, 0);
+        c->O = m.n_classes;
     } else {
-        return c->set_err(BNN_ERR_CONFIG,
-                          "model kind %d: only BNN_MODEL_MLP is implemented in this build", m.kind);
+        return c->set_err(BNN_ERR_CONFIG, "unknown model kind %d", m.kind);
     }
     c->P = off;
     c->P_pad = round_up(off, 64);
@@ -444,6 +479,160 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
     return BNN_OK;
 }
 
+
+// ------------------------------------------------------------------ ResNet graph (C3–C5)
+int conv_out_dim(int x, int k, int st, int p) { return (x + 2 * p - k) / st + 1; }
+
+int alloc_resnet(bnn_ctx* c) {
+    if (c->bf16)
+        return c->set_err(BNN_ERR_CONFIG,
+                          "RESNET18 runs in BNN_PREC_FP32 in this build (BF16 conv kernels: next round)");
+    const bnn_model_desc& m = c->model;
+    auto buf = [&](int H, int W, int C) {
+        c->rbufs.push_back(RBuf{H, W, C, nullptr, nullptr});
+        return (int)c->rbufs.size() - 1;
+    };
+    auto conv = [&](int src, int li, int res, int relu) {
+        const LayerDesc& L = c->layers[li];
+        const RBuf& S = c->rbufs[src];
+        const int d = buf(conv_out_dim(S.H, L.k, L.stride, L.pad), conv_out_dim(S.W, L.k, L.stride, L.pad),
+                          L.cout);
+        c->rops.push_back(ROp{0, li, src, d, res, relu});
+        return d;
+    };
+    int l = 0;
+    int cur = buf(m.in_h, m.in_w, m.in_c);
+    cur = conv(cur, l++, -1, 1);  // stem
+    int width = c->layers[0].cout;
+    for (int stage = 0; stage < 4; ++stage) {
+        const int cout = c->layers[0].cout << stage;
+        for (int blk = 0; blk < 2; ++blk) {
+            const int stride = (stage > 0 && blk == 0) ? 2 : 1;
+            const bool proj = stride != 1 || width != cout;
+            const int l1 = l++, l2 = l++, lp = proj ? l++ : -1;
+            const int in = cur;
+            const int a = conv(in, l1, -1, 1);
+            const int sc = proj ? conv(in, lp, -1, 0) : in;
+            cur = conv(a, l2, sc, 1);
+            width = cout;
+        }
+    }
+    const int g = buf(1, 1, width);
+    c->rops.push_back(ROp{1, -1, cur, g, -1, 0});
+    c->rlogits = conv(g, l++, -1, 0);
+    const int B = c->B_max, Sc = c->chunk;
+    for (size_t i = 0; i < c->rbufs.size(); ++i) {
+        RBuf& b = c->rbufs[i];
+        const size_t n = (size_t)Sc * B * b.H * b.W * b.C;
+        if (!c->alloc(&b.val, n) || !c->alloc(&b.grad, i == 0 ? 1 : n))
+            return c->set_err(BNN_ERR_CUDA, "out of memory (ResNet activations)");
+    }
+    int maxN = 0;
+    for (auto& L : c->layers) maxN = std::max(maxN, L.cout);
+    if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * maxN) || !c->alloc(&c->lossrow, (size_t)Sc * B))
+        return c->set_err(BNN_ERR_CUDA, "out of memory");
+    return BNN_OK;
+}
+
+ConvShape shape_of(const bnn_ctx* c, const ROp& op, int B) {
+    const LayerDesc& L = c->layers[op.layer];
+    const RBuf& S = c->rbufs[op.src];
+    const RBuf& D = c->rbufs[op.dst];
+    return ConvShape{B, S.H, S.W, S.C, D.H, D.W, D.C, L.k, L.stride, L.pad};
+}
+int64_t per_sample(const RBuf& b, int B) { return (int64_t)B * b.H * b.W * b.C; }
+
+// forward of one chunk; X0/sX0 = (augmented) input and its per-sample stride
+void resnet_forward(bnn_ctx* c, const float* mu, const SampleKeys& kk, int Sc, int B, const float* X0,
+                    int64_t sX0) {
+    cudaStream_t st = c->st;
+    auto val = [&](int i) -> const float* { return i == 0 ? X0 : c->rbufs[i].val; };
+    auto sval = [&](int i) -> int64_t { return i == 0 ? sX0 : per_sample(c->rbufs[i], B); };
+    for (const ROp& op : c->rops) {
+        if (op.type == 1) {
+            const RBuf& S = c->rbufs[op.src];
+            c->launch("gap", [&] { launch_gap_fwd(c->rbufs[op.src].val, Sc * B, S.H * S.W, S.C, c->rbufs[op.dst].val, st); });
+            continue;
+        }
+        SampledLayer sl = sampled(c, op.layer, mu);
+        ConvShape cs = shape_of(c, op, B);
+        const float* R = op.res >= 0 ? val(op.res) : nullptr;
+        const int64_t sR = op.res >= 0 ? sval(op.res) : 0;
+        c->launch("fwd", [&] {
+            launch_conv_fwd_fp32(sl, kk, Sc, cs, val(op.src), sval(op.src), R, sR, c->rbufs[op.dst].val,
+                                 per_sample(c->rbufs[op.dst], B), op.relu != 0, st);
+        });
+    }
+}
+
+int resnet_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, const float* yreg,
+                 int B, int B_glob, int S_glob, int Sc, uint32_t s0, uint64_t seed, uint32_t step,
+                 float* acc_mu, float* acc_rho, float* acc_loss) {
+    cudaStream_t st = c->st;
+    SampleKeys kk{make_key(seed), step, s0};
+    const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
+                                                     : 1.0f / ((float)S_glob * B_glob * c->O);
+    const RBuf& in = c->rbufs[0];
+    const float* X0 = x;
+    int64_t sX0 = 0;
+    if (c->cfg.aug == BNN_AUG_PER_SAMPLE) {
+        c->launch("aug", [&] {
+            launch_augment(x, Sc, B, in.H, in.W, in.C, seed, step, s0, c->gidx * B, c->rbufs[0].val, st);
+        });
+        X0 = c->rbufs[0].val;
+        sX0 = per_sample(in, B);
+    }
+    resnet_forward(c, mu, kk, Sc, B, X0, sX0);
+    RBuf& lg = c->rbufs[c->rlogits];
+    c->launch("loss", [&] {
+        launch_loss_head(lg.val, Sc, B, c->O, c->model.loss, ycls, yreg, lg.grad, c->O, false, c->lossrow,
+                         nullptr, st);
+    });
+    std::vector<char> written(c->rbufs.size(), 0);
+    written[c->rlogits] = 1;
+    auto val = [&](int i) -> const float* { return i == 0 ? X0 : c->rbufs[i].val; };
+    auto sval = [&](int i) -> int64_t { return i == 0 ? sX0 : per_sample(c->rbufs[i], B); };
+    for (int oi = (int)c->rops.size() - 1; oi >= 0; --oi) {
+        const ROp& op = c->rops[oi];
+        RBuf& D = c->rbufs[op.dst];
+        if (op.type == 1) {
+            const RBuf& S = c->rbufs[op.src];
+            c->launch("gap", [&] { launch_gap_bwd(D.grad, Sc * B, S.H * S.W, S.C, c->rbufs[op.src].grad, st); });
+            written[op.src] = 1;
+            continue;
+        }
+        const int64_t nD = Sc * per_sample(D, B);
+        if (op.relu) c->launch("mask", [&] { launch_relu_mask(D.grad, D.val, nD, st); });
+        SampledLayer sl = sampled(c, op.layer, mu);
+        ConvShape cs = shape_of(c, op, B);
+        const int64_t sD = per_sample(D, B);
+        c->launch("wgrad", [&] {
+            launch_conv_wgrad_fp32(sl, kk, Sc, cs, D.grad, sD, val(op.src), sval(op.src), scale, acc_mu, acc_rho, st);
+        });
+        c->launch("bias", [&] {
+            launch_bias_grad(sl, kk, Sc, D.grad, B * D.H * D.W, D.C, sD, scale, c->db_scratch, acc_mu, acc_rho, st);
+        }, 2);
+        if (op.res >= 0) {
+            RBuf& Rb = c->rbufs[op.res];
+            if (written[op.res])
+                c->launch("add", [&] { launch_add(Rb.grad, D.grad, nD, st); });
+            else
+                CUDA_TRY(c, cudaMemcpyAsync(Rb.grad, D.grad, sizeof(float) * nD, cudaMemcpyDeviceToDevice, st));
+            written[op.res] = 1;
+        }
+        if (op.src != 0) {
+            RBuf& Sb = c->rbufs[op.src];
+            const bool acc = written[op.src] != 0;
+            c->launch("dgrad", [&] {
+                launch_conv_dgrad_fp32(sl, kk, Sc, cs, D.grad, sD, Sb.grad, per_sample(Sb, B), acc, st);
+            });
+            written[op.src] = 1;
+        }
+    }
+    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    return BNN_OK;
+}
+
 int check_step_args(bnn_ctx* c, int B_loc, int B_glob, int S_glob) {
     if (B_loc <= 0 || B_loc > c->B_max)
         return c->set_err(BNN_ERR_CONFIG, "0 < B_loc <= max_B_loc (%d) violated: B_loc=%d", c->B_max, B_loc);
@@ -468,7 +657,7 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
     cudaStream_t st = c->st;
     CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(float) * c->acc_total, st));
     c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
-    if (c->bf16) {
+    if (c->bf16 && c->model.kind == BNN_MODEL_MLP) {
         const int K0 = c->widths[0];
         c->launch("cast", [&] { launch_to_bf16(x, B_loc, K0, c->ld[0], c->xb, st); });
     }
@@ -476,8 +665,12 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
     for (int s = 0; s < S_loc; s += c->chunk) {
         const int Sc = std::min(c->chunk, S_loc - s);
         const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
-        rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
-                       acc + c->P_pad, acc + 2 * c->P_pad);
+        if (c->model.kind == BNN_MODEL_MLP)
+            rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
+                           acc + c->P_pad, acc + 2 * c->P_pad);
+        else
+            rc = resnet_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
+                              acc + c->P_pad, acc + 2 * c->P_pad);
         if (rc) return rc;
     }
     CUDA_TRY(c, cudaGetLastError());
@@ -571,6 +764,8 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     if (rc) return fail(rc);
     if (model->kind == BNN_MODEL_MLP && cfg->aug != BNN_AUG_NONE)
         return fail(c->set_err(BNN_ERR_CONFIG, "augmentation applies to image models only"));
+    c->in_elems = model->kind == BNN_MODEL_MLP ? (int64_t)model->widths[0]
+                                              : (int64_t)model->in_h * model->in_w * model->in_c;
     // ---- device
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -586,14 +781,14 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     c->n_part = finalize_partials_count(c->P);
     if (!c->alloc(&c->sigma, c->P) || !c->alloc(&c->acc, c->acc_total) ||
         !c->alloc(&c->kl_part, c->n_part) || !c->alloc(&c->lossbuf, 4) ||
-        !c->alloc(&c->x_stage, (size_t)c->B_max * std::max(1, c->widths.empty() ? 1 : c->widths[0])) ||
+        !c->alloc(&c->x_stage, (size_t)c->B_max * c->in_elems) ||
         !c->alloc(&c->ycls_stage, c->B_max) || !c->alloc(&c->yreg_stage, (size_t)c->B_max * c->O) ||
         !c->alloc(&c->p_mean, (size_t)c->B_max * c->G * c->O) || !c->alloc(&c->p_m2, (size_t)c->B_max * c->G * c->O) ||
         !c->alloc(&c->g_means, (size_t)c->B_max * c->G * c->O * cfg->world) ||
         !c->alloc(&c->g_m2s, (size_t)c->B_max * c->G * c->O * cfg->world) ||
         !c->alloc(&c->g_counts, cfg->world))
         return fail(c->set_err(BNN_ERR_CUDA, "out of device memory"));
-    rc = alloc_mlp(c);
+    rc = model->kind == BNN_MODEL_MLP ? alloc_mlp(c) : alloc_resnet(c);
     if (rc) return fail(rc);
     // ---- communicator
     if (cfg->nccl_uid && cfg->world > 1) {
@@ -701,7 +896,7 @@ int bnn_elbo_step_host(bnn_ctx* c, const float* mu, const float* rho, const floa
                        float* grho) {
     if (!c || !x_host || !loss_host) return BNN_ERR_CONFIG;
     if (B_loc <= 0 || B_loc > c->B_max) return c->set_err(BNN_ERR_CONFIG, "0 < B_loc <= max_B_loc violated");
-    const size_t in = (size_t)c->widths[0];
+    const size_t in = (size_t)c->in_elems;
     CUDA_TRY(c, cudaMemcpyAsync(c->x_stage, x_host, sizeof(float) * in * B_loc, cudaMemcpyHostToDevice, c->st));
     if (ycls_host)
         CUDA_TRY(c, cudaMemcpyAsync(c->ycls_stage, ycls_host, sizeof(int32_t) * B_loc, cudaMemcpyHostToDevice, c->st));
@@ -723,12 +918,15 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
     const int S_loc = S_global / c->K;
     const int BO = B * c->O;
     c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
-    if (c->bf16) c->launch("cast", [&] { launch_to_bf16(x, B, c->widths[0], c->ld[0], c->xb, st); });
+    if (c->bf16 && c->model.kind == BNN_MODEL_MLP)
+        c->launch("cast", [&] { launch_to_bf16(x, B, c->widths[0], c->ld[0], c->xb, st); });
     // per chunk forward; stats over all local samples need all logits, so chunk == S_loc here
     if (S_loc > c->chunk) return c->set_err(BNN_ERR_CONFIG, "predict needs S/K <= sample_chunk");
     SampleKeys kk{make_key(seed), step, (uint32_t)(c->kidx * S_loc)};
+    const bool is_mlp = c->model.kind == BNN_MODEL_MLP;
+    if (!is_mlp) resnet_forward(c, mu, kk, S_loc, B, x, 0);
     const int nb = (int)round_up(std::min(B, 256), 16);
-    for (int l = 0; l < L; ++l) {
+    for (int l = 0; is_mlp && l < L; ++l) {
         if (!c->bf16) {
             SampledLayer sl = sampled(c, l, mu);
             const float* A = l == 0 ? x : (const float*)c->act[l];
@@ -755,7 +953,8 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, S_loc, st); });
         }
     }
-    c->launch("predict", [&] { launch_predict_stats(c->logits, S_loc, B, c->O, c->model.loss, c->p_mean, c->p_m2, st); });
+    const float* logits = is_mlp ? c->logits : c->rbufs[c->rlogits].val;
+    c->launch("predict", [&] { launch_predict_stats(logits, S_loc, B, c->O, c->model.loss, c->p_mean, c->p_m2, st); });
     const int R = c->cfg.world;
     if (c->comm && R > 1) {
         NCCL_TRY(c, ncclGroupStart());

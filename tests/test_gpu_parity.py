@@ -218,3 +218,51 @@ def test_c2_full_size_bf16_gradients():
     ref = O.elbo_step(C2, mu, rho, x, yc, None, cfg["S"], 0x5EED, 0, cfg["D"])
     assert max(_per_tensor_rel(ctx, gmu, ref["grad_mu"])) <= 2e-2
     assert max(_per_tensor_rel(ctx, grho, ref["grad_rho"])) <= 2e-2
+
+
+# ------------------------------------------------------------------ ResNet-18-shaped CNN (FP32 path)
+SMALL_CNN = dict(kind="resnet18", in_h=16, in_w=16, in_c=3, n_classes=10, base_width=8, loss="ce")
+
+
+@pytest.mark.parametrize("aug", ["none", "per_sample"])
+def test_cnn_fp32_matches_oracle(aug):
+    model, B, S, D = SMALL_CNN, 6, 3, 45000.0
+    mu, rho, x, yc, _ = _inputs(model, B, "wide")
+    ref = O.elbo_step(model, mu, rho, x, yc, None, S, 0xBEEF, 5, D,
+                      aug=O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE)
+    ctx, loss, gmu, grho = _run_gpu(model, "fp32", mu, rho, x, yc, None, S, 0xBEEF, 5, D, aug=aug)
+    assert abs(loss - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    assert max(_per_tensor_rel(ctx, gmu, ref["grad_mu"])) <= 1e-4
+    assert max(_per_tensor_rel(ctx, grho, ref["grad_rho"])) <= 1e-4
+
+
+def test_cnn_fp32_hybrid_virtual_ranks_with_augmentation():
+    native = _native()
+    model, B, S, D = SMALL_CNN, 4, 4, 100.0
+    mu, rho, x, yc, _ = _inputs(model, B, "wide")
+    mu_d, rho_d = _dev(mu), _dev(rho)
+    single = native.Context(model, precision="fp32", max_B_loc=B, max_S_loc=S, dataset_size=D,
+                            aug="per_sample")
+    l1, g1, r1 = single.finalize(mu_d, rho_d, single.elbo_partial(mu_d, rho_d, _dev(x), _dev(yc), B, S, 3, 1))
+    total = None
+    for rank in range(4):
+        ctx = native.Context(model, precision="fp32", mode="hybrid", K=2, G=2, rank=rank, world=4,
+                             max_B_loc=B // 2, max_S_loc=S // 2, dataset_size=D, aug="per_sample")
+        g = rank % 2
+        acc = ctx.elbo_partial(mu_d, rho_d, _dev(x[2 * g:2 * g + 2]), _dev(yc[2 * g:2 * g + 2]), B, S, 3, 1)
+        total = acc if total is None else total + acc
+    l2, g2, r2 = single.finalize(mu_d, rho_d, total)
+    torch.cuda.synchronize()
+    assert _rel(g2.cpu().numpy(), g1.cpu().numpy()) < 1e-5
+    assert _rel(r2.cpu().numpy(), r1.cpu().numpy()) < 1e-5
+
+
+def test_cnn_fp32_predict():
+    native = _native()
+    model, B, S = SMALL_CNN, 5, 4
+    mu, rho, x, _, _ = _inputs(model, B, "wide")
+    ctx = native.Context(model, precision="fp32", max_B_loc=B, max_S_loc=S, dataset_size=1.0)
+    mean, var = ctx.predict(_dev(mu), _dev(rho), _dev(x), S, 3, 0)
+    rm, rv = O.predict(model, mu, rho, x, S, 3, 0)
+    assert _rel(mean.cpu().numpy(), rm) < 1e-4
+    assert _rel(var.cpu().numpy(), rv) < 1e-3
