@@ -572,17 +572,30 @@ __global__ void bias_reduce_kernel(SampledLayer L, SampleKeys kk, const float* _
     db[(int64_t)(S + s) * L.N + n] = acc * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n);
 }
 
+// phase B: 32 features × 8 sample groups per block, fixed-order smem combine (deterministic)
 __global__ void bias_acc_kernel(SampledLayer L, int S, const float* __restrict__ db, float scale,
                                 float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= L.N) return;
+    __shared__ float red[2][8][33];
+    const int tx = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + tx;
     float am = 0.0f, ar = 0.0f;
-    for (int s = 0; s < S; ++s) {
-        am += db[(int64_t)s * L.N + n];
-        ar += db[(int64_t)(S + s) * L.N + n];
+    if (n < L.N)
+        for (int s = g; s < S; s += 8) {
+            am += db[(int64_t)s * L.N + n];
+            ar += db[(int64_t)(S + s) * L.N + n];
+        }
+    red[0][g][tx] = am;
+    red[1][g][tx] = ar;
+    __syncthreads();
+    if (g == 0 && n < L.N) {
+        float m = 0.0f, r = 0.0f;
+        for (int i = 0; i < 8; ++i) {
+            m += red[0][i][tx];
+            r += red[1][i][tx];
+        }
+        acc_mu[L.off_b + n] += scale * m;
+        acc_rho[L.off_b + n] += scale * r;
     }
-    acc_mu[L.off_b + n] += scale * am;
-    acc_rho[L.off_b + n] += scale * ar;
 }
 
 void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
@@ -590,7 +603,7 @@ void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const f
                       float* acc_mu, float* acc_rho, cudaStream_t st) {
     dim3 grid((L.N + 127) / 128, S);
     bias_reduce_kernel<<<grid, 128, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
-    bias_acc_kernel<<<(L.N + 127) / 128, 128, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
+    bias_acc_kernel<<<(L.N + 31) / 32, 256, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
 }
 
 }  // namespace bnn
