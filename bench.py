@@ -34,6 +34,37 @@ from paper_2604_04736_b200.configs import CONFIGS, MODELS, n_params  # noqa: E40
 
 METRIC = "ELBO-step sample·images/s"
 
+WORKLOAD_NAMES = {
+    "mlp_784_1024_1024_10": "Bayesian MLP 784-1024-1024-10 (CE)",
+    "mlp_8_16_1": "Bayesian MLP 8-16-1 (MSE)",
+    "resnet18_cifar": "ResNet-18-shaped Bayesian CNN, 32x32x3, per-sample crop+flip",
+}
+
+
+def run_plan(config, world, mode_arg=None):
+    """Samples / batch per rank for a BASELINE config at `world` GPUs."""
+    cfg = CONFIGS[config]
+    if config == "C3":  # weak: S = 8 per GPU, same batch everywhere
+        S_loc, B = cfg["S_per_gpu"], cfg["B"]
+        return dict(S=S_loc * world, S_loc=S_loc, B=B, B_loc=B, K=world, G=1, mode="sample",
+                    scaling="weak")
+    if config == "C4":  # strong: S = 64 fixed; sample-sharded (default) or data-sharded
+        mode = mode_arg or "sample"
+        if mode == "data":
+            return dict(S=cfg["S"], S_loc=cfg["S"], B=cfg["B"], B_loc=cfg["B"] // world, K=1,
+                        G=world, mode="data", scaling="strong")
+        return dict(S=cfg["S"], S_loc=cfg["S"] // world, B=cfg["B"], B_loc=cfg["B"], K=world,
+                    G=1, mode="sample", scaling="strong")
+    if config == "C5":  # hybrid 4 sample groups x 2 data groups (world 8); K = world/2 below 8
+        G = 2 if world >= 2 else 1
+        K = max(1, world // G)
+        return dict(S=cfg["S"], S_loc=cfg["S"] // K, B=cfg["B"], B_loc=cfg["B"] // G, K=K, G=G,
+                    mode="hybrid" if world > 1 else "sample", scaling="strong")
+    # C1 / C2: weak scaling, S = S_config per GPU
+    S_loc, B = cfg["S"], cfg["B"]
+    return dict(S=S_loc * world, S_loc=S_loc, B=B, B_loc=B, K=world, G=1, mode="sample",
+                scaling="weak")
+
 
 def _env_world():
     return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), \
@@ -98,7 +129,7 @@ class ClockSampler:
 
 
 # ====================================================================== reference arm
-def cpu_oracle_rate(model, B, D, budget_s=15.0, seed=0x5EED):
+def cpu_oracle_rate(model, B, D, budget_s=15.0, seed=0x5EED, aug="none"):
     """Time the fp64 oracle (as it stands) on the host cores over a bounded sample of the
     workload: all B examples, S_sample samples; returns (sample·images/s, cores, sample)."""
     import oracle as O
@@ -106,14 +137,24 @@ def cpu_oracle_rate(model, B, D, budget_s=15.0, seed=0x5EED):
     x, yc, yr = synth.make_batch(model, B, seed=1)
     cores = os.cpu_count() or 1
     O.lib()
+    a = O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE
+    # probe with a few images, then size the slice to ≈ budget_s of CPU work
+    Bp = min(B, 8)
     t0 = time.perf_counter()
-    O.elbo_partial(model, mu, rho, x, yc, yr, B, 0, 64, 0, 1, seed, 0)
-    t1 = time.perf_counter() - t0
-    S_sample = max(1, min(64, int(budget_s / max(t1, 1e-3))))
+    O.elbo_partial(model, mu, rho, x[:Bp], None if yc is None else yc[:Bp],
+                   None if yr is None else yr[:Bp], B, 0, 64, 0, 1, seed, 0, a)
+    t1 = (time.perf_counter() - t0) / Bp
+    n_img = max(1, int(budget_s / max(t1, 1e-6)))
+    if n_img >= B:
+        S_sample, B_s = max(1, min(64, n_img // B)), B
+    else:
+        S_sample, B_s = 1, n_img
     t0 = time.perf_counter()
-    O.elbo_partial(model, mu, rho, x, yc, yr, B, 0, 64, 0, S_sample, seed, 0)
+    O.elbo_partial(model, mu, rho, x[:B_s], None if yc is None else yc[:B_s],
+                   None if yr is None else yr[:B_s], B, 0, 64, 0, S_sample, seed, 0, a)
     dt = time.perf_counter() - t0
-    return S_sample * B / dt, cores, f"{S_sample} of 64 samples x {B} images (one step's slice), fp64"
+    return S_sample * B_s / dt, cores, (f"{S_sample} sample(s) x {B_s} of {B} images (a slice of "
+                                        f"one step), fp64, {cores} threads")
 
 
 def run_reference(args, world, rank):
@@ -121,19 +162,21 @@ def run_reference(args, world, rank):
         return
     cfg = CONFIGS[args.config]
     model = MODELS[cfg["model"]]
-    B, S = cfg["B"], cfg["S"] * (world if world > 1 else 1)
+    plan = run_plan(args.config, world, args.mode)
+    B, S = plan["B"], plan["S"]
     rates = []
     for i in range(args.warmup + args.steps):
-        r, cores, sample = cpu_oracle_rate(model, B, cfg["D"], budget_s=args.ref_budget)
+        r, cores, sample = cpu_oracle_rate(model, B, cfg["D"], budget_s=args.ref_budget,
+                                           aug=cfg.get("aug", "none"))
         if i >= args.warmup:
             rates.append(r)
     v = statistics.median(rates)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "sample·images/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": S * B / v * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: " + cfg["model"], "global_batch": B,
-                       "samples": S},
+            "scaling": plan["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
+                       "global_batch": B, "samples": S},
             "cpu_baseline": {"value": v, "unit": "sample·images/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "sample·images/s", "h2d_bytes_per_step": 0,
@@ -157,14 +200,18 @@ def run_ours(args, world, rank, local_rank):
         uid = obj[0]
     cfg = CONFIGS[args.config]
     model = MODELS[cfg["model"]]
-    B = cfg["B"]
-    S_loc = cfg["S"]
-    S = S_loc * world  # weak scaling: samples proportional to GPUs
+    plan = run_plan(args.config, world, args.mode)
+    B, B_loc, S, S_loc, K, G = plan["B"], plan["B_loc"], plan["S"], plan["S_loc"], plan["K"], plan["G"]
     D = cfg["D"]
     P = n_params(model)
+    g_idx = rank % G
 
     mu_h, rho_h = synth.init_params(model, seed=2)
     x_h, yc_h, yr_h = synth.make_batch(model, B, seed=1)
+    # this rank's data-group shard of the global batch
+    x_h = x_h[g_idx * B_loc:(g_idx + 1) * B_loc]
+    yc_h = None if yc_h is None else yc_h[g_idx * B_loc:(g_idx + 1) * B_loc]
+    yr_h = None if yr_h is None else yr_h[g_idx * B_loc:(g_idx + 1) * B_loc]
     mu = torch.from_numpy(mu_h).to(dev)
     rho = torch.from_numpy(rho_h).to(dev)
     x = torch.from_numpy(x_h).to(dev)
@@ -173,9 +220,9 @@ def run_ours(args, world, rank, local_rank):
     grho = torch.empty_like(rho)
     loss_dev = torch.zeros(1, device=dev)
     stream = torch.cuda.current_stream(dev)
-    ctx = native.Context(model, precision=args.precision, mode="sample", rank=rank, world=world,
-                         uid=uid, max_B_loc=B, max_S_loc=S_loc, dataset_size=D, device=local_rank,
-                         stream=stream.cuda_stream)
+    ctx = native.Context(model, precision=args.precision, mode=plan["mode"], K=K, G=G, rank=rank,
+                         world=world, uid=uid, max_B_loc=B_loc, max_S_loc=S_loc, dataset_size=D,
+                         device=local_rank, stream=stream.cuda_stream, aug=cfg.get("aug", "none"))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step(i):
@@ -249,9 +296,10 @@ def run_ours(args, world, rank, local_rank):
                         "d2h_bytes_per_step": 4},
                 "gpu_launches": int(launches),
                 "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()}}
-        line["roofline"] = roofline(model, B, S_loc, prof, args.steps, peaks, peak_src)
+        line["roofline"] = roofline(model, B_loc, S_loc, prof, args.steps, peaks, peak_src)
         if world == 1 and not args.no_cpu_baseline:
-            r, cores, sample = cpu_oracle_rate(model, B, D, budget_s=args.ref_budget)
+            r, cores, sample = cpu_oracle_rate(model, B, D, budget_s=args.ref_budget,
+                                               aug=cfg.get("aug", "none"))
             line["cpu_baseline"] = {"value": r, "unit": "sample·images/s", "cores": cores,
                                     "kind": "oracle", "sample": sample}
         print(json.dumps(line), flush=True)
@@ -260,42 +308,76 @@ def run_ours(args, world, rank, local_rank):
         dist.destroy_process_group()
 
 
+def conv_layers(model):
+    """(k, stride, cin, cout, out_h, out_w) of every layer in execution order (the CNN)."""
+    H, W, C = model["in_h"], model["in_w"], model["in_c"]
+    bw = model.get("base_width", 64)
+    out = []
+
+    def conv(h, w, cin, cout, k, st, p):
+        oh, ow = (h + 2 * p - k) // st + 1, (w + 2 * p - k) // st + 1
+        out.append((k, st, cin, cout, oh, ow))
+        return oh, ow
+
+    H, W = conv(H, W, C, bw, 3, 1, 1)
+    width = bw
+    for stage in range(4):
+        cout = bw << stage
+        for blk in range(2):
+            st = 2 if (stage > 0 and blk == 0) else 1
+            h1, w1 = conv(H, W, width, cout, 3, st, 1)
+            conv(h1, w1, cout, cout, 3, 1, 1)
+            if st != 1 or width != cout:
+                conv(H, W, width, cout, 1, st, 0)
+            H, W, width = h1, w1, cout
+    out.append((1, 1, width, model["n_classes"], 1, 1))
+    return out
+
+
 def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
     """Dominant kernel class vs its bound.
 
-    The sampled-GEMM kernels are ALU-bound by ε regeneration; their unit is
-    ε normals generated, and the peak is the issue-slot ceiling derived in DESIGN.md §4:
-    148 SMs × 128 lanes × f_clk / (instructions per normal)."""
-    w = model["widths"]
-    layers = [(w[i + 1], w[i]) for i in range(len(w) - 1)]
-    nrm_fwd = S_loc * sum(n * k + n for n, k in layers)          # fwd generates every W_s and b_s
-    nrm_dgrad = S_loc * sum(n * k for n, k in layers[1:])        # dgrad skips layer 0
-    nrm_wgrad = S_loc * sum(n * k + n for n, k in layers)        # wgrad epilogue (+ bias kernel)
-    flops = {"fwd": 2 * B * S_loc * sum(n * k for n, k in layers),
-             "dgrad": 2 * B * S_loc * sum(n * k for n, k in layers[1:]),
-             "wgrad": 2 * B * S_loc * sum(n * k for n, k in layers)}
-    normals = {"fwd": nrm_fwd, "dgrad": nrm_dgrad, "wgrad": nrm_wgrad}
-    dom = max(prof, key=lambda k: prof[k]["ms"]) if prof else None
+    MLP: the sampled-GEMM kernels are ALU-bound by ε regeneration; unit =
+    ε normals generated, peak = 148 SMs × 128 lanes × f_clk / (instructions per normal).
+    CNN: the conv kernels are tensor-bound; unit = dense bf16 FLOP, peak = measured cuBLAS
+    bf16 (sustained: the kernels are timed inside a multi-ms step)."""
+    dom = max((k for k in prof if k in ("fwd", "dgrad", "wgrad", "wgen")),
+              key=lambda k: prof[k]["ms"], default=None)
     if dom is None:
         return None
     ms = prof[dom]["ms"] / steps
-    instr_per_normal = INSTR_PER_NORMAL
-    clk_mhz = peaks.get("sm_max_mhz", 1965.0)
-    peak = 148 * 128 * clk_mhz * 1e6 / instr_per_normal / 1e9  # Gnormal/s
-    out = {"kernel": dom, "ms_per_step": ms}
-    if dom in normals:
+    if model["kind"] == "mlp":
+        w = model["widths"]
+        layers = [(w[i + 1], w[i]) for i in range(len(w) - 1)]
+        normals = {"fwd": S_loc * sum(n * k + n for n, k in layers),
+                   "dgrad": S_loc * sum(n * k for n, k in layers[1:]),
+                   "wgrad": S_loc * sum(n * k + n for n, k in layers)}
+        flops = {"fwd": 2 * B * S_loc * sum(n * k for n, k in layers),
+                 "dgrad": 2 * B * S_loc * sum(n * k for n, k in layers[1:]),
+                 "wgrad": 2 * B * S_loc * sum(n * k for n, k in layers)}
+        clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * clk_mhz * 1e6 / INSTR_PER_NORMAL / 1e9  # Gnormal/s
         ach = normals[dom] / (ms / 1e3) / 1e9
-        out.update({"bound": "alu", "achieved": ach, "peak": peak, "unit": "Gnormal/s",
-                    "frac": ach / peak, "traffic": _ncu_traffic(dom),
-                    "peak_source": f"derived: 148 SM x 128 lanes x {clk_mhz:.0f} MHz / "
-                                   f"{instr_per_normal} SASS instr per normal (DESIGN.md §4)",
-                    "tensor_tflops": flops[dom] / (ms / 1e3) / 1e12,
-                    "tensor_frac_of_measured": flops[dom] / (ms / 1e3) / 1e12
-                    / peaks.get("bf16_tflops", 1590.0)})
-    else:
-        out.update({"bound": "hbm", "achieved": None, "peak": peaks.get("hbm_gbs"),
-                    "unit": "GB/s", "frac": None, "traffic": None})
-    return out
+        return {"kernel": dom, "ms_per_step": ms, "bound": "alu", "achieved": ach, "peak": peak,
+                "unit": "Gnormal/s", "frac": ach / peak, "traffic": _ncu_traffic(dom),
+                "peak_source": f"derived: 148 SM x 128 lanes x {clk_mhz:.0f} MHz / "
+                               f"{INSTR_PER_NORMAL} SASS instr per normal (DESIGN.md §4)",
+                "tensor_tflops": flops[dom] / (ms / 1e3) / 1e12,
+                "tensor_frac_of_measured": flops[dom] / (ms / 1e3) / 1e12
+                / peaks.get("bf16_tflops", 1590.0)}
+    convs = conv_layers(model)
+    f_all = sum(2 * B * oh * ow * co * k * k * ci for k, st, ci, co, oh, ow in convs)
+    f_nostem = f_all - 2 * B * convs[0][4] * convs[0][5] * convs[0][3] * 9 * convs[0][2]
+    flops = {"fwd": S_loc * f_all, "dgrad": S_loc * f_nostem, "wgrad": S_loc * f_all}
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    if dom not in flops:
+        return {"kernel": dom, "ms_per_step": ms, "bound": "alu", "achieved": None, "peak": None,
+                "unit": None, "frac": None, "traffic": None}
+    ach = flops[dom] / (ms / 1e3) / 1e12
+    return {"kernel": dom, "ms_per_step": ms, "bound": "tensor", "achieved": ach, "peak": peak,
+            "unit": "TFLOP/s", "frac": ach / peak, "traffic": _ncu_traffic(dom),
+            "peak_source": f"measured bf16 sustained ({peak_src}, MEASURED_PEAKS.json); "
+                           f"burst {peaks.get('bf16_tflops')}"}
 
 
 # SASS instructions issued per ε normal by the fused generator (eps4 + W build), from
@@ -319,14 +401,18 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C2"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--mode", default=None, choices=["sample", "data"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=None,
+                    help="seconds of oracle CPU work per reference step (default: 150 s / (K+W))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world, rank, local_rank = _env_world()
     if args.gpus != world and world != 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if args.ref_budget is None:
+        args.ref_budget = min(15.0, max(1.0, 150.0 / (args.steps + args.warmup)))
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

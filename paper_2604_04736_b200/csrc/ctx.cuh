@@ -1,0 +1,256 @@
+// ctx.cuh — private: the bnn_ctx state shared by the runtime translation units.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/bnn.h"
+#include "kernels.cuh"
+#include "kernels_conv.cuh"
+#include "kernels_tc.cuh"
+
+using namespace bnn;
+
+namespace bnn_rt {
+extern thread_local std::string g_last_error;
+
+struct LayerDesc {
+    int cin, cout, k, stride, pad;
+    int64_t off_w, off_b;
+    uint32_t t_w, t_b;
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 3-D bf16 view [depth][rows][inner] with row pitch ld elements, box (64, box_rows, 1),
+// 128-byte swizzle, zero fill out of bounds.
+inline bool make_map(CUtensorMap* m, const void* base, int inner, int rows, int depth, int ld,
+              int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)depth};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * rows};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// generic bf16 tensor map: rank ≤ 5, dims[0] contiguous, strides in bytes for dims 1..rank-1
+inline bool make_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                        const uint64_t* strides, const uint32_t* box) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i > 0) st[i - 1] = strides[i - 1];
+    }
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, bx, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace bnn_rt
+using namespace bnn_rt;
+
+// ResNet graph (the CNN of C3–C5): every op is a fused conv (+bias, +residual, ReLU) or GAP.
+struct RBuf {
+    int H, W, C;
+    float* val;
+    float* grad;
+};
+struct ROp {
+    int type;  // 0 conv, 1 global average pool
+    int layer, src, dst, res, relu;
+};
+
+struct bnn_ctx {
+    bnn_model_desc model{};
+    bnn_config cfg{};
+    std::vector<LayerDesc> layers;
+    std::vector<int> widths;  // MLP widths
+    int64_t P = 0, P_pad = 0, acc_total = 0;
+    int O = 0;
+    int K = 1, G = 1, kidx = 0, gidx = 0;
+    int S_loc_max = 0, B_max = 0, chunk = 0;
+    bool bf16 = false;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    // workspace
+    float* sigma = nullptr;
+    float* acc = nullptr;
+    double* kl_part = nullptr;
+    int n_part = 0;
+    float* lossbuf = nullptr;  // [0] loss, [1] KL
+    float* lossrow = nullptr;
+    float* logits = nullptr;
+    std::vector<void*> act;    // act[l]: input of layer l (l ≥ 1)
+    std::vector<int> ld;       // padded row pitch of width l
+    std::vector<void*> grad;   // grad[l]: dℓ/dz of layer l output
+    std::vector<float*> dbpart;  // BF16: fp32 32-row column sums of grad[l] (l < L-1)
+    float* dz_f32 = nullptr;     // BF16: fp32 copy of the loss-head seed [S][B][O]
+    float* db_scratch = nullptr; // [S][max N] per-sample bias gradients
+    void* xb = nullptr;        // bf16 copy of the layer-0 input
+    float* x_stage = nullptr;  // device copy of a host batch
+    int32_t* ycls_stage = nullptr;
+    float* yreg_stage = nullptr;
+    float* p_mean = nullptr;
+    float* p_m2 = nullptr;
+    float* g_means = nullptr;
+    float* g_m2s = nullptr;
+    float* g_counts = nullptr;
+    float* acc_scratch = nullptr;  // for bnn_elbo_step_host / predict helpers
+    std::vector<RBuf> rbufs;       // ResNet activations / gradients, [S_chunk][B][H][W][C]
+    std::vector<ROp> rops;
+    int rlogits = -1;
+    int64_t in_elems = 0;          // per-example input elements
+    // BF16 ResNet state (parallel to rbufs / layers)
+    struct RBf {
+        __nv_bfloat16* val = nullptr;
+        __nv_bfloat16* grad = nullptr;
+        float* bpart = nullptr;    // fp32 bias-gradient partials of the buffer's producer
+        int nparts = 0;
+        int C_pad = 0;
+        int64_t bpart_cap = 0;
+    };
+    std::vector<RBf> rbf;
+    __nv_bfloat16* wscr = nullptr;  // W_s scratch of one layer for the sample chunk
+    float* wpart = nullptr;         // conv wgrad split partials
+    std::vector<int> kpad, nsplit;  // per layer
+    std::vector<CUtensorMap> cmap_w, cmap_wT, cmap_g;  // per layer
+    __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
+    // TMA descriptors (BF16)
+    std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;
+    // bookkeeping
+    std::string err;
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_next = 0;
+    std::vector<std::string> prof_names;
+    std::vector<double> prof_ms;
+    std::vector<int64_t> prof_n;
+    std::vector<void*> allocs;
+
+    int set_err(int code, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        g_last_error = buf;
+        return code;
+    }
+    template <class T>
+    bool alloc(T** p, size_t n) {
+        void* q = nullptr;
+        if (cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return false;
+        cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(T));
+        allocs.push_back(q);
+        *p = reinterpret_cast<T*>(q);
+        return true;
+    }
+    int prof_class(const char* name) {
+        for (size_t i = 0; i < prof_names.size(); ++i)
+            if (prof_names[i] == name) return (int)i;
+        prof_names.push_back(name);
+        prof_ms.push_back(0.0);
+        prof_n.push_back(0);
+        return (int)prof_names.size() - 1;
+    }
+    void prof_flush() {
+        if (pending.empty()) return;
+        cudaStreamSynchronize(st);
+        for (auto& p : pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+            prof_ms[p.first] += ms;
+            prof_n[p.first] += 1;
+        }
+        pending.clear();
+        ev_next = 0;
+    }
+    template <class F>
+    void launch(const char* cls, F&& f, int kernels = 1) {
+        int c = -1;
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (prof) {
+            c = prof_class(cls);
+            if (ev_next + 2 > ev_pool.size()) prof_flush();
+            if (ev_next + 2 > ev_pool.size()) {
+                for (int i = 0; i < 256; ++i) {
+                    cudaEvent_t e;
+                    cudaEventCreate(&e);
+                    ev_pool.push_back(e);
+                }
+            }
+            a = ev_pool[ev_next++];
+            b = ev_pool[ev_next++];
+            cudaEventRecord(a, st);
+        }
+        f();
+        launches += kernels;
+        if (prof) {
+            cudaEventRecord(b, st);
+            pending.push_back({c, {a, b}});
+        }
+    }
+};
+
+// ResNet entry points (runtime_resnet.cu)
+int alloc_resnet_bf16(bnn_ctx* c);
+int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
+                      const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
+                      uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss);
+void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B,
+                         uint64_t seed, uint32_t step, uint32_t s0, bool aug);
+SampledLayer sampled(const bnn_ctx* c, int l, const float* mu);
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return (ctx)->set_err(BNN_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));    \
+    } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                  \
+    do {                                                                                     \
+        ncclResult_t r_ = (expr);                                                            \
+        if (r_ != ncclSuccess)                                                               \
+            return (ctx)->set_err(BNN_ERR_COMM, "%s: %s", #expr, ncclGetErrorString(r_));    \
+    } while (0)
+

@@ -31,3 +31,79 @@ void launch_augment(const float* x, int S, int B, int H, int W, int C, uint64_t 
                     uint32_t step, uint32_t s0, int b_off, float* out, cudaStream_t st);
 
 }  // namespace bnn
+
+// ====================================================================== BF16 tcgen05 path
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+namespace bnn {
+
+// W_s of one layer for Sc samples, bf16 [s][CO][K_pad]; column kp = tap·C_pad + ci (zero
+// where ci ≥ C or tap ≥ k·k). The scratch of ONE layer for the current sample chunk: the
+// weight reuse of a convolution (every element feeds B·OH·OW ≥ 2 K pixels) is spread over
+// many CTAs, so W_s is formed once per (sample, layer, pass) into this L2-resident buffer
+// instead of per pixel tile.
+void launch_gen_wscratch(const SampledLayer& L, const SampleKeys& kk, int S, int C, int C_pad,
+                         int taps, int K_pad, __nv_bfloat16* out, cudaStream_t st);
+
+struct ConvTcArgs {
+    SampledLayer L;
+    SampleKeys kk;
+    int B, H, W, C, C_pad;  // conv input (per sample); C_pad = channel pitch of the input buffer
+    int OH, OW, CO;
+    int k, stride, pad;
+    int K_pad;
+    const __nv_bfloat16* src;  // fwd: input [s][B][H][W][C_pad]; dgrad: dY [s][B][OH][OW][CO]
+    int64_t src_stride_s;
+    __nv_bfloat16* out;        // fwd: Y [s][B][OH][OW][CO]; dgrad: dX [s][B][H][W][C]
+    int64_t out_stride_s;
+    const __nv_bfloat16* res;  // fwd: residual added before ReLU (or null)
+    int64_t res_stride_s;
+    const __nv_bfloat16* addsrc;  // dgrad: other contribution to dX added before the mask
+    int64_t addsrc_stride_s;
+    const __nv_bfloat16* mask;    // dgrad: ReLU mask source = conv input activation (or null)
+    int64_t mask_stride_s;
+    int relu;                  // fwd
+    float* bpart;              // dgrad: fp32 bias partials of the producer of the input
+    int64_t bpart_stride_s;    // per sample: (#classes·#pixel tiles·2)·C
+};
+// fwd: D[co][pixel] over K = (kh, kw, ci); A = W scratch (TMA, K-major), B = gathered input
+void launch_conv_tc_fwd(const CUtensorMap& wmap, const ConvTcArgs& a, int S, cudaStream_t st);
+// dgrad: D[ci][input pixel] over K = (tap, co); A = W scratchᵀ per tap (TMA, MN-major),
+// B = gathered dY; stride-2 convs run per input-pixel parity class
+void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const ConvTcArgs& a, int S, cudaStream_t st);
+int conv_dgrad_parts(const ConvTcArgs& a);  // bias partial count per sample
+
+struct ConvWgradArgs {
+    SampledLayer L;
+    SampleKeys kk;
+    int S;
+    int B, H, W, C, C_pad, OH, OW, CO, k, stride, pad;
+    const __nv_bfloat16* X;  // conv input [s][B][H][W][C_pad]
+    int64_t X_stride_s;
+    float scale;
+    float* part;             // [nsplit][2][CO·k·k·C] partial acc (μ then ρ), already scaled
+    int nsplit;
+};
+// wgrad (C % 64 == 0): D[co][tap·C + ci] = Σ_pix dY·X, per sample; acc_ρ partial += D ⊙ ε_s,
+// acc_μ partial = Σ_s D (tensor-core accumulated in TMEM). gmap: 3-D map over dY (CO, pix, s).
+void launch_conv_tc_wgrad(const CUtensorMap& gmap, const ConvWgradArgs& a, cudaStream_t st);
+void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off,
+                               float* acc_mu, float* acc_rho, cudaStream_t st);
+
+// image-path helpers on bf16 NHWC buffers
+void launch_input_bf16(const float* x, int S, int B, int H, int W, int C, int C_pad, int aug,
+                       uint64_t seed, uint32_t step, uint32_t s0, int b_off, __nv_bfloat16* out,
+                       cudaStream_t st);
+void launch_gap_fwd_bf16(const __nv_bfloat16* y, int R, int HW, int C, __nv_bfloat16* out,
+                         cudaStream_t st);
+// gy[r][hw][c] = mask(y > 0)·gpool[r][c]/HW (bf16) and part[r][c] = Σ_hw gy (fp32)
+void launch_gap_bwd_bf16(const __nv_bfloat16* gpool, int ldg, const __nv_bfloat16* y, int R,
+                         int HW, int C, __nv_bfloat16* gy, float* part, cudaStream_t st);
+// stem / generic small wgrad on bf16 operands (SIMT): same math as launch_conv_wgrad_fp32
+void launch_conv_wgrad_simt_bf16(const SampledLayer& L, const SampleKeys& kk, int S,
+                                 const ConvShape& c, int C_pad, const __nv_bfloat16* G,
+                                 int64_t sG, const __nv_bfloat16* X, int64_t sX, float scale,
+                                 float* acc_mu, float* acc_rho, cudaStream_t st);
+
+}  // namespace bnn

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
             const int nvalid = min(16, a.B - bc0);
             const bool live = m < a.M && nvalid > 0;
             uint16_t mraw[16];
-            if (MODE == 1 && live) {
+            if (MODE == 1 && live && a.mask) {
                 const uint16_t* mk = reinterpret_cast<const uint16_t*>(a.mask) + s * a.mask_stride_s +
                                      (int64_t)bc0 * a.ldm + m;
 #pragma unroll
@@ -272,13 +272,14 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                 for (int j = 0; j < 16; ++j) {
                     if (j < nvalid) {
                         // ReLU mask of the layer input: bf16 > 0 ⟺ sign bit clear and ≠ 0
-                        const float g = (mraw[j] != 0 && (mraw[j] & 0x8000u) == 0) ? v[j] : 0.0f;
+                        const float g =
+                            (!a.mask || (mraw[j] != 0 && (mraw[j] & 0x8000u) == 0)) ? v[j] : 0.0f;
                         part += g;
                         o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
                     }
                 }
                 // fp32 partial column sum over this 16-row chunk: the bias gradient source
-                a.dbpart[s * a.dbpart_stride_s + (int64_t)(bc0 >> 4) * a.M + m] = part;
+                if (a.dbpart) a.dbpart[s * a.dbpart_stride_s + (int64_t)(bc0 >> 4) * a.M + m] = part;
             }
         }
     }

@@ -11,216 +11,11 @@
 // change which global samples (EPS-v1 keys) and which examples a rank processes; the
 // global 1/(S·B) pre-scaling makes the flat allreduce sum compose over both axes
 // (reading R8).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <cuda_bf16.h>
-#include <cuda_runtime.h>
-#include <nccl.h>
+#include "ctx.cuh"
 
-#include <algorithm>
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstring>
-#include <map>
-#include <string>
-#include <vector>
-
-#include "../../include/bnn.h"
-#include "kernels.cuh"
-#include "kernels_conv.cuh"
-#include "kernels_tc.cuh"
-
-using namespace bnn;
-
-namespace {
-
+namespace bnn_rt {
 thread_local std::string g_last_error;
-
-struct LayerDesc {
-    int cin, cout, k, stride, pad;
-    int64_t off_w, off_b;
-    uint32_t t_w, t_b;
-};
-
-int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
 }
-
-// 3-D bf16 view [depth][rows][inner] with row pitch ld elements, box (64, box_rows, 1),
-// 128-byte swizzle, zero fill out of bounds.
-bool make_map(CUtensorMap* m, const void* base, int inner, int rows, int depth, int ld,
-              int box_rows) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)depth};
-    cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * rows};
-    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-}  // namespace
-
-// ResNet graph (the CNN of C3–C5): every op is a fused conv (+bias, +residual, ReLU) or GAP.
-struct RBuf {
-    int H, W, C;
-    float* val;
-    float* grad;
-};
-struct ROp {
-    int type;  // 0 conv, 1 global average pool
-    int layer, src, dst, res, relu;
-};
-
-struct bnn_ctx {
-    bnn_model_desc model{};
-    bnn_config cfg{};
-    std::vector<LayerDesc> layers;
-    std::vector<int> widths;  // MLP widths
-    int64_t P = 0, P_pad = 0, acc_total = 0;
-    int O = 0;
-    int K = 1, G = 1, kidx = 0, gidx = 0;
-    int S_loc_max = 0, B_max = 0, chunk = 0;
-    bool bf16 = false;
-    cudaStream_t st = nullptr;
-    bool own_stream = false;
-    ncclComm_t comm = nullptr;
-    // workspace
-    float* sigma = nullptr;
-    float* acc = nullptr;
-    double* kl_part = nullptr;
-    int n_part = 0;
-    float* lossbuf = nullptr;  // [0] loss, [1] KL
-    float* lossrow = nullptr;
-    float* logits = nullptr;
-    std::vector<void*> act;    // act[l]: input of layer l (l ≥ 1)
-    std::vector<int> ld;       // padded row pitch of width l
-    std::vector<void*> grad;   // grad[l]: dℓ/dz of layer l output
-    std::vector<float*> dbpart;  // BF16: fp32 32-row column sums of grad[l] (l < L-1)
-    float* dz_f32 = nullptr;     // BF16: fp32 copy of the loss-head seed [S][B][O]
-    float* db_scratch = nullptr; // [S][max N] per-sample bias gradients
-    void* xb = nullptr;        // bf16 copy of the layer-0 input
-    float* x_stage = nullptr;  // device copy of a host batch
-    int32_t* ycls_stage = nullptr;
-    float* yreg_stage = nullptr;
-    float* p_mean = nullptr;
-    float* p_m2 = nullptr;
-    float* g_means = nullptr;
-    float* g_m2s = nullptr;
-    float* g_counts = nullptr;
-    float* acc_scratch = nullptr;  // for bnn_elbo_step_host / predict helpers
-    std::vector<RBuf> rbufs;       // ResNet activations / gradients, [S_chunk][B][H][W][C]
-    std::vector<ROp> rops;
-    int rlogits = -1;
-    int64_t in_elems = 0;          // per-example input elements
-    // TMA descriptors (BF16)
-    std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;
-    // bookkeeping
-    std::string err;
-    int64_t launches = 0;
-    bool prof = false;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
-    std::vector<cudaEvent_t> ev_pool;
-    size_t ev_next = 0;
-    std::vector<std::string> prof_names;
-    std::vector<double> prof_ms;
-    std::vector<int64_t> prof_n;
-    std::vector<void*> allocs;
-
-    int set_err(int code, const char* fmt, ...) {
-        char buf[512];
-        va_list ap;
-        va_start(ap, fmt);
-        vsnprintf(buf, sizeof buf, fmt, ap);
-        va_end(ap);
-        err = buf;
-        g_last_error = buf;
-        return code;
-    }
-    template <class T>
-    bool alloc(T** p, size_t n) {
-        void* q = nullptr;
-        if (cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return false;
-        cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(T));
-        allocs.push_back(q);
-        *p = reinterpret_cast<T*>(q);
-        return true;
-    }
-    int prof_class(const char* name) {
-        for (size_t i = 0; i < prof_names.size(); ++i)
-            if (prof_names[i] == name) return (int)i;
-        prof_names.push_back(name);
-        prof_ms.push_back(0.0);
-        prof_n.push_back(0);
-        return (int)prof_names.size() - 1;
-    }
-    void prof_flush() {
-        if (pending.empty()) return;
-        cudaStreamSynchronize(st);
-        for (auto& p : pending) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, p.second.first, p.second.second);
-            prof_ms[p.first] += ms;
-            prof_n[p.first] += 1;
-        }
-        pending.clear();
-        ev_next = 0;
-    }
-    template <class F>
-    void launch(const char* cls, F&& f, int kernels = 1) {
-        int c = -1;
-        cudaEvent_t a = nullptr, b = nullptr;
-        if (prof) {
-            c = prof_class(cls);
-            if (ev_next + 2 > ev_pool.size()) prof_flush();
-            if (ev_next + 2 > ev_pool.size()) {
-                for (int i = 0; i < 256; ++i) {
-                    cudaEvent_t e;
-                    cudaEventCreate(&e);
-                    ev_pool.push_back(e);
-                }
-            }
-            a = ev_pool[ev_next++];
-            b = ev_pool[ev_next++];
-            cudaEventRecord(a, st);
-        }
-        f();
-        launches += kernels;
-        if (prof) {
-            cudaEventRecord(b, st);
-            pending.push_back({c, {a, b}});
-        }
-    }
-};
-
-#define CUDA_TRY(ctx, expr)                                                                  \
-    do {                                                                                     \
-        cudaError_t e_ = (expr);                                                             \
-        if (e_ != cudaSuccess)                                                               \
-            return (ctx)->set_err(BNN_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));    \
-    } while (0)
-
-#define NCCL_TRY(ctx, expr)                                                                  \
-    do {                                                                                     \
-        ncclResult_t r_ = (expr);                                                            \
-        if (r_ != ncclSuccess)                                                               \
-            return (ctx)->set_err(BNN_ERR_COMM, "%s: %s", #expr, ncclGetErrorString(r_));    \
-    } while (0)
 
 namespace {
 
@@ -276,6 +71,7 @@ int build_layers(bnn_ctx* c) {
     return BNN_OK;
 }
 
+}  // namespace
 SampledLayer sampled(const bnn_ctx* c, int l, const float* mu) {
     const LayerDesc& L = c->layers[l];
     SampledLayer s;
@@ -289,6 +85,8 @@ SampledLayer sampled(const bnn_ctx* c, int l, const float* mu) {
     s.t_b = L.t_b;
     return s;
 }
+
+namespace {
 
 int alloc_mlp(bnn_ctx* c) {
     const int L = (int)c->layers.size();
@@ -484,9 +282,6 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
 int conv_out_dim(int x, int k, int st, int p) { return (x + 2 * p - k) / st + 1; }
 
 int alloc_resnet(bnn_ctx* c) {
-    if (c->bf16)
-        return c->set_err(BNN_ERR_CONFIG,
-                          "RESNET18 runs in BNN_PREC_FP32 in this build (BF16 conv kernels: next round)");
     const bnn_model_desc& m = c->model;
     auto buf = [&](int H, int W, int C) {
         c->rbufs.push_back(RBuf{H, W, C, nullptr, nullptr});
@@ -520,6 +315,7 @@ int alloc_resnet(bnn_ctx* c) {
     const int g = buf(1, 1, width);
     c->rops.push_back(ROp{1, -1, cur, g, -1, 0});
     c->rlogits = conv(g, l++, -1, 0);
+    if (c->bf16) return alloc_resnet_bf16(c);
     const int B = c->B_max, Sc = c->chunk;
     for (size_t i = 0; i < c->rbufs.size(); ++i) {
         RBuf& b = c->rbufs[i];
@@ -668,6 +464,9 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
         if (c->model.kind == BNN_MODEL_MLP)
             rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
                            acc + c->P_pad, acc + 2 * c->P_pad);
+        else if (c->bf16)
+            rc = resnet_bf16_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
+                                   acc + c->P_pad, acc + 2 * c->P_pad);
         else
             rc = resnet_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
                               acc + c->P_pad, acc + 2 * c->P_pad);
@@ -924,7 +723,8 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
     if (S_loc > c->chunk) return c->set_err(BNN_ERR_CONFIG, "predict needs S/K <= sample_chunk");
     SampleKeys kk{make_key(seed), step, (uint32_t)(c->kidx * S_loc)};
     const bool is_mlp = c->model.kind == BNN_MODEL_MLP;
-    if (!is_mlp) resnet_forward(c, mu, kk, S_loc, B, x, 0);
+    if (!is_mlp && !c->bf16) resnet_forward(c, mu, kk, S_loc, B, x, 0);
+    if (!is_mlp && c->bf16) resnet_bf16_forward(c, mu, x, S_loc, B, seed, step, kk.s0, false);
     const int nb = (int)round_up(std::min(B, 256), 16);
     for (int l = 0; is_mlp && l < L; ++l) {
         if (!c->bf16) {
@@ -953,7 +753,7 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, S_loc, st); });
         }
     }
-    const float* logits = is_mlp ? c->logits : c->rbufs[c->rlogits].val;
+    const float* logits = (is_mlp || c->bf16) ? c->logits : c->rbufs[c->rlogits].val;
     c->launch("predict", [&] { launch_predict_stats(logits, S_loc, B, c->O, c->model.loss, c->p_mean, c->p_m2, st); });
     const int R = c->cfg.world;
     if (c->comm && R > 1) {

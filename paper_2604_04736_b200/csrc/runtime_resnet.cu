@@ -1,0 +1,380 @@
+// runtime_resnet.cu — BF16 orchestration of the ResNet-18-shaped Bayesian CNN (C3–C5).
+//
+// Per sample chunk (SURVEY.md §3.3 with the conv kernels of kernels_conv_tc.cu):
+//   input (K9 augmentation, bf16, channels padded to 8)
+//   → for each conv: W_s scratch (one layer, all chunk samples) → tcgen05 implicit-GEMM fwd
+//     with bias / residual / ReLU fused
+//   → GAP → linear head (the MLP generator kernel) → loss head
+//   → head wgrad/dgrad → GAP backward (+ReLU mask, bias partials)
+//   → for each conv in reverse: bias grad from fused partials, tcgen05 wgrad with the
+//     ε-regenerating sample-accumulating epilogue, W_s regenerated → tcgen05 dgrad with the
+//     residual contribution, the ReLU mask of the layer input and the producer's bias partials
+//     fused into the epilogue.
+#include "ctx.cuh"
+#include "common.cuh"
+
+namespace {
+
+bool is_fc(const bnn_ctx* c, const ROp& op) { return op.type == 0 && op.dst == c->rlogits; }
+
+// buffer whose gradient is "dL/d(this op's pre-activation output)": the op's own output,
+// except for a 1×1 projection, whose output sc is summed into the block output y
+int grad_src_buffer(const bnn_ctx* c, int dst) {
+    for (const ROp& op : c->rops)
+        if (op.type == 0 && op.res == dst) {
+            bool sc_is_conv_out = false;
+            for (const ROp& p : c->rops)
+                if (p.type == 0 && p.dst == dst) sc_is_conv_out = true;
+            if (sc_is_conv_out) return op.dst;
+        }
+    return dst;
+}
+
+bool is_proj_output(const bnn_ctx* c, int buf) { return grad_src_buffer(c, buf) != buf; }
+
+}  // namespace
+
+int alloc_resnet_bf16(bnn_ctx* c) {
+    const int B = c->B_max, Sc = c->chunk;
+    const int bw = c->layers[0].cout;
+    if (bw % 64 != 0)
+        return c->set_err(BNN_ERR_CONFIG, "BF16 ResNet needs base_width %% 64 == 0 (tcgen05 conv tiles)");
+    if (c->rbufs[0].H % 8 != 0 || c->rbufs[0].W % 8 != 0)
+        return c->set_err(BNN_ERR_CONFIG, "ResNet input H, W must be multiples of 8 (three stride-2 stages)");
+    const int nb = (int)c->rbufs.size();
+    c->rbf.assign(nb, bnn_ctx::RBf{});
+    for (int i = 0; i < nb; ++i) c->rbf[i].C_pad = i == 0 ? (int)round_up(c->rbufs[0].C, 8) : c->rbufs[i].C;
+    const int gbuf = c->rops[c->rops.size() - 2].dst;  // GAP output (pooled features)
+    for (int i = 0; i < nb; ++i) {
+        if (i == c->rlogits) continue;
+        const RBuf& R = c->rbufs[i];
+        bnn_ctx::RBf& b = c->rbf[i];
+        const size_t n = (size_t)Sc * B * R.H * R.W * b.C_pad;
+        if (!c->alloc(&b.val, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (activations)");
+        if (i != 0 && !c->alloc(&b.grad, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (gradients)");
+        if (i != 0 && i != gbuf) {
+            const int64_t npix = (int64_t)B * R.H * R.W;
+            b.bpart_cap = (int64_t)(4 * ((npix + 255) / 256) * 2 + B) * R.C;
+            if (!c->alloc(&b.bpart, (size_t)Sc * b.bpart_cap)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+        }
+    }
+    const int O = c->O;
+    if (!c->alloc(&c->logits, (size_t)Sc * B * O) || !c->alloc(&c->lossrow, (size_t)Sc * B) ||
+        !c->alloc(&c->dz_f32, (size_t)Sc * B * O) || !c->alloc(&c->fcG, (size_t)Sc * B * round_up(O, 8)))
+        return c->set_err(BNN_ERR_CUDA, "out of memory (head)");
+    // per-layer geometry, scratch sizes and TMA descriptors
+    const int L = (int)c->layers.size();
+    c->kpad.assign(L, 0);
+    c->nsplit.assign(L, 1);
+    c->cmap_w.resize(L);
+    c->cmap_wT.resize(L);
+    c->cmap_g.resize(L);
+    size_t wmax = 0, pmax = 0;
+    int maxN = 0;
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op)) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        const int Cp = c->rbf[op.src].C_pad, taps = Ld.k * Ld.k;
+        const int Kp = (int)round_up((int64_t)taps * Cp, 64);
+        c->kpad[op.layer] = Kp;
+        wmax = std::max(wmax, (size_t)Sc * Ld.cout * Kp);
+        maxN = std::max(maxN, Ld.cout);
+        const RBuf& D = c->rbufs[op.dst];
+        const int64_t npix = (int64_t)B * D.H * D.W;
+        if (Ld.cin % 64 == 0) {
+            const int tiles = ((Ld.cout + 127) / 128) * taps * (Ld.cin / 64);
+            const int blocks = (int)((npix + 63) / 64);
+            c->nsplit[op.layer] = std::max(1, std::min(blocks, (2 * bnn::kNumSMs) / tiles));
+            pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
+        }
+    }
+    if (!c->alloc(&c->wscr, wmax) || !c->alloc(&c->wpart, std::max<size_t>(pmax, 1)) ||
+        !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)))
+        return c->set_err(BNN_ERR_CUDA, "out of memory (scratch)");
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op)) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        const int Kp = c->kpad[op.layer], CO = Ld.cout, taps = Ld.k * Ld.k;
+        {
+            const uint64_t dims[3] = {(uint64_t)Kp, (uint64_t)CO, (uint64_t)Sc};
+            const uint64_t str[2] = {(uint64_t)Kp * 2, (uint64_t)CO * Kp * 2};
+            const uint32_t box[3] = {64, 128, 1};
+            if (!make_map_nd(&c->cmap_w[op.layer], c->wscr, 3, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch) failed");
+        }
+        if (Ld.cin % 64 == 0) {
+            const uint64_t dims[4] = {(uint64_t)Ld.cin, (uint64_t)taps, (uint64_t)CO, (uint64_t)Sc};
+            const uint64_t str[3] = {(uint64_t)Ld.cin * 2, (uint64_t)Kp * 2, (uint64_t)CO * Kp * 2};
+            const uint32_t box[4] = {64, 1, 64, 1};
+            if (!make_map_nd(&c->cmap_wT[op.layer], c->wscr, 4, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch transposed) failed");
+            const int gb = grad_src_buffer(c, op.dst);
+            const RBuf& D = c->rbufs[op.dst];
+            const uint64_t npix = (uint64_t)B * D.H * D.W;
+            const uint64_t gd[3] = {(uint64_t)CO, npix, (uint64_t)Sc};
+            const uint64_t gs[2] = {(uint64_t)CO * 2, npix * CO * 2};
+            const uint32_t gbx[3] = {64, 64, 1};
+            if (!make_map_nd(&c->cmap_g[op.layer], c->rbf[gb].grad, 3, gd, gs, gbx))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (dY) failed");
+        }
+    }
+    // head: pooled features [S][B][Cf] → logits, with the MLP kernels' descriptors
+    const int Cf = c->rbufs[gbuf].C, ldO = (int)round_up(O, 8);
+    c->map_fwdB.resize(1);
+    c->map_dgradB.resize(1);
+    c->map_wgG.resize(1);
+    c->map_wgX.resize(1);
+    if (!make_map(&c->map_fwdB[0], c->rbf[gbuf].val, Cf, B, Sc, Cf, 256) ||
+        !make_map(&c->map_wgX[0], c->rbf[gbuf].val, Cf, B, Sc, Cf, 64) ||
+        !make_map(&c->map_dgradB[0], c->fcG, O, B, Sc, ldO, 256) ||
+        !make_map(&c->map_wgG[0], c->fcG, O, B, Sc, ldO, 64))
+        return c->set_err(BNN_ERR_CUDA, "tensor map (head) failed");
+    return BNN_OK;
+}
+
+void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B, uint64_t seed,
+                         uint32_t step, uint32_t s0, bool aug) {
+    cudaStream_t st = c->st;
+    SampleKeys kk{make_key(seed), step, s0};
+    const RBuf& in = c->rbufs[0];
+    const int Cp0 = c->rbf[0].C_pad;
+    c->launch("aug", [&] {
+        launch_input_bf16(x, aug ? Sc : 1, B, in.H, in.W, in.C, Cp0, aug ? 1 : 0, seed, step, s0,
+                          c->gidx * B, c->rbf[0].val, st);
+    });
+    const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * Cp0 : 0;
+    for (const ROp& op : c->rops) {
+        if (op.type == 1) {
+            const RBuf& S = c->rbufs[op.src];
+            c->launch("gap", [&] {
+                launch_gap_fwd_bf16(c->rbf[op.src].val, Sc * B, S.H * S.W, S.C, c->rbf[op.dst].val, st);
+            });
+            continue;
+        }
+        SampledLayer sl = sampled(c, op.layer, mu);
+        if (is_fc(c, op)) {
+            TcGenArgs a{};
+            a.L = sl;
+            a.kk = kk;
+            a.mode = 0;
+            a.B = B;
+            a.b_shared = 0;
+            a.M = sl.N;
+            a.R = sl.K;
+            a.nb = (int)round_up(std::min(B, 256), 16);
+            a.out_f32 = 1;
+            a.relu = 0;
+            a.out = c->logits;
+            a.ldo = c->O;
+            a.out_stride_s = (int64_t)B * c->O;
+            a.vec_ok = (sl.K % 4 == 0 && sl.off_w % 4 == 0) ? 1 : 0;
+            c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[0], a, Sc, st); });
+            continue;
+        }
+        const LayerDesc& Ld = c->layers[op.layer];
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        const int Cp = c->rbf[op.src].C_pad;
+        c->launch("wgen", [&] {
+            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr, st);
+        });
+        ConvTcArgs a{};
+        a.L = sl;
+        a.kk = kk;
+        a.B = B;
+        a.H = Sb.H;
+        a.W = Sb.W;
+        a.C = Sb.C;
+        a.C_pad = Cp;
+        a.OH = Db.H;
+        a.OW = Db.W;
+        a.CO = Db.C;
+        a.k = Ld.k;
+        a.stride = Ld.stride;
+        a.pad = Ld.pad;
+        a.K_pad = c->kpad[op.layer];
+        a.src = c->rbf[op.src].val;
+        a.src_stride_s = op.src == 0 ? in_stride : (int64_t)B * Sb.H * Sb.W * Cp;
+        a.out = c->rbf[op.dst].val;
+        a.out_stride_s = (int64_t)B * Db.H * Db.W * Db.C;
+        if (op.res >= 0) {
+            a.res = c->rbf[op.res].val;
+            a.res_stride_s = a.out_stride_s;
+        }
+        a.relu = op.relu;
+        c->launch("fwd", [&] { launch_conv_tc_fwd(c->cmap_w[op.layer], a, Sc, st); });
+    }
+}
+
+int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
+                      const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
+                      uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+    cudaStream_t st = c->st;
+    SampleKeys kk{make_key(seed), step, s0};
+    const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
+                                                     : 1.0f / ((float)S_glob * B_glob * c->O);
+    const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
+    resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug);
+    const RBuf& in = c->rbufs[0];
+    const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * c->rbf[0].C_pad : 0;
+    const int O = c->O, ldO = (int)round_up(O, 8);
+    c->launch("loss", [&] {
+        launch_loss_head(c->logits, Sc, B, O, c->model.loss, ycls, yreg, c->fcG, ldO, true, c->lossrow,
+                         c->dz_f32, st);
+    });
+    // ---------------- head (linear layer on pooled features)
+    const ROp& fc = c->rops.back();
+    const ROp& gap = c->rops[c->rops.size() - 2];
+    const int gbuf = gap.dst, ylast = gap.src;
+    {
+        SampledLayer sl = sampled(c, fc.layer, mu);
+        TcWgradMaps maps;
+        maps.g[0] = c->map_wgG[0];
+        maps.x[0] = c->map_wgX[0];
+        TcWgradArgs w{};
+        w.kk = kk;
+        w.S = Sc;
+        w.B = B;
+        w.scale = scale;
+        w.acc_mu = acc_mu;
+        w.acc_rho = acc_rho;
+        w.nlayers = 1;
+        w.lay[0].L = sl;
+        w.lay[0].mtiles = (sl.N + 127) / 128;
+        w.lay[0].ktiles = (sl.K + 63) / 64;
+        w.lay[0].tile_base = 0;
+        w.lay[0].b_shared = 0;
+        c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, st); });
+        c->launch("bias", [&] {
+            launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, st);
+        }, 2);
+        TcGenArgs a{};
+        a.L = sl;
+        a.kk = kk;
+        a.mode = 1;
+        a.B = B;
+        a.M = sl.K;
+        a.R = sl.N;
+        a.nb = (int)round_up(std::min(B, 256), 16);
+        a.out = c->rbf[gbuf].grad;
+        a.ldo = sl.K;
+        a.out_stride_s = (int64_t)B * sl.K;
+        a.mask = nullptr;
+        a.dbpart = nullptr;
+        a.vec_ok = (sl.K % 4 == 0 && sl.off_w % 4 == 0) ? 1 : 0;
+        c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[0], a, Sc, st); });
+    }
+    // ---------------- GAP backward (+ ReLU mask of the last block output, bias partials)
+    {
+        const RBuf& Y = c->rbufs[ylast];
+        c->launch("gap", [&] {
+            launch_gap_bwd_bf16(c->rbf[gbuf].grad, Y.C, c->rbf[ylast].val, Sc * B, Y.H * Y.W, Y.C,
+                                c->rbf[ylast].grad, c->rbf[ylast].bpart, st);
+        });
+        c->rbf[ylast].nparts = B;
+    }
+    // ---------------- convolutions in reverse
+    const int nb = (int)c->rbufs.size();
+    std::vector<int> remaining(nb, 0);
+    std::vector<const __nv_bfloat16*> pending(nb, nullptr);
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op)) continue;
+        if (op.src != 0) remaining[op.src]++;
+        if (op.res >= 0 && !is_proj_output(c, op.res)) remaining[op.res]++;
+    }
+    for (int oi = (int)c->rops.size() - 1; oi >= 0; --oi) {
+        const ROp& op = c->rops[oi];
+        if (op.type != 0 || is_fc(c, op)) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        SampledLayer sl = sampled(c, op.layer, mu);
+        const int gb = grad_src_buffer(c, op.dst);
+        const RBuf& Db = c->rbufs[op.dst];
+        const RBuf& Sb = c->rbufs[op.src];
+        const bnn_ctx::RBf& G = c->rbf[gb];
+        const int64_t npix_out = (int64_t)B * Db.H * Db.W;
+        // bias gradient from the fused partials of dL/dz
+        c->launch("bias", [&] {
+            launch_bias_grad(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale, c->db_scratch,
+                             acc_mu, acc_rho, st);
+        }, 2);
+        // weight gradient with the sample-accumulating ε epilogue
+        if (Ld.cin % 64 == 0) {
+            ConvWgradArgs w{};
+            w.L = sl;
+            w.kk = kk;
+            w.S = Sc;
+            w.B = B;
+            w.H = Sb.H;
+            w.W = Sb.W;
+            w.C = Sb.C;
+            w.C_pad = c->rbf[op.src].C_pad;
+            w.OH = Db.H;
+            w.OW = Db.W;
+            w.CO = Db.C;
+            w.k = Ld.k;
+            w.stride = Ld.stride;
+            w.pad = Ld.pad;
+            w.X = c->rbf[op.src].val;
+            w.X_stride_s = op.src == 0 ? in_stride : (int64_t)B * Sb.H * Sb.W * Sb.C;
+            w.scale = scale;
+            w.part = c->wpart;
+            w.nsplit = c->nsplit[op.layer];
+            c->launch("wgrad", [&] { launch_conv_tc_wgrad(c->cmap_g[op.layer], w, st); });
+            const int64_t n = (int64_t)Ld.cout * Ld.k * Ld.k * Ld.cin;
+            c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, w.nsplit, n, Ld.off_w, acc_mu, acc_rho, st); });
+        } else {
+            ConvShape cs{B, Sb.H, Sb.W, Sb.C, Db.H, Db.W, Db.C, Ld.k, Ld.stride, Ld.pad};
+            c->launch("wgrad", [&] {
+                launch_conv_wgrad_simt_bf16(sl, kk, Sc, cs, c->rbf[op.src].C_pad, G.grad, npix_out * Db.C,
+                                            c->rbf[op.src].val, op.src == 0 ? in_stride : 0, scale, acc_mu,
+                                            acc_rho, st);
+            });
+        }
+        // identity residual: dL/dy flows unchanged into the block input
+        if (op.res >= 0 && !is_proj_output(c, op.res)) {
+            remaining[op.res]--;
+            pending[op.res] = G.grad;
+        }
+        if (op.src == 0) continue;
+        // data gradient: W_s regenerated, then the transposed implicit GEMM
+        remaining[op.src]--;
+        const bool final = remaining[op.src] == 0;
+        c->launch("wgen", [&] {
+            launch_gen_wscratch(sl, kk, Sc, Ld.cin, c->rbf[op.src].C_pad, Ld.k * Ld.k, c->kpad[op.layer], c->wscr, st);
+        });
+        ConvTcArgs a{};
+        a.L = sl;
+        a.kk = kk;
+        a.B = B;
+        a.H = Sb.H;
+        a.W = Sb.W;
+        a.C = Sb.C;
+        a.C_pad = c->rbf[op.src].C_pad;
+        a.OH = Db.H;
+        a.OW = Db.W;
+        a.CO = Db.C;
+        a.k = Ld.k;
+        a.stride = Ld.stride;
+        a.pad = Ld.pad;
+        a.K_pad = c->kpad[op.layer];
+        a.src = G.grad;
+        a.src_stride_s = npix_out * Db.C;
+        a.out = c->rbf[op.src].grad;
+        a.out_stride_s = (int64_t)B * Sb.H * Sb.W * Sb.C;
+        if (final) {
+            a.addsrc = pending[op.src];
+            a.addsrc_stride_s = a.out_stride_s;
+            a.mask = c->rbf[op.src].val;
+            a.mask_stride_s = a.out_stride_s;
+            a.bpart = c->rbf[op.src].bpart;
+            a.bpart_stride_s = (int64_t)conv_dgrad_parts(a) * Sb.C;
+            if (conv_dgrad_parts(a) * Sb.C > c->rbf[op.src].bpart_cap)
+                return c->set_err(BNN_ERR_CONFIG, "bias partial buffer too small");
+            c->rbf[op.src].nparts = conv_dgrad_parts(a);
+        }
+        c->launch("dgrad", [&] { launch_conv_tc_dgrad(c->cmap_wT[op.layer], a, Sc, st); });
+        if (!final) pending[op.src] = c->rbf[op.src].grad;
+    }
+    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    return BNN_OK;
+}
