@@ -193,7 +193,8 @@ def run_ours(args, world, rank, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     uid = None
-    if world > 1:
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
         obj = [native.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -232,7 +233,7 @@ def run_ours(args, world, rank, local_rank):
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -249,12 +250,12 @@ def run_ours(args, world, rank, local_rank):
     prof = ctx.profile_read()
     ctx.profile(False)
     launches = ctx.launch_count() - launches0
-    if world > 1:
+    if distributed:
         dist.barrier()
     times = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(times)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -266,7 +267,7 @@ def run_ours(args, world, rank, local_rank):
     for i in range(2):
         ctx.elbo_step_host(mu, rho, x_pin, y_pin, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho)
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     e_ms = []
     for i in range(args.steps):
@@ -276,7 +277,7 @@ def run_ours(args, world, rank, local_rank):
         ctx.elbo_step_host(mu, rho, x_pin, y_pin, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho)
         e_ms.append((time.perf_counter() - t0) * 1e3)
     te = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = S * B / (float(te.item()) / args.steps / 1e3)
 
@@ -295,6 +296,7 @@ def run_ours(args, world, rank, local_rank):
                         "h2d_bytes_per_step": int(x_pin.numel() * 4 + y_pin.numel() * 4),
                         "d2h_bytes_per_step": 4},
                 "gpu_launches": int(launches),
+                "nccl": bool(uid is not None),
                 "kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()}}
         line["roofline"] = roofline(model, B_loc, S_loc, prof, args.steps, peaks, peak_src)
         if world == 1 and not args.no_cpu_baseline:
@@ -304,7 +306,7 @@ def run_ours(args, world, rank, local_rank):
                                     "kind": "oracle", "sample": sample}
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

@@ -104,6 +104,6 @@ void launch_gap_bwd_bf16(const __nv_bfloat16* gpool, int ldg, const __nv_bfloat1
 void launch_conv_wgrad_simt_bf16(const SampledLayer& L, const SampleKeys& kk, int S,
                                  const ConvShape& c, int C_pad, const __nv_bfloat16* G,
                                  int64_t sG, const __nv_bfloat16* X, int64_t sX, float scale,
-                                 float* acc_mu, float* acc_rho, cudaStream_t st);
+                                 float* part, int nsplit, cudaStream_t st);
 
 }  // namespace bnn

@@ -642,7 +642,7 @@ void launch_gap_bwd_bf16(const __nv_bfloat16* gpool, int ldg, const __nv_bfloat1
 __global__ void __launch_bounds__(256) conv_wgrad_simt_bf16_kernel(
     SampledLayer L, SampleKeys kk, int S, ConvShape c, int C_pad, const __nv_bfloat16* __restrict__ G,
     int64_t sG, const __nv_bfloat16* __restrict__ X, int64_t sX, float scale,
-    float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
+    float* __restrict__ part, int nsplit) {
     __shared__ float Gs[16][68];
     __shared__ float Xs[16][68];
     const int col0 = blockIdx.x * 64, co0 = blockIdx.y * 64;
@@ -651,20 +651,22 @@ __global__ void __launch_bounds__(256) conv_wgrad_simt_bf16_kernel(
     const int gcol = col0 + (tid & 63);
     const int gci = gcol % c.C, gkhw = gcol / c.C, gkh = gkhw / c.k, gkw = gkhw % c.k;
     float am[4][4] = {}, ar[4][4] = {};
+    const int per = (npix + nsplit - 1) / nsplit;
+    const int pbeg = blockIdx.z * per, pend = min(npix, pbeg + per);
     for (int s = 0; s < S; ++s) {
         const __nv_bfloat16* Gg = G + s * sG;
         const __nv_bfloat16* Xg = X + s * sX;
         float d[4][4] = {};
-        for (int p0 = 0; p0 < npix; p0 += 16) {
+        for (int p0 = pbeg; p0 < pend; p0 += 16) {
             const int pr = tid >> 6;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int p = p0 + 4 * pr + j;
                 const int co = co0 + (tid & 63);
                 Gs[4 * pr + j][tid & 63] =
-                    (p < npix && co < c.CO) ? __bfloat162float(Gg[(int64_t)p * c.CO + co]) : 0.0f;
+                    (p < pend && co < c.CO) ? __bfloat162float(Gg[(int64_t)p * c.CO + co]) : 0.0f;
                 float v = 0.0f;
-                if (p < npix && gcol < Kt) {
+                if (p < pend && gcol < Kt) {
                     const int n = p / (c.OH * c.OW), rem = p % (c.OH * c.OW);
                     const int ih = (rem / c.OW) * c.stride + gkh - c.pad;
                     const int iw = (rem % c.OW) * c.stride + gkw - c.pad;
@@ -708,21 +710,22 @@ __global__ void __launch_bounds__(256) conv_wgrad_simt_bf16_kernel(
         for (int j = 0; j < 4; ++j) {
             const int col = col0 + tx * 4 + j;
             if (col >= Kt) continue;
-            const int64_t o = L.off_w + (int64_t)co * Kt + col;
-            acc_mu[o] += scale * am[i][j];
-            acc_rho[o] += scale * ar[i][j];
+            const int64_t n = (int64_t)c.CO * Kt;
+            const int64_t o = (int64_t)blockIdx.z * 2 * n + (int64_t)co * Kt + col;
+            part[o] = scale * am[i][j];
+            part[o + n] = scale * ar[i][j];
         }
     }
 }
 
 void launch_conv_wgrad_simt_bf16(const SampledLayer& L, const SampleKeys& kk, int S,
                                  const ConvShape& c, int C_pad, const __nv_bfloat16* G, int64_t sG,
-                                 const __nv_bfloat16* X, int64_t sX, float scale, float* acc_mu,
-                                 float* acc_rho, cudaStream_t st) {
+                                 const __nv_bfloat16* X, int64_t sX, float scale, float* part,
+                                 int nsplit, cudaStream_t st) {
     const int Kt = c.k * c.k * c.C;
-    dim3 grid((Kt + 63) / 64, (c.CO + 63) / 64);
-    conv_wgrad_simt_bf16_kernel<<<grid, 256, 0, st>>>(L, kk, S, c, C_pad, G, sG, X, sX, scale, acc_mu,
-                                                      acc_rho);
+    dim3 grid((Kt + 63) / 64, (c.CO + 63) / 64, nsplit);
+    conv_wgrad_simt_bf16_kernel<<<grid, 256, 0, st>>>(L, kk, S, c, C_pad, G, sG, X, sX, scale, part,
+                                                      nsplit);
 }
 
 }  // namespace bnn

@@ -590,7 +590,7 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     rc = model->kind == BNN_MODEL_MLP ? alloc_mlp(c) : alloc_resnet(c);
     if (rc) return fail(rc);
     // ---- communicator
-    if (cfg->nccl_uid && cfg->world > 1) {
+    if (cfg->nccl_uid) {  // also for world == 1 (exercises the NCCL path on one GPU)
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_uid, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&c->comm, cfg->world, id, cfg->rank);

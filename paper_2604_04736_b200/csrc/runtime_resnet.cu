@@ -85,8 +85,12 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const int tiles = ((Ld.cout + 127) / 128) * taps * (Ld.cin / 64);
             const int blocks = (int)((npix + 63) / 64);
             c->nsplit[op.layer] = std::max(1, std::min(blocks, (2 * bnn::kNumSMs) / tiles));
-            pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
+        } else {  // SIMT wgrad (the stem): split pixels so ≥ 2 waves of CTAs exist
+            const int tiles = (int)(((int64_t)taps * Ld.cin + 63) / 64) * ((Ld.cout + 63) / 64);
+            c->nsplit[op.layer] = (int)std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256,
+                                                                              (8 * bnn::kNumSMs) / tiles));
         }
+        pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
     }
     if (!c->alloc(&c->wscr, wmax) || !c->alloc(&c->wpart, std::max<size_t>(pmax, 1)) ||
         !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)))
@@ -324,11 +328,14 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, w.nsplit, n, Ld.off_w, acc_mu, acc_rho, st); });
         } else {
             ConvShape cs{B, Sb.H, Sb.W, Sb.C, Db.H, Db.W, Db.C, Ld.k, Ld.stride, Ld.pad};
+            const int nsp = c->nsplit[op.layer];
             c->launch("wgrad", [&] {
                 launch_conv_wgrad_simt_bf16(sl, kk, Sc, cs, c->rbf[op.src].C_pad, G.grad, npix_out * Db.C,
-                                            c->rbf[op.src].val, op.src == 0 ? in_stride : 0, scale, acc_mu,
-                                            acc_rho, st);
+                                            c->rbf[op.src].val, op.src == 0 ? in_stride : 0, scale, c->wpart,
+                                            nsp, st);
             });
+            const int64_t n = (int64_t)Ld.cout * Ld.k * Ld.k * Ld.cin;
+            c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, nsp, n, Ld.off_w, acc_mu, acc_rho, st); });
         }
         // identity residual: dL/dy flows unchanged into the block input
         if (op.res >= 0 && !is_proj_output(c, op.res)) {

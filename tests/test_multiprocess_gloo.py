@@ -1,0 +1,98 @@
+"""The N>1 host path on CPU: world-size-2 (and 4) process groups over gloo.
+
+Each rank computes the oracle's partial ELBO sums for its K×G shard (paper_2604_04736_b200.plan),
+the partials are SUM-allreduced over the process group (the one exchange of Alg. 2,
+PAPER.md:263), and the finalized loss/gradients must equal the single-process oracle —
+the same composition the CUDA path performs with NCCL.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2604_04736_b200 import plan, synth
+
+MODEL = dict(kind="mlp", widths=[6, 9, 4], loss="ce")
+CNN = dict(kind="resnet18", in_h=8, in_w=8, in_c=3, n_classes=10, base_width=2, loss="ce")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, K, G, model, S, B, aug, out):
+    import oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank 0 creates the "communicator id" and broadcasts it (bnn_get_unique_id analogue)
+    obj = [os.urandom(128) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    uid = obj[0]
+    K, G = plan.grid(mode, world, K, G)
+    sh = plan.shard(rank, K, G, S, B)
+    mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
+    x, yc, yr = synth.make_batch(model, B, seed=4)
+    xs = x[sh["b0"]:sh["b1"]]
+    ys = yc[sh["b0"]:sh["b1"]]
+    acc = O.elbo_partial(model, mu, rho, xs, ys, None, B, sh["b0"], S, sh["s0"], sh["s1"], 9, 2,
+                         O.AUG_PER_SAMPLE if aug else O.AUG_NONE, nthreads=1)
+    t = torch.from_numpy(acc)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    r = O.finalize(model, mu, rho, t.numpy(), 500.0)
+    out[rank] = (r["loss"], r["grad_mu"], r["grad_rho"], uid)
+    dist.destroy_process_group()
+
+
+def _run(world, mode, K=None, G=None, model=MODEL, S=8, B=8, aug=False):
+    import oracle as O
+    O.lib()  # build before spawning
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), mode, K, G, model, S, B, aug, out), nprocs=world,
+             join=True)
+    mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
+    x, yc, yr = synth.make_batch(model, B, seed=4)
+    ref = O.elbo_step(model, mu, rho, x, yc, None, S, 9, 2, 500.0,
+                      aug=O.AUG_PER_SAMPLE if aug else O.AUG_NONE, nthreads=1)
+    uids = {out[r][3] for r in range(world)}
+    assert len(uids) == 1  # every rank received rank 0's id
+    for r in range(world):
+        loss, gmu, grho, _ = out[r]
+        assert loss == pytest.approx(ref["loss"], rel=1e-12)
+        np.testing.assert_allclose(gmu, ref["grad_mu"], rtol=1e-10, atol=1e-14)
+        np.testing.assert_allclose(grho, ref["grad_rho"], rtol=1e-10, atol=1e-14)
+
+
+def test_plan_shards_partition_samples_and_examples():
+    for K, G in [(1, 1), (4, 1), (1, 4), (4, 2), (2, 4)]:
+        S, B = 32, 256
+        seen = np.zeros((S, B), int)
+        for r in range(K * G):
+            sh = plan.shard(r, K, G, S, B)
+            seen[sh["s0"]:sh["s1"], sh["b0"]:sh["b1"]] += 1
+        assert np.all(seen == 1)
+    with pytest.raises(ValueError):
+        plan.shard(0, 3, 1, 8, 8)  # S mod K != 0
+    with pytest.raises(ValueError):
+        plan.grid("hybrid", 8, 3, 2)
+
+
+def test_gloo_world2_sample_sharded():
+    _run(2, "sample")
+
+
+def test_gloo_world2_data_sharded():
+    _run(2, "data")
+
+
+def test_gloo_world4_hybrid_with_augmentation():
+    _run(4, "hybrid", K=2, G=2, model=CNN, S=4, B=4, aug=True)
