@@ -17,20 +17,21 @@ namespace {
 
 bool is_fc(const bnn_ctx* c, const ROp& op) { return op.type == 0 && op.dst == c->rlogits; }
 
-// buffer whose gradient is "dL/d(this op's pre-activation output)": the op's own output,
-// except for a 1×1 projection, whose output sc is summed into the block output y
-int grad_src_buffer(const bnn_ctx* c, int dst) {
-    for (const ROp& op : c->rops)
-        if (op.type == 0 && op.res == dst) {
-            bool sc_is_conv_out = false;
-            for (const ROp& p : c->rops)
-                if (p.type == 0 && p.dst == dst) sc_is_conv_out = true;
-            if (sc_is_conv_out) return op.dst;
-        }
-    return dst;
+// a 1×1 projection's output sc is the only conv output without ReLU (besides the head)
+bool is_proj_output(const bnn_ctx* c, int buf) {
+    for (const ROp& p : c->rops)
+        if (p.type == 0 && p.dst == buf && p.relu == 0 && !is_fc(c, p)) return true;
+    return false;
 }
 
-bool is_proj_output(const bnn_ctx* c, int buf) { return grad_src_buffer(c, buf) != buf; }
+// buffer whose gradient is "dL/d(this op's pre-activation output)": the op's own output,
+// except for a projection, whose output sc is summed into the block output y
+int grad_src_buffer(const bnn_ctx* c, int dst) {
+    if (is_proj_output(c, dst))
+        for (const ROp& op : c->rops)
+            if (op.type == 0 && op.res == dst) return op.dst;
+    return dst;
+}
 
 }  // namespace
 
