@@ -53,6 +53,8 @@ def lib():
         _lib.orc_philox_fill.argtypes = [C.c_void_p, C.c_void_p, C.c_long, C.c_void_p]
         _lib.orc_elbo_partial.argtypes = [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int] * 6 + [
             C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_elbo_partial_ex.argtypes = [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int] * 6 + [
+            C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int, C.c_int]
         _lib.orc_finalize.argtypes = [C.c_void_p] * 4 + [C.c_double] + [C.c_void_p] * 4
         _lib.orc_forward.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32,
                                                                          C.c_int, C.c_void_p]
@@ -150,16 +152,17 @@ def tensor_infos(model):
 
 
 def elbo_partial(model, mu, rho, x, y_cls, y_reg, B_glob, b_offset, S_glob, s0, s1, seed, step,
-                 aug=AUG_NONE, nthreads=0, act="relu"):
+                 aug=AUG_NONE, nthreads=0, act="relu", emu=False):
+    """emu=True: the BF16 tensor-core mode's rounding points (reading R14)."""
     m = model_struct(model, act)
     P = lib().orc_n_params(C.byref(m))
     mu, rho, x, yr = _d(mu), _d(rho), _d(x), _d(y_reg)
     yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
     B_loc = x.shape[0]
     acc = np.zeros(2 * P + 1, np.float64)
-    rc = lib().orc_elbo_partial(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), B_loc,
-                                b_offset, B_glob, S_glob, s0, s1, seed, step, aug, _p(acc),
-                                nthreads)
+    rc = lib().orc_elbo_partial_ex(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), B_loc,
+                                   b_offset, B_glob, S_glob, s0, s1, seed, step, aug, _p(acc),
+                                   nthreads, 1 if emu else 0)
     assert rc == 0, rc
     return acc
 
@@ -178,10 +181,10 @@ def finalize(model, mu, rho, acc, D, act="relu"):
 
 
 def elbo_step(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=AUG_NONE, nthreads=0,
-              act="relu"):
+              act="relu", emu=False):
     B = np.asarray(x).shape[0]
     acc = elbo_partial(model, mu, rho, x, y_cls, y_reg, B, 0, S, 0, S, seed, step, aug, nthreads,
-                       act)
+                       act, emu)
     return finalize(model, mu, rho, acc, D, act)
 
 

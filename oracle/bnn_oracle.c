@@ -206,6 +206,9 @@ typedef struct {
     long n_params;
     int n_out, loss, act;
     int in_h, in_w, in_c;
+    int has_act[MAXBUF];   /* an activation is applied to the buffer (BF16 emulation) */
+    int n_contrib[MAXBUF]; /* backward contributions to the buffer's gradient */
+    int out_buf;
 } ONet;
 
 static int add_buf(ONet* n, int h, int w, int c)
@@ -239,7 +242,15 @@ static int emit_conv(ONet* n, int src, int cout, int k, int stride, int pad, int
     return dst;
 }
 
+static int build_net_(const orc_model* m, ONet* n);
+static void net_flags(ONet* n);
 static int build_net(const orc_model* m, ONet* n)
+{
+    int rc = build_net_(m, n);
+    if (!rc) net_flags(n);
+    return rc;
+}
+static int build_net_(const orc_model* m, ONet* n)
 {
     memset(n, 0, sizeof(*n));
     n->loss = m->loss; n->act = m->act;
@@ -286,6 +297,18 @@ static int build_net(const orc_model* m, ONet* n)
     return -1;
 }
 
+static void net_flags(ONet* n)
+{
+    for (int b = 0; b < MAXBUF; ++b) { n->has_act[b] = 0; n->n_contrib[b] = 0; }
+    for (int i = 0; i < n->n_ops; ++i) {
+        const OOp* o = &n->ops[i];
+        if (o->type == OP_ACT) n->has_act[o->dst] = 1;
+        if (o->type == OP_CONV || o->type == OP_ADD || o->type == OP_GAP)
+            if (o->src != 0) n->n_contrib[o->src]++;
+        if (o->type == OP_CONV || o->type == OP_GAP) n->out_buf = o->dst;
+    }
+}
+
 long orc_n_params(const orc_model* m)
 {
     ONet n;
@@ -328,9 +351,25 @@ static double log_softplus(double r)
     return log(softplus(r));
 }
 
+/* ---- BF16 emulation (reading R14): the rounding points of the BF16 tensor-core
+ * mode, written from that reading (not from the CUDA code): w_s = RN_bf16(fma_f32(σ, ε, μ)),
+ * biases fma_f32; the network input and every stored activation RN_bf16 (logits stay fp32);
+ * gradients RN_bf16 where they are stored between layers, with the bias gradient taken from
+ * the unrounded value; accumulation in (here: double) precision. */
+static double bf16r(double x)
+{
+    float f = (float)x;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u; /* round to nearest even */
+    memcpy(&f, &u, 4);
+    return (double)f;
+}
+
 /* Sampled weights for global sample s: W = μ + σ·ε. eps_out optional. */
 static void sample_weights(const ONet* n, const double* mu, const double* sigma,
-                           uint64_t seed, uint32_t step, uint32_t s, double* W, double* eps_out)
+                           uint64_t seed, uint32_t step, uint32_t s, double* W, double* eps_out,
+                           int emu)
 {
     for (int l = 0; l < n->n_layers; ++l) {
         const OLayer* L = &n->L[l];
@@ -340,13 +379,14 @@ static void sample_weights(const ONet* n, const double* mu, const double* sigma,
                 long i = L->off_w + r * cols + c;
                 double e = (double)orc_eps(seed, step, s, (uint32_t)(2 * l), (uint32_t)r,
                                            (uint32_t)c);
-                W[i] = mu[i] + sigma[i] * e;
+                W[i] = emu ? bf16r(fmaf((float)sigma[i], (float)e, (float)mu[i]))
+                           : mu[i] + sigma[i] * e;
                 if (eps_out) eps_out[i] = e;
             }
         for (int c = 0; c < L->cout; ++c) {
             long i = L->off_b + c;
             double e = (double)orc_eps(seed, step, s, (uint32_t)(2 * l + 1), 0u, (uint32_t)c);
-            W[i] = mu[i] + sigma[i] * e;
+            W[i] = emu ? (double)fmaf((float)sigma[i], (float)e, (float)mu[i]) : mu[i] + sigma[i] * e;
             if (eps_out) eps_out[i] = e;
         }
     }
@@ -378,9 +418,11 @@ static void conv_fwd(const OLayer* L, const double* W, const double* x, int H, i
             }
 }
 
-/* dW += g ⊗ x (per the conv's index map), db += Σ g, gx += convᵀ(g) (gx may be NULL). */
+/* dW += scale·g ⊗ x (per the conv's index map), db += scale·Σ g, gx += convᵀ(g) (gx may be
+ * NULL). With emu the weight and data gradients use RN_bf16(g), the bias the unrounded g. */
 static void conv_bwd(const OLayer* L, const double* W, const double* x, int H, int Wd,
-                     const double* g, int OH, int OW, double* dW, double* gx)
+                     const double* g, int OH, int OW, double* dW, double* gx, double scale,
+                     int emu)
 {
     const double* w = W + L->off_w;
     double* dw = dW + L->off_w;
@@ -390,7 +432,9 @@ static void conv_bwd(const OLayer* L, const double* W, const double* x, int H, i
         for (int ow = 0; ow < OW; ++ow)
             for (int co = 0; co < L->cout; ++co) {
                 double gv = g[((long)oh * OW + ow) * L->cout + co];
-                db[co] += gv;
+                db[co] += scale * gv;
+                if (emu) gv = bf16r(gv);
+                const double sgv = scale * gv;
                 for (int kh = 0; kh < K; ++kh) {
                     int ih = oh * L->stride + kh - L->pad;
                     if (ih < 0 || ih >= H) continue;
@@ -399,7 +443,7 @@ static void conv_bwd(const OLayer* L, const double* W, const double* x, int H, i
                         if (iw < 0 || iw >= Wd) continue;
                         long xo = ((long)ih * Wd + iw) * C;
                         long wo = (((long)co * K + kh) * K + kw) * C;
-                        for (int ci = 0; ci < C; ++ci) dw[wo + ci] += gv * x[xo + ci];
+                        for (int ci = 0; ci < C; ++ci) dw[wo + ci] += sgv * x[xo + ci];
                         if (gx)
                             for (int ci = 0; ci < C; ++ci) gx[xo + ci] += gv * w[wo + ci];
                     }
@@ -430,8 +474,15 @@ static int work_alloc(const ONet* n, OWork* w, int with_grad)
 }
 
 /* Forward one example (buffer 0 must hold the input). Returns the output buffer index. */
-static int forward_one(const ONet* n, const double* W, OWork* w)
+static void round_buf(const ONet* n, OWork* w, int b)
 {
+    long sz = buf_size(n, b);
+    for (long k = 0; k < sz; ++k) w->val[b][k] = bf16r(w->val[b][k]);
+}
+
+static int forward_one(const ONet* n, const double* W, OWork* w, int emu)
+{
+    if (emu) round_buf(n, w, 0);
     int last = 0;
     for (int i = 0; i < n->n_ops; ++i) {
         const OOp* o = &n->ops[i];
@@ -440,10 +491,13 @@ static int forward_one(const ONet* n, const double* W, OWork* w)
                 conv_fwd(&n->L[o->layer], W, w->val[o->src], n->bh[o->src], n->bw[o->src],
                          w->val[o->dst], n->bh[o->dst], n->bw[o->dst]);
                 last = o->dst;
+                /* a stored conv output without activation (projection) is bf16 too */
+                if (emu && !n->has_act[o->dst] && o->dst != n->out_buf) round_buf(n, w, o->dst);
                 break;
             case OP_ACT: {
                 long sz = buf_size(n, o->dst);
                 for (long k = 0; k < sz; ++k) w->val[o->dst][k] = act_f(n->act, w->val[o->dst][k]);
+                if (emu) round_buf(n, w, o->dst);
                 break;
             }
             case OP_ADD: {
@@ -458,6 +512,7 @@ static int forward_one(const ONet* n, const double* W, OWork* w)
                     for (int p = 0; p < HW; ++p) acc += w->val[o->src][(long)p * C + c];
                     w->val[o->dst][c] = acc / HW;
                 }
+                if (emu) round_buf(n, w, o->dst);
                 last = o->dst;
                 break;
             }
@@ -466,17 +521,32 @@ static int forward_one(const ONet* n, const double* W, OWork* w)
     return last;
 }
 
-/* Backward one example; grad of the output buffer must be set; accumulates into dW. */
-static void backward_one(const ONet* n, const double* W, OWork* w, double* dW)
+/* Backward one example; grad of the output buffer must be set; accumulates into dW.
+ * With emu, a gradient contribution that is stored before it is summed (every contribution
+ * to a buffer except the last one in reverse order) is RN_bf16, and GAP's incoming gradient
+ * (the stored head dgrad) is RN_bf16. tmp holds one contribution (≥ the largest buffer). */
+static void backward_one(const ONet* n, const double* W, OWork* w, double* dW, double scale,
+                         int emu, double* tmp)
 {
+    int seen[MAXBUF] = {0};
     for (int i = n->n_ops - 1; i >= 0; --i) {
         const OOp* o = &n->ops[i];
         switch (o->type) {
-            case OP_CONV:
+            case OP_CONV: {
+                if (!emu || o->src == 0) {
+                    conv_bwd(&n->L[o->layer], W, w->val[o->src], n->bh[o->src], n->bw[o->src],
+                             w->grad[o->dst], n->bh[o->dst], n->bw[o->dst], dW,
+                             o->src == 0 ? NULL : w->grad[o->src], scale, emu);
+                    break;
+                }
+                long sz = buf_size(n, o->src);
+                memset(tmp, 0, sizeof(double) * (size_t)sz);
                 conv_bwd(&n->L[o->layer], W, w->val[o->src], n->bh[o->src], n->bw[o->src],
-                         w->grad[o->dst], n->bh[o->dst], n->bw[o->dst], dW,
-                         o->src == 0 ? NULL : w->grad[o->src]);
+                         w->grad[o->dst], n->bh[o->dst], n->bw[o->dst], dW, tmp, scale, emu);
+                int last = ++seen[o->src] == n->n_contrib[o->src];
+                for (long k = 0; k < sz; ++k) w->grad[o->src][k] += last ? tmp[k] : bf16r(tmp[k]);
                 break;
+            }
             case OP_ACT: {
                 long sz = buf_size(n, o->dst);
                 for (long k = 0; k < sz; ++k) w->grad[o->dst][k] *= act_d(n->act, w->val[o->dst][k]);
@@ -485,14 +555,20 @@ static void backward_one(const ONet* n, const double* W, OWork* w, double* dW)
             case OP_ADD: {
                 if (o->src == 0) break;
                 long sz = buf_size(n, o->dst);
-                for (long k = 0; k < sz; ++k) w->grad[o->src][k] += w->grad[o->dst][k];
+                int last = ++seen[o->src] == n->n_contrib[o->src];
+                int rnd = emu && n->has_act[o->src] && !last;
+                for (long k = 0; k < sz; ++k)
+                    w->grad[o->src][k] += rnd ? bf16r(w->grad[o->dst][k]) : w->grad[o->dst][k];
                 break;
             }
             case OP_GAP: {
                 int HW = n->bh[o->src] * n->bw[o->src], C = n->bc[o->src];
+                ++seen[o->src];
                 for (int p = 0; p < HW; ++p)
-                    for (int c = 0; c < C; ++c)
-                        w->grad[o->src][(long)p * C + c] += w->grad[o->dst][c] / HW;
+                    for (int c = 0; c < C; ++c) {
+                        double g = emu ? bf16r(w->grad[o->dst][c]) : w->grad[o->dst][c];
+                        w->grad[o->src][(long)p * C + c] += g / HW;
+                    }
                 break;
             }
         }
@@ -553,10 +629,10 @@ static double loss_one(const ONet* n, const double* z, const int* ycls, const do
  *   acc[2P]       += Σ_s Σ_b ℓ_{s,b} / (S·B_glob · (O if MSE))
  * Sums are in a fixed order for a fixed thread count.
  */
-int orc_elbo_partial(const orc_model* m, const double* mu, const double* rho, const double* x,
-                     const int* ycls, const double* yreg, int B_loc, int b_offset, int B_glob,
-                     int S_glob, int s0, int s1, uint64_t seed, uint32_t step, int aug,
-                     double* acc, int nthreads)
+int orc_elbo_partial_ex(const orc_model* m, const double* mu, const double* rho, const double* x,
+                        const int* ycls, const double* yreg, int B_loc, int b_offset, int B_glob,
+                        int S_glob, int s0, int s1, uint64_t seed, uint32_t step, int aug,
+                        double* acc, int nthreads, int emu)
 {
     ONet net;
     if (build_net(m, &net)) return -1;
@@ -578,10 +654,14 @@ int orc_elbo_partial(const orc_model* m, const double* mu, const double* rho, co
                                              : 1.0 / ((double)S_glob * B_glob * n->n_out);
     OWork* works = (OWork*)calloc((size_t)nthreads, sizeof(OWork));
     if (!works) return -2;
+    long maxbuf = 0;
+    for (int b = 0; b < n->n_bufs; ++b) if (buf_size(n, b) > maxbuf) maxbuf = buf_size(n, b);
+    double* tmps = (double*)malloc(sizeof(double) * (size_t)maxbuf * nthreads);
+    if (!tmps) return -2;
     for (int t = 0; t < nthreads; ++t)
         if (work_alloc(n, &works[t], 1)) return -2;
     for (int s = s0; s < s1; ++s) {
-        sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, E);
+        sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, E, emu);
         memset(dWt, 0, sizeof(double) * (size_t)P * nthreads);
         memset(lt, 0, sizeof(double) * (size_t)nthreads);
         #pragma omp parallel num_threads(nthreads)
@@ -597,11 +677,14 @@ int orc_elbo_partial(const orc_model* m, const double* mu, const double* rho, co
                 for (int k = 0; k < n->n_bufs; ++k)
                     memset(w->grad[k], 0, sizeof(double) * (size_t)buf_size(n, k));
                 load_input(n, x, b, b_offset + b, seed, step, (uint32_t)s, aug, w->val[0]);
-                int out = forward_one(n, W, w);
+                int out = forward_one(n, W, w, emu);
                 double l = loss_one(n, w->val[out], ycls, yreg, b, dz);
                 lt[tid] += l * scale;
-                for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = dz[k] * scale;
-                backward_one(n, W, w, dWt + (size_t)tid * P);
+                /* exact mode: the seed carries the 1/(S·B) scale; emulation: the unscaled seed
+                 * is what the bf16 operand rounds, the scale is applied at accumulation */
+                for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = emu ? dz[k] : dz[k] * scale;
+                backward_one(n, W, w, dWt + (size_t)tid * P, emu ? scale : 1.0, emu,
+                             tmps + (size_t)tid * maxbuf);
             }
         }
         /* fixed-order reduction over threads, then the sample accumulation */
@@ -618,8 +701,18 @@ int orc_elbo_partial(const orc_model* m, const double* mu, const double* rho, co
     }
     for (int t = 0; t < nthreads; ++t) free(works[t].pool);
     free(works);
+    free(tmps);
     free(sigma); free(W); free(E); free(dWt); free(lt);
     return 0;
+}
+
+int orc_elbo_partial(const orc_model* m, const double* mu, const double* rho, const double* x,
+                     const int* ycls, const double* yreg, int B_loc, int b_offset, int B_glob,
+                     int S_glob, int s0, int s1, uint64_t seed, uint32_t step, int aug,
+                     double* acc, int nthreads)
+{
+    return orc_elbo_partial_ex(m, mu, rho, x, ycls, yreg, B_loc, b_offset, B_glob, S_glob, s0, s1,
+                               seed, step, aug, acc, nthreads, 0);
 }
 
 /*
@@ -683,7 +776,7 @@ int orc_forward(const orc_model* m, const double* mu, const double* rho, const d
     for (int t = 0; t < nthreads; ++t)
         if (work_alloc(n, &works[t], 0)) return -2;
     for (int s = s0; s < s1; ++s) {
-        sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL);
+        sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, 0);
         #pragma omp parallel num_threads(nthreads)
         {
             int tid = 0;
@@ -694,7 +787,7 @@ int orc_forward(const orc_model* m, const double* mu, const double* rho, const d
             #pragma omp for schedule(static)
             for (int b = 0; b < B; ++b) {
                 load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w->val[0]);
-                int out = forward_one(n, W, w);
+                int out = forward_one(n, W, w, 0);
                 memcpy(z_out + ((long)(s - s0) * B + b) * n->n_out, w->val[out],
                        sizeof(double) * n->n_out);
             }

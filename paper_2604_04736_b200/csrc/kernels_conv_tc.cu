@@ -209,36 +209,53 @@ __global__ void __launch_bounds__(cv::kThreads, 2)
         const __nv_bfloat16* srcs = a.src + s * a.src_stride_s;
         const uint32_t rowoff = tid * 128;
         const uint32_t sw = tid & 7;
+        const int cpb = a.C_pad >> 6;  // 64-channel blocks per tap (0 for the 8-channel stem input)
         for (int kb = 0; kb < nkb; ++kb) {
             const int st = kb % kStages;
             const uint32_t ph2 = (kb / kStages) & 1;
             mbar_wait(&empty[st], ph2 ^ 1);
             const uint32_t base = smem_u32(sB + st * kBStage) + rowoff;
+            if (MODE == 0 && cpb == 0) {
+                // stem: 8 taps × 8 channels per K block
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const __nv_bfloat16* g = srcs;
-                uint32_t bytes = 0;
-                if (MODE == 0) {
-                    const int kidx = kb * 64 + 8 * j;
-                    const int tap = kidx / a.C_pad, ci = kidx % a.C_pad;
-                    const int kh = tap / a.k, kw = tap % a.k;
+                for (int j = 0; j < 8; ++j) {
+                    const int tap = kb * 8 + j;
+                    const int kh = tap / a.k, kw = tap - (tap / a.k) * a.k;
                     const int iy = py * a.stride + kh - a.pad, ix = px * a.stride + kw - a.pad;
-                    if (pvalid && tap < a.k * a.k && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
-                        g = srcs + (((int64_t)pn * a.H + iy) * a.W + ix) * a.C_pad + ci;
-                        bytes = 16;
-                    }
-                } else {
-                    const int tap = staps[kb / cblocks], co = (kb % cblocks) * 64 + 8 * j;
-                    const int kh = tap / a.k, kw = tap % a.k;
-                    const int oy = (py + a.pad - kh) / a.stride, ox = (px + a.pad - kw) / a.stride;
-                    const bool inr = (py + a.pad - kh) >= 0 && (px + a.pad - kw) >= 0 && oy < a.OH &&
-                                     ox < a.OW;
-                    if (pvalid && inr && co < a.CO) {
-                        g = srcs + (((int64_t)pn * a.OH + oy) * a.OW + ox) * a.CO + co;
-                        bytes = 16;
-                    }
+                    const bool ok = pvalid && tap < a.k * a.k && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                    const __nv_bfloat16* g =
+                        ok ? srcs + (((int64_t)pn * a.H + iy) * a.W + ix) * a.C_pad : srcs;
+                    cp_async16(base + ((j ^ sw) << 4), g, ok ? 16u : 0u);
                 }
-                cp_async16(base + ((j ^ sw) << 4), g, bytes);
+            } else {
+                // one tap and 64 consecutive channels per K block: one address, 8 chunks
+                int kh, kw, c0;
+                if (MODE == 0) {
+                    const int tap = kb / cpb;
+                    c0 = (kb - tap * cpb) * 64;
+                    kh = tap / a.k;
+                    kw = tap - kh * a.k;
+                } else {
+                    const int ti = kb / cblocks;
+                    const int tap = staps[ti];
+                    c0 = (kb - ti * cblocks) * 64;
+                    kh = tap / a.k;
+                    kw = tap - kh * a.k;
+                }
+                bool ok;
+                const __nv_bfloat16* g = srcs;
+                if (MODE == 0) {
+                    const int iy = py * a.stride + kh - a.pad, ix = px * a.stride + kw - a.pad;
+                    ok = pvalid && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                    if (ok) g = srcs + (((int64_t)pn * a.H + iy) * a.W + ix) * a.C_pad + c0;
+                } else {
+                    const int ty = py + a.pad - kh, tx = px + a.pad - kw;
+                    const int oy = ty / a.stride, ox = tx / a.stride;
+                    ok = pvalid && ty >= 0 && tx >= 0 && oy < a.OH && ox < a.OW;
+                    if (ok) g = srcs + (((int64_t)pn * a.OH + oy) * a.OW + ox) * a.CO + c0;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) cp_async16(base + ((j ^ sw) << 4), g + 8 * j, ok ? 16u : 0u);
             }
             cp_async_mbar_arrive(&full[st]);
         }
@@ -267,18 +284,22 @@ __global__ void __launch_bounds__(cv::kThreads, 2)
             for (int j = 0; j < 16; ++j) {
                 const int pp = p0 + c * 16 + j;
                 if (pp >= npix) break;
-                const int n = pp / (PH * PW), rem = pp % (PH * PW);
                 if (MODE == 0) {
                     const int64_t o = (int64_t)pp * a.CO + m;
                     float z = v[j] + bias;
                     if (a.res) z += __bfloat162float(a.res[s * a.res_stride_s + o]);
                     if (a.relu) z = fmaxf(z, 0.0f);
                     outs[o] = __float2bfloat16_rn(z);
-                    (void)n;
-                    (void)rem;
                 } else {
-                    const int iy = (rem / PW) * a.stride + ph, ix = (rem % PW) * a.stride + pw;
-                    const int64_t o = (((int64_t)n * a.H + iy) * a.W + ix) * a.C + m;
+                    int64_t o;
+                    if (a.stride == 1) {
+                        o = (int64_t)pp * a.C + m;  // class index == input pixel index
+                    } else {
+                        const int n = pp / (PH * PW), rem = pp - n * (PH * PW);
+                        const int r = rem / PW;
+                        const int iy = r * a.stride + ph, ix = (rem - r * PW) * a.stride + pw;
+                        o = (((int64_t)n * a.H + iy) * a.W + ix) * a.C + m;
+                    }
                     float g = v[j];
                     if (a.addsrc) g += __bfloat162float(a.addsrc[s * a.addsrc_stride_s + o]);
                     if (a.mask && !(__bfloat162float(a.mask[s * a.mask_stride_s + o]) > 0.0f)) g = 0.0f;

@@ -125,6 +125,12 @@ def test_elbo_step_matches_oracle(name, model, B, S, rho_mode, precision, tol):
     rr = _per_tensor_rel(ctx, grho, ref["grad_rho"])
     assert max(rm) <= tol, rm
     assert max(rr) <= tol, rr
+    if precision == "bf16":
+        # the BF16 kernels against the oracle with the same rounding points (reading R14)
+        emu = O.elbo_step(model, mu, rho, x, yc, yr, S, 0xC0FFEE, 3, D, emu=True)
+        assert abs(loss - emu["loss"]) <= 1e-4 * abs(emu["loss"])
+        assert max(_per_tensor_rel(ctx, gmu, emu["grad_mu"])) <= 2e-3
+        assert max(_per_tensor_rel(ctx, grho, emu["grad_rho"])) <= 2e-3
 
 
 def test_sigma_to_zero_limit_gpu():
@@ -272,27 +278,20 @@ def test_cnn_fp32_predict():
 BF16_CNN = dict(kind="resnet18", in_h=16, in_w=16, in_c=3, n_classes=10, base_width=64, loss="ce")
 
 
-@pytest.mark.parametrize("aug", ["none", "per_sample"])
-def test_cnn_bf16_matches_oracle(aug):
-    model, B, S, D = BF16_CNN, 4, 2, 45000.0
+@pytest.mark.parametrize("aug,hw,B", [("none", 16, 4), ("per_sample", 16, 4), ("per_sample", 8, 5)])
+def test_cnn_bf16_matches_emulating_oracle(aug, hw, B):
+    """The tcgen05 conv path against the oracle with R14's bf16 rounding points (tight), and
+    against the exact fp64 oracle (loose: bf16 rounding through 20 layers)."""
+    model, S, D = dict(BF16_CNN, in_h=hw, in_w=hw), 2, 45000.0
     mu, rho, x, yc, _ = _inputs(model, B, "init")
-    ref = O.elbo_step(model, mu, rho, x, yc, None, S, 0xBEEF, 5, D,
-                      aug=O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE)
+    a = O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE
+    emu = O.elbo_step(model, mu, rho, x, yc, None, S, 0xBEEF, 5, D, aug=a, emu=True)
     ctx, loss, gmu, grho = _run_gpu(model, "bf16", mu, rho, x, yc, None, S, 0xBEEF, 5, D, aug=aug)
+    assert abs(loss - emu["loss"]) <= 1e-3 * abs(emu["loss"])
+    rm = _per_tensor_rel(ctx, gmu, emu["grad_mu"])
+    rr = _per_tensor_rel(ctx, grho, emu["grad_rho"])
+    assert max(rm) <= 1e-2, rm
+    assert max(rr) <= 1e-2, rr
+    ref = O.elbo_step(model, mu, rho, x, yc, None, S, 0xBEEF, 5, D, aug=a)
     assert abs(loss - ref["loss"]) <= 2e-2 * abs(ref["loss"])
-    rm = _per_tensor_rel(ctx, gmu, ref["grad_mu"])
-    rr = _per_tensor_rel(ctx, grho, ref["grad_rho"])
-    assert max(rm) <= 2e-2, rm
-    assert max(rr) <= 2e-2, rr
-
-
-def test_cnn_bf16_matches_fp32_path_at_8x8():
-    """Same step through the tcgen05 conv path and the FP32 SIMT path (ragged pixel tiles)."""
-    model = dict(BF16_CNN, in_h=8, in_w=8)
-    B, S, D = 5, 3, 100.0
-    mu, rho, x, yc, _ = _inputs(model, B, "init")
-    _, l32, g32, r32 = _run_gpu(model, "fp32", mu, rho, x, yc, None, S, 7, 1, D, aug="per_sample")
-    ctx, l16, g16, r16 = _run_gpu(model, "bf16", mu, rho, x, yc, None, S, 7, 1, D, aug="per_sample")
-    assert abs(l16 - l32) <= 2e-2 * abs(l32)
-    assert max(_per_tensor_rel(ctx, g16, g32)) <= 2e-2
-    assert max(_per_tensor_rel(ctx, r16, r32)) <= 2e-2
+    assert max(_per_tensor_rel(ctx, gmu, ref["grad_mu"])) <= 0.3
