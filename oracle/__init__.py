@@ -58,6 +58,8 @@ def lib():
         _lib.orc_finalize.argtypes = [C.c_void_p] * 4 + [C.c_double] + [C.c_void_p] * 4
         _lib.orc_forward.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32,
                                                                          C.c_int, C.c_void_p]
+        _lib.orc_forward_ex.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32,
+                                                                            C.c_int, C.c_void_p, C.c_int]
         _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
                                                                          C.c_void_p, C.c_void_p]
     return _lib
@@ -188,14 +190,14 @@ def elbo_step(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=AUG_NONE, n
     return finalize(model, mu, rho, acc, D, act)
 
 
-def forward(model, mu, rho, x, s0, s1, seed, step, aug=AUG_NONE, act="relu"):
+def forward(model, mu, rho, x, s0, s1, seed, step, aug=AUG_NONE, act="relu", emu=False):
     m = model_struct(model, act)
     mu, rho, x = _d(mu), _d(rho), _d(x)
     B = x.shape[0]
     O = model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]
     z = np.zeros((s1 - s0, B, O))
-    assert lib().orc_forward(C.byref(m), _p(mu), _p(rho), _p(x), B, s0, s1, seed, step, aug,
-                             _p(z)) == 0
+    assert lib().orc_forward_ex(C.byref(m), _p(mu), _p(rho), _p(x), B, s0, s1, seed, step, aug,
+                                _p(z), 1 if emu else 0) == 0
     return z
 
 

@@ -756,8 +756,8 @@ int orc_elbo_step(const orc_model* m, const double* mu, const double* rho, const
 }
 
 /* Per-sample network outputs z[s][b][O] for samples [s0,s1) (no augmentation unless asked). */
-int orc_forward(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
-                int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out)
+int orc_forward_ex(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
+                   int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out, int emu)
 {
     ONet net;
     if (build_net(m, &net)) return -1;
@@ -776,7 +776,7 @@ int orc_forward(const orc_model* m, const double* mu, const double* rho, const d
     for (int t = 0; t < nthreads; ++t)
         if (work_alloc(n, &works[t], 0)) return -2;
     for (int s = s0; s < s1; ++s) {
-        sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, 0);
+        sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, emu);
         #pragma omp parallel num_threads(nthreads)
         {
             int tid = 0;
@@ -787,7 +787,7 @@ int orc_forward(const orc_model* m, const double* mu, const double* rho, const d
             #pragma omp for schedule(static)
             for (int b = 0; b < B; ++b) {
                 load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w->val[0]);
-                int out = forward_one(n, W, w, 0);
+                int out = forward_one(n, W, w, emu);
                 memcpy(z_out + ((long)(s - s0) * B + b) * n->n_out, w->val[out],
                        sizeof(double) * n->n_out);
             }
@@ -797,6 +797,12 @@ int orc_forward(const orc_model* m, const double* mu, const double* rho, const d
     free(works);
     free(sigma); free(W);
     return 0;
+}
+
+int orc_forward(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
+                int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out)
+{
+    return orc_forward_ex(m, mu, rho, x, B, s0, s1, seed, step, aug, z_out, 0);
 }
 
 /*

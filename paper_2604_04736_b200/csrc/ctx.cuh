@@ -150,6 +150,9 @@ struct bnn_ctx {
     float* wpart = nullptr;         // conv wgrad split partials
     std::vector<int> kpad, nsplit;  // per layer
     std::vector<CUtensorMap> cmap_w, cmap_wT, cmap_g;  // per layer
+    std::vector<CUtensorMap> cmap_bf, cmap_bd;         // per layer: 5-D activation / dY windows
+    std::vector<CUtensorMap> cmap_xw;                  // per layer: wgrad X windows (64 pixels)
+    std::vector<char> tma_fwd, tma_dgrad, tma_wgrad;   // stride-1 layers use them
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
     // TMA descriptors (BF16)
     std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;

@@ -66,12 +66,15 @@ struct ConvTcArgs {
     int relu;                  // fwd
     float* bpart;              // dgrad: fp32 bias partials of the producer of the input
     int64_t bpart_stride_s;    // per sample: (#classes·#pixel tiles·2)·C
+    int tma_b;                 // stride 1: B operand by 5-D TMA (bmap, box 64×tw×th×tn×1)
 };
 // fwd: D[co][pixel] over K = (kh, kw, ci); A = W scratch (TMA, K-major), B = gathered input
-void launch_conv_tc_fwd(const CUtensorMap& wmap, const ConvTcArgs& a, int S, cudaStream_t st);
+void launch_conv_tc_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const ConvTcArgs& a, int S,
+                        cudaStream_t st);
 // dgrad: D[ci][input pixel] over K = (tap, co); A = W scratchᵀ per tap (TMA, MN-major),
 // B = gathered dY; stride-2 convs run per input-pixel parity class
-void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const ConvTcArgs& a, int S, cudaStream_t st);
+void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const ConvTcArgs& a, int S,
+                          cudaStream_t st);
 int conv_dgrad_parts(const ConvTcArgs& a);  // bias partial count per sample
 
 struct ConvWgradArgs {
@@ -84,10 +87,12 @@ struct ConvWgradArgs {
     float scale;
     float* part;             // [nsplit][2][CO·k·k·C] partial acc (μ then ρ), already scaled
     int nsplit;
+    int tma_b;               // stride 1: X window by 5-D TMA (xmap, box 64 × 64 pixels)
 };
 // wgrad (C % 64 == 0): D[co][tap·C + ci] = Σ_pix dY·X, per sample; acc_ρ partial += D ⊙ ε_s,
 // acc_μ partial = Σ_s D (tensor-core accumulated in TMEM). gmap: 3-D map over dY (CO, pix, s).
-void launch_conv_tc_wgrad(const CUtensorMap& gmap, const ConvWgradArgs& a, cudaStream_t st);
+void launch_conv_tc_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
+                          cudaStream_t st);
 void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off,
                                float* acc_mu, float* acc_rho, cudaStream_t st);
 

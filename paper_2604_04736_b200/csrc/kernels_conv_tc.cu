@@ -85,7 +85,8 @@ constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256 + 128 * 4 + 64;
 
 template <int MODE>  // 0 fwd, 1 dgrad
 __global__ void __launch_bounds__(cv::kThreads, 2)
-    conv_tc_kernel(const __grid_constant__ CUtensorMap wmap, const ConvTcArgs a) {
+    conv_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
+                   const ConvTcArgs a) {
     using namespace cv;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(cv::kThreads, 2)
 
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], kProdWarps * 32 + 1);
+            mbar_init(&full[i], a.tma_b ? 1 : kProdWarps * 32 + 1);
             mbar_init(&empty[i], 1);
         }
         mbar_init(tfull, 1);
@@ -179,21 +180,37 @@ __global__ void __launch_bounds__(cv::kThreads, 2)
         }
         __syncwarp();
     } else if (warp == kProdWarps + 1) {
-        // ------------------------------------------------ TMA producer for A
+        // ------------------------------------------------ TMA producer: A (and B for stride 1)
         if (lane == 0 && nkb > 0) {
             tma_prefetch_desc(&wmap);
+            if (a.tma_b) tma_prefetch_desc(&bmap);
+            // tile origin in (image, row) of the pixel space (stride-1 tiles are row-aligned boxes)
+            const int n0 = p0 / (PH * PW), y0 = (p0 - n0 * (PH * PW)) / PW;
+            const int sb = a.src_stride_s == 0 ? 0 : s;
+            const int cpb_t = a.C_pad >> 6;
             for (int kb = 0; kb < nkb; ++kb) {
                 const int st = kb % kStages;
                 const uint32_t ph2 = (kb / kStages) & 1;
                 mbar_wait_sleep(&empty[st], ph2 ^ 1);
-                mbar_arrive_expect_tx(&full[st], kAStage);
+                mbar_arrive_expect_tx(&full[st], kAStage + (a.tma_b ? kBStage : 0));
                 uint8_t* dst = sA + st * kAStage;
                 if (MODE == 0) {
                     tma_load_3d(&wmap, &full[st], dst, kb * 64, m0, s);
+                    if (a.tma_b) {
+                        const int tap = kb / cpb_t, c0 = (kb - tap * cpb_t) * 64;
+                        const int kh = tap / a.k, kw = tap - kh * a.k;
+                        tma_load_5d(&bmap, &full[st], sB + st * kBStage, c0, kw - a.pad, y0 + kh - a.pad,
+                                    n0, sb);
+                    }
                 } else {
-                    const int tap = staps[kb / cblocks], cb = kb % cblocks;
+                    const int ti = kb / cblocks, tap = staps[ti], cb = kb - ti * cblocks;
                     tma_load_4d(&wmap, &full[st], dst, m0, tap, cb * 64, s);
                     tma_load_4d(&wmap, &full[st], dst + 8192, m0 + 64, tap, cb * 64, s);
+                    if (a.tma_b) {
+                        const int kh = tap / a.k, kw = tap - kh * a.k;
+                        tma_load_5d(&bmap, &full[st], sB + st * kBStage, cb * 64, a.pad - kw,
+                                    y0 + a.pad - kh, n0, s);
+                    }
                 }
             }
         }
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(cv::kThreads, 2)
         const uint32_t rowoff = tid * 128;
         const uint32_t sw = tid & 7;
         const int cpb = a.C_pad >> 6;  // 64-channel blocks per tap (0 for the 8-channel stem input)
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < (a.tma_b ? 0 : nkb); ++kb) {
             const int st = kb % kStages;
             const uint32_t ph2 = (kb / kStages) & 1;
             mbar_wait(&empty[st], ph2 ^ 1);
@@ -326,7 +343,8 @@ int conv_dgrad_parts(const ConvTcArgs& a) {
     return a.stride * a.stride * ((npix + 255) / 256) * 2;
 }
 
-void launch_conv_tc_fwd(const CUtensorMap& wmap, const ConvTcArgs& a, int S, cudaStream_t st) {
+void launch_conv_tc_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const ConvTcArgs& a, int S,
+                        cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(conv_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, cv::kSmem);
@@ -334,10 +352,11 @@ void launch_conv_tc_fwd(const CUtensorMap& wmap, const ConvTcArgs& a, int S, cud
     }
     const int npix = a.B * a.OH * a.OW;
     dim3 grid((a.CO + 127) / 128, (npix + 255) / 256, S);
-    conv_tc_kernel<0><<<grid, cv::kThreads, cv::kSmem, st>>>(wmap, a);
+    conv_tc_kernel<0><<<grid, cv::kThreads, cv::kSmem, st>>>(wmap, bmap, a);
 }
 
-void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const ConvTcArgs& a, int S, cudaStream_t st) {
+void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const ConvTcArgs& a, int S,
+                          cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, cv::kSmem);
@@ -345,7 +364,7 @@ void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const ConvTcArgs& a, int S, 
     }
     const int npix = a.B * (a.H / a.stride) * (a.W / a.stride);
     dim3 grid((a.C + 127) / 128, (npix + 255) / 256, S * a.stride * a.stride);
-    conv_tc_kernel<1><<<grid, cv::kThreads, cv::kSmem, st>>>(wmapT, a);
+    conv_tc_kernel<1><<<grid, cv::kThreads, cv::kSmem, st>>>(wmapT, bmap, a);
 }
 
 // ============================================================================ wgrad
@@ -360,7 +379,8 @@ constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
 }  // namespace cw
 
 __global__ void __launch_bounds__(cw::kThreads, 1)
-    conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap gmap, const ConvWgradArgs a) {
+    conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap xmap,
+                         const ConvWgradArgs a) {
     using namespace cw;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -396,7 +416,7 @@ __global__ void __launch_bounds__(cw::kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], kGatherWarps * 32 + 1);
+            mbar_init(&full[i], a.tma_b ? 1 : kGatherWarps * 32 + 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -415,16 +435,23 @@ __global__ void __launch_bounds__(cw::kThreads, 1)
         // ------------------------------------------------ TMA: dYᵀ blocks
         if (lane == 0 && nblk > 0) {
             tma_prefetch_desc(&gmap);
+            if (a.tma_b) tma_prefetch_desc(&xmap);
             int it = 0;
             for (int s = 0; s < S; ++s)
                 for (int b = 0; b < nblk; ++b, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
                     mbar_wait_sleep(&empty[st], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[st], kAStage);
+                    mbar_arrive_expect_tx(&full[st], kAStage + (a.tma_b ? kBStage : 0));
                     uint8_t* dst = sA + st * kAStage;
-                    tma_load_3d(&gmap, &full[st], dst, co0, (blk0 + b) * 64, s);
-                    tma_load_3d(&gmap, &full[st], dst + 8192, co0 + 64, (blk0 + b) * 64, s);
+                    const int pix0 = (blk0 + b) * 64;
+                    tma_load_3d(&gmap, &full[st], dst, co0, pix0, s);
+                    tma_load_3d(&gmap, &full[st], dst + 8192, co0 + 64, pix0, s);
+                    if (a.tma_b) {  // stride 1: the shifted input window of these 64 pixels
+                        const int n0 = pix0 / (a.OH * a.OW), y0 = (pix0 - n0 * a.OH * a.OW) / a.OW;
+                        tma_load_5d(&xmap, &full[st], sB + st * kBStage, ci0, kw - a.pad, y0 + kh - a.pad,
+                                    n0, a.X_stride_s == 0 ? 0 : s);
+                    }
                 }
         }
         __syncwarp();
@@ -462,7 +489,7 @@ __global__ void __launch_bounds__(cw::kThreads, 1)
         // ------------------------------------------------ gather X windows: 64 rows × 8 chunks
         const int gt = threadIdx.x - kEpiWarps * 32;  // 0..127
         int it = 0;
-        for (int s = 0; s < S; ++s) {
+        for (int s = 0; s < (a.tma_b ? 0 : S); ++s) {
             const __nv_bfloat16* xs = a.X + s * a.X_stride_s;
             for (int b = 0; b < nblk; ++b, ++it) {
                 const int st = it % kStages;
@@ -557,14 +584,15 @@ __global__ void __launch_bounds__(cw::kThreads, 1)
     }
 }
 
-void launch_conv_tc_wgrad(const CUtensorMap& gmap, const ConvWgradArgs& a, cudaStream_t st) {
+void launch_conv_tc_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
+                          cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(conv_wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cw::kSmem);
         attr = true;
     }
     const int tiles = ((a.CO + 127) / 128) * a.k * a.k * (a.C / 64) * a.nsplit;
-    conv_wgrad_tc_kernel<<<tiles, cw::kThreads, cw::kSmem, st>>>(gmap, a);
+    conv_wgrad_tc_kernel<<<tiles, cw::kThreads, cw::kSmem, st>>>(gmap, xmap, a);
 }
 
 __global__ void wgrad_split_reduce_kernel(const float* __restrict__ part, int nsplit, int64_t n,

@@ -70,6 +70,12 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->cmap_w.resize(L);
     c->cmap_wT.resize(L);
     c->cmap_g.resize(L);
+    c->cmap_bf.resize(L);
+    c->cmap_bd.resize(L);
+    c->cmap_xw.resize(L);
+    c->tma_fwd.assign(L, 0);
+    c->tma_dgrad.assign(L, 0);
+    c->tma_wgrad.assign(L, 0);
     size_t wmax = 0, pmax = 0;
     int maxN = 0;
     for (const ROp& op : c->rops) {
@@ -121,6 +127,51 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const uint32_t gbx[3] = {64, 64, 1};
             if (!make_map_nd(&c->cmap_g[op.layer], c->rbf[gb].grad, 3, gd, gs, gbx))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (dY) failed");
+        }
+    }
+    // stride-1 convs: the B operand (activation / dY window) by 5-D TMA with OOB zero fill
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op)) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        if (Ld.stride != 1) continue;
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        const int PW = Db.W, PH = Db.H;  // stride 1: output pixel space == input pixel space
+        if (256 % PW != 0) continue;
+        const int th = std::min(PH, 256 / PW);
+        if (PH % th != 0) continue;
+        const int tn = 256 / (PW * th);
+        const uint32_t box[5] = {64, (uint32_t)PW, (uint32_t)th, (uint32_t)tn, 1};
+        const int Cp = c->rbf[op.src].C_pad;
+        if (Cp % 64 == 0) {
+            const bool shared = op.src == 0 && c->cfg.aug != BNN_AUG_PER_SAMPLE;
+            const uint64_t dims[5] = {(uint64_t)Cp, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B,
+                                      (uint64_t)(shared ? 1 : Sc)};
+            const uint64_t str[4] = {(uint64_t)Cp * 2, (uint64_t)Sb.W * Cp * 2, (uint64_t)Sb.H * Sb.W * Cp * 2,
+                                     (uint64_t)B * Sb.H * Sb.W * Cp * 2};
+            if (!make_map_nd(&c->cmap_bf[op.layer], c->rbf[op.src].val, 5, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (activation window) failed");
+            c->tma_fwd[op.layer] = 1;
+            // wgrad: 64-pixel blocks of the output pixel space
+            if (64 % PW == 0 || PW % 64 == 0) {
+                const int wh = PW >= 64 ? 1 : std::min(PH, 64 / PW);
+                const int wn = 64 / (std::min(PW, 64) * wh);
+                if (PW <= 64 && PH % wh == 0 && wn >= 1) {
+                    const uint32_t wbox[5] = {64, (uint32_t)std::min(PW, 64), (uint32_t)wh, (uint32_t)wn, 1};
+                    if (!make_map_nd(&c->cmap_xw[op.layer], c->rbf[op.src].val, 5, dims, str, wbox))
+                        return c->set_err(BNN_ERR_CUDA, "tensor map (wgrad window) failed");
+                    c->tma_wgrad[op.layer] = Ld.cin % 64 == 0 ? 1 : 0;
+                }
+            }
+        }
+        if (op.src != 0 && Db.C % 64 == 0 && Ld.cin % 64 == 0) {
+            const int gb = grad_src_buffer(c, op.dst);
+            const uint64_t dims[5] = {(uint64_t)Db.C, (uint64_t)Db.W, (uint64_t)Db.H, (uint64_t)B, (uint64_t)Sc};
+            const uint64_t str[4] = {(uint64_t)Db.C * 2, (uint64_t)Db.W * Db.C * 2,
+                                     (uint64_t)Db.H * Db.W * Db.C * 2, (uint64_t)B * Db.H * Db.W * Db.C * 2};
+            if (!make_map_nd(&c->cmap_bd[op.layer], c->rbf[gb].grad, 5, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (dY window) failed");
+            c->tma_dgrad[op.layer] = 1;
         }
     }
     // head: pooled features [S][B][Cf] → logits, with the MLP kernels' descriptors
@@ -207,7 +258,8 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
             a.res_stride_s = a.out_stride_s;
         }
         a.relu = op.relu;
-        c->launch("fwd", [&] { launch_conv_tc_fwd(c->cmap_w[op.layer], a, Sc, st); });
+        a.tma_b = c->tma_fwd[op.layer];
+        c->launch("fwd", [&] { launch_conv_tc_fwd(c->cmap_w[op.layer], c->cmap_bf[op.layer], a, Sc, st); });
     }
 }
 
@@ -324,7 +376,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.scale = scale;
             w.part = c->wpart;
             w.nsplit = c->nsplit[op.layer];
-            c->launch("wgrad", [&] { launch_conv_tc_wgrad(c->cmap_g[op.layer], w, st); });
+            w.tma_b = c->tma_wgrad[op.layer];
+            c->launch("wgrad", [&] { launch_conv_tc_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
             const int64_t n = (int64_t)Ld.cout * Ld.k * Ld.k * Ld.cin;
             c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, w.nsplit, n, Ld.off_w, acc_mu, acc_rho, st); });
         } else {
@@ -380,7 +433,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
                 return c->set_err(BNN_ERR_CONFIG, "bias partial buffer too small");
             c->rbf[op.src].nparts = conv_dgrad_parts(a);
         }
-        c->launch("dgrad", [&] { launch_conv_tc_dgrad(c->cmap_wT[op.layer], a, Sc, st); });
+        a.tma_b = c->tma_dgrad[op.layer];
+        c->launch("dgrad", [&] { launch_conv_tc_dgrad(c->cmap_wT[op.layer], c->cmap_bd[op.layer], a, Sc, st); });
         if (!final) pending[op.src] = c->rbf[op.src].grad;
     }
     c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });

@@ -26,3 +26,12 @@ for t in ctx.tensors:
     print(f"t={t['t']:3d} {t['rows']:4d}x{t['cols']:5d}  mu: vs-emu {rel(gm, emu['grad_mu']):.2e} "
           f"vs-exact {rel(gm, ref['grad_mu']):.2e} emu-vs-exact {rel(emu['grad_mu'], ref['grad_mu']):.2e} | "
           f"rho: vs-emu {rel(gr, emu['grad_rho']):.2e} vs-exact {rel(gr, ref['grad_rho']):.2e}")
+
+# forward only: softmax of the GPU forward (predict, S=1) vs the emulated / exact forward
+mean, var = ctx.predict(torch.from_numpy(mu).cuda(), torch.from_numpy(rho).cuda(), torch.from_numpy(x).cuda(), 1, 7, 1)
+pg = mean.cpu().numpy()
+for emu_flag in (True, False):
+    z = O.forward(model, mu, rho, x, 0, 1, 7, 1, emu=emu_flag)[0]
+    p = np.exp(z - z.max(-1, keepdims=True)); p /= p.sum(-1, keepdims=True)
+    print("forward probs rel err", "emu" if emu_flag else "exact", np.linalg.norm(pg - p) / np.linalg.norm(p))
+    print("  logits", z[0][:5])
