@@ -201,6 +201,12 @@ int bnn_profile_enable(bnn_ctx* ctx, int32_t on);
 int bnn_profile_read(bnn_ctx* ctx, char* names, int32_t names_cap, double* ms, int64_t* launches,
                      int32_t max_entries, int32_t* n_entries);
 
+/* Test hook (ResNet contexts): copy the stored output (which = 0) or output gradient
+ * (which = 1) of layer `layer` of the last step, [S_chunk][B][H][W][C] as fp32, into out_dev
+ * (cap floats); *n_out receives the element count. Synchronises. */
+int bnn_debug_layer_output(bnn_ctx* ctx, int32_t layer, int32_t which, float* out_dev,
+                           int64_t cap, int64_t* n_out);
+
 /* Number of kernels the library launched since bnn_init (bench.py's gpu_launches). */
 int64_t bnn_launch_count(bnn_ctx* ctx);
 

@@ -211,3 +211,18 @@ def predict(model, mu, rho, x, S, seed, step):
     assert lib().orc_predict(C.byref(m), _p(mu), _p(rho), _p(x), B, S, seed, step, _p(mean),
                              _p(var)) == 0
     return mean, var
+
+
+def layer_output(model, mu, rho, x, b, s, seed, step, layer, aug=AUG_NONE, emu=False):
+    """Stored output of `layer` for example b, sample s (test hook)."""
+    m = model_struct(model)
+    L = lib()
+    L.orc_layer_output.restype = C.c_long
+    L.orc_layer_output.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32] + \
+        [C.c_int] * 3 + [C.c_void_p]
+    mu, rho, x = _d(mu), _d(rho), _d(x)
+    out = np.zeros(1 << 22)
+    n = L.orc_layer_output(C.byref(m), _p(mu), _p(rho), _p(x), b, s, seed, step, aug,
+                           1 if emu else 0, layer, _p(out))
+    assert n > 0, n
+    return out[:n]

@@ -868,3 +868,32 @@ void orc_philox_fill(const uint32_t ctr[4], const uint32_t key[2], long n, uint3
         orc_philox4x32_10(c, key, out + 4 * i);
     }
 }
+
+/* Debug/test hook: the stored output of layer `layer` (after its activation and, with emu,
+ * its bf16 rounding) for example b under sample s; returns the element count. */
+long orc_layer_output(const orc_model* m, const double* mu, const double* rho, const double* x,
+                      int b, int s, uint64_t seed, uint32_t step, int aug, int emu, int layer,
+                      double* out)
+{
+    ONet net;
+    if (build_net(m, &net)) return -1;
+    ONet* n = &net;
+    long P = n->n_params;
+    double* sigma = (double*)malloc(sizeof(double) * P);
+    double* W = (double*)malloc(sizeof(double) * P);
+    OWork w;
+    if (!sigma || !W || work_alloc(n, &w, 0)) return -2;
+    for (long i = 0; i < P; ++i) sigma[i] = softplus(rho[i]);
+    sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, emu);
+    load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w.val[0]);
+    forward_one(n, W, &w, emu);
+    long cnt = -3;
+    for (int i = 0; i < n->n_ops; ++i)
+        if (n->ops[i].type == OP_CONV && n->ops[i].layer == layer) {
+            int d = n->ops[i].dst;
+            cnt = buf_size(n, d);
+            memcpy(out, w.val[d], sizeof(double) * (size_t)cnt);
+        }
+    free(w.pool); free(sigma); free(W);
+    return cnt;
+}

@@ -50,6 +50,7 @@ void launch_predict_stats(const float* logits, int S, int B, int O, int loss_kin
 void launch_predict_merge(const float* means, const float* m2s, const float* counts, int R,
                           int BO, float* mean, float* var, cudaStream_t st);
 // x fp32 [B][K] → bf16 [B][ldx] (zero padding of columns K..ldx)
+void launch_bf16_to_f32(const void* x, int64_t n, float* y, cudaStream_t st);
 void launch_to_bf16(const float* x, int B, int K, int ldx, void* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- K11: FP32 SIMT sampled GEMMs

@@ -318,6 +318,15 @@ void launch_to_bf16(const float* x, int B, int K, int ldx, void* out, cudaStream
     to_bf16_kernel<<<grid, 256, 0, st>>>(x, B, K, ldx, reinterpret_cast<__nv_bfloat16*>(out));
 }
 
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ x, int64_t n, float* __restrict__ y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __bfloat162float(x[i]);
+}
+void launch_bf16_to_f32(const void* x, int64_t n, float* y, cudaStream_t st) {
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+    bf16_to_f32_kernel<<<std::max(grid, 1), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), n, y);
+}
+
 // ====================================================================== K11: FP32 SIMT GEMMs
 constexpr int TB = 64, TK = 16;
 

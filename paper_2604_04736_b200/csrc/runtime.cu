@@ -844,6 +844,31 @@ int bnn_profile_read(bnn_ctx* c, char* names, int32_t cap, double* ms, int64_t* 
 
 int64_t bnn_launch_count(bnn_ctx* c) { return c ? c->launches : -1; }
 
+int bnn_debug_layer_output(bnn_ctx* c, int32_t layer, int32_t which, float* out, int64_t cap,
+                           int64_t* n_out) {
+    if (!c || !out) return BNN_ERR_CONFIG;
+    if (c->model.kind != BNN_MODEL_RESNET18) return c->set_err(BNN_ERR_CONFIG, "ResNet contexts only");
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || op.layer != layer) continue;
+        const RBuf& D = c->rbufs[op.dst];
+        const int64_t n = (int64_t)c->chunk * c->B_max * D.H * D.W * D.C;
+        if (n > cap) return c->set_err(BNN_ERR_CONFIG, "debug buffer too small");
+        if (n_out) *n_out = n;
+        if (!c->bf16) {
+            const float* src = which == 0 ? D.val : D.grad;
+            CUDA_TRY(c, cudaMemcpyAsync(out, src, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->st));
+        } else if (op.dst == c->rlogits) {
+            CUDA_TRY(c, cudaMemcpyAsync(out, c->logits, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->st));
+        } else {
+            const __nv_bfloat16* src = which == 0 ? c->rbf[op.dst].val : c->rbf[op.dst].grad;
+            launch_bf16_to_f32(src, n, out, c->st);
+        }
+        CUDA_TRY(c, cudaStreamSynchronize(c->st));
+        return BNN_OK;
+    }
+    return c->set_err(BNN_ERR_CONFIG, "no such layer");
+}
+
 const char* bnn_last_error(bnn_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
 
 void bnn_destroy(bnn_ctx* c) {

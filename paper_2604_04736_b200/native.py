@@ -72,6 +72,7 @@ def lib():
     L.bnn_eps_transform_table.argtypes = [i32, vp, vp]
     L.bnn_profile_enable.argtypes = [vp, i32]
     L.bnn_profile_read.argtypes = [vp, vp, i32, vp, vp, i32, vp]
+    L.bnn_debug_layer_output.argtypes = [vp, i32, i32, vp, i64, vp]
     L.bnn_launch_count.argtypes = [vp]
     L.bnn_launch_count.restype = i64
     L.bnn_last_error.argtypes = [vp]
@@ -229,6 +230,14 @@ class Context:
         _check(self._L.bnn_profile_read(self._h, names, 1024, ms, n, 32, C.byref(cnt)), self._h)
         keys = names.value.decode().split(",") if cnt.value else []
         return {k: dict(ms=ms[i], launches=n[i]) for i, k in enumerate(keys)}
+
+    def layer_output(self, layer: int, which: int = 0) -> torch.Tensor:
+        """Test hook: stored output (0) or its gradient (1) of `layer` from the last step."""
+        cap = 1 << 27
+        out = torch.empty(cap, dtype=torch.float32, device=self.device)
+        n = C.c_int64()
+        _check(self._L.bnn_debug_layer_output(self._h, layer, which, _p(out), cap, C.byref(n)), self._h)
+        return out[:n.value].clone()
 
     def launch_count(self) -> int:
         return int(self._L.bnn_launch_count(self._h))
