@@ -35,3 +35,14 @@ for emu_flag in (True, False):
     p = np.exp(z - z.max(-1, keepdims=True)); p /= p.sum(-1, keepdims=True)
     print("forward probs rel err", "emu" if emu_flag else "exact", np.linalg.norm(pg - p) / np.linalg.norm(p))
     print("  logits", z[0][:5])
+
+# per-layer stored activations: GPU vs emulated oracle vs exact oracle (sample 0, example 0)
+for t in ctx.tensors[::2]:
+    l = t["t"] // 2
+    g = ctx.layer_output(l, 0).cpu().numpy().astype(np.float64)
+    e = O.layer_output(model, mu, rho, x, 0, 0, 7, 1, l, emu=True)
+    r = O.layer_output(model, mu, rho, x, 0, 0, 7, 1, l, emu=False)
+    g0 = g[:e.size]
+    print(f"layer {l:2d} out {e.size:6d}: gpu-vs-emu {np.linalg.norm(g0-e)/np.linalg.norm(e):.2e} "
+          f"gpu-vs-exact {np.linalg.norm(g0-r)/np.linalg.norm(r):.2e} emu-vs-exact {np.linalg.norm(e-r)/np.linalg.norm(r):.2e} "
+          f"max|gpu-emu| {np.abs(g0-e).max():.3e} frac!= {(g0 != e).mean():.3f}")
