@@ -226,3 +226,19 @@ def layer_output(model, mu, rho, x, b, s, seed, step, layer, aug=AUG_NONE, emu=F
                            1 if emu else 0, layer, _p(out))
     assert n > 0, n
     return out[:n]
+
+
+def layer_grad(model, mu, rho, x, y_cls, y_reg, b, s, seed, step, layer, aug=AUG_NONE, emu=False):
+    """Unscaled dℓ/d(stored output of `layer`) for example b, sample s (test hook)."""
+    m = model_struct(model)
+    L = lib()
+    L.orc_layer_grad.restype = C.c_long
+    L.orc_layer_grad.argtypes = [C.c_void_p] * 6 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32] + \
+        [C.c_int] * 3 + [C.c_void_p]
+    mu, rho, x, yr = _d(mu), _d(rho), _d(x), _d(y_reg)
+    yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
+    out = np.zeros(1 << 22)
+    n = L.orc_layer_grad(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), b, s, seed, step, aug,
+                         1 if emu else 0, layer, _p(out))
+    assert n > 0, n
+    return out[:n]
