@@ -46,3 +46,17 @@ for t in ctx.tensors[::2]:
     print(f"layer {l:2d} out {e.size:6d}: gpu-vs-emu {np.linalg.norm(g0-e)/np.linalg.norm(e):.2e} "
           f"gpu-vs-exact {np.linalg.norm(g0-r)/np.linalg.norm(r):.2e} emu-vs-exact {np.linalg.norm(e-r)/np.linalg.norm(r):.2e} "
           f"max|gpu-emu| {np.abs(g0-e).max():.3e} frac!= {(g0 != e).mean():.3f}")
+
+# per-layer gradients (unscaled dl/d out) and sample 1 activations
+for t in ctx.tensors[::2]:
+    l = t["t"] // 2
+    e = O.layer_output(model, mu, rho, x, 0, 1, 7, 1, l, emu=True)
+    g = ctx.layer_output(l, 0).cpu().numpy().astype(np.float64)
+    n = e.size
+    g1 = g[B * n:B * n + n]  # sample 1, example 0
+    ge = O.layer_grad(model, mu, rho, x, yc, None, 0, 0, 7, 1, l, emu=True)
+    gg = ctx.layer_output(l, 1).cpu().numpy().astype(np.float64)[:n] if l < 20 else None
+    msg = f"layer {l:2d}: s1 act gpu-vs-emu {np.linalg.norm(g1-e)/np.linalg.norm(e):.2e}"
+    if gg is not None:
+        msg += f"  grad gpu-vs-emu {np.linalg.norm(gg-ge)/max(np.linalg.norm(ge),1e-30):.2e} |ge| {np.linalg.norm(ge):.3e} |gg| {np.linalg.norm(gg):.3e}"
+    print(msg)
