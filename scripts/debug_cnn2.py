@@ -26,7 +26,7 @@ for t in ctx.tensors:
     r = lambda a, b: np.linalg.norm(a[sl] - b[sl]) / max(np.linalg.norm(b[sl]), 1e-30)
     print(f"t={t['t']:2d} {t['rows']:4d}x{t['cols']:5d} acc_mu {r(a_mu, e_mu):.2e} acc_rho {r(a_rho, e_rho):.2e} "
           f"|mu| {np.linalg.norm(e_mu[sl]):.3e}")
-for l in range(20):
+for l in []:
     gg = ctx.layer_output(l, 1).cpu().numpy().astype(np.float64)
     errs = []
     for s in range(S):
@@ -36,3 +36,13 @@ for l in range(20):
             g = gg[(s * B + b) * n:(s * B + b + 1) * n]
             errs.append(np.linalg.norm(g - ge) / max(np.linalg.norm(ge), 1e-30))
     print(f"layer {l:2d} grad per (s,b):", " ".join(f"{v:.1e}" for v in errs))
+for l in range(21):
+    ga = ctx.layer_output(l, 0).cpu().numpy().astype(np.float64)
+    errs = []
+    for s in range(S):
+        for b in range(B):
+            ee = O.layer_output(model, mu, rho, x, b, s, 7, 1, l, emu=True)
+            n = ee.size
+            g = ga[(s * B + b) * n:(s * B + b + 1) * n]
+            errs.append(np.linalg.norm(g - ee) / max(np.linalg.norm(ee), 1e-30))
+    print(f"layer {l:2d} act per (s,b):", " ".join(f"{v:.1e}" for v in errs))
