@@ -44,7 +44,32 @@ namespace bnn {
 // many CTAs, so W_s is formed once per (sample, layer, pass) into this L2-resident buffer
 // instead of per pixel tile.
 void launch_gen_wscratch(const SampledLayer& L, const SampleKeys& kk, int S, int C, int C_pad,
-                         int taps, int K_pad, __nv_bfloat16* out, cudaStream_t st);
+                         int taps, int K_pad, __nv_bfloat16* out, float* bias_out, cudaStream_t st);
+
+// Persistent swap-AB conv (kernels_conv2.cu): M = 128 pixels, N = n_tile channels.
+struct Conv2Args {
+    int S;
+    int B, H, W, C, C_pad;  // conv input per sample (C_pad = channel pitch of the input buffer)
+    int OH, OW, CO;
+    int k, stride, pad;
+    int K_pad;              // W scratch row pitch
+    int n_tile;             // 64, 128 or 256
+    int tma_a;              // stride 1: A window by 5-D TMA (amap, 128-pixel box)
+    const __nv_bfloat16* src;  // gathered A: fwd input [s][B][H][W][C_pad], dgrad dY [s][B][OH][OW][CO]
+    int64_t src_stride_s;      // 0 ⇒ the input is shared by all samples
+    __nv_bfloat16* out;        // fwd [s][B][OH][OW][CO]; dgrad [s][B][H][W][C]
+    int64_t out_stride_s;      // also the stride of res / addsrc / mask
+    const float* bias;         // fwd: sampled biases [S][CO]
+    const __nv_bfloat16* res;  // fwd residual
+    const __nv_bfloat16* addsrc;  // dgrad: other contribution, added before the mask
+    const __nv_bfloat16* mask;    // dgrad: ReLU mask source (the conv input activation)
+    int relu;
+    float* bpart;              // dgrad: fp32 bias partials [s][parts][C]
+    int64_t bpart_stride_s;
+};
+void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
+void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
+int conv2_dgrad_parts(const Conv2Args& a);
 
 struct ConvTcArgs {
     SampledLayer L;
@@ -88,6 +113,7 @@ struct ConvWgradArgs {
     float* part;             // [nsplit][2][CO·k·k·C] partial acc (μ then ρ), already scaled
     int nsplit;
     int tma_b;               // stride 1: X window by 5-D TMA (xmap, box 64 × 64 pixels)
+    int n_tile;              // conv2 wgrad: parameter columns per tile (64 | 128 | 192 | 256)
 };
 // wgrad (C % 64 == 0): D[co][tap·C + ci] = Σ_pix dY·X, per sample; acc_ρ partial += D ⊙ ε_s,
 // acc_μ partial = Σ_s D (tensor-core accumulated in TMEM). gmap: 3-D map over dY (CO, pix, s).
@@ -95,6 +121,15 @@ void launch_conv_tc_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, cons
                           cudaStream_t st);
 void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off,
                                float* acc_mu, float* acc_rho, cudaStream_t st);
+// conv2 wgrad, phase 1 (tensor cores): per-sample, per-pixel-split weight gradients
+//   part[s][split][co][tap·C + ci] = Σ_{pix ∈ split} dY_s[pix][co] · X_s[pix ⊕ tap][ci]   (fp32)
+// phase 2 (ALU): acc_μ += scale·Σ_s Σ_split part;  acc_ρ += scale·Σ_s ε_s ⊙ Σ_split part.
+void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
+                        cudaStream_t st);
+void launch_wgrad_eps_combine(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO,
+                              int Kt, const float* part, float scale, float* acc_mu, float* acc_rho,
+                              cudaStream_t st);
+int conv2_wgrad_ntile(int Kt);
 
 // image-path helpers on bf16 NHWC buffers
 void launch_input_bf16(const float* x, int S, int B, int H, int W, int C, int C_pad, int aug,

@@ -1,0 +1,707 @@
+// kernels_conv2.cu — persistent swap-AB tcgen05 implicit-GEMM convolution (K3 fwd, K4 dgrad).
+//
+//   fwd   D[pixel][co] = Σ_{kh,kw,ci} X[pixel ⊕ (kh,kw)][ci] · W_s[co][kh,kw,ci]
+//   dgrad D[pixel][ci] = Σ_{kh,kw,co} dY[pixel ⊖ (kh,kw)][co] · W_s[co][kh,kw,ci]
+//
+// M = 128 pixels (TMEM lanes), N = up to 256 channels (TMEM columns), K = 64 per stage.
+// Putting pixels on M makes every TMEM lane one NHWC row, so the epilogue reads 32
+// consecutive channels per tcgen05.ld and moves them with 16-byte vector loads/stores, with
+// bias, residual, ReLU, the ReLU mask of the layer input and the producer's bias-gradient
+// partials fused. A operand: the activation (fwd) or dY (dgrad) window — 5-D TMA with OOB
+// zero fill for stride-1 convs, a cp.async gather for stride 2 and the 3-channel stem. B
+// operand: the W_s scratch (K-major for fwd, MN-major for dgrad) by TMA. Persistent CTAs
+// walk a static tile schedule; two TMEM accumulators let tile i's epilogue overlap tile
+// i+1's main loop.
+#include <algorithm>
+
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "kernels_conv.cuh"
+#include "tc_ptx.cuh"
+
+namespace bnn {
+
+using namespace ptx;
+
+namespace c2 {
+constexpr int kEpiWarps = 4;
+constexpr int kGatherWarps = 4;
+constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
+constexpr int kStages = 4;
+constexpr int kAStage = 128 * 64 * 2;  // 16 KB pixel window
+constexpr int kBStage = 256 * 64 * 2;  // 32 KB weights (N ≤ 256)
+constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 512 + 1024;
+}  // namespace c2
+
+struct TileGeo {
+    int s, cls, ptile, ntile;
+};
+
+template <int MODE>
+__device__ __forceinline__ TileGeo tile_of(int t, int ntiles, int ptiles, int ncls) {
+    TileGeo g;
+    g.ntile = t % ntiles;
+    t /= ntiles;
+    g.ptile = t % ptiles;
+    t /= ptiles;
+    g.cls = t % ncls;
+    g.s = t / ncls;
+    return g;
+}
+
+// transpose-reduce: lane j ends with Σ over the warp's 32 lanes of v[j]
+__device__ __forceinline__ float warp_transpose_sum(float* v, int lane) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const float send = upper ? v[i] : v[i + off];
+            const float keep = upper ? v[i + off] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(c2::kThreads, 1)
+    conv2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap wmap,
+                 const Conv2Args a) {
+    using namespace c2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kAStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = bars + 2 * kStages + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    int* staps = reinterpret_cast<int*>(tslot + 4);  // [4 classes][9 taps] + counts
+    float* bred = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [2][4 warps][32]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncls = MODE == 1 ? a.stride * a.stride : 1;
+    const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
+    const int P = a.B * PH * PW;
+    const int ptiles = (P + 127) / 128;
+    const int Ntot = MODE == 0 ? a.CO : a.C;
+    const int ntiles = (Ntot + a.n_tile - 1) / a.n_tile;
+    const int T = a.S * ncls * ptiles * ntiles;
+    const int cblocks = (a.CO + 63) / 64;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1 + (a.tma_a ? 0 : kGatherWarps * 32));
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kEpiWarps);
+        }
+        mbar_fence_init();
+        // valid taps per parity class (dgrad): staps[cls*10 + 9] = count
+        for (int cl = 0; cl < ncls; ++cl) {
+            const int ph = cl / a.stride, pw = cl % a.stride;
+            int cnt = 0;
+            if (MODE == 1) {
+                for (int kh = 0; kh < a.k; ++kh)
+                    for (int kw = 0; kw < a.k; ++kw)
+                        if ((ph + a.pad - kh) % a.stride == 0 && (pw + a.pad - kw) % a.stride == 0)
+                            staps[cl * 10 + cnt++] = kh * a.k + kw;
+            }
+            staps[cl * 10 + 9] = cnt;
+        }
+    }
+    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    auto nkb_of = [&](int cls) { return MODE == 0 ? a.K_pad / 64 : staps[cls * 10 + 9] * cblocks; };
+
+    if (warp == kEpiWarps + kGatherWarps) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&wmap);
+            if (a.tma_a) tma_prefetch_desc(&amap);
+            const int cpb = a.C_pad >> 6;
+            const uint32_t bbytes = (uint32_t)a.n_tile * 128;
+            int it = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+                const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
+                const int p0 = g.ptile * 128, n0 = g.ntile * a.n_tile;
+                const int img0 = p0 / (PH * PW), y0 = (p0 - img0 * PH * PW) / PW;
+                const int nkb = nkb_of(g.cls);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[st], bbytes + (a.tma_a ? kAStage : 0));
+                    uint8_t* dA = sA + st * kAStage;
+                    uint8_t* dB = sB + st * kBStage;
+                    if (MODE == 0) {
+                        tma_load_3d(&wmap, &full[st], dB, kb * 64, n0, g.s);
+                        if (a.tma_a) {
+                            const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
+                            const int kh = tap / a.k, kw = tap - kh * a.k;
+                            tma_load_5d(&amap, &full[st], dA, c0, kw - a.pad, y0 + kh - a.pad, img0,
+                                        a.src_stride_s == 0 ? 0 : g.s);
+                        }
+                    } else {
+                        const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti], cb = kb - ti * cblocks;
+                        for (int j = 0; j < a.n_tile / 64; ++j)
+                            tma_load_4d(&wmap, &full[st], dB + j * 8192, n0 + 64 * j, tap, cb * 64, g.s);
+                        if (a.tma_a) {
+                            const int kh = tap / a.k, kw = tap - kh * a.k;
+                            tma_load_5d(&amap, &full[st], dA, cb * 64, a.pad - kw, y0 + a.pad - kh, img0, g.s);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kEpiWarps + kGatherWarps + 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, a.n_tile, 0, MODE == 1 ? 1 : 0);
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
+                const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
+                const int buf = tl & 1;
+                mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + buf * 256;
+                const int nkb = nkb_of(g.cls);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait_sleep(&full[st], ph);
+                    fence_proxy_async_smem();
+                    tc_fence_after();
+                    const uint32_t aBase = smem_u32(sA + st * kAStage);
+                    const uint32_t bBase = smem_u32(sB + st * kBStage);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t ad = sdesc_sw128(aBase + 32 * q, 16, 1024);
+                        const uint64_t bd = MODE == 0 ? sdesc_sw128(bBase + 32 * q, 16, 1024)
+                                                      : sdesc_sw128(bBase + 2048 * q, 8192, 1024);
+                        mma_bf16(d, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[buf]);  // no MMAs (empty parity class): arrives at once
+            }
+        }
+        __syncwarp();
+    } else if (warp >= kEpiWarps) {
+        // ------------------------------------------------ gather producers (stride 2 / stem)
+        if (!a.tma_a) {
+            const int r = threadIdx.x - kEpiWarps * 32;  // pixel row 0..127
+            const int cpb = a.C_pad >> 6;
+            int it = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+                const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
+                const int ph = g.cls / a.stride, pw = g.cls % a.stride;
+                const int pix = g.ptile * 128 + r;
+                const bool pv = pix < P;
+                const int pn = pv ? pix / (PH * PW) : 0;
+                const int rem = pv ? pix - pn * PH * PW : 0;
+                const int py = MODE == 0 ? rem / PW : (rem / PW) * a.stride + ph;
+                const int px = MODE == 0 ? rem % PW : (rem % PW) * a.stride + pw;
+                const __nv_bfloat16* src = a.src + g.s * a.src_stride_s;
+                const int nkb = nkb_of(g.cls);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t phs = (it / kStages) & 1;
+                    mbar_wait(&empty[st], phs ^ 1);
+                    const uint32_t base = smem_u32(sA + st * kAStage) + r * 128;
+                    if (MODE == 0 && cpb == 0) {  // stem: 8 taps × 8 channels per K block
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int tap = kb * 8 + j;
+                            const int kh = tap / a.k, kw = tap - (tap / a.k) * a.k;
+                            const int iy = py * a.stride + kh - a.pad, ix = px * a.stride + kw - a.pad;
+                            const bool ok = pv && tap < a.k * a.k && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                            const __nv_bfloat16* gp = ok ? src + (((int64_t)pn * a.H + iy) * a.W + ix) * a.C_pad : src;
+                            cp_async16(base + ((j ^ (r & 7)) << 4), gp, ok ? 16u : 0u);
+                        }
+                    } else {
+                        int kh, kw, c0;
+                        if (MODE == 0) {
+                            const int tap = kb / cpb;
+                            c0 = (kb - tap * cpb) * 64;
+                            kh = tap / a.k;
+                            kw = tap - kh * a.k;
+                        } else {
+                            const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti];
+                            c0 = (kb - ti * cblocks) * 64;
+                            kh = tap / a.k;
+                            kw = tap - kh * a.k;
+                        }
+                        bool ok;
+                        const __nv_bfloat16* gp = src;
+                        if (MODE == 0) {
+                            const int iy = py * a.stride + kh - a.pad, ix = px * a.stride + kw - a.pad;
+                            ok = pv && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                            if (ok) gp = src + (((int64_t)pn * a.H + iy) * a.W + ix) * a.C_pad + c0;
+                        } else {
+                            const int ty = py + a.pad - kh, tx = px + a.pad - kw;
+                            const int oy = ty / a.stride, ox = tx / a.stride;
+                            ok = pv && ty >= 0 && tx >= 0 && oy < a.OH && ox < a.OW;
+                            if (ok) gp = src + (((int64_t)pn * a.OH + oy) * a.OW + ox) * a.CO + c0;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            cp_async16(base + ((j ^ (r & 7)) << 4), gp + 8 * j, ok ? 16u : 0u);
+                    }
+                    cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue: thread = pixel row
+        const int row = 32 * warp + lane;
+        int tl = 0, nred = 0;
+        for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
+            const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
+            const int buf = tl & 1;
+            const int nkb = nkb_of(g.cls);
+            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            tc_fence_after();
+            const int pix = g.ptile * 128 + row;
+            const bool pv = pix < P;
+            int64_t rowoff = 0;  // element offset of this pixel's channel 0
+            if (pv) {
+                if (MODE == 0 || a.stride == 1) {
+                    rowoff = (int64_t)pix * Ntot;
+                } else {
+                    const int ph = g.cls / a.stride, pw = g.cls % a.stride;
+                    const int pn = pix / (PH * PW), rem = pix - pn * PH * PW;
+                    const int iy = (rem / PW) * a.stride + ph, ix = (rem % PW) * a.stride + pw;
+                    rowoff = (((int64_t)pn * a.H + iy) * a.W + ix) * a.C;
+                }
+            }
+            const int n0 = g.ntile * a.n_tile;
+            const int64_t so = (int64_t)g.s * a.out_stride_s;
+            for (int c = 0; c < a.n_tile / 32; ++c) {
+                float v[32];
+                __syncwarp();
+                if (nkb > 0) {
+                    tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + buf * 256 + c * 32, v);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+                }
+                const int ch0 = n0 + c * 32;
+                if (MODE == 0) {
+                    const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)g.s * a.CO + ch0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 b4 = __ldg(bs + q);
+                        v[4 * q] += b4.x;
+                        v[4 * q + 1] += b4.y;
+                        v[4 * q + 2] += b4.z;
+                        v[4 * q + 3] += b4.w;
+                    }
+                    if (pv) {
+                        if (a.res) {
+                            const uint4* rp = reinterpret_cast<const uint4*>(a.res + so + rowoff + ch0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint4 r4 = __ldg(rp + q);
+                                const uint32_t w4[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
+                                    v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+                                }
+                            }
+                        }
+                        uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            float z[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) z[e] = a.relu ? fmaxf(v[8 * q + e], 0.0f) : v[8 * q + e];
+                            op[q] = make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]),
+                                               pack_bf16x2(z[4], z[5]), pack_bf16x2(z[6], z[7]));
+                        }
+                    }
+                } else {
+                    if (pv) {
+                        if (a.addsrc) {
+                            const uint4* ap = reinterpret_cast<const uint4*>(a.addsrc + so + rowoff + ch0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint4 r4 = ap[q];
+                                const uint32_t w4[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
+                                    v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+                                }
+                            }
+                        }
+                        if (a.mask) {
+                            const uint4* mp = reinterpret_cast<const uint4*>(a.mask + so + rowoff + ch0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const uint4 m4 = __ldg(mp + q);
+                                const uint32_t w4[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    if (!(__uint_as_float(w4[e] << 16) > 0.0f)) v[8 * q + 2 * e] = 0.0f;
+                                    if (!(__uint_as_float(w4[e] & 0xFFFF0000u) > 0.0f)) v[8 * q + 2 * e + 1] = 0.0f;
+                                }
+                            }
+                        }
+                        uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            op[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                                               pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
+                                               pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+                    }
+                    if (a.bpart) {  // fp32 bias partials (pre-rounding) over the tile's 128 pixels
+                        float* red = bred + (nred++ & 1) * 128;
+                        red[warp * 32 + lane] = warp_transpose_sum(v, lane);
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (warp == 0)
+                            a.bpart[(int64_t)g.s * a.bpart_stride_s + (int64_t)(g.cls * ptiles + g.ptile) * a.C +
+                                    ch0 + lane] = (red[lane] + red[32 + lane]) + (red[64 + lane] + red[96 + lane]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kEpiWarps + kGatherWarps + 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+int conv2_dgrad_parts(const Conv2Args& a) {
+    const int P = a.B * (a.H / a.stride) * (a.W / a.stride);
+    return a.stride * a.stride * ((P + 127) / 128);
+}
+
+template <int MODE>
+static void launch_conv2(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a,
+                         cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(conv2_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2::kSmem);
+        attr = true;
+    }
+    const int ncls = MODE == 1 ? a.stride * a.stride : 1;
+    const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
+    const int P = a.B * PH * PW;
+    const int Ntot = MODE == 0 ? a.CO : a.C;
+    const int T = a.S * ncls * ((P + 127) / 128) * ((Ntot + a.n_tile - 1) / a.n_tile);
+    const int grid = std::min(T, kNumSMs);
+    conv2_kernel<MODE><<<grid, c2::kThreads, c2::kSmem, st>>>(amap, wmap, a);
+}
+
+void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st) {
+    launch_conv2<0>(amap, wmap, a, st);
+}
+void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st) {
+    launch_conv2<1>(amap, wmap, a, st);
+}
+
+// ============================================================================ wgrad
+namespace w2 {
+constexpr int kEpiWarps = 8;
+constexpr int kGatherWarps = 4;
+constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
+constexpr int kStages = 4;
+constexpr int kAStage = 64 * 128 * 2;  // dYᵀ: 64 pixels × 128 co (two 64-wide MN blocks)
+constexpr int kBStage = 64 * 256 * 2;  // X windows: 64 pixels × up to 4 × 64 parameter columns
+constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
+}  // namespace w2
+
+// Persistent: unit u = (((s·nsplit + split)·co_tiles + ct)·ntiles + nt); neighbouring CTAs share
+// (s, split) so the dY and X blocks they read are L2 hits. D[co][col] accumulates in TMEM
+// (two 256-column buffers: unit i's store overlaps unit i+1's main loop).
+__global__ void __launch_bounds__(w2::kThreads, 1)
+    conv2_wgrad_kernel(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap xmap,
+                       const ConvWgradArgs a) {
+    using namespace w2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kAStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = bars + 2 * kStages + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Kt = a.k * a.k * a.C;
+    const int ntiles = Kt / a.n_tile, co_tiles = (a.CO + 127) / 128;
+    const int nb = a.n_tile / 64;
+    const int npix = a.B * a.OH * a.OW;
+    const int nblk_all = (npix + 63) / 64;
+    const int per = (nblk_all + a.nsplit - 1) / a.nsplit;
+    const int T = a.S * a.nsplit * co_tiles * ntiles;
+    struct U {
+        int s, split, ct, nt, blk0, nblk;
+    };
+    auto unit = [&](int t) {
+        U u;
+        u.nt = t % ntiles;
+        t /= ntiles;
+        u.ct = t % co_tiles;
+        t /= co_tiles;
+        u.split = t % a.nsplit;
+        u.s = t / a.nsplit;
+        u.blk0 = u.split * per;
+        u.nblk = max(0, min(nblk_all, u.blk0 + per) - u.blk0);
+        return u;
+    };
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], a.tma_b ? 1 : kGatherWarps * 32 + 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kEpiWarps);
+        }
+        mbar_fence_init();
+    }
+    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == kEpiWarps + kGatherWarps) {
+        // ------------------------------------------------ TMA: dYᵀ blocks (+ X windows, stride 1)
+        if (lane == 0) {
+            tma_prefetch_desc(&gmap);
+            if (a.tma_b) tma_prefetch_desc(&xmap);
+            const uint32_t bytes = kAStage + (a.tma_b ? nb * 8192 : 0);
+            int it = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+                const U u = unit(t);
+                const int co0 = u.ct * 128;
+                for (int b = 0; b < u.nblk; ++b, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[st], bytes);
+                    uint8_t* dst = sA + st * kAStage;
+                    const int pix0 = (u.blk0 + b) * 64;
+                    tma_load_3d(&gmap, &full[st], dst, co0, pix0, u.s);
+                    tma_load_3d(&gmap, &full[st], dst + 8192, co0 + 64, pix0, u.s);
+                    if (a.tma_b) {
+                        const int n0 = pix0 / (a.OH * a.OW), y0 = (pix0 - n0 * a.OH * a.OW) / a.OW;
+                        for (int j = 0; j < nb; ++j) {
+                            const int col = u.nt * a.n_tile + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
+                            const int kh = tap / a.k, kw = tap - kh * a.k;
+                            tma_load_5d(&xmap, &full[st], sB + st * kBStage + j * 8192, ci0, kw - a.pad,
+                                        y0 + kh - a.pad, n0, a.X_stride_s == 0 ? 0 : u.s);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kEpiWarps + kGatherWarps + 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, a.n_tile, 1, 1);
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
+                const U u = unit(t);
+                const int buf = tl & 1;
+                mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + buf * 256;
+                for (int b = 0; b < u.nblk; ++b, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait_sleep(&full[st], ph);
+                    fence_proxy_async_smem();
+                    tc_fence_after();
+                    const uint32_t aBase = smem_u32(sA + st * kAStage);
+                    const uint32_t bBase = smem_u32(sB + st * kBStage);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t ad = sdesc_sw128(aBase + 2048 * q, 8192, 1024);
+                        const uint64_t bd = sdesc_sw128(bBase + 2048 * q, 8192, 1024);
+                        mma_bf16(d, ad, bd, idesc, (b | q) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= kEpiWarps) {
+        // ------------------------------------------------ gather X windows (stride 2): 64 rows × nb × 8 chunks
+        if (!a.tma_b) {
+            const int gt = threadIdx.x - kEpiWarps * 32;  // 0..127
+            int it = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+                const U u = unit(t);
+                const __nv_bfloat16* xs = a.X + u.s * a.X_stride_s;
+                for (int b = 0; b < u.nblk; ++b, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait(&empty[st], ph ^ 1);
+                    const uint32_t base = smem_u32(sB + st * kBStage);
+                    for (int idx = gt; idx < nb * 512; idx += 128) {
+                        const int j = idx >> 9, r = (idx >> 3) & 63, ch = idx & 7;
+                        const int col = u.nt * a.n_tile + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
+                        const int kh = tap / a.k, kw = tap - kh * a.k;
+                        const int pix = (u.blk0 + b) * 64 + r;
+                        const __nv_bfloat16* g = xs;
+                        uint32_t bytes = 0;
+                        if (pix < npix) {
+                            const int n = pix / (a.OH * a.OW), rem = pix - n * (a.OH * a.OW);
+                            const int iy = (rem / a.OW) * a.stride + kh - a.pad;
+                            const int ix = (rem % a.OW) * a.stride + kw - a.pad;
+                            if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+                                g = xs + (((int64_t)n * a.H + iy) * a.W + ix) * a.C_pad + ci0 + 8 * ch;
+                                bytes = 16;
+                            }
+                        }
+                        cp_async16(base + j * 8192 + r * 128 + ((ch ^ (r & 7)) << 4), g, bytes);
+                    }
+                    cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue: TMEM → fp32 per-sample partials
+        const int q = warp & 3, h = warp >> 2;
+        const int half = a.n_tile / 2;
+        int tl = 0;
+        for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
+            const U u = unit(t);
+            const int buf = tl & 1;
+            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            tc_fence_after();
+            const int co = u.ct * 128 + 32 * q + lane;
+            float* out = a.part + ((int64_t)(u.s * a.nsplit + u.split) * a.CO + co) * Kt + u.nt * a.n_tile + h * half;
+            for (int c = 0; c < half / 32; ++c) {
+                float v[32];
+                __syncwarp();
+                if (u.nblk > 0) {
+                    tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + h * half + 32 * c, v);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+                }
+                if (co < a.CO) {
+                    float4* o4 = reinterpret_cast<float4*>(out + 32 * c);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) o4[g] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kEpiWarps + kGatherWarps + 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+int conv2_wgrad_ntile(int Kt) {
+    for (int n : {256, 192, 128, 64})
+        if (Kt % n == 0) return n;
+    return 0;
+}
+
+void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
+                        cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(conv2_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, w2::kSmem);
+        attr = true;
+    }
+    const int Kt = a.k * a.k * a.C;
+    const int T = a.S * a.nsplit * ((a.CO + 127) / 128) * (Kt / a.n_tile);
+    conv2_wgrad_kernel<<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, a);
+}
+
+// Phase 2: thread = four consecutive parameter columns of one row; fixed summation order
+// (splits, then samples) ⇒ deterministic. ε_s is the same EPS-v1 draw as the forward's W_s.
+__global__ void wgrad_eps_combine_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int Kt,
+                                         const float* __restrict__ part, float scale,
+                                         float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
+    const int kq = Kt / 4;
+    const int64_t nq = (int64_t)CO * kq;
+    const int64_t ss = (int64_t)CO * Kt;  // one split of one sample
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+        const int co = (int)(i / kq), cq = (int)(i - (int64_t)co * kq);
+        const float* p = part + (int64_t)co * Kt + 4 * cq;
+        float4 m = make_float4(0.f, 0.f, 0.f, 0.f), r = m;
+        for (int s = 0; s < S; ++s) {
+            float4 d = __ldcs(reinterpret_cast<const float4*>(p + (int64_t)s * nsplit * ss));
+            for (int sp = 1; sp < nsplit; ++sp) {
+                const float4 e = __ldcs(reinterpret_cast<const float4*>(p + ((int64_t)s * nsplit + sp) * ss));
+                d.x += e.x;
+                d.y += e.y;
+                d.z += e.z;
+                d.w += e.w;
+            }
+            const float4 e = eps4(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)cq);
+            m.x += d.x;
+            m.y += d.y;
+            m.z += d.z;
+            m.w += d.w;
+            r.x = fmaf(d.x, e.x, r.x);
+            r.y = fmaf(d.y, e.y, r.y);
+            r.z = fmaf(d.z, e.z, r.z);
+            r.w = fmaf(d.w, e.w, r.w);
+        }
+        float4* am = reinterpret_cast<float4*>(acc_mu + L.off_w + (int64_t)co * Kt + 4 * cq);
+        float4* ar = reinterpret_cast<float4*>(acc_rho + L.off_w + (int64_t)co * Kt + 4 * cq);
+        float4 x = *am, y = *ar;
+        x.x = fmaf(scale, m.x, x.x);
+        x.y = fmaf(scale, m.y, x.y);
+        x.z = fmaf(scale, m.z, x.z);
+        x.w = fmaf(scale, m.w, x.w);
+        y.x = fmaf(scale, r.x, y.x);
+        y.y = fmaf(scale, r.y, y.y);
+        y.z = fmaf(scale, r.z, y.z);
+        y.w = fmaf(scale, r.w, y.w);
+        *am = x;
+        *ar = y;
+    }
+}
+
+void launch_wgrad_eps_combine(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO, int Kt,
+                              const float* part, float scale, float* acc_mu, float* acc_rho, cudaStream_t st) {
+    const int64_t nq = (int64_t)CO * Kt / 4;
+    const int grid = (int)std::min<int64_t>((nq + 255) / 256, (int64_t)kNumSMs * 8);
+    wgrad_eps_combine_kernel<<<std::max(grid, 1), 256, 0, st>>>(L, kk, S, nsplit, CO, Kt, part, scale, acc_mu,
+                                                                acc_rho);
+}
+
+}  // namespace bnn

@@ -25,7 +25,16 @@ using namespace ptx;
 
 // ============================================================================ W scratch
 __global__ void gen_wscratch_kernel(SampledLayer L, SampleKeys kk, int S, int C, int C_pad,
-                                    int taps, int K_pad, __nv_bfloat16* __restrict__ out) {
+                                    int taps, int K_pad, __nv_bfloat16* __restrict__ out,
+                                    float* __restrict__ bias_out) {
+    if (bias_out) {  // sampled biases b_s = fma(σ, ε_s, μ) in fp32, [S][N]
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)S * L.N;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int s = (int)(i / L.N), n = (int)(i % L.N);
+            bias_out[i] = __fmaf_rn(L.sigma[L.off_b + n], eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0u, (uint32_t)n),
+                                    L.mu[L.off_b + n]);
+        }
+    }
     const int64_t quads_per_sample = (int64_t)L.N * K_pad / 4;
     const int64_t total = quads_per_sample * S;
     const int Kt = L.K;  // = taps·C
@@ -67,10 +76,10 @@ __global__ void gen_wscratch_kernel(SampledLayer L, SampleKeys kk, int S, int C,
 }
 
 void launch_gen_wscratch(const SampledLayer& L, const SampleKeys& kk, int S, int C, int C_pad,
-                         int taps, int K_pad, __nv_bfloat16* out, cudaStream_t st) {
+                         int taps, int K_pad, __nv_bfloat16* out, float* bias_out, cudaStream_t st) {
     const int64_t total = (int64_t)S * L.N * K_pad / 4;
     const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
-    gen_wscratch_kernel<<<std::max(grid, 1), 256, 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out);
+    gen_wscratch_kernel<<<std::max(grid, 1), 256, 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out, bias_out);
 }
 
 // ============================================================================ fwd / dgrad

@@ -572,13 +572,30 @@ void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B,
 __global__ void bias_reduce_kernel(SampledLayer L, SampleKeys kk, const float* __restrict__ parts,
                                    int nparts, int ldp, int64_t strideS, int S,
                                    float* __restrict__ db) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x, s = blockIdx.y;
-    if (n >= L.N) return;
-    const float* p = parts + s * strideS + n;
+    __shared__ float red[8][33];
+    const int tx = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + tx, s = blockIdx.y;
     float acc = 0.0f;
-    for (int i = 0; i < nparts; ++i) acc += p[(int64_t)i * ldp];
-    db[(int64_t)s * L.N + n] = acc;
-    db[(int64_t)(S + s) * L.N + n] = acc * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n);
+    if (n < L.N) {  // group g: parts g, g+8, … (fixed order ⇒ deterministic)
+        const float* p = parts + s * strideS + n;
+        float a0 = 0.0f, a1 = 0.0f;
+        int i = g;
+        for (; i + 8 < nparts; i += 16) {
+            a0 += __ldg(p + (int64_t)i * ldp);
+            a1 += __ldg(p + (int64_t)(i + 8) * ldp);
+        }
+        if (i < nparts) a0 += __ldg(p + (int64_t)i * ldp);
+        acc = a0 + a1;
+    }
+    red[g][tx] = acc;
+    __syncthreads();
+    if (g == 0 && n < L.N) {
+        float t = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t += red[j][tx];
+        db[(int64_t)s * L.N + n] = t;
+        db[(int64_t)(S + s) * L.N + n] = t * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n);
+    }
 }
 
 // phase B: 32 features × 8 sample groups per block, fixed-order smem combine (deterministic)
@@ -610,8 +627,8 @@ __global__ void bias_acc_kernel(SampledLayer L, int S, const float* __restrict__
 void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
                       int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
                       float* acc_mu, float* acc_rho, cudaStream_t st) {
-    dim3 grid((L.N + 127) / 128, S);
-    bias_reduce_kernel<<<grid, 128, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
+    dim3 grid((L.N + 31) / 32, S);
+    bias_reduce_kernel<<<grid, 256, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
     bias_acc_kernel<<<(L.N + 31) / 32, 256, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
 }
 

@@ -55,7 +55,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         if (i != 0 && !c->alloc(&b.grad, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (gradients)");
         if (i != 0 && i != gbuf) {
             const int64_t npix = (int64_t)B * R.H * R.W;
-            b.bpart_cap = (int64_t)(4 * ((npix + 255) / 256) * 2 + B) * R.C;
+            b.bpart_cap = (int64_t)(4 * ((npix + 127) / 128) * 4 + B) * R.C;
             if (!c->alloc(&b.bpart, (size_t)Sc * b.bpart_cap)) return c->set_err(BNN_ERR_CUDA, "out of memory");
         }
     }
@@ -73,6 +73,11 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->cmap_bf.resize(L);
     c->cmap_bd.resize(L);
     c->cmap_xw.resize(L);
+    c->cmap_a2f.resize(L);
+    c->cmap_a2d.resize(L);
+    c->cmap_w2.resize(L);
+    c->tma_a2f.assign(L, 0);
+    c->tma_a2d.assign(L, 0);
     c->tma_fwd.assign(L, 0);
     c->tma_dgrad.assign(L, 0);
     c->tma_wgrad.assign(L, 0);
@@ -88,10 +93,14 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         maxN = std::max(maxN, Ld.cout);
         const RBuf& D = c->rbufs[op.dst];
         const int64_t npix = (int64_t)B * D.H * D.W;
-        if (Ld.cin % 64 == 0) {
-            const int tiles = ((Ld.cout + 127) / 128) * taps * (Ld.cin / 64);
+        if (Ld.cin % 64 == 0) {  // conv2 wgrad: units = samples × splits × co tiles × column tiles
+            const int Kt = taps * Ld.cin;
+            const int units = Sc * ((Ld.cout + 127) / 128) * (Kt / conv2_wgrad_ntile(Kt));
             const int blocks = (int)((npix + 63) / 64);
-            c->nsplit[op.layer] = std::max(1, std::min(blocks, (2 * bnn::kNumSMs) / tiles));
+            c->nsplit[op.layer] = std::max(1, std::min(blocks, (2 * bnn::kNumSMs + units - 1) / units));
+            if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
+            pmax = std::max(pmax, (size_t)Sc * c->nsplit[op.layer] * Ld.cout * Kt);
+            continue;
         } else {  // SIMT wgrad (the stem): split pixels so ≥ 2 waves of CTAs exist
             const int tiles = (int)(((int64_t)taps * Ld.cin + 63) / 64) * ((Ld.cout + 63) / 64);
             c->nsplit[op.layer] = (int)std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256,
@@ -100,6 +109,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
     }
     if (!c->alloc(&c->wscr, wmax) || !c->alloc(&c->wpart, std::max<size_t>(pmax, 1)) ||
+        !c->alloc(&c->bias_scr, (size_t)Sc * 512) ||
         !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)))
         return c->set_err(BNN_ERR_CUDA, "out of memory (scratch)");
     for (const ROp& op : c->rops) {
@@ -112,6 +122,9 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const uint32_t box[3] = {64, 128, 1};
             if (!make_map_nd(&c->cmap_w[op.layer], c->wscr, 3, dims, str, box))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch) failed");
+            const uint32_t box2[3] = {64, (uint32_t)std::min(CO, 256), 1};
+            if (!make_map_nd(&c->cmap_w2[op.layer], c->wscr, 3, dims, str, box2))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch, conv2) failed");
         }
         if (Ld.cin % 64 == 0) {
             const uint64_t dims[4] = {(uint64_t)Ld.cin, (uint64_t)taps, (uint64_t)CO, (uint64_t)Sc};
@@ -174,6 +187,40 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_dgrad[op.layer] = 1;
         }
     }
+    // conv2: 128-pixel windows for the A operand of stride-1 layers
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op)) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        if (Ld.stride != 1) continue;
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        const int PW = Db.W, PH = Db.H;
+        if (128 % PW != 0) continue;
+        const int th = std::min(PH, 128 / PW);
+        if (PH % th != 0) continue;
+        const int tn = 128 / (PW * th);
+        const uint32_t box[5] = {64, (uint32_t)PW, (uint32_t)th, (uint32_t)tn, 1};
+        const int Cp = c->rbf[op.src].C_pad;
+        if (Cp % 64 == 0) {
+            const bool shared = op.src == 0 && c->cfg.aug != BNN_AUG_PER_SAMPLE;
+            const uint64_t dims[5] = {(uint64_t)Cp, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B,
+                                      (uint64_t)(shared ? 1 : Sc)};
+            const uint64_t str[4] = {(uint64_t)Cp * 2, (uint64_t)Sb.W * Cp * 2, (uint64_t)Sb.H * Sb.W * Cp * 2,
+                                     (uint64_t)B * Sb.H * Sb.W * Cp * 2};
+            if (!make_map_nd(&c->cmap_a2f[op.layer], c->rbf[op.src].val, 5, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (conv2 activation window) failed");
+            c->tma_a2f[op.layer] = 1;
+        }
+        if (op.src != 0 && Db.C % 64 == 0 && Ld.cin % 64 == 0) {
+            const int gb = grad_src_buffer(c, op.dst);
+            const uint64_t dims[5] = {(uint64_t)Db.C, (uint64_t)Db.W, (uint64_t)Db.H, (uint64_t)B, (uint64_t)Sc};
+            const uint64_t str[4] = {(uint64_t)Db.C * 2, (uint64_t)Db.W * Db.C * 2,
+                                     (uint64_t)Db.H * Db.W * Db.C * 2, (uint64_t)B * Db.H * Db.W * Db.C * 2};
+            if (!make_map_nd(&c->cmap_a2d[op.layer], c->rbf[gb].grad, 5, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (conv2 dY window) failed");
+            c->tma_a2d[op.layer] = 1;
+        }
+    }
     // head: pooled features [S][B][Cf] → logits, with the MLP kernels' descriptors
     const int Cf = c->rbufs[gbuf].C, ldO = (int)round_up(O, 8);
     c->map_fwdB.resize(1);
@@ -232,11 +279,10 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         const RBuf& Db = c->rbufs[op.dst];
         const int Cp = c->rbf[op.src].C_pad;
         c->launch("wgen", [&] {
-            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr, st);
+            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr, c->bias_scr, st);
         });
-        ConvTcArgs a{};
-        a.L = sl;
-        a.kk = kk;
+        Conv2Args a{};
+        a.S = Sc;
         a.B = B;
         a.H = Sb.H;
         a.W = Sb.W;
@@ -249,17 +295,16 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         a.stride = Ld.stride;
         a.pad = Ld.pad;
         a.K_pad = c->kpad[op.layer];
+        a.n_tile = std::min(Db.C, 256);
+        a.tma_a = c->tma_a2f[op.layer];
         a.src = c->rbf[op.src].val;
         a.src_stride_s = op.src == 0 ? in_stride : (int64_t)B * Sb.H * Sb.W * Cp;
         a.out = c->rbf[op.dst].val;
         a.out_stride_s = (int64_t)B * Db.H * Db.W * Db.C;
-        if (op.res >= 0) {
-            a.res = c->rbf[op.res].val;
-            a.res_stride_s = a.out_stride_s;
-        }
+        a.bias = c->bias_scr;
+        a.res = op.res >= 0 ? c->rbf[op.res].val : nullptr;
         a.relu = op.relu;
-        a.tma_b = c->tma_fwd[op.layer];
-        c->launch("fwd", [&] { launch_conv_tc_fwd(c->cmap_w[op.layer], c->cmap_bf[op.layer], a, Sc, st); });
+        c->launch("fwd", [&] { launch_conv2_fwd(c->cmap_a2f[op.layer], c->cmap_w2[op.layer], a, st); });
     }
 }
 
@@ -377,9 +422,12 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.part = c->wpart;
             w.nsplit = c->nsplit[op.layer];
             w.tma_b = c->tma_wgrad[op.layer];
-            c->launch("wgrad", [&] { launch_conv_tc_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
-            const int64_t n = (int64_t)Ld.cout * Ld.k * Ld.k * Ld.cin;
-            c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, w.nsplit, n, Ld.off_w, acc_mu, acc_rho, st); });
+            w.n_tile = conv2_wgrad_ntile(Ld.k * Ld.k * Ld.cin);
+            c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
+            c->launch("wgrad", [&] {
+                launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Ld.k * Ld.k * Ld.cin, c->wpart, scale, acc_mu,
+                                         acc_rho, st);
+            });
         } else {
             ConvShape cs{B, Sb.H, Sb.W, Sb.C, Db.H, Db.W, Db.C, Ld.k, Ld.stride, Ld.pad};
             const int nsp = c->nsplit[op.layer];
@@ -401,11 +449,11 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         remaining[op.src]--;
         const bool final = remaining[op.src] == 0;
         c->launch("wgen", [&] {
-            launch_gen_wscratch(sl, kk, Sc, Ld.cin, c->rbf[op.src].C_pad, Ld.k * Ld.k, c->kpad[op.layer], c->wscr, st);
+            launch_gen_wscratch(sl, kk, Sc, Ld.cin, c->rbf[op.src].C_pad, Ld.k * Ld.k, c->kpad[op.layer], c->wscr,
+                                nullptr, st);
         });
-        ConvTcArgs a{};
-        a.L = sl;
-        a.kk = kk;
+        Conv2Args a{};
+        a.S = Sc;
         a.B = B;
         a.H = Sb.H;
         a.W = Sb.W;
@@ -418,23 +466,22 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         a.stride = Ld.stride;
         a.pad = Ld.pad;
         a.K_pad = c->kpad[op.layer];
+        a.n_tile = std::min(Sb.C, 256);
+        a.tma_a = c->tma_a2d[op.layer];
         a.src = G.grad;
         a.src_stride_s = npix_out * Db.C;
         a.out = c->rbf[op.src].grad;
         a.out_stride_s = (int64_t)B * Sb.H * Sb.W * Sb.C;
         if (final) {
             a.addsrc = pending[op.src];
-            a.addsrc_stride_s = a.out_stride_s;
             a.mask = c->rbf[op.src].val;
-            a.mask_stride_s = a.out_stride_s;
             a.bpart = c->rbf[op.src].bpart;
-            a.bpart_stride_s = (int64_t)conv_dgrad_parts(a) * Sb.C;
-            if (conv_dgrad_parts(a) * Sb.C > c->rbf[op.src].bpart_cap)
+            a.bpart_stride_s = (int64_t)conv2_dgrad_parts(a) * Sb.C;
+            if (conv2_dgrad_parts(a) * Sb.C > c->rbf[op.src].bpart_cap)
                 return c->set_err(BNN_ERR_CONFIG, "bias partial buffer too small");
-            c->rbf[op.src].nparts = conv_dgrad_parts(a);
+            c->rbf[op.src].nparts = conv2_dgrad_parts(a);
         }
-        a.tma_b = c->tma_dgrad[op.layer];
-        c->launch("dgrad", [&] { launch_conv_tc_dgrad(c->cmap_wT[op.layer], c->cmap_bd[op.layer], a, Sc, st); });
+        c->launch("dgrad", [&] { launch_conv2_dgrad(c->cmap_a2d[op.layer], c->cmap_wT[op.layer], a, st); });
         if (!final) pending[op.src] = c->rbf[op.src].grad;
     }
     c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
