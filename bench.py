@@ -287,7 +287,7 @@ def run_ours(args, world, rank, local_rank):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
-                "config": {"workload": f"{args.config}: Bayesian MLP 784-1024-1024-10 (CE)",
+                "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
                            "global_batch": B, "samples": S, "samples_per_gpu": S_loc,
                            "params": P, "parallelism": f"sample-sharded x{world}",
                            "l2": "flushed between timed steps (256 MiB memset outside events)"},

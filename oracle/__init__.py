@@ -242,3 +242,20 @@ def layer_grad(model, mu, rho, x, y_cls, y_reg, b, s, seed, step, layer, aug=AUG
                          1 if emu else 0, layer, _p(out))
     assert n > 0, n
     return out[:n]
+
+
+def layer_dump(model, mu, rho, x, y_cls, y_reg, b, s, seed, step, aug=AUG_NONE, emu=False, grad=False):
+    """All layers' stored outputs (grad=False) or unscaled dℓ/d(stored output) (grad=True) for
+    example b, sample s, concatenated in layer order (test hook; one pass for all layers)."""
+    m = model_struct(model)
+    L = lib()
+    L.orc_layer_dump.restype = C.c_long
+    L.orc_layer_dump.argtypes = [C.c_void_p] * 6 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32] + \
+        [C.c_int] * 3 + [C.c_void_p]
+    mu, rho, x, yr = _d(mu), _d(rho), _d(x), _d(y_reg)
+    yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
+    out = np.zeros(1 << 23)
+    n = L.orc_layer_dump(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), b, s, seed, step, aug,
+                         1 if emu else 0, 1 if grad else 0, _p(out))
+    assert n > 0, n
+    return out[:n]

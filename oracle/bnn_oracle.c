@@ -934,3 +934,45 @@ long orc_layer_grad(const orc_model* m, const double* mu, const double* rho, con
     free(w.pool); free(sigma); free(W); free(dW); free(tmp);
     return cnt;
 }
+
+/* Test hook: for example b under sample s, every layer's stored output (grad = 0) or the
+ * unscaled dℓ/d(stored output) after a full backward pass (grad = 1), concatenated in layer
+ * order — one forward (and backward) pass for all layers. Returns the element count. */
+long orc_layer_dump(const orc_model* m, const double* mu, const double* rho, const double* x,
+                    const int* ycls, const double* yreg, int b, int s, uint64_t seed, uint32_t step,
+                    int aug, int emu, int grad, double* out)
+{
+    ONet net;
+    if (build_net(m, &net)) return -1;
+    ONet* n = &net;
+    long P = n->n_params;
+    double* sigma = (double*)malloc(sizeof(double) * P);
+    double* W = (double*)malloc(sizeof(double) * P);
+    double* dW = (double*)calloc((size_t)P, sizeof(double));
+    long maxbuf = 0;
+    for (int q = 0; q < n->n_bufs; ++q) if (buf_size(n, q) > maxbuf) maxbuf = buf_size(n, q);
+    double* tmp = (double*)malloc(sizeof(double) * (size_t)maxbuf);
+    OWork w;
+    if (!sigma || !W || !dW || !tmp || work_alloc(n, &w, 1)) return -2;
+    for (long i = 0; i < P; ++i) sigma[i] = softplus(rho[i]);
+    sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, emu);
+    load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w.val[0]);
+    int outb = forward_one(n, W, &w, emu);
+    if (grad) {
+        double dz[4096];
+        loss_one(n, w.val[outb], ycls, yreg, b, dz);
+        for (int k = 0; k < n->n_out; ++k) w.grad[outb][k] = dz[k];
+        backward_one(n, W, &w, dW, 1.0, emu, tmp);
+    }
+    long cnt = 0;
+    for (int l = 0; l < n->n_layers; ++l)
+        for (int i = 0; i < n->n_ops; ++i)
+            if (n->ops[i].type == OP_CONV && n->ops[i].layer == l) {
+                int d = n->ops[i].dst;
+                long sz = buf_size(n, d);
+                memcpy(out + cnt, grad ? w.grad[d] : w.val[d], sizeof(double) * (size_t)sz);
+                cnt += sz;
+            }
+    free(w.pool); free(sigma); free(W); free(dW); free(tmp);
+    return cnt;
+}

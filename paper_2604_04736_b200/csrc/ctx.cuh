@@ -146,7 +146,8 @@ struct bnn_ctx {
         int64_t bpart_cap = 0;
     };
     std::vector<RBf> rbf;
-    __nv_bfloat16* wscr = nullptr;  // W_s scratch of one layer for the sample chunk
+    __nv_bfloat16* wscr = nullptr;  // W_s scratch of every conv layer for the sample chunk
+    std::vector<size_t> wscr_off;   // per layer: element offset of its slot (forward writes, dgrad reads)
     float* wpart = nullptr;         // conv wgrad split partials
     std::vector<int> kpad, nsplit;  // per layer
     std::vector<CUtensorMap> cmap_w, cmap_wT, cmap_g;  // per layer

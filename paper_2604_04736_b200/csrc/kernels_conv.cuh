@@ -129,7 +129,13 @@ void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const 
 void launch_wgrad_eps_combine(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO,
                               int Kt, const float* part, float scale, float* acc_mu, float* acc_rho,
                               cudaStream_t st);
+void launch_wgrad_eps_combine_stem(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO, int taps,
+                                   int C, int Ktp, const float* part, float scale, float* acc_mu, float* acc_rho,
+                                   cudaStream_t st);
 int conv2_wgrad_ntile(int Kt);
+int conv2_wgrad_nsplit(int base, int blocks);
+// partial columns: taps·C, or (stem, C_pad < 64) ⌈taps/8⌉·64
+inline int conv2_wgrad_cols(int taps, int C, int C_pad) { return C_pad < 64 ? ((taps + 7) / 8) * 64 : taps * C; }
 
 // image-path helpers on bf16 NHWC buffers
 void launch_input_bf16(const float* x, int S, int B, int H, int W, int C, int C_pad, int aug,

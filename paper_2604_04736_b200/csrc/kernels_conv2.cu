@@ -423,6 +423,12 @@ void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const 
 }
 
 // ============================================================================ wgrad
+// parameter columns of the partials: tap·C + ci, or for the stem (C_pad < 64) the padded
+// 8-taps × 8-channels blocks of the forward's K layout (tap·8 + ci, rounded up to 64)
+__host__ __device__ inline int conv2_wgrad_cols(const ConvWgradArgs& a) {
+    return a.C_pad < 64 ? ((a.k * a.k + 7) / 8) * 64 : a.k * a.k * a.C;  // = conv2_wgrad_cols(taps, C, C_pad)
+}
+
 namespace w2 {
 constexpr int kEpiWarps = 8;
 constexpr int kGatherWarps = 4;
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int Kt = a.k * a.k * a.C;
+    const int Kt = conv2_wgrad_cols(a);
     const int ntiles = Kt / a.n_tile, co_tiles = (a.CO + 127) / 128;
     const int nb = a.n_tile / 64;
     const int npix = a.B * a.OH * a.OW;
@@ -557,35 +563,58 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         }
         __syncwarp();
     } else if (warp >= kEpiWarps) {
-        // ------------------------------------------------ gather X windows (stride 2): 64 rows × nb × 8 chunks
+        // ------------------------------------------------ gather X windows (stride 2 / stem)
+        // thread: 16-byte chunk ch of pixel rows r0 + 16·i; index math hoisted per unit / k-step
         if (!a.tma_b) {
             const int gt = threadIdx.x - kEpiWarps * 32;  // 0..127
+            const int ch = gt & 7, r0 = gt >> 3;
+            const bool stem = a.C_pad < 64;  // 64 columns = 8 taps × 8 (padded) channels
+            const int OHW = a.OH * a.OW;
             int it = 0;
             for (int t = blockIdx.x; t < T; t += gridDim.x) {
                 const U u = unit(t);
                 const __nv_bfloat16* xs = a.X + u.s * a.X_stride_s;
+                int ky[4], kx[4], co_[4];
+                for (int j = 0; j < nb; ++j) {
+                    const int cb = u.nt * nb + j;
+                    int tap, c0;
+                    if (stem) {
+                        tap = cb * 8 + ch;
+                        c0 = 0;
+                    } else {
+                        tap = (cb * 64) / a.C;
+                        c0 = cb * 64 - tap * a.C + 8 * ch;
+                    }
+                    const int kh = tap / a.k;
+                    ky[j] = tap < a.k * a.k ? kh - a.pad : -(1 << 20);  // invalid tap: always OOB
+                    kx[j] = tap - kh * a.k - a.pad;
+                    co_[j] = c0;
+                }
                 for (int b = 0; b < u.nblk; ++b, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
+                    int iy0[4], ix0[4];
+                    int64_t nb0[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int pix = (u.blk0 + b) * 64 + r0 + 16 * i;
+                        const int n = pix / OHW, rem = pix - n * OHW;
+                        const int oy = rem / a.OW;
+                        iy0[i] = pix < npix ? oy * a.stride : -(1 << 20);
+                        ix0[i] = (rem - oy * a.OW) * a.stride;
+                        nb0[i] = (int64_t)n * a.H;
+                    }
                     mbar_wait(&empty[st], ph ^ 1);
-                    const uint32_t base = smem_u32(sB + st * kBStage);
-                    for (int idx = gt; idx < nb * 512; idx += 128) {
-                        const int j = idx >> 9, r = (idx >> 3) & 63, ch = idx & 7;
-                        const int col = u.nt * a.n_tile + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
-                        const int kh = tap / a.k, kw = tap - kh * a.k;
-                        const int pix = (u.blk0 + b) * 64 + r;
-                        const __nv_bfloat16* g = xs;
-                        uint32_t bytes = 0;
-                        if (pix < npix) {
-                            const int n = pix / (a.OH * a.OW), rem = pix - n * (a.OH * a.OW);
-                            const int iy = (rem / a.OW) * a.stride + kh - a.pad;
-                            const int ix = (rem % a.OW) * a.stride + kw - a.pad;
-                            if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
-                                g = xs + (((int64_t)n * a.H + iy) * a.W + ix) * a.C_pad + ci0 + 8 * ch;
-                                bytes = 16;
-                            }
+                    const uint32_t base = smem_u32(sB + st * kBStage) + ((ch ^ (r0 & 7)) << 4) + r0 * 128;
+                    for (int j = 0; j < nb; ++j) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int iy = iy0[i] + ky[j], ix = ix0[i] + kx[j];
+                            const bool ok = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                            const __nv_bfloat16* g =
+                                ok ? xs + ((nb0[i] + iy) * a.W + ix) * a.C_pad + co_[j] : xs;
+                            cp_async16(base + j * 8192 + i * 16 * 128, g, ok ? 16u : 0u);
                         }
-                        cp_async16(base + j * 8192 + r * 128 + ((ch ^ (r & 7)) << 4), g, bytes);
                     }
                     cp_async_mbar_arrive(&full[st]);
                 }
@@ -632,6 +661,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
 }
 
 int conv2_wgrad_ntile(int Kt) {
+    if (Kt < 64) return 0;
     for (int n : {256, 192, 128, 64})
         if (Kt % n == 0) return n;
     return 0;
@@ -644,7 +674,7 @@ void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const 
         cudaFuncSetAttribute(conv2_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, w2::kSmem);
         attr = true;
     }
-    const int Kt = a.k * a.k * a.C;
+    const int Kt = conv2_wgrad_cols(a);
     const int T = a.S * a.nsplit * ((a.CO + 127) / 128) * (Kt / a.n_tile);
     conv2_wgrad_kernel<<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, a);
 }
@@ -694,6 +724,51 @@ __global__ void wgrad_eps_combine_kernel(SampledLayer L, SampleKeys kk, int S, i
         *am = x;
         *ar = y;
     }
+}
+
+// The stem: partial columns are the padded tap·8 + ci; parameter columns tap·C + ci.
+__global__ void wgrad_eps_combine_stem_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int taps,
+                                              int C, int Ktp, const float* __restrict__ part, float scale,
+                                              float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
+    const int Kt = taps * C;
+    const int64_t n = (int64_t)CO * Kt;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int co = (int)(i / Kt), col = (int)(i - (int64_t)co * Kt);
+        const int tap = col / C, pc = tap * 8 + (col - tap * C);
+        float m = 0.0f, r = 0.0f;
+        for (int s = 0; s < S; ++s) {
+            float d = 0.0f;
+            for (int sp = 0; sp < nsplit; ++sp) d += part[((int64_t)(s * nsplit + sp) * CO + co) * Ktp + pc];
+            m += d;
+            r = fmaf(d, eps1(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)col), r);
+        }
+        acc_mu[L.off_w + i] = fmaf(scale, m, acc_mu[L.off_w + i]);
+        acc_rho[L.off_w + i] = fmaf(scale, r, acc_rho[L.off_w + i]);
+    }
+}
+
+void launch_wgrad_eps_combine_stem(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO, int taps,
+                                   int C, int Ktp, const float* part, float scale, float* acc_mu, float* acc_rho,
+                                   cudaStream_t st) {
+    const int64_t n = (int64_t)CO * taps * C;
+    wgrad_eps_combine_stem_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(L, kk, S, nsplit, CO, taps, C, Ktp, part,
+                                                                          scale, acc_mu, acc_rho);
+}
+
+// nsplit for `base` units per split: fewest waves per split (persistent grid of 148), and among
+// choices within 3 % of the best, the fewest splits (each split adds partial traffic)
+int conv2_wgrad_nsplit(int base, int blocks) {
+    double best = 1e30;
+    const int hi = std::max(1, std::min(blocks, 256));
+    for (int ns = 1; ns <= hi; ++ns) {
+        const int waves = (base * ns + kNumSMs - 1) / kNumSMs;
+        best = std::min(best, (double)waves / ns);
+    }
+    for (int ns = 1; ns <= hi; ++ns) {
+        const int waves = (base * ns + kNumSMs - 1) / kNumSMs;
+        if ((double)waves / ns <= best * 1.03) return ns;
+    }
+    return hi;
 }
 
 void launch_wgrad_eps_combine(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO, int Kt,

@@ -66,6 +66,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     // per-layer geometry, scratch sizes and TMA descriptors
     const int L = (int)c->layers.size();
     c->kpad.assign(L, 0);
+    c->wscr_off.assign(L, 0);
     c->nsplit.assign(L, 1);
     c->cmap_w.resize(L);
     c->cmap_wT.resize(L);
@@ -89,15 +90,17 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         const int Cp = c->rbf[op.src].C_pad, taps = Ld.k * Ld.k;
         const int Kp = (int)round_up((int64_t)taps * Cp, 64);
         c->kpad[op.layer] = Kp;
-        wmax = std::max(wmax, (size_t)Sc * Ld.cout * Kp);
+        c->wscr_off[op.layer] = wmax;
+        wmax += round_up((int64_t)Sc * Ld.cout * Kp, 512);
         maxN = std::max(maxN, Ld.cout);
         const RBuf& D = c->rbufs[op.dst];
         const int64_t npix = (int64_t)B * D.H * D.W;
-        if (Ld.cin % 64 == 0) {  // conv2 wgrad: units = samples × splits × co tiles × column tiles
-            const int Kt = taps * Ld.cin;
-            const int units = Sc * ((Ld.cout + 127) / 128) * (Kt / conv2_wgrad_ntile(Kt));
+        const int Cp_src = c->rbf[op.src].C_pad;
+        if (Ld.cin % 64 == 0 || Cp_src == 8) {  // conv2 wgrad: units = samples × splits × co tiles × column tiles
+            const int Kt = conv2_wgrad_cols(taps, Ld.cin, Cp_src);
+            const int base = Sc * ((Ld.cout + 127) / 128) * (Kt / conv2_wgrad_ntile(Kt));
             const int blocks = (int)((npix + 63) / 64);
-            c->nsplit[op.layer] = std::max(1, std::min(blocks, (2 * bnn::kNumSMs + units - 1) / units));
+            c->nsplit[op.layer] = conv2_wgrad_nsplit(base, blocks);
             if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
             pmax = std::max(pmax, (size_t)Sc * c->nsplit[op.layer] * Ld.cout * Kt);
             continue;
@@ -120,18 +123,13 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const uint64_t dims[3] = {(uint64_t)Kp, (uint64_t)CO, (uint64_t)Sc};
             const uint64_t str[2] = {(uint64_t)Kp * 2, (uint64_t)CO * Kp * 2};
             const uint32_t box[3] = {64, 128, 1};
-            if (!make_map_nd(&c->cmap_w[op.layer], c->wscr, 3, dims, str, box))
+            if (!make_map_nd(&c->cmap_w[op.layer], c->wscr + c->wscr_off[op.layer], 3, dims, str, box))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch) failed");
             const uint32_t box2[3] = {64, (uint32_t)std::min(CO, 256), 1};
-            if (!make_map_nd(&c->cmap_w2[op.layer], c->wscr, 3, dims, str, box2))
+            if (!make_map_nd(&c->cmap_w2[op.layer], c->wscr + c->wscr_off[op.layer], 3, dims, str, box2))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch, conv2) failed");
         }
-        if (Ld.cin % 64 == 0) {
-            const uint64_t dims[4] = {(uint64_t)Ld.cin, (uint64_t)taps, (uint64_t)CO, (uint64_t)Sc};
-            const uint64_t str[3] = {(uint64_t)Ld.cin * 2, (uint64_t)Kp * 2, (uint64_t)CO * Kp * 2};
-            const uint32_t box[4] = {64, 1, 64, 1};
-            if (!make_map_nd(&c->cmap_wT[op.layer], c->wscr, 4, dims, str, box))
-                return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch transposed) failed");
+        if (Ld.cin % 64 == 0 || c->rbf[op.src].C_pad == 8) {
             const int gb = grad_src_buffer(c, op.dst);
             const RBuf& D = c->rbufs[op.dst];
             const uint64_t npix = (uint64_t)B * D.H * D.W;
@@ -140,6 +138,13 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const uint32_t gbx[3] = {64, 64, 1};
             if (!make_map_nd(&c->cmap_g[op.layer], c->rbf[gb].grad, 3, gd, gs, gbx))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (dY) failed");
+        }
+        if (Ld.cin % 64 == 0) {
+            const uint64_t dims[4] = {(uint64_t)Ld.cin, (uint64_t)taps, (uint64_t)CO, (uint64_t)Sc};
+            const uint64_t str[3] = {(uint64_t)Ld.cin * 2, (uint64_t)Kp * 2, (uint64_t)CO * Kp * 2};
+            const uint32_t box[4] = {64, 1, 64, 1};
+            if (!make_map_nd(&c->cmap_wT[op.layer], c->wscr + c->wscr_off[op.layer], 4, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch transposed) failed");
         }
     }
     // stride-1 convs: the B operand (activation / dY window) by 5-D TMA with OOB zero fill
@@ -279,7 +284,8 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         const RBuf& Db = c->rbufs[op.dst];
         const int Cp = c->rbf[op.src].C_pad;
         c->launch("wgen", [&] {
-            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr, c->bias_scr, st);
+            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr + c->wscr_off[op.layer],
+                                c->bias_scr, st);
         });
         Conv2Args a{};
         a.S = Sc;
@@ -400,7 +406,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
                              acc_mu, acc_rho, st);
         }, 2);
         // weight gradient with the sample-accumulating ε epilogue
-        if (Ld.cin % 64 == 0) {
+        if (Ld.cin % 64 == 0 || c->rbf[op.src].C_pad == 8) {
             ConvWgradArgs w{};
             w.L = sl;
             w.kk = kk;
@@ -422,12 +428,19 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.part = c->wpart;
             w.nsplit = c->nsplit[op.layer];
             w.tma_b = c->tma_wgrad[op.layer];
-            w.n_tile = conv2_wgrad_ntile(Ld.k * Ld.k * Ld.cin);
+            const int taps = Ld.k * Ld.k, Kt = conv2_wgrad_cols(taps, Ld.cin, w.C_pad);
+            w.n_tile = conv2_wgrad_ntile(Kt);
             c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
-            c->launch("wgrad", [&] {
-                launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Ld.k * Ld.k * Ld.cin, c->wpart, scale, acc_mu,
-                                         acc_rho, st);
-            });
+            if (w.C_pad < 64) {
+                c->launch("wgrad", [&] {
+                    launch_wgrad_eps_combine_stem(sl, kk, Sc, w.nsplit, Ld.cout, taps, Ld.cin, Kt, c->wpart, scale,
+                                                  acc_mu, acc_rho, st);
+                });
+            } else {
+                c->launch("wgrad", [&] {
+                    launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Kt, c->wpart, scale, acc_mu, acc_rho, st);
+                });
+            }
         } else {
             ConvShape cs{B, Sb.H, Sb.W, Sb.C, Db.H, Db.W, Db.C, Ld.k, Ld.stride, Ld.pad};
             const int nsp = c->nsplit[op.layer];
@@ -445,13 +458,9 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             pending[op.res] = G.grad;
         }
         if (op.src == 0) continue;
-        // data gradient: W_s regenerated, then the transposed implicit GEMM
+        // data gradient: the transposed implicit GEMM on the forward's W_s slot of this layer
         remaining[op.src]--;
         const bool final = remaining[op.src] == 0;
-        c->launch("wgen", [&] {
-            launch_gen_wscratch(sl, kk, Sc, Ld.cin, c->rbf[op.src].C_pad, Ld.k * Ld.k, c->kpad[op.layer], c->wscr,
-                                nullptr, st);
-        });
         Conv2Args a{};
         a.S = Sc;
         a.B = B;

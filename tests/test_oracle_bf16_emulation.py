@@ -133,3 +133,22 @@ def test_emulation_single_linear_layer_exact_case():
     assert e["L_data"] == pytest.approx(r["L_data"], rel=1e-7)
     # grad_μ: weights use RN_bf16(seed); biases the unrounded seed
     assert np.allclose(e["grad_mu"], r["grad_mu"], rtol=1e-2, atol=1e-9)
+
+
+@pytest.mark.parametrize("emu", [False, True])
+def test_layer_dump_hook_equals_per_layer_hooks(emu):
+    """The one-pass dump hook returns exactly what the per-layer hooks return."""
+    model = dict(kind="resnet18", in_h=8, in_w=8, in_c=3, n_classes=10, base_width=8, loss="ce")
+    mu, rho = synth.init_params(model, seed=4)
+    x, yc, _ = synth.make_batch(model, 2, seed=5)
+    n_layers = len(O.tensor_infos(model)) // 2
+    for grad in (False, True):
+        d = O.layer_dump(model, mu, rho, x, yc, None, 1, 2, 11, 3, aug=O.AUG_PER_SAMPLE, emu=emu, grad=grad)
+        parts = []
+        for l in range(n_layers):
+            if grad:
+                parts.append(O.layer_grad(model, mu, rho, x, yc, None, 1, 2, 11, 3, l, aug=O.AUG_PER_SAMPLE,
+                                          emu=emu))
+            else:
+                parts.append(O.layer_output(model, mu, rho, x, 1, 2, 11, 3, l, aug=O.AUG_PER_SAMPLE, emu=emu))
+        np.testing.assert_array_equal(d, np.concatenate(parts))
