@@ -153,7 +153,7 @@ struct bnn_ctx {
     std::vector<CUtensorMap> cmap_w, cmap_wT, cmap_g;  // per layer
     std::vector<CUtensorMap> cmap_bf, cmap_bd;         // per layer: 5-D activation / dY windows
     std::vector<CUtensorMap> cmap_xw;                  // per layer: wgrad X windows (64 pixels)
-    std::vector<CUtensorMap> cmap_a2f, cmap_a2d, cmap_w2;  // conv2: 128-pixel A windows, W (n_tile rows)
+    std::vector<CUtensorMap> cmap_a2f, cmap_a2d, cmap_w2, cmap_w64;  // conv2: 128-pixel A windows, W (n_tile rows)
     std::vector<char> tma_a2f, tma_a2d;
     float* bias_scr = nullptr;                         // sampled conv biases [S][max CO]
     std::vector<char> tma_fwd, tma_dgrad, tma_wgrad;   // stride-1 layers use them

@@ -66,10 +66,17 @@ struct Conv2Args {
     int relu;
     float* bpart;              // dgrad: fp32 bias partials [s][parts][C]
     int64_t bpart_stride_s;
+    int dbg;                   // timing experiments only (BNN_CONV_DEBUG); 0 in production
 };
 void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
 void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
 int conv2_dgrad_parts(const Conv2Args& a);
+// conv3: M = 128 output channels (weights: fwd W scratch K-major map, box 64 × 64; dgrad the
+// transposed 4-D map, box 64 × 1 × 64 × 1), N = 256 pixels (tma_a: 5-D 256-pixel window map,
+// else cp.async gather). For layers with ≤ 128 output channels.
+void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
+void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
+int conv3_dgrad_parts(const Conv2Args& a);
 
 struct ConvTcArgs {
     SampledLayer L;
@@ -114,6 +121,7 @@ struct ConvWgradArgs {
     int nsplit;
     int tma_b;               // stride 1: X window by 5-D TMA (xmap, box 64 × 64 pixels)
     int n_tile;              // conv2 wgrad: parameter columns per tile (64 | 128 | 192 | 256)
+    int dbg;                 // timing experiments only (BNN_CONV_DEBUG); 0 in production
 };
 // wgrad (C % 64 == 0): D[co][tap·C + ci] = Σ_pix dY·X, per sample; acc_ρ partial += D ⊙ ε_s,
 // acc_μ partial = Σ_s D (tensor-core accumulated in TMEM). gmap: 3-D map over dY (CO, pix, s).

@@ -13,6 +13,7 @@
 // walk a static tile schedule; two TMEM accumulators let tile i's epilogue overlap tile
 // i+1's main loop.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 
@@ -24,14 +25,31 @@ namespace bnn {
 
 using namespace ptx;
 
+// pipeline depth cap (BNN_CONV_STAGES, default 4; ≤ 12), passed as a launch argument
+static int conv_stage_cap() {
+    static int cap = [] {
+        const char* e = getenv("BNN_CONV_STAGES");
+        const int v = e ? atoi(e) : 4;
+        return v < 2 ? 2 : (v > 12 ? 12 : v);
+    }();
+    return cap;
+}
+
+static int conv_debug() {  // BNN_CONV_DEBUG: 1 = skip MMAs, 2 = skip operand loads (timing experiments)
+    static int v = [] {
+        const char* e = getenv("BNN_CONV_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 namespace c2 {
 constexpr int kEpiWarps = 4;
 constexpr int kGatherWarps = 4;
 constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
-constexpr int kStages = 4;
 constexpr int kAStage = 128 * 64 * 2;  // 16 KB pixel window
-constexpr int kBStage = 256 * 64 * 2;  // 32 KB weights (N ≤ 256)
-constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 512 + 1024;
+constexpr int kData = 216 * 1024;      // stages: as many (A 16 KB + B n_tile·128 B) as fit
+constexpr int kSmem = 1024 + kData + 512 + 1024;
 }  // namespace c2
 
 struct TileGeo {
@@ -65,15 +83,99 @@ __device__ __forceinline__ float warp_transpose_sum(float* v, int lane) {
     return v[0];
 }
 
+// Epilogue of one NHWC row segment: this thread's pixel (row offset `rowoff`, valid `pv`) and the
+// 32 channels ch0 … ch0+31 in v (fp32 accumulators). fwd: + sampled bias, + residual, ReLU,
+// RN-bf16 store. dgrad: + the other contribution, ReLU mask of the layer input, RN-bf16 store;
+// v keeps the masked fp32 values (zero for invalid pixels) for the bias-gradient partials.
+template <int MODE, bool BIAS = true>
+__device__ __forceinline__ void epi_row32(const Conv2Args& a, float* v, bool pv, int64_t rowoff, int64_t so,
+                                          int s, int ch0) {
+    if (MODE == 0) {
+        if (BIAS) {
+        const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO + ch0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float4 b4 = __ldg(bs + q);
+            v[4 * q] += b4.x;
+            v[4 * q + 1] += b4.y;
+            v[4 * q + 2] += b4.z;
+            v[4 * q + 3] += b4.w;
+        }
+        }
+        if (!pv) return;
+        if (a.res) {
+            const uint4* rp = reinterpret_cast<const uint4*>(a.res + so + rowoff + ch0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 r4 = __ldg(rp + q);
+                const uint32_t w4[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
+                    v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+                }
+            }
+        }
+        uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float z[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) z[e] = a.relu ? fmaxf(v[8 * q + e], 0.0f) : v[8 * q + e];
+            op[q] = make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]), pack_bf16x2(z[4], z[5]),
+                               pack_bf16x2(z[6], z[7]));
+        }
+    } else {
+        if (!pv) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+            return;
+        }
+        if (a.addsrc) {
+            const uint4* ap = reinterpret_cast<const uint4*>(a.addsrc + so + rowoff + ch0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 r4 = ap[q];
+                const uint32_t w4[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
+                    v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+                }
+            }
+        }
+        if (a.mask) {
+            const uint4* mp = reinterpret_cast<const uint4*>(a.mask + so + rowoff + ch0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 m4 = __ldg(mp + q);
+                const uint32_t w4[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (!(__uint_as_float(w4[e] << 16) > 0.0f)) v[8 * q + 2 * e] = 0.0f;
+                    if (!(__uint_as_float(w4[e] & 0xFFFF0000u) > 0.0f)) v[8 * q + 2 * e + 1] = 0.0f;
+                }
+            }
+        }
+        uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            op[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                               pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+    }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(c2::kThreads, 1)
     conv2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap wmap,
-                 const Conv2Args a) {
+                 const Conv2Args a, const int g_max_stages_arg) {
     using namespace c2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
+    const int kBStage = a.n_tile * 128;
+    const int kStages = min(g_max_stages_arg, kData / (kAStage + kBStage));
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
     uint64_t* full = bars;
@@ -141,6 +243,10 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
                     mbar_wait_sleep(&empty[st], ph ^ 1);
+                    if (a.dbg & 2) {  // feed-rate experiment: no loads
+                        mbar_arrive_expect_tx(&full[st], 0);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[st], bbytes + (a.tma_a ? kAStage : 0));
                     uint8_t* dA = sA + st * kAStage;
                     uint8_t* dB = sB + st * kBStage;
@@ -154,8 +260,8 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                         }
                     } else {
                         const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti], cb = kb - ti * cblocks;
-                        for (int j = 0; j < a.n_tile / 64; ++j)
-                            tma_load_4d(&wmap, &full[st], dB + j * 8192, n0 + 64 * j, tap, cb * 64, g.s);
+                        // W_sᵀ: n_tile/64 channel blocks of 64 ci × 64 co in ONE op (5-D map, box 64×1×64×nb×1)
+                        tma_load_5d(&wmap, &full[st], dB, 0, tap, cb * 64, n0 / 64, g.s);
                         if (a.tma_a) {
                             const int kh = tap / a.k, kw = tap - kh * a.k;
                             tma_load_5d(&amap, &full[st], dA, cb * 64, a.pad - kw, y0 + a.pad - kh, img0, g.s);
@@ -190,7 +296,7 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                         const uint64_t ad = sdesc_sw128(aBase + 32 * q, 16, 1024);
                         const uint64_t bd = MODE == 0 ? sdesc_sw128(bBase + 32 * q, 16, 1024)
                                                       : sdesc_sw128(bBase + 2048 * q, 8192, 1024);
-                        mma_bf16(d, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
+                        if (!(a.dbg & 1)) mma_bf16(d, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
                     }
                     mma_commit(&empty[st]);
                 }
@@ -298,78 +404,8 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                     for (int j = 0; j < 32; ++j) v[j] = 0.0f;
                 }
                 const int ch0 = n0 + c * 32;
-                if (MODE == 0) {
-                    const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)g.s * a.CO + ch0);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 b4 = __ldg(bs + q);
-                        v[4 * q] += b4.x;
-                        v[4 * q + 1] += b4.y;
-                        v[4 * q + 2] += b4.z;
-                        v[4 * q + 3] += b4.w;
-                    }
-                    if (pv) {
-                        if (a.res) {
-                            const uint4* rp = reinterpret_cast<const uint4*>(a.res + so + rowoff + ch0);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint4 r4 = __ldg(rp + q);
-                                const uint32_t w4[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
-                                    v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
-                                }
-                            }
-                        }
-                        uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            float z[8];
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) z[e] = a.relu ? fmaxf(v[8 * q + e], 0.0f) : v[8 * q + e];
-                            op[q] = make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]),
-                                               pack_bf16x2(z[4], z[5]), pack_bf16x2(z[6], z[7]));
-                        }
-                    }
-                } else {
-                    if (pv) {
-                        if (a.addsrc) {
-                            const uint4* ap = reinterpret_cast<const uint4*>(a.addsrc + so + rowoff + ch0);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint4 r4 = ap[q];
-                                const uint32_t w4[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
-                                    v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
-                                }
-                            }
-                        }
-                        if (a.mask) {
-                            const uint4* mp = reinterpret_cast<const uint4*>(a.mask + so + rowoff + ch0);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint4 m4 = __ldg(mp + q);
-                                const uint32_t w4[4] = {m4.x, m4.y, m4.z, m4.w};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    if (!(__uint_as_float(w4[e] << 16) > 0.0f)) v[8 * q + 2 * e] = 0.0f;
-                                    if (!(__uint_as_float(w4[e] & 0xFFFF0000u) > 0.0f)) v[8 * q + 2 * e + 1] = 0.0f;
-                                }
-                            }
-                        }
-                        uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            op[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                                               pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
-                                               pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-                    }
+                epi_row32<MODE>(a, v, pv, rowoff, so, g.s, ch0);
+                if (MODE == 1) {
                     if (a.bpart) {  // fp32 bias partials (pre-rounding) over the tile's 128 pixels
                         float* red = bred + (nred++ & 1) * 128;
                         red[warp * 32 + lane] = warp_transpose_sum(v, lane);
@@ -412,7 +448,9 @@ static void launch_conv2(const CUtensorMap& amap, const CUtensorMap& wmap, const
     const int Ntot = MODE == 0 ? a.CO : a.C;
     const int T = a.S * ncls * ((P + 127) / 128) * ((Ntot + a.n_tile - 1) / a.n_tile);
     const int grid = std::min(T, kNumSMs);
-    conv2_kernel<MODE><<<grid, c2::kThreads, c2::kSmem, st>>>(amap, wmap, a);
+    Conv2Args b = a;
+    b.dbg = conv_debug();
+    conv2_kernel<MODE><<<grid, c2::kThreads, c2::kSmem, st>>>(amap, wmap, b, conv_stage_cap());
 }
 
 void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st) {
@@ -420,6 +458,346 @@ void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Co
 }
 void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st) {
     launch_conv2<1>(amap, wmap, a, st);
+}
+
+// ============================================================================ conv3 (channels on M)
+// For layers whose output channel count (fwd: CO, dgrad: C) is ≤ 128 the swap-AB tile would run
+// tcgen05.mma at N = 64/128 — and an M=128 MMA costs the same ~130 cycles per K=16 for any
+// N ≤ 256 (scripts/mma_bench.cu, profiles/r01). Here M = 128 channels (weights, the A operand)
+// and N = 256 pixels (activation / dY window, the B operand); the epilogue transposes each
+// warp's 32 channels × 32 pixels through shared memory so the NHWC row epilogue is reused.
+namespace c3 {
+constexpr int kEpiWarps = 8;
+constexpr int kGatherWarps = 4;
+constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
+constexpr int kStages = 3;  // pipeline depth is not the limiter (BNN_CONV_STAGES sweep, profiles/r01)
+constexpr int kAStage = 128 * 64 * 2;  // 16 KB weights (128 channel rows)
+constexpr int kBStage = 256 * 64 * 2;  // 32 KB pixel window (256 rows)
+constexpr int kTrans = kEpiWarps * 32 * 33 * 4;
+constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + kTrans + 512 + 2048;
+static_assert(kSmem <= 227 * 1024, "conv3 shared memory");
+}  // namespace c3
+
+template <int MODE>
+__global__ void __launch_bounds__(c3::kThreads, 1)
+    conv3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
+                 const Conv2Args a) {
+    using namespace c3;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kAStage;
+    float* trans = reinterpret_cast<float*>(sB + kStages * kBStage);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(trans) + kTrans);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = bars + 2 * kStages + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    int* staps = reinterpret_cast<int*>(tslot + 4);  // [4 classes][9 taps] + counts
+    float* bred = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [2][8 warps][32]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncls = MODE == 1 ? a.stride * a.stride : 1;
+    const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
+    const int P = a.B * PH * PW;
+    const int ptiles = (P + 255) / 256;
+    const bool dup = false;  // (a 64-channel layer leaves TMEM rows 64-127 zero; their warps idle)
+    const int Mtot = MODE == 0 ? a.CO : a.C;
+    const int mtiles = (Mtot + 127) / 128;
+    const int T = a.S * ncls * ptiles * mtiles;
+    const int cblocks = (a.CO + 63) / 64;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1 + (a.tma_a ? 0 : kGatherWarps * 32));
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kEpiWarps);
+        }
+        mbar_fence_init();
+        for (int cl = 0; cl < ncls; ++cl) {
+            const int ph = cl / a.stride, pw = cl % a.stride;
+            int cnt = 0;
+            if (MODE == 1) {
+                for (int kh = 0; kh < a.k; ++kh)
+                    for (int kw = 0; kw < a.k; ++kw)
+                        if ((ph + a.pad - kh) % a.stride == 0 && (pw + a.pad - kw) % a.stride == 0)
+                            staps[cl * 10 + cnt++] = kh * a.k + kw;
+            }
+            staps[cl * 10 + 9] = cnt;
+        }
+    }
+    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    auto nkb_of = [&](int cls) { return MODE == 0 ? a.K_pad / 64 : staps[cls * 10 + 9] * cblocks; };
+
+    if (warp == kEpiWarps + kGatherWarps) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&wmap);
+            if (a.tma_a) tma_prefetch_desc(&bmap);
+            const int cpb = a.C_pad >> 6;
+            int it = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+                const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
+                const int p0 = g.ptile * 256, m0 = g.ntile * 128;
+                const int img0 = p0 / (PH * PW), y0 = (p0 - img0 * PH * PW) / PW;
+                const int nkb = nkb_of(g.cls);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    if (a.dbg & 2) {  // feed-rate experiment: no loads
+                        mbar_arrive_expect_tx(&full[st], 0);
+                        continue;
+                    }
+                    // A box: 128 weight rows, or 64 for a 64-channel layer (rows 64-127 then unused)
+                    mbar_arrive_expect_tx(&full[st], (Mtot >= 128 ? 2 : 1) * 8192 + (a.tma_a ? kBStage : 0));
+                    uint8_t* dA = sA + st * kAStage;
+                    uint8_t* dB = sB + st * kBStage;
+                    if (MODE == 0) {
+                        tma_load_3d(&wmap, &full[st], dA, kb * 64, m0, g.s);
+                        if (a.tma_a) {
+                            const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
+                            const int kh = tap / a.k, kw = tap - kh * a.k;
+                            tma_load_5d(&bmap, &full[st], dB, c0, kw - a.pad, y0 + kh - a.pad, img0,
+                                        a.src_stride_s == 0 ? 0 : g.s);
+                        }
+                    } else {
+                        const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti], cb = kb - ti * cblocks;
+                        tma_load_5d(&wmap, &full[st], dA, 0, tap, cb * 64, m0 / 64, g.s);  // ≤ 2 ci blocks
+                        if (a.tma_a) {
+                            const int kh = tap / a.k, kw = tap - kh * a.k;
+                            tma_load_5d(&bmap, &full[st], dB, cb * 64, a.pad - kw, y0 + a.pad - kh, img0, g.s);
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kEpiWarps + kGatherWarps + 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, 256, MODE == 1 ? 1 : 0, 0);
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
+                const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
+                const int buf = tl & 1;
+                mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + buf * 256;
+                const int nkb = nkb_of(g.cls);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait_sleep(&full[st], ph);
+                    fence_proxy_async_smem();
+                    tc_fence_after();
+                    const uint32_t aBase = smem_u32(sA + st * kAStage);
+                    const uint32_t bBase = smem_u32(sB + st * kBStage);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t ad = MODE == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
+                                                      : sdesc_sw128(aBase + 2048 * q, 8192, 1024);
+                        const uint64_t bd = sdesc_sw128(bBase + 32 * q, 16, 1024);
+                        if (!(a.dbg & 1)) mma_bf16(d, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= kEpiWarps) {
+        // ------------------------------------------------ gather producers (stride 2 / stem): 256 rows
+        if (!a.tma_a) {
+            const int gt = threadIdx.x - kEpiWarps * 32;  // pixel rows gt and gt + 128
+            const int cpb = a.C_pad >> 6;
+            int it = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+                const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
+                const int ph = g.cls / a.stride, pw = g.cls % a.stride;
+                int py[2], px[2], pn[2];
+                bool pv[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pix = g.ptile * 256 + gt + 128 * h;
+                    pv[h] = pix < P;
+                    pn[h] = pv[h] ? pix / (PH * PW) : 0;
+                    const int rem = pv[h] ? pix - pn[h] * PH * PW : 0;
+                    py[h] = MODE == 0 ? rem / PW : (rem / PW) * a.stride + ph;
+                    px[h] = MODE == 0 ? rem % PW : (rem % PW) * a.stride + pw;
+                }
+                const __nv_bfloat16* src = a.src + g.s * a.src_stride_s;
+                const int nkb = nkb_of(g.cls);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t phs = (it / kStages) & 1;
+                    mbar_wait(&empty[st], phs ^ 1);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = gt + 128 * h;
+                        const uint32_t base = smem_u32(sB + st * kBStage) + r * 128;
+                        if (MODE == 0 && cpb == 0) {  // stem: 8 taps × 8 channels per K block
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const int tap = kb * 8 + j;
+                                const int kh = tap / a.k, kw = tap - kh * a.k;
+                                const int iy = py[h] * a.stride + kh - a.pad, ix = px[h] * a.stride + kw - a.pad;
+                                const bool ok = pv[h] && tap < a.k * a.k && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                                const __nv_bfloat16* gp =
+                                    ok ? src + (((int64_t)pn[h] * a.H + iy) * a.W + ix) * a.C_pad : src;
+                                cp_async16(base + ((j ^ (r & 7)) << 4), gp, ok ? 16u : 0u);
+                            }
+                        } else {
+                            int kh, kw, c0;
+                            if (MODE == 0) {
+                                const int tap = kb / cpb;
+                                c0 = (kb - tap * cpb) * 64;
+                                kh = tap / a.k;
+                                kw = tap - kh * a.k;
+                            } else {
+                                const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti];
+                                c0 = (kb - ti * cblocks) * 64;
+                                kh = tap / a.k;
+                                kw = tap - kh * a.k;
+                            }
+                            bool ok;
+                            const __nv_bfloat16* gp = src;
+                            if (MODE == 0) {
+                                const int iy = py[h] * a.stride + kh - a.pad, ix = px[h] * a.stride + kw - a.pad;
+                                ok = pv[h] && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                                if (ok) gp = src + (((int64_t)pn[h] * a.H + iy) * a.W + ix) * a.C_pad + c0;
+                            } else {
+                                const int ty = py[h] + a.pad - kh, tx = px[h] + a.pad - kw;
+                                const int oy = ty / a.stride, ox = tx / a.stride;
+                                ok = pv[h] && ty >= 0 && tx >= 0 && oy < a.OH && ox < a.OW;
+                                if (ok) gp = src + (((int64_t)pn[h] * a.OH + oy) * a.OW + ox) * a.CO + c0;
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                cp_async16(base + ((j ^ (r & 7)) << 4), gp + 8 * j, ok ? 16u : 0u);
+                        }
+                    }
+                    cp_async_mbar_arrive(&full[st]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue: 8 warps; warp ↔ TMEM lane quadrant q = warp & 3
+        // (32 channels), a subset of the tile's eight 32-pixel chunks; each chunk is transposed
+        // through shared memory so the thread = pixel NHWC row epilogue (epi_row32) applies.
+        // 64-channel layers (dup): quadrants 2,3 repeat channels 0-63, so all 8 warps work.
+        float* tr = trans + warp * 32 * 33;
+        const int q = warp & 3;
+        const int cg = dup ? (q & 1) : q;                                   // channel group
+        const int c_first = dup ? ((q >> 1) + 2 * (warp >> 2)) : (warp >> 2);  // first chunk
+        const int c_step = dup ? 4 : 2;
+        int tl = 0;
+        for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
+            const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
+            const int buf = tl & 1;
+            const int nkb = nkb_of(g.cls);
+            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            tc_fence_after();
+            const int ch0 = g.ntile * 128 + 32 * cg;
+            const bool active = ch0 < Mtot;
+            const int64_t so = (int64_t)g.s * a.out_stride_s;
+            const float bias = (MODE == 0 && active) ? __ldg(a.bias + (int64_t)g.s * a.CO + ch0 + lane) : 0.0f;
+            float bsum = 0.0f;
+            for (int c = c_first; c < 8; c += c_step) {  // 32 pixels per chunk
+                float v[32];
+                __syncwarp();
+                if (nkb > 0) {
+                    tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + c * 32, v);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+                }
+                if (!active) continue;
+                // v[j] = channel (ch0 + lane) at pixel 32c + j (+ its bias)  →  tr[j][lane]
+                const uint32_t trb = smem_u32(tr);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(trb + 4u * (j * 33 + lane)), "f"(v[j] + bias) : "memory");
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(trb + 4u * (lane * 33 + j)) : "memory");
+                const int pix = g.ptile * 256 + 32 * c + lane;
+                const bool pv = pix < P;
+                int64_t rowoff = 0;
+                if (pv) {
+                    if (MODE == 0 || a.stride == 1) {
+                        rowoff = (int64_t)pix * Mtot;
+                    } else {
+                        const int ph = g.cls / a.stride, pw = g.cls % a.stride;
+                        const int pn = pix / (PH * PW), rem = pix - pn * PH * PW;
+                        const int iy = (rem / PW) * a.stride + ph, ix = (rem % PW) * a.stride + pw;
+                        rowoff = (((int64_t)pn * a.H + iy) * a.W + ix) * a.C;
+                    }
+                }
+                epi_row32<MODE, false>(a, v, pv, rowoff, so, g.s, ch0);
+                if (MODE == 1 && a.bpart) bsum += warp_transpose_sum(v, lane);
+            }
+            if (MODE == 1 && a.bpart) {  // combine the warps of each channel group in a fixed order
+                float* red = bred + (tl & 1) * 256;
+                red[warp * 32 + lane] = bsum;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (active && warp < (dup ? 2 : 4)) {
+                    float t2 = 0.0f;
+                    for (int w = cg; w < 8; w += (dup ? 2 : 4)) t2 += red[w * 32 + lane];
+                    a.bpart[(int64_t)g.s * a.bpart_stride_s + (int64_t)(g.cls * ptiles + g.ptile) * a.C + ch0 +
+                            lane] = t2;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kEpiWarps + kGatherWarps + 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+int conv3_dgrad_parts(const Conv2Args& a) {
+    const int P = a.B * (a.H / a.stride) * (a.W / a.stride);
+    return a.stride * a.stride * ((P + 255) / 256);
+}
+
+template <int MODE>
+static void launch_conv3(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(conv3_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, c3::kSmem);
+        attr = true;
+    }
+    const int ncls = MODE == 1 ? a.stride * a.stride : 1;
+    const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
+    const int P = a.B * PH * PW;
+    const int Mtot = MODE == 0 ? a.CO : a.C;
+    const int T = a.S * ncls * ((P + 255) / 256) * ((Mtot + 127) / 128);
+    Conv2Args b = a;
+    b.dbg = conv_debug();
+    conv3_kernel<MODE><<<std::min(T, kNumSMs), c3::kThreads, c3::kSmem, st>>>(wmap, bmap, b);
+}
+
+void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+    launch_conv3<0>(wmap, bmap, a, st);
+}
+void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+    launch_conv3<1>(wmapT, bmap, a, st);
 }
 
 // ============================================================================ wgrad
@@ -433,10 +811,9 @@ namespace w2 {
 constexpr int kEpiWarps = 8;
 constexpr int kGatherWarps = 4;
 constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
-constexpr int kStages = 4;
 constexpr int kAStage = 64 * 128 * 2;  // dYᵀ: 64 pixels × 128 co (two 64-wide MN blocks)
-constexpr int kBStage = 64 * 256 * 2;  // X windows: 64 pixels × up to 4 × 64 parameter columns
-constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
+constexpr int kData = 216 * 1024;      // stages: as many (A 16 KB + B nb·8 KB X windows) as fit
+constexpr int kSmem = 1024 + kData + 512;
 }  // namespace w2
 
 // Persistent: unit u = (((s·nsplit + split)·co_tiles + ct)·ntiles + nt); neighbouring CTAs share
@@ -444,12 +821,14 @@ constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
 // (two 256-column buffers: unit i's store overlaps unit i+1's main loop).
 __global__ void __launch_bounds__(w2::kThreads, 1)
     conv2_wgrad_kernel(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap xmap,
-                       const ConvWgradArgs a) {
+                       const ConvWgradArgs a, const int g_max_stages_arg) {
     using namespace w2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
+    const int kBStage = 4 * 8192;  // up to 256 parameter columns
+    const int kStages = min(g_max_stages_arg, kData / (kAStage + kBStage));
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
     uint64_t* full = bars;
@@ -460,14 +839,14 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Kt = conv2_wgrad_cols(a);
-    const int ntiles = Kt / a.n_tile, co_tiles = (a.CO + 127) / 128;
-    const int nb = a.n_tile / 64;
+    // column tiles of 256 (the last one may be narrower: 64 … 256), one MMA width per unit
+    const int ntiles = (Kt + 255) / 256, co_tiles = (a.CO + 127) / 128;
     const int npix = a.B * a.OH * a.OW;
     const int nblk_all = (npix + 63) / 64;
     const int per = (nblk_all + a.nsplit - 1) / a.nsplit;
     const int T = a.S * a.nsplit * co_tiles * ntiles;
     struct U {
-        int s, split, ct, nt, blk0, nblk;
+        int s, split, ct, nt, blk0, nblk, w;
     };
     auto unit = [&](int t) {
         U u;
@@ -479,6 +858,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         u.s = t / a.nsplit;
         u.blk0 = u.split * per;
         u.nblk = max(0, min(nblk_all, u.blk0 + per) - u.blk0);
+        u.w = min(256, Kt - u.nt * 256);
         return u;
     };
 
@@ -504,27 +884,32 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         if (lane == 0) {
             tma_prefetch_desc(&gmap);
             if (a.tma_b) tma_prefetch_desc(&xmap);
-            const uint32_t bytes = kAStage + (a.tma_b ? nb * 8192 : 0);
             int it = 0;
             for (int t = blockIdx.x; t < T; t += gridDim.x) {
                 const U u = unit(t);
+                const int nb = u.w / 64;
+                const uint32_t bytes = (a.CO >= 128 ? 2 : 1) * 8192 + (a.tma_b ? nb * 8192 : 0);
                 const int co0 = u.ct * 128;
                 for (int b = 0; b < u.nblk; ++b, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
                     mbar_wait_sleep(&empty[st], ph ^ 1);
+                    if (a.dbg & 2) {  // feed-rate experiment: no loads
+                        mbar_arrive_expect_tx(&full[st], 0);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[st], bytes);
                     uint8_t* dst = sA + st * kAStage;
                     const int pix0 = (u.blk0 + b) * 64;
-                    tma_load_3d(&gmap, &full[st], dst, co0, pix0, u.s);
-                    tma_load_3d(&gmap, &full[st], dst + 8192, co0 + 64, pix0, u.s);
+                    tma_load_4d(&gmap, &full[st], dst, 0, pix0, co0 / 64, u.s);  // ≤ 2 co blocks, one op
                     if (a.tma_b) {
                         const int n0 = pix0 / (a.OH * a.OW), y0 = (pix0 - n0 * a.OH * a.OW) / a.OW;
-                        for (int j = 0; j < nb; ++j) {
-                            const int col = u.nt * a.n_tile + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
+                        const int cbx = min(nb, a.C / 64);  // channel blocks per op (same tap)
+                        for (int j = 0; j < nb; j += cbx) {
+                            const int col = u.nt * 256 + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
-                            tma_load_5d(&xmap, &full[st], sB + st * kBStage + j * 8192, ci0, kw - a.pad,
-                                        y0 + kh - a.pad, n0, a.X_stride_s == 0 ? 0 : u.s);
+                            tma_load_5d(&xmap, &full[st], sB + st * kBStage + j * 8192, 0, kw - a.pad,
+                                        y0 + kh - a.pad, u.s * a.B + n0, ci0 / 64);
                         }
                     }
                 }
@@ -534,10 +919,10 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     } else if (warp == kEpiWarps + kGatherWarps + 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = idesc_bf16(128, a.n_tile, 1, 1);
             int it = 0, tl = 0;
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const U u = unit(t);
+                const uint32_t idesc = idesc_bf16(128, u.w, 1, 1);
                 const int buf = tl & 1;
                 mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -554,7 +939,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t ad = sdesc_sw128(aBase + 2048 * q, 8192, 1024);
                         const uint64_t bd = sdesc_sw128(bBase + 2048 * q, 8192, 1024);
-                        mma_bf16(d, ad, bd, idesc, (b | q) != 0 ? 1u : 0u);
+                        if (!(a.dbg & 1)) mma_bf16(d, ad, bd, idesc, (b | q) != 0 ? 1u : 0u);
                     }
                     mma_commit(&empty[st]);
                 }
@@ -575,8 +960,9 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                 const U u = unit(t);
                 const __nv_bfloat16* xs = a.X + u.s * a.X_stride_s;
                 int ky[4], kx[4], co_[4];
+                const int nb = u.w / 64;
                 for (int j = 0; j < nb; ++j) {
-                    const int cb = u.nt * nb + j;
+                    const int cb = u.nt * 4 + j;
                     int tap, c0;
                     if (stem) {
                         tap = cb * 8 + ch;
@@ -623,7 +1009,6 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     } else {
         // ------------------------------------------------ epilogue: TMEM → fp32 per-sample partials
         const int q = warp & 3, h = warp >> 2;
-        const int half = a.n_tile / 2;
         int tl = 0;
         for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
             const U u = unit(t);
@@ -631,7 +1016,8 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
             mbar_wait(&tfull[buf], (tl >> 1) & 1);
             tc_fence_after();
             const int co = u.ct * 128 + 32 * q + lane;
-            float* out = a.part + ((int64_t)(u.s * a.nsplit + u.split) * a.CO + co) * Kt + u.nt * a.n_tile + h * half;
+            const int half = u.w / 2;
+            float* out = a.part + ((int64_t)(u.s * a.nsplit + u.split) * a.CO + co) * Kt + u.nt * 256 + h * half;
             for (int c = 0; c < half / 32; ++c) {
                 float v[32];
                 __syncwarp();
@@ -660,12 +1046,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     }
 }
 
-int conv2_wgrad_ntile(int Kt) {
-    if (Kt < 64) return 0;
-    for (int n : {256, 192, 128, 64})
-        if (Kt % n == 0) return n;
-    return 0;
-}
+int conv2_wgrad_ntile(int Kt) { return Kt >= 64 ? 256 : 0; }  // column-tile width (the last may be narrower)
 
 void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
                         cudaStream_t st) {
@@ -675,8 +1056,10 @@ void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const 
         attr = true;
     }
     const int Kt = conv2_wgrad_cols(a);
-    const int T = a.S * a.nsplit * ((a.CO + 127) / 128) * (Kt / a.n_tile);
-    conv2_wgrad_kernel<<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, a);
+    const int T = a.S * a.nsplit * ((a.CO + 127) / 128) * ((Kt + 255) / 256);
+    ConvWgradArgs b = a;
+    b.dbg = conv_debug();
+    conv2_wgrad_kernel<<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, b, conv_stage_cap());
 }
 
 // Phase 2: thread = four consecutive parameter columns of one row; fixed summation order

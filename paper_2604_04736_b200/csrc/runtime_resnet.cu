@@ -77,6 +77,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->cmap_a2f.resize(L);
     c->cmap_a2d.resize(L);
     c->cmap_w2.resize(L);
+    c->cmap_w64.resize(L);
     c->tma_a2f.assign(L, 0);
     c->tma_a2d.assign(L, 0);
     c->tma_fwd.assign(L, 0);
@@ -98,7 +99,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         const int Cp_src = c->rbf[op.src].C_pad;
         if (Ld.cin % 64 == 0 || Cp_src == 8) {  // conv2 wgrad: units = samples × splits × co tiles × column tiles
             const int Kt = conv2_wgrad_cols(taps, Ld.cin, Cp_src);
-            const int base = Sc * ((Ld.cout + 127) / 128) * (Kt / conv2_wgrad_ntile(Kt));
+            const int base = Sc * ((Ld.cout + 127) / 128) * ((Kt + 255) / 256);
             const int blocks = (int)((npix + 63) / 64);
             c->nsplit[op.layer] = conv2_wgrad_nsplit(base, blocks);
             if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
@@ -125,6 +126,9 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const uint32_t box[3] = {64, 128, 1};
             if (!make_map_nd(&c->cmap_w[op.layer], c->wscr + c->wscr_off[op.layer], 3, dims, str, box))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch) failed");
+            const uint32_t box64[3] = {64, 64, 1};
+            if (!make_map_nd(&c->cmap_w64[op.layer], c->wscr + c->wscr_off[op.layer], 3, dims, str, box64))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch, 64 rows) failed");
             const uint32_t box2[3] = {64, (uint32_t)std::min(CO, 256), 1};
             if (!make_map_nd(&c->cmap_w2[op.layer], c->wscr + c->wscr_off[op.layer], 3, dims, str, box2))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch, conv2) failed");
@@ -133,17 +137,20 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const int gb = grad_src_buffer(c, op.dst);
             const RBuf& D = c->rbufs[op.dst];
             const uint64_t npix = (uint64_t)B * D.H * D.W;
-            const uint64_t gd[3] = {(uint64_t)CO, npix, (uint64_t)Sc};
-            const uint64_t gs[2] = {(uint64_t)CO * 2, npix * CO * 2};
-            const uint32_t gbx[3] = {64, 64, 1};
-            if (!make_map_nd(&c->cmap_g[op.layer], c->rbf[gb].grad, 3, gd, gs, gbx))
+            // dY as (64 co, pixel, co block, sample): one op loads 64 pixels × 128 co
+            const uint64_t gd[4] = {64, npix, (uint64_t)(CO / 64), (uint64_t)Sc};
+            const uint64_t gs[3] = {(uint64_t)CO * 2, 128, npix * CO * 2};
+            const uint32_t gbx[4] = {64, 64, (uint32_t)std::min(2, CO / 64), 1};
+            if (!make_map_nd(&c->cmap_g[op.layer], c->rbf[gb].grad, 4, gd, gs, gbx))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (dY) failed");
         }
         if (Ld.cin % 64 == 0) {
-            const uint64_t dims[4] = {(uint64_t)Ld.cin, (uint64_t)taps, (uint64_t)CO, (uint64_t)Sc};
-            const uint64_t str[3] = {(uint64_t)Ld.cin * 2, (uint64_t)Kp * 2, (uint64_t)CO * Kp * 2};
-            const uint32_t box[4] = {64, 1, 64, 1};
-            if (!make_map_nd(&c->cmap_wT[op.layer], c->wscr + c->wscr_off[op.layer], 4, dims, str, box))
+            // W_sᵀ as (64 ci, tap, co, ci block, sample): one op loads cb blocks of 64 ci × 64 co
+            const int cb = Ld.cin <= 128 ? std::min(2, Ld.cin / 64) : std::min(Ld.cin, 256) / 64;
+            const uint64_t dims[5] = {64, (uint64_t)taps, (uint64_t)CO, (uint64_t)(Ld.cin / 64), (uint64_t)Sc};
+            const uint64_t str[4] = {(uint64_t)Ld.cin * 2, (uint64_t)Kp * 2, 128, (uint64_t)CO * Kp * 2};
+            const uint32_t box[5] = {64, 1, 64, (uint32_t)cb, 1};
+            if (!make_map_nd(&c->cmap_wT[op.layer], c->wscr + c->wscr_off[op.layer], 5, dims, str, box))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (W scratch transposed) failed");
         }
     }
@@ -174,9 +181,15 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             if (64 % PW == 0 || PW % 64 == 0) {
                 const int wh = PW >= 64 ? 1 : std::min(PH, 64 / PW);
                 const int wn = 64 / (std::min(PW, 64) * wh);
-                if (PW <= 64 && PH % wh == 0 && wn >= 1) {
-                    const uint32_t wbox[5] = {64, (uint32_t)std::min(PW, 64), (uint32_t)wh, (uint32_t)wn, 1};
-                    if (!make_map_nd(&c->cmap_xw[op.layer], c->rbf[op.src].val, 5, dims, str, wbox))
+                if (PW <= 64 && PH % wh == 0 && wn >= 1 && !shared) {
+                    // X as (64 ci, W, H, image·sample, ci block): one op loads cbx channel blocks
+                    const int Kt = Ld.k * Ld.k * Ld.cin;
+                    const int cbx = std::min(4, Ld.cin / 64);  // divides every column tile's block count
+                    (void)Kt;
+                    const uint64_t xd[5] = {64, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B * Sc, (uint64_t)(Cp / 64)};
+                    const uint64_t xs[4] = {(uint64_t)Cp * 2, (uint64_t)Sb.W * Cp * 2, (uint64_t)Sb.H * Sb.W * Cp * 2, 128};
+                    const uint32_t wbox[5] = {64, (uint32_t)std::min(PW, 64), (uint32_t)wh, (uint32_t)wn, (uint32_t)cbx};
+                    if (!make_map_nd(&c->cmap_xw[op.layer], c->rbf[op.src].val, 5, xd, xs, wbox))
                         return c->set_err(BNN_ERR_CUDA, "tensor map (wgrad window) failed");
                     c->tma_wgrad[op.layer] = Ld.cin % 64 == 0 ? 1 : 0;
                 }
@@ -310,7 +323,12 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         a.bias = c->bias_scr;
         a.res = op.res >= 0 ? c->rbf[op.res].val : nullptr;
         a.relu = op.relu;
-        c->launch("fwd", [&] { launch_conv2_fwd(c->cmap_a2f[op.layer], c->cmap_w2[op.layer], a, st); });
+        if (Db.C <= 128) {  // channels on M, 256 pixels on N (full-width MMA)
+            a.tma_a = c->tma_fwd[op.layer];
+            c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], c->cmap_bf[op.layer], a, st); });
+        } else {
+            c->launch("fwd", [&] { launch_conv2_fwd(c->cmap_a2f[op.layer], c->cmap_w2[op.layer], a, st); });
+        }
     }
 }
 
@@ -481,16 +499,23 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         a.src_stride_s = npix_out * Db.C;
         a.out = c->rbf[op.src].grad;
         a.out_stride_s = (int64_t)B * Sb.H * Sb.W * Sb.C;
+        const bool m_chan = Sb.C <= 128;  // conv3: channels on M, 256 pixels on N
+        if (m_chan) a.tma_a = c->tma_dgrad[op.layer];
         if (final) {
+            const int np = m_chan ? conv3_dgrad_parts(a) : conv2_dgrad_parts(a);
             a.addsrc = pending[op.src];
             a.mask = c->rbf[op.src].val;
             a.bpart = c->rbf[op.src].bpart;
-            a.bpart_stride_s = (int64_t)conv2_dgrad_parts(a) * Sb.C;
-            if (conv2_dgrad_parts(a) * Sb.C > c->rbf[op.src].bpart_cap)
+            a.bpart_stride_s = (int64_t)np * Sb.C;
+            if ((int64_t)np * Sb.C > c->rbf[op.src].bpart_cap)
                 return c->set_err(BNN_ERR_CONFIG, "bias partial buffer too small");
-            c->rbf[op.src].nparts = conv2_dgrad_parts(a);
+            c->rbf[op.src].nparts = np;
         }
-        c->launch("dgrad", [&] { launch_conv2_dgrad(c->cmap_a2d[op.layer], c->cmap_wT[op.layer], a, st); });
+        if (m_chan) {
+            c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], c->cmap_bd[op.layer], a, st); });
+        } else {
+            c->launch("dgrad", [&] { launch_conv2_dgrad(c->cmap_a2d[op.layer], c->cmap_wT[op.layer], a, st); });
+        }
         if (!final) pending[op.src] = c->rbf[op.src].grad;
     }
     c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });

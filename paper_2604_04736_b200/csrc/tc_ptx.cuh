@@ -3,6 +3,7 @@
 // follow the PTX ISA for tcgen05 (matrix descriptor, instruction descriptor kind::f16).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -40,9 +41,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Watchdog: a wait that has not completed after ~2^31 polls (seconds) is a lost TMA
+// transaction or a protocol bug — trap (a loud launch error) instead of hanging the GPU.
+__device__ __noinline__ inline void mbar_timeout(uint32_t addr, uint32_t parity) {
+    printf("bnn: mbarrier wait timeout: block %d thread %d bar 0x%x parity %u\n", (int)blockIdx.x,
+           (int)threadIdx.x, addr, parity);
+    __trap();
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr uint64_t kWaitTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait(a, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    uint32_t n = 0;
     while (!mbar_try_wait(a, parity)) {
+        if ((++n & 1023u) == 0 && globaltimer_ns() - t0 > kWaitTimeoutNs) mbar_timeout(a, parity);
     }
 }
 
@@ -60,7 +78,10 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t pari
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait_sleep(a, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait_sleep(a, parity)) {
+        if (globaltimer_ns() - t0 > kWaitTimeoutNs) mbar_timeout(a, parity);
     }
 }
 

@@ -1,0 +1,160 @@
+// tma_test.cu — checks the multi-block tensor-map views used by the conv kernels: one TMA
+// load per map into shared memory (SWIZZLE_128B), then every element against the expected
+// global element. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+//   -I../paper_2604_04736_b200/csrc tma_test.cu -o tma_test -lcuda
+#include <cstdio>
+#include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "tc_ptx.cuh"
+
+using namespace bnn::ptx;
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+static bool make(CUtensorMap* m, void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                 const uint32_t* box) {
+    cuuint64_t d[5], st[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i > 0) st[i - 1] = strides[i - 1];
+    }
+    CUresult r = encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) printf("  encode failed: %d\n", (int)r);
+    return r == CUDA_SUCCESS;
+}
+
+// one load; out = smem bytes un-swizzled into [row][64] (row = 128-byte smem row index)
+__global__ void load_kernel(const __grid_constant__ CUtensorMap map, int rank, int c0, int c1, int c2, int c3, int c4,
+                            uint32_t bytes, __nv_bfloat16* out, int* status) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bar, bytes);
+        if (rank == 3) tma_load_3d(&map, &bar, smem, c0, c1, c2);
+        if (rank == 4) tma_load_4d(&map, &bar, smem, c0, c1, c2, c3);
+        if (rank == 5) tma_load_5d(&map, &bar, smem, c0, c1, c2, c3, c4);
+        const uint64_t t0 = globaltimer_ns();
+        const uint32_t a = smem_u32(&bar);
+        bool ok = true;
+        while (!mbar_try_wait(a, 0)) {
+            if (globaltimer_ns() - t0 > 2000000000ull) {
+                ok = false;
+                break;
+            }
+        }
+        *status = ok ? 1 : -1;
+    }
+    __syncthreads();
+    if (*status != 1) return;
+    const int rows = bytes / 128;
+    for (int i = threadIdx.x; i < rows * 8; i += blockDim.x) {
+        const int r = i / 8, ch = i % 8;
+        const uint4 v = *reinterpret_cast<const uint4*>(smem + r * 128 + ((ch ^ (r & 7)) << 4));
+        *reinterpret_cast<uint4*>(out + r * 64 + ch * 8) = v;
+    }
+}
+
+struct Case {
+    const char* name;
+    int rank;
+    std::vector<uint64_t> dims, strides;  // strides in bytes (rank-1)
+    std::vector<uint32_t> box;
+    std::vector<int> coord;
+};
+
+int main() {
+    // global tensor: element value = its linear index (mod 2^13, exact in bf16 for < 256... use idx % 251)
+    const size_t N = 1 << 24;
+    std::vector<__nv_bfloat16> h(N);
+    for (size_t i = 0; i < N; ++i) h[i] = __float2bfloat16((float)(i % 251));
+    __nv_bfloat16 *g, *out;
+    int* st;
+    cudaMalloc(&g, N * 2);
+    cudaMalloc(&out, 1 << 20);
+    cudaMalloc(&st, 4);
+    cudaMemcpy(g, h.data(), N * 2, cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(load_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // shapes from the conv path: CO = 512 dY [S=2][npix=2048][CO]; X [S·B=16][H=4][W=4][C=512];
+    // W scratch [S][CO=512][Kp = 9·512]
+    const uint64_t CO = 512, npix = 2048, C = 512, Hh = 4, Ww = 4, SB = 16, Kp = 9 * 512;
+    std::vector<Case> cases = {
+        {"dY 4D (64 co, pix, co-block, s) box 64x64x2", 4, {64, npix, CO / 64, 2}, {CO * 2, 128, npix * CO * 2},
+         {64, 64, 2, 1}, {0, 128, 3, 1}},
+        {"X 5D (64 ci, W, H, img, ci-block) box 64x4x4x4x4", 5, {64, Ww, Hh, SB, C / 64},
+         {C * 2, Ww * C * 2, Hh * Ww * C * 2, 128}, {64, 4, 4, 4, 4}, {0, -1, 1, 4, 2}},
+        {"W^T 5D (64 ci, tap, co, ci-block, s) box 64x1x64x4x1", 5, {64, 9, CO, C / 64, 2},
+         {C * 2, Kp * 2, 128, CO * Kp * 2}, {64, 1, 64, 4, 1}, {0, 4, 64, 4, 1}},
+        {"dY 4D CO=64 view (box co-block 1)", 4, {64, npix, 1, 2}, {64 * 2, 128, npix * 64 * 2}, {64, 64, 1, 1},
+         {0, 64, 0, 1}},
+    };
+    int fails = 0;
+    for (auto& cs : cases) {
+        CUtensorMap m;
+        printf("%s\n", cs.name);
+        if (!make(&m, g, cs.rank, cs.dims.data(), cs.strides.data(), cs.box.data())) {
+            ++fails;
+            continue;
+        }
+        uint32_t bytes = 2;
+        for (auto b : cs.box) bytes *= b;
+        int c[5] = {0, 0, 0, 0, 0};
+        for (size_t i = 0; i < cs.coord.size(); ++i) c[i] = cs.coord[i];
+        cudaMemset(st, 0, 4);
+        load_kernel<<<1, 128, 200 * 1024>>>(m, cs.rank, c[0], c[1], c[2], c[3], c[4], bytes, out, st);
+        cudaError_t e = cudaDeviceSynchronize();
+        int hs = 0;
+        cudaMemcpy(&hs, st, 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess || hs != 1) {
+            printf("  FAIL: launch %s, status %d (−1 = transaction never completed)\n", cudaGetErrorString(e), hs);
+            ++fails;
+            continue;
+        }
+        std::vector<__nv_bfloat16> o(bytes / 2);
+        cudaMemcpy(o.data(), out, bytes, cudaMemcpyDeviceToHost);
+        // expected: iterate the box in dim order (dim0 fastest)
+        long bad = 0, k = 0;
+        int idx[5] = {0, 0, 0, 0, 0};
+        const int R = cs.rank;
+        for (;;) {
+            long off = 0;
+            bool oob = false;
+            for (int d = 0; d < R; ++d) {
+                const long x = (long)c[d] + idx[d];
+                if (x < 0 || x >= (long)cs.dims[d]) oob = true;
+                off += x * (d == 0 ? 2 : (long)cs.strides[d - 1]);
+            }
+            const float exp = oob ? 0.0f : (float)((off / 2) % 251);
+            const float got = __bfloat162float(o[k]);
+            if (exp != got && bad++ < 5) printf("  mismatch at box elem %ld: got %g expected %g\n", k, got, exp);
+            ++k;
+            int d = 0;
+            while (d < R && ++idx[d] == (int)cs.box[d]) idx[d++] = 0;
+            if (d == R) break;
+        }
+        printf("  %s (%ld elements, %ld bad)\n", bad ? "FAIL" : "ok", k, bad);
+        fails += bad != 0;
+    }
+    printf("%s\n", fails ? "TMA TEST FAILED" : "TMA TEST PASSED");
+    return fails != 0;
+}
