@@ -165,6 +165,51 @@ __device__ __forceinline__ void epi_row32(const Conv2Args& a, float* v, bool pv,
     }
 }
 
+// epi_row32 with the residual (fwd) / other contribution + mask (dgrad) rows already loaded
+// (x1, x2: 32 bf16 each) and the bias already added.
+template <int MODE>
+__device__ __forceinline__ void epi_apply32(const Conv2Args& a, float* v, bool pv, int64_t rowoff, int64_t so,
+                                            int ch0, const uint4* x1, const uint4* x2) {
+    if (!pv) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+        return;
+    }
+    const bool add = MODE == 0 ? a.res != nullptr : a.addsrc != nullptr;
+    if (add) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t w4[4] = {x1[q].x, x1[q].y, x1[q].z, x1[q].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                v[8 * q + 2 * e] += __uint_as_float(w4[e] << 16);
+                v[8 * q + 2 * e + 1] += __uint_as_float(w4[e] & 0xFFFF0000u);
+            }
+        }
+    }
+    if (MODE == 0) {
+        if (a.relu) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+        }
+    } else if (a.mask) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t w4[4] = {x2[q].x, x2[q].y, x2[q].z, x2[q].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (!(__uint_as_float(w4[e] << 16) > 0.0f)) v[8 * q + 2 * e] = 0.0f;
+                if (!(__uint_as_float(w4[e] & 0xFFFF0000u) > 0.0f)) v[8 * q + 2 * e + 1] = 0.0f;
+            }
+        }
+    }
+    uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        op[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                           pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(c2::kThreads, 1)
     conv2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap wmap,
@@ -503,7 +548,9 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
     const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
     const int P = a.B * PH * PW;
     const int ptiles = (P + 255) / 256;
-    const bool dup = false;  // (a 64-channel layer leaves TMEM rows 64-127 zero; their warps idle)
+    // 64-channel layers: TMEM rows 64-127 repeat rows 0-63 (the A tile is loaded twice), so all
+    // eight epilogue warps have channels to work on (MMA cost is the same for any M ≤ 128)
+    const bool dup = (MODE == 0 ? a.CO : a.C) <= 64;
     const int Mtot = MODE == 0 ? a.CO : a.C;
     const int mtiles = (Mtot + 127) / 128;
     const int T = a.S * ncls * ptiles * mtiles;
@@ -559,11 +606,12 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                         continue;
                     }
                     // A box: 128 weight rows, or 64 for a 64-channel layer (rows 64-127 then unused)
-                    mbar_arrive_expect_tx(&full[st], (Mtot >= 128 ? 2 : 1) * 8192 + (a.tma_a ? kBStage : 0));
+                    mbar_arrive_expect_tx(&full[st], kAStage + (a.tma_a ? kBStage : 0));
                     uint8_t* dA = sA + st * kAStage;
                     uint8_t* dB = sB + st * kBStage;
                     if (MODE == 0) {
-                        tma_load_3d(&wmap, &full[st], dA, kb * 64, m0, g.s);
+                        tma_load_3d(&wmap, &full[st], dA, kb * 64, m0, g.s);  // 128 rows, or 64 (dup)
+                        if (dup) tma_load_3d(&wmap, &full[st], dA + 8192, kb * 64, m0, g.s);
                         if (a.tma_a) {
                             const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
@@ -572,7 +620,8 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                         }
                     } else {
                         const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti], cb = kb - ti * cblocks;
-                        tma_load_5d(&wmap, &full[st], dA, 0, tap, cb * 64, m0 / 64, g.s);  // ≤ 2 ci blocks
+                        tma_load_5d(&wmap, &full[st], dA, 0, tap, cb * 64, m0 / 64, g.s);  // 2 ci blocks, or 1 (dup)
+                        if (dup) tma_load_5d(&wmap, &full[st], dA + 8192, 0, tap, cb * 64, m0 / 64, g.s);
                         if (a.tma_a) {
                             const int kh = tap / a.k, kw = tap - kh * a.k;
                             tma_load_5d(&bmap, &full[st], dB, cb * 64, a.pad - kw, y0 + a.pad - kh, img0, g.s);
@@ -712,6 +761,38 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             const int64_t so = (int64_t)g.s * a.out_stride_s;
             const float bias = (MODE == 0 && active) ? __ldg(a.bias + (int64_t)g.s * a.CO + ch0 + lane) : 0.0f;
             float bsum = 0.0f;
+            // pixel row of chunk c for this lane (thread = pixel after the transpose)
+            auto row_of = [&](int c, bool& pv) -> int64_t {
+                const int pix = g.ptile * 256 + 32 * c + lane;
+                pv = pix < P;
+                if (!pv) return 0;
+                if (MODE == 0 || a.stride == 1) return (int64_t)pix * Mtot;
+                const int ph = g.cls / a.stride, pw = g.cls % a.stride;
+                const int pn = pix / (PH * PW), rem = pix - pn * PH * PW;
+                const int iy = (rem / PW) * a.stride + ph, ix = (rem % PW) * a.stride + pw;
+                return (((int64_t)pn * a.H + iy) * a.W + ix) * a.C;
+            };
+            // the chunk's residual (fwd) or other-contribution + mask (dgrad) rows are issued at the
+            // end of the previous chunk, so their latency overlaps the TMEM load and transpose
+            uint4 o1[4], o2[4];
+            auto load_ops = [&](int c, uint4* x1, uint4* x2) {
+                bool pv;
+                const int64_t ro = row_of(c, pv);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) x1[i] = x2[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (!pv || !active) return;
+                const uint4* p1 = reinterpret_cast<const uint4*>((MODE == 0 ? a.res : a.addsrc) + so + ro + ch0);
+                if (MODE == 0 ? a.res != nullptr : a.addsrc != nullptr) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) x1[i] = MODE == 0 ? __ldg(p1 + i) : p1[i];
+                }
+                if (MODE == 1 && a.mask) {
+                    const uint4* p2 = reinterpret_cast<const uint4*>(a.mask + so + ro + ch0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) x2[i] = __ldg(p2 + i);
+                }
+            };
+            load_ops(c_first, o1, o2);
             for (int c = c_first; c < 8; c += c_step) {  // 32 pixels per chunk
                 float v[32];
                 __syncwarp();
@@ -731,20 +812,11 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(trb + 4u * (lane * 33 + j)) : "memory");
-                const int pix = g.ptile * 256 + 32 * c + lane;
-                const bool pv = pix < P;
-                int64_t rowoff = 0;
-                if (pv) {
-                    if (MODE == 0 || a.stride == 1) {
-                        rowoff = (int64_t)pix * Mtot;
-                    } else {
-                        const int ph = g.cls / a.stride, pw = g.cls % a.stride;
-                        const int pn = pix / (PH * PW), rem = pix - pn * PH * PW;
-                        const int iy = (rem / PW) * a.stride + ph, ix = (rem % PW) * a.stride + pw;
-                        rowoff = (((int64_t)pn * a.H + iy) * a.W + ix) * a.C;
-                    }
-                }
-                epi_row32<MODE, false>(a, v, pv, rowoff, so, g.s, ch0);
+                __syncwarp();
+                bool pv;
+                const int64_t rowoff = row_of(c, pv);
+                epi_apply32<MODE>(a, v, pv, rowoff, so, ch0, o1, o2);
+                if (c + c_step < 8) load_ops(c + c_step, o1, o2);  // in flight during the next TMEM load
                 if (MODE == 1 && a.bpart) bsum += warp_transpose_sum(v, lane);
             }
             if (MODE == 1 && a.bpart) {  // combine the warps of each channel group in a fixed order

@@ -146,7 +146,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         }
         if (Ld.cin % 64 == 0) {
             // W_sᵀ as (64 ci, tap, co, ci block, sample): one op loads cb blocks of 64 ci × 64 co
-            const int cb = Ld.cin <= 128 ? std::min(2, Ld.cin / 64) : std::min(Ld.cin, 256) / 64;
+            const int cb = Ld.cin <= 128 ? std::min(2, Ld.cin / 64) : std::min(Ld.cin, 256) / 64;  // 1: conv3 dup
             const uint64_t dims[5] = {64, (uint64_t)taps, (uint64_t)CO, (uint64_t)(Ld.cin / 64), (uint64_t)Sc};
             const uint64_t str[4] = {(uint64_t)Ld.cin * 2, (uint64_t)Kp * 2, 128, (uint64_t)CO * Kp * 2};
             const uint32_t box[5] = {64, 1, 64, (uint32_t)cb, 1};
