@@ -361,7 +361,7 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
         peak = 148 * 128 * clk_mhz * 1e6 / INSTR_PER_NORMAL / 1e9  # Gnormal/s
         ach = normals[dom] / (ms / 1e3) / 1e9
         return {"kernel": dom, "ms_per_step": ms, "bound": "alu", "achieved": ach, "peak": peak,
-                "unit": "Gnormal/s", "frac": ach / peak, "traffic": _ncu_traffic(dom),
+                "unit": "Gnormal/s", "frac": ach / peak, "traffic": _ncu_traffic("mlp", dom),
                 "peak_source": f"derived: 148 SM x 128 lanes x {clk_mhz:.0f} MHz / "
                                f"{INSTR_PER_NORMAL} SASS instr per normal (DESIGN.md §4)",
                 "tensor_tflops": flops[dom] / (ms / 1e3) / 1e12,
@@ -377,7 +377,7 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
                 "unit": None, "frac": None, "traffic": None}
     ach = flops[dom] / (ms / 1e3) / 1e12
     return {"kernel": dom, "ms_per_step": ms, "bound": "tensor", "achieved": ach, "peak": peak,
-            "unit": "TFLOP/s", "frac": ach / peak, "traffic": _ncu_traffic(dom),
+            "unit": "TFLOP/s", "frac": ach / peak, "traffic": _ncu_traffic("cnn", dom),
             "peak_source": f"measured bf16 sustained ({peak_src}, MEASURED_PEAKS.json); "
                            f"burst {peaks.get('bf16_tflops')}"}
 
@@ -387,11 +387,13 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
 INSTR_PER_NORMAL = 40.0
 
 
-def _ncu_traffic(kernel):
+def _ncu_traffic(kind, kernel):
+    """DRAM bytes (read + write) per launch of the class, from an ncu capture committed under
+    profiles/ (profiles/ncu_traffic.json, written by scripts/traffic_summary.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get(kernel)
+            return json.load(open(p)).get(f"{kind}:{kernel}")
         except Exception:
             return None
     return None

@@ -1134,68 +1134,102 @@ void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const 
     conv2_wgrad_kernel<<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, b, conv_stage_cap());
 }
 
-// Phase 2: thread = four consecutive parameter columns of one row; fixed summation order
-// (splits, then samples) ⇒ deterministic. ε_s is the same EPS-v1 draw as the forward's W_s.
-__global__ void wgrad_eps_combine_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int Kt,
-                                         const float* __restrict__ part, float scale,
-                                         float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
+// Phase 2: thread = four consecutive parameter columns of one row. The partials of up to 8
+// samples (and the accumulators) are loaded up front — independent loads, so the kernel
+// streams at memory speed — then summed over splits in split order and weighted by ε_s (the
+// same EPS-v1 draw as the forward's W_s) in sample order ⇒ deterministic.
+__global__ void __launch_bounds__(256)
+    wgrad_eps_combine_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int Kt,
+                             const float* __restrict__ part, float scale, float* __restrict__ acc_mu,
+                             float* __restrict__ acc_rho) {
     const int kq = Kt / 4;
     const int64_t nq = (int64_t)CO * kq;
     const int64_t ss = (int64_t)CO * Kt;  // one split of one sample
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
-        const int co = (int)(i / kq), cq = (int)(i - (int64_t)co * kq);
-        const float* p = part + (int64_t)co * Kt + 4 * cq;
-        float4 m = make_float4(0.f, 0.f, 0.f, 0.f), r = m;
-        for (int s = 0; s < S; ++s) {
-            float4 d = __ldcs(reinterpret_cast<const float4*>(p + (int64_t)s * nsplit * ss));
-            for (int sp = 1; sp < nsplit; ++sp) {
-                const float4 e = __ldcs(reinterpret_cast<const float4*>(p + ((int64_t)s * nsplit + sp) * ss));
-                d.x += e.x;
-                d.y += e.y;
-                d.z += e.z;
-                d.w += e.w;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    const int co = (int)(i / kq), cq = (int)(i - (int64_t)co * kq);
+    const float* p = part + (int64_t)co * Kt + 4 * cq;
+    float4* am = reinterpret_cast<float4*>(acc_mu + L.off_w + (int64_t)co * Kt + 4 * cq);
+    float4* ar = reinterpret_cast<float4*>(acc_rho + L.off_w + (int64_t)co * Kt + 4 * cq);
+    const float4 x0 = *am, y0 = *ar;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f), r = m;
+    for (int s0 = 0; s0 < S; s0 += 8) {
+        float4 d[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            d[j] = s0 + j < S ? __ldcs(reinterpret_cast<const float4*>(p + (int64_t)(s0 + j) * nsplit * ss))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int sp = 1; sp < nsplit; ++sp) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (s0 + j < S) {
+                    const float4 e = __ldcs(reinterpret_cast<const float4*>(p + ((int64_t)(s0 + j) * nsplit + sp) * ss));
+                    d[j].x += e.x;
+                    d[j].y += e.y;
+                    d[j].z += e.z;
+                    d[j].w += e.w;
+                }
             }
-            const float4 e = eps4(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)cq);
-            m.x += d.x;
-            m.y += d.y;
-            m.z += d.z;
-            m.w += d.w;
-            r.x = fmaf(d.x, e.x, r.x);
-            r.y = fmaf(d.y, e.y, r.y);
-            r.z = fmaf(d.z, e.z, r.z);
-            r.w = fmaf(d.w, e.w, r.w);
         }
-        float4* am = reinterpret_cast<float4*>(acc_mu + L.off_w + (int64_t)co * Kt + 4 * cq);
-        float4* ar = reinterpret_cast<float4*>(acc_rho + L.off_w + (int64_t)co * Kt + 4 * cq);
-        float4 x = *am, y = *ar;
-        x.x = fmaf(scale, m.x, x.x);
-        x.y = fmaf(scale, m.y, x.y);
-        x.z = fmaf(scale, m.z, x.z);
-        x.w = fmaf(scale, m.w, x.w);
-        y.x = fmaf(scale, r.x, y.x);
-        y.y = fmaf(scale, r.y, y.y);
-        y.z = fmaf(scale, r.z, y.z);
-        y.w = fmaf(scale, r.w, y.w);
-        *am = x;
-        *ar = y;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // the 8 Philox chains are independent (ILP); d = 0 past S
+            const float4 e = eps4(kk.key, kk.step, kk.s0 + s0 + j, L.t_w, (uint32_t)co, (uint32_t)cq);
+            m.x += d[j].x;
+            m.y += d[j].y;
+            m.z += d[j].z;
+            m.w += d[j].w;
+            r.x = fmaf(d[j].x, e.x, r.x);
+            r.y = fmaf(d[j].y, e.y, r.y);
+            r.z = fmaf(d[j].z, e.z, r.z);
+            r.w = fmaf(d[j].w, e.w, r.w);
+        }
     }
+    *am = make_float4(fmaf(scale, m.x, x0.x), fmaf(scale, m.y, x0.y), fmaf(scale, m.z, x0.z), fmaf(scale, m.w, x0.w));
+    *ar = make_float4(fmaf(scale, r.x, y0.x), fmaf(scale, r.y, y0.y), fmaf(scale, r.z, y0.z), fmaf(scale, r.w, y0.w));
 }
 
-// The stem: partial columns are the padded tap·8 + ci; parameter columns tap·C + ci.
-__global__ void wgrad_eps_combine_stem_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int taps,
-                                              int C, int Ktp, const float* __restrict__ part, float scale,
-                                              float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
+// The stem: partial columns are the padded tap·8 + ci, parameter columns tap·C + ci. Block =
+// 32 parameters × 8 sample lanes; each thread sums its (parameter, sample) over the splits
+// (four independent chains, fixed order), the sample lanes are combined in a fixed order.
+__global__ void __launch_bounds__(256)
+    wgrad_eps_combine_stem_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int taps, int C,
+                                  int Ktp, const float* __restrict__ part, float scale,
+                                  float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
+    __shared__ float red[2][8][33];
     const int Kt = taps * C;
     const int64_t n = (int64_t)CO * Kt;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int co = (int)(i / Kt), col = (int)(i - (int64_t)co * Kt);
+    const int tx = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + tx;
+    float m = 0.0f, r = 0.0f;
+    int co = 0, col = 0;
+    if (i < n) {
+        co = (int)(i / Kt);
+        col = (int)(i - (int64_t)co * Kt);
         const int tap = col / C, pc = tap * 8 + (col - tap * C);
-        float m = 0.0f, r = 0.0f;
-        for (int s = 0; s < S; ++s) {
-            float d = 0.0f;
-            for (int sp = 0; sp < nsplit; ++sp) d += part[((int64_t)(s * nsplit + sp) * CO + co) * Ktp + pc];
+        for (int s = sl; s < S; s += 8) {
+            const float* p = part + ((int64_t)s * nsplit * CO + co) * Ktp + pc;
+            const int64_t st = (int64_t)CO * Ktp;
+            float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+            int sp = 0;
+            for (; sp + 4 <= nsplit; sp += 4) {
+                q0 += __ldcs(p + sp * st);
+                q1 += __ldcs(p + (sp + 1) * st);
+                q2 += __ldcs(p + (sp + 2) * st);
+                q3 += __ldcs(p + (sp + 3) * st);
+            }
+            for (; sp < nsplit; ++sp) q0 += __ldcs(p + sp * st);
+            const float d = (q0 + q1) + (q2 + q3);
             m += d;
             r = fmaf(d, eps1(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)col), r);
+        }
+    }
+    red[0][sl][tx] = m;
+    red[1][sl][tx] = r;
+    __syncthreads();
+    if (sl == 0 && i < n) {
+        for (int j = 1; j < 8; ++j) {
+            m += red[0][j][tx];
+            r += red[1][j][tx];
         }
         acc_mu[L.off_w + i] = fmaf(scale, m, acc_mu[L.off_w + i]);
         acc_rho[L.off_w + i] = fmaf(scale, r, acc_rho[L.off_w + i]);
@@ -1206,8 +1240,8 @@ void launch_wgrad_eps_combine_stem(const SampledLayer& L, const SampleKeys& kk, 
                                    int C, int Ktp, const float* part, float scale, float* acc_mu, float* acc_rho,
                                    cudaStream_t st) {
     const int64_t n = (int64_t)CO * taps * C;
-    wgrad_eps_combine_stem_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(L, kk, S, nsplit, CO, taps, C, Ktp, part,
-                                                                          scale, acc_mu, acc_rho);
+    wgrad_eps_combine_stem_kernel<<<(int)((n + 31) / 32), 256, 0, st>>>(L, kk, S, nsplit, CO, taps, C, Ktp, part,
+                                                                        scale, acc_mu, acc_rho);
 }
 
 // nsplit for `base` units per split: fewest waves per split (persistent grid of 148), and among
@@ -1229,9 +1263,8 @@ int conv2_wgrad_nsplit(int base, int blocks) {
 void launch_wgrad_eps_combine(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO, int Kt,
                               const float* part, float scale, float* acc_mu, float* acc_rho, cudaStream_t st) {
     const int64_t nq = (int64_t)CO * Kt / 4;
-    const int grid = (int)std::min<int64_t>((nq + 255) / 256, (int64_t)kNumSMs * 8);
-    wgrad_eps_combine_kernel<<<std::max(grid, 1), 256, 0, st>>>(L, kk, S, nsplit, CO, Kt, part, scale, acc_mu,
-                                                                acc_rho);
+    wgrad_eps_combine_kernel<<<(int)((nq + 255) / 256), 256, 0, st>>>(L, kk, S, nsplit, CO, Kt, part, scale, acc_mu,
+                                                                     acc_rho);
 }
 
 }  // namespace bnn

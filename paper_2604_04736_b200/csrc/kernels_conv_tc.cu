@@ -24,62 +24,66 @@ namespace bnn {
 using namespace ptx;
 
 // ============================================================================ W scratch
-__global__ void gen_wscratch_kernel(SampledLayer L, SampleKeys kk, int S, int C, int C_pad,
-                                    int taps, int K_pad, __nv_bfloat16* __restrict__ out,
-                                    float* __restrict__ bias_out) {
-    if (bias_out) {  // sampled biases b_s = fma(σ, ε_s, μ) in fp32, [S][N]
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)S * L.N;
-             i += (int64_t)gridDim.x * blockDim.x) {
-            const int s = (int)(i / L.N), n = (int)(i % L.N);
-            bias_out[i] = __fmaf_rn(L.sigma[L.off_b + n], eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0u, (uint32_t)n),
-                                    L.mu[L.off_b + n]);
-        }
+// Block = one output-channel row co (blockIdx.x) of every sample; thread = column quads of the
+// row; μ and σ are loaded once per quad and reused for the S samples.
+__global__ void __launch_bounds__(256)
+    gen_wscratch_kernel(SampledLayer L, SampleKeys kk, int S, int C, int C_pad, int taps, int K_pad,
+                        __nv_bfloat16* __restrict__ out, float* __restrict__ bias_out) {
+    const int co = blockIdx.x;
+    for (int s = threadIdx.x; bias_out && s < S; s += blockDim.x) {  // sampled biases b_s, fp32 [S][N]
+        bias_out[(int64_t)s * L.N + co] = __fmaf_rn(
+            L.sigma[L.off_b + co], eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0u, (uint32_t)co), L.mu[L.off_b + co]);
     }
-    const int64_t quads_per_sample = (int64_t)L.N * K_pad / 4;
-    const int64_t total = quads_per_sample * S;
+    const int kq = K_pad / 4;
     const int Kt = L.K;  // = taps·C
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(q / quads_per_sample);
-        const int64_t r = q % quads_per_sample;
-        const int co = (int)(r / (K_pad / 4));
-        const int kp = (int)(r % (K_pad / 4)) * 4;
-        const uint32_t sg = kk.s0 + s;
-        float w[4] = {0.f, 0.f, 0.f, 0.f};
+    const int64_t srow = (int64_t)L.N * K_pad;
+    __nv_bfloat16* orow = out + (int64_t)co * K_pad;
+    for (int qd = threadIdx.x; qd < kq; qd += blockDim.x) {
+        const int kp = qd * 4;
         if (C_pad == C) {
             // column kp = tap·C + ci is the parameter column; C % 4 == 0 ⇒ one Philox quad
-            if (kp < Kt) {
+            float4 m = make_float4(0.f, 0.f, 0.f, 0.f), g = m;
+            const bool ok = kp < Kt;
+            if (ok) {
                 const int64_t i = L.off_w + (int64_t)co * Kt + kp;
-                const float4 e = eps4(kk.key, kk.step, sg, L.t_w, (uint32_t)co, (uint32_t)(kp >> 2));
-                const float4 m = __ldg(reinterpret_cast<const float4*>(L.mu + i));
-                const float4 g = __ldg(reinterpret_cast<const float4*>(L.sigma + i));
-                w[0] = __fmaf_rn(g.x, e.x, m.x);
-                w[1] = __fmaf_rn(g.y, e.y, m.y);
-                w[2] = __fmaf_rn(g.z, e.z, m.z);
-                w[3] = __fmaf_rn(g.w, e.w, m.w);
+                m = __ldg(reinterpret_cast<const float4*>(L.mu + i));
+                g = __ldg(reinterpret_cast<const float4*>(L.sigma + i));
+            }
+#pragma unroll 4
+            for (int s = 0; s < S; ++s) {  // independent Philox chains: unrolled for ILP
+                uint2 v = make_uint2(0u, 0u);
+                if (ok) {
+                    const float4 e = eps4(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)qd);
+                    v = make_uint2(pack_bf16x2(__fmaf_rn(g.x, e.x, m.x), __fmaf_rn(g.y, e.y, m.y)),
+                                   pack_bf16x2(__fmaf_rn(g.z, e.z, m.z), __fmaf_rn(g.w, e.w, m.w)));
+                }
+                *reinterpret_cast<uint2*>(orow + s * srow + kp) = v;
             }
         } else {
+            for (int s = 0; s < S; ++s) {
+                float w[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int tap = (kp + j) / C_pad, ci = (kp + j) % C_pad;
-                if (tap < taps && ci < C) {
-                    const int col = tap * C + ci;
-                    const int64_t i = L.off_w + (int64_t)co * Kt + col;
-                    w[j] = __fmaf_rn(L.sigma[i], eps1(kk.key, kk.step, sg, L.t_w, (uint32_t)co, (uint32_t)col),
-                                     L.mu[i]);
+                for (int j = 0; j < 4; ++j) {
+                    const int tap = (kp + j) / C_pad, ci = (kp + j) % C_pad;
+                    if (tap < taps && ci < C) {
+                        const int col = tap * C + ci;
+                        const int64_t i = L.off_w + (int64_t)co * Kt + col;
+                        w[j] = __fmaf_rn(L.sigma[i],
+                                         eps1(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)col), L.mu[i]);
+                    }
                 }
+                *reinterpret_cast<uint2*>(orow + s * srow + kp) =
+                    make_uint2(pack_bf16x2(w[0], w[1]), pack_bf16x2(w[2], w[3]));
             }
         }
-        uint2 v = make_uint2(pack_bf16x2(w[0], w[1]), pack_bf16x2(w[2], w[3]));
-        *reinterpret_cast<uint2*>(out + (int64_t)s * L.N * K_pad + (int64_t)co * K_pad + kp) = v;
     }
 }
 
 void launch_gen_wscratch(const SampledLayer& L, const SampleKeys& kk, int S, int C, int C_pad,
                          int taps, int K_pad, __nv_bfloat16* out, float* bias_out, cudaStream_t st) {
-    const int64_t total = (int64_t)S * L.N * K_pad / 4;
-    const int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
-    gen_wscratch_kernel<<<std::max(grid, 1), 256, 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out, bias_out);
+    const int kq = K_pad / 4;
+    const int threads = kq >= 256 ? 256 : ((kq + 31) / 32) * 32;
+    gen_wscratch_kernel<<<L.N, std::max(threads, 32), 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out, bias_out);
 }
 
 // ============================================================================ fwd / dgrad

@@ -450,12 +450,12 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.n_tile = conv2_wgrad_ntile(Kt);
             c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
             if (w.C_pad < 64) {
-                c->launch("wgrad", [&] {
+                c->launch("wcomb", [&] {
                     launch_wgrad_eps_combine_stem(sl, kk, Sc, w.nsplit, Ld.cout, taps, Ld.cin, Kt, c->wpart, scale,
                                                   acc_mu, acc_rho, st);
                 });
             } else {
-                c->launch("wgrad", [&] {
+                c->launch("wcomb", [&] {
                     launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Kt, c->wpart, scale, acc_mu, acc_rho, st);
                 });
             }
