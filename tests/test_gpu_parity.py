@@ -342,3 +342,63 @@ def test_cnn_bf16_end_to_end_vs_oracle(aug, hw, B):
     ref = O.elbo_step(model, mu, rho, x, yc, None, S, 0xBEEF, 5, D, aug=a)
     assert abs(loss - ref["loss"]) <= 2e-2 * abs(ref["loss"])
     assert max(_per_tensor_rel(ctx, gmu, ref["grad_mu"])) <= 0.3
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_cnn_sample_chunking_equals_single_chunk(precision):
+    """S = 4 in chunks of 2 (the C4 path: S_loc > chunk) = one chunk of 4, up to fp32
+    summation order of the per-chunk accumulation."""
+    native = _native()
+    model, B, S = dict(BF16_CNN, in_h=8, in_w=8), 3, 4
+    mu, rho, x, yc, _ = _inputs(model, B, "init")
+    out = []
+    for chunk in (0, 2):
+        ctx = native.Context(model, precision=precision, max_B_loc=B, max_S_loc=S, sample_chunk=chunk,
+                             dataset_size=1e4, aug="per_sample")
+        out.append(ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 21, 2))
+        torch.cuda.synchronize()
+    (l0, m0, r0), (l1, m1, r1) = out
+    assert abs(l0 - l1) <= 1e-6 * abs(l0)
+    assert _rel(m1.cpu().numpy(), m0.cpu().numpy()) < 1e-5
+    assert _rel(r1.cpu().numpy(), r0.cpu().numpy()) < 1e-5
+
+
+def test_cnn_bf16_full_size_c3_sampled_examples():
+    """C3 at full size in the bench launch configuration (ResNet-18, 32×32×3, B = 128, S = 8,
+    per-sample augmentation): the stored activations and gradients of two sampled
+    (sample, example) pairs — the first and the last — against the emulating oracle, with the
+    layer-wise bounds of test_cnn_bf16_layerwise_against_emulating_oracle."""
+    native = _native()
+    model = dict(kind="resnet18", in_h=32, in_w=32, in_c=3, n_classes=10, base_width=64, loss="ce")
+    B, S = 128, 8
+    mu, rho, x, yc, _ = _inputs(model, B, "init")
+    ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=45000.0,
+                         aug="per_sample")
+    ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0x5EED, 0)
+    torch.cuda.synchronize()
+    n_layers = len(ctx.tensors) // 2
+
+    def rel(u, v):
+        return np.linalg.norm(u - v) / max(np.linalg.norm(v), 1e-30)
+
+    outs = [ctx.layer_output(l, 0).cpu().numpy().astype(np.float64) for l in range(n_layers)]
+    grads = [ctx.layer_output(l, 1).cpu().numpy().astype(np.float64) if l < n_layers - 1 else None
+             for l in range(n_layers)]
+    sizes = [o.size // (S * B) for o in outs]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    for s, b in ((0, 0), (S - 1, B - 1)):
+        i = s * B + b
+        d = {(emu, g): O.layer_dump(model, mu, rho, x, yc, None, b, s, 0x5EED, 0, aug=O.AUG_PER_SAMPLE,
+                                    emu=emu, grad=g)
+             for emu in (True, False) for g in (False, True)}
+        for l in range(n_layers):
+            k = slice(i * sizes[l], (i + 1) * sizes[l])
+            o = slice(offs[l], offs[l + 1])
+            err, spread = rel(outs[l][k], d[True, False][o]), rel(d[True, False][o], d[False, False][o])
+            assert err <= max(3e-3, 2 * spread), (s, b, l, err, spread)
+            if l < 2:
+                assert err <= 3e-4, (s, b, l, err)
+            if grads[l] is not None and np.any(grads[l]):
+                gerr = rel(grads[l][k], d[True, True][o])
+                gspread = rel(d[True, True][o], d[False, True][o])
+                assert gerr <= max(2e-2, 3 * gspread), (s, b, l, gerr, gspread)
