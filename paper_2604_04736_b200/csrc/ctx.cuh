@@ -141,6 +141,7 @@ struct bnn_ctx {
         __nv_bfloat16* val = nullptr;
         __nv_bfloat16* grad = nullptr;
         float* bpart = nullptr;    // fp32 bias-gradient partials of the buffer's producer
+        uint32_t* mbits = nullptr; // ReLU bitmask [s][pixel][C/32] of a ReLU output (dgrad mask)
         int nparts = 0;
         int C_pad = 0;
         int64_t bpart_cap = 0;

@@ -67,6 +67,9 @@ struct Conv2Args {
     float* bpart;              // dgrad: fp32 bias partials [s][parts][C]
     int64_t bpart_stride_s;
     int dbg;                   // timing experiments only (BNN_CONV_DEBUG); 0 in production
+    uint32_t* mbits_out;       // fwd (relu): ReLU bitmask of the stored output, bit j of word
+                               //   [pixel][c/32] = (stored bf16 of channel c > 0); or null
+    const uint32_t* mbits;     // dgrad: bitmask of the layer input (replaces `mask` when set)
 };
 void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
 void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);

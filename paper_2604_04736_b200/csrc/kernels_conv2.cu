@@ -83,6 +83,22 @@ __device__ __forceinline__ float warp_transpose_sum(float* v, int lane) {
     return v[0];
 }
 
+// ReLU bitmask of 32 packed bf16 (4 × uint4, channel order): bit j = (channel j > 0)
+__device__ __forceinline__ uint32_t relu_bits32(const uint4* w) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t w4[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t lo = w4[e] & 0xFFFFu, hi = w4[e] >> 16;
+            bits |= (uint32_t)((lo & 0x7FFFu) != 0 && (lo & 0x8000u) == 0) << (8 * q + 2 * e);
+            bits |= (uint32_t)((hi & 0x7FFFu) != 0 && (hi & 0x8000u) == 0) << (8 * q + 2 * e + 1);
+        }
+    }
+    return bits;
+}
+
 // Epilogue of one NHWC row segment: this thread's pixel (row offset `rowoff`, valid `pv`) and the
 // 32 channels ch0 … ch0+31 in v (fp32 accumulators). fwd: + sampled bias, + residual, ReLU,
 // RN-bf16 store. dgrad: + the other contribution, ReLU mask of the layer input, RN-bf16 store;
@@ -117,14 +133,17 @@ __device__ __forceinline__ void epi_row32(const Conv2Args& a, float* v, bool pv,
             }
         }
         uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+        uint4 pk[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             float z[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) z[e] = a.relu ? fmaxf(v[8 * q + e], 0.0f) : v[8 * q + e];
-            op[q] = make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]), pack_bf16x2(z[4], z[5]),
+            pk[q] = make_uint4(pack_bf16x2(z[0], z[1]), pack_bf16x2(z[2], z[3]), pack_bf16x2(z[4], z[5]),
                                pack_bf16x2(z[6], z[7]));
+            op[q] = pk[q];
         }
+        if (a.mbits_out) a.mbits_out[(so + rowoff + ch0) >> 5] = relu_bits32(pk);
     } else {
         if (!pv) {
 #pragma unroll
@@ -144,7 +163,12 @@ __device__ __forceinline__ void epi_row32(const Conv2Args& a, float* v, bool pv,
                 }
             }
         }
-        if (a.mask) {
+        if (a.mbits) {
+            const uint32_t mb = __ldg(a.mbits + ((so + rowoff + ch0) >> 5));
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (!((mb >> j) & 1u)) v[j] = 0.0f;
+        } else if (a.mask) {
             const uint4* mp = reinterpret_cast<const uint4*>(a.mask + so + rowoff + ch0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -169,7 +193,7 @@ __device__ __forceinline__ void epi_row32(const Conv2Args& a, float* v, bool pv,
 // (x1, x2: 32 bf16 each) and the bias already added.
 template <int MODE>
 __device__ __forceinline__ void epi_apply32(const Conv2Args& a, float* v, bool pv, int64_t rowoff, int64_t so,
-                                            int ch0, const uint4* x1, const uint4* x2) {
+                                            int ch0, const uint4* x1, uint32_t mb) {
     if (!pv) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.0f;
@@ -192,22 +216,20 @@ __device__ __forceinline__ void epi_apply32(const Conv2Args& a, float* v, bool p
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
         }
-    } else if (a.mask) {
+    } else if (a.mbits) {  // mb = the input's ReLU bitmask word
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t w4[4] = {x2[q].x, x2[q].y, x2[q].z, x2[q].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (!(__uint_as_float(w4[e] << 16) > 0.0f)) v[8 * q + 2 * e] = 0.0f;
-                if (!(__uint_as_float(w4[e] & 0xFFFF0000u) > 0.0f)) v[8 * q + 2 * e + 1] = 0.0f;
-            }
-        }
+        for (int j = 0; j < 32; ++j)
+            if (!((mb >> j) & 1u)) v[j] = 0.0f;
     }
     uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + ch0);
+    uint4 pk[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-        op[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+    for (int q = 0; q < 4; ++q) {
+        pk[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
                            pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+        op[q] = pk[q];
+    }
+    if (MODE == 0 && a.mbits_out) a.mbits_out[(so + rowoff + ch0) >> 5] = relu_bits32(pk);
 }
 
 template <int MODE>
@@ -754,8 +776,6 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
             const int buf = tl & 1;
             const int nkb = nkb_of(g.cls);
-            mbar_wait(&tfull[buf], (tl >> 1) & 1);
-            tc_fence_after();
             const int ch0 = g.ntile * 128 + 32 * cg;
             const bool active = ch0 < Mtot;
             const int64_t so = (int64_t)g.s * a.out_stride_s;
@@ -774,25 +794,25 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             };
             // the chunk's residual (fwd) or other-contribution + mask (dgrad) rows are issued at the
             // end of the previous chunk, so their latency overlaps the TMEM load and transpose
-            uint4 o1[4], o2[4];
-            auto load_ops = [&](int c, uint4* x1, uint4* x2) {
+            uint4 o1[4];
+            uint32_t o2 = 0xFFFFFFFFu;
+            auto load_ops = [&](int c, uint4* x1, uint32_t& x2) {
                 bool pv;
                 const int64_t ro = row_of(c, pv);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) x1[i] = x2[i] = make_uint4(0u, 0u, 0u, 0u);
+                for (int i = 0; i < 4; ++i) x1[i] = make_uint4(0u, 0u, 0u, 0u);
+                x2 = 0xFFFFFFFFu;
                 if (!pv || !active) return;
                 const uint4* p1 = reinterpret_cast<const uint4*>((MODE == 0 ? a.res : a.addsrc) + so + ro + ch0);
                 if (MODE == 0 ? a.res != nullptr : a.addsrc != nullptr) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) x1[i] = MODE == 0 ? __ldg(p1 + i) : p1[i];
                 }
-                if (MODE == 1 && a.mask) {
-                    const uint4* p2 = reinterpret_cast<const uint4*>(a.mask + so + ro + ch0);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) x2[i] = __ldg(p2 + i);
-                }
+                if (MODE == 1 && a.mbits) x2 = __ldg(a.mbits + ((so + ro + ch0) >> 5));
             };
-            load_ops(c_first, o1, o2);
+            load_ops(c_first, o1, o2);  // independent of the accumulator: in flight while the MMAs finish
+            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            tc_fence_after();
             for (int c = c_first; c < 8; c += c_step) {  // 32 pixels per chunk
                 float v[32];
                 __syncwarp();

@@ -53,6 +53,9 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         const size_t n = (size_t)Sc * B * R.H * R.W * b.C_pad;
         if (!c->alloc(&b.val, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (activations)");
         if (i != 0 && !c->alloc(&b.grad, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (gradients)");
+        if (i != 0 && i != gbuf && R.C % 32 == 0 && c->rbufs[i].H > 1) {
+            if (!c->alloc(&b.mbits, n / 32)) return c->set_err(BNN_ERR_CUDA, "out of memory (masks)");
+        }
         if (i != 0 && i != gbuf) {
             const int64_t npix = (int64_t)B * R.H * R.W;
             b.bpart_cap = (int64_t)(4 * ((npix + 127) / 128) * 4 + B) * R.C;
@@ -323,6 +326,7 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         a.bias = c->bias_scr;
         a.res = op.res >= 0 ? c->rbf[op.res].val : nullptr;
         a.relu = op.relu;
+        a.mbits_out = op.relu ? c->rbf[op.dst].mbits : nullptr;
         if (Db.C <= 128) {  // channels on M, 256 pixels on N (full-width MMA)
             a.tma_a = c->tma_fwd[op.layer];
             c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], c->cmap_bf[op.layer], a, st); });
@@ -504,7 +508,10 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         if (final) {
             const int np = m_chan ? conv3_dgrad_parts(a) : conv2_dgrad_parts(a);
             a.addsrc = pending[op.src];
-            a.mask = c->rbf[op.src].val;
+            a.mbits = c->rbf[op.src].mbits;  // written by the producer's forward epilogue
+            a.mask = a.mbits ? nullptr : c->rbf[op.src].val;
+            if (!a.mbits && Sb.C <= 128)
+                return c->set_err(BNN_ERR_CONFIG, "conv3 dgrad needs the ReLU bitmask of its input");
             a.bpart = c->rbf[op.src].bpart;
             a.bpart_stride_s = (int64_t)np * Sb.C;
             if ((int64_t)np * Sb.C > c->rbf[op.src].bpart_cap)
