@@ -151,6 +151,7 @@ struct bnn_ctx {
     std::vector<size_t> wscr_off;   // per layer: element offset of its slot (forward writes, dgrad reads)
     float* wpart = nullptr;         // conv wgrad split partials
     std::vector<int> kpad, nsplit;  // per layer
+    std::vector<int> wkpx;          // per layer: wgrad pixels per k-step (64 or 128)
     std::vector<CUtensorMap> cmap_w, cmap_wT, cmap_g;  // per layer
     std::vector<CUtensorMap> cmap_bf, cmap_bd;         // per layer: 5-D activation / dY windows
     std::vector<CUtensorMap> cmap_xw;                  // per layer: wgrad X windows (64 pixels)

@@ -124,6 +124,7 @@ struct ConvWgradArgs {
     int nsplit;
     int tma_b;               // stride 1: X window by 5-D TMA (xmap, box 64 × 64 pixels)
     int n_tile;              // conv2 wgrad: parameter columns per tile (64 | 128 | 192 | 256)
+    int kpx;                 // pixels per k-step: 64, or 128 (TMA path, c_out ≤ 64)
     int dbg;                 // timing experiments only (BNN_CONV_DEBUG); 0 in production
 };
 // wgrad (C % 64 == 0): D[co][tap·C + ci] = Σ_pix dY·X, per sample; acc_ρ partial += D ⊙ ε_s,

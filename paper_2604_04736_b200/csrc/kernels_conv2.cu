@@ -903,8 +903,7 @@ namespace w2 {
 constexpr int kEpiWarps = 8;
 constexpr int kGatherWarps = 4;
 constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
-constexpr int kAStage = 64 * 128 * 2;  // dYᵀ: 64 pixels × 128 co (two 64-wide MN blocks)
-constexpr int kData = 216 * 1024;      // stages: as many (A 16 KB + B nb·8 KB X windows) as fit
+constexpr int kData = 216 * 1024;      // stages: as many (A 2 blocks + B 4 blocks of kpx·128 B) as fit
 constexpr int kSmem = 1024 + kData + 512;
 }  // namespace w2
 
@@ -919,7 +918,12 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
-    const int kBStage = 4 * 8192;  // up to 256 parameter columns
+    // k-step = kpx pixels (64, or 128 for 64-channel stride-1 layers: half the TMA ops per byte);
+    // one 64-wide MN block of an operand is kpx K-rows × 128 B
+    const int kpx = a.kpx;
+    const int blkB = kpx * 128;
+    const int kAStage = 2 * blkB;  // dYᵀ: up to 2 co blocks
+    const int kBStage = 4 * blkB;  // X windows: up to 256 parameter columns
     const int kStages = min(g_max_stages_arg, kData / (kAStage + kBStage));
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
@@ -934,7 +938,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     // column tiles of 256 (the last one may be narrower: 64 … 256), one MMA width per unit
     const int ntiles = (Kt + 255) / 256, co_tiles = (a.CO + 127) / 128;
     const int npix = a.B * a.OH * a.OW;
-    const int nblk_all = (npix + 63) / 64;
+    const int nblk_all = (npix + kpx - 1) / kpx;
     const int per = (nblk_all + a.nsplit - 1) / a.nsplit;
     const int T = a.S * a.nsplit * co_tiles * ntiles;
     struct U {
@@ -980,7 +984,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
             for (int t = blockIdx.x; t < T; t += gridDim.x) {
                 const U u = unit(t);
                 const int nb = u.w / 64;
-                const uint32_t bytes = (a.CO >= 128 ? 2 : 1) * 8192 + (a.tma_b ? nb * 8192 : 0);
+                const uint32_t bytes = (a.CO >= 128 ? 2 : 1) * blkB + (a.tma_b ? nb * blkB : 0);
                 const int co0 = u.ct * 128;
                 for (int b = 0; b < u.nblk; ++b, ++it) {
                     const int st = it % kStages;
@@ -992,7 +996,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                     }
                     mbar_arrive_expect_tx(&full[st], bytes);
                     uint8_t* dst = sA + st * kAStage;
-                    const int pix0 = (u.blk0 + b) * 64;
+                    const int pix0 = (u.blk0 + b) * kpx;
                     tma_load_4d(&gmap, &full[st], dst, 0, pix0, co0 / 64, u.s);  // ≤ 2 co blocks, one op
                     if (a.tma_b) {
                         const int n0 = pix0 / (a.OH * a.OW), y0 = (pix0 - n0 * a.OH * a.OW) / a.OW;
@@ -1000,7 +1004,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                         for (int j = 0; j < nb; j += cbx) {
                             const int col = u.nt * 256 + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
-                            tma_load_5d(&xmap, &full[st], sB + st * kBStage + j * 8192, 0, kw - a.pad,
+                            tma_load_5d(&xmap, &full[st], sB + st * kBStage + j * blkB, 0, kw - a.pad,
                                         y0 + kh - a.pad, u.s * a.B + n0, ci0 / 64);
                         }
                     }
@@ -1028,9 +1032,10 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
                     const uint32_t bBase = smem_u32(sB + st * kBStage);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint64_t ad = sdesc_sw128(aBase + 2048 * q, 8192, 1024);
-                        const uint64_t bd = sdesc_sw128(bBase + 2048 * q, 8192, 1024);
+                    for (int q = 0; q < 8; ++q) {  // K = 16 pixels per MMA
+                        if (q * 16 >= kpx) break;
+                        const uint64_t ad = sdesc_sw128(aBase + 2048 * q, blkB, 1024);
+                        const uint64_t bd = sdesc_sw128(bBase + 2048 * q, blkB, 1024);
                         if (!(a.dbg & 1)) mma_bf16(d, ad, bd, idesc, (b | q) != 0 ? 1u : 0u);
                     }
                     mma_commit(&empty[st]);

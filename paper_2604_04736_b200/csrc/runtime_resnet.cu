@@ -71,6 +71,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->kpad.assign(L, 0);
     c->wscr_off.assign(L, 0);
     c->nsplit.assign(L, 1);
+    c->wkpx.assign(L, 64);
     c->cmap_w.resize(L);
     c->cmap_wT.resize(L);
     c->cmap_g.resize(L);
@@ -103,7 +104,17 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         if (Ld.cin % 64 == 0 || Cp_src == 8) {  // conv2 wgrad: units = samples × splits × co tiles × column tiles
             const int Kt = conv2_wgrad_cols(taps, Ld.cin, Cp_src);
             const int base = Sc * ((Ld.cout + 127) / 128) * ((Kt + 255) / 256);
-            const int blocks = (int)((npix + 63) / 64);
+            // 64-channel stride-1 layers (TMA operand path): 128-pixel k-steps halve the TMA ops
+            {
+                const RBuf& Sb0 = c->rbufs[op.src];
+                const int PW = D.W, PH = D.H, kp = 128;
+                const int wh = PW >= kp ? 1 : std::min(PH, kp / PW);
+                const bool shared = op.src == 0 && c->cfg.aug != BNN_AUG_PER_SAMPLE;
+                if (Ld.stride == 1 && Ld.cout <= 64 && Ld.cin % 64 == 0 && !shared && Sb0.W == PW &&
+                    kp % PW == 0 && PH % wh == 0 && (kp / (PW * wh)) * PW * wh == kp)
+                    c->wkpx[op.layer] = kp;
+            }
+            const int blocks = (int)((npix + c->wkpx[op.layer] - 1) / c->wkpx[op.layer]);
             c->nsplit[op.layer] = conv2_wgrad_nsplit(base, blocks);
             if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
             pmax = std::max(pmax, (size_t)Sc * c->nsplit[op.layer] * Ld.cout * Kt);
@@ -143,7 +154,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             // dY as (64 co, pixel, co block, sample): one op loads 64 pixels × 128 co
             const uint64_t gd[4] = {64, npix, (uint64_t)(CO / 64), (uint64_t)Sc};
             const uint64_t gs[3] = {(uint64_t)CO * 2, 128, npix * CO * 2};
-            const uint32_t gbx[4] = {64, 64, (uint32_t)std::min(2, CO / 64), 1};
+            const uint32_t gbx[4] = {64, (uint32_t)c->wkpx[op.layer], (uint32_t)std::min(2, CO / 64), 1};
             if (!make_map_nd(&c->cmap_g[op.layer], c->rbf[gb].grad, 4, gd, gs, gbx))
                 return c->set_err(BNN_ERR_CUDA, "tensor map (dY) failed");
         }
@@ -182,8 +193,9 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_fwd[op.layer] = 1;
             // wgrad: 64-pixel blocks of the output pixel space
             if (64 % PW == 0 || PW % 64 == 0) {
-                const int wh = PW >= 64 ? 1 : std::min(PH, 64 / PW);
-                const int wn = 64 / (std::min(PW, 64) * wh);
+                const int kp = c->wkpx[op.layer];
+                const int wh = PW >= kp ? 1 : std::min(PH, kp / PW);
+                const int wn = kp / (std::min(PW, kp) * wh);
                 if (PW <= 64 && PH % wh == 0 && wn >= 1 && !shared) {
                     // X as (64 ci, W, H, image·sample, ci block): one op loads cbx channel blocks
                     const int Kt = Ld.k * Ld.k * Ld.cin;
@@ -191,7 +203,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                     (void)Kt;
                     const uint64_t xd[5] = {64, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B * Sc, (uint64_t)(Cp / 64)};
                     const uint64_t xs[4] = {(uint64_t)Cp * 2, (uint64_t)Sb.W * Cp * 2, (uint64_t)Sb.H * Sb.W * Cp * 2, 128};
-                    const uint32_t wbox[5] = {64, (uint32_t)std::min(PW, 64), (uint32_t)wh, (uint32_t)wn, (uint32_t)cbx};
+                    const uint32_t wbox[5] = {64, (uint32_t)std::min(PW, kp), (uint32_t)wh, (uint32_t)wn, (uint32_t)cbx};
                     if (!make_map_nd(&c->cmap_xw[op.layer], c->rbf[op.src].val, 5, xd, xs, wbox))
                         return c->set_err(BNN_ERR_CUDA, "tensor map (wgrad window) failed");
                     c->tma_wgrad[op.layer] = Ld.cin % 64 == 0 ? 1 : 0;
@@ -452,6 +464,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.tma_b = c->tma_wgrad[op.layer];
             const int taps = Ld.k * Ld.k, Kt = conv2_wgrad_cols(taps, Ld.cin, w.C_pad);
             w.n_tile = conv2_wgrad_ntile(Kt);
+            w.kpx = w.tma_b ? c->wkpx[op.layer] : 64;
+            if (w.kpx != c->wkpx[op.layer]) return c->set_err(BNN_ERR_CONFIG, "wgrad k-step / operand path mismatch");
             c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
             if (w.C_pad < 64) {
                 c->launch("wcomb", [&] {
