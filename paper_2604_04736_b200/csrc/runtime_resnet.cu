@@ -110,7 +110,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                 const int PW = D.W, PH = D.H, kp = 128;
                 const int wh = PW >= kp ? 1 : std::min(PH, kp / PW);
                 const bool shared = op.src == 0 && c->cfg.aug != BNN_AUG_PER_SAMPLE;
-                if (Ld.stride == 1 && Ld.cout <= 128 && Ld.cin % 64 == 0 && !shared && Sb0.W == PW &&
+                if (Ld.stride == 1 && Ld.cout <= 512 && Ld.cin % 64 == 0 && !shared && Sb0.W == PW &&
                     kp % PW == 0 && PH % wh == 0 && (kp / (PW * wh)) * PW * wh == kp)
                     c->wkpx[op.layer] = kp;
             }
