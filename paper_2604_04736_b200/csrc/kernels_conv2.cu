@@ -331,7 +331,11 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                         tma_load_5d(&wmap, &full[st], dB, 0, tap, cb * 64, n0 / 64, g.s);
                         if (a.tma_a) {
                             const int kh = tap / a.k, kw = tap - kh * a.k;
-                            tma_load_5d(&amap, &full[st], dA, cb * 64, a.pad - kw, y0 + a.pad - kh, img0, g.s);
+                            // dY window of this parity class: input pixel (s·y'+ph, s·x'+pw) takes
+                            // dY(y' + (ph+pad-kh)/s, x' + (pw+pad-kw)/s) — a plain shifted window
+                            const int ph = g.cls / a.stride, pw = g.cls - (g.cls / a.stride) * a.stride;
+                            tma_load_5d(&amap, &full[st], dA, cb * 64, (pw + a.pad - kw) / a.stride,
+                                        y0 + (ph + a.pad - kh) / a.stride, img0, g.s);
                         }
                     }
                 }
@@ -646,7 +650,9 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                         if (dup) tma_load_5d(&wmap, &full[st], dA + 8192, 0, tap, cb * 64, m0 / 64, g.s);
                         if (a.tma_a) {
                             const int kh = tap / a.k, kw = tap - kh * a.k;
-                            tma_load_5d(&bmap, &full[st], dB, cb * 64, a.pad - kw, y0 + a.pad - kh, img0, g.s);
+                            const int ph = g.cls / a.stride, pw = g.cls - (g.cls / a.stride) * a.stride;
+                            tma_load_5d(&bmap, &full[st], dB, cb * 64, (pw + a.pad - kw) / a.stride,
+                                        y0 + (ph + a.pad - kh) / a.stride, img0, g.s);
                         }
                     }
                 }

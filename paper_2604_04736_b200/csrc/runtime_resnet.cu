@@ -220,13 +220,38 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_dgrad[op.layer] = 1;
         }
     }
-    // conv2: 128-pixel windows for the A operand of stride-1 layers
+    // stride-2 dgrad: each input-pixel parity class reads a plain shifted window of dY over the
+    // output grid, so dY windows by TMA too (conv3: 256-pixel box; conv2: 128-pixel box below)
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op) || op.src == 0) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        if (Ld.stride != 2 || Sb.H != 2 * Db.H || Sb.W != 2 * Db.W) continue;
+        if (Db.C % 64 != 0 || Ld.cin % 64 != 0 || Sb.C > 128) continue;
+        const int PW = Db.W, PH = Db.H;
+        if (256 % PW != 0) continue;
+        const int th = std::min(PH, 256 / PW);
+        if (PH % th != 0) continue;
+        const uint32_t box[5] = {64, (uint32_t)PW, (uint32_t)th, (uint32_t)(256 / (PW * th)), 1};
+        const int gb = grad_src_buffer(c, op.dst);
+        const uint64_t dims[5] = {(uint64_t)Db.C, (uint64_t)Db.W, (uint64_t)Db.H, (uint64_t)B, (uint64_t)Sc};
+        const uint64_t str[4] = {(uint64_t)Db.C * 2, (uint64_t)Db.W * Db.C * 2, (uint64_t)Db.H * Db.W * Db.C * 2,
+                                 (uint64_t)B * Db.H * Db.W * Db.C * 2};
+        if (!make_map_nd(&c->cmap_bd[op.layer], c->rbf[gb].grad, 5, dims, str, box))
+            return c->set_err(BNN_ERR_CUDA, "tensor map (stride-2 dY window) failed");
+        c->tma_dgrad[op.layer] = 1;
+    }
+    // conv2: 128-pixel windows for the A operand (activation: stride 1; dY: stride 1 and 2)
     for (const ROp& op : c->rops) {
         if (op.type != 0 || is_fc(c, op)) continue;
         const LayerDesc& Ld = c->layers[op.layer];
-        if (Ld.stride != 1) continue;
         const RBuf& Sb = c->rbufs[op.src];
         const RBuf& Db = c->rbufs[op.dst];
+        // stride 1: activation and dY windows; stride 2 (Sb = 2·Db): the dY window of each
+        // input-pixel parity class (the forward's strided input stays a gather)
+        const bool s1 = Ld.stride == 1;
+        if (!s1 && (Ld.stride != 2 || Sb.H != 2 * Db.H || Sb.W != 2 * Db.W)) continue;
         const int PW = Db.W, PH = Db.H;
         if (128 % PW != 0) continue;
         const int th = std::min(PH, 128 / PW);
@@ -234,7 +259,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         const int tn = 128 / (PW * th);
         const uint32_t box[5] = {64, (uint32_t)PW, (uint32_t)th, (uint32_t)tn, 1};
         const int Cp = c->rbf[op.src].C_pad;
-        if (Cp % 64 == 0) {
+        if (s1 && Cp % 64 == 0) {
             const bool shared = op.src == 0 && c->cfg.aug != BNN_AUG_PER_SAMPLE;
             const uint64_t dims[5] = {(uint64_t)Cp, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B,
                                       (uint64_t)(shared ? 1 : Sc)};
