@@ -64,7 +64,7 @@ inline bool make_map(CUtensorMap* m, const void* base, int inner, int rows, int 
 
 // generic bf16 tensor map: rank ≤ 5, dims[0] contiguous, strides in bytes for dims 1..rank-1
 inline bool make_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                        const uint64_t* strides, const uint32_t* box) {
+                        const uint64_t* strides, const uint32_t* box, const uint32_t* estr = nullptr) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t d[5], st[4];
@@ -72,7 +72,7 @@ inline bool make_map_nd(CUtensorMap* m, const void* base, int rank, const uint64
     for (int i = 0; i < rank; ++i) {
         d[i] = dims[i];
         bx[i] = box[i];
-        es[i] = 1;
+        es[i] = estr ? estr[i] : 1;  // traversal stride (a strided conv window), box counts raw elements
         if (i > 0) st[i - 1] = strides[i - 1];
     }
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, bx, es,

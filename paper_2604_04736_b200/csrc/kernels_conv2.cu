@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                         if (a.tma_a) {
                             const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
-                            tma_load_5d(&amap, &full[st], dA, c0, kw - a.pad, y0 + kh - a.pad, img0,
+                            // stride s: the map traverses W and H with element stride s
+                            tma_load_5d(&amap, &full[st], dA, c0, kw - a.pad, a.stride * y0 + kh - a.pad, img0,
                                         a.src_stride_s == 0 ? 0 : g.s);
                         }
                     } else {
@@ -641,7 +642,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                         if (a.tma_a) {
                             const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
-                            tma_load_5d(&bmap, &full[st], dB, c0, kw - a.pad, y0 + kh - a.pad, img0,
+                            tma_load_5d(&bmap, &full[st], dB, c0, kw - a.pad, a.stride * y0 + kh - a.pad, img0,
                                         a.src_stride_s == 0 ? 0 : g.s);
                         }
                     } else {

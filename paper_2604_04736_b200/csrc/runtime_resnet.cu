@@ -220,6 +220,32 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_dgrad[op.layer] = 1;
         }
     }
+    // stride-2 forward: the input window of a 2-strided conv is a TMA box with element stride 2
+    // in W and H (box = 2·extent raw elements, every other one loaded); conv3 256-pixel and
+    // conv2 128-pixel tiles of the output grid
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op) || op.src == 0) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        const int Cp = c->rbf[op.src].C_pad;
+        if (Ld.stride != 2 || Cp % 64 != 0) continue;
+        const int PW = Db.W, PH = Db.H;
+        for (int px : {256, 128}) {
+            if (px % PW != 0 || 2 * PW > 256) continue;
+            const int th = std::min(PH, px / PW);
+            if (PH % th != 0 || 2 * th > 256) continue;
+            const uint32_t box[5] = {64, (uint32_t)(2 * PW), (uint32_t)(2 * th), (uint32_t)(px / (PW * th)), 1};
+            const uint32_t es[5] = {1, 2, 2, 1, 1};
+            const uint64_t dims[5] = {(uint64_t)Cp, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B, (uint64_t)Sc};
+            const uint64_t str[4] = {(uint64_t)Cp * 2, (uint64_t)Sb.W * Cp * 2, (uint64_t)Sb.H * Sb.W * Cp * 2,
+                                     (uint64_t)B * Sb.H * Sb.W * Cp * 2};
+            CUtensorMap* m = px == 256 ? &c->cmap_bf[op.layer] : &c->cmap_a2f[op.layer];
+            if (!make_map_nd(m, c->rbf[op.src].val, 5, dims, str, box, es))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (stride-2 activation window) failed");
+            (px == 256 ? c->tma_fwd : c->tma_a2f)[op.layer] = 1;
+        }
+    }
     // stride-2 dgrad: each input-pixel parity class reads a plain shifted window of dY over the
     // output grid, so dY windows by TMA too (conv3: 256-pixel box; conv2: 128-pixel box below)
     for (const ROp& op : c->rops) {

@@ -22,13 +22,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode() {
 }
 
 static bool make(CUtensorMap* m, void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                 const uint32_t* box) {
+                 const uint32_t* box, const uint32_t* estr = nullptr) {
     cuuint64_t d[5], st[4];
     cuuint32_t bx[5], es[5];
     for (int i = 0; i < rank; ++i) {
         d[i] = dims[i];
         bx[i] = box[i];
-        es[i] = 1;
+        es[i] = estr ? estr[i] : 1;
         if (i > 0) st[i - 1] = strides[i - 1];
     }
     CUresult r = encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -81,6 +81,7 @@ struct Case {
     std::vector<uint64_t> dims, strides;  // strides in bytes (rank-1)
     std::vector<uint32_t> box;
     std::vector<int> coord;
+    std::vector<uint32_t> es;  // element (traversal) strides; empty = all 1
 };
 
 int main() {
@@ -107,17 +108,26 @@ int main() {
          {C * 2, Kp * 2, 128, CO * Kp * 2}, {64, 1, 64, 4, 1}, {0, 4, 64, 4, 1}},
         {"dY 4D CO=64 view (box co-block 1)", 4, {64, npix, 1, 2}, {64 * 2, 128, npix * 64 * 2}, {64, 64, 1, 1},
          {0, 64, 0, 1}},
+        {"X 5D stride-2 window (64 ci, W=32, H=32, img, s) box 64x32x16x1x1, element strides 1,2,2,1,1", 5,
+         {64, 32, 32, 4, 2}, {64 * 2, 32 * 64 * 2, 32 * 32 * 64 * 2, 4 * 32 * 32 * 64 * 2}, {64, 32, 16, 1, 1},
+         {0, -1, 7, 2, 1}, {1, 2, 2, 1, 1}},
     };
     int fails = 0;
     for (auto& cs : cases) {
         CUtensorMap m;
         printf("%s\n", cs.name);
-        if (!make(&m, g, cs.rank, cs.dims.data(), cs.strides.data(), cs.box.data())) {
+        if (!make(&m, g, cs.rank, cs.dims.data(), cs.strides.data(), cs.box.data(),
+                  cs.es.empty() ? nullptr : cs.es.data())) {
             ++fails;
             continue;
         }
         uint32_t bytes = 2;
-        for (auto b : cs.box) bytes *= b;
+        uint32_t cnt[5];
+        for (size_t d = 0; d < cs.box.size(); ++d) {
+            const uint32_t e = cs.es.empty() ? 1 : cs.es[d];
+            cnt[d] = (cs.box[d] + e - 1) / e;
+            bytes *= cnt[d];
+        }
         int c[5] = {0, 0, 0, 0, 0};
         for (size_t i = 0; i < cs.coord.size(); ++i) c[i] = cs.coord[i];
         cudaMemset(st, 0, 4);
@@ -140,7 +150,7 @@ int main() {
             long off = 0;
             bool oob = false;
             for (int d = 0; d < R; ++d) {
-                const long x = (long)c[d] + idx[d];
+                const long x = (long)c[d] + (long)idx[d] * (cs.es.empty() ? 1 : cs.es[d]);
                 if (x < 0 || x >= (long)cs.dims[d]) oob = true;
                 off += x * (d == 0 ? 2 : (long)cs.strides[d - 1]);
             }
@@ -149,7 +159,7 @@ int main() {
             if (exp != got && bad++ < 5) printf("  mismatch at box elem %ld: got %g expected %g\n", k, got, exp);
             ++k;
             int d = 0;
-            while (d < R && ++idx[d] == (int)cs.box[d]) idx[d++] = 0;
+            while (d < R && ++idx[d] == (int)cnt[d]) idx[d++] = 0;
             if (d == R) break;
         }
         printf("  %s (%ld elements, %ld bad)\n", bad ? "FAIL" : "ok", k, bad);
