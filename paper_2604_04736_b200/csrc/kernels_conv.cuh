@@ -81,36 +81,6 @@ void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Co
 void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 int conv3_dgrad_parts(const Conv2Args& a);
 
-struct ConvTcArgs {
-    SampledLayer L;
-    SampleKeys kk;
-    int B, H, W, C, C_pad;  // conv input (per sample); C_pad = channel pitch of the input buffer
-    int OH, OW, CO;
-    int k, stride, pad;
-    int K_pad;
-    const __nv_bfloat16* src;  // fwd: input [s][B][H][W][C_pad]; dgrad: dY [s][B][OH][OW][CO]
-    int64_t src_stride_s;
-    __nv_bfloat16* out;        // fwd: Y [s][B][OH][OW][CO]; dgrad: dX [s][B][H][W][C]
-    int64_t out_stride_s;
-    const __nv_bfloat16* res;  // fwd: residual added before ReLU (or null)
-    int64_t res_stride_s;
-    const __nv_bfloat16* addsrc;  // dgrad: other contribution to dX added before the mask
-    int64_t addsrc_stride_s;
-    const __nv_bfloat16* mask;    // dgrad: ReLU mask source = conv input activation (or null)
-    int64_t mask_stride_s;
-    int relu;                  // fwd
-    float* bpart;              // dgrad: fp32 bias partials of the producer of the input
-    int64_t bpart_stride_s;    // per sample: (#classes·#pixel tiles·2)·C
-    int tma_b;                 // stride 1: B operand by 5-D TMA (bmap, box 64×tw×th×tn×1)
-};
-// fwd: D[co][pixel] over K = (kh, kw, ci); A = W scratch (TMA, K-major), B = gathered input
-void launch_conv_tc_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const ConvTcArgs& a, int S,
-                        cudaStream_t st);
-// dgrad: D[ci][input pixel] over K = (tap, co); A = W scratchᵀ per tap (TMA, MN-major),
-// B = gathered dY; stride-2 convs run per input-pixel parity class
-void launch_conv_tc_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const ConvTcArgs& a, int S,
-                          cudaStream_t st);
-int conv_dgrad_parts(const ConvTcArgs& a);  // bias partial count per sample
 
 struct ConvWgradArgs {
     SampledLayer L;
@@ -120,17 +90,14 @@ struct ConvWgradArgs {
     const __nv_bfloat16* X;  // conv input [s][B][H][W][C_pad]
     int64_t X_stride_s;
     float scale;
-    float* part;             // [nsplit][2][CO·k·k·C] partial acc (μ then ρ), already scaled
+    float* part;             // conv2 wgrad: [s][split][CO][cols] fp32 per-sample partials (unscaled);
+                             // SIMT wgrad: [nsplit][2][CO·k·k·C] (μ then ρ), scaled
     int nsplit;
-    int tma_b;               // stride 1: X window by 5-D TMA (xmap, box 64 × 64 pixels)
-    int n_tile;              // conv2 wgrad: parameter columns per tile (64 | 128 | 192 | 256)
-    int kpx;                 // pixels per k-step: 64, or 128 (TMA path, c_out ≤ 64)
+    int tma_b;               // stride 1: X window by 5-D TMA (xmap: 64 ci × kpx pixels × channel blocks)
+    int n_tile;              // conv2 wgrad: column-tile width (256; the last tile may be narrower)
+    int kpx;                 // pixels per k-step: 128 on the TMA path where the window fits, else 64
     int dbg;                 // timing experiments only (BNN_CONV_DEBUG); 0 in production
 };
-// wgrad (C % 64 == 0): D[co][tap·C + ci] = Σ_pix dY·X, per sample; acc_ρ partial += D ⊙ ε_s,
-// acc_μ partial = Σ_s D (tensor-core accumulated in TMEM). gmap: 3-D map over dY (CO, pix, s).
-void launch_conv_tc_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
-                          cudaStream_t st);
 void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off,
                                float* acc_mu, float* acc_rho, cudaStream_t st);
 // conv2 wgrad, phase 1 (tensor cores): per-sample, per-pixel-split weight gradients
