@@ -51,6 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     flags = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")] + ARCH
+    flags += os.environ.get("BNN_NVCC_FLAGS", "").split()  # experiments, e.g. -DBNN_WAIT_WATCHDOG=0
     objs = []
     procs = []
     for src in sources():

@@ -54,11 +54,13 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 constexpr uint64_t kWaitTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+// Spin waits (many threads, on the critical issue path) carry no watchdog: its loop counter
+// measurably slows the ALU-bound generator kernels (≈ 4.5 % on C2). Development builds give
+// the single-thread suspend-hint waits of the TMA / MMA roles one (a lost TMA transaction
+// stalls them too), which turns a hang into a trap with a message.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    uint32_t n = 0;
     while (!mbar_try_wait(a, parity)) {
-        if (++n == (1u << 30)) mbar_timeout(a, parity);  // ≫ seconds of polling
     }
 }
 
@@ -77,10 +79,15 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t pari
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait_sleep(a, parity)) return;
+#ifdef BNN_WATCHDOG  // development builds: BNN_NVCC_FLAGS=-DBNN_WATCHDOG (costs ≈ 2 % on C2)
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait_sleep(a, parity)) {
         if (globaltimer_ns() - t0 > kWaitTimeoutNs) mbar_timeout(a, parity);
     }
+#else
+    while (!mbar_try_wait_sleep(a, parity)) {
+    }
+#endif
 }
 
 // ------------------------------------------------------------------ proxy fences
