@@ -245,7 +245,7 @@ int alloc_resnet_bf16(bnn_ctx* c);
 int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                       const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
                       uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss);
-int resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B,
+void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B,
                          uint64_t seed, uint32_t step, uint32_t s0, bool aug);
 SampledLayer sampled(const bnn_ctx* c, int l, const float* mu);
 

@@ -70,9 +70,6 @@ struct Conv2Args {
     uint32_t* mbits_out;       // fwd (relu): ReLU bitmask of the stored output, bit j of word
                                //   [pixel][c/32] = (stored bf16 of channel c > 0); or null
     const uint32_t* mbits;     // dgrad: bitmask of the layer input (replaces `mask` when set)
-    int eop_tma;               // conv3, ≤ 64 channels, stride 1: the epilogue's residual / other
-                               //   contribution tile arrives by TMA (emap) and the bitmask rows by a
-                               //   bulk copy, into shared memory, ahead of the tile's epilogue
 };
 void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
 void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
@@ -80,10 +77,8 @@ int conv2_dgrad_parts(const Conv2Args& a);
 // conv3: M = 128 output channels (weights: fwd W scratch K-major map, box 64 × 64; dgrad the
 // transposed 4-D map, box 64 × 1 × 64 × 1), N = 256 pixels (tma_a: 5-D 256-pixel window map,
 // else cp.async gather). For layers with ≤ 128 output channels.
-void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const CUtensorMap& emap, const Conv2Args& a,
-                      cudaStream_t st);
-void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const CUtensorMap& emap,
-                        const Conv2Args& a, cudaStream_t st);
+void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
+void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 int conv3_dgrad_parts(const Conv2Args& a);
 
 

@@ -546,33 +546,27 @@ constexpr int kStages = 3;  // pipeline depth is not the limiter (BNN_CONV_STAGE
 constexpr int kAStage = 128 * 64 * 2;  // 16 KB weights (128 channel rows)
 constexpr int kBStage = 256 * 64 * 2;  // 32 KB pixel window (256 rows)
 constexpr int kTrans = kEpiWarps * 32 * 33 * 4;
-constexpr int kEop = 256 * 64 * 2;     // epilogue operand rows (64-channel layers): 32 KB
-constexpr int kEbits = 256 * 2 * 4;    // their ReLU bitmask words
-constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + kEop + kEbits + kTrans + 512 + 2048;
+constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + kTrans + 512 + 2048;
 static_assert(kSmem <= 227 * 1024, "conv3 shared memory");
 }  // namespace c3
 
 template <int MODE>
 __global__ void __launch_bounds__(c3::kThreads, 1)
     conv3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
-                 const __grid_constant__ CUtensorMap emap, const Conv2Args a) {
+                 const Conv2Args a) {
     using namespace c3;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * kAStage;
-    uint8_t* eop = sB + kStages * kBStage;  // 1024-aligned (SW128 TMA destination)
-    uint32_t* ebits = reinterpret_cast<uint32_t*>(eop + kEop);
-    float* trans = reinterpret_cast<float*>(eop + kEop + kEbits);
+    float* trans = reinterpret_cast<float*>(sB + kStages * kBStage);
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(trans) + kTrans);
     uint64_t* full = bars;
     uint64_t* empty = bars + kStages;
     uint64_t* tfull = bars + 2 * kStages;
     uint64_t* tempty = bars + 2 * kStages + 2;
-    uint64_t* efull = bars + 2 * kStages + 4;
-    uint64_t* eempty = bars + 2 * kStages + 5;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
     int* staps = reinterpret_cast<int*>(tslot + 4);  // [4 classes][9 taps] + counts
     float* bred = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [2][8 warps][32]
 
@@ -598,8 +592,6 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], kEpiWarps);
         }
-        mbar_init(efull, 1);
-        mbar_init(eempty, kEpiWarps);
         mbar_fence_init();
         for (int cl = 0; cl < ncls; ++cl) {
             const int ph = cl / a.stride, pw = cl % a.stride;
@@ -702,28 +694,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
         }
         __syncwarp();
     } else if (warp >= kEpiWarps) {
-        // ------------------------------------------------ epilogue operand producer (TMA path: the
-        // gather warps are idle): residual / other-contribution rows of the tile by one TMA op,
-        // the bitmask rows by one bulk copy, into a single buffer the epilogue releases per tile
-        if (a.eop_tma && warp == kEpiWarps && lane == 0) {
-            const bool rows = MODE == 0 ? a.res != nullptr : a.addsrc != nullptr;
-            const bool bits = MODE == 1 && a.mbits != nullptr;
-            const int cw = Mtot >> 5;  // bitmask words per pixel
-            tma_prefetch_desc(&emap);
-            int tl = 0;
-            for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
-                const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
-                const int p0 = g.ptile * 256;
-                const int img0 = p0 / (PH * PW), y0 = (p0 - img0 * PH * PW) / PW;
-                const uint32_t bbytes = bits ? (((uint32_t)min(256, P - p0) * cw * 4 + 15u) & ~15u) : 0u;
-                mbar_wait_sleep(eempty, (tl & 1) ^ 1);
-                mbar_arrive_expect_tx(efull, (rows ? kEop : 0) + bbytes);
-                if (rows) tma_load_5d(&emap, efull, eop, 0, 0, y0, img0, g.s);
-                if (bits)
-                    bulk_load(efull, ebits, a.mbits + (((int64_t)g.s * a.out_stride_s + (int64_t)p0 * Mtot) >> 5),
-                              bbytes);
-            }
-        }
+        // ------------------------------------------------ gather producers (stride 2 / stem): 256 rows
         if (!a.tma_a) {
             const int gt = threadIdx.x - kEpiWarps * 32;  // pixel rows gt and gt + 128
             const int cpb = a.C_pad >> 6;
@@ -846,11 +817,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 }
                 if (MODE == 1 && a.mbits) x2 = __ldg(a.mbits + ((so + ro + ch0) >> 5));
             };
-            if (a.eop_tma) {
-                mbar_wait(efull, tl & 1);  // the tile's operand rows are in shared memory
-            } else {
-                load_ops(c_first, o1, o2);  // independent of the accumulator: in flight while the MMAs finish
-            }
+            load_ops(c_first, o1, o2);  // independent of the accumulator: in flight while the MMAs finish
             mbar_wait(&tfull[buf], (tl >> 1) & 1);
             tc_fence_after();
             for (int c = c_first; c < 8; c += c_step) {  // 32 pixels per chunk
@@ -875,23 +842,8 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 __syncwarp();
                 bool pv;
                 const int64_t rowoff = row_of(c, pv);
-                if (a.eop_tma) {  // operand rows from shared memory (SW128 rows of 64 channels)
-                    const int r = 32 * c + lane, k0 = (ch0 & 63) >> 3;
-                    const uint32_t rb = smem_u32(eop) + r * 128;
-                    if (MODE == 0 ? a.res != nullptr : a.addsrc != nullptr) {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(o1[i].x), "=r"(o1[i].y), "=r"(o1[i].z), "=r"(o1[i].w)
-                                         : "r"(rb + ((((k0 + i) ^ (r & 7))) << 4)));
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) o1[i] = make_uint4(0u, 0u, 0u, 0u);
-                    }
-                    o2 = (MODE == 1 && a.mbits) ? ebits[r * (Mtot >> 5) + ((ch0 & 63) >> 5)] : 0xFFFFFFFFu;
-                }
                 epi_apply32<MODE>(a, v, pv, rowoff, so, ch0, o1, o2);
-                if (!a.eop_tma && c + c_step < 8) load_ops(c + c_step, o1, o2);  // in flight during the next TMEM load
+                if (c + c_step < 8) load_ops(c + c_step, o1, o2);  // in flight during the next TMEM load
                 if (MODE == 1 && a.bpart) bsum += warp_transpose_sum(v, lane);
             }
             if (MODE == 1 && a.bpart) {  // combine the warps of each channel group in a fixed order
@@ -907,10 +859,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&tempty[buf]);
-                if (a.eop_tma) mbar_arrive(eempty);
-            }
+            if (lane == 0) mbar_arrive(&tempty[buf]);
         }
     }
     tc_fence_before();
@@ -927,8 +876,7 @@ int conv3_dgrad_parts(const Conv2Args& a) {
 }
 
 template <int MODE>
-static void launch_conv3(const CUtensorMap& wmap, const CUtensorMap& bmap, const CUtensorMap& emap, const Conv2Args& a,
-                         cudaStream_t st) {
+static void launch_conv3(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(conv3_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, c3::kSmem);
@@ -941,16 +889,14 @@ static void launch_conv3(const CUtensorMap& wmap, const CUtensorMap& bmap, const
     const int T = a.S * ncls * ((P + 255) / 256) * ((Mtot + 127) / 128);
     Conv2Args b = a;
     b.dbg = conv_debug();
-    conv3_kernel<MODE><<<std::min(T, kNumSMs), c3::kThreads, c3::kSmem, st>>>(wmap, bmap, emap, b);
+    conv3_kernel<MODE><<<std::min(T, kNumSMs), c3::kThreads, c3::kSmem, st>>>(wmap, bmap, b);
 }
 
-void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const CUtensorMap& emap, const Conv2Args& a,
-                      cudaStream_t st) {
-    launch_conv3<0>(wmap, bmap, emap, a, st);
+void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+    launch_conv3<0>(wmap, bmap, a, st);
 }
-void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const CUtensorMap& emap,
-                        const Conv2Args& a, cudaStream_t st) {
-    launch_conv3<1>(wmapT, bmap, emap, a, st);
+void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+    launch_conv3<1>(wmapT, bmap, a, st);
 }
 
 // ============================================================================ wgrad

@@ -724,9 +724,7 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
     SampleKeys kk{make_key(seed), step, (uint32_t)(c->kidx * S_loc)};
     const bool is_mlp = c->model.kind == BNN_MODEL_MLP;
     if (!is_mlp && !c->bf16) resnet_forward(c, mu, kk, S_loc, B, x, 0);
-    if (!is_mlp && c->bf16) {
-        if (int rc = resnet_bf16_forward(c, mu, x, S_loc, B, seed, step, kk.s0, false)) return rc;
-    }
+    if (!is_mlp && c->bf16) resnet_bf16_forward(c, mu, x, S_loc, B, seed, step, kk.s0, false);
     const int nb = (int)round_up(std::min(B, 256), 16);
     for (int l = 0; is_mlp && l < L; ++l) {
         if (!c->bf16) {

@@ -54,7 +54,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         if (!c->alloc(&b.val, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (activations)");
         if (i != 0 && !c->alloc(&b.grad, n)) return c->set_err(BNN_ERR_CUDA, "out of memory (gradients)");
         if (i != 0 && i != gbuf && R.C % 32 == 0 && c->rbufs[i].H > 1) {
-            if (!c->alloc(&b.mbits, n / 32 + 16)) return c->set_err(BNN_ERR_CUDA, "out of memory (masks)");
+            if (!c->alloc(&b.mbits, n / 32)) return c->set_err(BNN_ERR_CUDA, "out of memory (masks)");
         }
         if (i != 0 && i != gbuf) {
             const int64_t npix = (int64_t)B * R.H * R.W;
@@ -319,23 +319,8 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     return BNN_OK;
 }
 
-// 256-pixel row tile (64 channels) of a bf16 NHWC buffer [s][B][H][W][C]: the conv3 epilogue's
-// residual / other-contribution operand, loaded by TMA at the same tiles the kernel walks
-static bool eop_map(bnn_ctx* c, CUtensorMap* m, const __nv_bfloat16* base, const RBuf& R, int B, int Sc) {
-    (void)c;
-    const int PW = R.W, PH = R.H;
-    if (256 % PW != 0) return false;
-    const int th = std::min(PH, 256 / PW);
-    if (PH % th != 0) return false;
-    const uint32_t box[5] = {64, (uint32_t)PW, (uint32_t)th, (uint32_t)(256 / (PW * th)), 1};
-    const uint64_t dims[5] = {(uint64_t)R.C, (uint64_t)R.W, (uint64_t)R.H, (uint64_t)B, (uint64_t)Sc};
-    const uint64_t str[4] = {(uint64_t)R.C * 2, (uint64_t)R.W * R.C * 2, (uint64_t)R.H * R.W * R.C * 2,
-                             (uint64_t)B * R.H * R.W * R.C * 2};
-    return make_map_nd(m, base, 5, dims, str, box);
-}
-
-int resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B, uint64_t seed,
-                        uint32_t step, uint32_t s0, bool aug) {
+void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B, uint64_t seed,
+                         uint32_t step, uint32_t s0, bool aug) {
     cudaStream_t st = c->st;
     SampleKeys kk{make_key(seed), step, s0};
     const RBuf& in = c->rbufs[0];
@@ -407,20 +392,11 @@ int resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int
         a.mbits_out = op.relu ? c->rbf[op.dst].mbits : nullptr;
         if (Db.C <= 128) {  // channels on M, 256 pixels on N (full-width MMA)
             a.tma_a = c->tma_fwd[op.layer];
-            CUtensorMap emap{};
-            if (a.tma_a && Db.C <= 64 && Ld.stride == 1 && a.res) {  // residual rows by TMA (64-ch layers)
-                if (!eop_map(c, &emap, a.res, Db, B, Sc)) return c->set_err(BNN_ERR_CUDA, "tensor map (residual rows) failed");
-                a.eop_tma = 1;
-            }
-            c->launch("fwd", [&] {
-                launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], c->cmap_bf[op.layer], emap,
-                                 a, st);
-            });
+            c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], c->cmap_bf[op.layer], a, st); });
         } else {
             c->launch("fwd", [&] { launch_conv2_fwd(c->cmap_a2f[op.layer], c->cmap_w2[op.layer], a, st); });
         }
     }
-    return BNN_OK;
 }
 
 int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
@@ -431,7 +407,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
     const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
                                                      : 1.0f / ((float)S_glob * B_glob * c->O);
     const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
-    if (int rc = resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug)) return rc;
+    resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug);
     const RBuf& in = c->rbufs[0];
     const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * c->rbf[0].C_pad : 0;
     const int O = c->O, ldO = (int)round_up(O, 8);
@@ -608,13 +584,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             c->rbf[op.src].nparts = np;
         }
         if (m_chan) {
-            CUtensorMap emap{};
-            if (a.tma_a && Sb.C <= 64 && Ld.stride == 1 && (a.addsrc || a.mbits)) {  // operand rows by TMA
-                if (a.addsrc && !eop_map(c, &emap, a.addsrc, Sb, B, Sc))
-                    return c->set_err(BNN_ERR_CUDA, "tensor map (dgrad addend rows) failed");
-                a.eop_tma = 1;
-            }
-            c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], c->cmap_bd[op.layer], emap, a, st); });
+            c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], c->cmap_bd[op.layer], a, st); });
         } else {
             c->launch("dgrad", [&] { launch_conv2_dgrad(c->cmap_a2d[op.layer], c->cmap_wT[op.layer], a, st); });
         }

@@ -123,14 +123,6 @@ __device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint64_t* ba
         "r"(c3), "r"(c4)
         : "memory");
 }
-// contiguous bulk copy global → shared (bytes: multiple of 16, both addresses 16-B aligned)
-__device__ __forceinline__ void bulk_load(uint64_t* bar, void* dst, const void* src, uint32_t bytes) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 // 16-byte global→shared async copy; src_bytes = 0 writes zeros (implicit zero padding)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
