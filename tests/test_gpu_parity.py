@@ -402,3 +402,27 @@ def test_cnn_bf16_full_size_c3_sampled_examples():
                 gerr = rel(grads[l][k], d[True, True][o])
                 gspread = rel(d[True, True][o], d[False, True][o])
                 assert gerr <= max(2e-2, 3 * gspread), (s, b, l, gerr, gspread)
+
+
+def test_cnn_bf16_sample_sharded_virtual_ranks_equal_single_rank():
+    """BF16 CNN: K = 2 sample groups × G = 2 data groups (C5's grid shape) summed through
+    bnn_finalize equal the single rank within 1e-5 (north_star: sharded = single), with
+    per-sample augmentation keyed by global (s, b)."""
+    native = _native()
+    model, B, S, D = dict(BF16_CNN, in_h=8, in_w=8), 4, 4, 100.0
+    mu, rho, x, yc, _ = _inputs(model, B, "init")
+    mu_d, rho_d = _dev(mu), _dev(rho)
+    single = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=D, aug="per_sample")
+    l1, g1, r1 = single.finalize(mu_d, rho_d, single.elbo_partial(mu_d, rho_d, _dev(x), _dev(yc), B, S, 9, 4))
+    total = None
+    for rank in range(4):
+        ctx = native.Context(model, precision="bf16", mode="hybrid", K=2, G=2, rank=rank, world=4,
+                             max_B_loc=B // 2, max_S_loc=S // 2, dataset_size=D, aug="per_sample")
+        g = rank % 2
+        acc = ctx.elbo_partial(mu_d, rho_d, _dev(x[2 * g:2 * g + 2]), _dev(yc[2 * g:2 * g + 2]), B, S, 9, 4)
+        total = acc if total is None else total + acc
+    l2, g2, r2 = single.finalize(mu_d, rho_d, total)
+    torch.cuda.synchronize()
+    assert abs(l1.item() - l2.item()) <= 1e-5 * abs(l1.item())
+    assert _rel(g2.cpu().numpy(), g1.cpu().numpy()) < 1e-5
+    assert _rel(r2.cpu().numpy(), r1.cpu().numpy()) < 1e-5
