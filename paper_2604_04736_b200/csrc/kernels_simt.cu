@@ -569,21 +569,22 @@ void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B,
 // dgrad epilogue; the loss head's fp32 seed for the last layer).
 //   phase A: db[s][n] = Σ_p parts[s][p][n]
 //   phase B: acc_μ[b_n] += scale·Σ_s db[s][n];  acc_ρ[b_n] += scale·Σ_s db[s][n]·ε_s(t_b, 0, n)
-constexpr int kBiasGroups = 32;
+constexpr int kBiasGroups = 32;  // at most; a launch uses G = blockDim.x / 32 part groups
 __global__ void __launch_bounds__(32 * kBiasGroups)
     bias_reduce_kernel(SampledLayer L, SampleKeys kk, const float* __restrict__ parts, int nparts, int ldp,
                        int64_t strideS, int S, float* __restrict__ db) {
     __shared__ float red[kBiasGroups][33];
+    const int G = blockDim.x >> 5;
     const int tx = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int n = blockIdx.x * 32 + tx, s = blockIdx.y;
     float acc = 0.0f;
-    if (n < L.N) {  // group g: parts g, g+32, … (fixed order ⇒ deterministic)
+    if (n < L.N) {  // group g: parts g, g+G, … (fixed order ⇒ deterministic)
         const float* p = parts + s * strideS + n;
         float a0 = 0.0f, a1 = 0.0f;
         int i = g;
-        for (; i + kBiasGroups < nparts; i += 2 * kBiasGroups) {
+        for (; i + G < nparts; i += 2 * G) {
             a0 += __ldg(p + (int64_t)i * ldp);
-            a1 += __ldg(p + (int64_t)(i + kBiasGroups) * ldp);
+            a1 += __ldg(p + (int64_t)(i + G) * ldp);
         }
         if (i < nparts) a0 += __ldg(p + (int64_t)i * ldp);
         acc = a0 + a1;
@@ -592,8 +593,7 @@ __global__ void __launch_bounds__(32 * kBiasGroups)
     __syncthreads();
     if (g == 0 && n < L.N) {
         float t = 0.0f;
-#pragma unroll
-        for (int j = 0; j < kBiasGroups; ++j) t += red[j][tx];
+        for (int j = 0; j < G; ++j) t += red[j][tx];
         db[(int64_t)s * L.N + n] = t;
         db[(int64_t)(S + s) * L.N + n] = t * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n);
     }
@@ -629,7 +629,9 @@ void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const f
                       int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
                       float* acc_mu, float* acc_rho, cudaStream_t st) {
     dim3 grid((L.N + 31) / 32, S);
-    bias_reduce_kernel<<<grid, 32 * kBiasGroups, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
+    int G = 1;  // part groups per block: enough for the part count (≤ 32), fewer threads when few parts
+    while (G < kBiasGroups && G < nparts) G <<= 1;
+    bias_reduce_kernel<<<grid, 32 * G, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
     bias_acc_kernel<<<(L.N + 31) / 32, 256, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
 }
 
