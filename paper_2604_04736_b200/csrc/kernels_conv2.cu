@@ -1220,6 +1220,63 @@ __global__ void __launch_bounds__(256)
     *ar = make_float4(fmaf(scale, r.x, y0.x), fmaf(scale, r.y, y0.y), fmaf(scale, r.z, y0.z), fmaf(scale, r.w, y0.w));
 }
 
+// Small layers (few column quads, many pixel splits): block = 32 column quads × 8 sample lanes;
+// a thread sums its (quad, sample) over the splits (four independent chains, fixed order),
+// weights by ε_s, and the 8 sample lanes are combined in a fixed order ⇒ deterministic.
+__global__ void __launch_bounds__(256)
+    wgrad_eps_combine_lanes_kernel(SampledLayer L, SampleKeys kk, int S, int nsplit, int CO, int Kt,
+                                   const float* __restrict__ part, float scale, float* __restrict__ acc_mu,
+                                   float* __restrict__ acc_rho) {
+    __shared__ float4 red[2][8][32];
+    const int kq = Kt / 4;
+    const int64_t nq = (int64_t)CO * kq;
+    const int64_t ss = (int64_t)CO * Kt;
+    const int tx = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + tx;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f), r = m;
+    int co = 0, cq = 0;
+    if (i < nq) {
+        co = (int)(i / kq);
+        cq = (int)(i - (int64_t)co * kq);
+        const float* p = part + (int64_t)co * Kt + 4 * cq;
+        for (int s = sl; s < S; s += 8) {
+            float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+            const float* ps = p + (int64_t)s * nsplit * ss;
+            int sp = 0;
+            for (; sp + 2 <= nsplit; sp += 2) {
+                const float4 e0 = __ldcs(reinterpret_cast<const float4*>(ps + sp * ss));
+                const float4 e1 = __ldcs(reinterpret_cast<const float4*>(ps + (sp + 1) * ss));
+                q0.x += e0.x; q0.y += e0.y; q0.z += e0.z; q0.w += e0.w;
+                q1.x += e1.x; q1.y += e1.y; q1.z += e1.z; q1.w += e1.w;
+            }
+            if (sp < nsplit) {
+                const float4 e0 = __ldcs(reinterpret_cast<const float4*>(ps + sp * ss));
+                q0.x += e0.x; q0.y += e0.y; q0.z += e0.z; q0.w += e0.w;
+            }
+            const float4 d = make_float4(q0.x + q1.x, q0.y + q1.y, q0.z + q1.z, q0.w + q1.w);
+            const float4 e = eps4(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)cq);
+            m.x += d.x; m.y += d.y; m.z += d.z; m.w += d.w;
+            r.x = fmaf(d.x, e.x, r.x); r.y = fmaf(d.y, e.y, r.y);
+            r.z = fmaf(d.z, e.z, r.z); r.w = fmaf(d.w, e.w, r.w);
+        }
+    }
+    red[0][sl][tx] = m;
+    red[1][sl][tx] = r;
+    __syncthreads();
+    if (sl == 0 && i < nq) {
+        for (int j = 1; j < 8; ++j) {
+            const float4 a = red[0][j][tx], b = red[1][j][tx];
+            m.x += a.x; m.y += a.y; m.z += a.z; m.w += a.w;
+            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+        }
+        float4* am = reinterpret_cast<float4*>(acc_mu + L.off_w + (int64_t)co * Kt + 4 * cq);
+        float4* ar = reinterpret_cast<float4*>(acc_rho + L.off_w + (int64_t)co * Kt + 4 * cq);
+        const float4 x0 = *am, y0 = *ar;
+        *am = make_float4(fmaf(scale, m.x, x0.x), fmaf(scale, m.y, x0.y), fmaf(scale, m.z, x0.z), fmaf(scale, m.w, x0.w));
+        *ar = make_float4(fmaf(scale, r.x, y0.x), fmaf(scale, r.y, y0.y), fmaf(scale, r.z, y0.z), fmaf(scale, r.w, y0.w));
+    }
+}
+
 // The stem: partial columns are the padded tap·8 + ci, parameter columns tap·C + ci. Block =
 // 32 parameters × 8 sample lanes; each thread sums its (parameter, sample) over the splits
 // (four independent chains, fixed order), the sample lanes are combined in a fixed order.
@@ -1295,6 +1352,11 @@ int conv2_wgrad_nsplit(int base, int blocks) {
 void launch_wgrad_eps_combine(const SampledLayer& L, const SampleKeys& kk, int S, int nsplit, int CO, int Kt,
                               const float* part, float scale, float* acc_mu, float* acc_rho, cudaStream_t st) {
     const int64_t nq = (int64_t)CO * Kt / 4;
+    if (nq < (int64_t)kNumSMs * 256 && nsplit > 1) {  // few quads: spread the samples over lanes too
+        wgrad_eps_combine_lanes_kernel<<<(int)((nq + 31) / 32), 256, 0, st>>>(L, kk, S, nsplit, CO, Kt, part, scale,
+                                                                              acc_mu, acc_rho);
+        return;
+    }
     wgrad_eps_combine_kernel<<<(int)((nq + 255) / 256), 256, 0, st>>>(L, kk, S, nsplit, CO, Kt, part, scale, acc_mu,
                                                                      acc_rho);
 }
