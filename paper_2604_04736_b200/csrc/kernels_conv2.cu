@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                  const Conv2Args a, const int g_max_stages_arg) {
     using namespace c2;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
+    // address space, so plain loads/stores through it compile to LDS/STS
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     const int kBStage = a.n_tile * 128;
     const int kStages = min(g_max_stages_arg, kData / (kAStage + kBStage));
@@ -556,8 +557,9 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                  const Conv2Args a) {
     using namespace c3;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
+    // address space, so plain loads/stores through it compile to LDS/STS
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * kAStage;
     float* trans = reinterpret_cast<float*>(sB + kStages * kBStage);
@@ -831,14 +833,11 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 }
                 if (!active) continue;
                 // v[j] = channel (ch0 + lane) at pixel 32c + j (+ its bias)  →  tr[j][lane]
-                const uint32_t trb = smem_u32(tr);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(trb + 4u * (j * 33 + lane)), "f"(v[j] + bias) : "memory");
+                for (int j = 0; j < 32; ++j) tr[j * 33 + lane] = v[j] + bias;
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[j]) : "r"(trb + 4u * (lane * 33 + j)) : "memory");
+                for (int j = 0; j < 32; ++j) v[j] = tr[lane * 33 + j];
                 __syncwarp();
                 bool pv;
                 const int64_t rowoff = row_of(c, pv);
@@ -922,8 +921,9 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                        const ConvWgradArgs a, const int g_max_stages_arg) {
     using namespace w2;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
+    // address space, so plain loads/stores through it compile to LDS/STS
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     // k-step = kpx pixels (64, or 128 for 64-channel stride-1 layers: half the TMA ops per byte);
     // one 64-wide MN block of an operand is kpx K-rows × 128 B

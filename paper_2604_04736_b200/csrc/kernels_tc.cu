@@ -102,8 +102,9 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     gen_gemm_kernel(const __grid_constant__ CUtensorMap tmB, const TcGenArgs a) {
     using namespace gen;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
+    // address space, so plain loads/stores through it compile to LDS/STS
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
@@ -321,8 +322,9 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
     wgrad_tc_kernel(const __grid_constant__ TcWgradMaps maps, const TcWgradArgs a) {
     using namespace wg;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
+    // address space, so plain loads/stores through it compile to LDS/STS
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
