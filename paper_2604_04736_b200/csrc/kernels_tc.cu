@@ -77,7 +77,7 @@ __device__ __forceinline__ uint2 gen_w4(const SampledLayer& L, const SampleKeys&
 
 // Fast path: interior tile, 16-byte aligned μ/σ rows, no bounds checks.
 __device__ __forceinline__ uint2 gen_w4_fast(const float* __restrict__ mu,
-                                             const float* __restrict__ sigma, EpsKey key,
+                                             const float* __restrict__ sigma, const EpsKey& key,
                                              uint32_t step, uint32_t w3, uint32_t n, uint32_t cq) {
     const float4 m = __ldg(reinterpret_cast<const float4*>(mu));
     const float4 s = __ldg(reinterpret_cast<const float4*>(sigma));
@@ -310,15 +310,20 @@ void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStre
 
 // ============================================================================ K5
 namespace wg {
-constexpr int kEpiWarps = 8;
+// CTA = 128 n × 128 k weight tile, all S samples; one CTA per SM (TMEM: 2 × 128 columns of
+// per-sample dW_s + 128 columns of Σ_s dW_s). N = 128 MMAs: a tcgen05.mma costs ≈ 130 cycles
+// for any N ≤ 256 (profiles/r01/final/mma_bench.txt), so N = 64 tiles made this kernel
+// MMA-issue-bound; at N = 128 the two MMAs per K = 16 step hide under the ε regeneration.
+constexpr int kEpiWarps = 16;
 constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 constexpr int kStages = 4;
+constexpr int kTileK = 128;
 constexpr int kAStage = 64 * 128 * 2;  // G_sᵀ: 64 b × 128 n (two 64-wide MN blocks)
-constexpr int kBStage = 64 * 64 * 2;   // X_s : 64 b × 64 k
+constexpr int kBStage = 64 * 128 * 2;  // X_s : 64 b × 128 k (two 64-wide MN blocks)
 constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
 }  // namespace wg
 
-__global__ void __launch_bounds__(wg::kThreads, 2)
+__global__ void __launch_bounds__(wg::kThreads, 1)
     wgrad_tc_kernel(const __grid_constant__ TcWgradMaps maps, const TcWgradArgs a) {
     using namespace wg;
     extern __shared__ uint8_t smem_raw[];
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
     const WgradLayer& W = a.lay[li];
     const SampledLayer& L = W.L;
     const int tile = blockIdx.x - W.tile_base;
-    const int n0 = (tile / W.ktiles) * 128, k0 = (tile % W.ktiles) * 64;
+    const int n0 = (tile / W.ktiles) * 128, k0 = (tile % W.ktiles) * kTileK;
     const CUtensorMap* mapG = &maps.g[li];
     const CUtensorMap* mapX = &maps.x[li];
     const int nbb = (a.B + 63) / 64;
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
         }
         mbar_fence_init();
     }
-    if (warp == kEpiWarps + 1) tmem_alloc(tslot, 256);
+    if (warp == kEpiWarps + 1) tmem_alloc(tslot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -380,15 +385,16 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
                     uint8_t* a_st = sA + st * kAStage;
                     tma_load_3d(mapG, &full[st], a_st, n0, 64 * bb, s);
                     tma_load_3d(mapG, &full[st], a_st + 8192, n0 + 64, 64 * bb, s);
-                    tma_load_3d(mapX, &full[st], sB + st * kBStage, k0, 64 * bb,
-                                W.b_shared ? 0 : s);
+                    uint8_t* b_st = sB + st * kBStage;
+                    tma_load_3d(mapX, &full[st], b_st, k0, 64 * bb, W.b_shared ? 0 : s);
+                    tma_load_3d(mapX, &full[st], b_st + 8192, k0 + 64, 64 * bb, W.b_shared ? 0 : s);
                 }
         }
         __syncwarp();
     } else if (warp == kEpiWarps + 1) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+            const uint32_t idesc = idesc_bf16(128, kTileK, 1, 1);
             int it = 0;
             for (int s = 0; s < S; ++s) {
                 const int buf = s & 1;
@@ -406,9 +412,9 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
                         const uint64_t ad = sdesc_sw128(aBase + 2048 * q, 8192, 1024);
                         const uint64_t bd = sdesc_sw128(bBase + 2048 * q, 8192, 1024);
                         // per-sample dW_s (double-buffered) for the ε-weighted acc_ρ ...
-                        mma_bf16(tmem + buf * 64, ad, bd, idesc, (bb | q) != 0 ? 1u : 0u);
+                        mma_bf16(tmem + buf * kTileK, ad, bd, idesc, (bb | q) != 0 ? 1u : 0u);
                         // ... and acc_μ = Σ_s dW_s accumulated by the tensor core itself
-                        mma_bf16(tmem + 128, ad, bd, idesc, (s | bb | q) != 0 ? 1u : 0u);
+                        mma_bf16(tmem + 2 * kTileK, ad, bd, idesc, (s | bb | q) != 0 ? 1u : 0u);
                     }
                     mma_commit(&empty[st]);
                 }
@@ -431,7 +437,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
             tc_fence_after();
             float d[32];
             __syncwarp();
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 64 + 32 * h, d);
+            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kTileK + 32 * h, d);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -469,7 +475,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
         // acc_μ from TMEM (complete once the last sample's commit has landed)
         float am[32];
         __syncwarp();
-        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 128 + 32 * h, am);
+        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 2 * kTileK + 32 * h, am);
         if (S == 0) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) am[j] = 0.0f;
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(wg::kThreads, 2)
     __syncthreads();
     if (warp == kEpiWarps + 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 

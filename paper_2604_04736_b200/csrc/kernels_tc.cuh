@@ -32,7 +32,7 @@ struct TcGenArgs {
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
 
-// K5: grouped over up to 4 layers; CTA = 128 n × 64 k tile, loops over all S samples.
+// K5: grouped over up to 4 layers; CTA = 128 n × 128 k tile, loops over all S samples.
 constexpr int kMaxWgradLayers = 4;
 struct WgradLayer {
     SampledLayer L;
