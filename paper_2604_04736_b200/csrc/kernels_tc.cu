@@ -31,7 +31,8 @@ using namespace ptx;
 
 // ============================================================================ K2 / K4
 namespace gen {
-constexpr int kGenWarps = 8;
+constexpr int kGenWarps = 8;  // 16 was measured: issue-active 64 -> 76 %, no faster (56 regs)
+constexpr int kItems = kGenWarps == 16 ? 4 : 8;  // 4-element items per thread per k-block
 constexpr int kThreads = (kGenWarps + 1) * 32;  // + one control warp (TMEM alloc, MMA issue)
 constexpr int kStages = 2;
 constexpr int kAStage = 128 * 64 * 2;           // 16 KB generated W tile
@@ -171,18 +172,18 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     } else {
         // ------------------------------------------------ generator warps
         // Thread → item mapping (constant per thread; `it` advances the row):
-        //   fwd  : row = it*16 + (tid>>4) (output feature n), quad kq = tid&15 of the 64 k
-        //   dgrad: row = it*8 + (tid>>5) (output feature n = the MMA K dim), quad mq = tid&31
+        //   fwd  : row = it*rstep + (tid>>4) (output feature n), quad kq = tid&15 of the 64 k
+        //   dgrad: row = it*rstep + (tid>>5) (output feature n = the MMA K dim), quad mq = tid&31
         //          of the 128 k of this M tile (two 64-wide MN blocks)
         // The 128B-swizzle chunk depends on row&7, which is constant per thread.
         const int rsub = MODE == 0 ? (tid >> 4) : (tid >> 5);
         const int qd = MODE == 0 ? (tid & 15) : (tid & 31);
-        const int rstep = MODE == 0 ? 16 : 8;
+        const int rstep = MODE == 0 ? kGenWarps * 2 : kGenWarps;
         const uint32_t soff0 =
             MODE == 0 ? rsub * 128 + ((((qd >> 1) ^ (rsub & 7))) << 4) + ((qd & 1) << 3)
                       : (qd >> 4) * 8192 + rsub * 128 + (((((qd & 15) >> 1) ^ (rsub & 7))) << 4) +
                             ((qd & 1) << 3);
-        const uint32_t sstep = MODE == 0 ? 2048 : 1024;
+        const uint32_t sstep = rstep * 128;
         const bool vec = a.vec_ok != 0;
         const uint32_t w3 = (L.t_w << 20) | sg;
         const bool m_full = MODE == 0 ? (m0 + 128 <= L.N) : (m0 + 128 <= L.K);
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                 const float* sgp = L.sigma + e0;
                 const int64_t estep = (int64_t)rstep * L.K;
 #pragma unroll 4
-                for (int it = 0; it < 8; ++it) {
+                for (int it = 0; it < kItems; ++it) {
                     const uint2 w = gen_w4_fast(mup + it * estep, sgp + it * estep, a.kk.key,
                                                 a.kk.step, w3, (uint32_t)(n0 + it * rstep),
                                                 (uint32_t)(k0 >> 2));
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                 }
             } else {
 #pragma unroll 1
-                for (int it = 0; it < 8; ++it) {
+                for (int it = 0; it < kItems; ++it) {
                     const int n = MODE == 0 ? m0 + rsub + it * rstep : kb * 64 + rsub + it * rstep;
                     const int k = MODE == 0 ? kb * 64 + 4 * qd : m0 + 4 * qd;
                     sts64(tileA + it * sstep, gen_w4(L, a.kk, sg, n, k, vec));
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
         const int row = 32 * q + lane, m = m0 + row;
         const int nchunks = (a.nb + 15) / 16;
         const float bias = MODE == 0 ? sbias[row] : 0.0f;
-        for (int c = h; c < nchunks; c += 2) {
+        for (int c = h; c < nchunks; c += kGenWarps / 4) {
             const int bc0 = b0 + c * 16;
             const int nvalid = min(16, a.B - bc0);
             const bool live = m < a.M && nvalid > 0;
