@@ -60,6 +60,7 @@ def lib():
                                                                          C.c_int, C.c_void_p]
         _lib.orc_forward_ex.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32,
                                                                             C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_adam.argtypes = [C.c_long] + [C.c_void_p] * 4 + [C.c_double] * 4 + [C.c_int]
         _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
                                                                          C.c_void_p, C.c_void_p]
     return _lib
@@ -134,6 +135,15 @@ def aug_params(seed, step, s, b):
     dx, dy, fl = C.c_int(), C.c_int(), C.c_int()
     lib().orc_aug_params(seed, step, s, b, C.byref(dx), C.byref(dy), C.byref(fl))
     return dx.value, dy.value, fl.value
+
+
+# ---------------------------------------------------------------- Adam
+def adam(theta, g, m, v, lr, beta1, beta2, eps, t):
+    """In-place Adam update of fp64 arrays theta, m, v with gradient g (oracle/bnn_oracle.c
+    orc_adam: Kingma & Ba Algorithm 1, the optimizer PAPER.md:166 names)."""
+    for a in (theta, g, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    lib().orc_adam(theta.size, _p(theta), _p(g), _p(m), _p(v), lr, beta1, beta2, eps, t)
 
 
 # ---------------------------------------------------------------- model

@@ -738,6 +738,28 @@ int orc_finalize(const orc_model* m, const double* mu, const double* rho, const 
     return 0;
 }
 
+/*
+ * Adam (Kingma & Ba 2015, Algorithm 1) — the optimizer Alg. 1 l.13 / Alg. 2 l.16 name
+ * ("Update μ and σ using optimizer (e.g., Adam)"); SURVEY §8(f) f2.
+ * Applied elementwise to θ ∈ {μ, ρ} (σ is parameterised by ρ, R1) with gradient g:
+ *   m ← β1·m + (1 − β1)·g;   v ← β2·v + (1 − β2)·g²
+ *   m̂ = m / (1 − β1^t);     v̂ = v / (1 − β2^t);     θ ← θ − α·m̂ / (√v̂ + ε)
+ * t is the 1-based update count. fp64, in place.
+ */
+void orc_adam(long n, double* theta, const double* g, double* m, double* v, double alpha,
+              double beta1, double beta2, double eps, int t)
+{
+    double bc1 = 1.0 - pow(beta1, (double)t);
+    double bc2 = 1.0 - pow(beta2, (double)t);
+    for (long i = 0; i < n; ++i) {
+        m[i] = beta1 * m[i] + (1.0 - beta1) * g[i];
+        v[i] = beta2 * v[i] + (1.0 - beta2) * g[i] * g[i];
+        double mhat = m[i] / bc1;
+        double vhat = v[i] / bc2;
+        theta[i] = theta[i] - alpha * mhat / (sqrt(vhat) + eps);
+    }
+}
+
 /* Full single-process step: all S samples, all B examples. */
 int orc_elbo_step(const orc_model* m, const double* mu, const double* rho, const double* x,
                   const int* ycls, const double* yreg, int B, int S, uint64_t seed,

@@ -269,3 +269,42 @@ def test_predict_degenerate_and_consistency():
     p /= p.sum(-1, keepdims=True)
     assert np.allclose(mean, p.mean(0), rtol=1e-12)
     assert np.allclose(var, p.var(0), rtol=1e-10, atol=1e-15)
+
+
+# ---------------------------------------------------------------- Adam
+def test_adam_matches_torch_optim_adam():
+    """oracle.adam (Kingma & Ba Alg. 1, "e.g., Adam") pinned to the library
+    routine torch.optim.Adam (fp64, no weight decay / amsgrad) over several steps with
+    changing gradients, on a mixture of magnitudes including exact zeros."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    n = 1000
+    theta0 = rng.standard_normal(n)
+    lr, b1, b2, eps = 3e-3, 0.85, 0.995, 1e-6
+    th = theta0.copy()
+    m = np.zeros(n)
+    v = np.zeros(n)
+    p = torch.nn.Parameter(torch.tensor(theta0, dtype=torch.float64))
+    opt = torch.optim.Adam([p], lr=lr, betas=(b1, b2), eps=eps)
+    for t in range(1, 6):
+        g = rng.standard_normal(n) * np.logspace(-6, 1, n)
+        g[::97] = 0.0
+        O.adam(th, g, m, v, lr, b1, b2, eps, t)
+        p.grad = torch.tensor(g)
+        opt.step()
+        ref = p.detach().numpy()
+        np.testing.assert_allclose(th, ref, rtol=0, atol=1e-14)
+        st = opt.state[p]
+        np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-11, atol=0)
+        np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-11, atol=0)
+
+
+def test_adam_first_step_is_signed_lr():
+    """Closed form: at t = 1, m̂ = g and v̂ = g², so θ moves by −α·g/(|g| + ε)."""
+    g = np.array([2.0, -0.5, 0.0, 1e-3])
+    th = np.zeros(4)
+    m = np.zeros(4)
+    v = np.zeros(4)
+    O.adam(th, g, m, v, 0.1, 0.9, 0.999, 1e-8, 1)
+    np.testing.assert_allclose(th, -0.1 * g / (np.abs(g) + 1e-8), rtol=1e-15, atol=0)
