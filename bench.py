@@ -226,9 +226,27 @@ def run_ours(args, world, rank, local_rank):
                          device=local_rank, stream=stream.cuda_stream, aug=cfg.get("aug", "none"))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    adam = args.optimizer == "adam"
+    mom = [torch.zeros_like(mu) for _ in range(4)] if adam else None
+    n_upd = [0]
+
     def step(i):
-        ctx.elbo_step(mu, rho, x, y, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho,
-                      loss_dev=loss_dev, want_loss=False)
+        if adam:
+            # one training step: ELBO gradients + the fused Adam update of μ, ρ
+            n_upd[0] += 1
+            ctx.elbo_step_adam(mu, rho, x, y, B, S, 0x5EED, i, mom, t=n_upd[0], want_loss=False)
+        else:
+            ctx.elbo_step(mu, rho, x, y, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho,
+                          loss_dev=loss_dev, want_loss=False)
+
+    def step_host(i):
+        if adam:
+            x.copy_(x_pin, non_blocking=True)
+            y.copy_(y_pin, non_blocking=True)
+            n_upd[0] += 1
+            ctx.elbo_step_adam(mu, rho, x, y, B, S, 0x5EED, i, mom, t=n_upd[0], want_loss=True)
+        else:
+            ctx.elbo_step_host(mu, rho, x_pin, y_pin, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho)
 
     for i in range(args.warmup):
         step(i)
@@ -272,7 +290,7 @@ def run_ours(args, world, rank, local_rank):
     x_pin = torch.from_numpy(x_h).pin_memory()
     y_pin = torch.from_numpy(yc_h if yc_h is not None else yr_h).pin_memory()
     for i in range(2):
-        ctx.elbo_step_host(mu, rho, x_pin, y_pin, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho)
+        step_host(i)
     torch.cuda.synchronize()
     if distributed:
         dist.barrier()
@@ -281,7 +299,7 @@ def run_ours(args, world, rank, local_rank):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.elbo_step_host(mu, rho, x_pin, y_pin, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho)
+        step_host(i)
         e_ms.append((time.perf_counter() - t0) * 1e3)
     te = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
     if distributed:
@@ -297,6 +315,8 @@ def run_ours(args, world, rank, local_rank):
                 "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
                            "global_batch": B, "samples": S, "samples_per_gpu": S_loc,
                            "params": P, "parallelism": f"sample-sharded x{world}",
+                           "optimizer": "fused Adam (in the timed step)" if adam else
+                                        "none (step returns grad_mu, grad_rho; north_star boundary)",
                            "l2": "flushed between timed steps (256 MiB memset outside events)"},
                 "clocks": clk.summary(),
                 "e2e": {"value": e2e_value, "unit": "sample·images/s",
@@ -420,6 +440,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=None,
                     help="seconds of oracle CPU work per reference step (default: 150 s / (K+W))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--optimizer", default="none", choices=["none", "adam"],
+                    help="adam: each step also applies the fused Adam update (bnn_elbo_step_adam)")
     args = ap.parse_args()
     world, rank, local_rank = _env_world()
     if args.gpus != world and world != 1:

@@ -15,7 +15,8 @@
  * with the S samples (and optionally the batch) sharded over the ranks of one node and a
  * single SUM-allreduce of the gradient partials (§4.1, Alg. 2
  * PAPER.md:250-264; hybrid sample×data grid PAPER.md:283-295, §4.2). The optimizer step
- * (Alg. 1 l.13) is the caller's. Readings of points the paper leaves open are DESIGN.md §2.
+ * (Alg. 1 l.13) is the caller's, or fused into the finalize pass (bnn_elbo_step_adam,
+ * Adam). Readings of points the paper leaves open are DESIGN.md §2.
  *
  * Conventions for every entry point:
  *  - Return value: BNN_OK (0) or a bnn_status code; bnn_last_error() names the violated
@@ -169,6 +170,35 @@ int bnn_elbo_partial(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev,
  *   loss = acc[2P] + ½Σ(σ² + μ² − 1 − 2 ln σ)/|D|. */
 int bnn_finalize(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* acc_dev,
                  float* loss_dev, float* grad_mu_dev, float* grad_rho_dev);
+
+/* Adam hyper-parameters of the fused optimizer step (PAPER.md:166 and
+ * :265, Alg. 1 l.13 / Alg. 2 l.16 "Update μ and σ using optimizer (e.g., Adam)"; Kingma & Ba
+ * Algorithm 1). Requires lr ≥ 0, 0 ≤ beta1, beta2 < 1, eps > 0, t ≥ 1 (BNN_ERR_CONFIG). */
+typedef struct bnn_adam {
+    float lr, beta1, beta2, eps;
+    int32_t t; /* 1-based update count: bias corrections 1 − beta1^t, 1 − beta2^t */
+} bnn_adam;
+
+/* Finalize + KL + Adam in one pass over the parameters: the gradients of bnn_finalize are
+ * formed in registers and, for θ ∈ {μ, ρ} with gradient g,
+ *   m ← β1·m + (1−β1)·g;  v ← β2·v + (1−β2)·g²;  θ ← θ − lr·(m/(1−β1^t)) / (√(v/(1−β2^t)) + eps)
+ * updates mu_dev, rho_dev and the four moment buffers in place (fp32 [n_params] each,
+ * caller-owned, zero before the first update). The loss (and KL) are those of the parameters
+ * BEFORE the update. grad_mu_dev / grad_rho_dev may be NULL (not written). */
+int bnn_finalize_adam(bnn_ctx* ctx, float* mu_dev, float* rho_dev, const float* acc_dev,
+                      const bnn_adam* adam, float* m_mu_dev, float* v_mu_dev, float* m_rho_dev,
+                      float* v_rho_dev, float* loss_dev, float* grad_mu_dev, float* grad_rho_dev);
+
+/* bnn_elbo_step whose finalize is bnn_finalize_adam: one training step (Alg. 1 l.4-13 /
+ * Alg. 2 l.5-16) with μ, ρ and the moments updated in place on every rank (all ranks apply
+ * the same update to the same allreduced gradient). Arguments as bnn_elbo_step and
+ * bnn_finalize_adam. */
+int bnn_elbo_step_adam(bnn_ctx* ctx, float* mu_dev, float* rho_dev, const float* x_dev,
+                       const int32_t* ycls_dev, const float* yreg_dev, int32_t B_loc,
+                       int32_t B_global, int32_t S_global, uint64_t seed, uint32_t step,
+                       const bnn_adam* adam, float* m_mu_dev, float* v_mu_dev, float* m_rho_dev,
+                       float* v_rho_dev, float* loss_dev, double* loss_host, float* grad_mu_dev,
+                       float* grad_rho_dev);
 
 /* Posterior predictive over S_global samples: per output element
  * the mean and the population variance (÷S) of softmax probabilities (CE) or outputs

@@ -31,6 +31,18 @@ void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
                      float* grad_mu, float* grad_rho, double* kl_partials, int n_part,
                      float* loss, cudaStream_t st);
 int finalize_partials_count(int64_t P);
+// K8 + fused Adam: μ, ρ and the moments updated in place; grads optional
+struct AdamHyper {
+    float lr, beta1, beta2, eps;
+    float omb1, omb2;  // 1 − β1, 1 − β2
+    float bc1, bc2;    // 1 − β1^t, 1 − β2^t (host, double precision, rounded once)
+};
+void launch_finalize_adam(float* mu, float* rho, const float* acc_mu, const float* acc_rho,
+                          const float* Ldata, int64_t P, double D, const AdamHyper& h,
+                          float* m_mu, float* v_mu, float* m_rho, float* v_rho, float* grad_mu,
+                          float* grad_rho, double* kl_partials, int n_part, float* loss,
+                          cudaStream_t st);
+
 // loss head on logits [S][B][O] fp32: writes dZ (unscaled gradient seed) as fp32 or bf16 with
 // row stride ldg, and per-(s,b) loss values.
 void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,

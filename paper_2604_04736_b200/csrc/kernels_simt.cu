@@ -113,6 +113,87 @@ void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
     finalize_loss_kernel<<<1, 1024, 0, st>>>(kl_partials, n_part, Ldata, 1.0 / D, loss);
 }
 
+// ---------------------------------------------------------------- K8 + Adam
+// The finalize of K8 followed, in the same pass over the parameters, by the Adam update the
+// paper's Alg. 1 l.13 / Alg. 2 l.16 name (Kingma & Ba Alg. 1):
+//   m ← β1 m + (1−β1) g;  v ← β2 v + (1−β2) g²;  θ ← θ − lr·(m/bc1)/(√(v/bc2) + ε)
+// for θ ∈ {μ, ρ}. KL and the loss use the parameters before the update. One HBM pass:
+// reads μ, ρ, acc_μ, acc_ρ and the four moments, writes μ, ρ and the moments (+ the gradients
+// when requested): 56 B/param (64 with gradients).
+__device__ __forceinline__ void adam_one(float& th, float g, float& m, float& v, const AdamHyper& h) {
+    m = __fmaf_rn(h.beta1, m, h.omb1 * g);
+    v = __fmaf_rn(h.beta2, v, h.omb2 * (g * g));
+    const float mhat = m / h.bc1;
+    const float vhat = v / h.bc2;
+    th = th - h.lr * mhat / (sqrtf(vhat) + h.eps);
+}
+
+__global__ void __launch_bounds__(256) finalize_adam_kernel(
+    float* __restrict__ mu, float* __restrict__ rho, const float* __restrict__ acc_mu,
+    const float* __restrict__ acc_rho, int64_t P, float invD, const AdamHyper h,
+    float* __restrict__ m_mu, float* __restrict__ v_mu, float* __restrict__ m_rho,
+    float* __restrict__ v_rho, float* __restrict__ grad_mu, float* __restrict__ grad_rho,
+    double* __restrict__ kl_partials) {
+    double kl = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t P4 = P / 4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
+        float4 m = reinterpret_cast<const float4*>(mu)[i];
+        float4 r = reinterpret_cast<const float4*>(rho)[i];
+        const float4 a = reinterpret_cast<const float4*>(acc_mu)[i];
+        const float4 b = reinterpret_cast<const float4*>(acc_rho)[i];
+        float4 mm = reinterpret_cast<const float4*>(m_mu)[i];
+        float4 vm = reinterpret_cast<const float4*>(v_mu)[i];
+        float4 mr = reinterpret_cast<const float4*>(m_rho)[i];
+        float4 vr = reinterpret_cast<const float4*>(v_rho)[i];
+        float4 gm, gr;
+        kl += fin_one(m.x, r.x, a.x, b.x, invD, gm.x, gr.x);
+        kl += fin_one(m.y, r.y, a.y, b.y, invD, gm.y, gr.y);
+        kl += fin_one(m.z, r.z, a.z, b.z, invD, gm.z, gr.z);
+        kl += fin_one(m.w, r.w, a.w, b.w, invD, gm.w, gr.w);
+        adam_one(m.x, gm.x, mm.x, vm.x, h); adam_one(r.x, gr.x, mr.x, vr.x, h);
+        adam_one(m.y, gm.y, mm.y, vm.y, h); adam_one(r.y, gr.y, mr.y, vr.y, h);
+        adam_one(m.z, gm.z, mm.z, vm.z, h); adam_one(r.z, gr.z, mr.z, vr.z, h);
+        adam_one(m.w, gm.w, mm.w, vm.w, h); adam_one(r.w, gr.w, mr.w, vr.w, h);
+        reinterpret_cast<float4*>(mu)[i] = m;
+        reinterpret_cast<float4*>(rho)[i] = r;
+        reinterpret_cast<float4*>(m_mu)[i] = mm;
+        reinterpret_cast<float4*>(v_mu)[i] = vm;
+        reinterpret_cast<float4*>(m_rho)[i] = mr;
+        reinterpret_cast<float4*>(v_rho)[i] = vr;
+        if (grad_mu) reinterpret_cast<float4*>(grad_mu)[i] = gm;
+        if (grad_rho) reinterpret_cast<float4*>(grad_rho)[i] = gr;
+    }
+    for (int64_t i = 4 * P4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
+        float gm, gr;
+        kl += fin_one(mu[i], rho[i], acc_mu[i], acc_rho[i], invD, gm, gr);
+        adam_one(mu[i], gm, m_mu[i], v_mu[i], h);
+        adam_one(rho[i], gr, m_rho[i], v_rho[i], h);
+        if (grad_mu) grad_mu[i] = gm;
+        if (grad_rho) grad_rho[i] = gr;
+    }
+    __shared__ double red[8];
+    kl = warp_sum(kl);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = kl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        kl_partials[blockIdx.x] = t;
+    }
+}
+
+void launch_finalize_adam(float* mu, float* rho, const float* acc_mu, const float* acc_rho,
+                          const float* Ldata, int64_t P, double D, const AdamHyper& h,
+                          float* m_mu, float* v_mu, float* m_rho, float* v_rho, float* grad_mu,
+                          float* grad_rho, double* kl_partials, int n_part, float* loss,
+                          cudaStream_t st) {
+    finalize_adam_kernel<<<n_part, 256, 0, st>>>(mu, rho, acc_mu, acc_rho, P, (float)(1.0 / D), h,
+                                                 m_mu, v_mu, m_rho, v_rho, grad_mu, grad_rho,
+                                                 kl_partials);
+    finalize_loss_kernel<<<1, 1024, 0, st>>>(kl_partials, n_part, Ldata, 1.0 / D, loss);
+}
+
 // ====================================================================== K6: loss head
 __global__ void loss_head_kernel(const float* __restrict__ logits, int rows, int B, int O,
                                  int loss_kind, const int32_t* __restrict__ ycls,

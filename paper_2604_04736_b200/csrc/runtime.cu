@@ -648,20 +648,17 @@ int bnn_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc
     return run_finalize(c, mu, rho, acc_dev, loss_dev, gmu, grho);
 }
 
-int bnn_elbo_step(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
-                  const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
-                  uint32_t step, float* loss_dev, double* loss_host, float* gmu, float* grho) {
-    if (!c || !mu || !rho || !x || !gmu || !grho) {
-        if (c) return c->set_err(BNN_ERR_CONFIG, "null tensor argument");
-        return BNN_ERR_CONFIG;
-    }
+namespace {
+// This rank's partial + the one SUM-allreduce of [acc_μ | acc_ρ | L_data] (PAPER.md:243,
+// :263-264); afterwards c->acc holds the global sums on every rank.
+int run_reduced(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
+                const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                uint32_t step) {
     if (c->cfg.world > 1 && !c->comm)
         return c->set_err(BNN_ERR_CONFIG, "world > 1 without a communicator: use bnn_elbo_partial + bnn_finalize");
     int rc = run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, c->acc);
     if (rc) return rc;
     if (c->comm) {
-        const int64_t t0 = c->launches;
-        (void)t0;
         int cls = -1;
         cudaEvent_t a = nullptr, b = nullptr;
         if (c->prof) {
@@ -683,7 +680,77 @@ int bnn_elbo_step(bnn_ctx* c, const float* mu, const float* rho, const float* x,
             c->pending.push_back({cls, {a, b}});
         }
     }
+    return BNN_OK;
+}
+
+int check_adam(bnn_ctx* c, const bnn_adam* h, AdamHyper* out) {
+    if (!h) return c->set_err(BNN_ERR_CONFIG, "null bnn_adam");
+    if (!(h->lr >= 0.f) || !(h->beta1 >= 0.f && h->beta1 < 1.f) || !(h->beta2 >= 0.f && h->beta2 < 1.f) ||
+        !(h->eps > 0.f) || h->t < 1)
+        return c->set_err(BNN_ERR_CONFIG, "Adam hyper-parameters: lr >= 0, 0 <= beta < 1, eps > 0, t >= 1 violated");
+    out->lr = h->lr;
+    out->beta1 = h->beta1;
+    out->beta2 = h->beta2;
+    out->eps = h->eps;
+    out->omb1 = (float)(1.0 - (double)h->beta1);
+    out->omb2 = (float)(1.0 - (double)h->beta2);
+    out->bc1 = (float)(1.0 - std::pow((double)h->beta1, (double)h->t));
+    out->bc2 = (float)(1.0 - std::pow((double)h->beta2, (double)h->t));
+    return BNN_OK;
+}
+
+int run_finalize_adam(bnn_ctx* c, float* mu, float* rho, const float* acc, const bnn_adam* hp,
+                      float* m_mu, float* v_mu, float* m_rho, float* v_rho, float* loss_dev,
+                      float* gmu, float* grho) {
+    AdamHyper h;
+    int rc = check_adam(c, hp, &h);
+    if (rc) return rc;
+    if (!m_mu || !v_mu || !m_rho || !v_rho) return c->set_err(BNN_ERR_CONFIG, "null Adam moment buffer");
+    cudaStream_t st = c->st;
+    c->launch("finalize", [&] {
+        launch_finalize_adam(mu, rho, acc, acc + c->P_pad, acc + 2 * c->P_pad, c->P, c->cfg.dataset_size, h,
+                             m_mu, v_mu, m_rho, v_rho, gmu, grho, c->kl_part, c->n_part, c->lossbuf, st);
+    }, 2);
+    if (loss_dev) CUDA_TRY(c, cudaMemcpyAsync(loss_dev, c->lossbuf, sizeof(float), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(c, cudaGetLastError());
+    return BNN_OK;
+}
+}  // namespace
+
+int bnn_elbo_step(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
+                  const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                  uint32_t step, float* loss_dev, double* loss_host, float* gmu, float* grho) {
+    if (!c || !mu || !rho || !x || !gmu || !grho) {
+        if (c) return c->set_err(BNN_ERR_CONFIG, "null tensor argument");
+        return BNN_ERR_CONFIG;
+    }
+    int rc = run_reduced(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step);
+    if (rc) return rc;
     rc = run_finalize(c, mu, rho, c->acc, loss_dev, gmu, grho);
+    if (rc) return rc;
+    if (loss_host) return read_loss(c, loss_host);
+    return BNN_OK;
+}
+
+int bnn_finalize_adam(bnn_ctx* c, float* mu, float* rho, const float* acc_dev, const bnn_adam* h,
+                      float* m_mu, float* v_mu, float* m_rho, float* v_rho, float* loss_dev,
+                      float* gmu, float* grho) {
+    if (!c || !mu || !rho || !acc_dev) return BNN_ERR_CONFIG;
+    return run_finalize_adam(c, mu, rho, acc_dev, h, m_mu, v_mu, m_rho, v_rho, loss_dev, gmu, grho);
+}
+
+int bnn_elbo_step_adam(bnn_ctx* c, float* mu, float* rho, const float* x, const int32_t* ycls,
+                       const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global,
+                       uint64_t seed, uint32_t step, const bnn_adam* h, float* m_mu, float* v_mu,
+                       float* m_rho, float* v_rho, float* loss_dev, double* loss_host, float* gmu,
+                       float* grho) {
+    if (!c || !mu || !rho || !x) {
+        if (c) return c->set_err(BNN_ERR_CONFIG, "null tensor argument");
+        return BNN_ERR_CONFIG;
+    }
+    int rc = run_reduced(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step);
+    if (rc) return rc;
+    rc = run_finalize_adam(c, mu, rho, c->acc, h, m_mu, v_mu, m_rho, v_rho, loss_dev, gmu, grho);
     if (rc) return rc;
     if (loss_host) return read_loss(c, loss_host);
     return BNN_OK;

@@ -43,6 +43,12 @@ class BnnTensorInfo(C.Structure):
                 ("t", C.c_int32), ("is_bias", C.c_int32)]
 
 
+class BnnAdam(C.Structure):
+    """bnn_adam (include/bnn.h): hyper-parameters of the fused Adam step."""
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("eps", C.c_float), ("t", C.c_int32)]
+
+
 class BnnError(RuntimeError):
     pass
 
@@ -66,6 +72,8 @@ def lib():
     L.bnn_elbo_step_host.argtypes = step_args + [vp, vp, vp]
     L.bnn_elbo_partial.argtypes = step_args + [vp]
     L.bnn_finalize.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.bnn_finalize_adam.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.bnn_elbo_step_adam.argtypes = step_args + [vp] * 9
     L.bnn_predict.argtypes = [vp, vp, vp, vp, i32, i32, u64, u32, vp, vp]
     L.bnn_eps_fill.argtypes = [u64, u32, u32, u32, u32, u32, u32, u32, vp, vp]
     L.bnn_eps_bench.argtypes = [u64, u64, vp, i32, vp]
@@ -184,6 +192,33 @@ class Context:
                                      C.byref(lh) if want_loss else None, _p(grad_mu),
                                      _p(grad_rho)), self._h)
         return (lh.value if want_loss else None), grad_mu, grad_rho
+
+    def elbo_step_adam(self, mu, rho, x, y, B_global, S_global, seed, step, moments, *, t,
+                       lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, grad_mu=None, grad_rho=None,
+                       want_loss=True):
+        """One training step with the fused Adam update (bnn_elbo_step_adam): mu, rho and
+        moments = (m_mu, v_mu, m_rho, v_rho) are updated in place; returns the loss of the
+        parameters before the update. grad_mu/grad_rho are written only when given."""
+        h = BnnAdam(lr, beta1, beta2, eps, t)
+        yc, yr = self._y(y)
+        lh = C.c_double()
+        m_mu, v_mu, m_rho, v_rho = moments
+        _check(self._L.bnn_elbo_step_adam(self._h, _p(mu), _p(rho), _p(x), yc, yr, x.shape[0],
+                                          B_global, S_global, seed, step, C.byref(h), _p(m_mu),
+                                          _p(v_mu), _p(m_rho), _p(v_rho), None,
+                                          C.byref(lh) if want_loss else None, _p(grad_mu),
+                                          _p(grad_rho)), self._h)
+        return lh.value if want_loss else None
+
+    def finalize_adam(self, mu, rho, acc, moments, *, t, lr=1e-3, beta1=0.9, beta2=0.999,
+                      eps=1e-8, grad_mu=None, grad_rho=None):
+        h = BnnAdam(lr, beta1, beta2, eps, t)
+        loss = torch.zeros(1, dtype=torch.float32, device=self.device)
+        m_mu, v_mu, m_rho, v_rho = moments
+        _check(self._L.bnn_finalize_adam(self._h, _p(mu), _p(rho), _p(acc), C.byref(h), _p(m_mu),
+                                         _p(v_mu), _p(m_rho), _p(v_rho), _p(loss), _p(grad_mu),
+                                         _p(grad_rho)), self._h)
+        return loss
 
     def elbo_step_host(self, mu, rho, x_host, y_host, B_global, S_global, seed, step, *,
                        grad_mu, grad_rho):

@@ -199,6 +199,96 @@ def test_predict_matches_oracle(precision, tol):
     assert _rel(var.cpu().numpy(), rv) < 5 * tol
 
 
+# ------------------------------------------------------------------ fused Adam
+def _adam_case(model, precision, B, S, steps, lr=1e-2, b1=0.9, b2=0.999, eps=1e-8, rho_mode="wide"):
+    native = _native()
+    mu, rho, x, yc, yr = _inputs(model, B, rho_mode)
+    D = 1000.0
+    ctx = native.Context(model, precision=precision, max_B_loc=B, max_S_loc=S, dataset_size=D)
+    y = _dev(yc) if yc is not None else _dev(yr)
+    dmu, drho, dx = _dev(mu), _dev(rho), _dev(x)
+    mom = [torch.zeros_like(dmu) for _ in range(4)]
+    gmu, grho = torch.empty_like(dmu), torch.empty_like(drho)
+    ref_mu, ref_rho = mu.astype(np.float64).copy(), rho.astype(np.float64).copy()
+    rm = [np.zeros(ref_mu.size) for _ in range(4)]
+    out = []
+    for t in range(1, steps + 1):
+        loss = ctx.elbo_step_adam(dmu, drho, dx, y, B, S, 0xADA, 10 + t, mom, t=t, lr=lr, beta1=b1,
+                                  beta2=b2, eps=eps, grad_mu=gmu, grad_rho=grho)
+        ref = O.elbo_step(model, ref_mu, ref_rho, x, yc, yr, S, 0xADA, 10 + t, D)
+        O.adam(ref_mu, ref["grad_mu"], rm[0], rm[1], lr, b1, b2, eps, t)
+        O.adam(ref_rho, ref["grad_rho"], rm[2], rm[3], lr, b1, b2, eps, t)
+        torch.cuda.synchronize()
+        out.append(dict(loss=loss, ref_loss=ref["loss"], gmu=gmu.cpu().numpy(), grho=grho.cpu().numpy(),
+                        ref_gmu=ref["grad_mu"], ref_grho=ref["grad_rho"], mu=dmu.cpu().numpy(),
+                        rho=drho.cpu().numpy(), ref_mu=ref_mu.copy(), ref_rho=ref_rho.copy(),
+                        mom=[m.cpu().numpy() for m in mom], ref_mom=[m.copy() for m in rm]))
+    return ctx, mu, rho, out
+
+
+def _displacement_ok(theta, ref, theta0, lr, steps):
+    """Adam moves an element by ≈ lr·sign(ĝ) per step, so an element whose reference gradient
+    is below the fp32 error level can legitimately move the other way; the displacement is
+    compared as a whole (≤ 5e-3 relative) and elementwise to 1e-3·lr except for ≤ 0.1 % of
+    elements (those near-zero-gradient sign ties)."""
+    d, dr = theta - theta0, ref - theta0
+    rel = np.linalg.norm(d - dr) / max(np.linalg.norm(dr), 1e-300)
+    bad = np.mean(np.abs(d - dr) > 1e-3 * lr * steps + 1e-6 * np.abs(ref))
+    return rel, bad
+
+
+@pytest.mark.parametrize("model,B,S", [(C1, 32, 4), (RAGGED, 77, 3), (RAGGED_MSE, 40, 5)])
+def test_fused_adam_step_matches_oracle_fp32(model, B, S):
+    """bnn_elbo_step_adam (FP32 mode) over 3 updates against oracle.elbo_step + oracle.adam
+    (Kingma & Ba, pinned to torch.optim.Adam): loss and gradients ≤ 1e-4 per tensor, the
+    moments ≤ 1e-4 / 2e-4, μ and ρ displacements as _displacement_ok."""
+    lr, steps = 1e-2, 3
+    ctx, mu0, rho0, out = _adam_case(model, "fp32", B, S, steps, lr=lr)
+    for k, o in enumerate(out):
+        assert abs(o["loss"] - o["ref_loss"]) <= 1e-4 * abs(o["ref_loss"]), k
+        assert max(_per_tensor_rel(ctx, o["gmu"], o["ref_gmu"])) <= 1e-4, k
+        assert max(_per_tensor_rel(ctx, o["grho"], o["ref_grho"])) <= 1e-4, k
+    last = out[-1]
+    assert _rel(last["mom"][0], last["ref_mom"][0]) <= 1e-3
+    assert _rel(last["mom"][2], last["ref_mom"][2]) <= 1e-3
+    assert _rel(last["mom"][1], last["ref_mom"][1]) <= 2e-3
+    assert _rel(last["mom"][3], last["ref_mom"][3]) <= 2e-3
+    for th, ref, th0 in ((last["mu"], last["ref_mu"], mu0), (last["rho"], last["ref_rho"], rho0)):
+        rel, bad = _displacement_ok(th.astype(np.float64), ref, th0.astype(np.float64), lr, steps)
+        assert rel <= 5e-3 and bad <= 1e-3, (rel, bad)
+
+
+def test_fused_adam_bf16_consistent_with_plain_step():
+    """BF16 C2-shaped step: the fused step's gradients are bit-identical to bnn_elbo_step's on
+    the same inputs, and its first update is exactly m = RN((1−β1)·g), v = RN((1−β2)·RN(g²)),
+    θ' = θ − lr·(m/bc1)/(√(v/bc2)+ε) in fp32."""
+    native = _native()
+    model, B, S = C2, 256, 4
+    mu, rho, x, yc, _ = _inputs(model, B, "init")
+    ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=60000.0)
+    y = _dev(yc)
+    loss0, g0, r0 = ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), y, B, S, 5, 1)
+    dmu, drho = _dev(mu), _dev(rho)
+    mom = [torch.zeros_like(dmu) for _ in range(4)]
+    gmu, grho = torch.empty_like(dmu), torch.empty_like(dmu)
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    loss1 = ctx.elbo_step_adam(dmu, drho, _dev(x), y, B, S, 5, 1, mom, t=1, lr=lr, beta1=b1, beta2=b2,
+                               eps=eps, grad_mu=gmu, grad_rho=grho)
+    torch.cuda.synchronize()
+    assert loss1 == loss0
+    assert torch.equal(gmu, g0) and torch.equal(grho, r0)
+    # the library rounds β to fp32 and forms 1 − β and the bias corrections in double
+    omb1 = float(np.float32(1.0 - float(np.float32(b1))))
+    omb2 = float(np.float32(1.0 - float(np.float32(b2))))
+    assert torch.equal(mom[0], g0 * omb1) and torch.equal(mom[2], r0 * omb1)
+    assert torch.equal(mom[1], (g0 * g0) * omb2) and torch.equal(mom[3], (r0 * r0) * omb2)
+    for th, th0, g, m, v in ((dmu, _dev(mu), g0, mom[0], mom[1]), (drho, _dev(rho), r0, mom[2], mom[3])):
+        bc1, bc2 = omb1, omb2  # t = 1
+        expect = th0 - lr * (m / bc1) / (torch.sqrt(v / bc2) + eps)
+        assert torch.allclose(th, expect, rtol=0, atol=1e-6)
+        assert float((th - th0).abs().max()) <= 1.01 * lr
+
+
 # ------------------------------------------------------------------ full BASELINE size (C2)
 def test_c2_full_size_bf16_loss_and_logits():
     """BASELINE.json configs[1] at full size (B=256, S=64), bench launch configuration:
