@@ -60,6 +60,8 @@ def lib():
                                                                          C.c_int, C.c_void_p]
         _lib.orc_forward_ex.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32,
                                                                             C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_elbo_step_mean.argtypes = [C.c_void_p] * 6 + [C.c_int] * 2 + [
+            C.c_uint64, C.c_uint32, C.c_int, C.c_double] + [C.c_void_p] * 4 + [C.c_int]
         _lib.orc_adam.argtypes = [C.c_long] + [C.c_void_p] * 4 + [C.c_double] * 4 + [C.c_int]
         _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
                                                                          C.c_void_p, C.c_void_p]
@@ -193,8 +195,26 @@ def finalize(model, mu, rho, acc, D, act="relu"):
 
 
 def elbo_step(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=AUG_NONE, nthreads=0,
-              act="relu", emu=False):
+              act="relu", emu=False, agg="sample"):
+    """agg="sample": L_data = mean over samples of the per-sample loss (Alg. 1 l.9, the path's
+    default); agg="mean": the loss of the mean prediction (exact aggregation, PAPER.md:272-281,
+    orc_elbo_step_mean)."""
     B = np.asarray(x).shape[0]
+    if agg == "mean":
+        assert not emu
+        m = model_struct(model, act)
+        P = lib().orc_n_params(C.byref(m))
+        mu, rho, x, yr = _d(mu), _d(rho), _d(x), _d(y_reg)
+        yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
+        gmu, grho = np.zeros(P), np.zeros(P)
+        loss, kl = C.c_double(), C.c_double()
+        rc = lib().orc_elbo_step_mean(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), B, S,
+                                      seed, step, aug, D, C.byref(loss), C.byref(kl), _p(gmu),
+                                      _p(grho), nthreads)
+        assert rc == 0, rc
+        return dict(loss=loss.value, kl=kl.value, grad_mu=gmu, grad_rho=grho,
+                    L_data=loss.value - kl.value / D)
+    assert agg == "sample"
     acc = elbo_partial(model, mu, rho, x, y_cls, y_reg, B, 0, S, 0, S, seed, step, aug, nthreads,
                        act, emu)
     return finalize(model, mu, rho, acc, D, act)

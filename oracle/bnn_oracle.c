@@ -629,10 +629,29 @@ static double loss_one(const ONet* n, const double* z, const int* ycls, const do
  *   acc[2P]       += Σ_s Σ_b ℓ_{s,b} / (S·B_glob · (O if MSE))
  * Sums are in a fixed order for a fixed thread count.
  */
+static int elbo_partial_core(const orc_model* m, const double* mu, const double* rho,
+                             const double* x, const int* ycls, const double* yreg, int B_loc,
+                             int b_offset, int B_glob, int S_glob, int s0, int s1, uint64_t seed,
+                             uint32_t step, int aug, double* acc, int nthreads, int emu,
+                             const double* seeds);
+
 int orc_elbo_partial_ex(const orc_model* m, const double* mu, const double* rho, const double* x,
                         const int* ycls, const double* yreg, int B_loc, int b_offset, int B_glob,
                         int S_glob, int s0, int s1, uint64_t seed, uint32_t step, int aug,
                         double* acc, int nthreads, int emu)
+{
+    return elbo_partial_core(m, mu, rho, x, ycls, yreg, B_loc, b_offset, B_glob, S_glob, s0, s1,
+                             seed, step, aug, acc, nthreads, emu, NULL);
+}
+
+/* seeds == NULL: the per-sample loss of loss_one (Alg. 1 l.9). Otherwise seeds[s][b][O]
+ * (global sample s, local example b) is the complete ∂L_data/∂z_{s,b}, scale included, and
+ * no loss is accumulated (the exact-aggregation step below computes L_data itself). */
+static int elbo_partial_core(const orc_model* m, const double* mu, const double* rho,
+                             const double* x, const int* ycls, const double* yreg, int B_loc,
+                             int b_offset, int B_glob, int S_glob, int s0, int s1, uint64_t seed,
+                             uint32_t step, int aug, double* acc, int nthreads, int emu,
+                             const double* seeds)
 {
     ONet net;
     if (build_net(m, &net)) return -1;
@@ -678,11 +697,16 @@ int orc_elbo_partial_ex(const orc_model* m, const double* mu, const double* rho,
                     memset(w->grad[k], 0, sizeof(double) * (size_t)buf_size(n, k));
                 load_input(n, x, b, b_offset + b, seed, step, (uint32_t)s, aug, w->val[0]);
                 int out = forward_one(n, W, w, emu);
-                double l = loss_one(n, w->val[out], ycls, yreg, b, dz);
-                lt[tid] += l * scale;
-                /* exact mode: the seed carries the 1/(S·B) scale; emulation: the unscaled seed
-                 * is what the bf16 operand rounds, the scale is applied at accumulation */
-                for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = emu ? dz[k] : dz[k] * scale;
+                if (seeds) {
+                    const double* sd = seeds + ((size_t)s * B_loc + b) * n->n_out;
+                    for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = sd[k];
+                } else {
+                    double l = loss_one(n, w->val[out], ycls, yreg, b, dz);
+                    lt[tid] += l * scale;
+                    /* exact mode: the seed carries the 1/(S·B) scale; emulation: the unscaled
+                     * seed is what the bf16 operand rounds, the scale is applied at accumulation */
+                    for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = emu ? dz[k] : dz[k] * scale;
+                }
                 backward_one(n, W, w, dWt + (size_t)tid * P, emu ? scale : 1.0, emu,
                              tmps + (size_t)tid * maxbuf);
             }
@@ -774,6 +798,84 @@ int orc_elbo_step(const orc_model* m, const double* mu, const double* rho, const
                               nthreads);
     if (!rc) rc = orc_finalize(m, mu, rho, acc, D, out_loss, out_kl, grad_mu, grad_rho);
     free(acc);
+    return rc;
+}
+
+/*
+ * Exact aggregation (§4.1 "an exact algorithm where the standard deviation
+ * and mean are aggregated across multiple GPUs"): the data term is the loss
+ * of the MEAN prediction over the S samples instead of the mean of per-sample losses:
+ *   CE  ("cross-entropy loss on the (arithmetic) mean of the class probabilities"):
+ *       p_s = softmax(z_s);  P̄_b = (1/S) Σ_s p_{s,b,y_b};  L_data = (1/B) Σ_b −ln P̄_b
+ *   MSE ("MSE loss of the averaged predictions"):
+ *       ȳ = (1/S) Σ_s z_s;  L_data = (1/(B·O)) Σ_{b,o} (ȳ_{b,o} − y_{b,o})²
+ * loss = L_data + KL/|D|. Backward by the chain rule through the statistic:
+ *   CE:  ∂L/∂z_{s,b,k} = (1/(S·B)) · (p_{s,b,y}/P̄_b) · (p_{s,b,k} − [k = y_b])
+ *   MSE: ∂L/∂z_{s,b,o} = (2/(S·B·O)) · (ȳ_{b,o} − y_{b,o})
+ * then the same per-sample backward and sample accumulation as orc_elbo_partial.
+ */
+int orc_forward_ex(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
+                   int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out, int emu);
+
+int orc_elbo_step_mean(const orc_model* m, const double* mu, const double* rho, const double* x,
+                       const int* ycls, const double* yreg, int B, int S, uint64_t seed,
+                       uint32_t step, int aug, double D, double* out_loss, double* out_kl,
+                       double* grad_mu, double* grad_rho, int nthreads)
+{
+    long P = orc_n_params(m);
+    if (P < 0) return -1;
+    ONet net;
+    if (build_net(m, &net)) return -1;
+    const int O = net.n_out;
+    double* z = (double*)malloc(sizeof(double) * (size_t)S * B * O);
+    double* seeds = (double*)malloc(sizeof(double) * (size_t)S * B * O);
+    double* acc = (double*)calloc((size_t)(2 * P + 1), sizeof(double));
+    if (!z || !seeds || !acc) return -2;
+    int rc = orc_forward_ex(m, mu, rho, x, B, 0, S, seed, step, aug, z, 0);
+    if (rc) return rc;
+    double L = 0.0;
+    if (m->loss == ORC_CE) {
+        double* p = (double*)malloc(sizeof(double) * (size_t)S * B * O);
+        if (!p) return -2;
+        for (long r = 0; r < (long)S * B; ++r) {   /* p_s = softmax(z_s) */
+            const double* zr = z + r * O;
+            double mx = zr[0];
+            for (int k = 1; k < O; ++k) if (zr[k] > mx) mx = zr[k];
+            double se = 0.0;
+            for (int k = 0; k < O; ++k) se += exp(zr[k] - mx);
+            for (int k = 0; k < O; ++k) p[r * O + k] = exp(zr[k] - mx) / se;
+        }
+        for (int b = 0; b < B; ++b) {
+            const int y = ycls[b];
+            double pbar = 0.0;
+            for (int s = 0; s < S; ++s) pbar += p[((long)s * B + b) * O + y];
+            pbar /= S;
+            L += -log(pbar) / B;
+            for (int s = 0; s < S; ++s) {
+                const double* ps = p + ((long)s * B + b) * O;
+                double* sd = seeds + ((long)s * B + b) * O;
+                for (int k = 0; k < O; ++k)
+                    sd[k] = (ps[y] / pbar) * (ps[k] - (k == y ? 1.0 : 0.0)) / ((double)S * B);
+            }
+        }
+        free(p);
+    } else {
+        for (int b = 0; b < B; ++b)
+            for (int k = 0; k < O; ++k) {
+                double ybar = 0.0;
+                for (int s = 0; s < S; ++s) ybar += z[((long)s * B + b) * O + k];
+                ybar /= S;
+                const double d = ybar - yreg[(long)b * O + k];
+                L += d * d / ((double)B * O);
+                for (int s = 0; s < S; ++s)
+                    seeds[((long)s * B + b) * O + k] = 2.0 * d / ((double)S * B * O);
+            }
+    }
+    rc = elbo_partial_core(m, mu, rho, x, ycls, yreg, B, 0, B, S, 0, S, seed, step, aug, acc,
+                           nthreads, 0, seeds);
+    acc[2 * P] = L;
+    if (!rc) rc = orc_finalize(m, mu, rho, acc, D, out_loss, out_kl, grad_mu, grad_rho);
+    free(z); free(seeds); free(acc);
     return rc;
 }
 

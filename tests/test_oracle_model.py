@@ -97,14 +97,14 @@ def test_uniform_ce_is_ln10_and_log_softmax_values():
         assert acc[2 * P] == pytest.approx(val, abs=1e-8)
 
 
-def _fd_check(model, mu, rho, x, yc, yr, S, D, act, idx_mu, idx_rho, aug=0, h=1e-4):
+def _fd_check(model, mu, rho, x, yc, yr, S, D, act, idx_mu, idx_rho, aug=0, h=1e-4, agg="sample"):
     """Fourth-order central differences: (8[L(+h) − L(−h)] − [L(+2h) − L(−2h)]) / 12h."""
-    base = O.elbo_step(model, mu, rho, x, yc, yr, S, 11, 4, D, aug=aug, act=act)
+    base = O.elbo_step(model, mu, rho, x, yc, yr, S, 11, 4, D, aug=aug, act=act, agg=agg)
     g_mu, g_rho = base["grad_mu"], base["grad_rho"]
     gmax = max(np.abs(g_mu).max(), np.abs(g_rho).max())
 
     def L(m, r):
-        return O.elbo_step(model, m, r, x, yc, yr, S, 11, 4, D, aug=aug, act=act)["loss"]
+        return O.elbo_step(model, m, r, x, yc, yr, S, 11, 4, D, aug=aug, act=act, agg=agg)["loss"]
 
     for vec, grad, idxs, which in ((mu, g_mu, idx_mu, "mu"), (rho, g_rho, idx_rho, "rho")):
         for i in idxs:
@@ -308,3 +308,81 @@ def test_adam_first_step_is_signed_lr():
     v = np.zeros(4)
     O.adam(th, g, m, v, 0.1, 0.9, 0.999, 1e-8, 1)
     np.testing.assert_allclose(th, -0.1 * g / (np.abs(g) + 1e-8), rtol=1e-15, atol=0)
+
+
+# ---------------------------------------------------------------- exact aggregation
+@pytest.mark.parametrize("loss", ["ce", "mse"])
+def test_mean_aggregation_finite_differences(loss):
+    """The loss of the mean prediction: whole gradient vs central FD."""
+    if loss == "ce":
+        model, B, S, D = dict(kind="mlp", widths=[6, 7, 5], loss="ce"), 9, 3, 500.0
+    else:
+        model, B, S, D = C1, 16, 4, 1024.0
+    mu, rho = synth.init_params(model, seed=5, rho_mode="wide")
+    x, yc, yr = synth.make_batch(model, B, seed=4)
+    P = n_params(model)
+    _fd_check(model, mu.astype(np.float64), rho.astype(np.float64), x, yc, yr, S, D, "tanh",
+              range(P), range(P), agg="mean")
+
+
+@pytest.mark.parametrize("loss", ["ce", "mse"])
+def test_mean_aggregation_against_torch_autograd(loss):
+    """Independent fp64 torch formulation (mean of softmax probabilities / of predictions,
+    F.nll_loss / F.mse_loss, autograd) on a ReLU MLP, σ wide."""
+    model = dict(kind="mlp", widths=[12, 16, 9, 4], loss=loss)
+    mu, rho = synth.init_params(model, seed=8, rho_mode="wide")
+    x, yc, yr = synth.make_batch(model, 7, seed=9)
+    o = O.elbo_step(model, mu, rho, x, yc, yr, 5, 0xABC, 2, 777.0, agg="mean")
+    t = torch_ref.elbo(model, mu, rho, x, yc, yr, 5, 0xABC, 2, 777.0, agg="mean")
+    assert o["loss"] == pytest.approx(t["loss"], rel=1e-12)
+    assert o["L_data"] == pytest.approx(t["L_data"], rel=1e-11)
+    _cmp(o["grad_mu"], t["grad_mu"], 1e-10)
+    _cmp(o["grad_rho"], t["grad_rho"], 1e-10)
+
+
+@pytest.mark.parametrize("loss", ["ce", "mse"])
+def test_mean_aggregation_single_sample_equals_per_sample(loss):
+    """S = 1: the mean prediction is the prediction, so both aggregations coincide."""
+    model = dict(kind="mlp", widths=[10, 12, 5], loss=loss)
+    mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
+    x, yc, yr = synth.make_batch(model, 6, seed=3)
+    a = O.elbo_step(model, mu, rho, x, yc, yr, 1, 9, 0, 100.0)
+    b = O.elbo_step(model, mu, rho, x, yc, yr, 1, 9, 0, 100.0, agg="mean")
+    assert b["loss"] == pytest.approx(a["loss"], rel=1e-13)
+    _cmp(b["grad_mu"], a["grad_mu"], 1e-12)
+    _cmp(b["grad_rho"], a["grad_rho"], 1e-12)
+
+
+def test_geometric_mean_gap_ce():
+    """averaging per-sample CE (the sample-sharded approximation with one
+    sample per GPU) is CE of the GEOMETRIC mean of the true-class probabilities, the exact loss
+    CE of the ARITHMETIC mean; so L_sample = −mean_b ln GM_s(p) ≥ L_mean = −mean_b ln AM_s(p)
+    (AM-GM). Statistics recomputed here with numpy from the oracle's per-sample logits."""
+    model = dict(kind="mlp", widths=[10, 12, 5], loss="ce")
+    mu, rho = synth.init_params(model, seed=4, rho_mode="wide")
+    x, yc, _ = synth.make_batch(model, 8, seed=6)
+    S, D = 6, 1e9
+    z = O.forward(model, mu, rho, x, 0, S, 21, 0)
+    p = np.exp(z - z.max(-1, keepdims=True))
+    p /= p.sum(-1, keepdims=True)
+    py = np.take_along_axis(p, yc[None, :, None].astype(np.int64), -1)[..., 0]  # [S, B]
+    gm = np.exp(np.log(py).mean(0))
+    am = py.mean(0)
+    a = O.elbo_step(model, mu, rho, x, yc, None, S, 21, 0, D)
+    b = O.elbo_step(model, mu, rho, x, yc, None, S, 21, 0, D, agg="mean")
+    assert a["L_data"] == pytest.approx(float(-np.log(gm).mean()), rel=1e-12)
+    assert b["L_data"] == pytest.approx(float(-np.log(am).mean()), rel=1e-12)
+    assert a["L_data"] > b["L_data"]
+
+
+def test_bias_variance_gap_mse():
+    """MSE: mean_s (ŷ_s − y)² = (ȳ − y)² + Var_s(ŷ) (population), so the per-sample data term
+    exceeds the exact one by the predictive variance of bnn_predict's oracle."""
+    model = C1
+    mu, rho = synth.init_params(model, seed=2, rho_mode="wide")
+    x, _, yr = synth.make_batch(model, 32, seed=1)
+    S = 8
+    a = O.elbo_step(model, mu, rho, x, None, yr, S, 5, 1, 1e9)
+    b = O.elbo_step(model, mu, rho, x, None, yr, S, 5, 1, 1e9, agg="mean")
+    _, var = O.predict(model, mu, rho, x, S, 5, 1)
+    assert a["L_data"] - b["L_data"] == pytest.approx(float(var.mean()), rel=1e-10)

@@ -69,8 +69,9 @@ def _forward(model, ws, x, act):
     return F.linear(h, ws[2 * l], ws[2 * l + 1].reshape(-1))
 
 
-def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu"):
-    """Return loss, L_data, KL, grad_mu, grad_rho (numpy fp64) via autograd."""
+def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu", agg="sample"):
+    """Return loss, L_data, KL, grad_mu, grad_rho (numpy fp64) via autograd. agg="mean": the
+    loss of the mean prediction (mean softmax probability for CE, mean output for MSE)."""
     lay = layout(model)
     mu_t = torch.tensor(np.asarray(mu, np.float64), requires_grad=True)
     rho_t = torch.tensor(np.asarray(rho, np.float64), requires_grad=True)
@@ -78,6 +79,7 @@ def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu
     X = torch.tensor(np.asarray(x, np.float64))
     B = X.shape[0]
     L_data = 0.0
+    zs = []
     for s in range(S):
         ws = []
         for ti in lay:
@@ -90,11 +92,21 @@ def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu
         if aug:
             Xs = torch.stack([_augment(X[b], seed, step, s, b) for b in range(B)])
         z = _forward(model, ws, Xs, act)
+        if agg == "mean":
+            zs.append(z)
+            continue
         if model["loss"] == "ce":
             l = F.cross_entropy(z, torch.tensor(np.asarray(y_cls, np.int64)), reduction="mean")
         else:
             l = F.mse_loss(z, torch.tensor(np.asarray(y_reg, np.float64)), reduction="mean")
         L_data = L_data + l / S
+    if agg == "mean":
+        Z = torch.stack(zs)
+        if model["loss"] == "ce":
+            pbar = torch.softmax(Z, dim=-1).mean(0)
+            L_data = F.nll_loss(torch.log(pbar), torch.tensor(np.asarray(y_cls, np.int64)))
+        else:
+            L_data = F.mse_loss(Z.mean(0), torch.tensor(np.asarray(y_reg, np.float64)))
     kl = 0.5 * torch.sum(sigma ** 2 + mu_t ** 2 - 1.0 - torch.log(sigma ** 2))
     loss = L_data + kl / D
     loss.backward()
