@@ -201,14 +201,16 @@ def run_ours(args, world, rank, local_rank):
         uid = obj[0]
     cfg = CONFIGS[args.config]
     model = MODELS[cfg["model"]]
+    if args.agg == "mean":  # exact aggregation: loss of the mean prediction
+        model = dict(model, loss=model["loss"] + "_mean")
     plan = run_plan(args.config, world, args.mode)
     B, B_loc, S, S_loc, K, G = plan["B"], plan["B_loc"], plan["S"], plan["S_loc"], plan["K"], plan["G"]
     D = cfg["D"]
     P = n_params(model)
     g_idx = rank % G
 
-    mu_h, rho_h = synth.init_params(model, seed=2)
-    x_h, yc_h, yr_h = synth.make_batch(model, B, seed=1)
+    mu_h, rho_h = synth.init_params(MODELS[cfg["model"]], seed=2)
+    x_h, yc_h, yr_h = synth.make_batch(MODELS[cfg["model"]], B, seed=1)
     # this rank's data-group shard of the global batch
     x_h = x_h[g_idx * B_loc:(g_idx + 1) * B_loc]
     yc_h = None if yc_h is None else yc_h[g_idx * B_loc:(g_idx + 1) * B_loc]
@@ -315,6 +317,8 @@ def run_ours(args, world, rank, local_rank):
                 "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
                            "global_batch": B, "samples": S, "samples_per_gpu": S_loc,
                            "params": P, "parallelism": f"sample-sharded x{world}",
+                           "loss_aggregation": "loss of the mean prediction (exact, PAPER.md:272-281)"
+                                               if args.agg == "mean" else "mean of per-sample losses (Alg. 1 l.9)",
                            "optimizer": "fused Adam (in the timed step)" if adam else
                                         "none (step returns grad_mu, grad_rho; north_star boundary)",
                            "l2": "flushed between timed steps (256 MiB memset outside events)"},
@@ -329,7 +333,7 @@ def run_ours(args, world, rank, local_rank):
                                   "untimed steps (profiling off in the timed region)"}
         line["roofline"] = roofline(model, B_loc, S_loc, prof, prof_steps, peaks, peak_src)
         if world == 1 and not args.no_cpu_baseline:
-            r, cores, sample = cpu_oracle_rate(model, B, D, budget_s=args.ref_budget,
+            r, cores, sample = cpu_oracle_rate(MODELS[cfg["model"]], B, D, budget_s=args.ref_budget,
                                                aug=cfg.get("aug", "none"))
             line["cpu_baseline"] = {"value": r, "unit": "sample·images/s", "cores": cores,
                                     "kind": "oracle", "sample": sample}
@@ -440,6 +444,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=None,
                     help="seconds of oracle CPU work per reference step (default: 150 s / (K+W))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--agg", default="sample", choices=["sample", "mean"],
+                    help="mean: exact aggregation, the loss of the mean prediction (MLP configs)")
     ap.add_argument("--optimizer", default="none", choices=["none", "adam"],
                     help="adam: each step also applies the fused Adam update (bnn_elbo_step_adam)")
     args = ap.parse_args()

@@ -57,7 +57,14 @@ typedef enum {
 } bnn_status;
 
 enum { BNN_MODEL_MLP = 0, BNN_MODEL_RESNET18 = 1 };
-enum { BNN_LOSS_CE = 0, BNN_LOSS_MSE = 1 };
+/* BNN_LOSS_CE / _MSE: L_data = (1/S) Σ_s Loss(ŷ_s, y), the per-sample average of Alg. 1 l.9
+ * (PAPER.md:162). BNN_LOSS_CE_MEAN / _MSE_MEAN: exact aggregation (§4.1;
+ * SURVEY.md §8(f) f1), the loss of the MEAN prediction — CE of the arithmetic mean of the
+ * class probabilities over the S samples, MSE of the mean output. The mean
+ * needs every sample group's statistic before any backward: bnn_elbo_step exchanges it with
+ * one extra allgather between forward and backward; virtual ranks use bnn_mean_stats +
+ * bnn_elbo_partial_mean. MLP models only (BNN_ERR_CONFIG otherwise). */
+enum { BNN_LOSS_CE = 0, BNN_LOSS_MSE = 1, BNN_LOSS_CE_MEAN = 2, BNN_LOSS_MSE_MEAN = 3 };
 enum { BNN_PREC_FP32 = 0, BNN_PREC_BF16 = 1 };
 enum { BNN_MODE_SAMPLE_SHARDED = 0, BNN_MODE_DATA_SHARDED = 1, BNN_MODE_HYBRID = 2 };
 enum { BNN_AUG_NONE = 0, BNN_AUG_PER_SAMPLE = 1 };
@@ -170,6 +177,20 @@ int bnn_elbo_partial(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev,
  *   loss = acc[2P] + ½Σ(σ² + μ² − 1 − 2 ln σ)/|D|. */
 int bnn_finalize(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* acc_dev,
                  float* loss_dev, float* grad_mu_dev, float* grad_rho_dev);
+
+/* Exact aggregation, virtual-rank form (BNN_LOSS_*_MEAN only). bnn_mean_stats runs this
+ * rank's sampled forward passes and writes its statistic: stats_dev[b·w + j] = Σ over the
+ * rank's samples of p_{s,b,y_b} (CE, w = 1) or of ŷ_{s,b,j} (MSE, w = outputs), fp32, for its
+ * B_loc examples. Summing the stats of the K sample groups of a data group (any order gives
+ * the same value up to fp32 rounding) and passing the sum to bnn_elbo_partial_mean yields
+ * this rank's acc partial of the exact step (the data loss is counted by sample group 0). */
+int bnn_mean_stats(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* x_dev,
+                   const int32_t* ycls_dev, int32_t B_loc, int32_t B_global, int32_t S_global,
+                   uint64_t seed, uint32_t step, float* stats_dev);
+int bnn_elbo_partial_mean(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev,
+                          const float* x_dev, const int32_t* ycls_dev, const float* yreg_dev,
+                          int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
+                          uint32_t step, const float* stats_global_dev, float* acc_dev);
 
 /* Adam hyper-parameters of the fused optimizer step (PAPER.md:166 and
  * :265, Alg. 1 l.13 / Alg. 2 l.16 "Update μ and σ using optimizer (e.g., Adam)"; Kingma & Ba

@@ -105,6 +105,11 @@ struct bnn_ctx {
     int K = 1, G = 1, kidx = 0, gidx = 0;
     int S_loc_max = 0, B_max = 0, chunk = 0;
     bool bf16 = false;
+    int agg = 0;               // 1: loss of the mean prediction (BNN_LOSS_*_MEAN), SURVEY §8(f) f1
+    int stat_w = 0;            // agg: statistic width per example (CE 1, MSE O)
+    float* mstats = nullptr;   // agg: this rank's Σ_s statistic [B_max × stat_w]
+    float* mstats_g = nullptr; // agg: merged over the sample groups
+    float* mgather = nullptr;  // agg: allgather buffer [world × B_max × stat_w]
     cudaStream_t st = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;

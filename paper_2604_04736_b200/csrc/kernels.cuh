@@ -48,6 +48,17 @@ void launch_finalize_adam(float* mu, float* rho, const float* acc_mu, const floa
 void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,
                       const int32_t* ycls, const float* yreg, void* dz, int ldg, bool dz_bf16,
                       float* lossrow, float* dz_f32, cudaStream_t st);
+// exact aggregation: loss of the mean prediction over the S samples
+void launch_mean_stats(const float* logits, int Sc, int B, int O, int loss_kind,
+                       const int32_t* ycls, float* stats, cudaStream_t st);
+void launch_mean_merge(const float* gathered, int world, int G, int g, int64_t n, float* out,
+                       cudaStream_t st);
+void launch_mean_loss_head(const float* logits, int S, int B, int O, int loss_kind,
+                           const int32_t* ycls, const float* yreg, const float* gstats,
+                           int S_glob, void* dz, int ldg, bool dz_bf16, float* dz_f32,
+                           cudaStream_t st);
+void launch_mean_loss_value(const float* gstats, int B, int O, int loss_kind, const float* yreg,
+                            int S_glob, float scale, float* acc_slot, cudaStream_t st);
 // acc[2P] += scale · Σ lossrow[0..n) in fixed order
 void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slot,
                         cudaStream_t st);

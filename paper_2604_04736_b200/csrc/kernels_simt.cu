@@ -265,6 +265,146 @@ void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slo
     loss_reduce_kernel<<<1, 1024, 0, st>>>(lossrow, n, scale, acc_slot);
 }
 
+// ---------------------------------------------------------------- exact aggregation
+// Loss of the mean prediction over all S samples: CE of the arithmetic
+// mean of the true-class probabilities, or MSE of the mean output. The per-rank statistic is
+// a plain fp32 sum over this rank's samples (CE: Σ_s p_{s,b,y}, width 1; MSE: Σ_s ŷ_{s,b,o},
+// width O), accumulated sample by sample in order (deterministic), merged over the sample
+// groups, then turned into per-sample gradient seeds.
+__global__ void mean_stats_kernel(const float* __restrict__ logits, int Sc, int B, int O,
+                                  int loss_kind, const int32_t* __restrict__ ycls,
+                                  float* __restrict__ stats) {
+    if (loss_kind == 0) {  // CE: one warp per example, lanes over samples, fixed-order warp sum
+        const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+        const int lane = threadIdx.x & 31;
+        if (b >= B) return;
+        const int y = ycls[b];
+        float part = 0.0f;
+        for (int s = lane; s < Sc; s += 32) {
+            const float* z = logits + ((int64_t)s * B + b) * O;
+            float m = z[0];
+            for (int k = 1; k < O; ++k) m = fmaxf(m, z[k]);
+            float se = 0.0f;
+            for (int k = 0; k < O; ++k) se += expf(z[k] - m);
+            part += expf(z[y] - m) / se;
+        }
+        part = warp_sum(part);
+        if (lane == 0) stats[b] += part;
+    } else {  // MSE: one thread per (example, output), samples in order
+        const int i = blockIdx.x * blockDim.x + threadIdx.x;
+        if (i >= B * O) return;
+        float acc = stats[i];
+        for (int s = 0; s < Sc; ++s) acc += logits[(int64_t)s * B * O + i];
+        stats[i] = acc;
+    }
+}
+
+void launch_mean_stats(const float* logits, int Sc, int B, int O, int loss_kind,
+                       const int32_t* ycls, float* stats, cudaStream_t st) {
+    if (loss_kind == 0)
+        mean_stats_kernel<<<(B + 7) / 8, 256, 0, st>>>(logits, Sc, B, O, loss_kind, ycls, stats);
+    else
+        mean_stats_kernel<<<(B * O + 127) / 128, 128, 0, st>>>(logits, Sc, B, O, loss_kind, ycls, stats);
+}
+
+// out[i] = Σ over ranks r with r % G == g (the sample groups of data group g), in rank order
+__global__ void mean_merge_kernel(const float* __restrict__ gathered, int world, int G, int g,
+                                  int64_t n, float* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float acc = 0.0f;
+    for (int r = g; r < world; r += G) acc += gathered[(int64_t)r * n + i];
+    out[i] = acc;
+}
+
+void launch_mean_merge(const float* gathered, int world, int G, int g, int64_t n, float* out,
+                       cudaStream_t st) {
+    mean_merge_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(gathered, world, G, g, n, out);
+}
+
+// Gradient seed of the mean-prediction loss for each (s, b) row, unscaled like loss_head_kernel
+// (the 1/(S·B) or 1/(S·B·O) scale is applied downstream):
+//   CE:  dz_k = (S·p_{s,y}/Σ_s' p_{s',y}) · (p_k − [k = y])      (= (p_y/P̄)(p − onehot))
+//   MSE: dz_o = 2·(Σ_s' ŷ_{s',o}/S − y_o)
+__global__ void mean_loss_head_kernel(const float* __restrict__ logits, int rows, int B, int O,
+                                      int loss_kind, const int32_t* __restrict__ ycls,
+                                      const float* __restrict__ yreg,
+                                      const float* __restrict__ gstats, float S_glob,
+                                      void* __restrict__ dz, int ldg, int dz_bf16,
+                                      float* __restrict__ dz_f32) {
+    const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (warp >= rows) return;
+    const int b = warp % B;
+    const float* z = logits + (int64_t)warp * O;
+    auto put = [&](int k, float v) {
+        if (dz_f32 && k < O) dz_f32[(int64_t)warp * O + k] = v;
+        if (dz_bf16)
+            reinterpret_cast<__nv_bfloat16*>(dz)[(int64_t)warp * ldg + k] = __float2bfloat16_rn(v);
+        else
+            reinterpret_cast<float*>(dz)[(int64_t)warp * ldg + k] = v;
+    };
+    if (loss_kind == 0) {
+        float m = -INFINITY;
+        for (int k = lane; k < O; k += 32) m = fmaxf(m, z[k]);
+        m = warp_max(m);
+        float se = 0.0f;
+        for (int k = lane; k < O; k += 32) se += expf(z[k] - m);
+        se = warp_sum(se);
+        const float lse = m + logf(se);
+        const int y = ycls[b];
+        const float w = S_glob * expf(z[y] - lse) / gstats[b];
+        for (int k = lane; k < O; k += 32) put(k, w * (expf(z[k] - lse) - (k == y ? 1.0f : 0.0f)));
+    } else {
+        for (int k = lane; k < O; k += 32)
+            put(k, 2.0f * (gstats[(int64_t)b * O + k] / S_glob - yreg[(int64_t)b * O + k]));
+    }
+    for (int k = O + lane; k < ldg; k += 32) put(k, 0.0f);
+}
+
+void launch_mean_loss_head(const float* logits, int S, int B, int O, int loss_kind,
+                           const int32_t* ycls, const float* yreg, const float* gstats,
+                           int S_glob, void* dz, int ldg, bool dz_bf16, float* dz_f32,
+                           cudaStream_t st) {
+    const int rows = S * B;
+    mean_loss_head_kernel<<<(rows + 7) / 8, 256, 0, st>>>(logits, rows, B, O, loss_kind, ycls, yreg,
+                                                          gstats, (float)S_glob, dz, ldg,
+                                                          dz_bf16 ? 1 : 0, dz_f32);
+}
+
+// acc_slot += scale · Σ_b ℓ_b with ℓ_b = −ln(Σ_s p_y / S) (CE) or Σ_o (Σ_s ŷ_o / S − y_o)² (MSE)
+__global__ void mean_loss_value_kernel(const float* __restrict__ gstats, int B, int O,
+                                       int loss_kind, const float* __restrict__ yreg,
+                                       float S_glob, float scale, float* __restrict__ acc_slot) {
+    __shared__ double red[32];
+    double t = 0.0;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        if (loss_kind == 0) {
+            t += -log((double)gstats[b] / (double)S_glob);
+        } else {
+            for (int k = 0; k < O; ++k) {
+                const double d = (double)gstats[(int64_t)b * O + k] / (double)S_glob -
+                                 (double)yreg[(int64_t)b * O + k];
+                t += d * d;
+            }
+        }
+    }
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        acc_slot[0] = (float)((double)acc_slot[0] + s * (double)scale);
+    }
+}
+
+void launch_mean_loss_value(const float* gstats, int B, int O, int loss_kind, const float* yreg,
+                            int S_glob, float scale, float* acc_slot, cudaStream_t st) {
+    mean_loss_value_kernel<<<1, 1024, 0, st>>>(gstats, B, O, loss_kind, yreg, (float)S_glob, scale,
+                                               acc_slot);
+}
+
 // ====================================================================== K1: ε fill / bench
 __global__ void eps_fill_kernel(EpsKey key, uint32_t step, uint32_t s, uint32_t t, uint32_t r0,
                                 uint32_t nr, uint32_t c0, uint32_t nc, float* __restrict__ out) {

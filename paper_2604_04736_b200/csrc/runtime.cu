@@ -148,9 +148,14 @@ int alloc_mlp(bnn_ctx* c) {
 }
 
 // ------------------------------------------------------------------ one chunk of samples
+// phase 0: forward, per-sample loss head, backward (Alg. 1 l.7-12 for the chunk)
+// phase 1: forward + the exact-aggregation statistic only
+// phase 2: (forward unless skip_fwd,) mean-prediction loss head from gstats, backward
+enum { kPhaseFull = 0, kPhaseStats = 1, kPhaseMeanBwd = 2 };
 int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
               const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
-              uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+              uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss,
+              int phase = kPhaseFull, bool skip_fwd = false, const float* gstats = nullptr) {
     const int L = (int)c->layers.size();
     cudaStream_t st = c->st;
     SampleKeys kk{make_key(seed), step, s0};
@@ -158,7 +163,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                                                      : 1.0f / ((float)S_glob * B_glob * c->O);
     if (!c->bf16) {
         // ---------------- FP32 SIMT path (parity mode)
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < L && !skip_fwd; ++l) {
             SampledLayer sl = sampled(c, l, mu);
             const float* A = l == 0 ? x : (const float*)c->act[l];
             const int64_t sA = l == 0 ? 0 : (int64_t)B * c->ld[l];
@@ -166,10 +171,20 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             const int64_t sZ = (int64_t)B * (l == L - 1 ? c->O : c->ld[l + 1]);
             c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, Sc, B, A, sA, Z, sZ, l < L - 1, st); });
         }
-        c->launch("loss", [&] {
-            launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1], c->O,
-                             false, c->lossrow, nullptr, st);
-        });
+        if (phase == kPhaseStats) {
+            c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->model.loss, ycls, c->mstats, st); });
+            return BNN_OK;
+        }
+        if (phase == kPhaseMeanBwd)
+            c->launch("loss", [&] {
+                launch_mean_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, gstats, S_glob,
+                                      c->grad[L - 1], c->O, false, nullptr, st);
+            });
+        else
+            c->launch("loss", [&] {
+                launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1], c->O,
+                                 false, c->lossrow, nullptr, st);
+            });
         for (int l = L - 1; l >= 0; --l) {
             SampledLayer sl = sampled(c, l, mu);
             const float* Gl = (const float*)c->grad[l];
@@ -193,7 +208,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
         // ---------------- BF16 tcgen05 path
         if (B > 256 * 64) return c->set_err(BNN_ERR_CONFIG, "B_loc too large");
         const int nb = (int)round_up(std::min(B, 256), 16);
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < L && !skip_fwd; ++l) {
             TcGenArgs a{};
             a.L = sampled(c, l, mu);
             a.kk = kk;
@@ -211,10 +226,20 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, Sc, st); });
         }
-        c->launch("loss", [&] {
-            launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1],
-                             c->ld[L], true, c->lossrow, c->dz_f32, st);
-        });
+        if (phase == kPhaseStats) {
+            c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->model.loss, ycls, c->mstats, st); });
+            return BNN_OK;
+        }
+        if (phase == kPhaseMeanBwd)
+            c->launch("loss", [&] {
+                launch_mean_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, gstats, S_glob,
+                                      c->grad[L - 1], c->ld[L], true, c->dz_f32, st);
+            });
+        else
+            c->launch("loss", [&] {
+                launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1],
+                                 c->ld[L], true, c->lossrow, c->dz_f32, st);
+            });
         for (int l = L - 1; l >= 1; --l) {
             TcGenArgs a{};
             a.L = sampled(c, l, mu);
@@ -273,7 +298,8 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             }, 2);
         }
     }
-    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    if (phase == kPhaseFull)
+        c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
     return BNN_OK;
 }
 
@@ -442,34 +468,87 @@ int check_step_args(bnn_ctx* c, int B_loc, int B_glob, int S_glob) {
     return BNN_OK;
 }
 
-// local partial sums into acc (zeroed first)
+// local partial sums into acc (zeroed first).
+// Exact aggregation (c->agg): stats_out != NULL → only this rank's statistic
+// (bnn_mean_stats); gstats_in != NULL → the backward with the caller's merged statistic
+// (bnn_elbo_partial_mean); neither → both phases with the statistic exchanged over the
+// communicator (one allgather between forward and backward) or, for world 1, used as is.
 int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
                 const float* yreg, int B_loc, int B_glob, int S_glob, uint64_t seed, uint32_t step,
-                float* acc) {
+                float* acc, const float* gstats_in = nullptr, float* stats_out = nullptr) {
     int rc = check_step_args(c, B_loc, B_glob, S_glob);
     if (rc) return rc;
     if (c->model.loss == BNN_LOSS_CE && !ycls) return c->set_err(BNN_ERR_CONFIG, "CE loss needs int32 labels");
     if (c->model.loss == BNN_LOSS_MSE && !yreg) return c->set_err(BNN_ERR_CONFIG, "MSE loss needs fp32 targets");
+    if ((gstats_in || stats_out) && !c->agg)
+        return c->set_err(BNN_ERR_CONFIG, "mean statistics need a BNN_LOSS_*_MEAN model");
     cudaStream_t st = c->st;
-    CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(float) * c->acc_total, st));
+    if (!stats_out) CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(float) * c->acc_total, st));
     c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
     if (c->bf16 && c->model.kind == BNN_MODEL_MLP) {
         const int K0 = c->widths[0];
         c->launch("cast", [&] { launch_to_bf16(x, B_loc, K0, c->ld[0], c->xb, st); });
     }
     const int S_loc = S_glob / c->K;
+    float* accm = acc;
+    float* accr = acc ? acc + c->P_pad : nullptr;
+    float* accl = acc ? acc + 2 * c->P_pad : nullptr;
+    if (c->agg) {
+        const bool single = S_loc <= c->chunk;  // activations of the stats pass stay valid
+        const float* gstats = gstats_in;
+        if (!gstats_in) {
+            CUDA_TRY(c, cudaMemsetAsync(c->mstats, 0, sizeof(float) * (size_t)B_loc * c->stat_w, st));
+            for (int s = 0; s < S_loc; s += c->chunk) {
+                const int Sc = std::min(c->chunk, S_loc - s);
+                const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
+                rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr,
+                               accl, kPhaseStats);
+                if (rc) return rc;
+            }
+            if (stats_out) {
+                CUDA_TRY(c, cudaMemcpyAsync(stats_out, c->mstats, sizeof(float) * (size_t)B_loc * c->stat_w,
+                                            cudaMemcpyDeviceToDevice, st));
+                CUDA_TRY(c, cudaGetLastError());
+                return BNN_OK;
+            }
+            if (c->comm) {
+                // Σ over the K sample groups of this data group, in rank order (PAPER.md:281
+                // "additional communication"); one allgather, then a deterministic merge
+                const int64_t n = (int64_t)B_loc * c->stat_w;
+                NCCL_TRY(c, ncclAllGather(c->mstats, c->mgather, (size_t)n, ncclFloat32, c->comm, st));
+                c->launch("loss", [&] { launch_mean_merge(c->mgather, c->cfg.world, c->G, c->gidx, n, c->mstats_g, st); });
+                gstats = c->mstats_g;
+            } else {
+                if (c->K != 1)
+                    return c->set_err(BNN_ERR_CONFIG, "K > 1 without a communicator: use bnn_mean_stats + bnn_elbo_partial_mean");
+                gstats = c->mstats;
+            }
+        }
+        for (int s = 0; s < S_loc; s += c->chunk) {
+            const int Sc = std::min(c->chunk, S_loc - s);
+            const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
+            rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl,
+                           kPhaseMeanBwd, single && !gstats_in, gstats);
+            if (rc) return rc;
+        }
+        if (c->kidx == 0) {  // the data loss counts each example once: sample group 0 adds it
+            const float sc = c->model.loss == BNN_LOSS_CE ? 1.0f / (float)B_glob : 1.0f / ((float)B_glob * c->O);
+            c->launch("loss", [&] {
+                launch_mean_loss_value(gstats, B_loc, c->O, c->model.loss, yreg, S_glob, sc, accl, st);
+            });
+        }
+        CUDA_TRY(c, cudaGetLastError());
+        return BNN_OK;
+    }
     for (int s = 0; s < S_loc; s += c->chunk) {
         const int Sc = std::min(c->chunk, S_loc - s);
         const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
         if (c->model.kind == BNN_MODEL_MLP)
-            rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
-                           acc + c->P_pad, acc + 2 * c->P_pad);
+            rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
         else if (c->bf16)
-            rc = resnet_bf16_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
-                                   acc + c->P_pad, acc + 2 * c->P_pad);
+            rc = resnet_bf16_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
         else
-            rc = resnet_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, acc,
-                              acc + c->P_pad, acc + 2 * c->P_pad);
+            rc = resnet_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
         if (rc) return rc;
     }
     CUDA_TRY(c, cudaGetLastError());
@@ -553,8 +632,15 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown precision"));
     if (cfg->aug != BNN_AUG_NONE && cfg->aug != BNN_AUG_PER_SAMPLE)
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown aug mode"));
-    if (model->loss != BNN_LOSS_CE && model->loss != BNN_LOSS_MSE)
+    if (model->loss < BNN_LOSS_CE || model->loss > BNN_LOSS_MSE_MEAN)
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown loss"));
+    if (model->loss >= BNN_LOSS_CE_MEAN) {
+        // exact aggregation: the base loss family, plus the mean-statistic exchange
+        if (model->kind != BNN_MODEL_MLP)
+            return fail(c->set_err(BNN_ERR_CONFIG, "mean-prediction losses are implemented for MLP models"));
+        c->agg = 1;
+        c->model.loss = model->loss == BNN_LOSS_CE_MEAN ? BNN_LOSS_CE : BNN_LOSS_MSE;
+    }
     c->bf16 = cfg->precision == BNN_PREC_BF16;
     c->B_max = cfg->max_B_loc;
     c->S_loc_max = cfg->max_S_loc;
@@ -589,6 +675,12 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
         return fail(c->set_err(BNN_ERR_CUDA, "out of device memory"));
     rc = model->kind == BNN_MODEL_MLP ? alloc_mlp(c) : alloc_resnet(c);
     if (rc) return fail(rc);
+    if (c->agg) {
+        c->stat_w = c->model.loss == BNN_LOSS_CE ? 1 : c->O;
+        const size_t n = (size_t)c->B_max * c->stat_w;
+        if (!c->alloc(&c->mstats, n) || !c->alloc(&c->mstats_g, n) || !c->alloc(&c->mgather, n * cfg->world))
+            return fail(c->set_err(BNN_ERR_CUDA, "out of device memory"));
+    }
     // ---- communicator
     if (cfg->nccl_uid) {  // also for world == 1 (exercises the NCCL path on one GPU)
         ncclUniqueId id;
@@ -640,6 +732,26 @@ int bnn_elbo_partial(bnn_ctx* c, const float* mu, const float* rho, const float*
                      uint32_t step, float* acc_dev) {
     if (!c || !mu || !rho || !x || !acc_dev) return BNN_ERR_CONFIG;
     return run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, acc_dev);
+}
+
+int bnn_mean_stats(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
+                   int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed, uint32_t step,
+                   float* stats_dev) {
+    if (!c || !mu || !rho || !x || !stats_dev) return BNN_ERR_CONFIG;
+    if (!c->agg) return c->set_err(BNN_ERR_CONFIG, "bnn_mean_stats needs a BNN_LOSS_*_MEAN model");
+    // MSE statistics need no targets; pass a dummy non-null pointer through the label checks
+    const float* yreg = c->model.loss == BNN_LOSS_MSE ? x : nullptr;
+    return run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, nullptr, nullptr,
+                       stats_dev);
+}
+
+int bnn_elbo_partial_mean(bnn_ctx* c, const float* mu, const float* rho, const float* x,
+                          const int32_t* ycls, const float* yreg, int32_t B_loc, int32_t B_global,
+                          int32_t S_global, uint64_t seed, uint32_t step, const float* stats_global_dev,
+                          float* acc_dev) {
+    if (!c || !mu || !rho || !x || !acc_dev || !stats_global_dev) return BNN_ERR_CONFIG;
+    return run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, acc_dev,
+                       stats_global_dev);
 }
 
 int bnn_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc_dev, float* loss_dev,

@@ -18,7 +18,7 @@ _SO = os.path.join(_HERE, "libbnn.so")
 _lib = None
 
 MODEL_MLP, MODEL_RESNET18 = 0, 1
-LOSS = {"ce": 0, "mse": 1}
+LOSS = {"ce": 0, "mse": 1, "ce_mean": 2, "mse_mean": 3}  # *_mean: exact aggregation
 PREC = {"fp32": 0, "bf16": 1}
 MODE = {"sample": 0, "data": 1, "hybrid": 2}
 AUG = {"none": 0, "per_sample": 1}
@@ -72,6 +72,8 @@ def lib():
     L.bnn_elbo_step_host.argtypes = step_args + [vp, vp, vp]
     L.bnn_elbo_partial.argtypes = step_args + [vp]
     L.bnn_finalize.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.bnn_mean_stats.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, u64, u32, vp]
+    L.bnn_elbo_partial_mean.argtypes = step_args + [vp, vp]
     L.bnn_finalize_adam.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.bnn_elbo_step_adam.argtypes = step_args + [vp] * 9
     L.bnn_predict.argtypes = [vp, vp, vp, vp, i32, i32, u64, u32, vp, vp]
@@ -236,6 +238,23 @@ class Context:
         yc, yr = self._y(y)
         _check(self._L.bnn_elbo_partial(self._h, _p(mu), _p(rho), _p(x), yc, yr, x.shape[0],
                                         B_global, S_global, seed, step, _p(acc)), self._h)
+        return acc
+
+    def mean_stats(self, mu, rho, x, y, B_global, S_global, seed, step, width):
+        """This rank's exact-aggregation statistic [B_loc, width] (bnn_mean_stats)."""
+        out = torch.zeros(x.shape[0] * width, dtype=torch.float32, device=self.device)
+        yc, _ = self._y(y)
+        _check(self._L.bnn_mean_stats(self._h, _p(mu), _p(rho), _p(x), yc, x.shape[0], B_global,
+                                      S_global, seed, step, _p(out)), self._h)
+        return out
+
+    def elbo_partial_mean(self, mu, rho, x, y, B_global, S_global, seed, step, stats, acc=None):
+        if acc is None:
+            acc = torch.zeros(self.acc_total, dtype=torch.float32, device=self.device)
+        yc, yr = self._y(y)
+        _check(self._L.bnn_elbo_partial_mean(self._h, _p(mu), _p(rho), _p(x), yc, yr, x.shape[0],
+                                             B_global, S_global, seed, step, _p(stats), _p(acc)),
+               self._h)
         return acc
 
     def finalize(self, mu, rho, acc):
