@@ -34,10 +34,9 @@ namespace gen {
 constexpr int kGenWarps = 8;  // 16 was measured: issue-active 64 -> 76 %, no faster (56 regs)
 constexpr int kItems = kGenWarps == 16 ? 4 : 8;  // 4-element items per thread per k-block
 constexpr int kThreads = (kGenWarps + 1) * 32;  // + one control warp (TMEM alloc, MMA issue)
-constexpr int kStages = 2;
 constexpr int kAStage = 128 * 64 * 2;           // 16 KB generated W tile
 constexpr int kBStage = 256 * 64 * 2;           // 32 KB activation/gradient tile
-constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256 + 128 * 4;
+constexpr int smem_bytes(int stages) { return 1024 + stages * (kAStage + kBStage) + 256 + 128 * 4; }
 }  // namespace gen
 
 __device__ __forceinline__ void load_mu_sigma4(const SampledLayer& L, int64_t i, int kvalid,
@@ -98,7 +97,7 @@ __device__ __forceinline__ void sts64(uint32_t addr, uint2 v) {
     asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
 }
 
-template <int MODE>
+template <int MODE, int STAGES>
 __global__ void __launch_bounds__(gen::kThreads, 2)
     gen_gemm_kernel(const __grid_constant__ CUtensorMap tmB, const TcGenArgs a) {
     using namespace gen;
@@ -107,13 +106,13 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     // address space, so plain loads/stores through it compile to LDS/STS
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + kStages * kAStage;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+    uint8_t* sB = smem + STAGES * kAStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * kBStage);
     uint64_t* full_gen = bars;
-    uint64_t* full_tma = bars + kStages;
-    uint64_t* empty = bars + 2 * kStages;
-    uint64_t* tfull = bars + 3 * kStages;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 * kStages + 1);
+    uint64_t* full_tma = bars + STAGES;
+    uint64_t* empty = bars + 2 * STAGES;
+    uint64_t* tfull = bars + 3 * STAGES;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
     float* sbias = reinterpret_cast<float*>(bars + 32);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -122,7 +121,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     const SampledLayer& L = a.L;
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full_gen[i], kGenWarps);
             mbar_init(&full_tma[i], 1);
             mbar_init(&empty[i], 1);
@@ -150,10 +149,10 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
         if (lane == 0) {
             const uint32_t idesc = idesc_bf16(128, a.nb, MODE == 1 ? 1 : 0, 0);
             for (int kb = 0; kb < nkb; ++kb) {
-                const int st = kb % kStages;
-                const uint32_t ph = (kb / kStages) & 1;
-                mbar_wait_sleep(&full_gen[st], ph);
-                mbar_wait_sleep(&full_tma[st], ph);
+                const int st = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait_suspend(&full_gen[st], ph);
+                mbar_wait_suspend(&full_tma[st], ph);
                 tc_fence_after();
                 const uint32_t aBase = smem_u32(sA + st * kAStage);
                 const uint32_t bBase = smem_u32(sB + st * kBStage);
@@ -188,8 +187,8 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
         const uint32_t w3 = (L.t_w << 20) | sg;
         const bool m_full = MODE == 0 ? (m0 + 128 <= L.N) : (m0 + 128 <= L.K);
         for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb % kStages;
-            const uint32_t ph = (kb / kStages) & 1;
+            const int st = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
             mbar_wait(&empty[st], ph ^ 1);
             if (tid == 0) {
                 mbar_arrive_expect_tx(&full_tma[st], kBStage);
@@ -227,7 +226,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
             if (lane == 0) mbar_arrive(&full_gen[st]);
         }
         // ------------------------------------------------ epilogue
-        mbar_wait_sleep(tfull, 0);
+        mbar_wait_suspend(tfull, 0);
         tc_fence_after();
         const int q = warp & 3, h = warp >> 2;
         const int row = 32 * q + lane, m = m0 + row;
@@ -293,20 +292,28 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     }
 }
 
-void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st) {
+// STAGES = 2 (2 CTAs/SM) for the wide layers, whose generation hides the TMA latency; a
+// single-M-tile forward layer (the 10-wide output layer: 10 of 128 rows generated) is
+// TMA-latency-bound instead and gets 4 stages (prefetch distance 3, 1 CTA/SM).
+template <int MODE, int STAGES>
+static void launch_gen_gemm_t(dim3 grid, const CUtensorMap& tmB, const TcGenArgs& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gen_gemm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             gen::kSmem);
-        cudaFuncSetAttribute(gen_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             gen::kSmem);
+        cudaFuncSetAttribute(gen_gemm_kernel<MODE, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             gen::smem_bytes(STAGES));
         attr = true;
     }
+    gen_gemm_kernel<MODE, STAGES><<<grid, gen::kThreads, gen::smem_bytes(STAGES), st>>>(tmB, a);
+}
+
+void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st) {
     dim3 grid((a.M + 127) / 128, S, (a.B + 255) / 256);
-    if (a.mode == 0)
-        gen_gemm_kernel<0><<<grid, gen::kThreads, gen::kSmem, st>>>(tmB, a);
+    if (a.mode == 0 && grid.x == 1)
+        launch_gen_gemm_t<0, 4>(grid, tmB, a, st);
+    else if (a.mode == 0)
+        launch_gen_gemm_t<0, 2>(grid, tmB, a, st);
     else
-        gen_gemm_kernel<1><<<grid, gen::kThreads, gen::kSmem, st>>>(tmB, a);
+        launch_gen_gemm_t<1, 2>(grid, tmB, a, st);
 }
 
 // ============================================================================ K5
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
                 for (int bb = 0; bb < nbb; ++bb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    mbar_wait_suspend(&empty[st], ph ^ 1);
                     mbar_arrive_expect_tx(&full[st], kAStage + kBStage);
                     uint8_t* a_st = sA + st * kAStage;
                     tma_load_3d(mapG, &full[st], a_st, n0, 64 * bb, s);
@@ -399,12 +406,12 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
             int it = 0;
             for (int s = 0; s < S; ++s) {
                 const int buf = s & 1;
-                mbar_wait_sleep(&tempty[buf], ((s >> 1) & 1) ^ 1);
+                mbar_wait_suspend(&tempty[buf], ((s >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int bb = 0; bb < nbb; ++bb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&full[st], ph);
+                    mbar_wait_suspend(&full[st], ph);
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
                     const uint32_t bBase = smem_u32(sB + st * kBStage);

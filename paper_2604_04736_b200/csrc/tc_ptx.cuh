@@ -76,10 +76,39 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t pari
         : "memory");
     return ok != 0;
 }
+// Single-thread role waits (TMA producer, MMA issuer). BNN_SUSPEND_WAITS selects the
+// suspend-hint form (try_wait with a 1 ms hint: ptxas emits a NANOSLEEP.SYNCS after each
+// failed probe); the default polls with the plain try_wait, whose wake-up follows the phase
+// flip directly — the suspended form was measured to delay the MMA issue of short k-loops.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+#ifdef BNN_SUSPEND_WAITS
     if (mbar_try_wait_sleep(a, parity)) return;
+#else
+    if (mbar_try_wait(a, parity)) return;
+#endif
 #ifdef BNN_WATCHDOG  // development builds: BNN_NVCC_FLAGS=-DBNN_WATCHDOG (costs ≈ 2 % on C2)
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try_wait(a, parity)) {
+        if (globaltimer_ns() - t0 > kWaitTimeoutNs) mbar_timeout(a, parity);
+    }
+#elif defined(BNN_SUSPEND_WAITS)
+    while (!mbar_try_wait_sleep(a, parity)) {
+    }
+#else
+    while (!mbar_try_wait(a, parity)) {
+    }
+#endif
+}
+
+// The suspend-hint form for role threads that share an SMSP with ALU-bound warps (the MLP
+// generator kernels): a polling MMA/TMA thread there costs the generators issue slots
+// (C2: 0.875 → 0.885 ms/step polling), while the conv kernels gain from polling (C3 6.84 →
+// 6.75 ms/step).
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait_sleep(a, parity)) return;
+#ifdef BNN_WATCHDOG
     const uint64_t t0 = globaltimer_ns();
     while (!mbar_try_wait_sleep(a, parity)) {
         if (globaltimer_ns() - t0 > kWaitTimeoutNs) mbar_timeout(a, parity);
