@@ -90,6 +90,20 @@ void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B,
                        int64_t strideG, const float* A, int64_t strideA, float scale,
                        float* acc_mu, float* acc_rho, cudaStream_t st);
 // bias gradient from fp32 partial column sums parts[s][p][n] (p < nparts, row pitch ldp)
+// all bias tensors of up to 4 layers in two launches (per-layer parts as launch_bias_grad;
+// db_scratch holds 2·S·N_l floats per layer, consecutively)
+constexpr int kMaxBiasGroup = 4;
+struct BiasGroup {
+    SampledLayer L[kMaxBiasGroup];
+    const float* parts[kMaxBiasGroup];
+    int nparts[kMaxBiasGroup], ldp[kMaxBiasGroup];
+    int64_t strideS[kMaxBiasGroup];
+    int blk_base[kMaxBiasGroup];
+    int64_t db_off[kMaxBiasGroup];
+    int n;
+};
+void launch_bias_grad_grouped(BiasGroup g, const SampleKeys& k, int S, float scale,
+                              float* db_scratch, float* acc_mu, float* acc_rho, cudaStream_t st);
 void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
                       int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
                       float* acc_mu, float* acc_rho, cudaStream_t st);

@@ -846,6 +846,88 @@ __global__ void bias_acc_kernel(SampledLayer L, int S, const float* __restrict__
     }
 }
 
+// Grouped form (all layers of the MLP step in two launches instead of two per layer): the
+// same per-layer arithmetic and summation order as bias_reduce_kernel / bias_acc_kernel.
+__global__ void __launch_bounds__(32 * kBiasGroups)
+    bias_reduce_grouped_kernel(const BiasGroup g, SampleKeys kk, int S, float* __restrict__ db_base) {
+    __shared__ float red[kBiasGroups][33];
+    int l = 0;
+    while (l + 1 < g.n && (int)blockIdx.x >= g.blk_base[l + 1]) ++l;
+    const SampledLayer& L = g.L[l];
+    const int nparts = g.nparts[l], ldp = g.ldp[l];
+    float* db = db_base + g.db_off[l];
+    const int G = blockDim.x >> 5;
+    const int tx = threadIdx.x & 31, gi = threadIdx.x >> 5;
+    const int n = (blockIdx.x - g.blk_base[l]) * 32 + tx, s = blockIdx.y;
+    float acc = 0.0f;
+    if (n < L.N) {
+        const float* p = g.parts[l] + s * g.strideS[l] + n;
+        float a0 = 0.0f, a1 = 0.0f;
+        int i = gi;
+        for (; i + G < nparts; i += 2 * G) {
+            a0 += __ldg(p + (int64_t)i * ldp);
+            a1 += __ldg(p + (int64_t)(i + G) * ldp);
+        }
+        if (i < nparts) a0 += __ldg(p + (int64_t)i * ldp);
+        acc = a0 + a1;
+    }
+    red[gi][tx] = acc;
+    __syncthreads();
+    if (gi == 0 && n < L.N) {
+        float t = 0.0f;
+        for (int j = 0; j < G; ++j) t += red[j][tx];
+        db[(int64_t)s * L.N + n] = t;
+        db[(int64_t)(S + s) * L.N + n] = t * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n);
+    }
+}
+
+__global__ void bias_acc_grouped_kernel(const BiasGroup g, int S, const float* __restrict__ db_base,
+                                        float scale, float* __restrict__ acc_mu,
+                                        float* __restrict__ acc_rho) {
+    __shared__ float red[2][8][33];
+    int l = 0;
+    while (l + 1 < g.n && (int)blockIdx.x >= g.blk_base[l + 1]) ++l;
+    const SampledLayer& L = g.L[l];
+    const float* db = db_base + g.db_off[l];
+    const int tx = threadIdx.x & 31, gi = threadIdx.x >> 5;
+    const int n = (blockIdx.x - g.blk_base[l]) * 32 + tx;
+    float am = 0.0f, ar = 0.0f;
+    if (n < L.N)
+        for (int s = gi; s < S; s += 8) {
+            am += db[(int64_t)s * L.N + n];
+            ar += db[(int64_t)(S + s) * L.N + n];
+        }
+    red[0][gi][tx] = am;
+    red[1][gi][tx] = ar;
+    __syncthreads();
+    if (gi == 0 && n < L.N) {
+        float m = 0.0f, r = 0.0f;
+        for (int i = 0; i < 8; ++i) {
+            m += red[0][i][tx];
+            r += red[1][i][tx];
+        }
+        acc_mu[L.off_b + n] += scale * m;
+        acc_rho[L.off_b + n] += scale * r;
+    }
+}
+
+void launch_bias_grad_grouped(BiasGroup g, const SampleKeys& k, int S, float scale,
+                              float* db_scratch, float* acc_mu, float* acc_rho, cudaStream_t st) {
+    int blocks = 0, maxp = 1;
+    int64_t off = 0;
+    for (int l = 0; l < g.n; ++l) {
+        g.blk_base[l] = blocks;
+        g.db_off[l] = off;
+        blocks += (g.L[l].N + 31) / 32;
+        off += (int64_t)2 * S * g.L[l].N;
+        maxp = std::max(maxp, g.nparts[l]);
+    }
+    int G = 1;
+    while (G < kBiasGroups && G < maxp) G <<= 1;
+    bias_reduce_grouped_kernel<<<dim3(blocks, S), 32 * G, 0, st>>>(g, k, S, db_scratch);
+    bias_acc_grouped_kernel<<<blocks, 256, 0, st>>>(g, S, db_scratch, scale, acc_mu, acc_rho);
+}
+
 void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
                       int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
                       float* acc_mu, float* acc_rho, cudaStream_t st) {

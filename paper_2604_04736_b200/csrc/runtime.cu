@@ -114,9 +114,9 @@ int alloc_mlp(bnn_ctx* c) {
     }
     if (!c->alloc(&c->logits, (size_t)Sc * B * c->O) || !c->alloc(&c->lossrow, (size_t)Sc * B))
         return c->set_err(BNN_ERR_CUDA, "out of memory (logits)");
-    int maxN = 0;
-    for (int l = 0; l < L; ++l) maxN = std::max(maxN, c->widths[l + 1]);
-    if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+    int sumN = 0;  // the grouped bias launch keeps every layer's [2][S][N_l] block
+    for (int l = 0; l < L; ++l) sumN += c->widths[l + 1];
+    if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * sumN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
     if (c->bf16) {
         if (!c->alloc(&c->dz_f32, (size_t)Sc * B * c->O)) return c->set_err(BNN_ERR_CUDA, "out of memory");
         c->dbpart.assign(L, nullptr);
@@ -285,16 +285,20 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             }
             c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, st); });
         }
-        for (int l = 0; l < L; ++l) {
-            SampledLayer sl = sampled(c, l, mu);
-            const bool last = l == L - 1;
-            const int nbc = (B + 15) / 16;
-            const float* parts = last ? c->dz_f32 : c->dbpart[l];
-            const int nparts = last ? B : nbc;
-            const int ldp = last ? c->O : sl.N;
+        for (int l0 = 0; l0 < L; l0 += kMaxBiasGroup) {
+            BiasGroup bg{};
+            for (int l = l0; l < std::min(L, l0 + kMaxBiasGroup); ++l) {
+                const bool last = l == L - 1;
+                const int nbc = (B + 15) / 16;
+                const int i = bg.n++;
+                bg.L[i] = sampled(c, l, mu);
+                bg.parts[i] = last ? c->dz_f32 : c->dbpart[l];
+                bg.nparts[i] = last ? B : nbc;
+                bg.ldp[i] = last ? c->O : bg.L[i].N;
+                bg.strideS[i] = (int64_t)bg.nparts[i] * bg.ldp[i];
+            }
             c->launch("bias", [&] {
-                launch_bias_grad(sl, kk, Sc, parts, nparts, ldp, (int64_t)nparts * ldp, scale,
-                                 c->db_scratch, acc_mu, acc_rho, st);
+                launch_bias_grad_grouped(bg, kk, Sc, scale, c->db_scratch, acc_mu, acc_rho, st);
             }, 2);
         }
     }
