@@ -112,6 +112,10 @@ struct bnn_ctx {
     float* mgather = nullptr;  // agg: allgather buffer [world × B_max × stat_w]
     cudaStream_t st = nullptr;
     bool own_stream = false;
+    // side stream for the small kernels that overlap the wgrad GEMM (loss reduction, bias
+    // gradients): forked from / joined into st with events; unused while profiling
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     ncclComm_t comm = nullptr;
     // workspace
     float* sigma = nullptr;

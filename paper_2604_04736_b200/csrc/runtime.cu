@@ -148,6 +148,20 @@ int alloc_mlp(bnn_ctx* c) {
 }
 
 // ------------------------------------------------------------------ one chunk of samples
+// Side-stream fork/join: work enqueued on the returned stream after fork() runs concurrently
+// with what follows on c->st until join(). While profiling, everything stays on c->st.
+cudaStream_t fork_side(bnn_ctx* c) {
+    if (c->prof || !c->side) return c->st;
+    cudaEventRecord(c->ev_fork, c->st);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    return c->side;
+}
+void join_side(bnn_ctx* c) {
+    if (c->prof || !c->side) return;
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(c->st, c->ev_join, 0);
+}
+
 // phase 0: forward, per-sample loss head, backward (Alg. 1 l.7-12 for the chunk)
 // phase 1: forward + the exact-aggregation statistic only
 // phase 2: (forward unless skip_fwd,) mean-prediction loss head from gstats, backward
@@ -240,6 +254,12 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                 launch_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, c->grad[L - 1],
                                  c->ld[L], true, c->lossrow, c->dz_f32, st);
             });
+        bool forked = false;
+        if (phase == kPhaseFull) {  // the loss reduction overlaps the backward
+            cudaStream_t ss = fork_side(c);
+            forked = true;
+            c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, ss); });
+        }
         for (int l = L - 1; l >= 1; --l) {
             TcGenArgs a{};
             a.L = sampled(c, l, mu);
@@ -260,6 +280,26 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.dbpart = c->dbpart[l - 1];
             a.dbpart_stride_s = (int64_t)((B + 15) / 16) * a.L.K;
             c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[l], a, Sc, st); });
+        }
+        for (int l0 = 0; l0 < L; l0 += kMaxBiasGroup) {
+            BiasGroup bg{};
+            for (int l = l0; l < std::min(L, l0 + kMaxBiasGroup); ++l) {
+                const bool last = l == L - 1;
+                const int nbc = (B + 15) / 16;
+                const int i = bg.n++;
+                bg.L[i] = sampled(c, l, mu);
+                bg.parts[i] = last ? c->dz_f32 : c->dbpart[l];
+                bg.nparts[i] = last ? B : nbc;
+                bg.ldp[i] = last ? c->O : bg.L[i].N;
+                bg.strideS[i] = (int64_t)bg.nparts[i] * bg.ldp[i];
+            }
+            // the bias gradients (dgrad's fp32 partials, the loss head's seed) overlap the
+            // wgrad GEMM, which leaves SMs free (128 tiles on 148 SMs)
+            cudaStream_t ss = fork_side(c);
+            forked = true;
+            c->launch("bias", [&] {
+                launch_bias_grad_grouped(bg, kk, Sc, scale, c->db_scratch, acc_mu, acc_rho, ss);
+            }, 2);
         }
         for (int l0 = 0; l0 < L; l0 += kMaxWgradLayers) {
             TcWgradMaps maps;
@@ -285,22 +325,8 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             }
             c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, st); });
         }
-        for (int l0 = 0; l0 < L; l0 += kMaxBiasGroup) {
-            BiasGroup bg{};
-            for (int l = l0; l < std::min(L, l0 + kMaxBiasGroup); ++l) {
-                const bool last = l == L - 1;
-                const int nbc = (B + 15) / 16;
-                const int i = bg.n++;
-                bg.L[i] = sampled(c, l, mu);
-                bg.parts[i] = last ? c->dz_f32 : c->dbpart[l];
-                bg.nparts[i] = last ? B : nbc;
-                bg.ldp[i] = last ? c->O : bg.L[i].N;
-                bg.strideS[i] = (int64_t)bg.nparts[i] * bg.ldp[i];
-            }
-            c->launch("bias", [&] {
-                launch_bias_grad_grouped(bg, kk, Sc, scale, c->db_scratch, acc_mu, acc_rho, st);
-            }, 2);
-        }
+        if (forked) join_side(c);
+        if (phase == kPhaseFull) return BNN_OK;  // loss reduced on the side stream
     }
     if (phase == kPhaseFull)
         c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
@@ -666,6 +692,10 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     if (prop.major != 10)
         return fail(c->set_err(BNN_ERR_CUDA, "device is sm_%d%d; libbnn is built for sm_100a only", prop.major, prop.minor));
     c->st = reinterpret_cast<cudaStream_t>(cfg->stream);  // NULL = legacy default stream
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return fail(c->set_err(BNN_ERR_CUDA, "stream/event creation failed"));
     // ---- workspace
     c->n_part = finalize_partials_count(c->P);
     if (!c->alloc(&c->sigma, c->P) || !c->alloc(&c->acc, c->acc_total) ||
@@ -1060,6 +1090,12 @@ void bnn_destroy(bnn_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     for (void* p : c->allocs) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream && c->st) cudaStreamDestroy(c->st);
     delete c;
 }
