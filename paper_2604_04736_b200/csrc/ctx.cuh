@@ -249,6 +249,21 @@ struct bnn_ctx {
     }
 };
 
+// Side-stream fork/join: work enqueued on the returned stream after fork_side() runs
+// concurrently with what follows on c->st until join_side(). While profiling, everything
+// stays on c->st (class timing needs a single stream).
+inline cudaStream_t fork_side(bnn_ctx* c) {
+    if (c->prof || !c->side) return c->st;
+    cudaEventRecord(c->ev_fork, c->st);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    return c->side;
+}
+inline void join_side(bnn_ctx* c) {
+    if (c->prof || !c->side) return;
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(c->st, c->ev_join, 0);
+}
+
 // ResNet entry points (runtime_resnet.cu)
 int alloc_resnet_bf16(bnn_ctx* c);
 int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,

@@ -148,20 +148,6 @@ int alloc_mlp(bnn_ctx* c) {
 }
 
 // ------------------------------------------------------------------ one chunk of samples
-// Side-stream fork/join: work enqueued on the returned stream after fork() runs concurrently
-// with what follows on c->st until join(). While profiling, everything stays on c->st.
-cudaStream_t fork_side(bnn_ctx* c) {
-    if (c->prof || !c->side) return c->st;
-    cudaEventRecord(c->ev_fork, c->st);
-    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-    return c->side;
-}
-void join_side(bnn_ctx* c) {
-    if (c->prof || !c->side) return;
-    cudaEventRecord(c->ev_join, c->side);
-    cudaStreamWaitEvent(c->st, c->ev_join, 0);
-}
-
 // phase 0: forward, per-sample loss head, backward (Alg. 1 l.7-12 for the chunk)
 // phase 1: forward + the exact-aggregation statistic only
 // phase 2: (forward unless skip_fwd,) mean-prediction loss head from gstats, backward

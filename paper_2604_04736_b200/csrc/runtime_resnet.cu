@@ -434,12 +434,17 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         w.nlayers = 1;
         w.lay[0].L = sl;
         w.lay[0].mtiles = (sl.N + 127) / 128;
-        w.lay[0].ktiles = (sl.K + 63) / 64;
+        w.lay[0].ktiles = (sl.K + 127) / 128;  // 128 × 128 tiles (kernels_tc.cu wg::)
         w.lay[0].tile_base = 0;
         w.lay[0].b_shared = 0;
-        c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, st); });
+        // weight-side work of every layer (wgrad, ε combine, bias) runs on the side stream,
+        // overlapping the data-gradient chain on st (fork after its inputs exist; in order on
+        // the side stream, so the shared wpart / db_scratch scratch is reused safely)
+        cudaStream_t ss = fork_side(c);
+        c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, ss); });
+        c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, ss); });
         c->launch("bias", [&] {
-            launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, st);
+            launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, ss);
         }, 2);
         TcGenArgs a{};
         a.L = sl;
@@ -485,10 +490,11 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         const RBuf& Sb = c->rbufs[op.src];
         const bnn_ctx::RBf& G = c->rbf[gb];
         const int64_t npix_out = (int64_t)B * Db.H * Db.W;
-        // bias gradient from the fused partials of dL/dz
+        // bias gradient from the fused partials of dL/dz (side stream, see the head)
+        cudaStream_t ss = fork_side(c);
         c->launch("bias", [&] {
             launch_bias_grad(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale, c->db_scratch,
-                             acc_mu, acc_rho, st);
+                             acc_mu, acc_rho, ss);
         }, 2);
         // weight gradient with the sample-accumulating ε epilogue
         if (Ld.cin % 64 == 0 || c->rbf[op.src].C_pad == 8) {
@@ -517,15 +523,15 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.n_tile = conv2_wgrad_ntile(Kt);
             w.kpx = w.tma_b ? c->wkpx[op.layer] : 64;
             if (w.kpx != c->wkpx[op.layer]) return c->set_err(BNN_ERR_CONFIG, "wgrad k-step / operand path mismatch");
-            c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, st); });
+            c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, ss); });
             if (w.C_pad < 64) {
                 c->launch("wcomb", [&] {
                     launch_wgrad_eps_combine_stem(sl, kk, Sc, w.nsplit, Ld.cout, taps, Ld.cin, Kt, c->wpart, scale,
-                                                  acc_mu, acc_rho, st);
+                                                  acc_mu, acc_rho, ss);
                 });
             } else {
                 c->launch("wcomb", [&] {
-                    launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Kt, c->wpart, scale, acc_mu, acc_rho, st);
+                    launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Kt, c->wpart, scale, acc_mu, acc_rho, ss);
                 });
             }
         } else {
@@ -534,10 +540,10 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             c->launch("wgrad", [&] {
                 launch_conv_wgrad_simt_bf16(sl, kk, Sc, cs, c->rbf[op.src].C_pad, G.grad, npix_out * Db.C,
                                             c->rbf[op.src].val, op.src == 0 ? in_stride : 0, scale, c->wpart,
-                                            nsp, st);
+                                            nsp, ss);
             });
             const int64_t n = (int64_t)Ld.cout * Ld.k * Ld.k * Ld.cin;
-            c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, nsp, n, Ld.off_w, acc_mu, acc_rho, st); });
+            c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, nsp, n, Ld.off_w, acc_mu, acc_rho, ss); });
         }
         // identity residual: dL/dy flows unchanged into the block input
         if (op.res >= 0 && !is_proj_output(c, op.res)) {
@@ -590,6 +596,6 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         }
         if (!final) pending[op.src] = c->rbf[op.src].grad;
     }
-    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    join_side(c);  // the next chunk's forward overwrites what the side stream reads
     return BNN_OK;
 }
