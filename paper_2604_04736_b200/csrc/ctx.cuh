@@ -166,7 +166,8 @@ struct bnn_ctx {
     std::vector<CUtensorMap> cmap_xw;                  // per layer: wgrad X windows (64 pixels)
     std::vector<CUtensorMap> cmap_a2f, cmap_a2d, cmap_w2, cmap_w64;  // conv2: 128-pixel A windows, W (n_tile rows)
     std::vector<char> tma_a2f, tma_a2d;
-    float* bias_scr = nullptr;                         // sampled conv biases [S][max CO]
+    float* bias_scr = nullptr;                         // sampled conv biases [layer][S][512]
+    std::vector<cudaEvent_t> wgen_ev;                  // per layer: W_s slot written (side stream)
     std::vector<char> tma_fwd, tma_dgrad, tma_wgrad;   // stride-1 layers use them
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
     // TMA descriptors (BF16)

@@ -1080,6 +1080,8 @@ void bnn_destroy(bnn_ctx* c) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);
     }
+    for (auto e : c->wgen_ev)
+        if (e) cudaEventDestroy(e);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream && c->st) cudaStreamDestroy(c->st);

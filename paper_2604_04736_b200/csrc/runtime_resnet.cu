@@ -127,7 +127,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
     }
     if (!c->alloc(&c->wscr, wmax) || !c->alloc(&c->wpart, std::max<size_t>(pmax, 1)) ||
-        !c->alloc(&c->bias_scr, (size_t)Sc * 512) ||
+        !c->alloc(&c->bias_scr, (size_t)Sc * 512 * c->layers.size()) ||  // one slot per layer
         !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)))
         return c->set_err(BNN_ERR_CUDA, "out of memory (scratch)");
     for (const ROp& op : c->rops) {
@@ -305,6 +305,11 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_a2d[op.layer] = 1;
         }
     }
+    // one event per layer: its W_s slot is written (the side stream generates ahead)
+    c->wgen_ev.assign(c->layers.size(), nullptr);
+    for (auto& e : c->wgen_ev)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return c->set_err(BNN_ERR_CUDA, "event creation failed");
     // head: pooled features [S][B][Cf] → logits, with the MLP kernels' descriptors
     const int Cf = c->rbufs[gbuf].C, ldO = (int)round_up(O, 8);
     c->map_fwdB.resize(1);
@@ -330,6 +335,21 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
                           c->gidx * B, c->rbf[0].val, st);
     });
     const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * Cp0 : 0;
+    // every conv layer's W_s slot and sampled biases, generated ahead on the side stream in
+    // layer order (they depend on σ only); the forward conv of layer l waits for its event
+    const bool ahead = !c->prof && c->side;
+    cudaStream_t ss = fork_side(c);
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op)) continue;
+        SampledLayer sl = sampled(c, op.layer, mu);
+        const LayerDesc& Ld = c->layers[op.layer];
+        const int Cp = c->rbf[op.src].C_pad;
+        c->launch("wgen", [&] {
+            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr + c->wscr_off[op.layer],
+                                c->bias_scr + (size_t)op.layer * Sc * 512, ss);
+        });
+        if (ahead) cudaEventRecord(c->wgen_ev[op.layer], ss);
+    }
     for (const ROp& op : c->rops) {
         if (op.type == 1) {
             const RBuf& S = c->rbufs[op.src];
@@ -362,10 +382,7 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         const RBuf& Sb = c->rbufs[op.src];
         const RBuf& Db = c->rbufs[op.dst];
         const int Cp = c->rbf[op.src].C_pad;
-        c->launch("wgen", [&] {
-            launch_gen_wscratch(sl, kk, Sc, Ld.cin, Cp, Ld.k * Ld.k, c->kpad[op.layer], c->wscr + c->wscr_off[op.layer],
-                                c->bias_scr, st);
-        });
+        if (ahead) cudaStreamWaitEvent(st, c->wgen_ev[op.layer], 0);
         Conv2Args a{};
         a.S = Sc;
         a.B = B;
@@ -386,7 +403,7 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         a.src_stride_s = op.src == 0 ? in_stride : (int64_t)B * Sb.H * Sb.W * Cp;
         a.out = c->rbf[op.dst].val;
         a.out_stride_s = (int64_t)B * Db.H * Db.W * Db.C;
-        a.bias = c->bias_scr;
+        a.bias = c->bias_scr + (size_t)op.layer * Sc * 512;
         a.res = op.res >= 0 ? c->rbf[op.res].val : nullptr;
         a.relu = op.relu;
         a.mbits_out = op.relu ? c->rbf[op.dst].mbits : nullptr;
