@@ -312,11 +312,11 @@ def run_ours(args, world, rank, local_rank):
         peaks, peak_src = _peaks()
         line = {"metric": METRIC, "value": value, "unit": "sample·images/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": plan["scaling"], "vs_baseline": None,
                 "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
                 "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
                            "global_batch": B, "samples": S, "samples_per_gpu": S_loc,
-                           "params": P, "parallelism": f"sample-sharded x{world}",
+                           "params": P, "parallelism": f"{plan['mode']}-sharded K{K}xG{G}",
                            "loss_aggregation": "loss of the mean prediction (exact, PAPER.md:272-281)"
                                                if args.agg == "mean" else "mean of per-sample losses (Alg. 1 l.9)",
                            "optimizer": "fused Adam (in the timed step)" if adam else
