@@ -6,7 +6,8 @@ import json
 import sys
 
 CLASSES = {
-    "mlp": {"fwd": ["gen_gemm_kernel<0>"], "dgrad": ["gen_gemm_kernel<1>"], "wgrad": ["wgrad_tc_kernel"]},
+    "mlp": {"fwd": ["gen_gemm_kernel<0, 2>", "gen_gemm_kernel<0, 4>"], "dgrad": ["gen_gemm_kernel<1, 2>"],
+            "wgrad": ["wgrad_tc_kernel"]},
     "cnn": {"fwd": ["conv2_kernel<0>", "conv3_kernel<0>"], "dgrad": ["conv2_kernel<1>", "conv3_kernel<1>"],
             "wgrad": ["conv2_wgrad_kernel", "wgrad_eps_combine_kernel"]},
 }
