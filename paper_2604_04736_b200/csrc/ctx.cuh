@@ -265,11 +265,18 @@ inline void join_side(bnn_ctx* c) {
     cudaStreamWaitEvent(c->st, c->ev_join, 0);
 }
 
+// Chunk phases (exact aggregation):
+//   kPhaseFull    forward, per-sample loss head, backward (Alg. 1 l.7-12 for the chunk)
+//   kPhaseStats   forward + the mean-prediction statistic only
+//   kPhaseMeanBwd (forward unless skip_fwd,) mean-prediction loss head from gstats, backward
+enum { kPhaseFull = 0, kPhaseStats = 1, kPhaseMeanBwd = 2 };
+
 // ResNet entry points (runtime_resnet.cu)
 int alloc_resnet_bf16(bnn_ctx* c);
 int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                       const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
-                      uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss);
+                      uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss,
+                      int phase = kPhaseFull, bool skip_fwd = false, const float* gstats = nullptr);
 void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, int B,
                          uint64_t seed, uint32_t step, uint32_t s0, bool aug);
 SampledLayer sampled(const bnn_ctx* c, int l, const float* mu);

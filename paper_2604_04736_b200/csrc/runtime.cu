@@ -148,10 +148,7 @@ int alloc_mlp(bnn_ctx* c) {
 }
 
 // ------------------------------------------------------------------ one chunk of samples
-// phase 0: forward, per-sample loss head, backward (Alg. 1 l.7-12 for the chunk)
-// phase 1: forward + the exact-aggregation statistic only
-// phase 2: (forward unless skip_fwd,) mean-prediction loss head from gstats, backward
-enum { kPhaseFull = 0, kPhaseStats = 1, kPhaseMeanBwd = 2 };
+// phases: kPhaseFull / kPhaseStats / kPhaseMeanBwd (ctx.cuh)
 int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
               const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
               uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss,
@@ -405,7 +402,8 @@ void resnet_forward(bnn_ctx* c, const float* mu, const SampleKeys& kk, int Sc, i
 
 int resnet_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, const float* yreg,
                  int B, int B_glob, int S_glob, int Sc, uint32_t s0, uint64_t seed, uint32_t step,
-                 float* acc_mu, float* acc_rho, float* acc_loss) {
+                 float* acc_mu, float* acc_rho, float* acc_loss, int phase = kPhaseFull,
+                 bool skip_fwd = false, const float* gstats = nullptr) {
     cudaStream_t st = c->st;
     SampleKeys kk{make_key(seed), step, s0};
     const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
@@ -414,18 +412,29 @@ int resnet_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycl
     const float* X0 = x;
     int64_t sX0 = 0;
     if (c->cfg.aug == BNN_AUG_PER_SAMPLE) {
-        c->launch("aug", [&] {
-            launch_augment(x, Sc, B, in.H, in.W, in.C, seed, step, s0, c->gidx * B, c->rbufs[0].val, st);
-        });
+        if (!skip_fwd)
+            c->launch("aug", [&] {
+                launch_augment(x, Sc, B, in.H, in.W, in.C, seed, step, s0, c->gidx * B, c->rbufs[0].val, st);
+            });
         X0 = c->rbufs[0].val;
         sX0 = per_sample(in, B);
     }
-    resnet_forward(c, mu, kk, Sc, B, X0, sX0);
+    if (!skip_fwd) resnet_forward(c, mu, kk, Sc, B, X0, sX0);
     RBuf& lg = c->rbufs[c->rlogits];
-    c->launch("loss", [&] {
-        launch_loss_head(lg.val, Sc, B, c->O, c->model.loss, ycls, yreg, lg.grad, c->O, false, c->lossrow,
-                         nullptr, st);
-    });
+    if (phase == kPhaseStats) {
+        c->launch("loss", [&] { launch_mean_stats(lg.val, Sc, B, c->O, c->model.loss, ycls, c->mstats, st); });
+        return BNN_OK;
+    }
+    if (phase == kPhaseMeanBwd)
+        c->launch("loss", [&] {
+            launch_mean_loss_head(lg.val, Sc, B, c->O, c->model.loss, ycls, yreg, gstats, S_glob, lg.grad, c->O,
+                                  false, nullptr, st);
+        });
+    else
+        c->launch("loss", [&] {
+            launch_loss_head(lg.val, Sc, B, c->O, c->model.loss, ycls, yreg, lg.grad, c->O, false, c->lossrow,
+                             nullptr, st);
+        });
     std::vector<char> written(c->rbufs.size(), 0);
     written[c->rlogits] = 1;
     auto val = [&](int i) -> const float* { return i == 0 ? X0 : c->rbufs[i].val; };
@@ -467,7 +476,8 @@ int resnet_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycl
             written[op.src] = 1;
         }
     }
-    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    if (phase == kPhaseFull)
+        c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
     return BNN_OK;
 }
 
@@ -482,6 +492,19 @@ int check_step_args(bnn_ctx* c, int B_loc, int B_glob, int S_glob) {
         return c->set_err(BNN_ERR_CONFIG, "S/K <= max_S_loc violated (%d > %d)", S_glob / c->K, c->S_loc_max);
     if (S_glob >= (1 << 20)) return c->set_err(BNN_ERR_CONFIG, "S < 2^20 (EPS-v1 counter) violated");
     return BNN_OK;
+}
+
+int any_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, const float* yreg, int B,
+              int B_glob, int S_glob, int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* am, float* ar,
+              float* al, int phase, bool skip_fwd, const float* gstats) {
+    if (c->model.kind == BNN_MODEL_MLP)
+        return mlp_chunk(c, mu, x, ycls, yreg, B, B_glob, S_glob, Sc, s0, seed, step, am, ar, al, phase, skip_fwd,
+                         gstats);
+    if (c->bf16)
+        return resnet_bf16_chunk(c, mu, x, ycls, yreg, B, B_glob, S_glob, Sc, s0, seed, step, am, ar, al, phase,
+                                 skip_fwd, gstats);
+    return resnet_chunk(c, mu, x, ycls, yreg, B, B_glob, S_glob, Sc, s0, seed, step, am, ar, al, phase, skip_fwd,
+                        gstats);
 }
 
 // local partial sums into acc (zeroed first).
@@ -517,8 +540,8 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
             for (int s = 0; s < S_loc; s += c->chunk) {
                 const int Sc = std::min(c->chunk, S_loc - s);
                 const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
-                rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr,
-                               accl, kPhaseStats);
+                rc = any_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr,
+                               accl, kPhaseStats, false, nullptr);
                 if (rc) return rc;
             }
             if (stats_out) {
@@ -543,7 +566,7 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
         for (int s = 0; s < S_loc; s += c->chunk) {
             const int Sc = std::min(c->chunk, S_loc - s);
             const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
-            rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl,
+            rc = any_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl,
                            kPhaseMeanBwd, single && !gstats_in, gstats);
             if (rc) return rc;
         }
@@ -652,8 +675,6 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown loss"));
     if (model->loss >= BNN_LOSS_CE_MEAN) {
         // exact aggregation: the base loss family, plus the mean-statistic exchange
-        if (model->kind != BNN_MODEL_MLP)
-            return fail(c->set_err(BNN_ERR_CONFIG, "mean-prediction losses are implemented for MLP models"));
         c->agg = 1;
         c->model.loss = model->loss == BNN_LOSS_CE_MEAN ? BNN_LOSS_CE : BNN_LOSS_MSE;
     }

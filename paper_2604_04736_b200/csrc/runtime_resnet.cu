@@ -418,20 +418,31 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
 
 int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                       const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
-                      uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+                      uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss,
+                      int phase, bool skip_fwd, const float* gstats) {
     cudaStream_t st = c->st;
     SampleKeys kk{make_key(seed), step, s0};
     const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
                                                      : 1.0f / ((float)S_glob * B_glob * c->O);
     const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
-    resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug);
+    if (!skip_fwd) resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug);
     const RBuf& in = c->rbufs[0];
     const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * c->rbf[0].C_pad : 0;
     const int O = c->O, ldO = (int)round_up(O, 8);
-    c->launch("loss", [&] {
-        launch_loss_head(c->logits, Sc, B, O, c->model.loss, ycls, yreg, c->fcG, ldO, true, c->lossrow,
-                         c->dz_f32, st);
-    });
+    if (phase == kPhaseStats) {
+        c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, O, c->model.loss, ycls, c->mstats, st); });
+        return BNN_OK;
+    }
+    if (phase == kPhaseMeanBwd)
+        c->launch("loss", [&] {
+            launch_mean_loss_head(c->logits, Sc, B, O, c->model.loss, ycls, yreg, gstats, S_glob, c->fcG, ldO, true,
+                                  c->dz_f32, st);
+        });
+    else
+        c->launch("loss", [&] {
+            launch_loss_head(c->logits, Sc, B, O, c->model.loss, ycls, yreg, c->fcG, ldO, true, c->lossrow,
+                             c->dz_f32, st);
+        });
     // ---------------- head (linear layer on pooled features)
     const ROp& fc = c->rops.back();
     const ROp& gap = c->rops[c->rops.size() - 2];
@@ -458,7 +469,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         // overlapping the data-gradient chain on st (fork after its inputs exist; in order on
         // the side stream, so the shared wpart / db_scratch scratch is reused safely)
         cudaStream_t ss = fork_side(c);
-        c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, ss); });
+        if (phase == kPhaseFull)
+            c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, ss); });
         c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, ss); });
         c->launch("bias", [&] {
             launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, ss);

@@ -386,3 +386,19 @@ def test_bias_variance_gap_mse():
     b = O.elbo_step(model, mu, rho, x, None, yr, S, 5, 1, 1e9, agg="mean")
     _, var = O.predict(model, mu, rho, x, S, 5, 1)
     assert a["L_data"] - b["L_data"] == pytest.approx(float(var.mean()), rel=1e-10)
+
+
+def test_mean_aggregation_cnn_against_torch_autograd():
+    """Exact aggregation on a tiny ResNet-18-shaped net with augmentation: oracle vs the
+    independent torch formulation (mean softmax probability, F.nll_loss, autograd)."""
+    model = dict(kind="resnet18", in_h=8, in_w=8, in_c=3, n_classes=10, base_width=4, loss="ce")
+    # init σ: with σ up to 0.69 this BatchNorm-free net saturates the softmax and the true-class
+    # mean probability underflows to 0 (an infinite loss, reading R21)
+    mu, rho = synth.init_params(model, seed=8, rho_mode="init")
+    x, yc, _ = synth.make_batch(model, 3, seed=9)
+    o = O.elbo_step(model, mu, rho, x, yc, None, 2, 0xABC, 2, 777.0, aug=O.AUG_PER_SAMPLE, agg="mean")
+    assert np.isfinite(o["loss"])
+    t = torch_ref.elbo(model, mu, rho, x, yc, None, 2, 0xABC, 2, 777.0, aug=True, agg="mean")
+    assert o["loss"] == pytest.approx(t["loss"], rel=1e-12)
+    _cmp(o["grad_mu"], t["grad_mu"], 1e-10)
+    _cmp(o["grad_rho"], t["grad_rho"], 1e-10)

@@ -104,7 +104,9 @@ def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu
         Z = torch.stack(zs)
         if model["loss"] == "ce":
             pbar = torch.softmax(Z, dim=-1).mean(0)
-            L_data = F.nll_loss(torch.log(pbar), torch.tensor(np.asarray(y_cls, np.int64)))
+            yt = torch.tensor(np.asarray(y_cls, np.int64))
+            # log of the true-class column only (another class's P̄ may underflow to 0)
+            L_data = -torch.log(pbar.gather(1, yt[:, None])).mean()
         else:
             L_data = F.mse_loss(Z.mean(0), torch.tensor(np.asarray(y_reg, np.float64)))
     kl = 0.5 * torch.sum(sigma ** 2 + mu_t ** 2 - 1.0 - torch.log(sigma ** 2))
