@@ -318,14 +318,15 @@ void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStre
 
 // ============================================================================ K5
 namespace wg {
-// CTA = 128 n × 128 k weight tile, all S samples; one CTA per SM (TMEM: 2 × 128 columns of
-// per-sample dW_s + 128 columns of Σ_s dW_s). N = 128 MMAs: a tcgen05.mma costs ≈ 130 cycles
-// for any N ≤ 256 (profiles/r01/final/mma_bench.txt), so N = 64 tiles made this kernel
-// MMA-issue-bound; at N = 128 the two MMAs per K = 16 step hide under the ε regeneration.
+// CTA = 128 n × 112 k weight tile, all S samples; one CTA per SM (TMEM: 2 × 112 columns of
+// per-sample dW_s + 112 columns of Σ_s dW_s). 112 = 784 / 7: the C2 layers give 128 full
+// tiles + 18 narrow ones = 146 CTAs, one wave on 148 SMs (128-wide tiles left 20 SMs idle;
+// 96-wide ones need a second wave). N = 112 MMAs: a tcgen05.mma costs ≈ 130 cycles for any
+// N ≤ 256 (profiles/r01/final/mma_bench.txt); two per K = 16 step hide under the ε work.
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
 constexpr int kStages = 4;
-constexpr int kTileK = 128;
+constexpr int kTileK = kWgradTileK;
 constexpr int kAStage = 64 * 128 * 2;  // G_sᵀ: 64 b × 128 n (two 64-wide MN blocks)
 constexpr int kBStage = 64 * 128 * 2;  // X_s : 64 b × 128 k (two 64-wide MN blocks)
 constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + 256;
@@ -434,18 +435,21 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
         // ------------------------------------------------ epilogue: ε regeneration + accumulation
         const int q = warp & 3, h = warp >> 2;
         const int n = n0 + 32 * q + lane;
-        const int k = k0 + 32 * h;
-        const bool kfull = k + 32 <= L.K;
-        float ar[32];
+        constexpr int kCW = kTileK / 4;  // columns per epilogue warp (28: four warps per lane quadrant)
+        static_assert(kCW == 28, "tmem_ld28 below");
+        const int k = k0 + kCW * h;
+        const int kend = min(k0 + kTileK, L.K);  // this tile's column range ends here
+        const bool kfull = k + kCW <= kend;
+        float ar[kCW];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) ar[j] = 0.0f;
+        for (int j = 0; j < kCW; ++j) ar[j] = 0.0f;
         for (int s = 0; s < S; ++s) {
             const int buf = s & 1;
             mbar_wait(&tfull[buf], (s >> 1) & 1);
             tc_fence_after();
-            float d[32];
+            float d[kCW];
             __syncwarp();
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kTileK + 32 * h, d);
+            tmem_ld28(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * kTileK + kCW * h, d);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -453,7 +457,7 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
                 const uint32_t sgw = ((L.t_w << 20) | (a.kk.s0 + s));
                 if (kfull) {
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) {
+                    for (int g = 0; g < kCW / 4; ++g) {
                         const uint4 y = philox10(make_uint4((uint32_t)((k >> 2) + g), (uint32_t)n, sgw,
                                                             a.kk.step), a.kk.key);
                         const float R0 = bm_radius(y.x);
@@ -467,8 +471,8 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
                     }
                 } else {
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) {
-                        if (k + 4 * g < L.K) {
+                    for (int g = 0; g < kCW / 4; ++g) {
+                        if (k + 4 * g < kend) {
                             const float4 e = eps4(a.kk.key, a.kk.step, a.kk.s0 + s, L.t_w, (uint32_t)n,
                                                   (uint32_t)((k >> 2) + g));
                             float dd[4] = {d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]};
@@ -481,12 +485,12 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
             }
         }
         // acc_μ from TMEM (complete once the last sample's commit has landed)
-        float am[32];
+        float am[kCW];
         __syncwarp();
-        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + 2 * kTileK + 32 * h, am);
+        tmem_ld28(tmem + (static_cast<uint32_t>(32 * q) << 16) + 2 * kTileK + kCW * h, am);
         if (S == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) am[j] = 0.0f;
+            for (int j = 0; j < kCW; ++j) am[j] = 0.0f;
         }
         if (n < L.N) {
             const int64_t base = L.off_w + (int64_t)n * L.K + k;
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
             const bool v4 = ((base & 3) == 0) && kfull;
             if (v4) {
 #pragma unroll
-                for (int g = 0; g < 8; ++g) {
+                for (int g = 0; g < kCW / 4; ++g) {
                     float4 x = reinterpret_cast<float4*>(pm)[g];
                     float4 y = reinterpret_cast<float4*>(pr)[g];
                     x.x += a.scale * am[4 * g + 0]; x.y += a.scale * am[4 * g + 1];
@@ -507,8 +511,8 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (k + j < L.K) {
+                for (int j = 0; j < kCW; ++j) {
+                    if (k + j < kend) {
                         pm[j] += a.scale * am[j];
                         pr[j] += a.scale * ar[j];
                     }

@@ -32,8 +32,9 @@ struct TcGenArgs {
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
 
-// K5: grouped over up to 4 layers; CTA = 128 n × 128 k tile, loops over all S samples.
+// K5: grouped over up to 4 layers; CTA = 128 n × kWgradTileK k tile, loops over all S samples.
 constexpr int kMaxWgradLayers = 4;
+constexpr int kWgradTileK = 112;  // multiple of 16 (MMA N), ≤ 128 (two 64-wide TMA blocks)
 struct WgradLayer {
     SampledLayer L;
     int mtiles, ktiles, tile_base;

@@ -298,7 +298,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                 WgradLayer& wl = w.lay[w.nlayers];
                 wl.L = sampled(c, l, mu);
                 wl.mtiles = (wl.L.N + 127) / 128;
-                wl.ktiles = (wl.L.K + 127) / 128;  // 128 × 128 tiles (kernels_tc.cu wg::)
+                wl.ktiles = (wl.L.K + kWgradTileK - 1) / kWgradTileK;
                 wl.tile_base = base;
                 wl.b_shared = l == 0 ? 1 : 0;
                 base += wl.mtiles * wl.ktiles;

@@ -462,7 +462,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         w.nlayers = 1;
         w.lay[0].L = sl;
         w.lay[0].mtiles = (sl.N + 127) / 128;
-        w.lay[0].ktiles = (sl.K + 127) / 128;  // 128 × 128 tiles (kernels_tc.cu wg::)
+        w.lay[0].ktiles = (sl.K + kWgradTileK - 1) / kWgradTileK;
         w.lay[0].tile_base = 0;
         w.lay[0].b_shared = 0;
         // weight-side work of every layer (wgrad, ε combine, bias) runs on the side stream,
