@@ -116,6 +116,9 @@ struct bnn_ctx {
     // gradients): forked from / joined into st with events; unused while profiling
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // second side stream (CNN bias gradients, beside the wgrad / ε-combine stream)
+    cudaStream_t side2 = nullptr;
+    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     ncclComm_t comm = nullptr;
     // workspace
     float* sigma = nullptr;
@@ -263,6 +266,16 @@ inline void join_side(bnn_ctx* c) {
     if (c->prof || !c->side) return;
     cudaEventRecord(c->ev_join, c->side);
     cudaStreamWaitEvent(c->st, c->ev_join, 0);
+    if (c->side2) {
+        cudaEventRecord(c->ev_join2, c->side2);
+        cudaStreamWaitEvent(c->st, c->ev_join2, 0);
+    }
+}
+inline cudaStream_t fork_side2(bnn_ctx* c) {
+    if (c->prof || !c->side2) return c->st;
+    cudaEventRecord(c->ev_fork2, c->st);
+    cudaStreamWaitEvent(c->side2, c->ev_fork2, 0);
+    return c->side2;
 }
 
 // Chunk phases (exact aggregation):

@@ -701,7 +701,10 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     c->st = reinterpret_cast<cudaStream_t>(cfg->stream);  // NULL = legacy default stream
     if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess)
         return fail(c->set_err(BNN_ERR_CUDA, "stream/event creation failed"));
     // ---- workspace
     c->n_part = finalize_partials_count(c->P);
@@ -1097,10 +1100,13 @@ void bnn_destroy(bnn_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     for (void* p : c->allocs) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    if (c->side) {
-        cudaStreamSynchronize(c->side);
-        cudaStreamDestroy(c->side);
-    }
+    for (cudaStream_t q : {c->side, c->side2})
+        if (q) {
+            cudaStreamSynchronize(q);
+            cudaStreamDestroy(q);
+        }
+    for (cudaEvent_t e : {c->ev_fork2, c->ev_join2})
+        if (e) cudaEventDestroy(e);
     for (auto e : c->wgen_ev)
         if (e) cudaEventDestroy(e);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);

@@ -472,8 +472,9 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         if (phase == kPhaseFull)
             c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, ss); });
         c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, ss); });
+        cudaStream_t sb = fork_side2(c);  // every bias launch shares db_scratch: one stream
         c->launch("bias", [&] {
-            launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, ss);
+            launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, sb);
         }, 2);
         TcGenArgs a{};
         a.L = sl;
@@ -519,12 +520,14 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         const RBuf& Sb = c->rbufs[op.src];
         const bnn_ctx::RBf& G = c->rbf[gb];
         const int64_t npix_out = (int64_t)B * Db.H * Db.W;
-        // bias gradient from the fused partials of dL/dz (side stream, see the head)
-        cudaStream_t ss = fork_side(c);
+        // bias gradient from the fused partials of dL/dz (second side stream: the bias chain
+        // and the wgrad / ε-combine chain each overlap the data-gradient chain on st)
+        cudaStream_t sb = fork_side2(c);
         c->launch("bias", [&] {
             launch_bias_grad(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale, c->db_scratch,
-                             acc_mu, acc_rho, ss);
+                             acc_mu, acc_rho, sb);
         }, 2);
+        cudaStream_t ss = fork_side(c);
         // weight gradient with the sample-accumulating ε epilogue
         if (Ld.cin % 64 == 0 || c->rbf[op.src].C_pad == 8) {
             ConvWgradArgs w{};
