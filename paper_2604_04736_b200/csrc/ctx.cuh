@@ -161,7 +161,11 @@ struct bnn_ctx {
     std::vector<RBf> rbf;
     __nv_bfloat16* wscr = nullptr;  // W_s scratch of every conv layer for the sample chunk
     std::vector<size_t> wscr_off;   // per layer: element offset of its slot (forward writes, dgrad reads)
-    float* wpart = nullptr;         // conv wgrad split partials
+    float* wpart = nullptr;         // conv wgrad split partials (buffer 0)
+    float* wpart2 = nullptr;        // buffer 1: consecutive layers alternate, so the ε combine of
+                                    // one layer overlaps the wgrad GEMM of the next
+    cudaStream_t side3 = nullptr;   // ε-combine stream
+    cudaEvent_t ev_wg[2] = {nullptr, nullptr}, ev_comb[2] = {nullptr, nullptr}, ev_join3 = nullptr;
     std::vector<int> kpad, nsplit;  // per layer
     std::vector<int> wkpx;          // per layer: wgrad pixels per k-step (64 or 128)
     std::vector<CUtensorMap> cmap_w, cmap_wT, cmap_g;  // per layer
@@ -269,6 +273,10 @@ inline void join_side(bnn_ctx* c) {
     if (c->side2) {
         cudaEventRecord(c->ev_join2, c->side2);
         cudaStreamWaitEvent(c->st, c->ev_join2, 0);
+    }
+    if (c->side3) {
+        cudaEventRecord(c->ev_join3, c->side3);
+        cudaStreamWaitEvent(c->st, c->ev_join3, 0);
     }
 }
 inline cudaStream_t fork_side2(bnn_ctx* c) {

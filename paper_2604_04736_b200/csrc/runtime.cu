@@ -1100,12 +1100,13 @@ void bnn_destroy(bnn_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     for (void* p : c->allocs) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    for (cudaStream_t q : {c->side, c->side2})
+    for (cudaStream_t q : {c->side, c->side2, c->side3})
         if (q) {
             cudaStreamSynchronize(q);
             cudaStreamDestroy(q);
         }
-    for (cudaEvent_t e : {c->ev_fork2, c->ev_join2})
+    for (cudaEvent_t e : {c->ev_fork2, c->ev_join2, c->ev_join3, c->ev_wg[0], c->ev_wg[1], c->ev_comb[0],
+                          c->ev_comb[1]})
         if (e) cudaEventDestroy(e);
     for (auto e : c->wgen_ev)
         if (e) cudaEventDestroy(e);

@@ -127,6 +127,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
     }
     if (!c->alloc(&c->wscr, wmax) || !c->alloc(&c->wpart, std::max<size_t>(pmax, 1)) ||
+        !c->alloc(&c->wpart2, std::max<size_t>(pmax, 1)) ||
         !c->alloc(&c->bias_scr, (size_t)Sc * 512 * c->layers.size()) ||  // one slot per layer
         !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)))
         return c->set_err(BNN_ERR_CUDA, "out of memory (scratch)");
@@ -305,6 +306,13 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_a2d[op.layer] = 1;
         }
     }
+    if (cudaStreamCreateWithFlags(&c->side3, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join3, cudaEventDisableTiming) != cudaSuccess)
+        return c->set_err(BNN_ERR_CUDA, "stream creation failed");
+    for (int i = 0; i < 2; ++i)
+        if (cudaEventCreateWithFlags(&c->ev_wg[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_comb[i], cudaEventDisableTiming) != cudaSuccess)
+            return c->set_err(BNN_ERR_CUDA, "event creation failed");
     // one event per layer: its W_s slot is written (the side stream generates ahead)
     c->wgen_ev.assign(c->layers.size(), nullptr);
     for (auto& e : c->wgen_ev)
@@ -510,6 +518,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         if (op.src != 0) remaining[op.src]++;
         if (op.res >= 0 && !is_proj_output(c, op.res)) remaining[op.res]++;
     }
+    int wbuf = 0;  // wpart buffer of the next conv wgrad (alternates per layer)
+    const bool split3 = !c->prof && c->side3;
     for (int oi = (int)c->rops.size() - 1; oi >= 0; --oi) {
         const ROp& op = c->rops[oi];
         if (op.type != 0 || is_fc(c, op)) continue;
@@ -548,34 +558,49 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             w.X = c->rbf[op.src].val;
             w.X_stride_s = op.src == 0 ? in_stride : (int64_t)B * Sb.H * Sb.W * Sb.C;
             w.scale = scale;
-            w.part = c->wpart;
+            float* wp = wbuf ? c->wpart2 : c->wpart;
+            w.part = wp;
             w.nsplit = c->nsplit[op.layer];
             w.tma_b = c->tma_wgrad[op.layer];
             const int taps = Ld.k * Ld.k, Kt = conv2_wgrad_cols(taps, Ld.cin, w.C_pad);
             w.n_tile = conv2_wgrad_ntile(Kt);
             w.kpx = w.tma_b ? c->wkpx[op.layer] : 64;
             if (w.kpx != c->wkpx[op.layer]) return c->set_err(BNN_ERR_CONFIG, "wgrad k-step / operand path mismatch");
+            // the buffer is free once the ε combine that last read it (two layers back) is done
+            if (split3) cudaStreamWaitEvent(ss, c->ev_comb[wbuf], 0);
             c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, ss); });
+            cudaStream_t sc = ss;
+            if (split3) {  // ε combine on the third stream, overlapping the next layer's wgrad GEMM
+                cudaEventRecord(c->ev_wg[wbuf], ss);
+                cudaStreamWaitEvent(c->side3, c->ev_wg[wbuf], 0);
+                sc = c->side3;
+            }
             if (w.C_pad < 64) {
                 c->launch("wcomb", [&] {
-                    launch_wgrad_eps_combine_stem(sl, kk, Sc, w.nsplit, Ld.cout, taps, Ld.cin, Kt, c->wpart, scale,
-                                                  acc_mu, acc_rho, ss);
+                    launch_wgrad_eps_combine_stem(sl, kk, Sc, w.nsplit, Ld.cout, taps, Ld.cin, Kt, wp, scale,
+                                                  acc_mu, acc_rho, sc);
                 });
             } else {
                 c->launch("wcomb", [&] {
-                    launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Kt, c->wpart, scale, acc_mu, acc_rho, ss);
+                    launch_wgrad_eps_combine(sl, kk, Sc, w.nsplit, Ld.cout, Kt, wp, scale, acc_mu, acc_rho, sc);
                 });
             }
+            if (split3) cudaEventRecord(c->ev_comb[wbuf], sc);
+            wbuf ^= 1;
         } else {
             ConvShape cs{B, Sb.H, Sb.W, Sb.C, Db.H, Db.W, Db.C, Ld.k, Ld.stride, Ld.pad};
             const int nsp = c->nsplit[op.layer];
+            float* wp = wbuf ? c->wpart2 : c->wpart;
+            if (split3) cudaStreamWaitEvent(ss, c->ev_comb[wbuf], 0);
             c->launch("wgrad", [&] {
                 launch_conv_wgrad_simt_bf16(sl, kk, Sc, cs, c->rbf[op.src].C_pad, G.grad, npix_out * Db.C,
-                                            c->rbf[op.src].val, op.src == 0 ? in_stride : 0, scale, c->wpart,
+                                            c->rbf[op.src].val, op.src == 0 ? in_stride : 0, scale, wp,
                                             nsp, ss);
             });
             const int64_t n = (int64_t)Ld.cout * Ld.k * Ld.k * Ld.cin;
-            c->launch("wgrad", [&] { launch_wgrad_split_reduce(c->wpart, nsp, n, Ld.off_w, acc_mu, acc_rho, ss); });
+            c->launch("wgrad", [&] { launch_wgrad_split_reduce(wp, nsp, n, Ld.off_w, acc_mu, acc_rho, ss); });
+            if (split3) cudaEventRecord(c->ev_comb[wbuf], ss);
+            wbuf ^= 1;
         }
         // identity residual: dL/dy flows unchanged into the block input
         if (op.res >= 0 && !is_proj_output(c, op.res)) {
