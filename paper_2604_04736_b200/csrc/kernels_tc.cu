@@ -226,22 +226,36 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
             if (lane == 0) mbar_arrive(&full_gen[st]);
         }
         // ------------------------------------------------ epilogue
-        mbar_wait_suspend(tfull, 0);
-        tc_fence_after();
         const int q = warp & 3, h = warp >> 2;
         const int row = 32 * q + lane, m = m0 + row;
         const int nchunks = (a.nb + 15) / 16;
+        constexpr int kCStep = kGenWarps / 4;
+        // dgrad: the ReLU-mask rows of a chunk are loaded one chunk ahead (the first before the
+        // accumulator wait), so their latency overlaps the MMA and the previous chunk
+        uint16_t mnext[16];
+        auto load_mask = [&](int c) {
+            const int bc0 = b0 + c * 16;
+            const int nvalid = min(16, a.B - bc0);
+            if (MODE == 1 && a.mask && m < a.M && nvalid > 0 && c < nchunks) {
+                const uint16_t* mk = reinterpret_cast<const uint16_t*>(a.mask) + s * a.mask_stride_s +
+                                     (int64_t)bc0 * a.ldm + m;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) mnext[j] = j < nvalid ? __ldg(mk + (int64_t)j * a.ldm) : 0;
+            }
+        };
+        if (MODE == 1) load_mask(h);
+        mbar_wait_suspend(tfull, 0);
+        tc_fence_after();
         const float bias = MODE == 0 ? sbias[row] : 0.0f;
-        for (int c = h; c < nchunks; c += kGenWarps / 4) {
+        for (int c = h; c < nchunks; c += kCStep) {
             const int bc0 = b0 + c * 16;
             const int nvalid = min(16, a.B - bc0);
             const bool live = m < a.M && nvalid > 0;
             uint16_t mraw[16];
-            if (MODE == 1 && live && a.mask) {
-                const uint16_t* mk = reinterpret_cast<const uint16_t*>(a.mask) + s * a.mask_stride_s +
-                                     (int64_t)bc0 * a.ldm + m;
+            if (MODE == 1) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) mraw[j] = j < nvalid ? __ldg(mk + (int64_t)j * a.ldm) : 0;
+                for (int j = 0; j < 16; ++j) mraw[j] = mnext[j];
+                load_mask(c + kCStep);
             }
             float v[16];
             __syncwarp();
