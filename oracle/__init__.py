@@ -62,6 +62,10 @@ def lib():
                                                                             C.c_int, C.c_void_p, C.c_int]
         _lib.orc_elbo_step_mean.argtypes = [C.c_void_p] * 6 + [C.c_int] * 2 + [
             C.c_uint64, C.c_uint32, C.c_int, C.c_double] + [C.c_void_p] * 4 + [C.c_int]
+        _lib.orc_mean_stats.argtypes = [C.c_void_p] * 5 + [C.c_int] * 4 + [C.c_uint64, C.c_uint32,
+                                                                           C.c_int, C.c_void_p]
+        _lib.orc_elbo_partial_mean.argtypes = [C.c_void_p] * 6 + [C.c_int] * 6 + [
+            C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int]
         _lib.orc_adam.argtypes = [C.c_long] + [C.c_void_p] * 4 + [C.c_double] * 4 + [C.c_int]
         _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
                                                                          C.c_void_p, C.c_void_p]
@@ -137,6 +141,37 @@ def aug_params(seed, step, s, b):
     dx, dy, fl = C.c_int(), C.c_int(), C.c_int()
     lib().orc_aug_params(seed, step, s, b, C.byref(dx), C.byref(dy), C.byref(fl))
     return dx.value, dy.value, fl.value
+
+
+# ---------------------------------------------------------------- exact aggregation, sharded
+def mean_stats(model, mu, rho, x, y_cls, b_offset, s0, s1, seed, step, aug=AUG_NONE):
+    """This shard's statistic of the mean prediction (orc_mean_stats): [B_loc, 1] (CE) or
+    [B_loc, outputs] (MSE)."""
+    m = model_struct(model)
+    mu, rho, x = _d(mu), _d(rho), _d(x)
+    yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
+    B = x.shape[0]
+    O = model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]
+    w = 1 if model["loss"] == "ce" else O
+    out = np.zeros((B, w))
+    assert lib().orc_mean_stats(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), B, b_offset, s0, s1, seed,
+                                step, aug, _p(out)) == 0
+    return out
+
+
+def elbo_partial_mean(model, mu, rho, x, y_cls, y_reg, B_glob, b_offset, S_glob, s0, s1, seed, step,
+                      gstats, add_loss, aug=AUG_NONE, nthreads=0):
+    """This shard's acc partial of the exact step given the merged statistic
+    (orc_elbo_partial_mean)."""
+    m = model_struct(model)
+    P = lib().orc_n_params(C.byref(m))
+    mu, rho, x, yr, g = _d(mu), _d(rho), _d(x), _d(y_reg), _d(gstats)
+    yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
+    acc = np.zeros(2 * P + 1)
+    assert lib().orc_elbo_partial_mean(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), x.shape[0],
+                                       b_offset, B_glob, S_glob, s0, s1, seed, step, aug, _p(g),
+                                       1 if add_loss else 0, _p(acc), nthreads) == 0
+    return acc
 
 
 # ---------------------------------------------------------------- Adam (SURVEY §8(f) f2)

@@ -814,9 +814,103 @@ int orc_elbo_step(const orc_model* m, const double* mu, const double* rho, const
  *   MSE: ∂L/∂z_{s,b,o} = (2/(S·B·O)) · (ȳ_{b,o} − y_{b,o})
  * then the same per-sample backward and sample accumulation as orc_elbo_partial.
  */
-int orc_forward_ex(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
-                   int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out, int emu);
+static int forward_off(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
+                       int b_offset, int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out,
+                       int emu);
 
+/* Shard statistic of the mean prediction for samples [s0,s1) and local examples [0,B_loc)
+ * (global index b_offset + b): stats[b] = Σ_s p_{s,b,y_b} (CE, p_s = softmax(z_s)) or
+ * stats[b·O + o] = Σ_s z_{s,b,o} (MSE). Summing the shards of all sample groups gives S·P̄_b or
+ * S·ȳ_{b,o} (the statistic exchanged between forward and backward). */
+int orc_mean_stats(const orc_model* m, const double* mu, const double* rho, const double* x,
+                   const int* ycls, int B_loc, int b_offset, int s0, int s1, uint64_t seed,
+                   uint32_t step, int aug, double* stats)
+{
+    ONet net;
+    if (build_net(m, &net)) return -1;
+    const int O = net.n_out, S = s1 - s0;
+    double* z = (double*)malloc(sizeof(double) * (size_t)(S > 0 ? S : 1) * B_loc * O);
+    if (!z) return -2;
+    int rc = forward_off(m, mu, rho, x, B_loc, b_offset, s0, s1, seed, step, aug, z, 0);
+    if (rc) return rc;
+    const int w = m->loss == ORC_CE ? 1 : O;
+    for (long i = 0; i < (long)B_loc * w; ++i) stats[i] = 0.0;
+    for (int s = 0; s < S; ++s)
+        for (int b = 0; b < B_loc; ++b) {
+            const double* zr = z + ((long)s * B_loc + b) * O;
+            if (m->loss == ORC_CE) {
+                double mx = zr[0];
+                for (int k = 1; k < O; ++k) if (zr[k] > mx) mx = zr[k];
+                double se = 0.0;
+                for (int k = 0; k < O; ++k) se += exp(zr[k] - mx);
+                stats[b] += exp(zr[ycls[b]] - mx) / se;
+            } else {
+                for (int k = 0; k < O; ++k) stats[(long)b * O + k] += zr[k];
+            }
+        }
+    free(z);
+    return 0;
+}
+
+/* Shard partial of the exact-aggregation step (the backward half): with the merged statistic
+ * gstats (Σ over ALL S_glob samples, layout of orc_mean_stats) the per-sample gradient seeds
+ *   CE:  ∂L/∂z_{s,b,k} = (1/(S·B)) · (p_{s,b,y}/P̄_b) · (p_{s,b,k} − [k = y_b]),  P̄_b = gstats[b]/S
+ *   MSE: ∂L/∂z_{s,b,o} = (2/(S·B·O)) · (ȳ_{b,o} − y_{b,o}),                     ȳ = gstats/S
+ * drive the per-sample backward of samples [s0,s1) into acc (as orc_elbo_partial); with
+ * add_loss the shard's examples add their data loss, (1/B)Σ_b −ln P̄_b or (1/(B·O))Σ(ȳ − y)²,
+ * to acc[2P] (one sample group adds it, so each example counts once). */
+int orc_elbo_partial_mean(const orc_model* m, const double* mu, const double* rho, const double* x,
+                          const int* ycls, const double* yreg, int B_loc, int b_offset, int B_glob,
+                          int S_glob, int s0, int s1, uint64_t seed, uint32_t step, int aug,
+                          const double* gstats, int add_loss, double* acc, int nthreads)
+{
+    long P = orc_n_params(m);
+    if (P < 0) return -1;
+    ONet net;
+    if (build_net(m, &net)) return -1;
+    const int O = net.n_out, S = s1 - s0;
+    double* z = (double*)malloc(sizeof(double) * (size_t)(S > 0 ? S : 1) * B_loc * O);
+    double* seeds = (double*)calloc((size_t)S_glob * B_loc * O, sizeof(double)); /* indexed by global s */
+    if (!z || !seeds) return -2;
+    int rc = forward_off(m, mu, rho, x, B_loc, b_offset, s0, s1, seed, step, aug, z, 0);
+    if (rc) return rc;
+    double L = 0.0;
+    for (int b = 0; b < B_loc; ++b) {
+        if (m->loss == ORC_CE) {
+            const int y = ycls[b];
+            const double pbar = gstats[b] / S_glob;
+            L += -log(pbar) / B_glob;
+            for (int s = s0; s < s1; ++s) {
+                const double* zr = z + ((long)(s - s0) * B_loc + b) * O;
+                double mx = zr[0];
+                for (int k = 1; k < O; ++k) if (zr[k] > mx) mx = zr[k];
+                double se = 0.0;
+                for (int k = 0; k < O; ++k) se += exp(zr[k] - mx);
+                const double py = exp(zr[y] - mx) / se;
+                double* sd = seeds + ((long)s * B_loc + b) * O;
+                for (int k = 0; k < O; ++k)
+                    sd[k] = (py / pbar) * (exp(zr[k] - mx) / se - (k == y ? 1.0 : 0.0)) /
+                            ((double)S_glob * B_glob);
+            }
+        } else {
+            for (int k = 0; k < O; ++k) {
+                const double ybar = gstats[(long)b * O + k] / S_glob;
+                const double d = ybar - yreg[(long)b * O + k];
+                L += d * d / ((double)B_glob * O);
+                for (int s = s0; s < s1; ++s)
+                    seeds[((long)s * B_loc + b) * O + k] = 2.0 * d / ((double)S_glob * B_glob * O);
+            }
+        }
+    }
+    rc = elbo_partial_core(m, mu, rho, x, ycls, yreg, B_loc, b_offset, B_glob, S_glob, s0, s1, seed, step,
+                           aug, acc, nthreads, 0, seeds);
+    if (add_loss) acc[2 * P] += L;
+    free(z);
+    free(seeds);
+    return rc;
+}
+
+/* The single-process exact step: the statistic of all S samples, then the backward. */
 int orc_elbo_step_mean(const orc_model* m, const double* mu, const double* rho, const double* x,
                        const int* ycls, const double* yreg, int B, int S, uint64_t seed,
                        uint32_t step, int aug, double D, double* out_loss, double* out_kl,
@@ -826,62 +920,31 @@ int orc_elbo_step_mean(const orc_model* m, const double* mu, const double* rho, 
     if (P < 0) return -1;
     ONet net;
     if (build_net(m, &net)) return -1;
-    const int O = net.n_out;
-    double* z = (double*)malloc(sizeof(double) * (size_t)S * B * O);
-    double* seeds = (double*)malloc(sizeof(double) * (size_t)S * B * O);
+    const int w = m->loss == ORC_CE ? 1 : net.n_out;
+    double* st = (double*)malloc(sizeof(double) * (size_t)B * w);
     double* acc = (double*)calloc((size_t)(2 * P + 1), sizeof(double));
-    if (!z || !seeds || !acc) return -2;
-    int rc = orc_forward_ex(m, mu, rho, x, B, 0, S, seed, step, aug, z, 0);
-    if (rc) return rc;
-    double L = 0.0;
-    if (m->loss == ORC_CE) {
-        double* p = (double*)malloc(sizeof(double) * (size_t)S * B * O);
-        if (!p) return -2;
-        for (long r = 0; r < (long)S * B; ++r) {   /* p_s = softmax(z_s) */
-            const double* zr = z + r * O;
-            double mx = zr[0];
-            for (int k = 1; k < O; ++k) if (zr[k] > mx) mx = zr[k];
-            double se = 0.0;
-            for (int k = 0; k < O; ++k) se += exp(zr[k] - mx);
-            for (int k = 0; k < O; ++k) p[r * O + k] = exp(zr[k] - mx) / se;
-        }
-        for (int b = 0; b < B; ++b) {
-            const int y = ycls[b];
-            double pbar = 0.0;
-            for (int s = 0; s < S; ++s) pbar += p[((long)s * B + b) * O + y];
-            pbar /= S;
-            L += -log(pbar) / B;
-            for (int s = 0; s < S; ++s) {
-                const double* ps = p + ((long)s * B + b) * O;
-                double* sd = seeds + ((long)s * B + b) * O;
-                for (int k = 0; k < O; ++k)
-                    sd[k] = (ps[y] / pbar) * (ps[k] - (k == y ? 1.0 : 0.0)) / ((double)S * B);
-            }
-        }
-        free(p);
-    } else {
-        for (int b = 0; b < B; ++b)
-            for (int k = 0; k < O; ++k) {
-                double ybar = 0.0;
-                for (int s = 0; s < S; ++s) ybar += z[((long)s * B + b) * O + k];
-                ybar /= S;
-                const double d = ybar - yreg[(long)b * O + k];
-                L += d * d / ((double)B * O);
-                for (int s = 0; s < S; ++s)
-                    seeds[((long)s * B + b) * O + k] = 2.0 * d / ((double)S * B * O);
-            }
-    }
-    rc = elbo_partial_core(m, mu, rho, x, ycls, yreg, B, 0, B, S, 0, S, seed, step, aug, acc,
-                           nthreads, 0, seeds);
-    acc[2 * P] = L;
+    if (!st || !acc) return -2;
+    int rc = orc_mean_stats(m, mu, rho, x, ycls, B, 0, 0, S, seed, step, aug, st);
+    if (!rc)
+        rc = orc_elbo_partial_mean(m, mu, rho, x, ycls, yreg, B, 0, B, S, 0, S, seed, step, aug, st, 1, acc,
+                                   nthreads);
     if (!rc) rc = orc_finalize(m, mu, rho, acc, D, out_loss, out_kl, grad_mu, grad_rho);
-    free(z); free(seeds); free(acc);
+    free(st);
+    free(acc);
     return rc;
 }
 
 /* Per-sample network outputs z[s][b][O] for samples [s0,s1) (no augmentation unless asked). */
 int orc_forward_ex(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
                    int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out, int emu)
+{
+    return forward_off(m, mu, rho, x, B, 0, s0, s1, seed, step, aug, z_out, emu);
+}
+
+/* as orc_forward_ex for local examples whose global indices are b_offset + b (augmentation key) */
+static int forward_off(const orc_model* m, const double* mu, const double* rho, const double* x, int B,
+                       int b_offset, int s0, int s1, uint64_t seed, uint32_t step, int aug, double* z_out,
+                       int emu)
 {
     ONet net;
     if (build_net(m, &net)) return -1;
@@ -910,7 +973,7 @@ int orc_forward_ex(const orc_model* m, const double* mu, const double* rho, cons
             OWork* w = &works[tid];
             #pragma omp for schedule(static)
             for (int b = 0; b < B; ++b) {
-                load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w->val[0]);
+                load_input(n, x, b, b_offset + b, seed, step, (uint32_t)s, aug, w->val[0]);
                 int out = forward_one(n, W, w, emu);
                 memcpy(z_out + ((long)(s - s0) * B + b) * n->n_out, w->val[out],
                        sizeof(double) * n->n_out);

@@ -96,3 +96,61 @@ def test_gloo_world2_data_sharded():
 
 def test_gloo_world4_hybrid_with_augmentation():
     _run(4, "hybrid", K=2, G=2, model=CNN, S=4, B=4, aug=True)
+
+
+# ---------------------------------------------------------------- exact aggregation (f1), two collectives
+def _worker_mean(rank, world, port, mode, K, G, model, S, B, aug, out):
+    """the statistic of the mean prediction is exchanged between forward and
+    backward (allgather + rank-ordered sum over the sample groups of this rank's data group,
+    as bnn_elbo_step does over NCCL), then the gradient partials are SUM-allreduced."""
+    import oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    K, G = plan.grid(mode, world, K, G)
+    sh = plan.shard(rank, K, G, S, B)
+    k, g = rank // G, rank % G
+    mu, rho = synth.init_params(model, seed=3, rho_mode="init")
+    x, yc, yr = synth.make_batch(model, B, seed=4)
+    sl = slice(sh["b0"], sh["b1"])
+    a = O.AUG_PER_SAMPLE if aug else O.AUG_NONE
+    st = torch.from_numpy(O.mean_stats(model, mu, rho, x[sl], None if yc is None else yc[sl], sh["b0"],
+                                       sh["s0"], sh["s1"], 9, 2, a))
+    allst = [torch.zeros_like(st) for _ in range(world)]
+    dist.all_gather(allst, st)
+    gst = None
+    for r in range(g, world, G):
+        gst = allst[r].clone() if gst is None else gst + allst[r]
+    acc = O.elbo_partial_mean(model, mu, rho, x[sl], None if yc is None else yc[sl],
+                              None if yr is None else yr[sl], B, sh["b0"], S, sh["s0"], sh["s1"], 9, 2,
+                              gst.numpy(), add_loss=(k == 0), aug=a, nthreads=1)
+    t = torch.from_numpy(acc)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    r_ = O.finalize(model, mu, rho, t.numpy(), 500.0)
+    out[rank] = (r_["loss"], r_["grad_mu"], r_["grad_rho"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("model,world,mode,K,G,aug", [
+    (MODEL, 2, "sample", None, None, False),
+    (dict(kind="mlp", widths=[5, 7, 3], loss="mse"), 2, "sample", None, None, False),
+    (MODEL, 4, "hybrid", 2, 2, False),
+    (CNN, 2, "hybrid", 1, 2, True),
+])
+def test_gloo_mean_aggregation_equals_single_process(model, world, mode, K, G, aug):
+    import oracle as O
+    O.lib()
+    S, B = 8, 8
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_mean, args=(world, _free_port(), mode, K, G, model, S, B, aug, out), nprocs=world,
+             join=True)
+    mu, rho = synth.init_params(model, seed=3, rho_mode="init")
+    x, yc, yr = synth.make_batch(model, B, seed=4)
+    ref = O.elbo_step(model, mu, rho, x, yc, yr, S, 9, 2, 500.0,
+                      aug=O.AUG_PER_SAMPLE if aug else O.AUG_NONE, nthreads=1, agg="mean")
+    for r in range(world):
+        loss, gmu, grho = out[r]
+        assert loss == pytest.approx(ref["loss"], rel=1e-12)
+        np.testing.assert_allclose(gmu, ref["grad_mu"], rtol=1e-9, atol=1e-13)
+        np.testing.assert_allclose(grho, ref["grad_rho"], rtol=1e-9, atol=1e-13)
