@@ -670,3 +670,23 @@ def test_cnn_bf16_mean_aggregation(chunk):
     assert _rel(g2.cpu().numpy(), gmu) < 1e-5
     assert _rel(r2.cpu().numpy(), grho) < 1e-5
     assert abs(float(l2) - loss) <= 1e-5 * abs(loss)
+
+
+@pytest.mark.parametrize("loss", ["ce_mean", "mse_mean"])
+def test_mean_statistic_matches_oracle(loss):
+    """bnn_mean_stats (the statistic exchanged between forward and backward) against the
+    oracle's orc_mean_stats for rank 3 of a 2×2 grid: samples [3, 6), global examples 40..79,
+    FP32 path: ≤ 1e-5 relative."""
+    native = _native()
+    base = RAGGED if loss == "ce_mean" else RAGGED_MSE
+    model = dict(base, loss=loss)
+    B, S = 80, 6
+    mu, rho, x, yc, yr = _inputs(base, B, "init")
+    y = yc if loss == "ce_mean" else yr
+    ctx = native.Context(model, precision="fp32", mode="hybrid", K=2, G=2, rank=1 * 2 + 1, world=4,
+                         max_B_loc=40, max_S_loc=3, dataset_size=100.0)
+    xs, ys = x[40:80], y[40:80]
+    width = 1 if loss == "ce_mean" else base["widths"][-1]
+    g = ctx.mean_stats(_dev(mu), _dev(rho), _dev(xs), _dev(ys), B, S, 11, 3, width).cpu().numpy()
+    ref = O.mean_stats(_base(model), mu, rho, xs, None if yc is None else yc[40:80], 40, 3, 6, 11, 3)
+    assert _rel(g, ref.reshape(-1)) <= 1e-5
