@@ -213,6 +213,23 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                                                 (uint32_t)(k0 >> 2));
                     sts64(tileA + it * sstep, w);
                 }
+            } else if (MODE == 0 && vec && m_full && ((L.K - kb * 64) & 3) == 0) {
+                // forward, last k-block of a fan-in that is not a multiple of 64 (784 = 12·64 + 16):
+                // the valid quads are spread over all threads (the fixed mapping above would leave
+                // 3/4 of the lanes idle for a 16-column block), the rest of the tile is zeroed
+                const int nq = (L.K - kb * 64) >> 2;  // valid 4-column quads per row
+                const uint32_t tile0 = smem_u32(sA + st * kAStage);
+                for (int i = tid; i < 128 * nq; i += kGenWarps * 32) {
+                    const int r = i / nq, qq = i - r * nq;
+                    const int64_t e = L.off_w + (int64_t)(m0 + r) * L.K + kb * 64 + 4 * qq;
+                    const uint2 w = gen_w4_fast(L.mu + e, L.sigma + e, a.kk.key, a.kk.step, w3,
+                                                (uint32_t)(m0 + r), (uint32_t)((kb * 64 >> 2) + qq));
+                    sts64(tile0 + r * 128 + ((((qq >> 1) ^ (r & 7))) << 4) + ((qq & 1) << 3), w);
+                }
+                for (int i = tid; i < 128 * (16 - nq); i += kGenWarps * 32) {
+                    const int r = i / (16 - nq), qq = nq + (i - r * (16 - nq));
+                    sts64(tile0 + r * 128 + ((((qq >> 1) ^ (r & 7))) << 4) + ((qq & 1) << 3), make_uint2(0u, 0u));
+                }
             } else {
 #pragma unroll 1
                 for (int it = 0; it < kItems; ++it) {
