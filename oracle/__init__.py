@@ -17,7 +17,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 MLP, RESNET18 = 0, 1
-CE, MSE = 0, 1
+CE, MSE, GNLL = 0, 1, 2
 RELU, TANH = 0, 1
 AUG_NONE, AUG_PER_SAMPLE = 0, 1
 
@@ -84,7 +84,7 @@ def model_struct(model: dict, act: str = "relu") -> OrcModel:
         m.in_h, m.in_w, m.in_c = model["in_h"], model["in_w"], model["in_c"]
         m.n_classes = model["n_classes"]
         m.base_width = model.get("base_width", 64)
-    m.loss = CE if model["loss"] == "ce" else MSE
+    m.loss = {"ce": CE, "mse": MSE, "gnll": GNLL}[model["loss"]]
     m.act = RELU if act == "relu" else TANH
     return m
 
@@ -152,7 +152,7 @@ def mean_stats(model, mu, rho, x, y_cls, b_offset, s0, s1, seed, step, aug=AUG_N
     yc = None if y_cls is None else np.ascontiguousarray(y_cls, np.int32)
     B = x.shape[0]
     O = model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]
-    w = 1 if model["loss"] == "ce" else O
+    w = {"ce": 1, "mse": O, "gnll": 2 * O}[model["loss"]]
     out = np.zeros((B, w))
     assert lib().orc_mean_stats(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), B, b_offset, s0, s1, seed,
                                 step, aug, _p(out)) == 0
@@ -250,6 +250,7 @@ def elbo_step(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=AUG_NONE, n
         return dict(loss=loss.value, kl=kl.value, grad_mu=gmu, grad_rho=grho,
                     L_data=loss.value - kl.value / D)
     assert agg == "sample"
+    assert model["loss"] != "gnll", "the Gaussian NLL of the predictive distribution needs agg='mean'"
     acc = elbo_partial(model, mu, rho, x, y_cls, y_reg, B, 0, S, 0, S, seed, step, aug, nthreads,
                        act, emu)
     return finalize(model, mu, rho, acc, D, act)

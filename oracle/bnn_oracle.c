@@ -174,7 +174,10 @@ void orc_aug_params(uint64_t seed, uint32_t step, uint32_t s, uint32_t b, int* d
  * ====================================================================================== */
 
 enum { ORC_MLP = 0, ORC_RESNET18 = 1 };
-enum { ORC_CE = 0, ORC_MSE = 1 };
+enum { ORC_CE = 0, ORC_MSE = 1, ORC_GNLL = 2 /* mean-prediction aggregation only */ };
+/* variance floor of the Gaussian NLL of the predictive distribution (reading R24) */
+#define ORC_GNLL_EPS 1e-6
+#define ORC_TWO_PI 6.283185307179586476925286766559
 enum { ORC_RELU = 0, ORC_TANH = 1 };
 enum { ORC_AUG_NONE = 0, ORC_AUG_PER_SAMPLE = 1 };
 
@@ -185,7 +188,7 @@ typedef struct {
     int widths[16];  /* MLP: widths[0] = input features, widths[n-1] = outputs */
     int in_h, in_w, in_c, n_classes; /* ResNet-18 input image and classes */
     int base_width;  /* ResNet-18 stage-1 width (64 for the paper-shaped model) */
-    int loss;        /* ORC_CE | ORC_MSE */
+    int loss;        /* ORC_CE | ORC_MSE | ORC_GNLL */
     int act;         /* ORC_RELU (the model) | ORC_TANH (FD self-check variant only) */
 } orc_model;
 
@@ -833,7 +836,7 @@ int orc_mean_stats(const orc_model* m, const double* mu, const double* rho, cons
     if (!z) return -2;
     int rc = forward_off(m, mu, rho, x, B_loc, b_offset, s0, s1, seed, step, aug, z, 0);
     if (rc) return rc;
-    const int w = m->loss == ORC_CE ? 1 : O;
+    const int w = m->loss == ORC_CE ? 1 : m->loss == ORC_GNLL ? 2 * O : O;
     for (long i = 0; i < (long)B_loc * w; ++i) stats[i] = 0.0;
     for (int s = 0; s < S; ++s)
         for (int b = 0; b < B_loc; ++b) {
@@ -844,6 +847,11 @@ int orc_mean_stats(const orc_model* m, const double* mu, const double* rho, cons
                 double se = 0.0;
                 for (int k = 0; k < O; ++k) se += exp(zr[k] - mx);
                 stats[b] += exp(zr[ycls[b]] - mx) / se;
+            } else if (m->loss == ORC_GNLL) {  /* Σ ŷ and Σ ŷ² (fp64) */
+                for (int k = 0; k < O; ++k) {
+                    stats[(long)b * 2 * O + k] += zr[k];
+                    stats[(long)b * 2 * O + O + k] += zr[k] * zr[k];
+                }
             } else {
                 for (int k = 0; k < O; ++k) stats[(long)b * O + k] += zr[k];
             }
@@ -892,6 +900,22 @@ int orc_elbo_partial_mean(const orc_model* m, const double* mu, const double* rh
                     sd[k] = (py / pbar) * (exp(zr[k] - mx) / se - (k == y ? 1.0 : 0.0)) /
                             ((double)S_glob * B_glob);
             }
+        } else if (m->loss == ORC_GNLL) {
+            /* Gaussian NLL of the predictive distribution (P:349 with P:148):
+             *   m = (1/S)Σ ŷ_s,  v = (1/S)Σ (ŷ_s − m)² + ε_v,
+             *   L = (1/(B·O)) Σ [ ½ ln(2π v) + (y − m)²/(2v) ]
+             *   ∂L/∂ŷ_s = (1/(S·B·O)) [ (ŷ_s − m)/v − (y − m)/v − (y − m)²(ŷ_s − m)/v² ] */
+            for (int k = 0; k < O; ++k) {
+                const double mean = gstats[(long)b * 2 * O + k] / S_glob;
+                const double v = gstats[(long)b * 2 * O + O + k] / S_glob - mean * mean + ORC_GNLL_EPS;
+                const double d = yreg[(long)b * O + k] - mean;
+                L += (0.5 * log(ORC_TWO_PI * v) + d * d / (2.0 * v)) / ((double)B_glob * O);
+                for (int s = s0; s < s1; ++s) {
+                    const double e = z[((long)(s - s0) * B_loc + b) * O + k] - mean;
+                    seeds[((long)s * B_loc + b) * O + k] =
+                        (e / v - d / v - d * d * e / (v * v)) / ((double)S_glob * B_glob * O);
+                }
+            }
         } else {
             for (int k = 0; k < O; ++k) {
                 const double ybar = gstats[(long)b * O + k] / S_glob;
@@ -920,7 +944,7 @@ int orc_elbo_step_mean(const orc_model* m, const double* mu, const double* rho, 
     if (P < 0) return -1;
     ONet net;
     if (build_net(m, &net)) return -1;
-    const int w = m->loss == ORC_CE ? 1 : net.n_out;
+    const int w = m->loss == ORC_CE ? 1 : m->loss == ORC_GNLL ? 2 * net.n_out : net.n_out;
     double* st = (double*)malloc(sizeof(double) * (size_t)B * w);
     double* acc = (double*)calloc((size_t)(2 * P + 1), sizeof(double));
     if (!st || !acc) return -2;

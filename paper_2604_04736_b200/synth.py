@@ -53,7 +53,7 @@ def make_batch(model: dict, B: int, seed: int = 1):
     rng = np.random.default_rng(seed)
     shp = input_shape(model)
     O = n_outputs(model)
-    if model["kind"] == "mlp" and model["loss"] == "mse":
+    if model["kind"] == "mlp" and model["loss"] in ("mse", "gnll"):
         x = rng.normal(0.0, 1.0, (B,) + shp)
         # fixed teacher network: widths of the model, ReLU hidden layers
         w = model["widths"]

@@ -402,3 +402,28 @@ def test_mean_aggregation_cnn_against_torch_autograd():
     assert o["loss"] == pytest.approx(t["loss"], rel=1e-12)
     _cmp(o["grad_mu"], t["grad_mu"], 1e-10)
     _cmp(o["grad_rho"], t["grad_rho"], 1e-10)
+
+
+# ---------------------------------------------------------------- Gaussian NLL of the predictive (f1)
+def test_gnll_mean_aggregation_finite_differences():
+    """Gaussian NLL with the samples' predictive mean and variance:
+    whole gradient vs central FD (tanh MLP, σ wide so the predictive variance is not tiny)."""
+    model = dict(kind="mlp", widths=[6, 7, 3], loss="gnll")
+    mu, rho = synth.init_params(model, seed=5, rho_mode="wide")
+    x, _, yr = synth.make_batch(model, 9, seed=4)
+    P = n_params(model)
+    _fd_check(model, mu.astype(np.float64), rho.astype(np.float64), x, None, yr, 4, 500.0, "tanh",
+              range(P), range(P), agg="mean")
+
+
+@pytest.mark.parametrize("rho_mode", ["wide", "init"])
+def test_gnll_against_torch_autograd(rho_mode):
+    """Oracle vs an independent torch formulation (torch.var, autograd) on a ReLU MLP."""
+    model = dict(kind="mlp", widths=[12, 16, 9, 4], loss="gnll")
+    mu, rho = synth.init_params(model, seed=8, rho_mode=rho_mode)
+    x, _, yr = synth.make_batch(model, 7, seed=9)
+    o = O.elbo_step(model, mu, rho, x, None, yr, 5, 0xABC, 2, 777.0, agg="mean")
+    t = torch_ref.elbo(model, mu, rho, x, None, yr, 5, 0xABC, 2, 777.0, agg="mean")
+    assert o["loss"] == pytest.approx(t["loss"], rel=1e-10)
+    _cmp(o["grad_mu"], t["grad_mu"], 1e-8)
+    _cmp(o["grad_rho"], t["grad_rho"], 1e-8)

@@ -107,6 +107,13 @@ def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu
             yt = torch.tensor(np.asarray(y_cls, np.int64))
             # log of the true-class column only (another class's P̄ may underflow to 0)
             L_data = -torch.log(pbar.gather(1, yt[:, None])).mean()
+        elif model["loss"] == "gnll":
+            # Gaussian NLL of the predictive distribution: mean and population variance over
+            # samples, variance floor 1e-6 (reading R24); torch's own moments + autograd
+            yt = torch.tensor(np.asarray(y_reg, np.float64))
+            m = Z.mean(0)
+            v = Z.var(0, unbiased=False) + 1e-6
+            L_data = (0.5 * torch.log(2.0 * torch.pi * v) + (yt - m) ** 2 / (2.0 * v)).mean()
         else:
             L_data = F.mse_loss(Z.mean(0), torch.tensor(np.asarray(y_reg, np.float64)))
     kl = 0.5 * torch.sum(sigma ** 2 + mu_t ** 2 - 1.0 - torch.log(sigma ** 2))
