@@ -203,6 +203,9 @@ def run_ours(args, world, rank, local_rank):
     model = MODELS[cfg["model"]]
     if args.agg == "mean":  # exact aggregation: loss of the mean prediction
         model = dict(model, loss=model["loss"] + "_mean")
+    elif args.agg == "gnll":  # Gaussian NLL of the predictive (regression configs, FP32)
+        assert model["loss"] == "mse", "--agg gnll needs a regression config (C1)"
+        model = dict(model, loss="gnll_mean")
     plan = run_plan(args.config, world, args.mode)
     B, B_loc, S, S_loc, K, G = plan["B"], plan["B_loc"], plan["S"], plan["S_loc"], plan["K"], plan["G"]
     D = cfg["D"]
@@ -317,8 +320,9 @@ def run_ours(args, world, rank, local_rank):
                 "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
                            "global_batch": B, "samples": S, "samples_per_gpu": S_loc,
                            "params": P, "parallelism": f"{plan['mode']}-sharded K{K}xG{G}",
-                           "loss_aggregation": "loss of the mean prediction (exact, PAPER.md:272-281)"
-                                               if args.agg == "mean" else "mean of per-sample losses (Alg. 1 l.9)",
+                           "loss_aggregation": {"mean": "loss of the mean prediction (exact, PAPER.md:272-281)",
+                                                "gnll": "Gaussian NLL of the predictive mean/variance (P:349, P:281)",
+                                                "sample": "mean of per-sample losses (Alg. 1 l.9)"}[args.agg],
                            "optimizer": "fused Adam (in the timed step)" if adam else
                                         "none (step returns grad_mu, grad_rho; north_star boundary)",
                            "l2": "flushed between timed steps (256 MiB memset outside events)"},
@@ -444,8 +448,9 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=None,
                     help="seconds of oracle CPU work per reference step (default: 150 s / (K+W))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--agg", default="sample", choices=["sample", "mean"],
-                    help="mean: exact aggregation, the loss of the mean prediction (MLP configs)")
+    ap.add_argument("--agg", default="sample", choices=["sample", "mean", "gnll"],
+                    help="mean: exact aggregation, the loss of the mean prediction; gnll: Gaussian "
+                         "NLL of the predictive mean and variance (C1, --precision fp32)")
     ap.add_argument("--optimizer", default="none", choices=["none", "adam"],
                     help="adam: each step also applies the fused Adam update (bnn_elbo_step_adam)")
     args = ap.parse_args()

@@ -64,7 +64,14 @@ enum { BNN_MODEL_MLP = 0, BNN_MODEL_RESNET18 = 1 };
  * needs every sample group's statistic before any backward: bnn_elbo_step exchanges it with
  * one extra allgather between forward and backward; virtual ranks use bnn_mean_stats +
  * bnn_elbo_partial_mean. MLP models only (BNN_ERR_CONFIG otherwise). */
-enum { BNN_LOSS_CE = 0, BNN_LOSS_MSE = 1, BNN_LOSS_CE_MEAN = 2, BNN_LOSS_MSE_MEAN = 3 };
+/* BNN_LOSS_GNLL_MEAN: Gaussian NLL of the predictive distribution, the two-parameter case of
+ * P:281 ("Gaussian negative log-likelihood"; mean and population variance of the S
+ * predictions per output, variance floor 1e-6, R24): fp32 targets [B, outputs];
+ * statistic per rank = Welford (mean, M2) of its samples, merged by Chan's update. MLP models,
+ * precision FP32 only (BNN_ERR_CONFIG otherwise: bf16-rounded predictions perturb the sample
+ * variance the gradient divides by beyond the BF16 tolerance). */
+enum { BNN_LOSS_CE = 0, BNN_LOSS_MSE = 1, BNN_LOSS_CE_MEAN = 2, BNN_LOSS_MSE_MEAN = 3,
+       BNN_LOSS_GNLL_MEAN = 4 };
 enum { BNN_PREC_FP32 = 0, BNN_PREC_BF16 = 1 };
 enum { BNN_MODE_SAMPLE_SHARDED = 0, BNN_MODE_DATA_SHARDED = 1, BNN_MODE_HYBRID = 2 };
 enum { BNN_AUG_NONE = 0, BNN_AUG_PER_SAMPLE = 1 };
@@ -181,12 +188,18 @@ int bnn_finalize(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const 
 /* Exact aggregation, virtual-rank form (BNN_LOSS_*_MEAN only). bnn_mean_stats runs this
  * rank's sampled forward passes and writes its statistic: stats_dev[b·w + j] = Σ over the
  * rank's samples of p_{s,b,y_b} (CE, w = 1) or of ŷ_{s,b,j} (MSE, w = outputs), fp32, for its
- * B_loc examples. Summing the stats of the K sample groups of a data group (any order gives
- * the same value up to fp32 rounding) and passing the sum to bnn_elbo_partial_mean yields
- * this rank's acc partial of the exact step (the data loss is counted by sample group 0). */
+ * B_loc examples; GNLL: w = 2·outputs, [mean (outputs) | M2 (outputs)] of the rank's samples.
+ * Merging the stats of the K sample groups of a data group (bnn_mean_merge: the sum for CE /
+ * MSE, Chan's update for GNLL) and passing the result to bnn_elbo_partial_mean yields this
+ * rank's acc partial of the exact step (the data loss is counted by sample group 0). */
 int bnn_mean_stats(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev, const float* x_dev,
                    const int32_t* ycls_dev, int32_t B_loc, int32_t B_global, int32_t S_global,
                    uint64_t seed, uint32_t step, float* stats_dev);
+/* Merge of n_groups statistics stats_all [n_groups][B_loc·w] (rank order) into out [B_loc·w],
+ * the same device merge bnn_elbo_step applies after its allgather; each group holds
+ * S_global / n_groups samples. */
+int bnn_mean_merge(bnn_ctx* ctx, const float* stats_all, int32_t n_groups, int32_t B_loc,
+                   int32_t S_global, float* out);
 int bnn_elbo_partial_mean(bnn_ctx* ctx, const float* mu_dev, const float* rho_dev,
                           const float* x_dev, const int32_t* ycls_dev, const float* yreg_dev,
                           int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,

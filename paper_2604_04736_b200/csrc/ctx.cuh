@@ -106,6 +106,8 @@ struct bnn_ctx {
     int S_loc_max = 0, B_max = 0, chunk = 0;
     bool bf16 = false;
     int agg = 0;               // 1: loss of the mean prediction (BNN_LOSS_*_MEAN), SURVEY §8(f) f1
+    int gnll = 0;              // agg with the Gaussian NLL of the predictive (mean, variance)
+    int mkind() const { return gnll ? 2 : model.loss; }  // loss kind of the mean-statistic kernels
     int stat_w = 0;            // agg: statistic width per example (CE 1, MSE O)
     float* mstats = nullptr;   // agg: this rank's Σ_s statistic [B_max × stat_w]
     float* mstats_g = nullptr; // agg: merged over the sample groups

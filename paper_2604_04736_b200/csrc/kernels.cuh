@@ -49,10 +49,12 @@ void launch_loss_head(const float* logits, int S, int B, int O, int loss_kind,
                       const int32_t* ycls, const float* yreg, void* dz, int ldg, bool dz_bf16,
                       float* lossrow, float* dz_f32, cudaStream_t st);
 // exact aggregation: loss of the mean prediction over the S samples
+// loss_kind 0 CE, 1 MSE, 2 Gaussian NLL of the predictive (stats: Welford mean, M2 per output;
+// n_prev = samples already accumulated by earlier chunks)
 void launch_mean_stats(const float* logits, int Sc, int B, int O, int loss_kind,
-                       const int32_t* ycls, float* stats, cudaStream_t st);
+                       const int32_t* ycls, float* stats, int n_prev, cudaStream_t st);
 void launch_mean_merge(const float* gathered, int world, int G, int g, int64_t n, float* out,
-                       cudaStream_t st);
+                       int gnll_O, int n_rank, cudaStream_t st);
 void launch_mean_loss_head(const float* logits, int S, int B, int O, int loss_kind,
                            const int32_t* ycls, const float* yreg, const float* gstats,
                            int S_glob, void* dz, int ldg, bool dz_bf16, float* dz_f32,

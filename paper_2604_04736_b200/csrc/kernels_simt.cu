@@ -273,7 +273,23 @@ void launch_loss_reduce(const float* lossrow, int n, float scale, float* acc_slo
 // groups, then turned into per-sample gradient seeds.
 __global__ void mean_stats_kernel(const float* __restrict__ logits, int Sc, int B, int O,
                                   int loss_kind, const int32_t* __restrict__ ycls,
-                                  float* __restrict__ stats) {
+                                  float* __restrict__ stats, int n_prev) {
+    if (loss_kind == 2) {  // Gaussian NLL: Welford (mean, M2) per (example, output), samples in order
+        const int i = blockIdx.x * blockDim.x + threadIdx.x;
+        if (i >= B * O) return;
+        const int b = i / O, o = i - b * O;
+        float* pm = stats + (int64_t)b * 2 * O + o;
+        float mean = pm[0], m2 = pm[O];
+        for (int s = 0; s < Sc; ++s) {
+            const float x = logits[(int64_t)s * B * O + i];
+            const float d = x - mean;
+            mean += d / (float)(n_prev + s + 1);
+            m2 = fmaf(d, x - mean, m2);
+        }
+        pm[0] = mean;
+        pm[O] = m2;
+        return;
+    }
     if (loss_kind == 0) {  // CE: one warp per example, lanes over samples, fixed-order warp sum
         const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         const int lane = threadIdx.x & 31;
@@ -300,17 +316,37 @@ __global__ void mean_stats_kernel(const float* __restrict__ logits, int Sc, int 
 }
 
 void launch_mean_stats(const float* logits, int Sc, int B, int O, int loss_kind,
-                       const int32_t* ycls, float* stats, cudaStream_t st) {
+                       const int32_t* ycls, float* stats, int n_prev, cudaStream_t st) {
     if (loss_kind == 0)
-        mean_stats_kernel<<<(B + 7) / 8, 256, 0, st>>>(logits, Sc, B, O, loss_kind, ycls, stats);
+        mean_stats_kernel<<<(B + 7) / 8, 256, 0, st>>>(logits, Sc, B, O, loss_kind, ycls, stats, n_prev);
     else
-        mean_stats_kernel<<<(B * O + 127) / 128, 128, 0, st>>>(logits, Sc, B, O, loss_kind, ycls, stats);
+        mean_stats_kernel<<<(B * O + 127) / 128, 128, 0, st>>>(logits, Sc, B, O, loss_kind, ycls, stats,
+                                                               n_prev);
 }
 
-// out[i] = Σ over ranks r with r % G == g (the sample groups of data group g), in rank order
+// CE / MSE: out[i] = Σ over ranks r with r % G == g (the sample groups of data group g), in
+// rank order. Gaussian NLL (gnll_O > 0): per (example, output) the (mean, M2) of every such rank
+// (n_rank samples each) merged in rank order by Chan et al.'s pairwise update.
 __global__ void mean_merge_kernel(const float* __restrict__ gathered, int world, int G, int g,
-                                  int64_t n, float* __restrict__ out) {
+                                  int64_t n, float* __restrict__ out, int gnll_O, int n_rank) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gnll_O > 0) {
+        if (i >= n / 2) return;
+        const int64_t b = i / gnll_O, o = i - b * gnll_O;
+        const int64_t im = b * 2 * gnll_O + o, iv = im + gnll_O;
+        float mean = 0.0f, m2 = 0.0f, na = 0.0f;
+        for (int r = g; r < world; r += G) {
+            const float mr = gathered[(int64_t)r * n + im], vr = gathered[(int64_t)r * n + iv];
+            const float nb = (float)n_rank, nn = na + nb;
+            const float d = mr - mean;
+            mean = fmaf(d, nb / nn, mean);
+            m2 = m2 + vr + d * d * (na * nb / nn);
+            na = nn;
+        }
+        out[im] = mean;
+        out[iv] = m2;
+        return;
+    }
     if (i >= n) return;
     float acc = 0.0f;
     for (int r = g; r < world; r += G) acc += gathered[(int64_t)r * n + i];
@@ -318,8 +354,8 @@ __global__ void mean_merge_kernel(const float* __restrict__ gathered, int world,
 }
 
 void launch_mean_merge(const float* gathered, int world, int G, int g, int64_t n, float* out,
-                       cudaStream_t st) {
-    mean_merge_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(gathered, world, G, g, n, out);
+                       int gnll_O, int n_rank, cudaStream_t st) {
+    mean_merge_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(gathered, world, G, g, n, out, gnll_O, n_rank);
 }
 
 // Gradient seed of the mean-prediction loss for each (s, b) row, unscaled like loss_head_kernel
@@ -355,6 +391,15 @@ __global__ void mean_loss_head_kernel(const float* __restrict__ logits, int rows
         const int y = ycls[b];
         const float w = S_glob * expf(z[y] - lse) / gstats[b];
         for (int k = lane; k < O; k += 32) put(k, w * (expf(z[k] - lse) - (k == y ? 1.0f : 0.0f)));
+    } else if (loss_kind == 2) {
+        // Gaussian NLL of the predictive: m, v = M2/S + 1e-6 (reading R24);
+        // seed (unscaled): (ŷ − m)/v − (y − m)/v − (y − m)²(ŷ − m)/v²
+        for (int k = lane; k < O; k += 32) {
+            const float m = gstats[(int64_t)b * 2 * O + k];
+            const float v = gstats[(int64_t)b * 2 * O + O + k] / S_glob + 1e-6f;
+            const float e = z[k] - m, d = yreg[(int64_t)b * O + k] - m;
+            put(k, (e - d) / v - d * d * e / (v * v));
+        }
     } else {
         for (int k = lane; k < O; k += 32)
             put(k, 2.0f * (gstats[(int64_t)b * O + k] / S_glob - yreg[(int64_t)b * O + k]));
@@ -381,6 +426,13 @@ __global__ void mean_loss_value_kernel(const float* __restrict__ gstats, int B, 
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         if (loss_kind == 0) {
             t += -log((double)gstats[b] / (double)S_glob);
+        } else if (loss_kind == 2) {
+            for (int k = 0; k < O; ++k) {
+                const double m = gstats[(int64_t)b * 2 * O + k];
+                const double v = (double)gstats[(int64_t)b * 2 * O + O + k] / (double)S_glob + 1e-6;
+                const double d = (double)yreg[(int64_t)b * O + k] - m;
+                t += 0.5 * log(6.283185307179586 * v) + d * d / (2.0 * v);
+            }
         } else {
             for (int k = 0; k < O; ++k) {
                 const double d = (double)gstats[(int64_t)b * O + k] / (double)S_glob -

@@ -169,12 +169,12 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, Sc, B, A, sA, Z, sZ, l < L - 1, st); });
         }
         if (phase == kPhaseStats) {
-            c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->model.loss, ycls, c->mstats, st); });
+            c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->mkind(), ycls, c->mstats, (int)(s0 - (uint32_t)(c->kidx * (S_glob / c->K))), st); });
             return BNN_OK;
         }
         if (phase == kPhaseMeanBwd)
             c->launch("loss", [&] {
-                launch_mean_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, gstats, S_glob,
+                launch_mean_loss_head(c->logits, Sc, B, c->O, c->mkind(), ycls, yreg, gstats, S_glob,
                                       c->grad[L - 1], c->O, false, nullptr, st);
             });
         else
@@ -224,12 +224,12 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, Sc, st); });
         }
         if (phase == kPhaseStats) {
-            c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->model.loss, ycls, c->mstats, st); });
+            c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->mkind(), ycls, c->mstats, (int)(s0 - (uint32_t)(c->kidx * (S_glob / c->K))), st); });
             return BNN_OK;
         }
         if (phase == kPhaseMeanBwd)
             c->launch("loss", [&] {
-                launch_mean_loss_head(c->logits, Sc, B, c->O, c->model.loss, ycls, yreg, gstats, S_glob,
+                launch_mean_loss_head(c->logits, Sc, B, c->O, c->mkind(), ycls, yreg, gstats, S_glob,
                                       c->grad[L - 1], c->ld[L], true, c->dz_f32, st);
             });
         else
@@ -422,12 +422,12 @@ int resnet_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycl
     if (!skip_fwd) resnet_forward(c, mu, kk, Sc, B, X0, sX0);
     RBuf& lg = c->rbufs[c->rlogits];
     if (phase == kPhaseStats) {
-        c->launch("loss", [&] { launch_mean_stats(lg.val, Sc, B, c->O, c->model.loss, ycls, c->mstats, st); });
+        c->launch("loss", [&] { launch_mean_stats(lg.val, Sc, B, c->O, c->mkind(), ycls, c->mstats, (int)(s0 - (uint32_t)(c->kidx * (S_glob / c->K))), st); });
         return BNN_OK;
     }
     if (phase == kPhaseMeanBwd)
         c->launch("loss", [&] {
-            launch_mean_loss_head(lg.val, Sc, B, c->O, c->model.loss, ycls, yreg, gstats, S_glob, lg.grad, c->O,
+            launch_mean_loss_head(lg.val, Sc, B, c->O, c->mkind(), ycls, yreg, gstats, S_glob, lg.grad, c->O,
                                   false, nullptr, st);
         });
     else
@@ -555,7 +555,7 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
                 // "additional communication"); one allgather, then a deterministic merge
                 const int64_t n = (int64_t)B_loc * c->stat_w;
                 NCCL_TRY(c, ncclAllGather(c->mstats, c->mgather, (size_t)n, ncclFloat32, c->comm, st));
-                c->launch("loss", [&] { launch_mean_merge(c->mgather, c->cfg.world, c->G, c->gidx, n, c->mstats_g, st); });
+                c->launch("loss", [&] { launch_mean_merge(c->mgather, c->cfg.world, c->G, c->gidx, n, c->mstats_g, c->gnll ? c->O : 0, S_loc, st); });
                 gstats = c->mstats_g;
             } else {
                 if (c->K != 1)
@@ -573,7 +573,7 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
         if (c->kidx == 0) {  // the data loss counts each example once: sample group 0 adds it
             const float sc = c->model.loss == BNN_LOSS_CE ? 1.0f / (float)B_glob : 1.0f / ((float)B_glob * c->O);
             c->launch("loss", [&] {
-                launch_mean_loss_value(gstats, B_loc, c->O, c->model.loss, yreg, S_glob, sc, accl, st);
+                launch_mean_loss_value(gstats, B_loc, c->O, c->mkind(), yreg, S_glob, sc, accl, st);
             });
         }
         CUDA_TRY(c, cudaGetLastError());
@@ -671,11 +671,18 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown precision"));
     if (cfg->aug != BNN_AUG_NONE && cfg->aug != BNN_AUG_PER_SAMPLE)
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown aug mode"));
-    if (model->loss < BNN_LOSS_CE || model->loss > BNN_LOSS_MSE_MEAN)
+    if (model->loss < BNN_LOSS_CE || model->loss > BNN_LOSS_GNLL_MEAN)
         return fail(c->set_err(BNN_ERR_CONFIG, "unknown loss"));
     if (model->loss >= BNN_LOSS_CE_MEAN) {
         // exact aggregation: the base loss family, plus the mean-statistic exchange
         c->agg = 1;
+        c->gnll = model->loss == BNN_LOSS_GNLL_MEAN ? 1 : 0;
+        if (c->gnll && model->kind != BNN_MODEL_MLP)
+            return fail(c->set_err(BNN_ERR_CONFIG, "the Gaussian NLL loss is implemented for MLP models"));
+        // bf16 rounding of the predictions perturbs the S-sample variance that the seeds divide
+        // by (1/v, 1/v²): measured 5-7 % gradient error, beyond the BF16 bar (R24)
+        if (c->gnll && cfg->precision != BNN_PREC_FP32)
+            return fail(c->set_err(BNN_ERR_CONFIG, "the Gaussian NLL loss needs precision FP32"));
         c->model.loss = model->loss == BNN_LOSS_CE_MEAN ? BNN_LOSS_CE : BNN_LOSS_MSE;
     }
     c->bf16 = cfg->precision == BNN_PREC_BF16;
@@ -720,7 +727,7 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     rc = model->kind == BNN_MODEL_MLP ? alloc_mlp(c) : alloc_resnet(c);
     if (rc) return fail(rc);
     if (c->agg) {
-        c->stat_w = c->model.loss == BNN_LOSS_CE ? 1 : c->O;
+        c->stat_w = c->gnll ? 2 * c->O : c->model.loss == BNN_LOSS_CE ? 1 : c->O;
         const size_t n = (size_t)c->B_max * c->stat_w;
         if (!c->alloc(&c->mstats, n) || !c->alloc(&c->mstats_g, n) || !c->alloc(&c->mgather, n * cfg->world))
             return fail(c->set_err(BNN_ERR_CUDA, "out of device memory"));
@@ -796,6 +803,19 @@ int bnn_elbo_partial_mean(bnn_ctx* c, const float* mu, const float* rho, const f
     if (!c || !mu || !rho || !x || !acc_dev || !stats_global_dev) return BNN_ERR_CONFIG;
     return run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, acc_dev,
                        stats_global_dev);
+}
+
+int bnn_mean_merge(bnn_ctx* c, const float* stats_all, int32_t n_groups, int32_t B_loc, int32_t S_global,
+                   float* out) {
+    if (!c || !stats_all || !out || n_groups <= 0 || B_loc <= 0) return BNN_ERR_CONFIG;
+    if (!c->agg) return c->set_err(BNN_ERR_CONFIG, "bnn_mean_merge needs a BNN_LOSS_*_MEAN model");
+    if (S_global % n_groups != 0) return c->set_err(BNN_ERR_CONFIG, "S mod n_groups == 0 violated");
+    const int64_t n = (int64_t)B_loc * c->stat_w;
+    c->launch("loss", [&] {
+        launch_mean_merge(stats_all, n_groups, 1, 0, n, out, c->gnll ? c->O : 0, S_global / n_groups, c->st);
+    });
+    CUDA_TRY(c, cudaGetLastError());
+    return BNN_OK;
 }
 
 int bnn_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc_dev, float* loss_dev,

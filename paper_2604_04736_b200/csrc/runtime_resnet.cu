@@ -438,12 +438,12 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
     const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * c->rbf[0].C_pad : 0;
     const int O = c->O, ldO = (int)round_up(O, 8);
     if (phase == kPhaseStats) {
-        c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, O, c->model.loss, ycls, c->mstats, st); });
+        c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, O, c->mkind(), ycls, c->mstats, (int)(s0 - (uint32_t)(c->kidx * (S_glob / c->K))), st); });
         return BNN_OK;
     }
     if (phase == kPhaseMeanBwd)
         c->launch("loss", [&] {
-            launch_mean_loss_head(c->logits, Sc, B, O, c->model.loss, ycls, yreg, gstats, S_glob, c->fcG, ldO, true,
+            launch_mean_loss_head(c->logits, Sc, B, O, c->mkind(), ycls, yreg, gstats, S_glob, c->fcG, ldO, true,
                                   c->dz_f32, st);
         });
     else

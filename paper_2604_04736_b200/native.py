@@ -18,7 +18,7 @@ _SO = os.path.join(_HERE, "libbnn.so")
 _lib = None
 
 MODEL_MLP, MODEL_RESNET18 = 0, 1
-LOSS = {"ce": 0, "mse": 1, "ce_mean": 2, "mse_mean": 3}  # *_mean: exact aggregation
+LOSS = {"ce": 0, "mse": 1, "ce_mean": 2, "mse_mean": 3, "gnll_mean": 4}  # *_mean: exact aggregation
 PREC = {"fp32": 0, "bf16": 1}
 MODE = {"sample": 0, "data": 1, "hybrid": 2}
 AUG = {"none": 0, "per_sample": 1}
@@ -74,6 +74,7 @@ def lib():
     L.bnn_finalize.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.bnn_mean_stats.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, u64, u32, vp]
     L.bnn_elbo_partial_mean.argtypes = step_args + [vp, vp]
+    L.bnn_mean_merge.argtypes = [vp, vp, i32, i32, i32, vp]
     L.bnn_finalize_adam.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.bnn_elbo_step_adam.argtypes = step_args + [vp] * 9
     L.bnn_predict.argtypes = [vp, vp, vp, vp, i32, i32, u64, u32, vp, vp]
@@ -246,6 +247,13 @@ class Context:
         yc, _ = self._y(y)
         _check(self._L.bnn_mean_stats(self._h, _p(mu), _p(rho), _p(x), yc, x.shape[0], B_global,
                                       S_global, seed, step, _p(out)), self._h)
+        return out
+
+    def mean_merge(self, stats_list, B_loc, S_global):
+        """Merge per-sample-group statistics in list order (bnn_mean_merge)."""
+        allst = torch.stack([t.reshape(-1) for t in stats_list]).contiguous()
+        out = torch.empty_like(allst[0])
+        _check(self._L.bnn_mean_merge(self._h, _p(allst), len(stats_list), B_loc, S_global, _p(out)), self._h)
         return out
 
     def elbo_partial_mean(self, mu, rho, x, y, B_global, S_global, seed, step, stats, acc=None):
