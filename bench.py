@@ -385,6 +385,11 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
     if dom is None:
         return None
     ms = prof[dom]["ms"] / steps
+    if model["kind"] == "mlp" and n_params(model) < 10000:
+        # C1 (161 parameters, 78 KFLOP per step): launch/latency-bound, no roofline
+        return {"kernel": dom, "ms_per_step": ms, "bound": "latency", "achieved": None, "peak": None,
+                "unit": None, "frac": None, "traffic": None,
+                "note": "C1 is latency-bound (tiny MLP); SURVEY.md §8(d) reports µs/step only"}
     if model["kind"] == "mlp":
         w = model["widths"]
         layers = [(w[i + 1], w[i]) for i in range(len(w) - 1)]
