@@ -26,7 +26,7 @@ class OrcModel(C.Structure):
     _fields_ = [("kind", C.c_int), ("n_widths", C.c_int), ("widths", C.c_int * 16),
                 ("in_h", C.c_int), ("in_w", C.c_int), ("in_c", C.c_int),
                 ("n_classes", C.c_int), ("base_width", C.c_int), ("loss", C.c_int),
-                ("act", C.c_int)]
+                ("act", C.c_int), ("mcd", C.c_int), ("dropout_p", C.c_double)]
 
 
 def build():
@@ -66,6 +66,7 @@ def lib():
                                                                            C.c_int, C.c_void_p]
         _lib.orc_elbo_partial_mean.argtypes = [C.c_void_p] * 6 + [C.c_int] * 6 + [
             C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_dropout_keep.argtypes = [C.c_uint64] + [C.c_uint32] * 6
         _lib.orc_adam.argtypes = [C.c_long] + [C.c_void_p] * 4 + [C.c_double] * 4 + [C.c_int]
         _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
                                                                          C.c_void_p, C.c_void_p]
@@ -86,6 +87,9 @@ def model_struct(model: dict, act: str = "relu") -> OrcModel:
         m.base_width = model.get("base_width", 64)
     m.loss = {"ce": CE, "mse": MSE, "gnll": GNLL}[model["loss"]]
     m.act = RELU if act == "relu" else TANH
+    if model.get("method", "vi") == "mcd":  # MC dropout (R25)
+        m.mcd = 1
+        m.dropout_p = float(model.get("dropout_p", 0.1))
     return m
 
 
@@ -172,6 +176,13 @@ def elbo_partial_mean(model, mu, rho, x, y_cls, y_reg, B_glob, b_offset, S_glob,
                                        b_offset, B_glob, S_glob, s0, s1, seed, step, aug, _p(g),
                                        1 if add_loss else 0, _p(acc), nthreads) == 0
     return acc
+
+
+# ---------------------------------------------------------------- MC dropout mask (f4)
+def dropout_keep(seed, step, s, layer, b, j, p):
+    """Keep decision of unit j of hidden layer `layer`, global example b, sample s (R25)."""
+    p24 = int(round(p * 16777216.0))
+    return bool(lib().orc_dropout_keep(seed, step, s, layer, b, j, p24))
 
 
 # ---------------------------------------------------------------- Adam (SURVEY §8(f) f2)

@@ -166,6 +166,20 @@ void orc_aug_params(uint64_t seed, uint32_t step, uint32_t s, uint32_t b, int* d
     *flip = (int)(y[2] & 1u);
 }
 
+/* MC-dropout mask (R25): unit j of hidden layer
+ * `layer` for global example b under sample s is kept iff the 24 high bits of Philox word
+ * (b & 3) of counter ((layer << 24) | (b >> 2), j, (4094 << 20) | s, step) are ≥ P24, the drop
+ * probability in units of 2^-24 (P24 = round(p·2^24)). Integer decision: bit-exact everywhere. */
+int orc_dropout_keep(uint64_t seed, uint32_t step, uint32_t s, uint32_t layer, uint32_t b, uint32_t j,
+                     uint32_t p24)
+{
+    uint32_t ctr[4] = {(layer << 24) | (b >> 2), j, (4094u << 20) | s, step};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t y[4];
+    orc_philox4x32_10(ctr, key, y);
+    return (y[b & 3u] >> 8) >= p24;
+}
+
 /* ======================================================================================
  * Part 2. The model: every layer is a convolution over an NHWC image (a linear layer is
  * a 1×1 convolution over a 1×1 image). Tensor layout: for each layer in
@@ -190,6 +204,8 @@ typedef struct {
     int base_width;  /* ResNet-18 stage-1 width (64 for the paper-shaped model) */
     int loss;        /* ORC_CE | ORC_MSE | ORC_GNLL */
     int act;         /* ORC_RELU (the model) | ORC_TANH (FD self-check variant only) */
+    int mcd;         /* 1: MC dropout (f4): weights μ, dropout after every hidden activation */
+    double dropout_p;
 } orc_model;
 
 typedef struct { int cin, cout, k, stride, pad; long off_w, off_b; } OLayer;
@@ -208,6 +224,9 @@ typedef struct {
     int bh[MAXBUF], bw[MAXBUF], bc[MAXBUF]; /* buffer shapes (H, W, C) */
     long n_params;
     int n_out, loss, act;
+    int mcd;            /* MC dropout (R25) */
+    uint32_t p24;       /* drop threshold, units of 2^-24 */
+    double inv_keep;    /* 1 / (1 − p) */
     int in_h, in_w, in_c;
     int has_act[MAXBUF];   /* an activation is applied to the buffer (BF16 emulation) */
     int n_contrib[MAXBUF]; /* backward contributions to the buffer's gradient */
@@ -257,6 +276,12 @@ static int build_net_(const orc_model* m, ONet* n)
 {
     memset(n, 0, sizeof(*n));
     n->loss = m->loss; n->act = m->act;
+    n->mcd = m->mcd;
+    if (m->mcd) {
+        if (m->kind != ORC_MLP || m->act != ORC_RELU || !(m->dropout_p >= 0.0 && m->dropout_p < 1.0)) return -1;
+        n->p24 = (uint32_t)llround(m->dropout_p * 16777216.0);
+        n->inv_keep = 1.0 / (1.0 - m->dropout_p);
+    }
     if (m->kind == ORC_MLP) {
         if (m->n_widths < 2 || m->n_widths > 16) return -1;
         n->in_h = 1; n->in_w = 1; n->in_c = m->widths[0];
@@ -374,6 +399,19 @@ static void sample_weights(const ONet* n, const double* mu, const double* sigma,
                            uint64_t seed, uint32_t step, uint32_t s, double* W, double* eps_out,
                            int emu)
 {
+    if (n->mcd) {  /* MC dropout (R25): deterministic weights μ; the BF16 operand is RN_bf16(μ) */
+        for (long i = 0; i < n->n_params; ++i) {
+            W[i] = mu[i];
+            if (eps_out) eps_out[i] = 0.0;
+        }
+        if (emu)
+            for (int l = 0; l < n->n_layers; ++l) {
+                const OLayer* L = &n->L[l];
+                long nw = (long)L->cout * L->k * L->k * L->cin;
+                for (long i = 0; i < nw; ++i) W[L->off_w + i] = bf16r((double)(float)mu[L->off_w + i]);
+            }
+        return;
+    }
     for (int l = 0; l < n->n_layers; ++l) {
         const OLayer* L = &n->L[l];
         long cols = (long)L->k * L->k * L->cin;
@@ -458,7 +496,27 @@ static double act_f(int act, double z) { return act == ORC_TANH ? tanh(z) : (z >
 /* derivative expressed through the activation OUTPUT a (ReLU'(0) = 0, reading R13) */
 static double act_d(int act, double a) { return act == ORC_TANH ? 1.0 - a * a : (a > 0 ? 1.0 : 0.0); }
 
-typedef struct { double* val[MAXBUF]; double* grad[MAXBUF]; double* pool; } OWork;
+typedef struct {
+    double* val[MAXBUF];
+    double* grad[MAXBUF];
+    double* pool;
+    /* MC-dropout mask key of the example being processed (set by drop_ctx before forward_one) */
+    uint64_t seed;
+    uint32_t step, s, bg;
+} OWork;
+
+static void drop_ctx(OWork* w, uint64_t seed, uint32_t step, uint32_t s, int b_global)
+{
+    w->seed = seed; w->step = step; w->s = s; w->bg = (uint32_t)b_global;
+}
+
+/* layer whose convolution writes buffer b (MLP: every hidden activation buffer has one) */
+static int producer_layer(const ONet* n, int b)
+{
+    for (int i = 0; i < n->n_ops; ++i)
+        if (n->ops[i].type == OP_CONV && n->ops[i].dst == b) return n->ops[i].layer;
+    return -1;
+}
 
 static long buf_size(const ONet* n, int b) { return (long)n->bh[b] * n->bw[b] * n->bc[b]; }
 
@@ -500,6 +558,12 @@ static int forward_one(const ONet* n, const double* W, OWork* w, int emu)
             case OP_ACT: {
                 long sz = buf_size(n, o->dst);
                 for (long k = 0; k < sz; ++k) w->val[o->dst][k] = act_f(n->act, w->val[o->dst][k]);
+                if (n->mcd) {  /* inverted dropout after the hidden activation (R25) */
+                    const int l = producer_layer(n, o->dst);
+                    for (long k = 0; k < sz; ++k)
+                        w->val[o->dst][k] *= orc_dropout_keep(w->seed, w->step, w->s, (uint32_t)l, w->bg,
+                                                              (uint32_t)k, n->p24) ? n->inv_keep : 0.0;
+                }
                 if (emu) round_buf(n, w, o->dst);
                 break;
             }
@@ -552,7 +616,10 @@ static void backward_one(const ONet* n, const double* W, OWork* w, double* dW, d
             }
             case OP_ACT: {
                 long sz = buf_size(n, o->dst);
-                for (long k = 0; k < sz; ++k) w->grad[o->dst][k] *= act_d(n->act, w->val[o->dst][k]);
+                /* MC dropout: the stored value is ReLU(z)·m/(1−p), so 1[value > 0] = m·1[z > 0]
+                 * and the kept units' gradient carries the 1/(1−p) scale */
+                const double f = n->mcd ? n->inv_keep : 1.0;
+                for (long k = 0; k < sz; ++k) w->grad[o->dst][k] *= act_d(n->act, w->val[o->dst][k]) * f;
                 break;
             }
             case OP_ADD: {
@@ -699,6 +766,7 @@ static int elbo_partial_core(const orc_model* m, const double* mu, const double*
                 for (int k = 0; k < n->n_bufs; ++k)
                     memset(w->grad[k], 0, sizeof(double) * (size_t)buf_size(n, k));
                 load_input(n, x, b, b_offset + b, seed, step, (uint32_t)s, aug, w->val[0]);
+                drop_ctx(w, seed, step, (uint32_t)s, b_offset + b);
                 int out = forward_one(n, W, w, emu);
                 if (seeds) {
                     const double* sd = seeds + ((size_t)s * B_loc + b) * n->n_out;
@@ -752,6 +820,15 @@ int orc_finalize(const orc_model* m, const double* mu, const double* rho, const 
 {
     long P = orc_n_params(m);
     if (P < 0) return -1;
+    if (m->mcd) {  /* MC dropout (R25): no variational distribution, no prior term */
+        for (long i = 0; i < P; ++i) {
+            grad_mu[i] = acc[i];
+            grad_rho[i] = 0.0;
+        }
+        *out_kl = 0.0;
+        *out_loss = acc[2 * P];
+        return 0;
+    }
     double kl = 0.0;
     for (long i = 0; i < P; ++i) {
         double sg = softplus(rho[i]);
@@ -998,6 +1075,7 @@ static int forward_off(const orc_model* m, const double* mu, const double* rho, 
             #pragma omp for schedule(static)
             for (int b = 0; b < B; ++b) {
                 load_input(n, x, b, b_offset + b, seed, step, (uint32_t)s, aug, w->val[0]);
+                drop_ctx(w, seed, step, (uint32_t)s, b_offset + b);
                 int out = forward_one(n, W, w, emu);
                 memcpy(z_out + ((long)(s - s0) * B + b) * n->n_out, w->val[out],
                        sizeof(double) * n->n_out);
@@ -1097,6 +1175,7 @@ long orc_layer_output(const orc_model* m, const double* mu, const double* rho, c
     for (long i = 0; i < P; ++i) sigma[i] = softplus(rho[i]);
     sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, emu);
     load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w.val[0]);
+    drop_ctx(&w, seed, step, (uint32_t)s, b);
     forward_one(n, W, &w, emu);
     long cnt = -3;
     for (int i = 0; i < n->n_ops; ++i)
@@ -1130,6 +1209,7 @@ long orc_layer_grad(const orc_model* m, const double* mu, const double* rho, con
     for (long i = 0; i < P; ++i) sigma[i] = softplus(rho[i]);
     sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, emu);
     load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w.val[0]);
+    drop_ctx(&w, seed, step, (uint32_t)s, b);
     int outb = forward_one(n, W, &w, emu);
     double dz[4096];
     loss_one(n, w.val[outb], ycls, yreg, b, dz);
@@ -1168,6 +1248,7 @@ long orc_layer_dump(const orc_model* m, const double* mu, const double* rho, con
     for (long i = 0; i < P; ++i) sigma[i] = softplus(rho[i]);
     sample_weights(n, mu, sigma, seed, step, (uint32_t)s, W, NULL, emu);
     load_input(n, x, b, b, seed, step, (uint32_t)s, aug, w.val[0]);
+    drop_ctx(&w, seed, step, (uint32_t)s, b);
     int outb = forward_one(n, W, &w, emu);
     if (grad) {
         double dz[4096];

@@ -427,3 +427,45 @@ def test_gnll_against_torch_autograd(rho_mode):
     assert o["loss"] == pytest.approx(t["loss"], rel=1e-10)
     _cmp(o["grad_mu"], t["grad_mu"], 1e-8)
     _cmp(o["grad_rho"], t["grad_rho"], 1e-8)
+
+
+# ---------------------------------------------------------------- MC dropout
+MCD = dict(kind="mlp", widths=[12, 16, 9, 4], loss="mse", method="mcd", dropout_p=0.3)
+
+
+def test_dropout_mask_statistics():
+    """Keep rate 1 − p (binomial, 5σ) and independence across layers / samples / examples."""
+    p, n = 0.3, 20000
+    keep = np.array([O.dropout_keep(7, 3, 0, 1, b, j, p) for b in range(200) for j in range(100)])
+    assert abs(keep.mean() - (1 - p)) <= 5 * np.sqrt(p * (1 - p) / n)
+    other = np.array([O.dropout_keep(7, 3, 1, 1, b, j, p) for b in range(200) for j in range(100)])
+    other_l = np.array([O.dropout_keep(7, 3, 0, 2, b, j, p) for b in range(200) for j in range(100)])
+    agree = (1 - p) ** 2 + p ** 2
+    for o in (other, other_l):
+        assert abs(np.mean(keep == o) - agree) <= 5 * np.sqrt(agree * (1 - agree) / n)
+    assert all(O.dropout_keep(7, 3, 0, 1, b, j, 0.0) for b in range(8) for j in range(8))
+
+
+def test_mcd_p0_is_the_deterministic_network():
+    """p = 0: every sample is the network with weights μ (torch, library layers + autograd)."""
+    model = dict(MCD, dropout_p=0.0)
+    mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
+    x, _, yr = synth.make_batch(model, 10, seed=4)
+    o = O.elbo_step(model, mu, rho, x, None, yr, 3, 5, 1, 100.0)
+    l0, g0 = torch_ref.deterministic(model, mu, x, None, yr)
+    assert o["loss"] == pytest.approx(l0, rel=1e-12)
+    _cmp(o["grad_mu"], g0, 1e-10)
+    assert not np.any(o["grad_rho"]) and o["kl"] == 0.0
+
+
+@pytest.mark.parametrize("agg", ["sample", "mean"])
+def test_mcd_against_torch_autograd(agg):
+    """MC-dropout step (per-sample MSE and MSE of the averaged predictions) against the
+    independent torch formulation with the same keep masks."""
+    mu, rho = synth.init_params(MCD, seed=8, rho_mode="wide")
+    x, _, yr = synth.make_batch(MCD, 7, seed=9)
+    o = O.elbo_step(MCD, mu, rho, x, None, yr, 4, 0xABC, 2, 777.0, agg=agg)
+    t = torch_ref.elbo(MCD, mu, rho, x, None, yr, 4, 0xABC, 2, 777.0, agg=agg)
+    assert o["loss"] == pytest.approx(t["loss"], rel=1e-12)
+    _cmp(o["grad_mu"], t["grad_mu"], 1e-10)
+    assert not np.any(o["grad_rho"])

@@ -25,8 +25,9 @@ def _augment(x, seed, step, s, b_global):
     return out
 
 
-def _forward(model, ws, x, act):
-    """x: [B, features] (MLP) or [B, H, W, C] (CNN); ws: list of tensors in layout order."""
+def _forward(model, ws, x, act, masks=None):
+    """x: [B, features] (MLP) or [B, H, W, C] (CNN); ws: list of tensors in layout order;
+    masks[l]: MC-dropout keep mask of hidden layer l ([B, width], already scaled by 1/(1−p))."""
     a = torch.relu if act == "relu" else torch.tanh
     if model["kind"] == "mlp":
         h = x
@@ -36,6 +37,8 @@ def _forward(model, ws, x, act):
             h = F.linear(h, W, b)
             if l < n - 1:
                 h = a(h)
+                if masks is not None:
+                    h = h * masks[l]
         return h
     # ResNet-18 (reading R12), NCHW for torch
     cin = model["in_c"]
@@ -80,18 +83,29 @@ def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu
     B = X.shape[0]
     L_data = 0.0
     zs = []
+    mcd = model.get("method", "vi") == "mcd"
     for s in range(S):
         ws = []
         for ti in lay:
             n = ti["rows"] * ti["cols"]
             sl = slice(ti["offset"], ti["offset"] + n)
+            if mcd:  # MC dropout: deterministic weights μ
+                ws.append(mu_t[sl].reshape(ti["rows"], ti["cols"]))
+                continue
             e = torch.tensor(O.eps_fill(seed, step, s, ti["t"], 0, ti["rows"], 0, ti["cols"])
                              .astype(np.float64)).reshape(-1)
             ws.append((mu_t[sl] + sigma[sl] * e).reshape(ti["rows"], ti["cols"]))
         Xs = X
         if aug:
             Xs = torch.stack([_augment(X[b], seed, step, s, b) for b in range(B)])
-        z = _forward(model, ws, Xs, act)
+        masks = None
+        if mcd:  # keep decisions from the oracle's mask function (pinned separately)
+            p = model.get("dropout_p", 0.1)
+            widths = model["widths"]
+            masks = [torch.tensor([[O.dropout_keep(seed, step, s, l, b, j, p) / (1.0 - p)
+                                    for j in range(widths[l + 1])] for b in range(B)], dtype=torch.float64)
+                     for l in range(len(widths) - 2)]
+        z = _forward(model, ws, Xs, act, masks)
         if agg == "mean":
             zs.append(z)
             continue
@@ -117,10 +131,13 @@ def elbo(model, mu, rho, x, y_cls, y_reg, S, seed, step, D, aug=False, act="relu
         else:
             L_data = F.mse_loss(Z.mean(0), torch.tensor(np.asarray(y_reg, np.float64)))
     kl = 0.5 * torch.sum(sigma ** 2 + mu_t ** 2 - 1.0 - torch.log(sigma ** 2))
+    if mcd:  # no variational distribution, no prior term
+        kl = torch.zeros((), dtype=torch.float64)
     loss = L_data + kl / D
     loss.backward()
     return dict(loss=loss.item(), L_data=float(L_data.detach()), kl=kl.item(),
-                grad_mu=mu_t.grad.numpy().copy(), grad_rho=rho_t.grad.numpy().copy())
+                grad_mu=mu_t.grad.numpy().copy(),
+                grad_rho=(rho_t.grad.numpy().copy() if rho_t.grad is not None else np.zeros(rho_t.shape)))
 
 
 def deterministic(model, mu, x, y_cls, y_reg):
