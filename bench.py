@@ -38,6 +38,7 @@ WORKLOAD_NAMES = {
     "mlp_784_1024_1024_10": "Bayesian MLP 784-1024-1024-10 (CE)",
     "mlp_8_16_1": "Bayesian MLP 8-16-1 (MSE)",
     "resnet18_cifar": "ResNet-18-shaped Bayesian CNN, 32x32x3, per-sample crop+flip",
+    "mcd_mlp_96_128_128_24": "MC-dropout MLP 96-128-128-24 (p=0.1), MSE of the averaged predictions",
 }
 
 
@@ -60,7 +61,7 @@ def run_plan(config, world, mode_arg=None):
         K = max(1, world // G)
         return dict(S=cfg["S"], S_loc=cfg["S"] // K, B=cfg["B"], B_loc=cfg["B"] // G, K=K, G=G,
                     mode="hybrid" if world > 1 else "sample", scaling="strong")
-    # C1 / C2: weak scaling, S = S_config per GPU
+    # C1 / C2 / C6: weak scaling, S = S_config per GPU
     S_loc, B = cfg["S"], cfg["B"]
     return dict(S=S_loc * world, S_loc=S_loc, B=B, B_loc=B, K=world, G=1, mode="sample",
                 scaling="weak")
@@ -447,7 +448,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "C6"])
     ap.add_argument("--mode", default=None, choices=["sample", "data"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--ref-budget", type=float, default=None,

@@ -75,6 +75,11 @@ enum { BNN_LOSS_CE = 0, BNN_LOSS_MSE = 1, BNN_LOSS_CE_MEAN = 2, BNN_LOSS_MSE_MEA
 enum { BNN_PREC_FP32 = 0, BNN_PREC_BF16 = 1 };
 enum { BNN_MODE_SAMPLE_SHARDED = 0, BNN_MODE_DATA_SHARDED = 1, BNN_MODE_HYBRID = 2 };
 enum { BNN_AUG_NONE = 0, BNN_AUG_PER_SAMPLE = 1 };
+/* BNN_METHOD_MCD: Monte Carlo dropout (use case 2
+ * P:318-320; R25): the weights are μ (ρ is ignored, grad_rho = 0, no prior term),
+ * a "sample" is one draw of inverted-dropout masks on every hidden activation, keyed by
+ * (seed, step, global sample, layer, global example, unit). MLP models only. */
+enum { BNN_METHOD_VI = 0, BNN_METHOD_MCD = 1 };
 
 /* Model description.
  *  MLP:      widths[0] = input features, widths[n_widths-1] = outputs; ReLU between layers.
@@ -89,6 +94,8 @@ typedef struct bnn_model_desc {
     int32_t n_classes;
     int32_t base_width;
     int32_t loss; /* BNN_LOSS_CE (labels int32) | BNN_LOSS_MSE (targets fp32 [B, outputs]) */
+    int32_t method;   /* BNN_METHOD_VI (Bayes by backprop, default) | BNN_METHOD_MCD */
+    float dropout_p;  /* MCD: drop probability of every hidden unit, 0 ≤ p < 1 */
 } bnn_model_desc;
 
 /* Run configuration. Rank r of world P = K·G is sample group k = r / G, data group

@@ -85,7 +85,9 @@ def model_struct(model: dict, act: str = "relu") -> OrcModel:
         m.in_h, m.in_w, m.in_c = model["in_h"], model["in_w"], model["in_c"]
         m.n_classes = model["n_classes"]
         m.base_width = model.get("base_width", 64)
-    m.loss = {"ce": CE, "mse": MSE, "gnll": GNLL}[model["loss"]]
+    # the loss family; "*_mean" (exact aggregation) is selected by elbo_step(agg="mean")
+    m.loss = {"ce": CE, "mse": MSE, "gnll": GNLL, "ce_mean": CE, "mse_mean": MSE,
+              "gnll_mean": GNLL}[model["loss"]]
     m.act = RELU if act == "relu" else TANH
     if model.get("method", "vi") == "mcd":  # MC dropout (R25)
         m.mcd = 1

@@ -9,6 +9,10 @@ The five workloads C1-C5 are BASELINE.json's ``configs``
 * C3 — ResNet-18-shaped Bayesian CNN on 32×32×3, B=128, S=8 per GPU (weak scaling).
 * C4 — the same CNN, fixed S=64 (strong scaling), sample-sharded vs data-sharded.
 * C5 — 4 sample groups × 2 data groups, S=32, global batch 256.
+* C6 — not a BASELINE config: the MC-dropout use case shape (MLP
+  96-128-128-24 trained on the MSE of the averaged predictions), dropout
+  p = 0.1 (reading R25), B=256, S=64 (the paper's batch and sample counts for this use case
+  are not stated; C2's are used).
 
 |D| values follow SURVEY.md §8(d): 1024 (C1), 60000 (C2), 45000 (C3-C5).
 """
@@ -19,6 +23,8 @@ MODELS = {
     "mlp_784_1024_1024_10": dict(kind="mlp", widths=[784, 1024, 1024, 10], loss="ce"),
     "resnet18_cifar": dict(kind="resnet18", in_h=32, in_w=32, in_c=3, n_classes=10,
                            base_width=64, loss="ce"),
+    "mcd_mlp_96_128_128_24": dict(kind="mlp", widths=[96, 128, 128, 24], loss="mse_mean",
+                                  method="mcd", dropout_p=0.1),
 }
 
 CONFIGS = {
@@ -27,6 +33,7 @@ CONFIGS = {
     "C3": dict(model="resnet18_cifar", B=128, S_per_gpu=8, D=45000.0, aug="per_sample"),
     "C4": dict(model="resnet18_cifar", B=128, S=64, D=45000.0, aug="per_sample"),
     "C5": dict(model="resnet18_cifar", B=256, S=32, D=45000.0, aug="per_sample", K=4, G=2),
+    "C6": dict(model="mcd_mlp_96_128_128_24", B=256, S=64, D=1.0, aug="none", K=1, G=1),
 }
 
 

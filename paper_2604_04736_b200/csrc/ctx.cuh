@@ -107,6 +107,18 @@ struct bnn_ctx {
     bool bf16 = false;
     int agg = 0;               // 1: loss of the mean prediction (BNN_LOSS_*_MEAN), SURVEY §8(f) f1
     int gnll = 0;              // agg with the Gaussian NLL of the predictive (mean, variance)
+    int mcd = 0;               // MC dropout
+    uint32_t p24 = 0;          // MCD drop threshold, units of 2^-24
+    float inv_keep = 1.0f;
+    DropArgs drop_for(int layer, bool on, int B) const {
+        DropArgs d{};
+        d.on = (mcd && on) ? 1 : 0;
+        d.p24 = p24;
+        d.inv_keep = inv_keep;
+        d.layer = layer;
+        d.b_off = gidx * B;
+        return d;
+    }
     int mkind() const { return gnll ? 2 : model.loss; }  // loss kind of the mean-statistic kernels
     int stat_w = 0;            // agg: statistic width per example (CE 1, MSE O)
     float* mstats = nullptr;   // agg: this rank's Σ_s statistic [B_max × stat_w]

@@ -16,6 +16,16 @@ struct SampledLayer {
     uint32_t t_w, t_b;
 };
 
+// MC dropout of one hidden layer (R25): forward kernels multiply the
+// post-ReLU value by keep·inv_keep; dgrad kernels scale the masked gradient by inv_keep.
+struct DropArgs {
+    int on;
+    uint32_t p24;     // drop threshold in units of 2^-24
+    float inv_keep;   // 1 / (1 − p)
+    int layer;        // hidden-layer index of the mask key
+    int b_off;        // global index of the rank's first example
+};
+
 struct SampleKeys {
     EpsKey key;
     uint32_t step;
@@ -26,7 +36,7 @@ struct SampleKeys {
 void launch_sigma(const float* rho, float* sigma, int64_t n, cudaStream_t st);
 // grad_μ, grad_ρ, KL block partials (double), then loss = acc[2P] + KL/D
 // loss[0] = L_data + KL/D, loss[1] = KL
-void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
+void launch_finalize(int mcd, const float* mu, const float* rho, const float* acc_mu,
                      const float* acc_rho, const float* Ldata, int64_t P, double D,
                      float* grad_mu, float* grad_rho, double* kl_partials, int n_part,
                      float* loss, cudaStream_t st);
@@ -80,10 +90,10 @@ void launch_to_bf16(const float* x, int B, int K, int ldx, void* out, cudaStream
 
 // ---------------------------------------------------------------- K11: FP32 SIMT sampled GEMMs
 // Z[s][b][n] = act(Σ_k A[s][b][k]·W_s[n][k] + b_s[n]) for s in [0, S), b in [0, B).
-void launch_fwd_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* A,
+void launch_fwd_fp32(const SampledLayer& L, const SampleKeys& k, const DropArgs& d, int S, int B, const float* A,
                      int64_t strideA, float* Z, int64_t strideZ, bool relu, cudaStream_t st);
 // dA[s][b][k] = (Σ_n G[s][b][n]·W_s[n][k]) · 1[A[s][b][k] > 0]
-void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
+void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, const DropArgs& d, int S, int B, const float* G,
                        int64_t strideG, const float* Aprev, int64_t strideA, float* dA,
                        int64_t strideD, cudaStream_t st);
 // acc_μ[n][k] += scale·Σ_s dW_s[n][k]; acc_ρ[n][k] += scale·Σ_s dW_s[n][k]·ε_s[n][k] with

@@ -49,8 +49,17 @@ __device__ __forceinline__ double fin_one(float mu, float rho, float am, float a
 __global__ void __launch_bounds__(256) finalize_kernel(
     const float* __restrict__ mu, const float* __restrict__ rho, const float* __restrict__ acc_mu,
     const float* __restrict__ acc_rho, int64_t P, float invD, float* __restrict__ grad_mu,
-    float* __restrict__ grad_rho, double* __restrict__ kl_partials) {
+    float* __restrict__ grad_rho, double* __restrict__ kl_partials, int mcd) {
     double kl = 0.0;
+    if (mcd) {  // MC dropout (R25): grad_μ = the data gradient, no ρ, no prior term
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
+            grad_mu[i] = acc_mu[i];
+            grad_rho[i] = 0.0f;
+        }
+        if (threadIdx.x == 0) kl_partials[blockIdx.x] = 0.0;
+        return;
+    }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t P4 = P / 4;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P4; i += stride) {
@@ -104,12 +113,12 @@ int finalize_partials_count(int64_t P) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((P / 4 + 255) / 256, kNumSMs * 8));
 }
 
-void launch_finalize(const float* mu, const float* rho, const float* acc_mu,
+void launch_finalize(int mcd, const float* mu, const float* rho, const float* acc_mu,
                       const float* acc_rho, const float* Ldata, int64_t P, double D,
                       float* grad_mu, float* grad_rho, double* kl_partials, int n_part,
                       float* loss, cudaStream_t st) {
     finalize_kernel<<<n_part, 256, 0, st>>>(mu, rho, acc_mu, acc_rho, P, (float)(1.0 / D),
-                                            grad_mu, grad_rho, kl_partials);
+                                            grad_mu, grad_rho, kl_partials, mcd);
     finalize_loss_kernel<<<1, 1024, 0, st>>>(kl_partials, n_part, Ldata, 1.0 / D, loss);
 }
 
@@ -603,7 +612,7 @@ void launch_bf16_to_f32(const void* x, int64_t n, float* y, cudaStream_t st) {
 // ====================================================================== K11: FP32 SIMT GEMMs
 constexpr int TB = 64, TK = 16;
 
-__global__ void __launch_bounds__(256) fwd_fp32_kernel(SampledLayer L, SampleKeys kk, int B,
+__global__ void __launch_bounds__(256) fwd_fp32_kernel(SampledLayer L, SampleKeys kk, DropArgs d, int B,
                                                        const float* __restrict__ A,
                                                        int64_t strideA, float* __restrict__ Z,
                                                        int64_t strideZ, int relu) {
@@ -673,18 +682,21 @@ __global__ void __launch_bounds__(256) fwd_fp32_kernel(SampledLayer L, SampleKey
             if (n >= N) continue;
             float v = acc[i][j] + bias[tx * 4 + j];
             if (relu) v = fmaxf(v, 0.0f);
+            if (d.on)
+                v = dropout_keep(kk.key, kk.step, sg, (uint32_t)d.layer, (uint32_t)(d.b_off + b), (uint32_t)n, d.p24)
+                        ? v * d.inv_keep : 0.0f;
             Z[s * strideZ + (int64_t)b * N + n] = v;
         }
     }
 }
 
-void launch_fwd_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* A,
+void launch_fwd_fp32(const SampledLayer& L, const SampleKeys& k, const DropArgs& d, int S, int B, const float* A,
                      int64_t strideA, float* Z, int64_t strideZ, bool relu, cudaStream_t st) {
     dim3 grid((L.N + TB - 1) / TB, (B + TB - 1) / TB, S);
-    fwd_fp32_kernel<<<grid, 256, 0, st>>>(L, k, B, A, strideA, Z, strideZ, relu ? 1 : 0);
+    fwd_fp32_kernel<<<grid, 256, 0, st>>>(L, k, d, B, A, strideA, Z, strideZ, relu ? 1 : 0);
 }
 
-__global__ void __launch_bounds__(256) dgrad_fp32_kernel(SampledLayer L, SampleKeys kk, int B,
+__global__ void __launch_bounds__(256) dgrad_fp32_kernel(SampledLayer L, SampleKeys kk, DropArgs d, int B,
                                                          const float* __restrict__ G,
                                                          int64_t strideG,
                                                          const float* __restrict__ Ap,
@@ -746,17 +758,18 @@ __global__ void __launch_bounds__(256) dgrad_fp32_kernel(SampledLayer L, SampleK
         for (int j = 0; j < 4; ++j) {
             const int k = kt0 + tx * 4 + j;
             if (k >= K) continue;
-            const float m = Ap[s * strideA + (int64_t)b * K + k] > 0.0f ? 1.0f : 0.0f;
+            // ReLU (and, under MC dropout, the keep mask: the stored input is 0 where dropped)
+            const float m = Ap[s * strideA + (int64_t)b * K + k] > 0.0f ? (d.on ? d.inv_keep : 1.0f) : 0.0f;
             dA[s * strideD + (int64_t)b * K + k] = acc[i][j] * m;
         }
     }
 }
 
-void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
+void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, const DropArgs& d, int S, int B, const float* G,
                        int64_t strideG, const float* Aprev, int64_t strideA, float* dA,
                        int64_t strideD, cudaStream_t st) {
     dim3 grid((L.K + TB - 1) / TB, (B + TB - 1) / TB, S);
-    dgrad_fp32_kernel<<<grid, 256, 0, st>>>(L, k, B, G, strideG, Aprev, strideA, dA, strideD);
+    dgrad_fp32_kernel<<<grid, 256, 0, st>>>(L, k, d, B, G, strideG, Aprev, strideA, dA, strideD);
 }
 
 __global__ void __launch_bounds__(256) wgrad_fp32_kernel(SampledLayer L, SampleKeys kk, int S,

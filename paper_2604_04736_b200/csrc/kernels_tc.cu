@@ -292,6 +292,10 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                         if (j < nvalid) {
                             float z = v[j] + bias;
                             if (a.relu) z = fmaxf(z, 0.0f);
+                            if (a.drop.on)  // MC dropout after the hidden activation (R25)
+                                z = dropout_keep(a.kk.key, a.kk.step, sg, (uint32_t)a.drop.layer,
+                                                 (uint32_t)(a.drop.b_off + bc0 + j), (uint32_t)m, a.drop.p24)
+                                        ? z * a.drop.inv_keep : 0.0f;
                             o[(int64_t)j * a.ldo] = __float2bfloat16_rn(z);
                         }
                     }
@@ -304,8 +308,10 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                 for (int j = 0; j < 16; ++j) {
                     if (j < nvalid) {
                         // ReLU mask of the layer input: bf16 > 0 ⟺ sign bit clear and ≠ 0
+                        // (MC dropout: a dropped unit is stored as 0, a kept one carries 1/(1 − p))
                         const float g =
-                            (!a.mask || (mraw[j] != 0 && (mraw[j] & 0x8000u) == 0)) ? v[j] : 0.0f;
+                            (!a.mask || (mraw[j] != 0 && (mraw[j] & 0x8000u) == 0))
+                                ? (a.drop.on ? v[j] * a.drop.inv_keep : v[j]) : 0.0f;
                         part += g;
                         o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
                     }

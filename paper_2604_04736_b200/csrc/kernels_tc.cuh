@@ -29,6 +29,7 @@ struct TcGenArgs {
     int vec_ok;          // μ/σ rows are 16-byte aligned (float4 loads)
     float* dbpart;       // dgrad: fp32 column sums per 16-row chunk, [s][B/16][M]
     int64_t dbpart_stride_s;
+    DropArgs drop;       // MC dropout: fwd masks the ReLU output, dgrad scales by 1/(1 − p)
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
 

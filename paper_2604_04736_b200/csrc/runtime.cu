@@ -166,7 +166,8 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             const int64_t sA = l == 0 ? 0 : (int64_t)B * c->ld[l];
             float* Z = l == L - 1 ? c->logits : (float*)c->act[l + 1];
             const int64_t sZ = (int64_t)B * (l == L - 1 ? c->O : c->ld[l + 1]);
-            c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, Sc, B, A, sA, Z, sZ, l < L - 1, st); });
+            const DropArgs dr = c->drop_for(l, l < L - 1, B);
+            c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, dr, Sc, B, A, sA, Z, sZ, l < L - 1, st); });
         }
         if (phase == kPhaseStats) {
             c->launch("loss", [&] { launch_mean_stats(c->logits, Sc, B, c->O, c->mkind(), ycls, c->mstats, (int)(s0 - (uint32_t)(c->kidx * (S_glob / c->K))), st); });
@@ -197,7 +198,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             }, 2);
             if (l > 0)
                 c->launch("dgrad", [&] {
-                    launch_dgrad_fp32(sl, kk, Sc, B, Gl, sG, (const float*)c->act[l], sA,
+                    launch_dgrad_fp32(sl, kk, c->drop_for(l - 1, true, B), Sc, B, Gl, sG, (const float*)c->act[l], sA,
                                       (float*)c->grad[l - 1], (int64_t)B * c->ld[l], st);
                 });
         }
@@ -221,6 +222,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.ldo = l == L - 1 ? c->O : c->ld[l + 1];
             a.out_stride_s = (int64_t)B * a.ldo;
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
+            a.drop = c->drop_for(l, l < L - 1, B);
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, Sc, st); });
         }
         if (phase == kPhaseStats) {
@@ -262,6 +264,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
             a.dbpart = c->dbpart[l - 1];
             a.dbpart_stride_s = (int64_t)((B + 15) / 16) * a.L.K;
+            a.drop = c->drop_for(l - 1, true, B);
             c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[l], a, Sc, st); });
         }
         for (int l0 = 0; l0 < L; l0 += kMaxBiasGroup) {
@@ -523,7 +526,10 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
         return c->set_err(BNN_ERR_CONFIG, "mean statistics need a BNN_LOSS_*_MEAN model");
     cudaStream_t st = c->st;
     if (!stats_out) CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(float) * c->acc_total, st));
-    c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
+    if (c->mcd)  // MC dropout: the weights are μ (σ = 0 ⇒ W_s = fma(0, ε, μ) = μ), R25
+        CUDA_TRY(c, cudaMemsetAsync(c->sigma, 0, sizeof(float) * c->P, st));
+    else
+        c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
     if (c->bf16 && c->model.kind == BNN_MODEL_MLP) {
         const int K0 = c->widths[0];
         c->launch("cast", [&] { launch_to_bf16(x, B_loc, K0, c->ld[0], c->xb, st); });
@@ -598,7 +604,7 @@ int run_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc
                  float* gmu, float* grho) {
     cudaStream_t st = c->st;
     c->launch("finalize", [&] {
-        launch_finalize(mu, rho, acc, acc + c->P_pad, acc + 2 * c->P_pad, c->P, c->cfg.dataset_size,
+        launch_finalize(c->mcd, mu, rho, acc, acc + c->P_pad, acc + 2 * c->P_pad, c->P, c->cfg.dataset_size,
                         gmu, grho, c->kl_part, c->n_part, c->lossbuf, st);
     }, 2);
     if (loss_dev) CUDA_TRY(c, cudaMemcpyAsync(loss_dev, c->lossbuf, sizeof(float), cudaMemcpyDeviceToDevice, st));
@@ -684,6 +690,16 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
         if (c->gnll && cfg->precision != BNN_PREC_FP32)
             return fail(c->set_err(BNN_ERR_CONFIG, "the Gaussian NLL loss needs precision FP32"));
         c->model.loss = model->loss == BNN_LOSS_CE_MEAN ? BNN_LOSS_CE : BNN_LOSS_MSE;
+    }
+    if (model->method != BNN_METHOD_VI && model->method != BNN_METHOD_MCD)
+        return fail(c->set_err(BNN_ERR_CONFIG, "unknown method"));
+    if (model->method == BNN_METHOD_MCD) {  // MC dropout (R25)
+        if (model->kind != BNN_MODEL_MLP) return fail(c->set_err(BNN_ERR_CONFIG, "MC dropout is implemented for MLP models"));
+        if (!(model->dropout_p >= 0.0f && model->dropout_p < 1.0f))
+            return fail(c->set_err(BNN_ERR_CONFIG, "0 <= dropout_p < 1 violated"));
+        c->mcd = 1;
+        c->p24 = (uint32_t)llround((double)model->dropout_p * 16777216.0);
+        c->inv_keep = (float)(1.0 / (1.0 - (double)model->dropout_p));
     }
     c->bf16 = cfg->precision == BNN_PREC_BF16;
     c->B_max = cfg->max_B_loc;
@@ -878,6 +894,7 @@ int check_adam(bnn_ctx* c, const bnn_adam* h, AdamHyper* out) {
 int run_finalize_adam(bnn_ctx* c, float* mu, float* rho, const float* acc, const bnn_adam* hp,
                       float* m_mu, float* v_mu, float* m_rho, float* v_rho, float* loss_dev,
                       float* gmu, float* grho) {
+    if (c->mcd) return c->set_err(BNN_ERR_CONFIG, "the fused Adam step is for BNN_METHOD_VI models");
     AdamHyper h;
     int rc = check_adam(c, hp, &h);
     if (rc) return rc;
@@ -959,7 +976,10 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
     const int L = (int)c->layers.size();
     const int S_loc = S_global / c->K;
     const int BO = B * c->O;
-    c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
+    if (c->mcd)  // MC dropout: the weights are μ (σ = 0 ⇒ W_s = fma(0, ε, μ) = μ), R25
+        CUDA_TRY(c, cudaMemsetAsync(c->sigma, 0, sizeof(float) * c->P, st));
+    else
+        c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
     if (c->bf16 && c->model.kind == BNN_MODEL_MLP)
         c->launch("cast", [&] { launch_to_bf16(x, B, c->widths[0], c->ld[0], c->xb, st); });
     // per chunk forward; stats over all local samples need all logits, so chunk == S_loc here
@@ -976,7 +996,8 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
             const int64_t sA = l == 0 ? 0 : (int64_t)B * c->ld[l];
             float* Z = l == L - 1 ? c->logits : (float*)c->act[l + 1];
             const int64_t sZ = (int64_t)B * (l == L - 1 ? c->O : c->ld[l + 1]);
-            c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, S_loc, B, A, sA, Z, sZ, l < L - 1, st); });
+            const DropArgs dr = c->drop_for(l, l < L - 1, B);
+            c->launch("fwd", [&] { launch_fwd_fp32(sl, kk, dr, S_loc, B, A, sA, Z, sZ, l < L - 1, st); });
         } else {
             TcGenArgs a{};
             a.L = sampled(c, l, mu);
@@ -993,6 +1014,7 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
             a.ldo = l == L - 1 ? c->O : c->ld[l + 1];
             a.out_stride_s = (int64_t)B * a.ldo;
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
+            a.drop = c->drop_for(l, l < L - 1, B);
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, S_loc, st); });
         }
     }

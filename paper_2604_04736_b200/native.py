@@ -27,7 +27,8 @@ AUG = {"none": 0, "per_sample": 1}
 class BnnModelDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_widths", C.c_int32), ("widths", C.c_int32 * 16),
                 ("in_h", C.c_int32), ("in_w", C.c_int32), ("in_c", C.c_int32),
-                ("n_classes", C.c_int32), ("base_width", C.c_int32), ("loss", C.c_int32)]
+                ("n_classes", C.c_int32), ("base_width", C.c_int32), ("loss", C.c_int32),
+                ("method", C.c_int32), ("dropout_p", C.c_float)]
 
 
 class BnnConfig(C.Structure):
@@ -132,6 +133,9 @@ def model_desc(model: dict) -> BnnModelDesc:
         d.n_classes = model["n_classes"]
         d.base_width = model.get("base_width", 64)
     d.loss = LOSS[model["loss"]]
+    if model.get("method", "vi") == "mcd":  # MC dropout
+        d.method = 1
+        d.dropout_p = float(model.get("dropout_p", 0.1))
     return d
 
 

@@ -53,7 +53,7 @@ def make_batch(model: dict, B: int, seed: int = 1):
     rng = np.random.default_rng(seed)
     shp = input_shape(model)
     O = n_outputs(model)
-    if model["kind"] == "mlp" and model["loss"] in ("mse", "gnll"):
+    if model["kind"] == "mlp" and model["loss"].split("_")[0] in ("mse", "gnll"):
         x = rng.normal(0.0, 1.0, (B,) + shp)
         # fixed teacher network: widths of the model, ReLU hidden layers
         w = model["widths"]
@@ -70,7 +70,7 @@ def make_batch(model: dict, B: int, seed: int = 1):
         x = rng.uniform(0.0, 1.0, (B,) + shp)
     else:
         x = rng.normal(0.0, 1.0, (B,) + shp)
-    if model["loss"] == "ce":
+    if model["loss"].split("_")[0] == "ce":
         y = rng.integers(0, O, B).astype(np.int32)
         return x.astype(np.float32), y, None
     y = rng.normal(0.0, 1.0, (B, O))

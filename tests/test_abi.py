@@ -33,8 +33,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_binding_struct_sizes_match_header():
     from paper_2604_04736_b200 import native
-    # bnn_model_desc: 2 + 16 + 5 + 1 int32
-    assert C.sizeof(native.BnnModelDesc) == 4 * (2 + 16 + 6)
+    # bnn_model_desc: 2 + 16 + 5 + 1 int32, method int32, dropout_p float
+    assert C.sizeof(native.BnnModelDesc) == 4 * (2 + 16 + 6 + 2)
     # bnn_config: 6 int32, ptr, 4 int32, double, int32 (+pad), ptr
     assert C.sizeof(native.BnnConfig) == 24 + 8 + 16 + 8 + 8 + 8
     assert C.sizeof(native.BnnTensorInfo) == 8 + 4 * 4
