@@ -206,12 +206,20 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                 const float* mup = L.mu + e0;
                 const float* sgp = L.sigma + e0;
                 const int64_t estep = (int64_t)rstep * L.K;
+                if (a.mu_only) {  // MC dropout: RN_bf16(fma(0, ε, μ)) = RN_bf16(μ)
 #pragma unroll 4
-                for (int it = 0; it < kItems; ++it) {
-                    const uint2 w = gen_w4_fast(mup + it * estep, sgp + it * estep, a.kk.key,
-                                                a.kk.step, w3, (uint32_t)(n0 + it * rstep),
-                                                (uint32_t)(k0 >> 2));
-                    sts64(tileA + it * sstep, w);
+                    for (int it = 0; it < kItems; ++it) {
+                        const float4 m = __ldg(reinterpret_cast<const float4*>(mup + it * estep));
+                        sts64(tileA + it * sstep, make_uint2(pack_bf16x2(m.x, m.y), pack_bf16x2(m.z, m.w)));
+                    }
+                } else {
+#pragma unroll 4
+                    for (int it = 0; it < kItems; ++it) {
+                        const uint2 w = gen_w4_fast(mup + it * estep, sgp + it * estep, a.kk.key,
+                                                    a.kk.step, w3, (uint32_t)(n0 + it * rstep),
+                                                    (uint32_t)(k0 >> 2));
+                        sts64(tileA + it * sstep, w);
+                    }
                 }
             } else if (MODE == 0 && vec && m_full && ((L.K - kb * 64) & 3) == 0) {
                 // forward, last k-block of a fan-in that is not a multiple of 64 (784 = 12·64 + 16):
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
-            if (n < L.N) {
+            if (n < L.N && !a.skip_eps) {
                 const uint32_t sgw = ((L.t_w << 20) | (a.kk.s0 + s));
                 if (kfull) {
 #pragma unroll

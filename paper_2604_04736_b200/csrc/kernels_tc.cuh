@@ -30,6 +30,7 @@ struct TcGenArgs {
     float* dbpart;       // dgrad: fp32 column sums per 16-row chunk, [s][B/16][M]
     int64_t dbpart_stride_s;
     DropArgs drop;       // MC dropout: fwd masks the ReLU output, dgrad scales by 1/(1 − p)
+    int mu_only;         // MC dropout: σ = 0, so W_s = RN_bf16(μ) without drawing ε
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
 
@@ -42,6 +43,7 @@ struct WgradLayer {
     int b_shared;
 };
 struct TcWgradArgs {
+    int skip_eps;        // MC dropout: acc_ρ is not used, the epilogue draws no ε
     SampleKeys kk;
     int S, B;
     float scale;

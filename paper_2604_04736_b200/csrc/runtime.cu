@@ -223,6 +223,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.out_stride_s = (int64_t)B * a.ldo;
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
             a.drop = c->drop_for(l, l < L - 1, B);
+            a.mu_only = c->mcd;
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, Sc, st); });
         }
         if (phase == kPhaseStats) {
@@ -265,6 +266,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
             a.dbpart = c->dbpart[l - 1];
             a.dbpart_stride_s = (int64_t)((B + 15) / 16) * a.L.K;
             a.drop = c->drop_for(l - 1, true, B);
+            a.mu_only = c->mcd;
             c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[l], a, Sc, st); });
         }
         for (int l0 = 0; l0 < L; l0 += kMaxBiasGroup) {
@@ -290,6 +292,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
         for (int l0 = 0; l0 < L; l0 += kMaxWgradLayers) {
             TcWgradMaps maps;
             TcWgradArgs w{};
+            w.skip_eps = c->mcd;
             w.kk = kk;
             w.S = Sc;
             w.B = B;
@@ -1015,6 +1018,7 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
             a.out_stride_s = (int64_t)B * a.ldo;
             a.vec_ok = (a.L.K % 4 == 0 && a.L.off_w % 4 == 0) ? 1 : 0;
             a.drop = c->drop_for(l, l < L - 1, B);
+            a.mu_only = c->mcd;
             c->launch("fwd", [&] { launch_gen_gemm(c->map_fwdB[l], a, S_loc, st); });
         }
     }
