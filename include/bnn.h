@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 1
+#define BNN_ABI_VERSION 2  /* 2: bnn_model_desc.method / .dropout_p (MC dropout), Adam, mean-aggregation entry points */
 
 typedef enum {
     BNN_OK = 0,
