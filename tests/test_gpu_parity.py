@@ -832,3 +832,50 @@ def test_mcd_predict_matches_oracle():
     rm, rv = O.predict(MCD_MLP, mu, rho, x, S, 3, 0)
     assert _rel(mean.cpu().numpy(), rm) < 1e-4
     assert _rel(var.cpu().numpy(), rv) < 1e-3
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("bf16", 2e-2)])
+@pytest.mark.parametrize("model,B,S", [
+    (dict(kind="mlp", widths=[33, 17, 5], loss="ce"), 1, 1),          # one example, one sample
+    (dict(kind="mlp", widths=[130, 260, 10], loss="ce"), 300, 2),      # B > 256: two batch tiles, ragged tail
+    (dict(kind="mlp", widths=[1030, 129, 3], loss="mse"), 19, 3),      # K and N off every tile size
+])
+def test_edge_shapes_match_oracle(model, B, S, precision, tol):
+    mu, rho, x, yc, yr = _inputs(model, B, "init")
+    ctx, loss, gmu, grho = _run_gpu(model, precision, mu, rho, x, yc, yr, S, 0xE0, 1, 100.0)
+    ref = O.elbo_step(model, mu, rho, x, yc, yr, S, 0xE0, 1, 100.0)
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    assert max(_per_tensor_rel(ctx, gmu, ref["grad_mu"])) <= tol
+    assert max(_per_tensor_rel(ctx, grho, ref["grad_rho"])) <= tol
+
+
+def test_predict_single_sample_has_zero_variance():
+    """S = 1: the predictive variance is exactly 0 (population variance of one value)."""
+    native = _native()
+    mu, rho, x, _, _ = _inputs(RAGGED, 9, "wide")
+    ctx = native.Context(RAGGED, precision="bf16", max_B_loc=9, max_S_loc=1, dataset_size=1.0)
+    mean, var = ctx.predict(_dev(mu), _dev(rho), _dev(x), 1, 3, 0)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(var).item() == 0
+    assert torch.allclose(mean.sum(-1), torch.ones(9, device=mean.device), atol=1e-5)
+
+
+def test_invariant_violations_fail_loudly_on_device():
+    """Shape invariants of the step and a non-finite loss (BNN_ERR_NUMERIC)."""
+    native = _native()
+    mu, rho, x, yc, _ = _inputs(RAGGED, 8, "init")
+    ctx = native.Context(RAGGED, precision="bf16", max_B_loc=8, max_S_loc=2, dataset_size=1.0)
+    with pytest.raises(native.BnnError, match="max_S_loc"):
+        ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), _dev(yc), 8, 3, 1, 0)
+    with pytest.raises(native.BnnError, match="B_loc"):
+        big = np.concatenate([x, x])
+        ctx.elbo_step(_dev(mu), _dev(rho), _dev(big), _dev(np.concatenate([yc, yc])), 16, 2, 1, 0)
+    sh = native.Context(RAGGED, precision="bf16", mode="sample", K=2, rank=0, world=2, max_B_loc=8,
+                        max_S_loc=2, dataset_size=1.0)
+    with pytest.raises(native.BnnError, match="S mod K"):
+        sh.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), 8, 3, 1, 0)
+    bad = mu.copy()
+    bad[0] = np.nan
+    with pytest.raises(native.BnnError, match="non-finite"):
+        ctx.elbo_step(_dev(bad), _dev(rho), _dev(x), _dev(yc), 8, 2, 1, 0)
