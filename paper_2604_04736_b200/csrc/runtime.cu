@@ -528,15 +528,19 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
     if ((gstats_in || stats_out) && !c->agg)
         return c->set_err(BNN_ERR_CONFIG, "mean statistics need a BNN_LOSS_*_MEAN model");
     cudaStream_t st = c->st;
+    // the bf16 cast of the input overlaps the σ prologue (side stream, joined before the chunks)
+    const bool cast = c->bf16 && c->model.kind == BNN_MODEL_MLP;
+    if (cast) {
+        cudaStream_t ss = fork_side(c);
+        const int K0 = c->widths[0];
+        c->launch("cast", [&] { launch_to_bf16(x, B_loc, K0, c->ld[0], c->xb, ss); });
+    }
     if (!stats_out) CUDA_TRY(c, cudaMemsetAsync(acc, 0, sizeof(float) * c->acc_total, st));
     if (c->mcd)  // MC dropout: the weights are μ (σ = 0 ⇒ W_s = fma(0, ε, μ) = μ), R25
         CUDA_TRY(c, cudaMemsetAsync(c->sigma, 0, sizeof(float) * c->P, st));
     else
         c->launch("sigma", [&] { launch_sigma(rho, c->sigma, c->P, st); });
-    if (c->bf16 && c->model.kind == BNN_MODEL_MLP) {
-        const int K0 = c->widths[0];
-        c->launch("cast", [&] { launch_to_bf16(x, B_loc, K0, c->ld[0], c->xb, st); });
-    }
+    if (cast) join_side(c);
     const int S_loc = S_glob / c->K;
     float* accm = acc;
     float* accr = acc ? acc + c->P_pad : nullptr;
