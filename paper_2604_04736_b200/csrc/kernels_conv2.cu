@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    mbar_wait_role(&empty[st], ph ^ 1);
                     if (a.dbg & 2) {  // feed-rate experiment: no loads
                         mbar_arrive_expect_tx(&full[st], 0);
                         continue;
@@ -352,14 +352,14 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
                 const int buf = tl & 1;
-                mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 const int nkb = nkb_of(g.cls);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&full[st], ph);
+                    mbar_wait_role(&full[st], ph);
                     fence_proxy_async_smem();
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    mbar_wait_role(&empty[st], ph ^ 1);
                     if (a.dbg & 2) {  // feed-rate experiment: no loads
                         mbar_arrive_expect_tx(&full[st], 0);
                         continue;
@@ -670,14 +670,14 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
                 const int buf = tl & 1;
-                mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 const int nkb = nkb_of(g.cls);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&full[st], ph);
+                    mbar_wait_role(&full[st], ph);
                     fence_proxy_async_smem();
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
@@ -996,7 +996,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                 for (int b = 0; b < u.nblk; ++b, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&empty[st], ph ^ 1);
+                    mbar_wait_role(&empty[st], ph ^ 1);
                     if (a.dbg & 2) {  // feed-rate experiment: no loads
                         mbar_arrive_expect_tx(&full[st], 0);
                         continue;
@@ -1027,13 +1027,13 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                 const U u = unit(t);
                 const uint32_t idesc = idesc_bf16(128, u.w, 1, 1);
                 const int buf = tl & 1;
-                mbar_wait_sleep(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 for (int b = 0; b < u.nblk; ++b, ++it) {
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait_sleep(&full[st], ph);
+                    mbar_wait_role(&full[st], ph);
                     fence_proxy_async_smem();
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);

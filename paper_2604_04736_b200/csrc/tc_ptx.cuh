@@ -80,7 +80,7 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t pari
 // suspend-hint form (try_wait with a 1 ms hint: ptxas emits a NANOSLEEP.SYNCS after each
 // failed probe); the default polls with the plain try_wait, whose wake-up follows the phase
 // flip directly — the suspended form was measured to delay the MMA issue of short k-loops.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_role(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
 #ifdef BNN_SUSPEND_WAITS
     if (mbar_try_wait_sleep(a, parity)) return;
