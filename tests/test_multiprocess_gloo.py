@@ -42,8 +42,9 @@ def _worker(rank, world, port, mode, K, G, model, S, B, aug, out):
     mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
     x, yc, yr = synth.make_batch(model, B, seed=4)
     xs = x[sh["b0"]:sh["b1"]]
-    ys = yc[sh["b0"]:sh["b1"]]
-    acc = O.elbo_partial(model, mu, rho, xs, ys, None, B, sh["b0"], S, sh["s0"], sh["s1"], 9, 2,
+    ys = None if yc is None else yc[sh["b0"]:sh["b1"]]
+    yrs = None if yr is None else yr[sh["b0"]:sh["b1"]]
+    acc = O.elbo_partial(model, mu, rho, xs, ys, yrs, B, sh["b0"], S, sh["s0"], sh["s1"], 9, 2,
                          O.AUG_PER_SAMPLE if aug else O.AUG_NONE, nthreads=1)
     t = torch.from_numpy(acc)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -61,7 +62,7 @@ def _run(world, mode, K=None, G=None, model=MODEL, S=8, B=8, aug=False):
              join=True)
     mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
     x, yc, yr = synth.make_batch(model, B, seed=4)
-    ref = O.elbo_step(model, mu, rho, x, yc, None, S, 9, 2, 500.0,
+    ref = O.elbo_step(model, mu, rho, x, yc, yr, S, 9, 2, 500.0,
                       aug=O.AUG_PER_SAMPLE if aug else O.AUG_NONE, nthreads=1)
     uids = {out[r][3] for r in range(world)}
     assert len(uids) == 1  # every rank received rank 0's id
@@ -96,6 +97,13 @@ def test_gloo_world2_data_sharded():
 
 def test_gloo_world4_hybrid_with_augmentation():
     _run(4, "hybrid", K=2, G=2, model=CNN, S=4, B=4, aug=True)
+
+
+def test_gloo_world4_hybrid_mc_dropout():
+    """MC dropout (f4): masks keyed by global sample and global example, so the 2×2 grid's
+    allreduced partials equal the single process."""
+    _run(4, "hybrid", K=2, G=2, model=dict(kind="mlp", widths=[6, 9, 4], loss="mse", method="mcd",
+                                            dropout_p=0.25))
 
 
 # ---------------------------------------------------------------- exact aggregation (f1), two collectives
