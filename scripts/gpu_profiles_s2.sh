@@ -15,3 +15,5 @@ KREGEX="gen_gemm_kernel<.int.0, .int.2" CFG=C2 SKIP=1 TAG=full_c2_fwd bash scrip
 KREGEX="conv3_kernel<.int.1" CFG=C3 SKIP=6 TAG=full_c3_dgrad bash scripts/gpu_prof_one.sh
 python scripts/eps_rate.py > gpurun_out/eps_rate.txt 2>&1
 ls -la gpurun_out
+KREGEX="wgrad_tc_kernel" CFG=C2 SKIP=1 TAG=full_c2_wgrad bash scripts/gpu_prof_one.sh
+timeout 300 python bench.py --config C1 --precision fp32 --agg gnll --no-cpu-baseline > gpurun_out/bench_C1_gnll.log 2>&1
