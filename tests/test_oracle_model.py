@@ -469,3 +469,31 @@ def test_mcd_against_torch_autograd(agg):
     assert o["loss"] == pytest.approx(t["loss"], rel=1e-12)
     _cmp(o["grad_mu"], t["grad_mu"], 1e-10)
     assert not np.any(o["grad_rho"])
+
+
+def test_gnll_bayesian_linear_regression_large_S():
+    """Gaussian NLL of the predictive (R24) on a 1-layer Bayesian linear regression: as S grows
+    the sample mean and variance of the predictions converge to the closed forms
+    m = xᵀμ + μ_b, v = Σ x_k² σ_k² + σ_b², so the data term converges to
+    mean_b [½ ln(2π(v + 1e-6)) + (y − m)²/(2(v + 1e-6))]; with S = 20000 the oracle's value
+    lies within the delta-method error of the closed form."""
+    d, B, S = 5, 4, 20000
+    model = dict(kind="mlp", widths=[d, 1], loss="gnll")
+    rng = np.random.default_rng(11)
+    mu = rng.normal(0, 0.5, d + 1)
+    sigma = rng.uniform(0.2, 0.8, d + 1)
+    rho = np.log(np.expm1(sigma))
+    x = rng.normal(0, 1, (B, d)).astype(np.float32)
+    y = rng.normal(0, 1, (B, 1)).astype(np.float32)
+    xd, yd = x.astype(np.float64), y.astype(np.float64)[:, 0]
+    m = xd @ mu[:d] + mu[d]
+    v = (xd ** 2) @ sigma[:d] ** 2 + sigma[d] ** 2 + 1e-6
+    expect = np.mean(0.5 * np.log(2 * np.pi * v) + (yd - m) ** 2 / (2 * v))
+    o = O.elbo_step(model, mu, rho, x, None, y, S, 21, 0, 1e12, agg="mean")
+    # error of the estimate: ∂L/∂m · SE(m) + ∂L/∂v · SE(v) per example, averaged
+    dLdm = -(yd - m) / v
+    dLdv = 0.5 / v - (yd - m) ** 2 / (2 * v ** 2)
+    se = np.sqrt((dLdm ** 2) * v / S + (dLdv ** 2) * 2 * v ** 2 / S) / B  # per example (shared samples: add linearly)
+    tol = 5 * np.sum(se)
+    assert abs(o["L_data"] - expect) < tol, (o["L_data"], expect, tol)
+    assert tol < 0.02 * abs(expect) + 0.02  # the check is informative
