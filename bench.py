@@ -409,7 +409,10 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
                                f"{INSTR_PER_NORMAL} SASS instr per normal (DESIGN.md §4)",
                 "tensor_tflops": flops[dom] / (ms / 1e3) / 1e12,
                 "tensor_frac_of_measured": flops[dom] / (ms / 1e3) / 1e12
-                / peaks.get("bf16_tflops", 1590.0)}
+                / peaks.get("bf16_tflops", 1590.0),
+                # context: the standalone generator's measured rate (scripts/eps_rate.py; the
+                # fused kernels also load μ/σ, build and store W_s tiles, run the epilogue)
+                **_standalone_eps(ach)}
     convs = conv_layers(model)
     f_all = sum(2 * B * oh * ow * co * k * k * ci for k, st, ci, co, oh, ow in convs)
     f_nostem = f_all - 2 * B * convs[0][4] * convs[0][5] * convs[0][3] * 9 * convs[0][2]
@@ -423,6 +426,16 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
             "unit": "TFLOP/s", "frac": ach / peak, "traffic": _ncu_traffic("cnn", dom),
             "peak_source": f"measured bf16 sustained ({peak_src}, MEASURED_PEAKS.json); "
                            f"burst {peaks.get('bf16_tflops')}"}
+
+
+def _standalone_eps(achieved):
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "session2", "eps_rate.txt")
+    try:
+        rate = json.loads(open(path).read().strip().splitlines()[-1])["eps_bench_gnormal_per_s"]
+    except (OSError, ValueError, KeyError, IndexError):
+        return {}
+    return {"standalone_generator_gnormal_s": rate, "frac_of_standalone_generator": achieved / rate,
+            "standalone_source": "profiles/r01/session2/eps_rate.txt (scripts/eps_rate.py, measured)"}
 
 
 # SASS instructions issued per ε normal by the fused generator (eps4 + W build), from
