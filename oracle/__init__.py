@@ -215,7 +215,9 @@ def tensor_infos(model):
 
 def elbo_partial(model, mu, rho, x, y_cls, y_reg, B_glob, b_offset, S_glob, s0, s1, seed, step,
                  aug=AUG_NONE, nthreads=0, act="relu", emu=False):
-    """emu=True: the BF16 tensor-core mode's rounding points (reading R14)."""
+    """emu=True: the BF16 tensor-core mode's rounding points (DESIGN.md reading R14);
+    emu="weights": only the BF16 mode's sampled weight w_s = RN_bf16(fma_f32(σ, ε, μ)) (R14),
+    everything else exact fp64 (the conditioning probe of DESIGN.md R26)."""
     m = model_struct(model, act)
     P = lib().orc_n_params(C.byref(m))
     mu, rho, x, yr = _d(mu), _d(rho), _d(x), _d(y_reg)
@@ -224,7 +226,7 @@ def elbo_partial(model, mu, rho, x, y_cls, y_reg, B_glob, b_offset, S_glob, s0, 
     acc = np.zeros(2 * P + 1, np.float64)
     rc = lib().orc_elbo_partial_ex(C.byref(m), _p(mu), _p(rho), _p(x), _p(yc), _p(yr), B_loc,
                                    b_offset, B_glob, S_glob, s0, s1, seed, step, aug, _p(acc),
-                                   nthreads, 1 if emu else 0)
+                                   nthreads, 2 if emu == "weights" else (1 if emu else 0))
     assert rc == 0, rc
     return acc
 

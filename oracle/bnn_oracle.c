@@ -727,6 +727,9 @@ static int elbo_partial_core(const orc_model* m, const double* mu, const double*
     if (build_net(m, &net)) return -1;
     ONet* n = &net;
     long P = n->n_params;
+    /* emu = 1: every R14 rounding point; emu = 2: only the sampled weight of the BF16 mode,
+     * w_s = RN_bf16(fma_f32(σ, ε, μ)) (R14's definition of w_s), everything else exact fp64 */
+    const int emu_act = emu == 1;
 #ifdef _OPENMP
     if (nthreads <= 0) nthreads = omp_get_max_threads();
 #else
@@ -767,7 +770,7 @@ static int elbo_partial_core(const orc_model* m, const double* mu, const double*
                     memset(w->grad[k], 0, sizeof(double) * (size_t)buf_size(n, k));
                 load_input(n, x, b, b_offset + b, seed, step, (uint32_t)s, aug, w->val[0]);
                 drop_ctx(w, seed, step, (uint32_t)s, b_offset + b);
-                int out = forward_one(n, W, w, emu);
+                int out = forward_one(n, W, w, emu_act);
                 if (seeds) {
                     const double* sd = seeds + ((size_t)s * B_loc + b) * n->n_out;
                     for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = sd[k];
@@ -776,9 +779,9 @@ static int elbo_partial_core(const orc_model* m, const double* mu, const double*
                     lt[tid] += l * scale;
                     /* exact mode: the seed carries the 1/(S·B) scale; emulation: the unscaled
                      * seed is what the bf16 operand rounds, the scale is applied at accumulation */
-                    for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = emu ? dz[k] : dz[k] * scale;
+                    for (int k = 0; k < n->n_out; ++k) w->grad[out][k] = emu_act ? dz[k] : dz[k] * scale;
                 }
-                backward_one(n, W, w, dWt + (size_t)tid * P, emu ? scale : 1.0, emu,
+                backward_one(n, W, w, dWt + (size_t)tid * P, emu_act ? scale : 1.0, emu_act,
                              tmps + (size_t)tid * maxbuf);
             }
         }
