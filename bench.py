@@ -7,11 +7,19 @@ Rank 0 prints ONE JSON line. A "step" is one pass of the whole hot path (σ prol
 sampled forward, loss head, sampled backward with sample-accumulating wgrad, allreduce,
 finalize + KL) over one synthetic minibatch.
 
-N=1 workload: C2 = Bayesian MLP 784-1024-1024-10, B=256, S=64 (BASELINE.json configs[1]).
-For N>1 the run is weak-scaled: S = 64·N samples sharded over N ranks (same batch per rank).
+Default workload: C3 = the ResNet-18-shaped Bayesian CNN on 32×32×3 CIFAR-shaped batches,
+B = 128, S = 8 per GPU, per-sample crop+flip (BASELINE.json configs[2], the configuration its
+metric is quoted on); N > 1 is weak-scaled (S = 8·N sharded over N ranks, same batch).
+`--config C2` is the Bayesian MLP 784-1024-1024-10 (B = 256, S = 64), C4 the strong-scaled
+S = 64 run (sample- vs `--mode data`-sharded), C5 the 4×2 hybrid grid, C1/C6 the small MLPs.
 
-`--impl reference` times the CPU oracle (oracle/, fp64, all host cores) on a bounded sample
-of the same workload — the tier's reference arm.
+`--gpus N` with N > 1 outside torchrun re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL) and fails
+loudly when fewer than N GPUs are visible.
+
+`--impl reference` times the CPU oracle (oracle/, fp64, all host cores): each of its steps is
+a bounded, stated slice of the same workload (the full C3 step is ≈ 1 core-hour), timed as
+it runs — the tier's reference arm.
 """
 from __future__ import annotations
 
@@ -82,110 +90,143 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every 5 ms during the timed region (NVML, the
+    library nvidia-smi reads; nvidia-smi -lms as the fallback)."""
+
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.rows = []
-        self.proc = None
+        self.rows = []  # (sm_mhz, sm_max_mhz, reasons bitmask)
+        self.stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.idx]) if vis and vis.split(",")[0].isdigit() else self.idx
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self.stop.is_set():
+                    self.rows.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, reasons(h)))
+                    time.sleep(0.005)
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([v.strip() for v in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        if self.t is not None:
+            time.sleep(0.01)
+            self.stop.set()
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({k for r in self.rows for k, bit in self.BITS.items() if r[2] & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML every 5 ms inside the timed region"}
 
 
 # ====================================================================== reference arm
-def cpu_oracle_rate(model, B, D, budget_s=15.0, seed=0x5EED, aug="none"):
-    """Time the fp64 oracle (as it stands) on the host cores over a bounded sample of the
-    workload: all B examples, S_sample samples; returns (sample·images/s, cores, sample)."""
+def oracle_slice(model, B, budget_s, aug="none"):
+    """Size a bounded slice of one step for the fp64 oracle (as it stands, all host cores):
+    all B examples × n samples if one sample of the batch fits the budget, else 1 sample × n
+    examples (≥ the core count, the oracle parallelises over examples). Returns a callable
+    that runs the slice once, and its (samples, images, description)."""
     import oracle as O
     mu, rho = synth.init_params(model, seed=2)
     x, yc, yr = synth.make_batch(model, B, seed=1)
     cores = os.cpu_count() or 1
     O.lib()
     a = O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE
-    # probe with a few images, then size the slice to ≈ budget_s of CPU work
-    Bp = min(B, 8)
+
+    def run(S_s, B_s):
+        O.elbo_partial(model, mu, rho, x[:B_s], None if yc is None else yc[:B_s],
+                       None if yr is None else yr[:B_s], B, 0, 64, 0, S_s, 0x5EED, 0, a)
+
+    Bp = min(B, cores)
     t0 = time.perf_counter()
-    O.elbo_partial(model, mu, rho, x[:Bp], None if yc is None else yc[:Bp],
-                   None if yr is None else yr[:Bp], B, 0, 64, 0, 1, seed, 0, a)
-    t1 = (time.perf_counter() - t0) / Bp
-    n_img = max(1, int(budget_s / max(t1, 1e-6)))
+    run(1, Bp)
+    t_img = (time.perf_counter() - t0) / Bp  # wall seconds per sample·image with ≥ cores threads busy
+    n_img = max(1, int(budget_s / max(t_img, 1e-9)))
     if n_img >= B:
-        S_sample, B_s = max(1, min(64, n_img // B)), B
+        S_s, B_s = max(1, min(64, n_img // B)), B
     else:
-        S_sample, B_s = 1, n_img
+        S_s, B_s = 1, max(1, min(B, n_img))
+    desc = (f"{S_s} sample(s) x {B_s} of {B} images of one step (a bounded slice; value = "
+            f"sample-images of the slice / its wall time), fp64, {cores} threads")
+    return (lambda: run(S_s, B_s)), S_s, B_s, cores, desc
+
+
+def cpu_oracle_rate(model, B, budget_s, aug="none"):
+    fn, S_s, B_s, cores, desc = oracle_slice(model, B, budget_s, aug)
     t0 = time.perf_counter()
-    O.elbo_partial(model, mu, rho, x[:B_s], None if yc is None else yc[:B_s],
-                   None if yr is None else yr[:B_s], B, 0, 64, 0, S_sample, seed, 0, a)
+    fn()
     dt = time.perf_counter() - t0
-    return S_sample * B_s / dt, cores, (f"{S_sample} sample(s) x {B_s} of {B} images (a slice of "
-                                        f"one step), fp64, {cores} threads")
+    return S_s * B_s / dt, cores, desc
 
 
 def run_reference(args, world, rank):
+    """The tier's reference arm: the oracle as it stands, rank 0 only; each step is the same
+    bounded slice of the workload, timed as it runs (ms_per_step is that slice's time)."""
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
     model = MODELS[cfg["model"]]
     plan = run_plan(args.config, world, args.mode)
     B, S = plan["B"], plan["S"]
-    rates = []
-    for i in range(args.warmup + args.steps):
-        r, cores, sample = cpu_oracle_rate(model, B, cfg["D"], budget_s=args.ref_budget,
-                                           aug=cfg.get("aug", "none"))
-        if i >= args.warmup:
-            rates.append(r)
-    v = statistics.median(rates)
+    fn, S_s, B_s, cores, desc = oracle_slice(model, B, args.ref_budget, cfg.get("aug", "none"))
+    for _ in range(args.warmup):
+        fn()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    ms = sum(ts) / len(ts) * 1e3
+    v = S_s * B_s / (ms / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "sample·images/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": S * B / v * 1e3, "higher_is_better": True,
+            "ms_per_step": ms, "higher_is_better": True,
             "scaling": plan["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
-                       "global_batch": B, "samples": S},
+                       "global_batch": B, "samples": S,
+                       "reference_step": desc,
+                       "full_step_estimate_s": S * B / v},
             "cpu_baseline": {"value": v, "unit": "sample·images/s", "cores": cores,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": "sample·images/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ====================================================================== our arm
+def _time_steps(step, n, stream, flush, sampler=None):
+    """n steps, each bracketed by CUDA events on the library's stream, an L2 flush (a 256 MiB
+    memset, > the 126 MB L2) between them outside the events; returns the summed ms."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for i in range(n):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step(i)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev)
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
@@ -214,11 +255,13 @@ def run_ours(args, world, rank, local_rank):
     g_idx = rank % G
 
     mu_h, rho_h = synth.init_params(MODELS[cfg["model"]], seed=2)
-    x_h, yc_h, yr_h = synth.make_batch(MODELS[cfg["model"]], B, seed=1)
-    # this rank's data-group shard of the global batch
-    x_h = x_h[g_idx * B_loc:(g_idx + 1) * B_loc]
-    yc_h = None if yc_h is None else yc_h[g_idx * B_loc:(g_idx + 1) * B_loc]
-    yr_h = None if yr_h is None else yr_h[g_idx * B_loc:(g_idx + 1) * B_loc]
+    x_all, yc_all, yr_all = synth.make_batch(MODELS[cfg["model"]], B, seed=1)
+
+    def shard(gi, bl):
+        return (x_all[gi * bl:(gi + 1) * bl], None if yc_all is None else yc_all[gi * bl:(gi + 1) * bl],
+                None if yr_all is None else yr_all[gi * bl:(gi + 1) * bl])
+
+    x_h, yc_h, yr_h = shard(g_idx, B_loc)
     mu = torch.from_numpy(mu_h).to(dev)
     rho = torch.from_numpy(rho_h).to(dev)
     x = torch.from_numpy(x_h).to(dev)
@@ -229,7 +272,8 @@ def run_ours(args, world, rank, local_rank):
     stream = torch.cuda.current_stream(dev)
     ctx = native.Context(model, precision=args.precision, mode=plan["mode"], K=K, G=G, rank=rank,
                          world=world, uid=uid, max_B_loc=B_loc, max_S_loc=S_loc, dataset_size=D,
-                         device=local_rank, stream=stream.cuda_stream, aug=cfg.get("aug", "none"))
+                         device=local_rank, stream=stream.cuda_stream, aug=cfg.get("aug", "none"),
+                         sample_chunk=args.sample_chunk)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     adam = args.optimizer == "adam"
@@ -260,17 +304,12 @@ def run_ours(args, world, rank, local_rank):
     if distributed:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     launches0 = ctx.launch_count()
     with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the events)
-            ev[i][0].record(stream)
-            step(args.warmup + i)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
+        total_ms = _time_steps(lambda i: step(args.warmup + i), args.steps, stream, flush)
     launches = ctx.launch_count() - launches0
+    if distributed:
+        dist.barrier()
     # per-kernel-class timing (the roofline line) in separate, untimed steps: the class events
     # the library records around its launches would otherwise sit inside the timed region
     prof_steps = max(3, min(args.steps, 10))
@@ -281,10 +320,6 @@ def run_ours(args, world, rank, local_rank):
     torch.cuda.synchronize()
     prof = ctx.profile_read()
     ctx.profile(False)
-    if distributed:
-        dist.barrier()
-    times = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(times)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -293,8 +328,8 @@ def run_ours(args, world, rank, local_rank):
     value = S * B / (ms_per_step / 1e3)
 
     # ---------------- end to end through the public API with host buffers
-    x_pin = torch.from_numpy(x_h).pin_memory()
-    y_pin = torch.from_numpy(yc_h if yc_h is not None else yr_h).pin_memory()
+    x_pin = torch.from_numpy(np.ascontiguousarray(x_h)).pin_memory()
+    y_pin = torch.from_numpy(np.ascontiguousarray(yc_h if yc_h is not None else yr_h)).pin_memory()
     for i in range(2):
         step_host(i)
     torch.cuda.synchronize()
@@ -311,6 +346,39 @@ def run_ours(args, world, rank, local_rank):
     if distributed:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = S * B / (float(te.item()) / args.steps / 1e3)
+    ctx.close()
+
+    # ---------------- the paper's comparison: the same library, DDP-style data-sharded
+    # (K = 1, G = world: every rank draws all S samples for its B/world examples),
+    # same global S and B, timed the same way (N > 1 only; at N = 1 the two modes coincide)
+    ddp = None
+    if world > 1 and args.config in ("C3", "C4") and args.mode != "data" and not args.no_ddp and B % world == 0:
+        Bd = B // world
+        xd_h, ycd_h, yrd_h = shard(rank, Bd)
+        xd = torch.from_numpy(np.ascontiguousarray(xd_h)).to(dev)
+        yd = torch.from_numpy(np.ascontiguousarray(ycd_h if ycd_h is not None else yrd_h)).to(dev)
+        obj = [native.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        cd = native.Context(model, precision=args.precision, mode="data", K=1, G=world, rank=rank,
+                            world=world, uid=obj[0], max_B_loc=Bd, max_S_loc=S, dataset_size=D,
+                            device=local_rank, stream=stream.cuda_stream, aug=cfg.get("aug", "none"),
+                            sample_chunk=min(S, max(8, args.sample_chunk)))
+
+        def dstep(i):
+            cd.elbo_step(mu, rho, xd, yd, B, S, 0x5EED, i, grad_mu=gmu, grad_rho=grho,
+                         loss_dev=loss_dev, want_loss=False)
+        for i in range(args.warmup):
+            dstep(i)
+        torch.cuda.synchronize()
+        dist.barrier()
+        td = torch.tensor([_time_steps(lambda i: dstep(args.warmup + i), args.steps, stream, flush)],
+                          dtype=torch.float64, device=dev)
+        dist.all_reduce(td, op=dist.ReduceOp.MAX)
+        ms_d = float(td.item()) / args.steps
+        ddp = {"value": S * B / (ms_d / 1e3), "ms_per_step": ms_d, "unit": "sample·images/s",
+               "parallelism": f"data-sharded K1xG{world} (S_loc={S}, B_loc={Bd})",
+               "note": "the paper's DDP-style comparison (P:185-193, P:390-394), same library/kernels"}
+        cd.close()
 
     if rank == 0:
         peaks, peak_src = _peaks()
@@ -320,12 +388,14 @@ def run_ours(args, world, rank, local_rank):
                 "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
                 "config": {"workload": f"{args.config}: {WORKLOAD_NAMES[cfg['model']]}",
                            "global_batch": B, "samples": S, "samples_per_gpu": S_loc,
+                           "batch_per_gpu": B_loc,
                            "params": P, "parallelism": f"{plan['mode']}-sharded K{K}xG{G}",
                            "loss_aggregation": {"mean": "loss of the mean prediction (exact, PAPER.md:272-281)",
                                                 "gnll": "Gaussian NLL of the predictive mean/variance (P:349, P:281)",
                                                 "sample": "mean of per-sample losses (Alg. 1 l.9)"}[args.agg],
                            "optimizer": "fused Adam (in the timed step)" if adam else
                                         "none (step returns grad_mu, grad_rho; north_star boundary)",
+                           "init": "Kaiming mu, rho = softplus^-1(1/fan_in) (PAPER.md:148; DESIGN.md §5)",
                            "l2": "flushed between timed steps (256 MiB memset outside events)"},
                 "clocks": clk.summary(),
                 "e2e": {"value": e2e_value, "unit": "sample·images/s",
@@ -336,14 +406,15 @@ def run_ours(args, world, rank, local_rank):
                 "kernel_ms_per_step": {k: v["ms"] / prof_steps for k, v in prof.items()},
                 "kernel_ms_note": f"per kernel class, CUDA events around each launch, {prof_steps} extra "
                                   "untimed steps (profiling off in the timed region)"}
+        if ddp is not None:
+            line["ddp_comparison"] = ddp
         line["roofline"] = roofline(model, B_loc, S_loc, prof, prof_steps, peaks, peak_src)
         if world == 1 and not args.no_cpu_baseline:
-            r, cores, sample = cpu_oracle_rate(MODELS[cfg["model"]], B, D, budget_s=args.ref_budget,
+            r, cores, sample = cpu_oracle_rate(MODELS[cfg["model"]], B, args.ref_budget,
                                                aug=cfg.get("aug", "none"))
             line["cpu_baseline"] = {"value": r, "unit": "sample·images/s", "cores": cores,
                                     "kind": "oracle", "sample": sample}
         print(json.dumps(line), flush=True)
-    ctx.close()
     if distributed:
         dist.destroy_process_group()
 
@@ -386,6 +457,17 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
     if dom is None:
         return None
     ms = prof[dom]["ms"] / steps
+    if model["kind"] == "mlp" and model.get("method") == "mcd":
+        # C6 (MC dropout): weights μ, no ε drawn (R25); 96-128-128-24 at B = 256 is a few
+        # GFLOP per step, far below every roofline: latency-bound, reported with its tensor rate
+        w = model["widths"]
+        fl = {"fwd": 2 * B * S_loc * sum(w[i] * w[i + 1] for i in range(len(w) - 1)),
+              "dgrad": 2 * B * S_loc * sum(w[i] * w[i + 1] for i in range(1, len(w) - 1)),
+              "wgrad": 2 * B * S_loc * sum(w[i] * w[i + 1] for i in range(len(w) - 1))}
+        return {"kernel": dom, "ms_per_step": ms, "bound": "latency", "achieved": None, "peak": None,
+                "unit": None, "frac": None, "traffic": None,
+                "tensor_tflops": fl[dom] / (ms / 1e3) / 1e12,
+                "note": "MC dropout draws no eps (weights mu); tiny GEMMs: launch/latency-bound"}
     if model["kind"] == "mlp" and n_params(model) < 10000:
         # C1 (161 parameters, 78 KFLOP per step): launch/latency-bound, no roofline
         return {"kernel": dom, "ms_per_step": ms, "bound": "latency", "achieved": None, "peak": None,
@@ -455,18 +537,36 @@ def _ncu_traffic(kind, kernel):
     return None
 
 
+def _spawn(args_list, n):
+    """Re-execute this script under torchrun with n ranks (one per GPU) on 127.0.0.1."""
+    import socket
+    import torch
+    if torch.cuda.device_count() < n:
+        print(f"bench.py: --gpus {n} but only {torch.cuda.device_count()} GPU(s) visible", file=sys.stderr)
+        sys.exit(2)
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + args_list
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "C6"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5", "C6"])
     ap.add_argument("--mode", default=None, choices=["sample", "data"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--sample-chunk", type=int, default=0,
+                    help="samples per pass through the network (0: the library default, all local samples)")
     ap.add_argument("--ref-budget", type=float, default=None,
-                    help="seconds of oracle CPU work per reference step (default: 150 s / (K+W))")
+                    help="seconds of oracle CPU work per reference step (default: 150 s / (K+W), ≤ 15 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ddp", action="store_true", help="skip the data-sharded comparison line (N > 1)")
     ap.add_argument("--agg", default="sample", choices=["sample", "mean", "gnll"],
                     help="mean: exact aggregation, the loss of the mean prediction; gnll: Gaussian "
                          "NLL of the predictive mean and variance (C1, --precision fp32)")
@@ -474,8 +574,14 @@ def main():
                     help="adam: each step also applies the fused Adam update (bnn_elbo_step_adam)")
     args = ap.parse_args()
     world, rank, local_rank = _env_world()
-    if args.gpus != world and world != 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _spawn(sys.argv[1:], args.gpus)
+    if args.gpus != world:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.warmup < 3:
+        print("bench.py: --warmup must be >= 3", file=sys.stderr)
+        sys.exit(2)
     if args.ref_budget is None:
         args.ref_budget = min(15.0, max(1.0, 150.0 / (args.steps + args.warmup)))
     if args.impl == "reference":

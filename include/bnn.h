@@ -63,7 +63,7 @@ enum { BNN_MODEL_MLP = 0, BNN_MODEL_RESNET18 = 1 };
  * class probabilities over the S samples, MSE of the mean output. The mean
  * needs every sample group's statistic before any backward: bnn_elbo_step exchanges it with
  * one extra allgather between forward and backward; virtual ranks use bnn_mean_stats +
- * bnn_elbo_partial_mean. MLP models only (BNN_ERR_CONFIG otherwise). */
+ * bnn_elbo_partial_mean. MLP and ResNet models, both precisions. */
 /* BNN_LOSS_GNLL_MEAN: Gaussian NLL of the predictive distribution, the two-parameter case of
  * P:281 ("Gaussian negative log-likelihood"; mean and population variance of the S
  * predictions per output, variance floor 1e-6, R24): fp32 targets [B, outputs];
@@ -110,7 +110,11 @@ typedef struct bnn_config {
     const uint8_t* nccl_uid;  /* 128-byte id from bnn_get_unique_id on rank 0 (broadcast by the
                                  caller), or NULL: no communicator. With NULL and world > 1 the
                                  context is a "virtual rank": use bnn_elbo_partial/bnn_finalize. */
-    int32_t max_B_loc;        /* largest per-rank batch a step will pass */
+    int32_t max_B_loc;        /* largest per-rank batch a step will pass. FP32 contexts and BF16
+                                 MLP contexts accept any 0 < B_loc <= max_B_loc per step (the BF16
+                                 MLP re-encodes its TMA descriptors on the host when B_loc changes);
+                                 BF16 ResNet contexts lay out descriptors, scratch splits and grids
+                                 for max_B_loc and require B_loc == max_B_loc (BNN_ERR_CONFIG) */
     int32_t max_S_loc;        /* largest per-rank sample count a step will use */
     int32_t sample_chunk;     /* samples processed together (0 = all local samples) */
     int32_t aug;              /* BNN_AUG_NONE | BNN_AUG_PER_SAMPLE (images only; docs/EPS.md §4) */

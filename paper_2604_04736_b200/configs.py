@@ -42,35 +42,37 @@ def layout(model: dict) -> list[dict]:
 
     Each layer contributes a weight tensor t=2l viewed as [rows=c_out, cols=k·k·c_in]
     (OHWI, c_in fastest) and a bias tensor t=2l+1 viewed as [1, c_out]. Returned dicts
-    carry t, offset, rows, cols and the layer's fan-in (used only by the initialiser).
+    carry t, offset, rows, cols, the layer's fan-in and its role ("hidden"/"out" for the MLP;
+    "stem", "c1"/"c2" (first/second conv of a BasicBlock), "proj", "out" for the ResNet) — the
+    last two are used only by the initialiser.
     """
-    layers = []  # (cin, cout, k)
+    layers = []  # (cin, cout, k, role)
     if model["kind"] == "mlp":
         w = model["widths"]
         for i in range(1, len(w)):
-            layers.append((w[i - 1], w[i], 1))
+            layers.append((w[i - 1], w[i], 1, "hidden" if i < len(w) - 1 else "out"))
     elif model["kind"] == "resnet18":
         b = model.get("base_width", 64)
-        layers.append((model["in_c"], b, 3))
+        layers.append((model["in_c"], b, 3, "stem"))
         width = b
         for stage in range(4):
             cout = b << stage
             for blk in range(2):
                 stride = 2 if (stage > 0 and blk == 0) else 1
-                layers.append((width, cout, 3))
-                layers.append((cout, cout, 3))
+                layers.append((width, cout, 3, "c1"))
+                layers.append((cout, cout, 3, "c2"))
                 if stride != 1 or width != cout:
-                    layers.append((width, cout, 1))
+                    layers.append((width, cout, 1, "proj"))
                 width = cout
-        layers.append((width, model["n_classes"], 1))
+        layers.append((width, model["n_classes"], 1, "out"))
     else:
         raise ValueError(model["kind"])
     out, off = [], 0
-    for l, (cin, cout, k) in enumerate(layers):
+    for l, (cin, cout, k, role) in enumerate(layers):
         cols = k * k * cin
-        out.append(dict(t=2 * l, offset=off, rows=cout, cols=cols, fan_in=cols))
+        out.append(dict(t=2 * l, offset=off, rows=cout, cols=cols, fan_in=cols, role=role))
         off += cout * cols
-        out.append(dict(t=2 * l + 1, offset=off, rows=1, cols=cout, fan_in=cols))
+        out.append(dict(t=2 * l + 1, offset=off, rows=1, cols=cout, fan_in=cols, role=role))
         off += cout
     return out
 

@@ -193,6 +193,7 @@ struct bnn_ctx {
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
     // TMA descriptors (BF16)
     std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;
+    int map_B = 0;  // the B_loc the BF16 descriptors are encoded for
     // bookkeeping
     std::string err;
     int64_t launches = 0;

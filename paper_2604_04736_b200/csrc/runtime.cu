@@ -88,6 +88,30 @@ SampledLayer sampled(const bnn_ctx* c, int l, const float* mu) {
 
 namespace {
 
+// TMA descriptors of the BF16 MLP path for a batch of B rows per sample. The kernels store
+// activations and gradients with sample stride B·ld (the step's B_loc), so the descriptors are
+// re-encoded whenever a step's B_loc differs from the last one (host-side encode, no launch);
+// TMA zero-fills rows ≥ B, which the wgrad reduction over batch rows relies on.
+int mlp_encode_maps(bnn_ctx* c, int B) {
+    const int L = (int)c->layers.size();
+    const int Sc = c->chunk;
+    c->map_fwdB.resize(L);
+    c->map_dgradB.resize(L);
+    c->map_wgG.resize(L);
+    c->map_wgX.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const void* in = l == 0 ? c->xb : c->act[l];
+        const int depth = l == 0 ? 1 : Sc;
+        if (!make_map(&c->map_fwdB[l], in, c->widths[l], B, depth, c->ld[l], 256) ||
+            !make_map(&c->map_wgX[l], in, c->widths[l], B, depth, c->ld[l], 64) ||
+            !make_map(&c->map_dgradB[l], c->grad[l], c->widths[l + 1], B, Sc, c->ld[l + 1], 256) ||
+            !make_map(&c->map_wgG[l], c->grad[l], c->widths[l + 1], B, Sc, c->ld[l + 1], 64))
+            return c->set_err(BNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l);
+    }
+    c->map_B = B;
+    return BNN_OK;
+}
+
 int alloc_mlp(bnn_ctx* c) {
     const int L = (int)c->layers.size();
     const int B = c->B_max, Sc = c->chunk;
@@ -129,20 +153,7 @@ int alloc_mlp(bnn_ctx* c) {
         __nv_bfloat16* xb;
         if (!c->alloc(&xb, (size_t)B * c->ld[0])) return c->set_err(BNN_ERR_CUDA, "out of memory");
         c->xb = xb;
-        // TMA descriptors
-        c->map_fwdB.resize(L);
-        c->map_dgradB.resize(L);
-        c->map_wgG.resize(L);
-        c->map_wgX.resize(L);
-        for (int l = 0; l < L; ++l) {
-            const void* in = l == 0 ? c->xb : c->act[l];
-            const int depth = l == 0 ? 1 : Sc;
-            if (!make_map(&c->map_fwdB[l], in, c->widths[l], B, depth, c->ld[l], 256) ||
-                !make_map(&c->map_wgX[l], in, c->widths[l], B, depth, c->ld[l], 64) ||
-                !make_map(&c->map_dgradB[l], c->grad[l], c->widths[l + 1], B, Sc, c->ld[l + 1], 256) ||
-                !make_map(&c->map_wgG[l], c->grad[l], c->widths[l + 1], B, Sc, c->ld[l + 1], 64))
-                return c->set_err(BNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l);
-        }
+        return mlp_encode_maps(c, B);
     }
     return BNN_OK;
 }
@@ -497,6 +508,18 @@ int check_step_args(bnn_ctx* c, int B_loc, int B_glob, int S_glob) {
     if (S_glob / c->K > c->S_loc_max)
         return c->set_err(BNN_ERR_CONFIG, "S/K <= max_S_loc violated (%d > %d)", S_glob / c->K, c->S_loc_max);
     if (S_glob >= (1 << 20)) return c->set_err(BNN_ERR_CONFIG, "S < 2^20 (EPS-v1 counter) violated");
+    if (c->bf16 && B_loc != c->map_B) {
+        // the BF16 ResNet's descriptors, scratch splits and per-layer grids are laid out for
+        // max_B_loc in bnn_init; the MLP's descriptors are re-encoded for the new batch size
+        if (c->model.kind != BNN_MODEL_MLP)
+            return c->set_err(BNN_ERR_CONFIG,
+                              "BF16 ResNet: B_loc == max_B_loc required (B_loc=%d, max_B_loc=%d); "
+                              "create a context with max_B_loc = B_loc for a smaller batch", B_loc, c->B_max);
+        // the previous step's kernels read the old descriptors by value (kernel parameters),
+        // so re-encoding on the host does not race with work still in flight
+        int rc = mlp_encode_maps(c, B_loc);
+        if (rc) return rc;
+    }
     return BNN_OK;
 }
 

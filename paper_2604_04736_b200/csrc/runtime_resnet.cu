@@ -329,6 +329,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         !make_map(&c->map_dgradB[0], c->fcG, O, B, Sc, ldO, 256) ||
         !make_map(&c->map_wgG[0], c->fcG, O, B, Sc, ldO, 64))
         return c->set_err(BNN_ERR_CUDA, "tensor map (head) failed");
+    c->map_B = B;
     return BNN_OK;
 }
 

@@ -27,7 +27,12 @@ Two parameter regimes (reading R26):
   (1 ± 10 %)), σ = v/(2·fan_in) (the sampled noise comparable to the μ spread), biases
   μ = 0.2 + 0.01·U(0,1); the output layer is signed, μ ~ N(0, h²/fan_in) with h = 1 (MLP) or
   1/16 (CNN, whose features grow ×2 per residual block) so the logits are O(1); inputs
-  x ~ U(0.5, 1.5). CNN images should be ≥ 16×16: at 8×8 stage 4 is 1×1 and a 3×3 kernel sees
+  x ~ U(0.5, 1.5). A quarter of the units of every layer whose output goes only through a ReLU
+  into the next layer (MLP hidden layers; the CNN stem and the first conv of every BasicBlock)
+  have the mirrored sign (weights and bias × −1): their pre-activation is ≈ −(input mean) ×
+  (1 ± 10 %), firmly below 0, so the ReLU masks of the forward and of the dgrad epilogues are
+  exercised without near-ties (their inputs to the next layer are exact zeros, whose
+  pre-activations stay positive). CNN images should be ≥ 16×16: at 8×8 stage 4 is 1×1 and a 3×3 kernel sees
   only its centre tap (1/9 of the mean), which brings a few units back near 0. Every weight is still a distinct signed number,
   so a wrong index, tap, tile or operand changes the result by O(1) of the spread.
 """
@@ -45,30 +50,43 @@ def _softplus_inv(s: np.ndarray) -> np.ndarray:
     return np.log(np.expm1(s))
 
 
-def _positive_params(model: dict, seed: int):
+def _positive_params(model: dict, seed: int, off_frac: float = 0.25):
     rng = np.random.default_rng(seed)
     lay = layout(model)
     P = n_params(model)
     mu = np.empty(P, np.float64)
     rho = np.empty(P, np.float64)
-    last = len(lay) // 2 - 1
     # output-layer scale: features grow ×2 per residual block (both block inputs positive)
     head = 1.0 if model["kind"] == "mlp" else 1.0 / 16.0
+    off = {}  # layer → boolean row mask of the "off" units (pre-activation firmly < 0)
     for ti in lay:
         n = ti["rows"] * ti["cols"]
         sl = slice(ti["offset"], ti["offset"] + n)
         f = ti["fan_in"]
         layer = ti["t"] // 2
-        if ti["rows"] > 1 or model["kind"] == "mlp" and ti["t"] % 2 == 0:
-            if layer < last:
+        role = ti["role"]
+        if role in ("hidden", "stem", "c1") and layer not in off:
+            # a quarter of the units (rows) of every layer whose output feeds only a ReLU and
+            # then the next conv / linear (never a residual sum) get the mirrored sign
+            off[layer] = rng.uniform(0.0, 1.0, ti["rows"] if ti["t"] % 2 == 0 else ti["cols"]) < off_frac
+        sign = np.where(off[layer], -1.0, 1.0) if layer in off else None
+        if ti["t"] % 2 == 0:  # weight [rows = units, cols = fan-in]
+            if role != "out":
                 v = 0.1 * math.sqrt(f)
-                mu[sl] = (1.0 + v * rng.normal(0.0, 1.0, n)) / f
+                w = (1.0 + v * rng.normal(0.0, 1.0, (ti["rows"], ti["cols"]))) / f
+                if sign is not None:
+                    w *= sign[:, None]
+                mu[sl] = w.reshape(-1)
                 sig = 0.5 * v / f
             else:
                 mu[sl] = rng.normal(0.0, head / math.sqrt(f), n)
                 sig = 0.5 * head / math.sqrt(f)
-        else:  # bias
-            mu[sl] = 0.2 + 0.01 * rng.uniform(0.0, 1.0, n) if layer < last else 0.0
+        else:  # bias [units]
+            if role != "out":
+                b = 0.2 + 0.01 * rng.uniform(0.0, 1.0, n)
+                mu[sl] = b * sign if sign is not None else b
+            else:
+                mu[sl] = 0.0
             sig = 0.005
         rho[sl] = _softplus_inv(np.full(n, sig))
     return mu.astype(np.float32), rho.astype(np.float32)

@@ -13,7 +13,8 @@ tests/test_gpu_parity.py rest on:
   cause: the change grows like √(perturbation) (a count of decisions crossing 0, each a
   finite jump), and the same network with tanh (no decisions) moves by ≈ 1 %.
 * Positive regime (synth regime="positive"): every ReLU pre-activation is bounded away from 0
-  and the same rounding moves every tensor by < 1 %, so 2e-2 is a meaningful bar there.
+  (most units firmly on, a quarter of the stem / first-block-conv / MLP hidden units firmly
+  off) and the same rounding moves every tensor by < 1 %, so 2e-2 is a meaningful bar there.
 """
 import numpy as np
 import pytest
@@ -85,16 +86,39 @@ def test_positive_regime_cnn_is_well_conditioned(aug):
     wr = _partial(model, mu, rho, x, yc, yr, 2, aug=aug, emu="weights")
     assert max(_per_tensor(model, exact, wr)) < 1e-2
     # no ReLU decision near a tie: every stored layer output of every (sample, example) is
-    # ≥ 5 % of its layer mean (the projections, stored before the block's ReLU, included)
-    # conv layer l writes cout × (16 / 2^stage)² values, stage = log2(cout / 64)
-    couts = [ti["rows"] for ti in layout(model) if ti["t"] % 2 == 0][:-1]
+    # either ≥ 5 % of its layer mean (the projections, stored before the block's ReLU, included)
+    # or belongs to an "off" unit (negative bias, stem and first block convs), whose whole
+    # channel is 0 and stays exactly 0 when its bias is raised by 5 % of the layer mean, i.e.
+    # its pre-activation is below −5 % of the mean everywhere.
+    # conv layer l writes cout × (16 / 2^stage)² values (HWC), stage = log2(cout / 64)
+    lay = layout(model)
+    wts = [ti for ti in lay if ti["t"] % 2 == 0][:-1]
+    couts = [ti["rows"] for ti in wts]
     sizes = [c * (16 >> int(np.log2(c // 64))) ** 2 for c in couts]
     offs = np.concatenate([[0], np.cumsum(sizes)])
+    biases = {ti["t"] // 2: ti for ti in lay if ti["t"] % 2 == 1}
     for s, b in ((0, 0), (1, 2)):
         d = O.layer_dump(model, mu, rho, x, yc, yr, b, s, 0x5EED, 0, aug=aug)
+        raised = mu.copy()
+        n_off = 0
         for layer in range(len(couts)):
-            o = d[offs[layer]:offs[layer + 1]]
-            assert o.min() >= 0.05 * o.mean(), (s, b, layer, o.min(), o.mean())
+            o = d[offs[layer]:offs[layer + 1]].reshape(-1, couts[layer])
+            bt = biases[layer]
+            offmask = mu[bt["offset"]:bt["offset"] + bt["cols"]] < 0
+            on = o[:, ~offmask]
+            assert on.min() >= 0.05 * on.mean(), (s, b, layer, on.min(), on.mean())
+            if offmask.any():
+                assert wts[layer]["role"] in ("stem", "c1")
+                assert not o[:, offmask].any(), (s, b, layer)
+                raised[bt["offset"]:bt["offset"] + bt["cols"]][offmask] += 0.05 * on.mean()
+                n_off += int(offmask.sum())
+        assert n_off > 0
+        d2 = O.layer_dump(model, raised, rho, x, yc, yr, b, s, 0x5EED, 0, aug=aug)
+        for layer in range(len(couts)):
+            bt = biases[layer]
+            offmask = mu[bt["offset"]:bt["offset"] + bt["cols"]] < 0
+            o2 = d2[offs[layer]:offs[layer + 1]].reshape(-1, couts[layer])
+            assert not o2[:, offmask].any(), (s, b, layer)
 
 
 @pytest.mark.parametrize("model,B,S", [
