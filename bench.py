@@ -310,6 +310,13 @@ def run_ours(args, world, rank, local_rank):
     launches = ctx.launch_count() - launches0
     if distributed:
         dist.barrier()
+    if args.profile_run:  # under ncu: the timed steps only (their numbers are not bench values)
+        ctx.close()
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "launches": int(launches), "steps": args.steps}), flush=True)
+        if distributed:
+            dist.destroy_process_group()
+        return
     # per-kernel-class timing (the roofline line) in separate, untimed steps: the class events
     # the library records around its launches would otherwise sit inside the timed region
     prof_steps = max(3, min(args.steps, 10))
@@ -566,6 +573,9 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=None,
                     help="seconds of oracle CPU work per reference step (default: 150 s / (K+W), ≤ 15 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-run", action="store_true",
+                    help="for ncu launch lists: warm-up + timed steps only, no e2e / class profiling / "
+                         "CPU baseline; prints no bench line")
     ap.add_argument("--no-ddp", action="store_true", help="skip the data-sharded comparison line (N > 1)")
     ap.add_argument("--agg", default="sample", choices=["sample", "mean", "gnll"],
                     help="mean: exact aggregation, the loss of the mean prediction; gnll: Gaussian "
@@ -579,7 +589,7 @@ def main():
     if args.gpus != world:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         sys.exit(2)
-    if args.warmup < 3:
+    if args.warmup < 3 and not args.profile_run:
         print("bench.py: --warmup must be >= 3", file=sys.stderr)
         sys.exit(2)
     if args.ref_budget is None:
