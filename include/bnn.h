@@ -46,7 +46,8 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 2  /* 2: bnn_model_desc.method / .dropout_p (MC dropout), Adam, mean-aggregation entry points */
+#define BNN_ABI_VERSION 3  /* 3: bnn_config.comm_timeout_ms, bnn_sync (non-blocking communicator, bucketed exchange);
+                              2: bnn_model_desc.method / .dropout_p (MC dropout), Adam, mean-aggregation entry points */
 
 typedef enum {
     BNN_OK = 0,
@@ -121,6 +122,12 @@ typedef struct bnn_config {
     double dataset_size;      /* |D| of PAPER.md:164, > 0 */
     int32_t device;           /* CUDA device ordinal */
     void* stream;             /* cudaStream_t; NULL = the legacy default stream */
+    int32_t comm_timeout_ms;  /* > 0: a collective (or the communicator's init) that has not
+                                 completed after this long, or an NCCL async error, aborts the
+                                 communicator (ncclCommAbort) and the call returns BNN_ERR_COMM
+                                 (SPEC.md:397, :733). 0: env BNN_COMM_TIMEOUT_MS, else 600000.
+                                 Checked wherever the library waits on the host: bnn_init, the
+                                 loss read of bnn_elbo_step*, bnn_sync. */
 } bnn_config;
 
 typedef struct bnn_tensor_info {
@@ -286,6 +293,16 @@ int bnn_debug_layer_output(bnn_ctx* ctx, int32_t layer, int32_t which, float* ou
 int64_t bnn_launch_count(bnn_ctx* ctx);
 
 /* Message for the last error on ctx (or the last context-free error if ctx is NULL). */
+/* Wait on the host until everything enqueued on the context's stream (and its comm stream)
+ * has completed, polling the communicator: a failed or silent peer returns BNN_ERR_COMM after
+ * comm_timeout_ms (the communicator is aborted; bnn_destroy is the only valid call after it),
+ * a CUDA error BNN_ERR_CUDA. Without a communicator: cudaStreamSynchronize. */
+int bnn_sync(bnn_ctx* ctx);
+
+/* Diagnostic: the number of NCCL groups (layer buckets, the tail with L_data included) the
+ * last bnn_elbo_step* exchange issued; 0 without a communicator. */
+int32_t bnn_comm_buckets(bnn_ctx* ctx);
+
 const char* bnn_last_error(bnn_ctx* ctx);
 
 void bnn_destroy(bnn_ctx* ctx);

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -13,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../../include/bnn.h"
@@ -134,6 +136,16 @@ struct bnn_ctx {
     cudaStream_t side2 = nullptr;
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     ncclComm_t comm = nullptr;
+    // gradient exchange (comm.cu): non-blocking communicator, comm stream, layer buckets
+    cudaStream_t comm_st = nullptr;
+    cudaEvent_t ev_comm_in = nullptr, ev_comm_out = nullptr;
+    double comm_timeout_ms = 600000.0;
+    bool comm_aborted = false;
+    int64_t ar_bucket_bytes = 16 << 20;
+    bool ar_enabled = false, ar_live = false, ar_live_used = false;
+    int ar_top = -1, ar_buckets = 0;
+    std::vector<char> ar_done;
+    std::vector<std::array<cudaEvent_t, 2>> ar_ev;
     // workspace
     float* sigma = nullptr;
     float* acc = nullptr;
@@ -272,6 +284,16 @@ struct bnn_ctx {
     }
 };
 
+// NVTX range of one host-side phase (header-only NVTX v3: a no-op unless a tool such as
+// nsys / ncu --nvtx is attached). Names: bnn.step, bnn.partial, bnn.chunk, bnn.forward,
+// bnn.backward, bnn.exchange, bnn.finalize, bnn.predict.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Side-stream fork/join: work enqueued on the returned stream after fork_side() runs
 // concurrently with what follows on c->st until join_side(). While profiling, everything
 // stays on c->st (class timing needs a single stream).
@@ -306,6 +328,15 @@ inline cudaStream_t fork_side2(bnn_ctx* c) {
 //   kPhaseStats   forward + the mean-prediction statistic only
 //   kPhaseMeanBwd (forward unless skip_fwd,) mean-prediction loss head from gstats, backward
 enum { kPhaseFull = 0, kPhaseStats = 1, kPhaseMeanBwd = 2 };
+
+// gradient exchange (comm.cu)
+int comm_init(bnn_ctx* c, const uint8_t* uid, int world, int rank);
+int comm_check(bnn_ctx* c, ncclResult_t r, const char* what);
+int comm_sync(bnn_ctx* c, cudaStream_t st);
+void comm_destroy(bnn_ctx* c);
+void ar_begin(bnn_ctx* c);
+int ar_layer_done(bnn_ctx* c, int l, cudaStream_t w0, cudaStream_t w1);
+int ar_finish(bnn_ctx* c, cudaStream_t st);
 
 // ResNet entry points (runtime_resnet.cu)
 int alloc_resnet_bf16(bnn_ctx* c);

@@ -164,6 +164,7 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
               const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
               uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss,
               int phase = kPhaseFull, bool skip_fwd = false, const float* gstats = nullptr) {
+    NvtxRange nvtx_("bnn.chunk");
     const int L = (int)c->layers.size();
     cudaStream_t st = c->st;
     SampleKeys kk{make_key(seed), step, s0};
@@ -544,6 +545,7 @@ int any_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
 int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
                 const float* yreg, int B_loc, int B_glob, int S_glob, uint64_t seed, uint32_t step,
                 float* acc, const float* gstats_in = nullptr, float* stats_out = nullptr) {
+    NvtxRange nvtx_("bnn.partial");
     int rc = check_step_args(c, B_loc, B_glob, S_glob);
     if (rc) return rc;
     if (c->model.loss == BNN_LOSS_CE && !ycls) return c->set_err(BNN_ERR_CONFIG, "CE loss needs int32 labels");
@@ -590,7 +592,9 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
                 // Σ over the K sample groups of this data group, in rank order (PAPER.md:281
                 // "additional communication"); one allgather, then a deterministic merge
                 const int64_t n = (int64_t)B_loc * c->stat_w;
-                NCCL_TRY(c, ncclAllGather(c->mstats, c->mgather, (size_t)n, ncclFloat32, c->comm, st));
+                rc = comm_check(c, ncclAllGather(c->mstats, c->mgather, (size_t)n, ncclFloat32, c->comm, st),
+                                "ncclAllGather(mean statistic)");
+                if (rc) return rc;
                 c->launch("loss", [&] { launch_mean_merge(c->mgather, c->cfg.world, c->G, c->gidx, n, c->mstats_g, c->gnll ? c->O : 0, S_loc, st); });
                 gstats = c->mstats_g;
             } else {
@@ -602,8 +606,11 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
         for (int s = 0; s < S_loc; s += c->chunk) {
             const int Sc = std::min(c->chunk, S_loc - s);
             const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
+            c->ar_live = c->ar_enabled && s + Sc >= S_loc;  // acc segments final in the last chunk
+            c->ar_live_used |= c->ar_live;
             rc = any_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl,
                            kPhaseMeanBwd, single && !gstats_in, gstats);
+            c->ar_live = false;
             if (rc) return rc;
         }
         if (c->kidx == 0) {  // the data loss counts each example once: sample group 0 adds it
@@ -618,12 +625,15 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
     for (int s = 0; s < S_loc; s += c->chunk) {
         const int Sc = std::min(c->chunk, S_loc - s);
         const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
+        c->ar_live = c->ar_enabled && s + Sc >= S_loc;  // acc segments final in the last chunk
+        c->ar_live_used |= c->ar_live;
         if (c->model.kind == BNN_MODEL_MLP)
             rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
         else if (c->bf16)
             rc = resnet_bf16_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
         else
             rc = resnet_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
+        c->ar_live = false;
         if (rc) return rc;
     }
     CUDA_TRY(c, cudaGetLastError());
@@ -632,6 +642,7 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
 
 int run_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc, float* loss_dev,
                  float* gmu, float* grho) {
+    NvtxRange nvtx_("bnn.finalize");
     cudaStream_t st = c->st;
     c->launch("finalize", [&] {
         launch_finalize(c->mcd, mu, rho, acc, acc + c->P_pad, acc + 2 * c->P_pad, c->P, c->cfg.dataset_size,
@@ -645,7 +656,8 @@ int run_finalize(bnn_ctx* c, const float* mu, const float* rho, const float* acc
 int read_loss(bnn_ctx* c, double* loss_host) {
     float h = 0.f;
     CUDA_TRY(c, cudaMemcpyAsync(&h, c->lossbuf, sizeof(float), cudaMemcpyDeviceToHost, c->st));
-    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    int rc = comm_sync(c, c->st);  // polls the communicator: a dead peer is BNN_ERR_COMM, not a hang
+    if (rc) return rc;
     *loss_host = h;
     if (!std::isfinite(h)) return c->set_err(BNN_ERR_NUMERIC, "non-finite loss %f", (double)h);
     return BNN_OK;
@@ -780,10 +792,10 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
     }
     // ---- communicator
     if (cfg->nccl_uid) {  // also for world == 1 (exercises the NCCL path on one GPU)
-        ncclUniqueId id;
-        memcpy(&id, cfg->nccl_uid, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&c->comm, cfg->world, id, cfg->rank);
-        if (r != ncclSuccess) return fail(c->set_err(BNN_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+        if (cfg->comm_timeout_ms > 0) c->comm_timeout_ms = cfg->comm_timeout_ms;
+        else if (const char* e = getenv("BNN_COMM_TIMEOUT_MS")) c->comm_timeout_ms = atof(e);
+        rc = comm_init(c, cfg->nccl_uid, cfg->world, cfg->rank);
+        if (rc) return fail(rc);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) return fail(c->set_err(BNN_ERR_CUDA, "init sync failed"));
     *out = c;
@@ -878,7 +890,14 @@ int run_reduced(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
                 uint32_t step) {
     if (c->cfg.world > 1 && !c->comm)
         return c->set_err(BNN_ERR_CONFIG, "world > 1 without a communicator: use bnn_elbo_partial + bnn_finalize");
+    if (c->comm) {
+        // bucketed exchange: the ResNet backward reduces each finished bucket of layers on the
+        // comm stream (ar_layer_done); the tail and L_data follow (ar_finish)
+        ar_begin(c);
+        c->ar_enabled = c->model.kind != BNN_MODEL_MLP && c->bf16;
+    }
     int rc = run_partial(c, mu, rho, x, ycls, yreg, B_loc, B_global, S_global, seed, step, c->acc);
+    c->ar_enabled = false;
     if (rc) return rc;
     if (c->comm) {
         int cls = -1;
@@ -896,7 +915,10 @@ int run_reduced(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
             b = c->ev_pool[c->ev_next++];
             cudaEventRecord(a, c->st);
         }
-        NCCL_TRY(c, ncclAllReduce(c->acc, c->acc, (size_t)(2 * c->P_pad + 1), ncclFloat32, ncclSum, c->comm, c->st));
+        NvtxRange nv("bnn.exchange");
+        rc = ar_finish(c, c->st);
+        c->ar_live_used = false;
+        if (rc) return rc;
         if (c->prof) {
             cudaEventRecord(b, c->st);
             c->pending.push_back({cls, {a, b}});
@@ -924,6 +946,7 @@ int check_adam(bnn_ctx* c, const bnn_adam* h, AdamHyper* out) {
 int run_finalize_adam(bnn_ctx* c, float* mu, float* rho, const float* acc, const bnn_adam* hp,
                       float* m_mu, float* v_mu, float* m_rho, float* v_rho, float* loss_dev,
                       float* gmu, float* grho) {
+    NvtxRange nvtx_("bnn.finalize");
     if (c->mcd) return c->set_err(BNN_ERR_CONFIG, "the fused Adam step is for BNN_METHOD_VI models");
     AdamHyper h;
     int rc = check_adam(c, hp, &h);
@@ -943,6 +966,7 @@ int run_finalize_adam(bnn_ctx* c, float* mu, float* rho, const float* acc, const
 int bnn_elbo_step(bnn_ctx* c, const float* mu, const float* rho, const float* x, const int32_t* ycls,
                   const float* yreg, int32_t B_loc, int32_t B_global, int32_t S_global, uint64_t seed,
                   uint32_t step, float* loss_dev, double* loss_host, float* gmu, float* grho) {
+    NvtxRange nvtx_("bnn.step");
     if (!c || !mu || !rho || !x || !gmu || !grho) {
         if (c) return c->set_err(BNN_ERR_CONFIG, "null tensor argument");
         return BNN_ERR_CONFIG;
@@ -998,6 +1022,7 @@ int bnn_elbo_step_host(bnn_ctx* c, const float* mu, const float* rho, const floa
 
 int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, int32_t B, int32_t S_global,
                 uint64_t seed, uint32_t step, float* mean, float* var) {
+    NvtxRange nvtx_("bnn.predict");
     if (!c || !mu || !rho || !x || !mean || !var) return BNN_ERR_CONFIG;
     if (c->G != 1) return c->set_err(BNN_ERR_CONFIG, "predict is sample-sharded only (G == 1)");
     int rc = check_step_args(c, B, B * c->G, S_global);
@@ -1053,10 +1078,11 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
     c->launch("predict", [&] { launch_predict_stats(logits, S_loc, B, c->O, c->model.loss, c->p_mean, c->p_m2, st); });
     const int R = c->cfg.world;
     if (c->comm && R > 1) {
-        NCCL_TRY(c, ncclGroupStart());
-        NCCL_TRY(c, ncclAllGather(c->p_mean, c->g_means, BO, ncclFloat32, c->comm, st));
-        NCCL_TRY(c, ncclAllGather(c->p_m2, c->g_m2s, BO, ncclFloat32, c->comm, st));
-        NCCL_TRY(c, ncclGroupEnd());
+        if ((rc = comm_check(c, ncclGroupStart(), "ncclGroupStart")) ||
+            (rc = comm_check(c, ncclAllGather(c->p_mean, c->g_means, BO, ncclFloat32, c->comm, st), "ncclAllGather(mean)")) ||
+            (rc = comm_check(c, ncclAllGather(c->p_m2, c->g_m2s, BO, ncclFloat32, c->comm, st), "ncclAllGather(M2)")) ||
+            (rc = comm_check(c, ncclGroupEnd(), "ncclGroupEnd")))
+            return rc;
     } else if (R > 1) {
         return c->set_err(BNN_ERR_CONFIG, "predict with world > 1 needs a communicator");
     } else {
@@ -1165,12 +1191,19 @@ int bnn_debug_layer_output(bnn_ctx* c, int32_t layer, int32_t which, float* out,
     return c->set_err(BNN_ERR_CONFIG, "no such layer");
 }
 
+int32_t bnn_comm_buckets(bnn_ctx* c) { return c ? c->ar_buckets : 0; }
+
+int bnn_sync(bnn_ctx* c) {
+    if (!c) return BNN_ERR_CONFIG;
+    return comm_sync(c, c->st);
+}
+
 const char* bnn_last_error(bnn_ctx* c) { return c ? c->err.c_str() : g_last_error.c_str(); }
 
 void bnn_destroy(bnn_ctx* c) {
     if (!c) return;
     if (!c->allocs.empty()) cudaStreamSynchronize(c->st);
-    if (c->comm) ncclCommDestroy(c->comm);
+    comm_destroy(c);
     for (void* p : c->allocs) cudaFree(p);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     for (cudaStream_t q : {c->side, c->side2, c->side3})

@@ -429,12 +429,17 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
                       const float* yreg, int B, int B_glob, int S_glob, int Sc, uint32_t s0,
                       uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss,
                       int phase, bool skip_fwd, const float* gstats) {
+    NvtxRange nvtx_("bnn.chunk");
     cudaStream_t st = c->st;
     SampleKeys kk{make_key(seed), step, s0};
     const float scale = c->model.loss == BNN_LOSS_CE ? 1.0f / ((float)S_glob * B_glob)
                                                      : 1.0f / ((float)S_glob * B_glob * c->O);
     const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
-    if (!skip_fwd) resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug);
+    if (!skip_fwd) {
+        NvtxRange nv("bnn.forward");
+        resnet_bf16_forward(c, mu, x, Sc, B, seed, step, s0, aug);
+    }
+    NvtxRange nvb("bnn.backward");
     const RBuf& in = c->rbufs[0];
     const int64_t in_stride = aug ? (int64_t)B * in.H * in.W * c->rbf[0].C_pad : 0;
     const int O = c->O, ldO = (int)round_up(O, 8);
@@ -500,6 +505,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         a.dbpart = nullptr;
         a.vec_ok = (sl.K % 4 == 0 && sl.off_w % 4 == 0) ? 1 : 0;
         c->launch("dgrad", [&] { launch_gen_gemm(c->map_dgradB[0], a, Sc, st); });
+        int rc = ar_layer_done(c, fc.layer, ss, sb);  // the head's acc segments: bucket candidate
+        if (rc) return rc;
     }
     // ---------------- GAP backward (+ ReLU mask of the last block output, bias partials)
     {
@@ -588,6 +595,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             }
             if (split3) cudaEventRecord(c->ev_comb[wbuf], sc);
             wbuf ^= 1;
+            int rc = ar_layer_done(c, op.layer, sc, sb);  // acc_μ/acc_ρ of this layer final (last chunk)
+            if (rc) return rc;
         } else {
             ConvShape cs{B, Sb.H, Sb.W, Sb.C, Db.H, Db.W, Db.C, Ld.k, Ld.stride, Ld.pad};
             const int nsp = c->nsplit[op.layer];
@@ -602,6 +611,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             c->launch("wgrad", [&] { launch_wgrad_split_reduce(wp, nsp, n, Ld.off_w, acc_mu, acc_rho, ss); });
             if (split3) cudaEventRecord(c->ev_comb[wbuf], ss);
             wbuf ^= 1;
+            int rc = ar_layer_done(c, op.layer, ss, sb);
+            if (rc) return rc;
         }
         // identity residual: dL/dy flows unchanged into the block input
         if (op.res >= 0 && !is_proj_output(c, op.res)) {

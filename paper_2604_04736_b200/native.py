@@ -36,7 +36,7 @@ class BnnConfig(C.Structure):
                 ("G", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_uid", C.c_void_p), ("max_B_loc", C.c_int32), ("max_S_loc", C.c_int32),
                 ("sample_chunk", C.c_int32), ("aug", C.c_int32), ("dataset_size", C.c_double),
-                ("device", C.c_int32), ("stream", C.c_void_p)]
+                ("device", C.c_int32), ("stream", C.c_void_p), ("comm_timeout_ms", C.c_int32)]
 
 
 class BnnTensorInfo(C.Structure):
@@ -73,6 +73,8 @@ def lib():
     L.bnn_elbo_step_host.argtypes = step_args + [vp, vp, vp]
     L.bnn_elbo_partial.argtypes = step_args + [vp]
     L.bnn_finalize.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.bnn_sync.argtypes = [vp]
+    L.bnn_comm_buckets.argtypes = [vp]
     L.bnn_mean_stats.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, u64, u32, vp]
     L.bnn_elbo_partial_mean.argtypes = step_args + [vp, vp]
     L.bnn_mean_merge.argtypes = [vp, vp, i32, i32, i32, vp]
@@ -144,7 +146,8 @@ class Context:
 
     def __init__(self, model: dict, *, precision="bf16", mode="sample", K=1, G=1, rank=0,
                  world=1, uid: bytes | None = None, max_B_loc=256, max_S_loc=64,
-                 sample_chunk=0, aug="none", dataset_size=60000.0, device=0, stream=None):
+                 sample_chunk=0, aug="none", dataset_size=60000.0, device=0, stream=None,
+                 comm_timeout_ms=0):
         self.model = model
         self._L = lib()
         self._desc = model_desc(model)
@@ -157,6 +160,7 @@ class Context:
             cfg.nccl_uid = C.addressof(self._uid)
         cfg.max_B_loc, cfg.max_S_loc, cfg.sample_chunk = max_B_loc, max_S_loc, sample_chunk
         cfg.aug, cfg.dataset_size, cfg.device = AUG[aug], float(dataset_size), device
+        cfg.comm_timeout_ms = comm_timeout_ms
         if stream is None:
             stream = torch.cuda.current_stream(device).cuda_stream
         cfg.stream = stream
@@ -304,6 +308,13 @@ class Context:
         n = C.c_int64()
         _check(self._L.bnn_debug_layer_output(self._h, layer, which, _p(out), cap, C.byref(n)), self._h)
         return out[:n.value].clone()
+
+    def sync(self):
+        """bnn_sync: host wait for the context's streams, polling the communicator."""
+        _check(self._L.bnn_sync(self._h), self._h)
+
+    def comm_buckets(self) -> int:
+        return int(self._L.bnn_comm_buckets(self._h))
 
     def launch_count(self) -> int:
         return int(self._L.bnn_launch_count(self._h))

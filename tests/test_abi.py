@@ -3,6 +3,7 @@ every entry point include/bnn.h declares; the Python binding mirrors the C struc
 import ctypes as C
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -31,13 +32,28 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
 
 
-def test_binding_struct_sizes_match_header():
+def test_binding_struct_sizes_match_header(tmp_path):
+    """The ctypes structs against the C compiler's layout of include/bnn.h: sizeof and the
+    offset of every field (a small C program compiled with gcc against the header)."""
     from paper_2604_04736_b200 import native
-    # bnn_model_desc: 2 + 16 + 5 + 1 int32, method int32, dropout_p float
-    assert C.sizeof(native.BnnModelDesc) == 4 * (2 + 16 + 6 + 2)
-    # bnn_config: 6 int32, ptr, 4 int32, double, int32 (+pad), ptr
-    assert C.sizeof(native.BnnConfig) == 24 + 8 + 16 + 8 + 8 + 8
-    assert C.sizeof(native.BnnTensorInfo) == 8 + 4 * 4
+    structs = {"bnn_model_desc": native.BnnModelDesc, "bnn_config": native.BnnConfig,
+               "bnn_tensor_info": native.BnnTensorInfo, "bnn_adam": native.BnnAdam}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "bnn.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)]).decode().split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l.strip()}
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
 
 
 def test_init_without_gpu_fails_loudly():

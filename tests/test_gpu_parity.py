@@ -977,3 +977,57 @@ def test_bf16_resnet_partial_batch_is_rejected():
     ctx = native.Context(model, precision="bf16", max_B_loc=4, max_S_loc=2, dataset_size=1.0)
     with pytest.raises(native.BnnError, match="B_loc == max_B_loc"):
         ctx.elbo_step(_dev(mu), _dev(rho), _dev(x[:3]), _dev(yc[:3]), 3, 2, 1, 0)
+
+
+# ------------------------------------------------------------------ gradient exchange (a7)
+@pytest.mark.parametrize("chunk", [0, 2])
+def test_cnn_bucketed_exchange_world1_equals_no_communicator(chunk, monkeypatch):
+    """The layer-bucketed allreduce on the comm stream (comm.cu): with a 0.25 MB bucket the
+    ResNet exchange is split into many NCCL groups issued during the backward (last sample chunk
+    only when S_loc > chunk); on one GPU every allreduce is the identity, so loss and gradients
+    equal the no-communicator step bit for bit, and the stream ordering (comm stream waits for
+    each bucket's writers, the finalize waits for the comm stream) is exercised."""
+    native = _native()
+    monkeypatch.setenv("BNN_AR_BUCKET_MB", "0.25")
+    model = dict(BF16_CNN, in_h=16, in_w=16)
+    B, S = 3, 4
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    out = []
+    for uid in (None, native.get_unique_id()):
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=500.0, uid=uid,
+                             aug="per_sample", sample_chunk=chunk)
+        for step in (4, 5):  # two steps: the second one's acc zeroing must follow the first exchange
+            l, g, r = ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 3, step)
+        torch.cuda.synchronize()
+        out.append((l, g.cpu(), r.cpu(), ctx.comm_buckets()))
+        ctx.close()
+    assert out[0][3] == 0 and out[1][3] >= 6, out[1][3]
+    assert out[0][0] == out[1][0]
+    assert torch.equal(out[0][1], out[1][1]) and torch.equal(out[0][2], out[1][2])
+
+
+def test_comm_timeout_returns_err_comm():
+    """A communicator whose peer never joins (world 2, only rank 0 calls bnn_init) fails with
+    BNN_ERR_COMM after comm_timeout_ms instead of hanging. Run in a child
+    process so a hang cannot take the test session down."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, time; sys.path.insert(0, '.')\n"
+        "from paper_2604_04736_b200 import native\n"
+        "t0 = time.time()\n"
+        "try:\n"
+        "    native.Context(dict(kind='mlp', widths=[8, 16, 1], loss='mse'), precision='fp32', mode='sample',\n"
+        "                   K=2, rank=0, world=2, uid=native.get_unique_id(), max_B_loc=4, max_S_loc=2,\n"
+        "                   dataset_size=1.0, comm_timeout_ms=3000)\n"
+        "    print('NO-ERROR')\n"
+        "except native.BnnError as e:\n"
+        "    print('ERR', time.time() - t0, e)\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=120)
+    line = [l for l in r.stdout.splitlines() if l.startswith("ERR ")]  # NCCL may print its banner
+    assert line and "timeout" in line[0] and "BNN_ERR" not in line[0], (r.stdout, r.stderr[-2000:])
+    assert "libbnn error 3" in line[0], line[0]  # BNN_ERR_COMM
+    dt = float(line[0].split()[1])
+    assert 2.5 <= dt <= 60.0, dt
