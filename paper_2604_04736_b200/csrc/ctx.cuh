@@ -202,6 +202,8 @@ struct bnn_ctx {
     float* bias_scr = nullptr;                         // sampled conv biases [layer][S][512]
     std::vector<cudaEvent_t> wgen_ev;                  // per layer: W_s slot written (side stream)
     std::vector<char> tma_fwd, tma_dgrad, tma_wgrad;   // stride-1 layers use them
+    std::vector<CUtensorMap> cmap_hf, cmap_hd;  // conv3 HALO: 1-row (W + 2)-pixel boxes of the input / dY
+    std::vector<char> halo_fwd, halo_dgrad;
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
     // TMA descriptors (BF16)
     std::vector<CUtensorMap> map_fwdB, map_dgradB, map_wgG, map_wgX;

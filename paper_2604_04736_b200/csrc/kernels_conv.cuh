@@ -70,6 +70,8 @@ struct Conv2Args {
     uint32_t* mbits_out;       // fwd (relu): ReLU bitmask of the stored output, bit j of word
                                //   [pixel][c/32] = (stored bf16 of channel c > 0); or null
     const uint32_t* mbits;     // dgrad: bitmask of the layer input (replaces `mask` when set)
+    int halo;                  // conv3, stride-1 3×3, 64-channel B operand: padded-stream tiles with
+                               //   one halo window per tile (bmap = 1-row box of W + 2 pixels)
 };
 void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
 void launch_conv2_dgrad(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st);
@@ -80,6 +82,7 @@ int conv2_dgrad_parts(const Conv2Args& a);
 void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 int conv3_dgrad_parts(const Conv2Args& a);
+int conv3_halo_ok(int H, int W);
 
 
 struct ConvWgradArgs {

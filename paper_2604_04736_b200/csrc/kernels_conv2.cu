@@ -52,6 +52,11 @@ constexpr int kData = 216 * 1024;      // stages: as many (A 16 KB + B n_tile·1
 constexpr int kSmem = 1024 + kData + 512 + 1024;
 }  // namespace c2
 
+__host__ __device__ __forceinline__ int floor_div(int a, int b) {  // b > 0
+    const int q = a / b;
+    return (a % b != 0 && a < 0) ? q - 1 : q;
+}
+
 struct TileGeo {
     int s, cls, ptile, ntile;
 };
@@ -543,32 +548,63 @@ namespace c3 {
 constexpr int kEpiWarps = 8;
 constexpr int kGatherWarps = 4;
 constexpr int kThreads = (kEpiWarps + kGatherWarps + 2) * 32;
+// HALO variant: no gather warps (every operand arrives by TMA); 8 epilogue warps, 3 A stages,
+// two window stages, two 256-column TMEM accumulators, one CTA per SM. (Measured and reverted,
+// round 2: 16 epilogue warps, and two CTAs per SM with one window / accumulator each — both
+// slower; a thread = channel epilogue without the shared-memory transpose — 1.8× slower.)
+constexpr int kEpiWarpsH = 8;
+constexpr int kThreadsH = (kEpiWarpsH + 2) * 32;
+constexpr int kTransPitch = 33;  // floats per transposed row (conflict-free scalar stores and loads)
 constexpr int kStages = 3;  // pipeline depth is not the limiter (BNN_CONV_STAGES sweep, profiles/r01)
 constexpr int kAStage = 128 * 64 * 2;  // 16 KB weights (128 channel rows)
 constexpr int kBStage = 256 * 64 * 2;  // 32 KB pixel window (256 rows)
-constexpr int kTrans = kEpiWarps * 32 * 33 * 4;
+constexpr int kTrans = kEpiWarps * 32 * kTransPitch * 4;
+constexpr int kTransH = kEpiWarpsH * 32 * kTransPitch * 4;
+constexpr int kWin = kStages * kBStage / 2;  // HALO: two window stages in the B-stage region (48 KB each)
+constexpr int kStagesH = 3;                  // HALO: A stages
 constexpr int kSmem = 1024 + kStages * (kAStage + kBStage) + kTrans + 512 + 2048;
+constexpr int kSmemH = 1024 + kStagesH * kAStage + 2 * kWin + kTransH + 512 + 2 * kEpiWarpsH * 32 * 4;
+static_assert(kSmemH <= 227 * 1024, "conv3 halo shared memory");
 static_assert(kSmem <= 227 * 1024, "conv3 shared memory");
 }  // namespace c3
 
-template <int MODE>
-__global__ void __launch_bounds__(c3::kThreads, 1)
+// HALO (stride-1 3×3 convs with 64 input channels of the B operand): tiles are 256
+// consecutive pixels of the padded pixel stream — per image (H + 1) rows (the last one a zero
+// separator shared by neighbouring images) × (W + 2) columns (zero columns at both ends) — and
+// the CTA loads ONE window of whole padded rows around the tile per tile (≤ kWin bytes, one
+// 1-row TMA box per padded row with OOB zero fill). Every tap's B operand is the window at a
+// row offset dh·(W+2) + dw: SWIZZLE_128B is a function of the shared address, so a descriptor
+// may start at any 128-B row (scripts/halo_desc_test.cu, profiles/r02/halo_desc_test.txt).
+// L2→SM traffic per tile: one ≈ 48 KB window instead of nine 32 KB tap windows; the padded
+// rows / columns cost (H+1)(W+2)/(HW) − 1 = 9.6 % more MMA columns at 32×32.
+template <int MODE, bool HALO>
+__global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
     conv3_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
                  const Conv2Args a) {
     using namespace c3;
+    // HALO: the B stages become two window stages, so the 16 KB A (weight) stages can be deeper:
+    // the A loads are L2 hits but ~1–2 µs in flight, against ≈ 0.3 µs of MMAs per k-block
+    constexpr int NST = HALO ? kStagesH : kStages;
+    constexpr int NEPI = HALO ? kEpiWarpsH : kEpiWarps;     // epilogue warps 0 … NEPI-1
+    constexpr int NGATH = HALO ? 0 : kGatherWarps;          // gather warps (stride-2 / stem operands)
+    constexpr int WTMA = NEPI + NGATH, WMMA = WTMA + 1;     // the TMA and MMA warps
+    constexpr int NBUF = 2;                                 // TMEM accumulators of 256 columns
+    constexpr int NWIN = 2;                                 // HALO window stages
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
     // address space, so plain loads/stores through it compile to LDS/STS
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + kStages * kAStage;
-    float* trans = reinterpret_cast<float*>(sB + kStages * kBStage);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(trans) + kTrans);
+    uint8_t* sB = smem + NST * kAStage;
+    float* trans = reinterpret_cast<float*>(sB + (HALO ? NWIN * kWin : kStages * kBStage));  // B stages / HALO window
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(trans) + (HALO ? kTransH : kTrans));
     uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
-    uint64_t* tempty = bars + 2 * kStages + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    uint64_t* empty = bars + NST;
+    uint64_t* tfull = bars + 2 * NST;
+    uint64_t* tempty = bars + 2 * NST + 2;
+    uint64_t* wfull = bars + 2 * NST + 4;   // HALO: window stages (the sB region, 2 × kWin)
+    uint64_t* wempty = bars + 2 * NST + 6;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 8);
     int* staps = reinterpret_cast<int*>(tslot + 4);  // [4 classes][9 taps] + counts
     float* bred = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // [2][8 warps][32]
 
@@ -576,7 +612,9 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
     const int ncls = MODE == 1 ? a.stride * a.stride : 1;
     const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
     const int P = a.B * PH * PW;
-    const int ptiles = (P + 255) / 256;
+    // padded stream (HALO): PWp columns per row, PH + 1 rows per image
+    const int PWp = PW + 2, PHp = PH + 1;
+    const int ptiles = HALO ? (a.B * PHp * PWp + 255) / 256 : (P + 255) / 256;
     // 64-channel layers: TMEM rows 64-127 repeat rows 0-63 (the A tile is loaded twice), so all
     // eight epilogue warps have channels to work on (MMA cost is the same for any M ≤ 128)
     const bool dup = (MODE == 0 ? a.CO : a.C) <= 64;
@@ -586,13 +624,15 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
     const int cblocks = (a.CO + 63) / 64;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            mbar_init(&full[i], 1 + (a.tma_a ? 0 : kGatherWarps * 32));
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full[i], 1 + (a.tma_a ? 0 : NGATH * 32));
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], kEpiWarps);
+            mbar_init(&tempty[i], NEPI);
+            mbar_init(&wfull[i], 1);
+            mbar_init(&wempty[i], 1);
         }
         mbar_fence_init();
         for (int cl = 0; cl < ncls; ++cl) {
@@ -607,41 +647,57 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             staps[cl * 10 + 9] = cnt;
         }
     }
-    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, 512);
+    if (warp == WMMA) tmem_alloc(tslot, NBUF * 256);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
     auto nkb_of = [&](int cls) { return MODE == 0 ? a.K_pad / 64 : staps[cls * 10 + 9] * cblocks; };
 
-    if (warp == kEpiWarps + kGatherWarps) {
+    if (warp == WTMA) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             tma_prefetch_desc(&wmap);
             if (a.tma_a) tma_prefetch_desc(&bmap);
             const int cpb = a.C_pad >> 6;
-            int it = 0;
-            for (int t = blockIdx.x; t < T; t += gridDim.x) {
+            int it = 0, tl = 0;
+            for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
                 const int p0 = g.ptile * 256, m0 = g.ntile * 128;
                 const int img0 = p0 / (PH * PW), y0 = (p0 - img0 * PH * PW) / PW;
                 const int nkb = nkb_of(g.cls);
+                if (HALO) {  // the tile's window: padded rows rs … re, one TMA box per row
+                    const int ws = tl % NWIN;
+                    mbar_wait_role(&wempty[ws], ((tl / NWIN) & 1) ^ 1);
+                    const int rs = floor_div(p0 - PWp - 1, PWp), re = floor_div(p0 + 256 + PWp, PWp);
+                    uint8_t* win = sB + ws * kWin;
+                    if (a.dbg & 2) {
+                        mbar_arrive_expect_tx(&wfull[ws], 0);
+                    } else {
+                        mbar_arrive_expect_tx(&wfull[ws], (uint32_t)((re - rs + 1) * PWp * 128));
+                        for (int r = rs; r <= re; ++r) {
+                            const int b = floor_div(r, PHp), y = r - b * PHp;  // y == PH: separator (OOB: zeros)
+                            tma_load_5d(&bmap, &wfull[ws], win + (r - rs) * PWp * 128, 0, -1, y, b,
+                                        a.src_stride_s == 0 ? 0 : g.s);
+                        }
+                    }
+                }
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int st = it % kStages;
-                    const uint32_t ph = (it / kStages) & 1;
+                    const int st = it % NST;
+                    const uint32_t ph = (it / NST) & 1;
                     mbar_wait_role(&empty[st], ph ^ 1);
                     if (a.dbg & 2) {  // feed-rate experiment: no loads
                         mbar_arrive_expect_tx(&full[st], 0);
                         continue;
                     }
                     // A box: 128 weight rows, or 64 for a 64-channel layer (rows 64-127 then unused)
-                    mbar_arrive_expect_tx(&full[st], kAStage + (a.tma_a ? kBStage : 0));
+                    mbar_arrive_expect_tx(&full[st], kAStage + (a.tma_a && !HALO ? kBStage : 0));
                     uint8_t* dA = sA + st * kAStage;
                     uint8_t* dB = sB + st * kBStage;
                     if (MODE == 0) {
                         tma_load_3d(&wmap, &full[st], dA, kb * 64, m0, g.s);  // 128 rows, or 64 (dup)
                         if (dup) tma_load_3d(&wmap, &full[st], dA + 8192, kb * 64, m0, g.s);
-                        if (a.tma_a) {
+                        if (a.tma_a && !HALO) {
                             const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
                             tma_load_5d(&bmap, &full[st], dB, c0, kw - a.pad, a.stride * y0 + kh - a.pad, img0,
@@ -651,7 +707,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                         const int ti = kb / cblocks, tap = staps[g.cls * 10 + ti], cb = kb - ti * cblocks;
                         tma_load_5d(&wmap, &full[st], dA, 0, tap, cb * 64, m0 / 64, g.s);  // 2 ci blocks, or 1 (dup)
                         if (dup) tma_load_5d(&wmap, &full[st], dA + 8192, 0, tap, cb * 64, m0 / 64, g.s);
-                        if (a.tma_a) {
+                        if (a.tma_a && !HALO) {
                             const int kh = tap / a.k, kw = tap - kh * a.k;
                             const int ph = g.cls / a.stride, pw = g.cls - (g.cls / a.stride) * a.stride;
                             tma_load_5d(&bmap, &full[st], dB, cb * 64, (pw + a.pad - kw) / a.stride,
@@ -662,26 +718,36 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == kEpiWarps + kGatherWarps + 1) {
+    } else if (warp == WMMA) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t idesc = idesc_bf16(128, 256, MODE == 1 ? 1 : 0, 0);
             int it = 0, tl = 0;
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
-                const int buf = tl & 1;
-                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                const int buf = tl % NBUF;
+                mbar_wait_role(&tempty[buf], ((tl / NBUF) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 const int nkb = nkb_of(g.cls);
+                // HALO: row of the window where the tile's first pixel sits (tap (0, 0) offset)
+                const int ws = tl % NWIN;
+                const int wrow0 = HALO ? g.ptile * 256 - floor_div(g.ptile * 256 - PWp - 1, PWp) * PWp : 0;
+                if (HALO) mbar_wait_role(&wfull[ws], (tl / NWIN) & 1);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int st = it % kStages;
-                    const uint32_t ph = (it / kStages) & 1;
+                    const int st = it % NST;
+                    const uint32_t ph = (it / NST) & 1;
                     mbar_wait_role(&full[st], ph);
                     fence_proxy_async_smem();
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
-                    const uint32_t bBase = smem_u32(sB + st * kBStage);
+                    uint32_t bBase = smem_u32(sB + st * kBStage);
+                    if (HALO) {  // tap of this k-block (one 64-channel block per tap)
+                        const int tap = MODE == 0 ? kb : staps[g.cls * 10 + kb];
+                        const int kh = tap / 3, kw = tap - 3 * (tap / 3);
+                        const int dh = MODE == 0 ? kh - 1 : 1 - kh, dw = MODE == 0 ? kw - 1 : 1 - kw;
+                        bBase = smem_u32(sB + ws * kWin) + (uint32_t)(wrow0 + dh * PWp + dw) * 128u;
+                    }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint64_t ad = MODE == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
@@ -691,14 +757,15 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                     }
                     mma_commit(&empty[st]);
                 }
+                if (HALO) mma_commit(&wempty[ws]);  // the window is free once this tile's MMAs are done
                 mma_commit(&tfull[buf]);
             }
         }
         __syncwarp();
-    } else if (warp >= kEpiWarps) {
+    } else if (warp >= NEPI) {
         // ------------------------------------------------ gather producers (stride 2 / stem): 256 rows
-        if (!a.tma_a) {
-            const int gt = threadIdx.x - kEpiWarps * 32;  // pixel rows gt and gt + 128
+        if (!a.tma_a && !HALO) {
+            const int gt = threadIdx.x - NEPI * 32;  // pixel rows gt and gt + 128
             const int cpb = a.C_pad >> 6;
             int it = 0;
             for (int t = blockIdx.x; t < T; t += gridDim.x) {
@@ -718,8 +785,8 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 const __nv_bfloat16* src = a.src + g.s * a.src_stride_s;
                 const int nkb = nkb_of(g.cls);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int st = it % kStages;
-                    const uint32_t phs = (it / kStages) & 1;
+                    const int st = it % NST;
+                    const uint32_t phs = (it / NST) & 1;
                     mbar_wait(&empty[st], phs ^ 1);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -775,15 +842,17 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
         // (32 channels), a subset of the tile's eight 32-pixel chunks; each chunk is transposed
         // through shared memory so the thread = pixel NHWC row epilogue (epi_row32) applies.
         // 64-channel layers (dup): quadrants 2,3 repeat channels 0-63, so all 8 warps work.
-        float* tr = trans + warp * 32 * 33;
+        float* tr = trans + warp * 32 * kTransPitch;
         const int q = warp & 3;
         const int cg = dup ? (q & 1) : q;                                   // channel group
+        // the NEPI warps of each quadrant share its chunks: dup → 2·NEPI/8 warps per channel
+        // group over 8 chunks (8 warps: 2 chunks each; 16 warps: 1), else NEPI/4 warps per group
         const int c_first = dup ? ((q >> 1) + 2 * (warp >> 2)) : (warp >> 2);  // first chunk
-        const int c_step = dup ? 4 : 2;
+        const int c_step = dup ? NEPI / 2 : NEPI / 4;
         int tl = 0;
         for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
             const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
-            const int buf = tl & 1;
+            const int buf = tl % NBUF;
             const int nkb = nkb_of(g.cls);
             const int ch0 = g.ntile * 128 + 32 * cg;
             const bool active = ch0 < Mtot;
@@ -793,6 +862,11 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
             // pixel row of chunk c for this lane (thread = pixel after the transpose)
             auto row_of = [&](int c, bool& pv) -> int64_t {
                 const int pix = g.ptile * 256 + 32 * c + lane;
+                if (HALO) {  // padded stream → (image, row, column); pad columns / separator rows invalid
+                    const int r = pix / PWp, cx = pix - r * PWp, b = r / PHp, y = r - b * PHp;
+                    pv = b < a.B && y < PH && cx >= 1 && cx <= PW;
+                    return pv ? (((int64_t)b * PH + y) * PW + cx - 1) * Mtot : 0;
+                }
                 pv = pix < P;
                 if (!pv) return 0;
                 if (MODE == 0 || a.stride == 1) return (int64_t)pix * Mtot;
@@ -820,7 +894,7 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 if (MODE == 1 && a.mbits) x2 = __ldg(a.mbits + ((so + ro + ch0) >> 5));
             };
             load_ops(c_first, o1, o2);  // independent of the accumulator: in flight while the MMAs finish
-            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            mbar_wait(&tfull[buf], (tl / NBUF) & 1);
             tc_fence_after();
             for (int c = c_first; c < 8; c += c_step) {  // 32 pixels per chunk
                 float v[32];
@@ -834,10 +908,10 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 if (!active) continue;
                 // v[j] = channel (ch0 + lane) at pixel 32c + j (+ its bias)  →  tr[j][lane]
 #pragma unroll
-                for (int j = 0; j < 32; ++j) tr[j * 33 + lane] = v[j] + bias;
+                for (int j = 0; j < 32; ++j) tr[j * kTransPitch + lane] = v[j] + bias;
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = tr[lane * 33 + j];
+                for (int j = 0; j < 32; ++j) v[j] = tr[lane * kTransPitch + j];
                 __syncwarp();
                 bool pv;
                 const int64_t rowoff = row_of(c, pv);
@@ -846,12 +920,12 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
                 if (MODE == 1 && a.bpart) bsum += warp_transpose_sum(v, lane);
             }
             if (MODE == 1 && a.bpart) {  // combine the warps of each channel group in a fixed order
-                float* red = bred + (tl & 1) * 256;
+                float* red = bred + (tl & 1) * NEPI * 32;
                 red[warp * 32 + lane] = bsum;
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(NEPI * 32) : "memory");
                 if (active && warp < (dup ? 2 : 4)) {
                     float t2 = 0.0f;
-                    for (int w = cg; w < 8; w += (dup ? 2 : 4)) t2 += red[w * 32 + lane];
+                    for (int w = cg; w < NEPI; w += (dup ? 2 : 4)) t2 += red[w * 32 + lane];
                     a.bpart[(int64_t)g.s * a.bpart_stride_s + (int64_t)(g.cls * ptiles + g.ptile) * a.C + ch0 +
                             lane] = t2;
                 }
@@ -863,32 +937,49 @@ __global__ void __launch_bounds__(c3::kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == kEpiWarps + kGatherWarps + 1) {
+    if (warp == WMMA) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, NBUF * 256);
     }
 }
 
+int conv3_halo_ok(int H, int W) {  // the padded window of a 256-pixel tile fits one window stage
+    const int PWp = W + 2;
+    const int rows = (256 + 2 * PWp + 2 + PWp - 1) / PWp + 1;
+    return H >= 1 && rows * PWp * 128 <= c3::kWin ? 1 : 0;
+}
+
 int conv3_dgrad_parts(const Conv2Args& a) {
+    if (a.halo) return (a.B * (a.H + 1) * (a.W + 2) + 255) / 256;
     const int P = a.B * (a.H / a.stride) * (a.W / a.stride);
     return a.stride * a.stride * ((P + 255) / 256);
 }
 
-template <int MODE>
-static void launch_conv3(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+template <int MODE, bool HALO>
+static void launch_conv3_t(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(conv3_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, c3::kSmem);
+        cudaFuncSetAttribute(conv3_kernel<MODE, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             HALO ? c3::kSmemH : c3::kSmem);
         attr = true;
     }
     const int ncls = MODE == 1 ? a.stride * a.stride : 1;
     const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
-    const int P = a.B * PH * PW;
+    const int P = HALO ? a.B * (PH + 1) * (PW + 2) : a.B * PH * PW;
     const int Mtot = MODE == 0 ? a.CO : a.C;
     const int T = a.S * ncls * ((P + 255) / 256) * ((Mtot + 127) / 128);
     Conv2Args b = a;
     b.dbg = conv_debug();
-    conv3_kernel<MODE><<<std::min(T, kNumSMs), c3::kThreads, c3::kSmem, st>>>(wmap, bmap, b);
+    conv3_kernel<MODE, HALO><<<std::min(T, kNumSMs), HALO ? c3::kThreadsH : c3::kThreads,
+                               HALO ? c3::kSmemH : c3::kSmem, st>>>(wmap, bmap, b);
+}
+
+template <int MODE>
+static void launch_conv3(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+    if (a.halo)
+        launch_conv3_t<MODE, true>(wmap, bmap, a, st);
+    else
+        launch_conv3_t<MODE, false>(wmap, bmap, a, st);
 }
 
 void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {

@@ -221,6 +221,39 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->tma_dgrad[op.layer] = 1;
         }
     }
+    // conv3 HALO (stride-1 3×3 layers with 64-channel B operands, kernels_conv2.cu): one padded
+    // row (W + 2 pixels, OOB columns / rows zero-filled) per TMA box; BNN_CONV_HALO=0 disables
+    c->cmap_hf.resize(L);
+    c->cmap_hd.resize(L);
+    c->halo_fwd.assign(L, 0);
+    c->halo_dgrad.assign(L, 0);
+    const char* he = getenv("BNN_CONV_HALO");
+    const bool halo_on = !(he && atoi(he) == 0);
+    for (const ROp& op : c->rops) {
+        if (!halo_on || op.type != 0 || is_fc(c, op) || op.src == 0) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        if (Ld.stride != 1 || Ld.k != 3 || Ld.pad != 1 || !conv3_halo_ok(Db.H, Db.W)) continue;
+        const uint32_t box[5] = {64, (uint32_t)(Db.W + 2), 1, 1, 1};
+        if (c->rbf[op.src].C_pad == 64 && Db.C <= 128) {  // fwd: conv3 with a 64-channel input window
+            const uint64_t dims[5] = {64, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B, (uint64_t)Sc};
+            const uint64_t str[4] = {128, (uint64_t)Sb.W * 128, (uint64_t)Sb.H * Sb.W * 128,
+                                     (uint64_t)B * Sb.H * Sb.W * 128};
+            if (!make_map_nd(&c->cmap_hf[op.layer], c->rbf[op.src].val, 5, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (conv3 halo window) failed");
+            c->halo_fwd[op.layer] = 1;
+        }
+        if (Db.C == 64 && Sb.C <= 128 && Ld.cin % 64 == 0) {  // dgrad: conv3 over a 64-channel dY window
+            const int gb = grad_src_buffer(c, op.dst);
+            const uint64_t dims[5] = {64, (uint64_t)Db.W, (uint64_t)Db.H, (uint64_t)B, (uint64_t)Sc};
+            const uint64_t str[4] = {128, (uint64_t)Db.W * 128, (uint64_t)Db.H * Db.W * 128,
+                                     (uint64_t)B * Db.H * Db.W * 128};
+            if (!make_map_nd(&c->cmap_hd[op.layer], c->rbf[gb].grad, 5, dims, str, box))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (conv3 halo dY window) failed");
+            c->halo_dgrad[op.layer] = 1;
+        }
+    }
     // stride-2 forward: the input window of a 2-strided conv is a TMA box with element stride 2
     // in W and H (box = 2·extent raw elements, every other one loaded); conv3 256-pixel and
     // conv2 128-pixel tiles of the output grid
@@ -418,7 +451,9 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         a.mbits_out = op.relu ? c->rbf[op.dst].mbits : nullptr;
         if (Db.C <= 128) {  // channels on M, 256 pixels on N (full-width MMA)
             a.tma_a = c->tma_fwd[op.layer];
-            c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], c->cmap_bf[op.layer], a, st); });
+            a.halo = c->halo_fwd[op.layer];
+            const CUtensorMap& bm = a.halo ? c->cmap_hf[op.layer] : c->cmap_bf[op.layer];
+            c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], bm, a, st); });
         } else {
             c->launch("fwd", [&] { launch_conv2_fwd(c->cmap_a2f[op.layer], c->cmap_w2[op.layer], a, st); });
         }
@@ -645,6 +680,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         a.out_stride_s = (int64_t)B * Sb.H * Sb.W * Sb.C;
         const bool m_chan = Sb.C <= 128;  // conv3: channels on M, 256 pixels on N
         if (m_chan) a.tma_a = c->tma_dgrad[op.layer];
+        if (m_chan) a.halo = c->halo_dgrad[op.layer];
         if (final) {
             const int np = m_chan ? conv3_dgrad_parts(a) : conv2_dgrad_parts(a);
             a.addsrc = pending[op.src];
@@ -659,7 +695,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             c->rbf[op.src].nparts = np;
         }
         if (m_chan) {
-            c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], c->cmap_bd[op.layer], a, st); });
+            const CUtensorMap& bm = a.halo ? c->cmap_hd[op.layer] : c->cmap_bd[op.layer];
+            c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], bm, a, st); });
         } else {
             c->launch("dgrad", [&] { launch_conv2_dgrad(c->cmap_a2d[op.layer], c->cmap_wT[op.layer], a, st); });
         }
