@@ -36,8 +36,8 @@ def build():
 def lib():
     global _lib
     if _lib is None:
-        src = os.path.join(_HERE, "bnn_oracle.c")
-        if not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+        srcs = [os.path.join(_HERE, f) for f in ("bnn_oracle.c", "vit_oracle.c")]
+        if not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in srcs):
             build()
         _lib = C.CDLL(_LIB)
         _lib.orc_log24.restype = C.c_float
@@ -70,7 +70,86 @@ def lib():
         _lib.orc_adam.argtypes = [C.c_long] + [C.c_void_p] * 4 + [C.c_double] * 4 + [C.c_int]
         _lib.orc_predict.argtypes = [C.c_void_p] * 4 + [C.c_int] * 2 + [C.c_uint64, C.c_uint32,
                                                                          C.c_void_p, C.c_void_p]
+        # ViT (SURVEY §8(f) f3, vit_oracle.c)
+        _lib.orc_vit_n_params.restype = C.c_long
+        _lib.orc_vit_n_params.argtypes = [C.c_void_p]
+        _lib.orc_vit_n_tensors.argtypes = [C.c_void_p]
+        _lib.orc_vit_tensor_info.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        _lib.orc_vit_elbo_partial.argtypes = [C.c_void_p] * 5 + [C.c_int] * 6 + [
+            C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int]
+        _lib.orc_vit_forward.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32, C.c_int,
+                                                                             C.c_void_p]
+        _lib.orc_finalize_p.argtypes = [C.c_long] + [C.c_void_p] * 3 + [C.c_double] + [C.c_void_p] * 4
     return _lib
+
+
+# ---------------------------------------------------------------- Bayesian ViT (f3)
+class OrcVit(C.Structure):
+    _fields_ = [("in_h", C.c_int), ("in_w", C.c_int), ("in_c", C.c_int), ("patch", C.c_int),
+                ("dim", C.c_int), ("heads", C.c_int), ("depth", C.c_int), ("mlp", C.c_int),
+                ("n_classes", C.c_int)]
+
+
+def vit_struct(model: dict) -> OrcVit:
+    v = OrcVit()
+    for f, _ in OrcVit._fields_:
+        setattr(v, f, int(model[f]))
+    return v
+
+
+def vit_n_params(model) -> int:
+    return int(lib().orc_vit_n_params(C.byref(vit_struct(model))))
+
+
+def vit_tensor_infos(model):
+    v = vit_struct(model)
+    n = lib().orc_vit_n_tensors(C.byref(v))
+    out = []
+    for t in range(n):
+        info = np.zeros(3, np.int64)
+        assert lib().orc_vit_tensor_info(C.byref(v), t, info.ctypes.data) == 0
+        out.append(dict(t=t, offset=int(info[0]), rows=int(info[1]), cols=int(info[2])))
+    return out
+
+
+def vit_elbo_partial(model, mu, rho, x, y_cls, B_glob, b_offset, S_glob, s0, s1, seed, step, aug=AUG_NONE,
+                     nthreads=0):
+    """[acc_μ (P) | acc_ρ (P) | L_data] of samples [s0, s1) (vit_oracle.c)."""
+    v = vit_struct(model)
+    P = vit_n_params(model)
+    mu, rho, x = _d(mu), _d(rho), _d(x)
+    yc = np.ascontiguousarray(y_cls, np.int32)
+    acc = np.zeros(2 * P + 1, np.float64)
+    rc = lib().orc_vit_elbo_partial(C.byref(v), _p(mu), _p(rho), _p(x), _p(yc), x.shape[0], b_offset, B_glob,
+                                    S_glob, s0, s1, seed, step, aug, _p(acc), nthreads)
+    assert rc == 0, rc
+    return acc
+
+
+def vit_finalize(mu, rho, acc, D):
+    P = (len(acc) - 1) // 2
+    mu, rho, acc = _d(mu), _d(rho), _d(acc)
+    gmu, grho = np.zeros(P), np.zeros(P)
+    loss, kl = C.c_double(), C.c_double()
+    assert lib().orc_finalize_p(P, _p(mu), _p(rho), _p(acc), D, C.byref(loss), C.byref(kl), _p(gmu),
+                                _p(grho)) == 0
+    return dict(loss=loss.value, kl=kl.value, grad_mu=gmu, grad_rho=grho, L_data=acc[2 * P])
+
+
+def vit_elbo_step(model, mu, rho, x, y_cls, S, seed, step, D, aug=AUG_NONE, nthreads=0):
+    B = np.asarray(x).shape[0]
+    acc = vit_elbo_partial(model, mu, rho, x, y_cls, B, 0, S, 0, S, seed, step, aug, nthreads)
+    return vit_finalize(mu, rho, acc, D)
+
+
+def vit_forward(model, mu, rho, x, s0, s1, seed, step, aug=AUG_NONE):
+    """logits [s1 − s0, B, classes]"""
+    v = vit_struct(model)
+    mu, rho, x = _d(mu), _d(rho), _d(x)
+    B = x.shape[0]
+    out = np.zeros((s1 - s0, B, int(model["n_classes"])), np.float64)
+    assert lib().orc_vit_forward(C.byref(v), _p(mu), _p(rho), _p(x), B, s0, s1, seed, step, aug, _p(out)) == 0
+    return out
 
 
 def model_struct(model: dict, act: str = "relu") -> OrcModel:

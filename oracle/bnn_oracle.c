@@ -818,6 +818,23 @@ int orc_elbo_partial(const orc_model* m, const double* mu, const double* rho, co
  *   grad_μ = acc_μ + μ/|D|;  grad_ρ = sigmoid(ρ)·(acc_ρ + (σ − 1/σ)/|D|)
  *   KL = ½ Σ (σ² + μ² − 1 − 2 ln σ);   loss = L_data + KL/|D|
  */
+/* finalize of a P-parameter variational model (also the ViT oracle's, vit_oracle.c) */
+int orc_finalize_p(long P, const double* mu, const double* rho, const double* acc, double D,
+                   double* out_loss, double* out_kl, double* grad_mu, double* grad_rho)
+{
+    double kl = 0.0;
+    for (long i = 0; i < P; ++i) {
+        double sg = softplus(rho[i]);
+        double ls = log_softplus(rho[i]);
+        kl += 0.5 * (sg * sg + mu[i] * mu[i] - 1.0 - 2.0 * ls);
+        grad_mu[i] = acc[i] + mu[i] / D;
+        grad_rho[i] = sigmoid(rho[i]) * (acc[P + i] + (sg - 1.0 / sg) / D);
+    }
+    *out_kl = kl;
+    *out_loss = acc[2 * P] + kl / D;
+    return 0;
+}
+
 int orc_finalize(const orc_model* m, const double* mu, const double* rho, const double* acc,
                  double D, double* out_loss, double* out_kl, double* grad_mu, double* grad_rho)
 {
@@ -832,17 +849,7 @@ int orc_finalize(const orc_model* m, const double* mu, const double* rho, const 
         *out_loss = acc[2 * P];
         return 0;
     }
-    double kl = 0.0;
-    for (long i = 0; i < P; ++i) {
-        double sg = softplus(rho[i]);
-        double ls = log_softplus(rho[i]);
-        kl += 0.5 * (sg * sg + mu[i] * mu[i] - 1.0 - 2.0 * ls);
-        grad_mu[i] = acc[i] + mu[i] / D;
-        grad_rho[i] = sigmoid(rho[i]) * (acc[P + i] + (sg - 1.0 / sg) / D);
-    }
-    *out_kl = kl;
-    *out_loss = acc[2 * P] + kl / D;
-    return 0;
+    return orc_finalize_p(P, mu, rho, acc, D, out_loss, out_kl, grad_mu, grad_rho);
 }
 
 /*

@@ -25,6 +25,9 @@ MODELS = {
                            base_width=64, loss="ce"),
     "mcd_mlp_96_128_128_24": dict(kind="mlp", widths=[96, 128, 128, 24], loss="mse_mean",
                                   method="mcd", dropout_p=0.1),
+    # use case 1: 4×4 patches, width 192, 3 heads, 6 layers, MLP 768
+    "vit_cifar": dict(kind="vit", in_h=32, in_w=32, in_c=3, patch=4, dim=192, heads=3, depth=6,
+                      mlp=768, n_classes=10, loss="ce"),
 }
 
 CONFIGS = {
@@ -34,6 +37,8 @@ CONFIGS = {
     "C4": dict(model="resnet18_cifar", B=128, S=64, D=45000.0, aug="per_sample"),
     "C5": dict(model="resnet18_cifar", B=256, S=32, D=45000.0, aug="per_sample", K=4, G=2),
     "C6": dict(model="mcd_mlp_96_128_128_24", B=256, S=64, D=1.0, aug="none", K=1, G=1),
+    # not a BASELINE config: SURVEY §8(f) f3, the paper's primary use case (ViT on CIFAR-10)
+    "C7": dict(model="vit_cifar", B=128, S_per_gpu=8, D=45000.0, aug="per_sample"),
 }
 
 
@@ -46,6 +51,8 @@ def layout(model: dict) -> list[dict]:
     "stem", "c1"/"c2" (first/second conv of a BasicBlock), "proj", "out" for the ResNet) — the
     last two are used only by the initialiser.
     """
+    if model["kind"] == "vit":
+        return _vit_layout(model)
     layers = []  # (cin, cout, k, role)
     if model["kind"] == "mlp":
         w = model["widths"]
@@ -77,13 +84,32 @@ def layout(model: dict) -> list[dict]:
     return out
 
 
+def _vit_layout(model: dict) -> list[dict]:
+    """ViT tensors in the order of oracle/vit_oracle.c and the library: each
+    [rows, cols] (1-D tensors [1, n]; pos [1, T·D]); role and fan-in for the initialiser."""
+    D, M, O = model["dim"], model["mlp"], model["n_classes"]
+    T = 1 + (model["in_h"] // model["patch"]) * (model["in_w"] // model["patch"])
+    pk = model["patch"] * model["patch"] * model["in_c"]
+    spec = [(D, pk, "w", pk), (1, D, "b", pk), (1, D, "cls", D), (1, T * D, "pos", D)]
+    for _ in range(model["depth"]):
+        spec += [(1, D, "ln_g", D), (1, D, "ln_b", D), (3 * D, D, "w", D), (1, 3 * D, "b", D),
+                 (D, D, "w", D), (1, D, "b", D), (1, D, "ln_g", D), (1, D, "ln_b", D),
+                 (M, D, "w", D), (1, M, "b", D), (D, M, "w", M), (1, D, "b", M)]
+    spec += [(1, D, "ln_g", D), (1, D, "ln_b", D), (O, D, "w", D), (1, O, "b", D)]
+    out, off = [], 0
+    for t, (r, c, role, fan) in enumerate(spec):
+        out.append(dict(t=t, offset=off, rows=r, cols=c, fan_in=fan, role=role))
+        off += r * c
+    return out
+
+
 def n_params(model: dict) -> int:
     last = layout(model)[-1]
     return last["offset"] + last["rows"] * last["cols"]
 
 
 def n_outputs(model: dict) -> int:
-    return model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]
+    return model["widths"][-1] if model["kind"] == "mlp" else model["n_classes"]  # CNN, ViT
 
 
 def input_shape(model: dict) -> tuple:

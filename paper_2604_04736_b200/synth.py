@@ -92,9 +92,41 @@ def _positive_params(model: dict, seed: int, off_frac: float = 0.25):
     return mu.astype(np.float32), rho.astype(np.float32)
 
 
+def _vit_params(model: dict, seed: int, rho_mode: str):
+    """ViT: Kaiming μ for every linear weight and bias (as the other models),
+    LayerNorm gains μ = 1 and offsets μ = 0, cls / position embeddings μ ~ N(0, 0.02²) (the ViT
+    convention); σ = 1/fan_in ("scaled inversely with the layer width") or, for the
+    finite-difference tests, ρ ~ U(−3, 0)."""
+    rng = np.random.default_rng(seed)
+    P = n_params(model)
+    mu = np.empty(P, np.float64)
+    rho = np.empty(P, np.float64)
+    for ti in layout(model):
+        n = ti["rows"] * ti["cols"]
+        sl = slice(ti["offset"], ti["offset"] + n)
+        f, role = ti["fan_in"], ti["role"]
+        if role in ("w", "b"):
+            mu[sl] = rng.normal(0.0, math.sqrt(2.0 / f), n)
+        elif role == "ln_g":
+            mu[sl] = 1.0
+        elif role == "ln_b":
+            mu[sl] = 0.0
+        else:  # cls, pos
+            mu[sl] = rng.normal(0.0, 0.02, n)
+        if rho_mode == "wide":
+            rho[sl] = rng.uniform(-3.0, 0.0, n)
+        elif rho_mode == "tiny":
+            rho[sl] = -40.0
+        else:
+            rho[sl] = _softplus_inv(np.full(n, 1.0 / f))
+    return mu.astype(np.float32), rho.astype(np.float32)
+
+
 def init_params(model: dict, seed: int = 2, rho_mode: str = "init", sigma_c: float = 1.0,
                 regime: str = "kaiming"):
     """Return (mu, rho) as float32 arrays of length n_params(model)."""
+    if model["kind"] == "vit":
+        return _vit_params(model, seed, rho_mode)
     if regime == "positive":
         assert rho_mode == "init"
         return _positive_params(model, seed)

@@ -153,3 +153,56 @@ def deterministic(model, mu, x, y_cls, y_reg):
         l = F.mse_loss(z, torch.tensor(np.asarray(y_reg, np.float64)))
     l.backward()
     return l.item(), mu_t.grad.numpy().copy()
+
+
+# ---------------------------------------------------------------- Bayesian ViT
+def vit_forward(model, ws, x):
+    """Library-routine formulation of the ViT of oracle/vit_oracle.c (pre-norm encoder,
+    F.layer_norm eps 1e-6, exact-erf F.gelu, softmax attention); x: [B, H, W, C]."""
+    p, D, nh = model["patch"], model["dim"], model["heads"]
+    B, H, W, C = x.shape
+    dh = D // nh
+    pt = x.reshape(B, H // p, p, W // p, p, C).permute(0, 1, 3, 2, 4, 5).reshape(B, -1, p * p * C)
+    T = pt.shape[1] + 1
+    it = iter(ws)
+    Wp, bp, cls, pos = next(it), next(it), next(it), next(it)
+    X = torch.cat([cls.reshape(1, 1, D).expand(B, 1, D), F.linear(pt, Wp, bp.reshape(-1))], 1)
+    X = X + pos.reshape(1, T, D)
+    for _ in range(model["depth"]):
+        g1, b1, Wq, bq, Wo, bo, g2, b2, W1, c1, W2, c2 = [next(it) for _ in range(12)]
+        h = F.layer_norm(X, (D,), g1.reshape(-1), b1.reshape(-1), eps=1e-6)
+        q, k, v = F.linear(h, Wq, bq.reshape(-1)).split(D, dim=-1)
+        q, k, v = (t.reshape(B, T, nh, dh).transpose(1, 2) for t in (q, k, v))
+        att = torch.softmax(q @ k.transpose(-1, -2) / dh ** 0.5, dim=-1)
+        o = (att @ v).transpose(1, 2).reshape(B, T, D)
+        X = X + F.linear(o, Wo, bo.reshape(-1))
+        h2 = F.layer_norm(X, (D,), g2.reshape(-1), b2.reshape(-1), eps=1e-6)
+        X = X + F.linear(F.gelu(F.linear(h2, W1, c1.reshape(-1))), W2, c2.reshape(-1))
+    gf, bf, Wh, bh = next(it), next(it), next(it), next(it)
+    hf = F.layer_norm(X, (D,), gf.reshape(-1), bf.reshape(-1), eps=1e-6)
+    return F.linear(hf[:, 0], Wh, bh.reshape(-1))
+
+
+def vit_acc(model, mu, rho, x, y, S, seed, step, aug=False, s0=0):
+    """[acc_μ | acc_ρ | L_data] of the ViT data term over global samples s0 … s0+S−1 (scale
+    1/(S·B) as in the oracle) by torch autograd with the oracle's ε and crop/flip draws."""
+    lay = layout(model)
+    B = x.shape[0]
+    mu = torch.tensor(np.asarray(mu, np.float64))
+    sig = F.softplus(torch.tensor(np.asarray(rho, np.float64)))
+    xt = torch.tensor(np.asarray(x, np.float64))
+    P = mu.numel()
+    am, ar, ld = torch.zeros(P, dtype=torch.float64), torch.zeros(P, dtype=torch.float64), 0.0
+    for s in range(s0, s0 + S):
+        eps = torch.cat([torch.tensor(O.eps_fill(seed, step, s, ti["t"], 0, ti["rows"], 0, ti["cols"]).astype(np.float64))
+                         .reshape(-1) for ti in lay])
+        w = (mu + sig * eps).clone().requires_grad_(True)
+        ws = [w[ti["offset"]:ti["offset"] + ti["rows"] * ti["cols"]].reshape(ti["rows"], ti["cols"]) for ti in lay]
+        xs = torch.stack([_augment(xt[b], seed, step, s, b) for b in range(B)]) if aug else xt
+        z = vit_forward(model, ws, xs)
+        loss = F.cross_entropy(z, torch.tensor(np.asarray(y, np.int64)), reduction="sum") / (S * B)
+        loss.backward()
+        am += w.grad
+        ar += eps * w.grad
+        ld += float(loss.detach())
+    return np.concatenate([am.numpy(), ar.numpy(), [ld]])
