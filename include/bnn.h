@@ -57,7 +57,7 @@ typedef enum {
     BNN_ERR_CUDA = 5     /* CUDA runtime/driver error, or no sm_100 device */
 } bnn_status;
 
-enum { BNN_MODEL_MLP = 0, BNN_MODEL_RESNET18 = 1 };
+enum { BNN_MODEL_MLP = 0, BNN_MODEL_RESNET18 = 1, BNN_MODEL_VIT = 2 };
 /* BNN_LOSS_CE / _MSE: L_data = (1/S) Σ_s Loss(ŷ_s, y), the per-sample average of Alg. 1 l.9
  * (PAPER.md:162). BNN_LOSS_CE_MEAN / _MSE_MEAN: exact aggregation (§4.1;
  * SURVEY.md §8(f) f1), the loss of the MEAN prediction — CE of the arithmetic mean of the
@@ -97,6 +97,12 @@ typedef struct bnn_model_desc {
     int32_t loss; /* BNN_LOSS_CE (labels int32) | BNN_LOSS_MSE (targets fp32 [B, outputs]) */
     int32_t method;   /* BNN_METHOD_VI (Bayes by backprop, default) | BNN_METHOD_MCD */
     float dropout_p;  /* MCD: drop probability of every hidden unit, 0 ≤ p < 1 */
+    /* BNN_MODEL_VIT: in_h × in_w × in_c images (NHWC fp32),
+     * patch × patch patches, width dim, `heads` attention heads, `depth` pre-norm encoder
+     * layers with an MLP of width mlp, n_classes outputs, loss BNN_LOSS_CE, precision FP32.
+     * Tensor order and shapes: oracle/vit_oracle.c header / DESIGN.md §3 (every tensor,
+     * LayerNorm g/b, cls and pos included, is variational). */
+    int32_t patch, dim, heads, depth, mlp;
 } bnn_model_desc;
 
 /* Run configuration. Rank r of world P = K·G is sample group k = r / G, data group

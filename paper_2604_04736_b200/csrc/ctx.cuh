@@ -202,6 +202,22 @@ struct bnn_ctx {
     float* bias_scr = nullptr;                         // sampled conv biases [layer][S][512]
     std::vector<cudaEvent_t> wgen_ev;                  // per layer: W_s slot written (side stream)
     std::vector<char> tma_fwd, tma_dgrad, tma_wgrad;   // stride-1 layers use them
+    // Bayesian ViT (runtime_vit.cu): tensor table, activations per layer, gradient scratch
+    struct VitTensor {
+        int64_t off;
+        int rows, cols;
+    };
+    struct VitAct {
+        float *X = nullptr, *H1 = nullptr, *st1 = nullptr, *QKV = nullptr, *Att = nullptr, *O = nullptr,
+              *Xmid = nullptr, *H2 = nullptr, *st2 = nullptr, *U = nullptr, *A = nullptr;
+    };
+    std::vector<VitTensor> vtens;
+    int vNP = 0, vT = 0, vD = 0, vM = 0, vPK = 0;
+    float *vP = nullptr, *vE = nullptr, *vX0 = nullptr, *vXout = nullptr, *vHc = nullptr, *vstf = nullptr;
+    float *vdX = nullptr, *vdH = nullptr, *vdQKV = nullptr, *vdO = nullptr, *vdU = nullptr, *vdyxh = nullptr,
+          *vdE = nullptr, *vdHc = nullptr;
+    std::vector<VitAct> vl;
+    std::vector<float*> vvec;  // sampled 1-D tensors [chunk][n] (LayerNorm g/b, cls, pos), else null
     std::vector<CUtensorMap> cmap_hf, cmap_hd;  // conv3 HALO: 1-row (W + 2)-pixel boxes of the input / dY
     std::vector<char> halo_fwd, halo_dgrad;
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
@@ -339,6 +355,12 @@ void comm_destroy(bnn_ctx* c);
 void ar_begin(bnn_ctx* c);
 int ar_layer_done(bnn_ctx* c, int l, cudaStream_t w0, cudaStream_t w1);
 int ar_finish(bnn_ctx* c, cudaStream_t st);
+
+// ViT entry points (runtime_vit.cu)
+int build_vit(bnn_ctx* c);
+int alloc_vit(bnn_ctx* c);
+int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, int B, int B_glob, int S_glob,
+              int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss);
 
 // ResNet entry points (runtime_resnet.cu)
 int alloc_resnet_bf16(bnn_ctx* c);

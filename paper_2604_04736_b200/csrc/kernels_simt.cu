@@ -759,7 +759,10 @@ __global__ void __launch_bounds__(256) dgrad_fp32_kernel(SampledLayer L, SampleK
             const int k = kt0 + tx * 4 + j;
             if (k >= K) continue;
             // ReLU (and, under MC dropout, the keep mask: the stored input is 0 where dropped)
-            const float m = Ap[s * strideA + (int64_t)b * K + k] > 0.0f ? (d.on ? d.inv_keep : 1.0f) : 0.0f;
+            // (Ap == null: no activation mask — the ViT's projections, whose nonlinearities are
+            // separate kernels)
+            const float m = Ap == nullptr ? 1.0f
+                            : Ap[s * strideA + (int64_t)b * K + k] > 0.0f ? (d.on ? d.inv_keep : 1.0f) : 0.0f;
             dA[s * strideD + (int64_t)b * K + k] = acc[i][j] * m;
         }
     }

@@ -1,0 +1,325 @@
+// kernels_vit.cu — the non-GEMM kernels of the Bayesian ViT step (
+// PAPER.md:305-315): patch extraction with the per-sample crop/flip, token assembly with the
+// sampled cls / position embeddings, LayerNorm, softmax attention, GELU and their backward
+// passes. The sampled projections (patch embedding, QKV, output projection, MLP, head) run on
+// the sampled-layer GEMM kernels shared with the MLP (kernels_simt.cu FP32 / kernels_tc.cu BF16).
+//
+// Layout: token rows [s][b][t][·] (t = 0 the cls token), fp32. LayerNorm and attention follow
+// oracle/vit_oracle.c's definitions (LN eps 1e-6 with the biased variance; scores / √dh;
+// exact-erf GELU) — written independently, no shared code.
+#include <algorithm>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels_vit.cuh"
+
+namespace bnn {
+
+// ------------------------------------------------------------------------ sampled vectors
+// w[s][i] = μ[off + i] + σ[off + i]·ε(t, 0, i) for the 1-D tensors (LayerNorm g/b, cls, pos)
+__global__ void vit_sample_vec_kernel(const float* __restrict__ mu, const float* __restrict__ sigma, int64_t off,
+                                      uint32_t t, int n, SampleKeys kk, float* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, s = blockIdx.y;
+    if (i >= n) return;
+    out[(int64_t)s * n + i] = __fmaf_rn(sigma[off + i], eps1(kk.key, kk.step, kk.s0 + s, t, 0u, (uint32_t)i), mu[off + i]);
+}
+
+void launch_vit_sample_vec(const float* mu, const float* sigma, int64_t off, uint32_t t, int n, const SampleKeys& kk,
+                           int S, float* out, cudaStream_t st) {
+    vit_sample_vec_kernel<<<dim3((n + 255) / 256, S), 256, 0, st>>>(mu, sigma, off, t, n, kk, out);
+}
+
+// ------------------------------------------------------------------------ patches
+// P[s][b][pi][(dy·p + dx)·C + c] of the (crop + flip augmented, docs/EPS.md §4) image b
+__global__ void vit_patchify_kernel(const float* __restrict__ x, int B, int H, int W, int C, int p, int aug,
+                                    EpsKey key, uint32_t step, uint32_t s0, int b_off, float* __restrict__ P) {
+    const int b = blockIdx.x, s = blockIdx.y;
+    int dx = 4, dy = 4, flip = 0;
+    if (aug) {
+        const uint4 y = philox10(make_uint4(0u, (uint32_t)(b_off + b), (4095u << 20) | (s0 + s), step), key);
+        dx = (int)(y.x % 9u);
+        dy = (int)(y.y % 9u);
+        flip = (int)(y.z & 1u);
+    }
+    const float* src = x + (int64_t)b * H * W * C;
+    const int pw = W / p, pk = p * p * C, np = (H / p) * pw;
+    float* dst = P + ((int64_t)s * B + b) * np * pk;
+    for (int i = threadIdx.x; i < np * pk; i += blockDim.x) {
+        const int pi = i / pk, e = i - pi * pk;
+        const int c = e % C, q = e / C, ddx = q % p, ddy = q / p;
+        const int r = (pi / pw) * p + ddy, cc = (pi % pw) * p + ddx;
+        const int jj = flip ? W - 1 - cc : cc;
+        const int si = r + dy - 4, sj = jj + dx - 4;
+        dst[i] = (si >= 0 && si < H && sj >= 0 && sj < W) ? src[((int64_t)si * W + sj) * C + c] : 0.0f;
+    }
+}
+
+void launch_vit_patchify(const float* x, int S, int B, int H, int W, int C, int p, int aug, uint64_t seed,
+                         uint32_t step, uint32_t s0, int b_off, float* P, cudaStream_t st) {
+    vit_patchify_kernel<<<dim3(B, S), 256, 0, st>>>(x, B, H, W, C, p, aug, make_key(seed), step, s0, b_off, P);
+}
+
+// X0[s][b][0] = cls_s + pos_s[0];  X0[s][b][t] = E[s][b][t−1] + pos_s[t]
+__global__ void vit_embed_kernel(const float* __restrict__ E, const float* __restrict__ cls,
+                                 const float* __restrict__ pos, int B, int T, int D, float* __restrict__ X) {
+    const int64_t n = (int64_t)B * T * D;
+    const int s = blockIdx.y;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (int)(i % D), t = (int)((i / D) % T), b = (int)(i / ((int64_t)T * D));
+        const float v = t == 0 ? cls[(int64_t)s * D + d] : E[(((int64_t)s * B + b) * (T - 1) + t - 1) * D + d];
+        X[(int64_t)s * n + i] = v + pos[(int64_t)s * T * D + (int64_t)t * D + d];
+    }
+}
+
+void launch_vit_embed(const float* E, const float* cls, const float* pos, int S, int B, int T, int D, float* X,
+                      cudaStream_t st) {
+    vit_embed_kernel<<<dim3(256, S), 256, 0, st>>>(E, cls, pos, B, T, D, X);
+}
+
+// ------------------------------------------------------------------------ LayerNorm
+// one warp per row; rows of one sample are `rows` rows `ld` floats apart (ld = D: all tokens;
+// ld = T·D: the cls rows); g, b: sampled [s][D]
+__global__ void vit_ln_fwd_kernel(const float* __restrict__ X, int rows, int64_t ld, int64_t sX, int D,
+                                  const float* __restrict__ g, const float* __restrict__ bb, float* __restrict__ Y,
+                                  int64_t ldy, int64_t sY, float* __restrict__ stats) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, s = blockIdx.y;
+    if (warp >= rows) return;
+    const float* x = X + s * sX + warp * ld;
+    float sum = 0.f;
+    for (int i = lane; i < D; i += 32) sum += x[i];
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum / D;
+    float sq = 0.f;
+    for (int i = lane; i < D; i += 32) sq += (x[i] - mean) * (x[i] - mean);
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    const float rstd = rsqrtf(sq / D + 1e-6f);
+    float* y = Y + s * sY + warp * ldy;
+    for (int i = lane; i < D; i += 32) y[i] = g[(int64_t)s * D + i] * ((x[i] - mean) * rstd) + bb[(int64_t)s * D + i];
+    if (lane == 0) {
+        stats[((int64_t)s * rows + warp) * 2] = mean;
+        stats[((int64_t)s * rows + warp) * 2 + 1] = rstd;
+    }
+}
+
+void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, int D, const float* g, const float* b,
+                       float* Y, int64_t ldy, int64_t sY, float* stats, cudaStream_t st) {
+    vit_ln_fwd_kernel<<<dim3((rows + 7) / 8, S), 256, 0, st>>>(X, rows, ld, sX, D, g, b, Y, ldy, sY, stats);
+}
+
+// dX += rstd·(dx̂ − mean(dx̂) − x̂·mean(dx̂ ⊙ x̂)), dx̂ = dY ⊙ g; dyxh = dY ⊙ x̂ (the g-gradient rows)
+__global__ void vit_ln_bwd_kernel(const float* __restrict__ dY, int64_t ldy, int64_t sdY, const float* __restrict__ X,
+                                  int rows, int64_t ld, int64_t sX, int D, const float* __restrict__ g,
+                                  const float* __restrict__ stats, float* __restrict__ dX, float* __restrict__ dyxh) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, s = blockIdx.y;
+    if (warp >= rows) return;
+    const float mean = stats[((int64_t)s * rows + warp) * 2], rstd = stats[((int64_t)s * rows + warp) * 2 + 1];
+    const float* x = X + s * sX + warp * ld;
+    const float* dy = dY + s * sdY + warp * ldy;
+    float m1 = 0.f, m2 = 0.f;
+    for (int i = lane; i < D; i += 32) {
+        const float xh = (x[i] - mean) * rstd, dxh = dy[i] * g[(int64_t)s * D + i];
+        m1 += dxh;
+        m2 += dxh * xh;
+    }
+    for (int o = 16; o; o >>= 1) {
+        m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+        m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    }
+    m1 /= D;
+    m2 /= D;
+    float* dx = dX + s * sX + warp * ld;
+    float* dg = dyxh + ((int64_t)s * rows + warp) * D;
+    for (int i = lane; i < D; i += 32) {
+        const float xh = (x[i] - mean) * rstd;
+        dx[i] += rstd * (dy[i] * g[(int64_t)s * D + i] - m1 - xh * m2);
+        dg[i] = dy[i] * xh;
+    }
+}
+
+void launch_vit_ln_bwd(const float* dY, int64_t ldy, int64_t sdY, const float* X, int S, int rows, int64_t ld,
+                       int64_t sX, int D, const float* g, const float* stats, float* dX, float* dyxh, cudaStream_t st) {
+    vit_ln_bwd_kernel<<<dim3((rows + 7) / 8, S), 256, 0, st>>>(dY, ldy, sdY, X, rows, ld, sX, D, g, stats, dX, dyxh);
+}
+
+// ------------------------------------------------------------------------ attention
+// block = (head h, example b, sample s); QKV rows [T][3D] (Q | K | V, head h at columns h·dh …);
+// O[t][h·dh + e]; A[s][b][h][T][T] kept for the backward. One warp per query row.
+__global__ void vit_attn_fwd_kernel(const float* __restrict__ QKV, int B, int T, int D, int dh,
+                                    float* __restrict__ O, float* __restrict__ A) {
+    extern __shared__ float sm[];
+    const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    float* Ks = sm;                  // [T][dh + 1]
+    float* Vs = Ks + T * (dh + 1);   // [T][dh]
+    float* Ps = Vs + T * dh;         // [nw][T]
+    const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
+    for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
+        const int t = i / dh, e = i - t * dh;
+        Ks[t * (dh + 1) + e] = base[(int64_t)t * 3 * D + D + h * dh + e];
+        Vs[i] = base[(int64_t)t * 3 * D + 2 * D + h * dh + e];
+    }
+    __syncthreads();
+    const float sc = rsqrtf((float)dh);
+    float* pr = Ps + warp * T;
+    for (int i = warp; i < T; i += nw) {
+        const float* q = base + (int64_t)i * 3 * D + h * dh;
+        float mx = -INFINITY;
+        for (int j = lane; j < T; j += 32) {
+            float d = 0.f;
+            for (int e = 0; e < dh; ++e) d += q[e] * Ks[j * (dh + 1) + e];
+            d *= sc;
+            pr[j] = d;
+            mx = fmaxf(mx, d);
+        }
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float se = 0.f;
+        for (int j = lane; j < T; j += 32) {
+            const float e = __expf(pr[j] - mx);
+            pr[j] = e;
+            se += e;
+        }
+        for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const float inv = 1.0f / se;
+        float* arow = A + ((((int64_t)s * B + b) * nh + h) * T + i) * T;
+        for (int j = lane; j < T; j += 32) {
+            pr[j] *= inv;
+            arow[j] = pr[j];
+        }
+        __syncwarp();
+        for (int e = lane; e < dh; e += 32) {
+            float acc = 0.f;
+            for (int j = 0; j < T; ++j) acc += pr[j] * Vs[j * dh + e];
+            O[(((int64_t)s * B + b) * T + i) * D + h * dh + e] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A,
+                         cudaStream_t st) {
+    const int dh = D / heads, threads = 256;
+    const size_t smem = sizeof(float) * ((size_t)T * (dh + 1) + (size_t)T * dh + (size_t)(threads / 32) * T);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(vit_attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    vit_attn_fwd_kernel<<<dim3(heads, B, S), threads, smem, st>>>(QKV, B, T, D, dh, O, A);
+}
+
+// dA_ij = dO_i·V_j; dS_ij = A_ij(dA_ij − Σ_k A_ik dA_ik)/√dh; dQ_i = Σ_j dS_ij K_j;
+// dK_j = Σ_i dS_ij Q_i; dV_j = Σ_i A_ij dO_i. Written into dQKV (Q | K | V columns of head h).
+__global__ void vit_attn_bwd_kernel(const float* __restrict__ QKV, const float* __restrict__ A,
+                                    const float* __restrict__ dO, int B, int T, int D, int dh,
+                                    float* __restrict__ dQKV) {
+    extern __shared__ float sm[];
+    const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int P1 = dh + 1, TP = T + 1;
+    float* Qs = sm;              // [T][dh+1]
+    float* Ks = Qs + T * P1;
+    float* Vs = Ks + T * P1;
+    float* dOs = Vs + T * P1;
+    float* As = dOs + T * P1;    // [T][T+1]
+    float* dSs = As + T * TP;    // [T][T+1]
+    const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
+    const float* dob = dO + ((int64_t)s * B + b) * T * D;
+    const float* ab = A + (((int64_t)s * B + b) * nh + h) * T * T;
+    for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
+        const int t = i / dh, e = i - t * dh;
+        Qs[t * P1 + e] = base[(int64_t)t * 3 * D + h * dh + e];
+        Ks[t * P1 + e] = base[(int64_t)t * 3 * D + D + h * dh + e];
+        Vs[t * P1 + e] = base[(int64_t)t * 3 * D + 2 * D + h * dh + e];
+        dOs[t * P1 + e] = dob[(int64_t)t * D + h * dh + e];
+    }
+    for (int i = threadIdx.x; i < T * T; i += blockDim.x) As[(i / T) * TP + i % T] = ab[i];
+    __syncthreads();
+    const float sc = rsqrtf((float)dh);
+    float* out = dQKV + ((int64_t)s * B + b) * T * 3 * D;
+    for (int i = warp; i < T; i += nw) {  // rows: dS and dQ
+        float rd = 0.f;
+        for (int j = lane; j < T; j += 32) {
+            float d = 0.f;
+            for (int e = 0; e < dh; ++e) d += dOs[i * P1 + e] * Vs[j * P1 + e];
+            dSs[i * TP + j] = d;
+            rd += As[i * TP + j] * d;
+        }
+        for (int o = 16; o; o >>= 1) rd += __shfl_xor_sync(0xffffffffu, rd, o);
+        for (int j = lane; j < T; j += 32) dSs[i * TP + j] = As[i * TP + j] * (dSs[i * TP + j] - rd) * sc;
+        __syncwarp();
+        for (int e = lane; e < dh; e += 32) {
+            float acc = 0.f;
+            for (int j = 0; j < T; ++j) acc += dSs[i * TP + j] * Ks[j * P1 + e];
+            out[(int64_t)i * 3 * D + h * dh + e] = acc;
+        }
+    }
+    __syncthreads();
+    for (int j = warp; j < T; j += nw) {  // columns: dK and dV
+        for (int e = lane; e < dh; e += 32) {
+            float k = 0.f, v = 0.f;
+            for (int i = 0; i < T; ++i) {
+                k += dSs[i * TP + j] * Qs[i * P1 + e];
+                v += As[i * TP + j] * dOs[i * P1 + e];
+            }
+            out[(int64_t)j * 3 * D + D + h * dh + e] = k;
+            out[(int64_t)j * 3 * D + 2 * D + h * dh + e] = v;
+        }
+    }
+}
+
+void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D, int heads,
+                         float* dQKV, cudaStream_t st) {
+    const int dh = D / heads;
+    const size_t smem = sizeof(float) * (4 * (size_t)T * (dh + 1) + 2 * (size_t)T * (T + 1));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(vit_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    vit_attn_bwd_kernel<<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, dh, dQKV);
+}
+
+// ------------------------------------------------------------------------ elementwise
+__device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.0f + erff(u * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_df(float u) {
+    return 0.5f * (1.0f + erff(u * 0.70710678118654752f)) + u * 0.39894228040143268f * __expf(-0.5f * u * u);
+}
+
+__global__ void vit_gelu_kernel(const float* __restrict__ U, int64_t n, float* __restrict__ Aout) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        Aout[i] = gelu_f(U[i]);
+}
+__global__ void vit_gelu_bwd_kernel(const float* __restrict__ U, int64_t n, float* __restrict__ dA) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dA[i] *= gelu_df(U[i]);
+}
+__global__ void vit_add_kernel(float* __restrict__ Y, const float* __restrict__ X, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        Y[i] += X[i];
+}
+// rows r of [S][rows][D] that are token t0 + (r mod per)… : out[s][b][k][d] = in[s][b][t0 + k][d]
+__global__ void vit_gather_tokens_kernel(const float* __restrict__ in, int B, int T, int t0, int nt, int D,
+                                         float* __restrict__ out) {
+    const int64_t n = (int64_t)B * nt * D;
+    const int s = blockIdx.y;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (int)(i % D), k = (int)((i / D) % nt), b = (int)(i / ((int64_t)nt * D));
+        out[(int64_t)s * n + i] = in[(((int64_t)s * B + b) * T + t0 + k) * D + d];
+    }
+}
+
+void launch_vit_gelu(const float* U, int64_t n, float* A, cudaStream_t st) {
+    vit_gelu_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, A);
+}
+void launch_vit_gelu_bwd(const float* U, int64_t n, float* dA, cudaStream_t st) {
+    vit_gelu_bwd_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, dA);
+}
+void launch_vit_add(float* Y, const float* X, int64_t n, cudaStream_t st) {
+    vit_add_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(Y, X, n);
+}
+void launch_vit_gather_tokens(const float* in, int S, int B, int T, int t0, int nt, int D, float* out,
+                              cudaStream_t st) {
+    vit_gather_tokens_kernel<<<dim3(256, S), 256, 0, st>>>(in, B, T, t0, nt, D, out);
+}
+
+}  // namespace bnn

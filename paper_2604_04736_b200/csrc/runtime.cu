@@ -61,6 +61,8 @@ int build_layers(bnn_ctx* c) {
         }
         add(width, m.n_classes, 1, 1, 0);
         c->O = m.n_classes;
+    } else if (m.kind == BNN_MODEL_VIT) {
+        return build_vit(c);  // its own tensor table (runtime_vit.cu)
     } else {
         return c->set_err(BNN_ERR_CONFIG, "unknown model kind %d", m.kind);
     }
@@ -627,7 +629,9 @@ int run_partial(bnn_ctx* c, const float* mu, const float* rho, const float* x, c
         const uint32_t s0 = (uint32_t)(c->kidx * S_loc + s);
         c->ar_live = c->ar_enabled && s + Sc >= S_loc;  // acc segments final in the last chunk
         c->ar_live_used |= c->ar_live;
-        if (c->model.kind == BNN_MODEL_MLP)
+        if (c->model.kind == BNN_MODEL_VIT)
+            rc = vit_chunk(c, mu, x, ycls, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
+        else if (c->model.kind == BNN_MODEL_MLP)
             rc = mlp_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
         else if (c->bf16)
             rc = resnet_bf16_chunk(c, mu, x, ycls, yreg, B_loc, B_glob, S_glob, Sc, s0, seed, step, accm, accr, accl);
@@ -782,7 +786,7 @@ int bnn_init(const bnn_model_desc* model, const bnn_config* cfg, bnn_ctx** out) 
         !c->alloc(&c->g_m2s, (size_t)c->B_max * c->G * c->O * cfg->world) ||
         !c->alloc(&c->g_counts, cfg->world))
         return fail(c->set_err(BNN_ERR_CUDA, "out of device memory"));
-    rc = model->kind == BNN_MODEL_MLP ? alloc_mlp(c) : alloc_resnet(c);
+    rc = model->kind == BNN_MODEL_MLP ? alloc_mlp(c) : model->kind == BNN_MODEL_VIT ? alloc_vit(c) : alloc_resnet(c);
     if (rc) return fail(rc);
     if (c->agg) {
         c->stat_w = c->gnll ? 2 * c->O : c->model.loss == BNN_LOSS_CE ? 1 : c->O;
@@ -806,6 +810,18 @@ int bnn_param_layout(bnn_ctx* c, int64_t* n_params, int32_t* n_tensors, bnn_tens
                      int32_t max_infos) {
     if (!c) return BNN_ERR_CONFIG;
     if (n_params) *n_params = c->P;
+    if (c->model.kind == BNN_MODEL_VIT) {
+        const int nt = (int)c->vtens.size();
+        if (n_tensors) *n_tensors = nt;
+        for (int t = 0; infos && t < nt && t < max_infos; ++t) {
+            infos[t].t = t;
+            infos[t].offset = c->vtens[t].off;
+            infos[t].rows = c->vtens[t].rows;
+            infos[t].cols = c->vtens[t].cols;
+            infos[t].is_bias = c->vtens[t].rows == 1 ? 1 : 0;
+        }
+        return BNN_OK;
+    }
     const int nt = (int)c->layers.size() * 2;
     if (n_tensors) *n_tensors = nt;
     if (infos) {
@@ -1025,6 +1041,7 @@ int bnn_predict(bnn_ctx* c, const float* mu, const float* rho, const float* x, i
     NvtxRange nvtx_("bnn.predict");
     if (!c || !mu || !rho || !x || !mean || !var) return BNN_ERR_CONFIG;
     if (c->G != 1) return c->set_err(BNN_ERR_CONFIG, "predict is sample-sharded only (G == 1)");
+    if (c->model.kind == BNN_MODEL_VIT) return c->set_err(BNN_ERR_CONFIG, "predict: MLP and ResNet models");
     int rc = check_step_args(c, B, B * c->G, S_global);
     if (rc) return rc;
     cudaStream_t st = c->st;

@@ -1,0 +1,261 @@
+// runtime_vit.cu — the Bayesian ViT step (use case 1):
+// tensor table, workspace and the per-chunk forward + backward, FP32 mode.
+//
+// Per sample chunk (Sc samples of the same B_loc examples; rows R = B·T tokens):
+//   patches (crop/flip keyed by global (s, b)) → sampled patch projection → [cls; E] + pos
+//   per encoder layer: LN1 → sampled QKV → softmax attention → sampled proj + residual →
+//                      LN2 → sampled fc1 → GELU → sampled fc2 + residual
+//   final LN of the cls rows → sampled head → per-sample CE (K6, shared with the MLP / CNN)
+// and the backward in reverse. The sampled projections use the K2/K4/K5-family FP32 kernels
+// of the MLP (W_s generated on chip from μ, σ and EPS-v1; never stored); the 1-D variational
+// tensors (LayerNorm g/b, cls, pos) are drawn once per chunk into [Sc][n] buffers; every
+// 1-D tensor's gradient (biases, g, b, cls, pos) goes through the bias-gradient reduction
+// (Σ rows, then acc_μ += Σ_s, acc_ρ += Σ_s ε_s ⊙ ·).
+#include "ctx.cuh"
+#include "kernels_vit.cuh"
+
+namespace {
+
+SampledLayer lin(const bnn_ctx* c, const float* mu, int t_w) {
+    SampledLayer L{};
+    L.mu = mu;
+    L.sigma = c->sigma;
+    L.off_w = c->vtens[t_w].off;
+    L.off_b = c->vtens[t_w + 1].off;
+    L.N = c->vtens[t_w].rows;
+    L.K = c->vtens[t_w].cols;
+    L.t_w = (uint32_t)t_w;
+    L.t_b = (uint32_t)(t_w + 1);
+    return L;
+}
+
+// a 1-D tensor t as the "bias" of a SampledLayer (the bias-gradient path reads off_b, t_b, N)
+SampledLayer vec(const bnn_ctx* c, const float* mu, int t) {
+    SampledLayer L{};
+    L.mu = mu;
+    L.sigma = c->sigma;
+    L.off_w = c->vtens[t].off;
+    L.off_b = c->vtens[t].off;
+    L.N = c->vtens[t].cols;
+    L.K = 0;
+    L.t_w = L.t_b = (uint32_t)t;
+    return L;
+}
+
+}  // namespace
+
+int build_vit(bnn_ctx* c) {
+    const bnn_model_desc& m = c->model;
+    if (m.patch < 1 || m.in_h % m.patch || m.in_w % m.patch || m.dim < 32 || m.heads < 1 || m.dim % m.heads ||
+        m.depth < 1 || m.depth > 64 || m.mlp < 1 || m.n_classes < 1 || m.in_c < 1)
+        return c->set_err(BNN_ERR_CONFIG, "ViT: patch | in_h, in_w; dim %% heads == 0, dim >= 32; 1 <= depth <= 64");
+    if (m.dim / m.heads > 128) return c->set_err(BNN_ERR_CONFIG, "ViT: head dimension <= 128");
+    c->vNP = (m.in_h / m.patch) * (m.in_w / m.patch);
+    c->vT = 1 + c->vNP;
+    if (c->vT > 1024) return c->set_err(BNN_ERR_CONFIG, "ViT: at most 1023 patches");
+    c->vD = m.dim;
+    c->vM = m.mlp;
+    c->vPK = m.patch * m.patch * m.in_c;
+    const int D = c->vD, M = c->vM, T = c->vT;
+    auto add = [&](int rows, int cols) { c->vtens.push_back({0, rows, cols}); };
+    add(D, c->vPK); add(1, D); add(1, D); add(1, T * D);
+    for (int l = 0; l < m.depth; ++l) {
+        add(1, D); add(1, D); add(3 * D, D); add(1, 3 * D); add(D, D); add(1, D);
+        add(1, D); add(1, D); add(M, D); add(1, M); add(D, M); add(1, D);
+    }
+    add(1, D); add(1, D); add(m.n_classes, D); add(1, m.n_classes);
+    int64_t off = 0;
+    for (auto& t : c->vtens) {
+        t.off = off;
+        off += (int64_t)t.rows * t.cols;
+    }
+    c->O = m.n_classes;
+    c->P = off;
+    c->P_pad = round_up(off, 64);
+    c->acc_total = 2 * c->P_pad + 64;
+    return BNN_OK;
+}
+
+int alloc_vit(bnn_ctx* c) {
+    if (c->bf16) return c->set_err(BNN_ERR_CONFIG, "ViT: precision FP32 (the BF16 path is not built)");
+    if (c->agg || c->mcd) return c->set_err(BNN_ERR_CONFIG, "ViT: per-sample CE, Bayes by backprop only");
+    const int B = c->B_max, Sc = c->chunk, T = c->vT, D = c->vD, M = c->vM, L = c->model.depth;
+    const int64_t R = (int64_t)B * T;
+    const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
+    bool ok = c->alloc(&c->vP, (size_t)(aug ? Sc : 1) * B * c->vNP * c->vPK) &&
+              c->alloc(&c->vE, (size_t)Sc * B * c->vNP * D) && c->alloc(&c->vX0, (size_t)Sc * R * D) &&
+              c->alloc(&c->vXout, (size_t)Sc * R * D) && c->alloc(&c->vHc, (size_t)Sc * B * D) &&
+              c->alloc(&c->vstf, (size_t)Sc * B * 2) && c->alloc(&c->logits, (size_t)Sc * B * c->O) &&
+              c->alloc(&c->lossrow, (size_t)Sc * B) && c->alloc(&c->dz_f32, (size_t)Sc * B * c->O) &&
+              c->alloc(&c->vdX, (size_t)Sc * R * D) && c->alloc(&c->vdH, (size_t)Sc * R * D) &&
+              c->alloc(&c->vdQKV, (size_t)Sc * R * 3 * D) && c->alloc(&c->vdO, (size_t)Sc * R * D) &&
+              c->alloc(&c->vdU, (size_t)Sc * R * M) && c->alloc(&c->vdyxh, (size_t)Sc * R * D) &&
+              c->alloc(&c->vdE, (size_t)Sc * B * c->vNP * D) && c->alloc(&c->vdHc, (size_t)Sc * B * D);
+    if (!ok) return c->set_err(BNN_ERR_CUDA, "out of memory (ViT)");
+    c->vl.assign(L, bnn_ctx::VitAct{});
+    for (int l = 0; l < L; ++l) {
+        bnn_ctx::VitAct& a = c->vl[l];
+        ok = c->alloc(&a.X, (size_t)Sc * R * D) && c->alloc(&a.H1, (size_t)Sc * R * D) &&
+             c->alloc(&a.st1, (size_t)Sc * R * 2) && c->alloc(&a.QKV, (size_t)Sc * R * 3 * D) &&
+             c->alloc(&a.Att, (size_t)Sc * B * c->model.heads * T * T) && c->alloc(&a.O, (size_t)Sc * R * D) &&
+             c->alloc(&a.Xmid, (size_t)Sc * R * D) && c->alloc(&a.H2, (size_t)Sc * R * D) &&
+             c->alloc(&a.st2, (size_t)Sc * R * 2) && c->alloc(&a.U, (size_t)Sc * R * M) &&
+             c->alloc(&a.A, (size_t)Sc * R * M);
+        if (!ok) return c->set_err(BNN_ERR_CUDA, "out of memory (ViT layer activations)");
+    }
+    // sampled 1-D tensors [Sc][n]: every tensor with rows == 1 that is not a linear bias
+    c->vvec.assign(c->vtens.size(), nullptr);
+    auto want = [&](int t) {
+        if (t == 2 || t == 3) return true;                      // cls, pos
+        const int nt = (int)c->vtens.size();
+        if (t >= nt - 4) return t == nt - 4 || t == nt - 3;     // final LN g, b
+        const int r = (t - 4) % 12;
+        return r == 0 || r == 1 || r == 6 || r == 7;            // LN1 / LN2 g, b
+    };
+    for (int t = 0; t < (int)c->vtens.size(); ++t)
+        if (want(t) && !c->alloc(&c->vvec[t], (size_t)Sc * c->vtens[t].cols))
+            return c->set_err(BNN_ERR_CUDA, "out of memory (ViT sampled vectors)");
+    const int maxN = std::max({M, 3 * D, T * D, c->O});
+    if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+    return BNN_OK;
+}
+
+int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, int B, int B_glob, int S_glob,
+              int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+    NvtxRange nvtx_("bnn.chunk");
+    cudaStream_t st = c->st;
+    const SampleKeys kk{make_key(seed), step, s0};
+    const int T = c->vT, D = c->vD, M = c->vM, L = c->model.depth, Hh = c->model.heads, NP = c->vNP;
+    const int64_t R = (int64_t)B * T, RD = R * D;
+    const int nt = (int)c->vtens.size();
+    const float scale = 1.0f / ((float)S_glob * B_glob);
+    const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
+    const DropArgs nod{};
+    const int64_t sP = aug ? (int64_t)B * NP * c->vPK : 0;
+    // ---------------- forward
+    {
+        NvtxRange nv("bnn.forward");
+        for (int t = 0; t < nt; ++t)
+            if (c->vvec[t])
+                c->launch("sample", [&] {
+                    launch_vit_sample_vec(mu, c->sigma, c->vtens[t].off, (uint32_t)t, c->vtens[t].cols, kk, Sc,
+                                          c->vvec[t], st);
+                });
+        c->launch("elem", [&] {
+            launch_vit_patchify(x, aug ? Sc : 1, B, c->model.in_h, c->model.in_w, c->model.in_c, c->model.patch,
+                                aug ? 1 : 0, seed, step, s0, c->gidx * B, c->vP, st);
+        });
+        const SampledLayer Lp = lin(c, mu, 0);
+        c->launch("fwd", [&] {
+            launch_fwd_fp32(Lp, kk, nod, Sc, B * NP, c->vP, sP, c->vE, (int64_t)B * NP * D, false, st);
+        });
+        c->launch("elem", [&] { launch_vit_embed(c->vE, c->vvec[2], c->vvec[3], Sc, B, T, D, c->vX0, st); });
+        const float* X = c->vX0;
+        for (int l = 0; l < L; ++l) {
+            bnn_ctx::VitAct& a = c->vl[l];
+            const int tb = 4 + 12 * l;
+            c->launch("elem", [&] { cudaMemcpyAsync(a.X, X, sizeof(float) * Sc * RD, cudaMemcpyDeviceToDevice, st); });
+            c->launch("ln", [&] {
+                launch_vit_ln_fwd(a.X, Sc, (int)R, D, RD, D, c->vvec[tb], c->vvec[tb + 1], a.H1, D, RD, a.st1, st);
+            });
+            const SampledLayer Lq = lin(c, mu, tb + 2), Lo = lin(c, mu, tb + 4), L1 = lin(c, mu, tb + 8),
+                               L2 = lin(c, mu, tb + 10);
+            c->launch("fwd", [&] { launch_fwd_fp32(Lq, kk, nod, Sc, (int)R, a.H1, RD, a.QKV, 3 * RD, false, st); });
+            c->launch("attn", [&] { launch_vit_attn_fwd(a.QKV, Sc, B, T, D, Hh, a.O, a.Att, st); });
+            c->launch("fwd", [&] { launch_fwd_fp32(Lo, kk, nod, Sc, (int)R, a.O, RD, a.Xmid, RD, false, st); });
+            c->launch("elem", [&] { launch_vit_add(a.Xmid, a.X, Sc * RD, st); });
+            c->launch("ln", [&] {
+                launch_vit_ln_fwd(a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], c->vvec[tb + 7], a.H2, D, RD, a.st2, st);
+            });
+            c->launch("fwd", [&] { launch_fwd_fp32(L1, kk, nod, Sc, (int)R, a.H2, RD, a.U, R * M, false, st); });
+            c->launch("elem", [&] { launch_vit_gelu(a.U, Sc * R * M, a.A, st); });
+            c->launch("fwd", [&] { launch_fwd_fp32(L2, kk, nod, Sc, (int)R, a.A, R * M, c->vXout, RD, false, st); });
+            c->launch("elem", [&] { launch_vit_add(c->vXout, a.Xmid, Sc * RD, st); });
+            X = c->vXout;
+        }
+        // final LayerNorm of the cls rows, head, per-sample CE
+        c->launch("ln", [&] {
+            launch_vit_ln_fwd(c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4], c->vvec[nt - 3], c->vHc, D,
+                              (int64_t)B * D, c->vstf, st);
+        });
+        const SampledLayer Lh = lin(c, mu, nt - 2);
+        c->launch("fwd", [&] {
+            launch_fwd_fp32(Lh, kk, nod, Sc, B, c->vHc, (int64_t)B * D, c->logits, (int64_t)B * c->O, false, st);
+        });
+    }
+    c->launch("loss", [&] {
+        launch_loss_head(c->logits, Sc, B, c->O, BNN_LOSS_CE, ycls, nullptr, c->dz_f32, c->O, false, c->lossrow,
+                         nullptr, st);
+    });
+    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    // ---------------- backward
+    NvtxRange nvb("bnn.backward");
+    auto bias = [&](const SampledLayer& Lb, const float* G, int rows, int64_t ldp, int64_t sG) {
+        c->launch("bias", [&] {
+            launch_bias_grad(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->db_scratch, acc_mu, acc_rho, st);
+        }, 2);
+    };
+    {
+        const SampledLayer Lh = lin(c, mu, nt - 2);
+        c->launch("wgrad", [&] {
+            launch_wgrad_fp32(Lh, kk, Sc, B, c->dz_f32, (int64_t)B * c->O, c->vHc, (int64_t)B * D, scale, acc_mu,
+                              acc_rho, st);
+        });
+        bias(Lh, c->dz_f32, B, c->O, (int64_t)B * c->O);
+        c->launch("dgrad", [&] {
+            launch_dgrad_fp32(Lh, kk, nod, Sc, B, c->dz_f32, (int64_t)B * c->O, nullptr, 0, c->vdHc, (int64_t)B * D, st);
+        });
+        CUDA_TRY(c, cudaMemsetAsync(c->vdX, 0, sizeof(float) * Sc * RD, st));
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(c->vdHc, D, (int64_t)B * D, c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4],
+                              c->vstf, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, nt - 4), c->vdyxh, B, D, (int64_t)B * D);
+        bias(vec(c, mu, nt - 3), c->vdHc, B, D, (int64_t)B * D);
+    }
+    for (int l = L - 1; l >= 0; --l) {
+        bnn_ctx::VitAct& a = c->vl[l];
+        const int tb = 4 + 12 * l;
+        const SampledLayer Lq = lin(c, mu, tb + 2), Lo = lin(c, mu, tb + 4), L1 = lin(c, mu, tb + 8),
+                           L2 = lin(c, mu, tb + 10);
+        // X_out = X_mid + fc2(GELU(fc1(LN2(X_mid))))
+        c->launch("wgrad", [&] { launch_wgrad_fp32(L2, kk, Sc, (int)R, c->vdX, RD, a.A, R * M, scale, acc_mu, acc_rho, st); });
+        bias(L2, c->vdX, (int)R, D, RD);
+        c->launch("dgrad", [&] { launch_dgrad_fp32(L2, kk, nod, Sc, (int)R, c->vdX, RD, nullptr, 0, c->vdU, R * M, st); });
+        c->launch("elem", [&] { launch_vit_gelu_bwd(a.U, Sc * R * M, c->vdU, st); });
+        c->launch("wgrad", [&] { launch_wgrad_fp32(L1, kk, Sc, (int)R, c->vdU, R * M, a.H2, RD, scale, acc_mu, acc_rho, st); });
+        bias(L1, c->vdU, (int)R, M, R * M);
+        c->launch("dgrad", [&] { launch_dgrad_fp32(L1, kk, nod, Sc, (int)R, c->vdU, R * M, nullptr, 0, c->vdH, RD, st); });
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(c->vdH, D, RD, a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], a.st2, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, tb + 6), c->vdyxh, (int)R, D, RD);
+        bias(vec(c, mu, tb + 7), c->vdH, (int)R, D, RD);
+        // X_mid = X + proj(attention(LN1(X)))
+        c->launch("wgrad", [&] { launch_wgrad_fp32(Lo, kk, Sc, (int)R, c->vdX, RD, a.O, RD, scale, acc_mu, acc_rho, st); });
+        bias(Lo, c->vdX, (int)R, D, RD);
+        c->launch("dgrad", [&] { launch_dgrad_fp32(Lo, kk, nod, Sc, (int)R, c->vdX, RD, nullptr, 0, c->vdO, RD, st); });
+        c->launch("attn", [&] { launch_vit_attn_bwd(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
+        c->launch("wgrad", [&] { launch_wgrad_fp32(Lq, kk, Sc, (int)R, c->vdQKV, 3 * RD, a.H1, RD, scale, acc_mu, acc_rho, st); });
+        bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
+        c->launch("dgrad", [&] { launch_dgrad_fp32(Lq, kk, nod, Sc, (int)R, c->vdQKV, 3 * RD, nullptr, 0, c->vdH, RD, st); });
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(c->vdH, D, RD, a.X, Sc, (int)R, D, RD, D, c->vvec[tb], a.st1, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, tb), c->vdyxh, (int)R, D, RD);
+        bias(vec(c, mu, tb + 1), c->vdH, (int)R, D, RD);
+    }
+    // X_0 = [cls; patch·W_pᵀ + b_p] + pos
+    bias(vec(c, mu, 2), c->vdX, B, (int64_t)T * D, RD);  // cls: token-0 rows
+    {
+        SampledLayer Lpos = vec(c, mu, 3);  // pos [1, T·D]: Σ over the B examples of the whole [T·D] row
+        bias(Lpos, c->vdX, B, (int64_t)T * D, RD);
+    }
+    c->launch("elem", [&] { launch_vit_gather_tokens(c->vdX, Sc, B, T, 1, NP, D, c->vdE, st); });
+    const SampledLayer Lp = lin(c, mu, 0);
+    c->launch("wgrad", [&] {
+        launch_wgrad_fp32(Lp, kk, Sc, B * NP, c->vdE, (int64_t)B * NP * D, c->vP, sP, scale, acc_mu, acc_rho, st);
+    });
+    bias(Lp, c->vdE, B * NP, D, (int64_t)B * NP * D);
+    return BNN_OK;
+}

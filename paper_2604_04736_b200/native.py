@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libbnn.so")
 _lib = None
 
-MODEL_MLP, MODEL_RESNET18 = 0, 1
+MODEL_MLP, MODEL_RESNET18, MODEL_VIT = 0, 1, 2
 LOSS = {"ce": 0, "mse": 1, "ce_mean": 2, "mse_mean": 3, "gnll_mean": 4}  # *_mean: exact aggregation
 PREC = {"fp32": 0, "bf16": 1}
 MODE = {"sample": 0, "data": 1, "hybrid": 2}
@@ -28,7 +28,8 @@ class BnnModelDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_widths", C.c_int32), ("widths", C.c_int32 * 16),
                 ("in_h", C.c_int32), ("in_w", C.c_int32), ("in_c", C.c_int32),
                 ("n_classes", C.c_int32), ("base_width", C.c_int32), ("loss", C.c_int32),
-                ("method", C.c_int32), ("dropout_p", C.c_float)]
+                ("method", C.c_int32), ("dropout_p", C.c_float), ("patch", C.c_int32), ("dim", C.c_int32),
+                ("heads", C.c_int32), ("depth", C.c_int32), ("mlp", C.c_int32)]
 
 
 class BnnConfig(C.Structure):
@@ -129,6 +130,11 @@ def model_desc(model: dict) -> BnnModelDesc:
         d.n_widths = len(model["widths"])
         for i, w in enumerate(model["widths"]):
             d.widths[i] = w
+    elif model["kind"] == "vit":
+        d.kind = MODEL_VIT
+        d.in_h, d.in_w, d.in_c = model["in_h"], model["in_w"], model["in_c"]
+        d.n_classes = model["n_classes"]
+        d.patch, d.dim, d.heads, d.depth, d.mlp = (model[k] for k in ("patch", "dim", "heads", "depth", "mlp"))
     else:
         d.kind = MODEL_RESNET18
         d.in_h, d.in_w, d.in_c = model["in_h"], model["in_w"], model["in_c"]

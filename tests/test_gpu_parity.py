@@ -1031,3 +1031,82 @@ def test_comm_timeout_returns_err_comm():
     assert "libbnn error 3" in line[0], line[0]  # BNN_ERR_COMM
     dt = float(line[0].split()[1])
     assert 2.5 <= dt <= 60.0, dt
+
+
+# ------------------------------------------------------------------ Bayesian ViT
+VIT_TINY = dict(kind="vit", in_h=8, in_w=8, in_c=3, patch=4, dim=32, heads=2, depth=2, mlp=64, n_classes=3,
+                loss="ce")
+VIT = MODELS["vit_cifar"]
+
+
+@pytest.mark.parametrize("aug,rho_mode", [("none", "wide"), ("per_sample", "wide"), ("per_sample", "init")])
+def test_vit_fp32_matches_oracle(aug, rho_mode):
+    """The ViT step (FP32: sampled projections on the MLP's kernels, LayerNorm / attention /
+    GELU kernels) against the exact ViT oracle: loss, grad_μ, grad_ρ and the data term ≤ 1e-4."""
+    native = _native()
+    model, B, S, D = VIT_TINY, 5, 3, 300.0
+    mu, rho = synth.init_params(model, seed=2, rho_mode=rho_mode)
+    x, yc, _ = synth.make_batch(model, B, seed=1)
+    a = O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE
+    ctx = native.Context(model, precision="fp32", max_B_loc=B, max_S_loc=S, dataset_size=D, aug=aug)
+    loss, gmu, grho = ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0x7177, 2)
+    torch.cuda.synchronize()
+    ref = O.vit_elbo_step(model, mu, rho, x, yc, S, 0x7177, 2, D, aug=a)
+    assert abs(loss - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    _assert_close(ctx, gmu.cpu().numpy(), ref["grad_mu"], 1e-4, "grad_mu")
+    _assert_close(ctx, grho.cpu().numpy(), ref["grad_rho"], 1e-4, "grad_rho")
+    am, ar, al = _acc_parts(ctx, ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0x7177, 2))
+    ra = O.vit_elbo_partial(model, mu, rho, x, yc, B, 0, S, 0, S, 0x7177, 2, a)
+    P = ctx.n_params
+    _assert_close(ctx, am, ra[:P], 1e-4, "acc_mu")
+    _assert_close(ctx, ar, ra[P:2 * P], 1e-4, "acc_rho")
+
+
+def test_vit_fp32_paper_size_matches_oracle():
+    """The paper's ViT (32×32 CIFAR-shaped, 4×4 patches, width 192, 3 heads, 6 layers, MLP 768)
+    with per-sample augmentation, B = 3, S = 2: every tensor ≤ 1e-4."""
+    native = _native()
+    B, S, D = 3, 2, 45000.0
+    mu, rho = synth.init_params(VIT, seed=2)
+    x, yc, _ = synth.make_batch(VIT, B, seed=1)
+    ctx = native.Context(VIT, precision="fp32", max_B_loc=B, max_S_loc=S, dataset_size=D, aug="per_sample")
+    mu_d, rho_d = _dev(mu), _dev(rho)
+    acc = ctx.elbo_partial(mu_d, rho_d, _dev(x), _dev(yc), B, S, 0x5EED, 0)
+    loss, gmu, grho = ctx.finalize(mu_d, rho_d, acc)
+    torch.cuda.synchronize()
+    ra = O.vit_elbo_partial(VIT, mu, rho, x, yc, B, 0, S, 0, S, 0x5EED, 0, O.AUG_PER_SAMPLE)
+    ref = O.vit_finalize(mu, rho, ra, D)
+    P = ctx.n_params
+    am, ar, al = _acc_parts(ctx, acc)
+    _assert_close(ctx, am, ra[:P], 1e-4, "acc_mu")
+    _assert_close(ctx, ar, ra[P:2 * P], 1e-4, "acc_rho")
+    assert abs(al - ra[-1]) <= 1e-4 * abs(ra[-1])
+    _assert_close(ctx, gmu.cpu().numpy(), ref["grad_mu"], 1e-4, "grad_mu")
+    _assert_close(ctx, grho.cpu().numpy(), ref["grad_rho"], 1e-4, "grad_rho")
+
+
+@pytest.mark.parametrize("mode,K,G,chunk", [("hybrid", 2, 2, 0), ("sample", 1, 1, 1)])
+def test_vit_virtual_ranks_and_chunks_equal_single(mode, K, G, chunk):
+    """ViT: a 2×2 sample × data grid of virtual ranks (augmentation keyed by global (s, b)), and
+    sample chunks of 1, equal the single-rank single-chunk step within 1e-5."""
+    native = _native()
+    model, B, S, D = VIT_TINY, 4, 4, 100.0
+    mu, rho = synth.init_params(model, seed=3, rho_mode="wide")
+    x, yc, _ = synth.make_batch(model, B, seed=4)
+    mu_d, rho_d = _dev(mu), _dev(rho)
+    single = native.Context(model, precision="fp32", max_B_loc=B, max_S_loc=S, dataset_size=D, aug="per_sample")
+    l1, g1, r1 = single.finalize(mu_d, rho_d, single.elbo_partial(mu_d, rho_d, _dev(x), _dev(yc), B, S, 5, 1))
+    world = K * G
+    total = None
+    for rank in range(world):
+        ctx = native.Context(model, precision="fp32", mode=mode, K=K, G=G, rank=rank, world=world,
+                             max_B_loc=B // G, max_S_loc=S // K, dataset_size=D, aug="per_sample", sample_chunk=chunk)
+        g = rank % G
+        sl = slice(g * (B // G), (g + 1) * (B // G))
+        acc = ctx.elbo_partial(mu_d, rho_d, _dev(x[sl]), _dev(yc[sl]), B, S, 5, 1)
+        total = acc if total is None else total + acc
+    l2, g2, r2 = single.finalize(mu_d, rho_d, total)
+    torch.cuda.synchronize()
+    assert abs(float(l2) - float(l1)) <= 1e-5 * abs(float(l1))
+    assert _rel(g2.cpu().numpy(), g1.cpu().numpy()) < 1e-5
+    assert _rel(r2.cpu().numpy(), r1.cpu().numpy()) < 1e-5
