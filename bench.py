@@ -47,13 +47,14 @@ WORKLOAD_NAMES = {
     "mlp_8_16_1": "Bayesian MLP 8-16-1 (MSE)",
     "resnet18_cifar": "ResNet-18-shaped Bayesian CNN, 32x32x3, per-sample crop+flip",
     "mcd_mlp_96_128_128_24": "MC-dropout MLP 96-128-128-24 (p=0.1), MSE of the averaged predictions",
+    "vit_cifar": "Bayesian ViT (4x4 patches, width 192, 3 heads, 6 layers, MLP 768), 32x32x3, per-sample crop+flip",
 }
 
 
 def run_plan(config, world, mode_arg=None):
     """Samples / batch per rank for a BASELINE config at `world` GPUs."""
     cfg = CONFIGS[config]
-    if config == "C3":  # weak: S = 8 per GPU, same batch everywhere
+    if config in ("C3", "C7"):  # weak: S = 8 per GPU, same batch everywhere
         S_loc, B = cfg["S_per_gpu"], cfg["B"]
         return dict(S=S_loc * world, S_loc=S_loc, B=B, B_loc=B, K=world, G=1, mode="sample",
                     scaling="weak")
@@ -153,6 +154,9 @@ def oracle_slice(model, B, budget_s, aug="none"):
     a = O.AUG_PER_SAMPLE if aug == "per_sample" else O.AUG_NONE
 
     def run(S_s, B_s):
+        if model["kind"] == "vit":
+            O.vit_elbo_partial(model, mu, rho, x[:B_s], yc[:B_s], B, 0, 64, 0, S_s, 0x5EED, 0, a)
+            return
         O.elbo_partial(model, mu, rho, x[:B_s], None if yc is None else yc[:B_s],
                        None if yr is None else yr[:B_s], B, 0, 64, 0, S_s, 0x5EED, 0, a)
 
@@ -502,6 +506,8 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
                 # context: the standalone generator's measured rate (scripts/eps_rate.py; the
                 # fused kernels also load μ/σ, build and store W_s tiles, run the epilogue)
                 **_standalone_eps(ach)}
+    if model["kind"] == "vit":
+        return vit_roofline(model, B, S_loc, prof, steps, peaks, peak_src)
     convs = conv_layers(model)
     f_all = sum(2 * B * oh * ow * co * k * k * ci for k, st, ci, co, oh, ow in convs)
     f_nostem = f_all - 2 * B * convs[0][4] * convs[0][5] * convs[0][3] * 9 * convs[0][2]
@@ -515,6 +521,31 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
             "unit": "TFLOP/s", "frac": ach / peak, "traffic": _ncu_traffic("cnn", dom),
             "peak_source": f"measured bf16 sustained ({peak_src}, MEASURED_PEAKS.json); "
                            f"burst {peaks.get('bf16_tflops')}"}
+
+
+def vit_flops(model, B):
+    """GEMM-shaped FLOP of one forward per sample (projections + attention products)."""
+    D, M, h, L = model["dim"], model["mlp"], model["heads"], model["depth"]
+    T = 1 + (model["in_h"] // model["patch"]) * (model["in_w"] // model["patch"])
+    pk = model["patch"] ** 2 * model["in_c"]
+    proj = 2 * B * T * L * (3 * D * D + D * D + 2 * D * M) + 2 * B * (T - 1) * pk * D + 2 * B * D * model["n_classes"]
+    attn = 2 * 2 * B * L * h * T * T * (D // h)
+    return proj, attn
+
+
+def vit_roofline(model, B, S_loc, prof, steps, peaks, peak_src):
+    """The ViT's sampled projections (fwd + dgrad + wgrad classes) against the FP32 FMA peak
+    (FP32 mode: SIMT kernels; 148 SM × 128 FMA/clk × 2 FLOP × f_max)."""
+    proj, attn = vit_flops(model, B)
+    ms = sum(prof[k]["ms"] for k in ("fwd", "dgrad", "wgrad") if k in prof) / steps
+    fl = 3 * proj * S_loc
+    clk = peaks.get("sm_max_mhz", 1965.0)
+    peak = 148 * 128 * 2 * clk * 1e6 / 1e12
+    ach = fl / (ms / 1e3) / 1e12
+    return {"kernel": "fwd+dgrad+wgrad (sampled projections)", "ms_per_step": ms, "bound": "alu", "achieved": ach,
+            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
+            "peak_source": f"derived FP32 FMA peak: 148 SM x 128 lanes x 2 FLOP x {clk:.0f} MHz",
+            "attention_tflop_per_step": 3 * attn * S_loc / 1e12}
 
 
 def _standalone_eps(achieved):
@@ -565,9 +596,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5", "C6"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5", "C6", "C7"])
     ap.add_argument("--mode", default=None, choices=["sample", "data"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default=None, choices=["bf16", "fp32"],
+                    help="default bf16 (C7, the ViT: fp32)")
     ap.add_argument("--sample-chunk", type=int, default=0,
                     help="samples per pass through the network (0: the library default, all local samples)")
     ap.add_argument("--ref-budget", type=float, default=None,
@@ -589,6 +621,8 @@ def main():
     if args.gpus != world:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
         sys.exit(2)
+    if args.precision is None:
+        args.precision = "fp32" if args.config == "C7" else "bf16"
     if args.warmup < 3 and not args.profile_run:
         print("bench.py: --warmup must be >= 3", file=sys.stderr)
         sys.exit(2)

@@ -217,6 +217,8 @@ struct bnn_ctx {
     float *vdX = nullptr, *vdH = nullptr, *vdQKV = nullptr, *vdO = nullptr, *vdU = nullptr, *vdyxh = nullptr,
           *vdE = nullptr, *vdHc = nullptr;
     std::vector<VitAct> vl;
+    float* vwpart = nullptr;  // row-split wgrad partials
+    int64_t vwpart_cap = 0;
     std::vector<float*> vvec;  // sampled 1-D tensors [chunk][n] (LayerNorm g/b, cls, pos), else null
     std::vector<CUtensorMap> cmap_hf, cmap_hd;  // conv3 HALO: 1-row (W + 2)-pixel boxes of the input / dY
     std::vector<char> halo_fwd, halo_dgrad;

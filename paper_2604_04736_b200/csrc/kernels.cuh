@@ -98,9 +98,14 @@ void launch_dgrad_fp32(const SampledLayer& L, const SampleKeys& k, const DropArg
                        int64_t strideD, cudaStream_t st);
 // acc_μ[n][k] += scale·Σ_s dW_s[n][k]; acc_ρ[n][k] += scale·Σ_s dW_s[n][k]·ε_s[n][k] with
 // dW_s = Σ_b G[s][b][n]·A[s][b][k]; plus the bias: db_s[n] = Σ_b G[s][b][n].
+// part (optional, capacity part_cap floats): split the B rows over blocks (the ViT's token rows)
+// with scaled partials [split][μ|ρ][N·K] reduced in split order into acc (deterministic).
 void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
                        int64_t strideG, const float* A, int64_t strideA, float scale,
-                       float* acc_mu, float* acc_rho, cudaStream_t st);
+                       float* acc_mu, float* acc_rho, cudaStream_t st, float* part = nullptr,
+                       int64_t part_cap = 0);
+void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off, float* acc_mu,
+                               float* acc_rho, cudaStream_t st);
 // bias gradient from fp32 partial column sums parts[s][p][n] (p < nparts, row pitch ldp)
 // all bias tensors of up to 4 layers in two launches (per-layer parts as launch_bias_grad;
 // db_scratch holds 2·S·N_l floats per layer, consecutively)

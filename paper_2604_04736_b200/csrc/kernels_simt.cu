@@ -781,10 +781,14 @@ __global__ void __launch_bounds__(256) wgrad_fp32_kernel(SampledLayer L, SampleK
                                                          const float* __restrict__ A,
                                                          int64_t strideA, float scale,
                                                          float* __restrict__ acc_mu,
-                                                         float* __restrict__ acc_rho) {
+                                                         float* __restrict__ acc_rho, int rows_per,
+                                                         float* __restrict__ part) {
     __shared__ float Gs[TK][TB + 4];  // [b][n]
     __shared__ float As[TK][TB + 4];  // [b][k]
     const int kt0 = blockIdx.x * TB, n0 = blockIdx.y * TB;
+    // row split z (the ViT's token rows): rows [z·rows_per, …) of every sample; the scaled
+    // partial sums go to part[z][μ|ρ][N·K] and a fixed-order reduction adds them to acc
+    const int r0 = blockIdx.z * rows_per, r1 = min(B, r0 + rows_per);
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int N = L.N, K = L.K;
     float am[4][4] = {}, ar[4][4] = {};
@@ -792,14 +796,14 @@ __global__ void __launch_bounds__(256) wgrad_fp32_kernel(SampledLayer L, SampleK
         const float* Gg = G + s * strideG;
         const float* Ag = A + s * strideA;
         float d[4][4] = {};
-        for (int b0 = 0; b0 < B; b0 += TK) {
+        for (int b0 = r0; b0 < r1; b0 += TK) {
             {
                 const int bb = tid >> 4, q = (tid & 15) * 4;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int n = n0 + q + j, k = kt0 + q + j, b = b0 + bb;
-                    Gs[bb][q + j] = (b < B && n < N) ? Gg[(int64_t)b * N + n] : 0.0f;
-                    As[bb][q + j] = (b < B && k < K) ? Ag[(int64_t)b * K + k] : 0.0f;
+                    Gs[bb][q + j] = (b < r1 && n < N) ? Gg[(int64_t)b * N + n] : 0.0f;
+                    As[bb][q + j] = (b < r1 && k < K) ? Ag[(int64_t)b * K + k] : 0.0f;
                 }
             }
             __syncthreads();
@@ -838,19 +842,34 @@ __global__ void __launch_bounds__(256) wgrad_fp32_kernel(SampledLayer L, SampleK
         for (int j = 0; j < 4; ++j) {
             const int k = kt0 + tx * 4 + j;
             if (k >= K) continue;
-            const int64_t o = L.off_w + (int64_t)n * K + k;
-            acc_mu[o] += scale * am[i][j];
-            acc_rho[o] += scale * ar[i][j];
+            if (part) {
+                const int64_t nk = (int64_t)N * K, o = (int64_t)n * K + k;
+                part[(int64_t)blockIdx.z * 2 * nk + o] = scale * am[i][j];
+                part[(int64_t)blockIdx.z * 2 * nk + nk + o] = scale * ar[i][j];
+            } else {
+                const int64_t o = L.off_w + (int64_t)n * K + k;
+                acc_mu[o] += scale * am[i][j];
+                acc_rho[o] += scale * ar[i][j];
+            }
         }
     }
 }
 
 void launch_wgrad_fp32(const SampledLayer& L, const SampleKeys& k, int S, int B, const float* G,
                        int64_t strideG, const float* A, int64_t strideA, float scale,
-                       float* acc_mu, float* acc_rho, cudaStream_t st) {
-    dim3 grid((L.K + TB - 1) / TB, (L.N + TB - 1) / TB);
+                       float* acc_mu, float* acc_rho, cudaStream_t st, float* part, int64_t part_cap) {
+    const int tiles = ((L.K + TB - 1) / TB) * ((L.N + TB - 1) / TB);
+    int nsplit = 1;
+    if (part) {  // enough row splits for ≈ 2 blocks per SM, within the scratch capacity
+        nsplit = std::max(1, std::min({(2 * kNumSMs + tiles - 1) / tiles, (B + TK - 1) / TK,
+                                       (int)(part_cap / (2 * (int64_t)L.N * L.K))}));
+    }
+    const int rows_per = ((B + nsplit - 1) / nsplit + TK - 1) / TK * TK;
+    nsplit = (B + rows_per - 1) / rows_per;
+    dim3 grid((L.K + TB - 1) / TB, (L.N + TB - 1) / TB, nsplit);
     wgrad_fp32_kernel<<<grid, 256, 0, st>>>(L, k, S, B, G, strideG, A, strideA, scale, acc_mu,
-                                            acc_rho);
+                                            acc_rho, rows_per, nsplit > 1 ? part : nullptr);
+    if (nsplit > 1) launch_wgrad_split_reduce(part, nsplit, (int64_t)L.N * L.K, L.off_w, acc_mu, acc_rho, st);
 }
 
 // Bias gradient in two deterministic phases. parts[s][p][n] are fp32 partial column sums

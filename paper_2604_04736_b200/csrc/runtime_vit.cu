@@ -115,6 +115,8 @@ int alloc_vit(bnn_ctx* c) {
     for (int t = 0; t < (int)c->vtens.size(); ++t)
         if (want(t) && !c->alloc(&c->vvec[t], (size_t)Sc * c->vtens[t].cols))
             return c->set_err(BNN_ERR_CUDA, "out of memory (ViT sampled vectors)");
+    c->vwpart_cap = (int64_t)4 << 20;  // row-split wgrad partials (launch_wgrad_fp32), 16 MB
+    if (!c->alloc(&c->vwpart, (size_t)c->vwpart_cap)) return c->set_err(BNN_ERR_CUDA, "out of memory");
     const int maxN = std::max({M, 3 * D, T * D, c->O});
     if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
     return BNN_OK;
@@ -198,8 +200,7 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
     {
         const SampledLayer Lh = lin(c, mu, nt - 2);
         c->launch("wgrad", [&] {
-            launch_wgrad_fp32(Lh, kk, Sc, B, c->dz_f32, (int64_t)B * c->O, c->vHc, (int64_t)B * D, scale, acc_mu,
-                              acc_rho, st);
+            launch_wgrad_fp32(Lh, kk, Sc, B, c->dz_f32, (int64_t)B * c->O, c->vHc, (int64_t)B * D, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap);
         });
         bias(Lh, c->dz_f32, B, c->O, (int64_t)B * c->O);
         c->launch("dgrad", [&] {
@@ -219,11 +220,11 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
         const SampledLayer Lq = lin(c, mu, tb + 2), Lo = lin(c, mu, tb + 4), L1 = lin(c, mu, tb + 8),
                            L2 = lin(c, mu, tb + 10);
         // X_out = X_mid + fc2(GELU(fc1(LN2(X_mid))))
-        c->launch("wgrad", [&] { launch_wgrad_fp32(L2, kk, Sc, (int)R, c->vdX, RD, a.A, R * M, scale, acc_mu, acc_rho, st); });
+        c->launch("wgrad", [&] { launch_wgrad_fp32(L2, kk, Sc, (int)R, c->vdX, RD, a.A, R * M, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(L2, c->vdX, (int)R, D, RD);
         c->launch("dgrad", [&] { launch_dgrad_fp32(L2, kk, nod, Sc, (int)R, c->vdX, RD, nullptr, 0, c->vdU, R * M, st); });
         c->launch("elem", [&] { launch_vit_gelu_bwd(a.U, Sc * R * M, c->vdU, st); });
-        c->launch("wgrad", [&] { launch_wgrad_fp32(L1, kk, Sc, (int)R, c->vdU, R * M, a.H2, RD, scale, acc_mu, acc_rho, st); });
+        c->launch("wgrad", [&] { launch_wgrad_fp32(L1, kk, Sc, (int)R, c->vdU, R * M, a.H2, RD, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(L1, c->vdU, (int)R, M, R * M);
         c->launch("dgrad", [&] { launch_dgrad_fp32(L1, kk, nod, Sc, (int)R, c->vdU, R * M, nullptr, 0, c->vdH, RD, st); });
         c->launch("ln", [&] {
@@ -232,11 +233,11 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
         bias(vec(c, mu, tb + 6), c->vdyxh, (int)R, D, RD);
         bias(vec(c, mu, tb + 7), c->vdH, (int)R, D, RD);
         // X_mid = X + proj(attention(LN1(X)))
-        c->launch("wgrad", [&] { launch_wgrad_fp32(Lo, kk, Sc, (int)R, c->vdX, RD, a.O, RD, scale, acc_mu, acc_rho, st); });
+        c->launch("wgrad", [&] { launch_wgrad_fp32(Lo, kk, Sc, (int)R, c->vdX, RD, a.O, RD, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(Lo, c->vdX, (int)R, D, RD);
         c->launch("dgrad", [&] { launch_dgrad_fp32(Lo, kk, nod, Sc, (int)R, c->vdX, RD, nullptr, 0, c->vdO, RD, st); });
         c->launch("attn", [&] { launch_vit_attn_bwd(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
-        c->launch("wgrad", [&] { launch_wgrad_fp32(Lq, kk, Sc, (int)R, c->vdQKV, 3 * RD, a.H1, RD, scale, acc_mu, acc_rho, st); });
+        c->launch("wgrad", [&] { launch_wgrad_fp32(Lq, kk, Sc, (int)R, c->vdQKV, 3 * RD, a.H1, RD, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
         c->launch("dgrad", [&] { launch_dgrad_fp32(Lq, kk, nod, Sc, (int)R, c->vdQKV, 3 * RD, nullptr, 0, c->vdH, RD, st); });
         c->launch("ln", [&] {
@@ -254,7 +255,7 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
     c->launch("elem", [&] { launch_vit_gather_tokens(c->vdX, Sc, B, T, 1, NP, D, c->vdE, st); });
     const SampledLayer Lp = lin(c, mu, 0);
     c->launch("wgrad", [&] {
-        launch_wgrad_fp32(Lp, kk, Sc, B * NP, c->vdE, (int64_t)B * NP * D, c->vP, sP, scale, acc_mu, acc_rho, st);
+        launch_wgrad_fp32(Lp, kk, Sc, B * NP, c->vdE, (int64_t)B * NP * D, c->vP, sP, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap);
     });
     bias(Lp, c->vdE, B * NP, D, (int64_t)B * NP * D);
     return BNN_OK;
