@@ -419,7 +419,7 @@ def run_ours(args, world, rank, local_rank):
                                   "untimed steps (profiling off in the timed region)"}
         if ddp is not None:
             line["ddp_comparison"] = ddp
-        line["roofline"] = roofline(model, B_loc, S_loc, prof, prof_steps, peaks, peak_src)
+        line["roofline"] = roofline(model, B_loc, S_loc, prof, prof_steps, peaks, peak_src, args.precision == "bf16")
         if world == 1 and not args.no_cpu_baseline:
             r, cores, sample = cpu_oracle_rate(MODELS[cfg["model"]], B, args.ref_budget,
                                                aug=cfg.get("aug", "none"))
@@ -456,7 +456,7 @@ def conv_layers(model):
     return out
 
 
-def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
+def roofline(model, B, S_loc, prof, steps, peaks, peak_src, bf16=True):
     """Dominant kernel class vs its bound.
 
     MLP: the sampled-GEMM kernels are ALU-bound by ε regeneration; unit =
@@ -507,7 +507,7 @@ def roofline(model, B, S_loc, prof, steps, peaks, peak_src):
                 # fused kernels also load μ/σ, build and store W_s tiles, run the epilogue)
                 **_standalone_eps(ach)}
     if model["kind"] == "vit":
-        return vit_roofline(model, B, S_loc, prof, steps, peaks, peak_src)
+        return vit_roofline(model, B, S_loc, prof, steps, peaks, peak_src, bf16)
     convs = conv_layers(model)
     f_all = sum(2 * B * oh * ow * co * k * k * ci for k, st, ci, co, oh, ow in convs)
     f_nostem = f_all - 2 * B * convs[0][4] * convs[0][5] * convs[0][3] * 9 * convs[0][2]
@@ -533,19 +533,29 @@ def vit_flops(model, B):
     return proj, attn
 
 
-def vit_roofline(model, B, S_loc, prof, steps, peaks, peak_src):
-    """The ViT's sampled projections (fwd + dgrad + wgrad classes) against the FP32 FMA peak
-    (FP32 mode: SIMT kernels; 148 SM × 128 FMA/clk × 2 FLOP × f_max)."""
+def vit_roofline(model, B, S_loc, prof, steps, peaks, peak_src, bf16):
+    """The ViT's sampled projections (fwd + dgrad + wgrad classes): BF16 — tcgen05 against the
+    measured bf16 peak (W_s is regenerated per 256-row tile, so like C2 the generator's ALU work
+    is the co-limiter); FP32 — SIMT against the FP32 FMA peak (148 SM × 128 FMA/clk × 2 × f_max)."""
     proj, attn = vit_flops(model, B)
     ms = sum(prof[k]["ms"] for k in ("fwd", "dgrad", "wgrad") if k in prof) / steps
     fl = 3 * proj * S_loc
-    clk = peaks.get("sm_max_mhz", 1965.0)
-    peak = 148 * 128 * 2 * clk * 1e6 / 1e12
     ach = fl / (ms / 1e3) / 1e12
-    return {"kernel": "fwd+dgrad+wgrad (sampled projections)", "ms_per_step": ms, "bound": "alu", "achieved": ach,
-            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-            "peak_source": f"derived FP32 FMA peak: 148 SM x 128 lanes x 2 FLOP x {clk:.0f} MHz",
-            "attention_tflop_per_step": 3 * attn * S_loc / 1e12}
+    if bf16:
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        src = f"measured bf16 sustained ({peak_src}, MEASURED_PEAKS.json)"
+        bound = "tensor"
+    else:
+        clk = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * clk * 1e6 / 1e12
+        src = f"derived FP32 FMA peak: 148 SM x 128 lanes x 2 FLOP x {clk:.0f} MHz"
+        bound = "alu"
+    step_ms = sum(v["ms"] for v in prof.values()) / steps
+    return {"kernel": "fwd+dgrad+wgrad (sampled projections)", "ms_per_step": ms, "bound": bound, "achieved": ach,
+            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "traffic": None, "peak_source": src,
+            "attention_ms_per_step": prof.get("attn", {}).get("ms", 0.0) / steps,
+            "attention_tflop_per_step": 3 * attn * S_loc / 1e12,
+            "projection_share_of_profiled_step": ms / step_ms if step_ms else None}
 
 
 def _standalone_eps(achieved):

@@ -79,6 +79,7 @@ def lib():
             C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_int]
         _lib.orc_vit_forward.argtypes = [C.c_void_p] * 4 + [C.c_int] * 3 + [C.c_uint64, C.c_uint32, C.c_int,
                                                                              C.c_void_p]
+        _lib.orc_vit_set_emu_weights.argtypes = [C.c_int]
         _lib.orc_finalize_p.argtypes = [C.c_long] + [C.c_void_p] * 3 + [C.c_double] + [C.c_void_p] * 4
     return _lib
 
@@ -113,8 +114,10 @@ def vit_tensor_infos(model):
 
 
 def vit_elbo_partial(model, mu, rho, x, y_cls, B_glob, b_offset, S_glob, s0, s1, seed, step, aug=AUG_NONE,
-                     nthreads=0):
-    """[acc_μ (P) | acc_ρ (P) | L_data] of samples [s0, s1) (vit_oracle.c)."""
+                     nthreads=0, emu=False):
+    """[acc_μ (P) | acc_ρ (P) | L_data] of samples [s0, s1) (vit_oracle.c). emu="weights": only the
+    BF16 mode's sampled weights RN_bf16(fma_f32(σ, ε, μ)) (R14), the rest exact (conditioning probe)."""
+    lib().orc_vit_set_emu_weights(1 if emu == "weights" else 0)
     v = vit_struct(model)
     P = vit_n_params(model)
     mu, rho, x = _d(mu), _d(rho), _d(x)
@@ -122,6 +125,7 @@ def vit_elbo_partial(model, mu, rho, x, y_cls, B_glob, b_offset, S_glob, s0, s1,
     acc = np.zeros(2 * P + 1, np.float64)
     rc = lib().orc_vit_elbo_partial(C.byref(v), _p(mu), _p(rho), _p(x), _p(yc), x.shape[0], b_offset, B_glob,
                                     S_glob, s0, s1, seed, step, aug, _p(acc), nthreads)
+    lib().orc_vit_set_emu_weights(0)
     assert rc == 0, rc
     return acc
 

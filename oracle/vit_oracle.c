@@ -116,6 +116,21 @@ int orc_vit_tensor_info(const orc_vit* m, int t, long* info)
 static double softplus(double r) { return (r > 0 ? r : 0.0) + log1p(exp(-fabs(r))); }
 
 /* w_s = μ + σ ε_s for every parameter of global sample s (ε fp32 bits widened). eps_out keeps ε. */
+/* BF16 mode's sampled weight (reading R14): RN_bf16(fma_f32(σ, ε, μ)) — used only by
+ * the conditioning probe (emu_w = 1), the exact oracle keeps fp64 weights */
+static double bf16_weight(double mu, double sigma, double e)
+{
+    float w = fmaf((float)sigma, (float)e, (float)mu);
+    uint32_t u;
+    memcpy(&u, &w, 4);
+    uint32_t lsb = (u >> 16) & 1u;
+    u = (u + 0x7FFFu + lsb) & 0xFFFF0000u;
+    memcpy(&w, &u, 4);
+    return (double)w;
+}
+
+static int g_emu_w = 0;
+
 static void vit_sample(const VGeo* g, const double* mu, const double* sigma, uint64_t seed, uint32_t step,
                        uint32_t s, double* W, double* eps_out)
 {
@@ -126,7 +141,7 @@ static void vit_sample(const VGeo* g, const double* mu, const double* sigma, uin
                 long i = g->off[t] + r * g->cols[t] + c;
                 double e = (double)orc_eps(seed, step, s, (uint32_t)t, (uint32_t)r, (uint32_t)c);
                 eps_out[i] = e;
-                W[i] = mu[i] + sigma[i] * e;
+                W[i] = g_emu_w ? bf16_weight(mu[i], sigma[i], e) : mu[i] + sigma[i] * e;
             }
     }
 }
@@ -425,6 +440,10 @@ static double ce_loss(const double* z, int O, int y, double* dz)
  *   acc[0 .. P) += Σ_s Σ_b dℓ/dw / (S·B_glob); acc[P .. 2P) += Σ_s ε_s ⊙ Σ_b dℓ/dw / (S·B_glob);
  *   acc[2P] += Σ_s Σ_b ℓ / (S·B_glob). Fixed summation order for a fixed thread count.
  */
+/* emu_w = 1: the sampled weights as the BF16 mode defines them (R14), everything else exact —
+ * the conditioning probe of the BF16 tolerance (tests/test_conditioning.py) */
+void orc_vit_set_emu_weights(int on) { g_emu_w = on; }
+
 int orc_vit_elbo_partial(const orc_vit* m, const double* mu, const double* rho, const double* x, const int* ycls,
                          int B_loc, int b_offset, int B_glob, int S_glob, int s0, int s1, uint64_t seed,
                          uint32_t step, int aug, double* acc, int nthreads)

@@ -217,6 +217,17 @@ struct bnn_ctx {
     float *vdX = nullptr, *vdH = nullptr, *vdQKV = nullptr, *vdO = nullptr, *vdU = nullptr, *vdyxh = nullptr,
           *vdE = nullptr, *vdHc = nullptr;
     std::vector<VitAct> vl;
+    // BF16 mode: bf16 GEMM operands and the tcgen05 descriptors of every projection
+    struct VitB {
+        __nv_bfloat16 *H1 = nullptr, *O = nullptr, *H2 = nullptr, *A = nullptr;
+    };
+    struct VitMaps {
+        CUtensorMap fwd, dg, wg_g, wg_x;
+    };
+    std::vector<VitB> vlb;
+    std::vector<VitMaps> vmaps;  // [0] patch, [1 + 4l + {0 qkv, 1 proj, 2 fc1, 3 fc2}], [last] head
+    __nv_bfloat16 *vPb = nullptr, *vHcb = nullptr, *vdXb = nullptr, *vdXb2 = nullptr, *vdUb = nullptr,
+                  *vdQKVb = nullptr, *vdEb = nullptr, *vdzb = nullptr;
     float* vwpart = nullptr;  // row-split wgrad partials
     int64_t vwpart_cap = 0;
     std::vector<float*> vvec;  // sampled 1-D tensors [chunk][n] (LayerNorm g/b, cls, pos), else null
@@ -363,6 +374,8 @@ int build_vit(bnn_ctx* c);
 int alloc_vit(bnn_ctx* c);
 int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, int B, int B_glob, int S_glob,
               int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss);
+int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, int B, int B_glob, int S_glob,
+                   int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss);
 
 // ResNet entry points (runtime_resnet.cu)
 int alloc_resnet_bf16(bnn_ctx* c);

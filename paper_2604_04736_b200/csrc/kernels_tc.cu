@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
             } else {
                 __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + s * a.out_stride_s +
                                    (int64_t)bc0 * a.ldo + m;
+                float* of = reinterpret_cast<float*>(a.out) + s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
                 float part = 0.0f;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -321,7 +322,11 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
                             (!a.mask || (mraw[j] != 0 && (mraw[j] & 0x8000u) == 0))
                                 ? (a.drop.on ? v[j] * a.drop.inv_keep : v[j]) : 0.0f;
                         part += g;
-                        o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
+                        // out_f32: the ViT's dgrad outputs feed fp32 LayerNorm / GELU / attention backward
+                        if (a.out_f32)
+                            of[(int64_t)j * a.ldo] = g;
+                        else
+                            o[(int64_t)j * a.ldo] = __float2bfloat16_rn(g);
                     }
                 }
                 // fp32 partial column sum over this 16-row chunk: the bias gradient source

@@ -19,7 +19,7 @@ struct TcGenArgs {
     int b_shared;        // B operand is shared by all samples (layer-0 input)
     int M, R;
     int nb;              // MMA N: round_up(min(B, 256), 16)
-    void* out;           // fwd: bf16 activations or fp32 logits; dgrad: bf16 gradients
+    void* out;           // fwd: bf16 activations or fp32 logits; dgrad: bf16 gradients (fp32: out_f32)
     int64_t out_stride_s;
     int ldo;
     int out_f32, relu;

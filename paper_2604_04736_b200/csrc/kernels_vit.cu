@@ -8,12 +8,18 @@
 // oracle/vit_oracle.c's definitions (LN eps 1e-6 with the biased variance; scores / √dh;
 // exact-erf GELU) — written independently, no shared code.
 #include <algorithm>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
 #include "kernels_vit.cuh"
 
 namespace bnn {
+
+__device__ __forceinline__ float ldf(const float* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ float ldf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
+__device__ __forceinline__ void stf(float* p, int64_t i, float v) { p[i] = v; }
+__device__ __forceinline__ void stf(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
 
 // ------------------------------------------------------------------------ sampled vectors
 // w[s][i] = μ[off + i] + σ[off + i]·ε(t, 0, i) for the 1-D tensors (LayerNorm g/b, cls, pos)
@@ -31,8 +37,9 @@ void launch_vit_sample_vec(const float* mu, const float* sigma, int64_t off, uin
 
 // ------------------------------------------------------------------------ patches
 // P[s][b][pi][(dy·p + dx)·C + c] of the (crop + flip augmented, docs/EPS.md §4) image b
+template <class TO>
 __global__ void vit_patchify_kernel(const float* __restrict__ x, int B, int H, int W, int C, int p, int aug,
-                                    EpsKey key, uint32_t step, uint32_t s0, int b_off, float* __restrict__ P) {
+                                    EpsKey key, uint32_t step, uint32_t s0, int b_off, TO* __restrict__ P) {
     const int b = blockIdx.x, s = blockIdx.y;
     int dx = 4, dy = 4, flip = 0;
     if (aug) {
@@ -43,20 +50,25 @@ __global__ void vit_patchify_kernel(const float* __restrict__ x, int B, int H, i
     }
     const float* src = x + (int64_t)b * H * W * C;
     const int pw = W / p, pk = p * p * C, np = (H / p) * pw;
-    float* dst = P + ((int64_t)s * B + b) * np * pk;
+    TO* dst = P + ((int64_t)s * B + b) * np * pk;
     for (int i = threadIdx.x; i < np * pk; i += blockDim.x) {
         const int pi = i / pk, e = i - pi * pk;
         const int c = e % C, q = e / C, ddx = q % p, ddy = q / p;
         const int r = (pi / pw) * p + ddy, cc = (pi % pw) * p + ddx;
         const int jj = flip ? W - 1 - cc : cc;
         const int si = r + dy - 4, sj = jj + dx - 4;
-        dst[i] = (si >= 0 && si < H && sj >= 0 && sj < W) ? src[((int64_t)si * W + sj) * C + c] : 0.0f;
+        stf(dst, i, (si >= 0 && si < H && sj >= 0 && sj < W) ? src[((int64_t)si * W + sj) * C + c] : 0.0f);
     }
 }
 
 void launch_vit_patchify(const float* x, int S, int B, int H, int W, int C, int p, int aug, uint64_t seed,
                          uint32_t step, uint32_t s0, int b_off, float* P, cudaStream_t st) {
-    vit_patchify_kernel<<<dim3(B, S), 256, 0, st>>>(x, B, H, W, C, p, aug, make_key(seed), step, s0, b_off, P);
+    vit_patchify_kernel<float><<<dim3(B, S), 256, 0, st>>>(x, B, H, W, C, p, aug, make_key(seed), step, s0, b_off, P);
+}
+void launch_vit_patchify(const float* x, int S, int B, int H, int W, int C, int p, int aug, uint64_t seed,
+                         uint32_t step, uint32_t s0, int b_off, __nv_bfloat16* P, cudaStream_t st) {
+    vit_patchify_kernel<__nv_bfloat16><<<dim3(B, S), 256, 0, st>>>(x, B, H, W, C, p, aug, make_key(seed), step, s0,
+                                                                    b_off, P);
 }
 
 // X0[s][b][0] = cls_s + pos_s[0];  X0[s][b][t] = E[s][b][t−1] + pos_s[t]
@@ -79,8 +91,9 @@ void launch_vit_embed(const float* E, const float* cls, const float* pos, int S,
 // ------------------------------------------------------------------------ LayerNorm
 // one warp per row; rows of one sample are `rows` rows `ld` floats apart (ld = D: all tokens;
 // ld = T·D: the cls rows); g, b: sampled [s][D]
+template <class TY>
 __global__ void vit_ln_fwd_kernel(const float* __restrict__ X, int rows, int64_t ld, int64_t sX, int D,
-                                  const float* __restrict__ g, const float* __restrict__ bb, float* __restrict__ Y,
+                                  const float* __restrict__ g, const float* __restrict__ bb, TY* __restrict__ Y,
                                   int64_t ldy, int64_t sY, float* __restrict__ stats) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, s = blockIdx.y;
     if (warp >= rows) return;
@@ -93,8 +106,8 @@ __global__ void vit_ln_fwd_kernel(const float* __restrict__ X, int rows, int64_t
     for (int i = lane; i < D; i += 32) sq += (x[i] - mean) * (x[i] - mean);
     for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
     const float rstd = rsqrtf(sq / D + 1e-6f);
-    float* y = Y + s * sY + warp * ldy;
-    for (int i = lane; i < D; i += 32) y[i] = g[(int64_t)s * D + i] * ((x[i] - mean) * rstd) + bb[(int64_t)s * D + i];
+    TY* y = Y + s * sY + warp * ldy;
+    for (int i = lane; i < D; i += 32) stf(y, i, g[(int64_t)s * D + i] * ((x[i] - mean) * rstd) + bb[(int64_t)s * D + i]);
     if (lane == 0) {
         stats[((int64_t)s * rows + warp) * 2] = mean;
         stats[((int64_t)s * rows + warp) * 2 + 1] = rstd;
@@ -103,21 +116,27 @@ __global__ void vit_ln_fwd_kernel(const float* __restrict__ X, int rows, int64_t
 
 void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, int D, const float* g, const float* b,
                        float* Y, int64_t ldy, int64_t sY, float* stats, cudaStream_t st) {
-    vit_ln_fwd_kernel<<<dim3((rows + 7) / 8, S), 256, 0, st>>>(X, rows, ld, sX, D, g, b, Y, ldy, sY, stats);
+    vit_ln_fwd_kernel<float><<<dim3((rows + 7) / 8, S), 256, 0, st>>>(X, rows, ld, sX, D, g, b, Y, ldy, sY, stats);
+}
+void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, int D, const float* g, const float* b,
+                       __nv_bfloat16* Y, int64_t ldy, int64_t sY, float* stats, cudaStream_t st) {
+    vit_ln_fwd_kernel<__nv_bfloat16><<<dim3((rows + 7) / 8, S), 256, 0, st>>>(X, rows, ld, sX, D, g, b, Y, ldy, sY,
+                                                                              stats);
 }
 
 // dX += rstd·(dx̂ − mean(dx̂) − x̂·mean(dx̂ ⊙ x̂)), dx̂ = dY ⊙ g; dyxh = dY ⊙ x̂ (the g-gradient rows)
-__global__ void vit_ln_bwd_kernel(const float* __restrict__ dY, int64_t ldy, int64_t sdY, const float* __restrict__ X,
+template <class TD>
+__global__ void vit_ln_bwd_kernel(const TD* __restrict__ dY, int64_t ldy, int64_t sdY, const float* __restrict__ X,
                                   int rows, int64_t ld, int64_t sX, int D, const float* __restrict__ g,
                                   const float* __restrict__ stats, float* __restrict__ dX, float* __restrict__ dyxh) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, s = blockIdx.y;
     if (warp >= rows) return;
     const float mean = stats[((int64_t)s * rows + warp) * 2], rstd = stats[((int64_t)s * rows + warp) * 2 + 1];
     const float* x = X + s * sX + warp * ld;
-    const float* dy = dY + s * sdY + warp * ldy;
+    const TD* dy = dY + s * sdY + warp * ldy;
     float m1 = 0.f, m2 = 0.f;
     for (int i = lane; i < D; i += 32) {
-        const float xh = (x[i] - mean) * rstd, dxh = dy[i] * g[(int64_t)s * D + i];
+        const float xh = (x[i] - mean) * rstd, dxh = ldf(dy, i) * g[(int64_t)s * D + i];
         m1 += dxh;
         m2 += dxh * xh;
     }
@@ -131,21 +150,29 @@ __global__ void vit_ln_bwd_kernel(const float* __restrict__ dY, int64_t ldy, int
     float* dg = dyxh + ((int64_t)s * rows + warp) * D;
     for (int i = lane; i < D; i += 32) {
         const float xh = (x[i] - mean) * rstd;
-        dx[i] += rstd * (dy[i] * g[(int64_t)s * D + i] - m1 - xh * m2);
-        dg[i] = dy[i] * xh;
+        const float d = ldf(dy, i);
+        dx[i] += rstd * (d * g[(int64_t)s * D + i] - m1 - xh * m2);
+        dg[i] = d * xh;
     }
 }
 
 void launch_vit_ln_bwd(const float* dY, int64_t ldy, int64_t sdY, const float* X, int S, int rows, int64_t ld,
                        int64_t sX, int D, const float* g, const float* stats, float* dX, float* dyxh, cudaStream_t st) {
-    vit_ln_bwd_kernel<<<dim3((rows + 7) / 8, S), 256, 0, st>>>(dY, ldy, sdY, X, rows, ld, sX, D, g, stats, dX, dyxh);
+    vit_ln_bwd_kernel<float><<<dim3((rows + 7) / 8, S), 256, 0, st>>>(dY, ldy, sdY, X, rows, ld, sX, D, g, stats, dX,
+                                                                        dyxh);
+}
+void launch_vit_ln_bwd(const __nv_bfloat16* dY, int64_t ldy, int64_t sdY, const float* X, int S, int rows, int64_t ld,
+                       int64_t sX, int D, const float* g, const float* stats, float* dX, float* dyxh, cudaStream_t st) {
+    vit_ln_bwd_kernel<__nv_bfloat16><<<dim3((rows + 7) / 8, S), 256, 0, st>>>(dY, ldy, sdY, X, rows, ld, sX, D, g, stats,
+                                                                                dX, dyxh);
 }
 
 // ------------------------------------------------------------------------ attention
 // block = (head h, example b, sample s); QKV rows [T][3D] (Q | K | V, head h at columns h·dh …);
 // O[t][h·dh + e]; A[s][b][h][T][T] kept for the backward. One warp per query row.
+template <class TO>
 __global__ void vit_attn_fwd_kernel(const float* __restrict__ QKV, int B, int T, int D, int dh,
-                                    float* __restrict__ O, float* __restrict__ A) {
+                                    TO* __restrict__ O, float* __restrict__ A) {
     extern __shared__ float sm[];
     const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -189,28 +216,37 @@ __global__ void vit_attn_fwd_kernel(const float* __restrict__ QKV, int B, int T,
         for (int e = lane; e < dh; e += 32) {
             float acc = 0.f;
             for (int j = 0; j < T; ++j) acc += pr[j] * Vs[j * dh + e];
-            O[(((int64_t)s * B + b) * T + i) * D + h * dh + e] = acc;
+            stf(O, (((int64_t)s * B + b) * T + i) * D + h * dh + e, acc);
         }
         __syncwarp();
     }
 }
 
-void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A,
-                         cudaStream_t st) {
+template <class TO>
+static void attn_fwd_t(const float* QKV, int S, int B, int T, int D, int heads, TO* O, float* A, cudaStream_t st) {
     const int dh = D / heads, threads = 256;
     const size_t smem = sizeof(float) * ((size_t)T * (dh + 1) + (size_t)T * dh + (size_t)(threads / 32) * T);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(vit_attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(vit_attn_fwd_kernel<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    vit_attn_fwd_kernel<<<dim3(heads, B, S), threads, smem, st>>>(QKV, B, T, D, dh, O, A);
+    vit_attn_fwd_kernel<TO><<<dim3(heads, B, S), threads, smem, st>>>(QKV, B, T, D, dh, O, A);
+}
+void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A,
+                         cudaStream_t st) {
+    attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
+}
+void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, __nv_bfloat16* O, float* A,
+                         cudaStream_t st) {
+    attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
 }
 
 // dA_ij = dO_i·V_j; dS_ij = A_ij(dA_ij − Σ_k A_ik dA_ik)/√dh; dQ_i = Σ_j dS_ij K_j;
 // dK_j = Σ_i dS_ij Q_i; dV_j = Σ_i A_ij dO_i. Written into dQKV (Q | K | V columns of head h).
+template <class TD>
 __global__ void vit_attn_bwd_kernel(const float* __restrict__ QKV, const float* __restrict__ A,
-                                    const float* __restrict__ dO, int B, int T, int D, int dh,
+                                    const TD* __restrict__ dO, int B, int T, int D, int dh,
                                     float* __restrict__ dQKV) {
     extern __shared__ float sm[];
     const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
@@ -223,14 +259,14 @@ __global__ void vit_attn_bwd_kernel(const float* __restrict__ QKV, const float* 
     float* As = dOs + T * P1;    // [T][T+1]
     float* dSs = As + T * TP;    // [T][T+1]
     const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
-    const float* dob = dO + ((int64_t)s * B + b) * T * D;
+    const TD* dob = dO + ((int64_t)s * B + b) * T * D;
     const float* ab = A + (((int64_t)s * B + b) * nh + h) * T * T;
     for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
         const int t = i / dh, e = i - t * dh;
         Qs[t * P1 + e] = base[(int64_t)t * 3 * D + h * dh + e];
         Ks[t * P1 + e] = base[(int64_t)t * 3 * D + D + h * dh + e];
         Vs[t * P1 + e] = base[(int64_t)t * 3 * D + 2 * D + h * dh + e];
-        dOs[t * P1 + e] = dob[(int64_t)t * D + h * dh + e];
+        dOs[t * P1 + e] = ldf(dob, (int64_t)t * D + h * dh + e);
     }
     for (int i = threadIdx.x; i < T * T; i += blockDim.x) As[(i / T) * TP + i % T] = ab[i];
     __syncthreads();
@@ -267,16 +303,25 @@ __global__ void vit_attn_bwd_kernel(const float* __restrict__ QKV, const float* 
     }
 }
 
-void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D, int heads,
-                         float* dQKV, cudaStream_t st) {
+template <class TD>
+static void attn_bwd_t(const float* QKV, const float* A, const TD* dO, int S, int B, int T, int D, int heads,
+                       float* dQKV, cudaStream_t st) {
     const int dh = D / heads;
     const size_t smem = sizeof(float) * (4 * (size_t)T * (dh + 1) + 2 * (size_t)T * (T + 1));
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(vit_attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(vit_attn_bwd_kernel<TD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    vit_attn_bwd_kernel<<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, dh, dQKV);
+    vit_attn_bwd_kernel<TD><<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, dh, dQKV);
+}
+void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D, int heads,
+                         float* dQKV, cudaStream_t st) {
+    attn_bwd_t(QKV, A, dO, S, B, T, D, heads, dQKV, st);
+}
+void launch_vit_attn_bwd(const float* QKV, const float* A, const __nv_bfloat16* dO, int S, int B, int T, int D,
+                         int heads, float* dQKV, cudaStream_t st) {
+    attn_bwd_t(QKV, A, dO, S, B, T, D, heads, dQKV, st);
 }
 
 // ------------------------------------------------------------------------ elementwise
@@ -308,6 +353,40 @@ __global__ void vit_gather_tokens_kernel(const float* __restrict__ in, int B, in
     }
 }
 
+__global__ void vit_gelu_bf16_kernel(const float* __restrict__ U, int64_t n, __nv_bfloat16* __restrict__ Aout) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        Aout[i] = __float2bfloat16_rn(gelu_f(U[i]));
+}
+// dU = dA ⊙ GELU'(U) from the bf16 dgrad output: fp32 (bias gradient) and bf16 (next GEMM operand)
+__global__ void vit_gelu_bwd_bf16_kernel(const float* __restrict__ U, int64_t n, const __nv_bfloat16* __restrict__ dA,
+                                         float* __restrict__ dU, __nv_bfloat16* __restrict__ dUb) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = __bfloat162float(dA[i]) * gelu_df(U[i]);
+        dU[i] = v;
+        dUb[i] = __float2bfloat16_rn(v);
+    }
+}
+__global__ void vit_cast_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __float2bfloat16_rn(x[i]);
+}
+void launch_vit_gelu(const float* U, int64_t n, __nv_bfloat16* A, cudaStream_t st) {
+    vit_gelu_bf16_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, A);
+}
+void launch_vit_gelu_bwd(const float* U, int64_t n, const __nv_bfloat16* dA, float* dU, __nv_bfloat16* dUb,
+                         cudaStream_t st) {
+    vit_gelu_bwd_bf16_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, dA, dU, dUb);
+}
+__global__ void vit_widen_kernel(const __nv_bfloat16* __restrict__ x, int64_t n, float* __restrict__ y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __bfloat162float(x[i]);
+}
+void launch_vit_widen(const __nv_bfloat16* x, int64_t n, float* y, cudaStream_t st) {
+    vit_widen_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(x, n, y);
+}
+void launch_vit_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
+    vit_cast_bf16_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(x, n, y);
+}
 void launch_vit_gelu(const float* U, int64_t n, float* A, cudaStream_t st) {
     vit_gelu_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, A);
 }

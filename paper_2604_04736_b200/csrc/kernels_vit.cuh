@@ -1,6 +1,7 @@
 // kernels_vit.cuh — launchers of the Bayesian ViT's non-GEMM kernels (kernels_vit.cu).
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -30,6 +31,23 @@ void launch_vit_gelu(const float* U, int64_t n, float* A, cudaStream_t st);
 void launch_vit_gelu_bwd(const float* U, int64_t n, float* dA, cudaStream_t st);  // dA ⊙= GELU'(U)
 void launch_vit_add(float* Y, const float* X, int64_t n, cudaStream_t st);       // Y += X
 // out[s][b][k] = in[s][b][t0 + k], k < nt (token rows of width D, T per example)
+// BF16 mode (the projections on tcgen05): bf16 outputs of the GEMM operands, bf16 inputs of
+// the dgrad outputs
+void launch_vit_patchify(const float* x, int S, int B, int H, int W, int C, int p, int aug, uint64_t seed,
+                         uint32_t step, uint32_t s0, int b_off, __nv_bfloat16* P, cudaStream_t st);
+void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, int D, const float* g, const float* b,
+                       __nv_bfloat16* Y, int64_t ldy, int64_t sY, float* stats, cudaStream_t st);
+void launch_vit_ln_bwd(const __nv_bfloat16* dY, int64_t ldy, int64_t sdY, const float* X, int S, int rows, int64_t ld,
+                       int64_t sX, int D, const float* g, const float* stats, float* dX, float* dyxh, cudaStream_t st);
+void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, __nv_bfloat16* O, float* A,
+                         cudaStream_t st);
+void launch_vit_attn_bwd(const float* QKV, const float* A, const __nv_bfloat16* dO, int S, int B, int T, int D,
+                         int heads, float* dQKV, cudaStream_t st);
+void launch_vit_gelu(const float* U, int64_t n, __nv_bfloat16* A, cudaStream_t st);
+void launch_vit_gelu_bwd(const float* U, int64_t n, const __nv_bfloat16* dA, float* dU, __nv_bfloat16* dUb,
+                         cudaStream_t st);
+void launch_vit_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st);
+void launch_vit_widen(const __nv_bfloat16* x, int64_t n, float* y, cudaStream_t st);
 void launch_vit_gather_tokens(const float* in, int S, int B, int T, int t0, int nt, int D, float* out,
                               cudaStream_t st);
 

@@ -1,5 +1,5 @@
 // runtime_vit.cu — the Bayesian ViT step (use case 1):
-// tensor table, workspace and the per-chunk forward + backward, FP32 mode.
+// tensor table, workspace and the per-chunk forward + backward (FP32 and BF16 modes).
 //
 // Per sample chunk (Sc samples of the same B_loc examples; rows R = B·T tokens):
 //   patches (crop/flip keyed by global (s, b)) → sampled patch projection → [cls; E] + pos
@@ -12,6 +12,7 @@
 // 1-D tensor's gradient (biases, g, b, cls, pos) goes through the bias-gradient reduction
 // (Σ rows, then acc_μ += Σ_s, acc_ρ += Σ_s ε_s ⊙ ·).
 #include "ctx.cuh"
+#include "kernels_tc.cuh"
 #include "kernels_vit.cuh"
 
 namespace {
@@ -77,7 +78,6 @@ int build_vit(bnn_ctx* c) {
 }
 
 int alloc_vit(bnn_ctx* c) {
-    if (c->bf16) return c->set_err(BNN_ERR_CONFIG, "ViT: precision FP32 (the BF16 path is not built)");
     if (c->agg || c->mcd) return c->set_err(BNN_ERR_CONFIG, "ViT: per-sample CE, Bayes by backprop only");
     const int B = c->B_max, Sc = c->chunk, T = c->vT, D = c->vD, M = c->vM, L = c->model.depth;
     const int64_t R = (int64_t)B * T;
@@ -119,11 +119,255 @@ int alloc_vit(bnn_ctx* c) {
     if (!c->alloc(&c->vwpart, (size_t)c->vwpart_cap)) return c->set_err(BNN_ERR_CUDA, "out of memory");
     const int maxN = std::max({M, 3 * D, T * D, c->O});
     if (!c->alloc(&c->db_scratch, (size_t)2 * Sc * maxN)) return c->set_err(BNN_ERR_CUDA, "out of memory");
+    if (!c->bf16) return BNN_OK;
+    // ---- BF16 mode: bf16 copies of every projection's input (kept for its weight gradient), the
+    // output gradients as GEMM operands, and the descriptors (all widths are multiples of 8 except
+    // the head's classes: pitch round_up(O, 8))
+    const int NP = c->vNP, PK = c->vPK, ldO = (int)round_up(c->O, 8);
+    if (PK % 8 != 0 || D % 8 != 0 || M % 8 != 0)
+        return c->set_err(BNN_ERR_CONFIG, "ViT BF16: patch·patch·in_c, dim and mlp must be multiples of 8");
+    c->vlb.assign(L, bnn_ctx::VitB{});
+    for (int l = 0; l < L; ++l) {
+        bnn_ctx::VitB& b = c->vlb[l];
+        if (!(c->alloc(&b.H1, (size_t)Sc * R * D) && c->alloc(&b.O, (size_t)Sc * R * D) &&
+              c->alloc(&b.H2, (size_t)Sc * R * D) && c->alloc(&b.A, (size_t)Sc * R * M)))
+            return c->set_err(BNN_ERR_CUDA, "out of memory (ViT bf16 activations)");
+    }
+    ok = c->alloc(&c->vPb, (size_t)(aug ? Sc : 1) * B * NP * PK) && c->alloc(&c->vHcb, (size_t)Sc * B * D) &&
+         c->alloc(&c->vdXb, (size_t)Sc * R * D) && c->alloc(&c->vdXb2, (size_t)Sc * R * D) &&
+         c->alloc(&c->vdUb, (size_t)Sc * R * M) && c->alloc(&c->vdQKVb, (size_t)Sc * R * 3 * D) &&
+         c->alloc(&c->vdEb, (size_t)Sc * B * NP * D) && c->alloc(&c->vdzb, (size_t)Sc * B * ldO);
+    if (!ok) return c->set_err(BNN_ERR_CUDA, "out of memory (ViT bf16 gradients)");
+    c->vmaps.assign(2 + 4 * L, bnn_ctx::VitMaps{});
+    // (input X [.][rows][K], gradient G [.][rows][N]) of one projection
+    auto maps = [&](bnn_ctx::VitMaps& m, const void* Xb, int K, int ldK, int rows, int xdepth, const void* Gb, int N,
+                    int ldN) {
+        return make_map(&m.fwd, Xb, K, rows, xdepth, ldK, 256) && make_map(&m.wg_x, Xb, K, rows, xdepth, ldK, 64) &&
+               make_map(&m.dg, Gb, N, rows, Sc, ldN, 256) && make_map(&m.wg_g, Gb, N, rows, Sc, ldN, 64);
+    };
+    ok = maps(c->vmaps[0], c->vPb, PK, PK, B * NP, aug ? Sc : 1, c->vdEb, D, D);
+    for (int l = 0; l < L && ok; ++l) {
+        const bnn_ctx::VitB& b = c->vlb[l];
+        ok = maps(c->vmaps[1 + 4 * l], b.H1, D, D, (int)R, Sc, c->vdQKVb, 3 * D, 3 * D) &&
+             maps(c->vmaps[2 + 4 * l], b.O, D, D, (int)R, Sc, c->vdXb2, D, D) &&
+             maps(c->vmaps[3 + 4 * l], b.H2, D, D, (int)R, Sc, c->vdUb, M, M) &&
+             maps(c->vmaps[4 + 4 * l], b.A, M, M, (int)R, Sc, c->vdXb, D, D);
+    }
+    ok = ok && maps(c->vmaps[1 + 4 * L], c->vHcb, D, D, B, Sc, c->vdzb, c->O, ldO);
+    if (!ok) return c->set_err(BNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (ViT)");
+    c->map_B = B;
+    return BNN_OK;
+}
+
+namespace {
+// Z[s][rows][N] (fp32) = Xb · W_sᵀ + b_s on tcgen05, W_s generated on chip (K2, kernels_tc.cu)
+void proj_fwd(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CUtensorMap& m, int Sc, int rows,
+              bool shared, float* Z, cudaStream_t st) {
+    TcGenArgs a{};
+    a.L = Lw;
+    a.kk = kk;
+    a.mode = 0;
+    a.B = rows;
+    a.b_shared = shared ? 1 : 0;
+    a.M = Lw.N;
+    a.R = Lw.K;
+    a.nb = (int)round_up(std::min(rows, 256), 16);
+    a.out = Z;
+    a.ldo = Lw.N;
+    a.out_stride_s = (int64_t)rows * Lw.N;
+    a.out_f32 = 1;
+    a.relu = 0;
+    a.vec_ok = (Lw.K % 4 == 0 && Lw.off_w % 4 == 0) ? 1 : 0;
+    c->launch("fwd", [&] { launch_gen_gemm(m, a, Sc, st); });
+}
+// dX[s][rows][K] (fp32) = G_s · W_s (K4, W_s regenerated on chip; bf16 operands, fp32 result)
+void proj_dgrad(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CUtensorMap& m, int Sc, int rows,
+                float* dXb, cudaStream_t st) {
+    TcGenArgs a{};
+    a.L = Lw;
+    a.kk = kk;
+    a.mode = 1;
+    a.B = rows;
+    a.M = Lw.K;
+    a.R = Lw.N;
+    a.nb = (int)round_up(std::min(rows, 256), 16);
+    a.out = dXb;
+    a.out_f32 = 1;
+    a.ldo = Lw.K;
+    a.out_stride_s = (int64_t)rows * Lw.K;
+    a.vec_ok = (Lw.K % 4 == 0 && Lw.off_w % 4 == 0) ? 1 : 0;
+    c->launch("dgrad", [&] { launch_gen_gemm(m, a, Sc, st); });
+}
+// weight gradients of up to 4 projections in one K5 launch (ε-weighted sample sums in the epilogue)
+struct WgItem {
+    SampledLayer L;
+    const bnn_ctx::VitMaps* m;
+    int shared;
+};
+void proj_wgrad(bnn_ctx* c, const SampleKeys& kk, int Sc, int rows, float scale, float* am, float* ar,
+                const WgItem* it, int n, cudaStream_t st) {
+    TcWgradMaps maps;
+    TcWgradArgs w{};
+    w.kk = kk;
+    w.S = Sc;
+    w.B = rows;
+    w.scale = scale;
+    w.acc_mu = am;
+    w.acc_rho = ar;
+    int base = 0;
+    for (int i = 0; i < n; ++i) {
+        WgradLayer& wl = w.lay[w.nlayers];
+        wl.L = it[i].L;
+        wl.mtiles = (wl.L.N + 127) / 128;
+        wl.ktiles = (wl.L.K + kWgradTileK - 1) / kWgradTileK;
+        wl.tile_base = base;
+        wl.b_shared = it[i].shared;
+        base += wl.mtiles * wl.ktiles;
+        maps.g[w.nlayers] = it[i].m->wg_g;
+        maps.x[w.nlayers] = it[i].m->wg_x;
+        ++w.nlayers;
+    }
+    c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, st); });
+}
+}  // namespace
+
+// BF16 mode: the projections (patch, QKV, proj, fc1, fc2, head) on the tcgen05 sampled-layer
+// kernels with W_s formed on chip (K2 fwd, K4 dgrad) and the ε-weighted sample sums of the
+// weight gradient in the K5 epilogue; their inputs are stored once more in bf16 (GEMM operands),
+// their outputs in fp32; LayerNorm, attention, GELU and the residual stream stay fp32 (R14:
+// bf16 operands, fp32 accumulation).
+int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, int B, int B_glob, int S_glob,
+                   int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+    NvtxRange nvtx_("bnn.chunk");
+    cudaStream_t st = c->st;
+    if (B != c->map_B)
+        return c->set_err(BNN_ERR_CONFIG, "ViT BF16: B_loc == max_B_loc required (B_loc=%d, max_B_loc=%d)", B, c->B_max);
+    const SampleKeys kk{make_key(seed), step, s0};
+    const int T = c->vT, D = c->vD, M = c->vM, L = c->model.depth, Hh = c->model.heads, NP = c->vNP;
+    const int64_t R = (int64_t)B * T, RD = R * D;
+    const int nt = (int)c->vtens.size(), ldO = (int)round_up(c->O, 8);
+    const float scale = 1.0f / ((float)S_glob * B_glob);
+    const bool aug = c->cfg.aug == BNN_AUG_PER_SAMPLE;
+    {
+        NvtxRange nv("bnn.forward");
+        for (int t = 0; t < nt; ++t)
+            if (c->vvec[t])
+                c->launch("sample", [&] {
+                    launch_vit_sample_vec(mu, c->sigma, c->vtens[t].off, (uint32_t)t, c->vtens[t].cols, kk, Sc,
+                                          c->vvec[t], st);
+                });
+        c->launch("elem", [&] {
+            launch_vit_patchify(x, aug ? Sc : 1, B, c->model.in_h, c->model.in_w, c->model.in_c, c->model.patch,
+                                aug ? 1 : 0, seed, step, s0, c->gidx * B, c->vPb, st);
+        });
+        proj_fwd(c, lin(c, mu, 0), kk, c->vmaps[0].fwd, Sc, B * NP, !aug, c->vE, st);
+        c->launch("elem", [&] { launch_vit_embed(c->vE, c->vvec[2], c->vvec[3], Sc, B, T, D, c->vX0, st); });
+        const float* X = c->vX0;
+        for (int l = 0; l < L; ++l) {
+            bnn_ctx::VitAct& a = c->vl[l];
+            bnn_ctx::VitB& b = c->vlb[l];
+            const int tb = 4 + 12 * l;
+            c->launch("elem", [&] { cudaMemcpyAsync(a.X, X, sizeof(float) * Sc * RD, cudaMemcpyDeviceToDevice, st); });
+            c->launch("ln", [&] {
+                launch_vit_ln_fwd(a.X, Sc, (int)R, D, RD, D, c->vvec[tb], c->vvec[tb + 1], b.H1, D, RD, a.st1, st);
+            });
+            proj_fwd(c, lin(c, mu, tb + 2), kk, c->vmaps[1 + 4 * l].fwd, Sc, (int)R, false, a.QKV, st);
+            c->launch("attn", [&] { launch_vit_attn_fwd(a.QKV, Sc, B, T, D, Hh, b.O, a.Att, st); });
+            proj_fwd(c, lin(c, mu, tb + 4), kk, c->vmaps[2 + 4 * l].fwd, Sc, (int)R, false, a.Xmid, st);
+            c->launch("elem", [&] { launch_vit_add(a.Xmid, a.X, Sc * RD, st); });
+            c->launch("ln", [&] {
+                launch_vit_ln_fwd(a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], c->vvec[tb + 7], b.H2, D, RD, a.st2, st);
+            });
+            proj_fwd(c, lin(c, mu, tb + 8), kk, c->vmaps[3 + 4 * l].fwd, Sc, (int)R, false, a.U, st);
+            c->launch("elem", [&] { launch_vit_gelu(a.U, Sc * R * M, b.A, st); });
+            proj_fwd(c, lin(c, mu, tb + 10), kk, c->vmaps[4 + 4 * l].fwd, Sc, (int)R, false, c->vXout, st);
+            c->launch("elem", [&] { launch_vit_add(c->vXout, a.Xmid, Sc * RD, st); });
+            X = c->vXout;
+        }
+        c->launch("ln", [&] {
+            launch_vit_ln_fwd(c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4], c->vvec[nt - 3], c->vHcb, D,
+                              (int64_t)B * D, c->vstf, st);
+        });
+        proj_fwd(c, lin(c, mu, nt - 2), kk, c->vmaps[1 + 4 * L].fwd, Sc, B, false, c->logits, st);
+    }
+    // the loss head writes the bf16 seed (GEMM operand) and its fp32 copy (bias gradient)
+    c->launch("loss", [&] {
+        launch_loss_head(c->logits, Sc, B, c->O, BNN_LOSS_CE, ycls, nullptr, c->vdzb, ldO, true, c->lossrow,
+                         c->dz_f32, st);
+    });
+    c->launch("loss", [&] { launch_loss_reduce(c->lossrow, Sc * B, scale, acc_loss, st); });
+    NvtxRange nvb("bnn.backward");
+    auto bias = [&](const SampledLayer& Lb, const float* G, int rows, int64_t ldp, int64_t sG) {
+        c->launch("bias", [&] {
+            launch_bias_grad(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->db_scratch, acc_mu, acc_rho, st);
+        }, 2);
+    };
+    {
+        const SampledLayer Lh = lin(c, mu, nt - 2);
+        const WgItem w{Lh, &c->vmaps[1 + 4 * L], 0};
+        proj_wgrad(c, kk, Sc, B, scale, acc_mu, acc_rho, &w, 1, st);
+        bias(Lh, c->dz_f32, B, c->O, (int64_t)B * c->O);
+        proj_dgrad(c, Lh, kk, c->vmaps[1 + 4 * L].dg, Sc, B, c->vdHc, st);
+        CUDA_TRY(c, cudaMemsetAsync(c->vdX, 0, sizeof(float) * Sc * RD, st));
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(c->vdHc, D, (int64_t)B * D, c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4],
+                              c->vstf, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, nt - 4), c->vdyxh, B, D, (int64_t)B * D);
+        bias(vec(c, mu, nt - 3), c->vdHc, B, D, (int64_t)B * D);
+    }
+    for (int l = L - 1; l >= 0; --l) {
+        bnn_ctx::VitAct& a = c->vl[l];
+        const int tb = 4 + 12 * l;
+        const SampledLayer Lq = lin(c, mu, tb + 2), Lo = lin(c, mu, tb + 4), L1 = lin(c, mu, tb + 8),
+                           L2 = lin(c, mu, tb + 10);
+        const bnn_ctx::VitMaps &mq = c->vmaps[1 + 4 * l], &mo = c->vmaps[2 + 4 * l], &m1 = c->vmaps[3 + 4 * l],
+                               &m2 = c->vmaps[4 + 4 * l];
+        // fc2: G = dX_out
+        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb, st); });
+        bias(L2, c->vdX, (int)R, D, RD);
+        proj_dgrad(c, L2, kk, m2.dg, Sc, (int)R, c->vdU, st);
+        c->launch("elem", [&] { launch_vit_gelu_bwd(a.U, Sc * R * M, c->vdU, st); });  // dU = dA ⊙ GELU'(U)
+        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdU, Sc * R * M, c->vdUb, st); });
+        bias(L1, c->vdU, (int)R, M, R * M);
+        proj_dgrad(c, L1, kk, m1.dg, Sc, (int)R, c->vdH, st);
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(c->vdH, D, RD, a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], a.st2, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, tb + 6), c->vdyxh, (int)R, D, RD);
+        bias(vec(c, mu, tb + 7), c->vdH, (int)R, D, RD);
+        // proj: G = dX_mid
+        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb2, st); });
+        bias(Lo, c->vdX, (int)R, D, RD);
+        proj_dgrad(c, Lo, kk, mo.dg, Sc, (int)R, c->vdO, st);
+        c->launch("attn", [&] { launch_vit_attn_bwd(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
+        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdQKV, Sc * R * 3 * D, c->vdQKVb, st); });
+        bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
+        proj_dgrad(c, Lq, kk, mq.dg, Sc, (int)R, c->vdH, st);
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(c->vdH, D, RD, a.X, Sc, (int)R, D, RD, D, c->vvec[tb], a.st1, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, tb), c->vdyxh, (int)R, D, RD);
+        bias(vec(c, mu, tb + 1), c->vdH, (int)R, D, RD);
+        // the four weight gradients of the layer (their G / X operands are still intact here)
+        const WgItem w[4] = {{L2, &m2, 0}, {L1, &m1, 0}, {Lo, &mo, 0}, {Lq, &mq, 0}};
+        proj_wgrad(c, kk, Sc, (int)R, scale, acc_mu, acc_rho, w, 4, st);
+    }
+    bias(vec(c, mu, 2), c->vdX, B, (int64_t)T * D, RD);
+    bias(vec(c, mu, 3), c->vdX, B, (int64_t)T * D, RD);
+    c->launch("elem", [&] { launch_vit_gather_tokens(c->vdX, Sc, B, T, 1, NP, D, c->vdE, st); });
+    c->launch("elem", [&] { launch_vit_cast_bf16(c->vdE, (int64_t)Sc * B * NP * D, c->vdEb, st); });
+    const SampledLayer Lp = lin(c, mu, 0);
+    const WgItem wp{Lp, &c->vmaps[0], aug ? 0 : 1};
+    proj_wgrad(c, kk, Sc, B * NP, scale, acc_mu, acc_rho, &wp, 1, st);
+    bias(Lp, c->vdE, B * NP, D, (int64_t)B * NP * D);
     return BNN_OK;
 }
 
 int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, int B, int B_glob, int S_glob,
               int Sc, uint32_t s0, uint64_t seed, uint32_t step, float* acc_mu, float* acc_rho, float* acc_loss) {
+    if (c->bf16)
+        return vit_chunk_bf16(c, mu, x, ycls, B, B_glob, S_glob, Sc, s0, seed, step, acc_mu, acc_rho, acc_loss);
     NvtxRange nvtx_("bnn.chunk");
     cudaStream_t st = c->st;
     const SampleKeys kk{make_key(seed), step, s0};
