@@ -94,7 +94,9 @@ typedef struct bnn_model_desc {
     int32_t in_h, in_w, in_c;
     int32_t n_classes;
     int32_t base_width;
-    int32_t loss; /* BNN_LOSS_CE (labels int32) | BNN_LOSS_MSE (targets fp32 [B, outputs]) */
+    int32_t loss; /* BNN_LOSS_CE (labels int32 in [0, n_classes); an out-of-range label gives a
+                     NaN loss, i.e. BNN_ERR_NUMERIC when the loss is read, never an out-of-bounds
+                     read) | BNN_LOSS_MSE (targets fp32 [B, outputs]) */
     int32_t method;   /* BNN_METHOD_VI (Bayes by backprop, default) | BNN_METHOD_MCD */
     float dropout_p;  /* MCD: drop probability of every hidden unit, 0 ≤ p < 1 */
     /* BNN_MODEL_VIT: in_h × in_w × in_c images (NHWC fp32),

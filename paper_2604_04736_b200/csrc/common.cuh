@@ -8,6 +8,12 @@ namespace bnn {
 
 constexpr int kNumSMs = 148;  // B200
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize of kernel `func` on the current device, set once
+// per (kernel, device) — the attribute is per device, and launchers may run from several host
+// threads (round-1 ADVICE: a function-static flag skipped a second device and raced). Defined in
+// kernels_simt.cu.
+void ensure_smem_attr(const void* func, int bytes);
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

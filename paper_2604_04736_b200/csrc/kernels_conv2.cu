@@ -515,11 +515,7 @@ int conv2_dgrad_parts(const Conv2Args& a) {
 template <int MODE>
 static void launch_conv2(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a,
                          cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(conv2_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, c2::kSmem);
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(conv2_kernel<MODE>), c2::kSmem);
     const int ncls = MODE == 1 ? a.stride * a.stride : 1;
     const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
     const int P = a.B * PH * PW;
@@ -957,12 +953,7 @@ int conv3_dgrad_parts(const Conv2Args& a) {
 
 template <int MODE, bool HALO>
 static void launch_conv3_t(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(conv3_kernel<MODE, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             HALO ? c3::kSmemH : c3::kSmem);
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(conv3_kernel<MODE, HALO>), HALO ? c3::kSmemH : c3::kSmem);
     const int ncls = MODE == 1 ? a.stride * a.stride : 1;
     const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
     const int P = HALO ? a.B * (PH + 1) * (PW + 2) : a.B * PH * PW;
@@ -1245,11 +1236,7 @@ int conv2_wgrad_ntile(int Kt) { return Kt >= 64 ? 256 : 0; }  // column-tile wid
 
 void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
                         cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(conv2_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, w2::kSmem);
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(conv2_wgrad_kernel), w2::kSmem);
     const int Kt = conv2_wgrad_cols(a);
     const int T = a.S * a.nsplit * ((a.CO + 127) / 128) * ((Kt + 255) / 256);
     ConvWgradArgs b = a;

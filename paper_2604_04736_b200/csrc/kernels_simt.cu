@@ -12,10 +12,25 @@
 
 #include <cuda_bf16.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace bnn {
+
+void ensure_smem_attr(const void* func, int bytes) {
+    static std::mutex m;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(m);
+    if (done.insert({func, dev}).second)
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 
 // ====================================================================== K7: σ prologue
 __global__ void sigma_kernel(const float* __restrict__ rho, float* __restrict__ sigma,
@@ -230,9 +245,13 @@ __global__ void loss_head_kernel(const float* __restrict__ logits, int rows, int
         for (int k = lane; k < O; k += 32) se += expf(z[k] - m);
         se = warp_sum(se);
         const float lse = m + logf(se);
-        const int y = ycls[b];
-        for (int k = lane; k < O; k += 32) put(k, expf(z[k] - lse) - (k == y ? 1.0f : 0.0f));
-        loss = lse - z[y];
+        // a label outside [0, O) is a caller error: no out-of-bounds read, a NaN loss (the
+        // loss read returns BNN_ERR_NUMERIC) and a zero gradient seed for the example
+        const int y0 = ycls[b];
+        const bool ok = y0 >= 0 && y0 < O;
+        const int y = ok ? y0 : 0;
+        for (int k = lane; k < O; k += 32) put(k, ok ? expf(z[k] - lse) - (k == y ? 1.0f : 0.0f) : 0.0f);
+        loss = ok ? lse - z[y] : __int_as_float(0x7fc00000);
     } else {  // MSE
         float l = 0.0f;
         for (int k = lane; k < O; k += 32) {
@@ -303,8 +322,9 @@ __global__ void mean_stats_kernel(const float* __restrict__ logits, int Sc, int 
         const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
         const int lane = threadIdx.x & 31;
         if (b >= B) return;
-        const int y = ycls[b];
-        float part = 0.0f;
+        const int y0 = ycls[b];
+        const int y = (y0 >= 0 && y0 < O) ? y0 : 0;  // out-of-range label: NaN statistic below
+        float part = (y0 >= 0 && y0 < O) ? 0.0f : __int_as_float(0x7fc00000);
         for (int s = lane; s < Sc; s += 32) {
             const float* z = logits + ((int64_t)s * B + b) * O;
             float m = z[0];
@@ -397,7 +417,8 @@ __global__ void mean_loss_head_kernel(const float* __restrict__ logits, int rows
         for (int k = lane; k < O; k += 32) se += expf(z[k] - m);
         se = warp_sum(se);
         const float lse = m + logf(se);
-        const int y = ycls[b];
+        const int y0 = ycls[b];
+        const int y = (y0 >= 0 && y0 < O) ? y0 : 0;  // out-of-range label: the statistic is NaN already
         const float w = S_glob * expf(z[y] - lse) / gstats[b];
         for (int k = lane; k < O; k += 32) put(k, w * (expf(z[k] - lse) - (k == y ? 1.0f : 0.0f)));
     } else if (loss_kind == 2) {
@@ -1023,6 +1044,38 @@ void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const f
     while (G < kBiasGroups && G < nparts) G <<= 1;
     bias_reduce_kernel<<<grid, 32 * G, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
     bias_acc_kernel<<<(L.N + 31) / 32, 256, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
+}
+
+// Many rows (the ViT's token rows): first each 64-row chunk is summed in row order into
+// chunk[s][q][n] (one thread per (chunk, column), every chunk of a sample in parallel), then the
+// two-phase reduction above runs on the chunk sums — the same fixed order every call.
+__global__ void bias_rows_chunk_kernel(const float* __restrict__ parts, int nrows, int ldp, int64_t strideS, int N,
+                                       int nchunks, float* __restrict__ chunk) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, q = blockIdx.y, s = blockIdx.z;
+    if (n >= N) return;
+    const float* p = parts + s * strideS + (int64_t)q * 64 * ldp + n;
+    const int r1 = min(64, nrows - q * 64);
+    float a0 = 0.f, a1 = 0.f;
+    int r = 0;
+    for (; r + 1 < r1; r += 2) {
+        a0 += __ldg(p + (int64_t)r * ldp);
+        a1 += __ldg(p + (int64_t)(r + 1) * ldp);
+    }
+    if (r < r1) a0 += __ldg(p + (int64_t)r * ldp);
+    chunk[((int64_t)s * nchunks + q) * N + n] = a0 + a1;
+}
+
+void launch_bias_grad_rows(const SampledLayer& L, const SampleKeys& k, int S, const float* parts, int nrows, int ldp,
+                           int64_t strideS, float scale, float* scratch, int64_t scratch_cap, float* db_scratch,
+                           float* acc_mu, float* acc_rho, cudaStream_t st) {
+    const int nchunks = (nrows + 63) / 64;
+    if (nrows <= 512 || !scratch || (int64_t)S * nchunks * L.N > scratch_cap) {
+        launch_bias_grad(L, k, S, parts, nrows, ldp, strideS, scale, db_scratch, acc_mu, acc_rho, st);
+        return;
+    }
+    bias_rows_chunk_kernel<<<dim3((L.N + 127) / 128, nchunks, S), 128, 0, st>>>(parts, nrows, ldp, strideS, L.N,
+                                                                               nchunks, scratch);
+    launch_bias_grad(L, k, S, scratch, nchunks, L.N, (int64_t)nchunks * L.N, scale, db_scratch, acc_mu, acc_rho, st);
 }
 
 }  // namespace bnn

@@ -289,9 +289,19 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
             if (MODE == 0) {
                 if (a.out_f32) {
                     float* o = reinterpret_cast<float*>(a.out) + s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
+                    // res_f32: + the fp32 residual stream (the ViT's X + proj(·), X + fc2(·))
+                    float rv[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) rv[j] = 0.0f;
+                    if (a.res_f32) {  // all 16 loads issued before any store (o and r may not alias)
+                        const float* r = a.res_f32 + s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < nvalid) rv[j] = __ldg(r + (int64_t)j * a.ldo);
+                    }
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (j < nvalid) o[(int64_t)j * a.ldo] = v[j] + bias;
+                        if (j < nvalid) o[(int64_t)j * a.ldo] = v[j] + bias + rv[j];
                 } else {
                     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + s * a.out_stride_s +
                                        (int64_t)bc0 * a.ldo + m;
@@ -347,12 +357,7 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
 // TMA-latency-bound instead and gets 4 stages (prefetch distance 3, 1 CTA/SM).
 template <int MODE, int STAGES>
 static void launch_gen_gemm_t(dim3 grid, const CUtensorMap& tmB, const TcGenArgs& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(gen_gemm_kernel<MODE, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             gen::smem_bytes(STAGES));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(gen_gemm_kernel<MODE, STAGES>), gen::smem_bytes(STAGES));
     gen_gemm_kernel<MODE, STAGES><<<grid, gen::kThreads, gen::smem_bytes(STAGES), st>>>(tmB, a);
 }
 
@@ -579,12 +584,7 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
 }
 
 void launch_wgrad_tc(const TcWgradMaps& maps, const TcWgradArgs& a, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             wg::kSmem);
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(wgrad_tc_kernel), wg::kSmem);
     const WgradLayer& last = a.lay[a.nlayers - 1];
     const int ntiles = last.tile_base + last.mtiles * last.ktiles;
     wgrad_tc_kernel<<<ntiles, wg::kThreads, wg::kSmem, st>>>(maps, a);

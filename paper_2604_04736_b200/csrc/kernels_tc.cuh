@@ -31,6 +31,7 @@ struct TcGenArgs {
     int64_t dbpart_stride_s;
     DropArgs drop;       // MC dropout: fwd masks the ReLU output, dgrad scales by 1/(1 − p)
     int mu_only;         // MC dropout: σ = 0, so W_s = RN_bf16(μ) without drawing ε
+    const float* res_f32;  // fwd, out_f32: added to the output (same layout), or null
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
 

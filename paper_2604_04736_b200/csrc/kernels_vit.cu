@@ -168,70 +168,112 @@ void launch_vit_ln_bwd(const __nv_bfloat16* dY, int64_t ldy, int64_t sdY, const 
 }
 
 // ------------------------------------------------------------------------ attention
-// block = (head h, example b, sample s); QKV rows [T][3D] (Q | K | V, head h at columns h·dh …);
-// O[t][h·dh + e]; A[s][b][h][T][T] kept for the backward. One warp per query row.
+// One block per (head h, example b, sample s), 256 threads. Every operand of the head is staged
+// in shared memory as a [TP][PP] tile (T ≤ TP rows, zero padded; pitch 68) and each of
+// the small products (S = QKᵀ, O = PV; dP = dO Vᵀ, dQ = dS K, dK = dSᵀ Q, dV = Pᵀ dO) is a
+// register-tiled SIMT product: a thread owns a 4 × 4 block of the result, reading 4 + 4
+// operands per 16 FMAs from shared memory. fp32 throughout (the ViT's parity mode is FP32).
+constexpr int kAttT = 68;   // padded token count (T = 65 for 32×32 images, 4×4 patches)
+constexpr int kAttP = 68;   // row pitch (floats): 6 tiles = 111 KB, two backward blocks per SM
+
+// C[m][n] (m < Mr, n < Nc, both < kAttT) = Σ_{k<K} A(m, k)·B(k, n), A(m, k) = A[m·am + k·ak],
+// B(k, n) = B[k·bk + n·bn]; the 4 × 4 blocks are dealt to the block's threads round-robin and
+// handed to `out(m, n, value)`.
+template <class F>
+__device__ __forceinline__ void att_product(const float* A, int am, int ak, const float* Bm, int bk, int bn, int Mr,
+                                            int Nc, int K, F out) {
+    const int mt = (Mr + 3) / 4, nt = (Nc + 3) / 4;
+    for (int t = threadIdx.x; t < mt * nt; t += blockDim.x) {
+        const int m0 = (t / nt) * 4, n0 = (t % nt) * 4;
+        float c[4][4] = {};
+        for (int k = 0; k < K; ++k) {
+            float a[4], bb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = A[(m0 + i) * am + k * ak];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bb[j] = Bm[k * bk + (n0 + j) * bn];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) c[i][j] = fmaf(a[i], bb[j], c[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (m0 + i < Mr && n0 + j < Nc) out(m0 + i, n0 + j, c[i][j]);
+    }
+}
+
+// stage rows [0, T) of `cols` columns (global row pitch ld, column offset c0) into a zero-padded
+// [kAttT][kAttP] tile
+template <class TI>
+__device__ __forceinline__ void att_stage(float* dst, const TI* src, int T, int ld, int c0, int cols) {
+    for (int i = threadIdx.x; i < kAttT * kAttP; i += blockDim.x) {
+        const int r = i / kAttP, e = i - r * kAttP;
+        dst[i] = (r < T && e < cols) ? ldf(src, (int64_t)r * ld + c0 + e) : 0.0f;
+    }
+}
+
+// transposed: dst[e][r] = src[r][c0 + e] (so that a product reading the operand along its rows
+// walks consecutive shared addresses across the warp — a column walk at pitch 72 hits one bank)
+template <class TI>
+__device__ __forceinline__ void att_stage_t(float* dst, const TI* src, int T, int ld, int c0, int cols) {
+    for (int i = threadIdx.x; i < kAttT * kAttP; i += blockDim.x) {
+        const int e = i / kAttP, r = i - e * kAttP;
+        dst[i] = (r < T && e < cols) ? ldf(src, (int64_t)r * ld + c0 + e) : 0.0f;
+    }
+}
+
 template <class TO>
-__global__ void vit_attn_fwd_kernel(const float* __restrict__ QKV, int B, int T, int D, int dh,
-                                    TO* __restrict__ O, float* __restrict__ A) {
+__global__ void __launch_bounds__(256) vit_attn_fwd_kernel(const float* __restrict__ QKV, int B, int T, int D, int dh,
+                                                           TO* __restrict__ O, float* __restrict__ A) {
     extern __shared__ float sm[];
     const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    float* Ks = sm;                  // [T][dh + 1]
-    float* Vs = Ks + T * (dh + 1);   // [T][dh]
-    float* Ps = Vs + T * dh;         // [nw][T]
+    float* Qs = sm;
+    float* Ks = Qs + kAttT * kAttP;
+    float* Vs = Ks + kAttT * kAttP;
+    float* Ps = Vs + kAttT * kAttP;
     const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
-    for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
-        const int t = i / dh, e = i - t * dh;
-        Ks[t * (dh + 1) + e] = base[(int64_t)t * 3 * D + D + h * dh + e];
-        Vs[i] = base[(int64_t)t * 3 * D + 2 * D + h * dh + e];
-    }
+    att_stage(Qs, base, T, 3 * D, h * dh, dh);
+    att_stage_t(Ks, base, T, 3 * D, D + h * dh, dh);  // Kᵀ
+    att_stage(Vs, base, T, 3 * D, 2 * D + h * dh, dh);
     __syncthreads();
     const float sc = rsqrtf((float)dh);
-    float* pr = Ps + warp * T;
-    for (int i = warp; i < T; i += nw) {
-        const float* q = base + (int64_t)i * 3 * D + h * dh;
+    // S = Q Kᵀ / √dh
+    att_product(Qs, kAttP, 1, Ks, kAttP, 1, T, T, dh, [&](int m, int n, float v) { Ps[m * kAttP + n] = v * sc; });
+    __syncthreads();
+    float* arow_base = A + (((int64_t)s * B + b) * nh + h) * T * T;
+    for (int i = warp; i < T; i += nw) {  // row softmax, kept for the backward
+        float* pr = Ps + i * kAttP;
         float mx = -INFINITY;
-        for (int j = lane; j < T; j += 32) {
-            float d = 0.f;
-            for (int e = 0; e < dh; ++e) d += q[e] * Ks[j * (dh + 1) + e];
-            d *= sc;
-            pr[j] = d;
-            mx = fmaxf(mx, d);
-        }
-        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int j = lane; j < T; j += 32) mx = fmaxf(mx, pr[j]);
+        mx = warp_max(mx);
         float se = 0.f;
         for (int j = lane; j < T; j += 32) {
             const float e = __expf(pr[j] - mx);
             pr[j] = e;
             se += e;
         }
-        for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        se = warp_sum(se);
         const float inv = 1.0f / se;
-        float* arow = A + ((((int64_t)s * B + b) * nh + h) * T + i) * T;
         for (int j = lane; j < T; j += 32) {
             pr[j] *= inv;
-            arow[j] = pr[j];
+            arow_base[(int64_t)i * T + j] = pr[j];
         }
-        __syncwarp();
-        for (int e = lane; e < dh; e += 32) {
-            float acc = 0.f;
-            for (int j = 0; j < T; ++j) acc += pr[j] * Vs[j * dh + e];
-            stf(O, (((int64_t)s * B + b) * T + i) * D + h * dh + e, acc);
-        }
-        __syncwarp();
     }
+    __syncthreads();
+    // O = P V
+    TO* ob = O + ((int64_t)s * B + b) * T * D + h * dh;
+    att_product(Ps, kAttP, 1, Vs, kAttP, 1, T, dh, T, [&](int m, int n, float v) { stf(ob, (int64_t)m * D + n, v); });
 }
 
 template <class TO>
 static void attn_fwd_t(const float* QKV, int S, int B, int T, int D, int heads, TO* O, float* A, cudaStream_t st) {
-    const int dh = D / heads, threads = 256;
-    const size_t smem = sizeof(float) * ((size_t)T * (dh + 1) + (size_t)T * dh + (size_t)(threads / 32) * T);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(vit_attn_fwd_kernel<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    vit_attn_fwd_kernel<TO><<<dim3(heads, B, S), threads, smem, st>>>(QKV, B, T, D, dh, O, A);
+    const size_t smem = sizeof(float) * 4 * kAttT * kAttP;
+    ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_fwd_kernel<TO>), (int)smem);
+    vit_attn_fwd_kernel<TO><<<dim3(heads, B, S), 256, smem, st>>>(QKV, B, T, D, D / heads, O, A);
 }
 void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A,
                          cudaStream_t st) {
@@ -242,78 +284,49 @@ void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads
     attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
 }
 
-// dA_ij = dO_i·V_j; dS_ij = A_ij(dA_ij − Σ_k A_ik dA_ik)/√dh; dQ_i = Σ_j dS_ij K_j;
-// dK_j = Σ_i dS_ij Q_i; dV_j = Σ_i A_ij dO_i. Written into dQKV (Q | K | V columns of head h).
+// dP = dO Vᵀ; dS = A ⊙ (dP − rowsum(A ⊙ dP)) / √dh; dQ = dS K; dK = dSᵀ Q; dV = Aᵀ dO —
+// written into dQKV (Q | K | V columns of head h)
 template <class TD>
-__global__ void vit_attn_bwd_kernel(const float* __restrict__ QKV, const float* __restrict__ A,
-                                    const TD* __restrict__ dO, int B, int T, int D, int dh,
-                                    float* __restrict__ dQKV) {
+__global__ void __launch_bounds__(256) vit_attn_bwd_kernel(const float* __restrict__ QKV, const float* __restrict__ A,
+                                                           const TD* __restrict__ dO, int B, int T, int D, int dh,
+                                                           float* __restrict__ dQKV) {
     extern __shared__ float sm[];
     const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int P1 = dh + 1, TP = T + 1;
-    float* Qs = sm;              // [T][dh+1]
-    float* Ks = Qs + T * P1;
-    float* Vs = Ks + T * P1;
-    float* dOs = Vs + T * P1;
-    float* As = dOs + T * P1;    // [T][T+1]
-    float* dSs = As + T * TP;    // [T][T+1]
+    constexpr int TILE = kAttT * kAttP;
+    float *Qs = sm, *Ks = sm + TILE, *Vs = sm + 2 * TILE, *dOs = sm + 3 * TILE, *As = sm + 4 * TILE, *dSs = sm + 5 * TILE;
     const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
-    const TD* dob = dO + ((int64_t)s * B + b) * T * D;
-    const float* ab = A + (((int64_t)s * B + b) * nh + h) * T * T;
-    for (int i = threadIdx.x; i < T * dh; i += blockDim.x) {
-        const int t = i / dh, e = i - t * dh;
-        Qs[t * P1 + e] = base[(int64_t)t * 3 * D + h * dh + e];
-        Ks[t * P1 + e] = base[(int64_t)t * 3 * D + D + h * dh + e];
-        Vs[t * P1 + e] = base[(int64_t)t * 3 * D + 2 * D + h * dh + e];
-        dOs[t * P1 + e] = ldf(dob, (int64_t)t * D + h * dh + e);
-    }
-    for (int i = threadIdx.x; i < T * T; i += blockDim.x) As[(i / T) * TP + i % T] = ab[i];
+    att_stage(Qs, base, T, 3 * D, h * dh, dh);
+    att_stage(Ks, base, T, 3 * D, D + h * dh, dh);
+    att_stage_t(Vs, base, T, 3 * D, 2 * D + h * dh, dh);  // Vᵀ
+    att_stage(dOs, dO + ((int64_t)s * B + b) * T * D, T, D, h * dh, dh);
+    att_stage(As, A + (((int64_t)s * B + b) * nh + h) * T * T, T, T, 0, T);
+    __syncthreads();
+    att_product(dOs, kAttP, 1, Vs, kAttP, 1, T, T, dh, [&](int m, int n, float v) { dSs[m * kAttP + n] = v; });
     __syncthreads();
     const float sc = rsqrtf((float)dh);
-    float* out = dQKV + ((int64_t)s * B + b) * T * 3 * D;
-    for (int i = warp; i < T; i += nw) {  // rows: dS and dQ
+    for (int i = warp; i < T; i += nw) {
         float rd = 0.f;
-        for (int j = lane; j < T; j += 32) {
-            float d = 0.f;
-            for (int e = 0; e < dh; ++e) d += dOs[i * P1 + e] * Vs[j * P1 + e];
-            dSs[i * TP + j] = d;
-            rd += As[i * TP + j] * d;
-        }
-        for (int o = 16; o; o >>= 1) rd += __shfl_xor_sync(0xffffffffu, rd, o);
-        for (int j = lane; j < T; j += 32) dSs[i * TP + j] = As[i * TP + j] * (dSs[i * TP + j] - rd) * sc;
-        __syncwarp();
-        for (int e = lane; e < dh; e += 32) {
-            float acc = 0.f;
-            for (int j = 0; j < T; ++j) acc += dSs[i * TP + j] * Ks[j * P1 + e];
-            out[(int64_t)i * 3 * D + h * dh + e] = acc;
-        }
+        for (int j = lane; j < T; j += 32) rd += As[i * kAttP + j] * dSs[i * kAttP + j];
+        rd = warp_sum(rd);
+        for (int j = lane; j < T; j += 32) dSs[i * kAttP + j] = As[i * kAttP + j] * (dSs[i * kAttP + j] - rd) * sc;
     }
     __syncthreads();
-    for (int j = warp; j < T; j += nw) {  // columns: dK and dV
-        for (int e = lane; e < dh; e += 32) {
-            float k = 0.f, v = 0.f;
-            for (int i = 0; i < T; ++i) {
-                k += dSs[i * TP + j] * Qs[i * P1 + e];
-                v += As[i * TP + j] * dOs[i * P1 + e];
-            }
-            out[(int64_t)j * 3 * D + D + h * dh + e] = k;
-            out[(int64_t)j * 3 * D + 2 * D + h * dh + e] = v;
-        }
-    }
+    float* out = dQKV + ((int64_t)s * B + b) * T * 3 * D;
+    att_product(dSs, kAttP, 1, Ks, kAttP, 1, T, dh, T,
+                [&](int m, int n, float v) { out[(int64_t)m * 3 * D + h * dh + n] = v; });
+    att_product(dSs, 1, kAttP, Qs, kAttP, 1, T, dh, T,
+                [&](int m, int n, float v) { out[(int64_t)m * 3 * D + D + h * dh + n] = v; });
+    att_product(As, 1, kAttP, dOs, kAttP, 1, T, dh, T,
+                [&](int m, int n, float v) { out[(int64_t)m * 3 * D + 2 * D + h * dh + n] = v; });
 }
 
 template <class TD>
 static void attn_bwd_t(const float* QKV, const float* A, const TD* dO, int S, int B, int T, int D, int heads,
                        float* dQKV, cudaStream_t st) {
-    const int dh = D / heads;
-    const size_t smem = sizeof(float) * (4 * (size_t)T * (dh + 1) + 2 * (size_t)T * (T + 1));
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(vit_attn_bwd_kernel<TD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    vit_attn_bwd_kernel<TD><<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, dh, dQKV);
+    const size_t smem = sizeof(float) * 6 * kAttT * kAttP;
+    ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_bwd_kernel<TD>), (int)smem);
+    vit_attn_bwd_kernel<TD><<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, D / heads, dQKV);
 }
 void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D, int heads,
                          float* dQKV, cudaStream_t st) {
@@ -383,6 +396,17 @@ __global__ void vit_widen_kernel(const __nv_bfloat16* __restrict__ x, int64_t n,
 }
 void launch_vit_widen(const __nv_bfloat16* x, int64_t n, float* y, cudaStream_t st) {
     vit_widen_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(x, n, y);
+}
+__global__ void vit_gelu_bwd_cast_kernel(const float* __restrict__ U, int64_t n, float* __restrict__ dA,
+                                         __nv_bfloat16* __restrict__ dUb) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = dA[i] * gelu_df(U[i]);
+        dA[i] = v;
+        dUb[i] = __float2bfloat16_rn(v);
+    }
+}
+void launch_vit_gelu_bwd_cast(const float* U, int64_t n, float* dA, __nv_bfloat16* dUb, cudaStream_t st) {
+    vit_gelu_bwd_cast_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, dA, dUb);
 }
 void launch_vit_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
     vit_cast_bf16_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(x, n, y);

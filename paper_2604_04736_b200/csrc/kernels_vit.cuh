@@ -47,6 +47,8 @@ void launch_vit_gelu(const float* U, int64_t n, __nv_bfloat16* A, cudaStream_t s
 void launch_vit_gelu_bwd(const float* U, int64_t n, const __nv_bfloat16* dA, float* dU, __nv_bfloat16* dUb,
                          cudaStream_t st);
 void launch_vit_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st);
+// dA ⊙= GELU'(U) in place, and its bf16 copy
+void launch_vit_gelu_bwd_cast(const float* U, int64_t n, float* dA, __nv_bfloat16* dUb, cudaStream_t st);
 void launch_vit_widen(const __nv_bfloat16* x, int64_t n, float* y, cudaStream_t st);
 void launch_vit_gather_tokens(const float* in, int S, int B, int T, int t0, int nt, int D, float* out,
                               cudaStream_t st);

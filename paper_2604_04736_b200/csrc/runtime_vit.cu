@@ -53,7 +53,8 @@ int build_vit(bnn_ctx* c) {
     if (m.dim / m.heads > 128) return c->set_err(BNN_ERR_CONFIG, "ViT: head dimension <= 128");
     c->vNP = (m.in_h / m.patch) * (m.in_w / m.patch);
     c->vT = 1 + c->vNP;
-    if (c->vT > 1024) return c->set_err(BNN_ERR_CONFIG, "ViT: at most 1023 patches");
+    if (c->vT > 68 || m.dim / m.heads > 68)
+        return c->set_err(BNN_ERR_CONFIG, "ViT: at most 67 patches and head dimension <= 68 (attention tiles)");
     c->vD = m.dim;
     c->vM = m.mlp;
     c->vPK = m.patch * m.patch * m.in_c;
@@ -162,7 +163,7 @@ int alloc_vit(bnn_ctx* c) {
 namespace {
 // Z[s][rows][N] (fp32) = Xb · W_sᵀ + b_s on tcgen05, W_s generated on chip (K2, kernels_tc.cu)
 void proj_fwd(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CUtensorMap& m, int Sc, int rows,
-              bool shared, float* Z, cudaStream_t st) {
+              bool shared, float* Z, cudaStream_t st, const float* res = nullptr) {
     TcGenArgs a{};
     a.L = Lw;
     a.kk = kk;
@@ -177,6 +178,7 @@ void proj_fwd(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CU
     a.out_stride_s = (int64_t)rows * Lw.N;
     a.out_f32 = 1;
     a.relu = 0;
+    a.res_f32 = res;
     a.vec_ok = (Lw.K % 4 == 0 && Lw.off_w % 4 == 0) ? 1 : 0;
     c->launch("fwd", [&] { launch_gen_gemm(m, a, Sc, st); });
 }
@@ -261,28 +263,26 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
                                 aug ? 1 : 0, seed, step, s0, c->gidx * B, c->vPb, st);
         });
         proj_fwd(c, lin(c, mu, 0), kk, c->vmaps[0].fwd, Sc, B * NP, !aug, c->vE, st);
-        c->launch("elem", [&] { launch_vit_embed(c->vE, c->vvec[2], c->vvec[3], Sc, B, T, D, c->vX0, st); });
-        const float* X = c->vX0;
+        // the layers' inputs are written in place: the embedding into layer 0's X, each fc2
+        // (with its residual fused into the GEMM epilogue) into the next layer's X
+        c->launch("elem", [&] { launch_vit_embed(c->vE, c->vvec[2], c->vvec[3], Sc, B, T, D, c->vl[0].X, st); });
         for (int l = 0; l < L; ++l) {
             bnn_ctx::VitAct& a = c->vl[l];
             bnn_ctx::VitB& b = c->vlb[l];
             const int tb = 4 + 12 * l;
-            c->launch("elem", [&] { cudaMemcpyAsync(a.X, X, sizeof(float) * Sc * RD, cudaMemcpyDeviceToDevice, st); });
             c->launch("ln", [&] {
                 launch_vit_ln_fwd(a.X, Sc, (int)R, D, RD, D, c->vvec[tb], c->vvec[tb + 1], b.H1, D, RD, a.st1, st);
             });
             proj_fwd(c, lin(c, mu, tb + 2), kk, c->vmaps[1 + 4 * l].fwd, Sc, (int)R, false, a.QKV, st);
             c->launch("attn", [&] { launch_vit_attn_fwd(a.QKV, Sc, B, T, D, Hh, b.O, a.Att, st); });
-            proj_fwd(c, lin(c, mu, tb + 4), kk, c->vmaps[2 + 4 * l].fwd, Sc, (int)R, false, a.Xmid, st);
-            c->launch("elem", [&] { launch_vit_add(a.Xmid, a.X, Sc * RD, st); });
+            proj_fwd(c, lin(c, mu, tb + 4), kk, c->vmaps[2 + 4 * l].fwd, Sc, (int)R, false, a.Xmid, st, a.X);
             c->launch("ln", [&] {
                 launch_vit_ln_fwd(a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], c->vvec[tb + 7], b.H2, D, RD, a.st2, st);
             });
             proj_fwd(c, lin(c, mu, tb + 8), kk, c->vmaps[3 + 4 * l].fwd, Sc, (int)R, false, a.U, st);
             c->launch("elem", [&] { launch_vit_gelu(a.U, Sc * R * M, b.A, st); });
-            proj_fwd(c, lin(c, mu, tb + 10), kk, c->vmaps[4 + 4 * l].fwd, Sc, (int)R, false, c->vXout, st);
-            c->launch("elem", [&] { launch_vit_add(c->vXout, a.Xmid, Sc * RD, st); });
-            X = c->vXout;
+            float* Xn = l + 1 < L ? c->vl[l + 1].X : c->vXout;
+            proj_fwd(c, lin(c, mu, tb + 10), kk, c->vmaps[4 + 4 * l].fwd, Sc, (int)R, false, Xn, st, a.Xmid);
         }
         c->launch("ln", [&] {
             launch_vit_ln_fwd(c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4], c->vvec[nt - 3], c->vHcb, D,
@@ -299,7 +299,8 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
     NvtxRange nvb("bnn.backward");
     auto bias = [&](const SampledLayer& Lb, const float* G, int rows, int64_t ldp, int64_t sG) {
         c->launch("bias", [&] {
-            launch_bias_grad(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->db_scratch, acc_mu, acc_rho, st);
+            launch_bias_grad_rows(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->vwpart, c->vwpart_cap, c->db_scratch,
+                                  acc_mu, acc_rho, st);
         }, 2);
     };
     {
@@ -327,8 +328,8 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb, st); });
         bias(L2, c->vdX, (int)R, D, RD);
         proj_dgrad(c, L2, kk, m2.dg, Sc, (int)R, c->vdU, st);
-        c->launch("elem", [&] { launch_vit_gelu_bwd(a.U, Sc * R * M, c->vdU, st); });  // dU = dA ⊙ GELU'(U)
-        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdU, Sc * R * M, c->vdUb, st); });
+        // dU = dA ⊙ GELU'(U), in place (fp32, bias gradient) and as the bf16 GEMM operand
+        c->launch("elem", [&] { launch_vit_gelu_bwd_cast(a.U, Sc * R * M, c->vdU, c->vdUb, st); });
         bias(L1, c->vdU, (int)R, M, R * M);
         proj_dgrad(c, L1, kk, m1.dg, Sc, (int)R, c->vdH, st);
         c->launch("ln", [&] {
@@ -438,7 +439,8 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
     NvtxRange nvb("bnn.backward");
     auto bias = [&](const SampledLayer& Lb, const float* G, int rows, int64_t ldp, int64_t sG) {
         c->launch("bias", [&] {
-            launch_bias_grad(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->db_scratch, acc_mu, acc_rho, st);
+            launch_bias_grad_rows(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->vwpart, c->vwpart_cap, c->db_scratch,
+                                  acc_mu, acc_rho, st);
         }, 2);
     };
     {

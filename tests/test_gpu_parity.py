@@ -1150,3 +1150,16 @@ def test_vit_bf16_matches_exact_oracle(model, B, S, aug):
     assert abs(float(loss) - ref["loss"]) <= 2e-2 * abs(ref["loss"])
     close(gmu.cpu().numpy(), ref["grad_mu"], "grad_mu")
     close(grho.cpu().numpy(), ref["grad_rho"], "grad_rho")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_out_of_range_label_is_a_numeric_error(precision):
+    """A class label outside [0, n_classes) (round-1 ADVICE): no out-of-bounds read, the loss is
+    NaN and the step returns BNN_ERR_NUMERIC."""
+    native = _native()
+    mu, rho, x, yc, _ = _inputs(RAGGED, 8, "init")
+    bad = yc.copy()
+    bad[3] = 10
+    ctx = native.Context(RAGGED, precision=precision, max_B_loc=8, max_S_loc=2, dataset_size=1.0)
+    with pytest.raises(native.BnnError, match="non-finite"):
+        ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), _dev(bad), 8, 2, 1, 0)
