@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "kernels.cuh"
 #include "kernels_tc.cuh"
 #include "tc_ptx.cuh"
 
@@ -352,6 +353,214 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
     }
 }
 
+// ============================================================================ K2 / K4, W-stationary
+// For layers with many batch rows per sample (the ViT's token rows: 33 tiles of 256 per sample)
+// the kernel above regenerates the same W_s tile once per 256-row tile. Here a CTA owns
+// (m-tile, sample, a chunk of row tiles): its generator warps form the whole W_s tile ONCE into
+// resident shared memory (R ≤ 256: ≤ 4 k-blocks, 64 KB), then the CTA streams the chunk's row
+// tiles through it — a TMA warp fills a ring of activation / gradient stages, the MMA thread
+// accumulates each row tile in one of two TMEM buffers, and the generator warps, done
+// generating, run the epilogue of tile i while tile i+1 is multiplied. W_s is still never in HBM
+// and ε is drawn once per (element, sample, chunk) instead of once per (element, sample, tile).
+// Epilogue features: fwd — fp32 out (+ bias, + res_f32) or bf16 (+ bias, ReLU); dgrad — fp32 or
+// bf16 out, no activation mask (the ViT's projections).
+namespace gws {
+constexpr int kMaxKb = 4;                          // R ≤ 256
+constexpr int kBStages = 3;
+constexpr int kThreads = (gen::kGenWarps + 2) * 32;  // + MMA warp + TMA warp
+constexpr int kSmem = 1024 + kMaxKb * gen::kAStage + kBStages * gen::kBStage + 256 + 128 * 4;
+}  // namespace gws
+
+template <int MODE>
+__global__ void __launch_bounds__(gws::kThreads, 1)
+    gen_gemm_ws_kernel(const __grid_constant__ CUtensorMap tmB, const TcGenArgs a, int tiles_per) {
+    using namespace gen;
+    using gws::kBStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;                                   // resident W_s k-blocks
+    uint8_t* sB = smem + gws::kMaxKb * kAStage;            // ring of row-tile k-blocks
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kBStages * kBStage);
+    uint64_t* wfull = bars;                                // [kMaxKb] W_s k-block formed
+    uint64_t* full = bars + gws::kMaxKb;                   // [kBStages]
+    uint64_t* empty = full + kBStages;                     // [kBStages]
+    uint64_t* tfull = empty + kBStages;                    // [2]
+    uint64_t* tempty = tfull + 2;                          // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sbias = reinterpret_cast<float*>(bars + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int m0 = blockIdx.x * 128, s = blockIdx.y;
+    const int ntiles_b = (a.B + 255) / 256;
+    const int t0 = blockIdx.z * tiles_per, t1 = min(ntiles_b, t0 + tiles_per);
+    const uint32_t sg = a.kk.s0 + s;
+    const SampledLayer& L = a.L;
+    const int nkb = (a.R + 63) / 64;
+    const int WMMA = kGenWarps, WTMA = kGenWarps + 1;
+
+    if (tid == 0) {
+        for (int i = 0; i < gws::kMaxKb; ++i) mbar_init(&wfull[i], kGenWarps);
+        for (int i = 0; i < kBStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kGenWarps);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == WMMA) tmem_alloc(tslot, 512);
+    if (MODE == 0 && tid < 128) {
+        const int n = m0 + tid;
+        sbias[tid] = n < L.N ? __fmaf_rn(L.sigma[L.off_b + n], eps1(a.kk.key, a.kk.step, sg, L.t_b, 0u, (uint32_t)n),
+                                         L.mu[L.off_b + n])
+                             : 0.0f;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == WTMA) {
+        // ------------------------------------------------ TMA: row tiles × k-blocks through the ring
+        if (lane == 0) {
+            int it = 0;
+            for (int bt = t0; bt < t1; ++bt)
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kBStages;
+                    mbar_wait_role(&empty[st], ((it / kBStages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[st], kBStage);
+                    tma_load_3d(&tmB, &full[st], sB + st * kBStage, kb * 64, bt * 256, a.b_shared ? 0 : s);
+                }
+        }
+        __syncwarp();
+    } else if (warp == WMMA) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, a.nb, MODE == 1 ? 1 : 0, 0);
+            for (int kb = 0; kb < nkb; ++kb) mbar_wait_role(&wfull[kb], 0);
+            int it = 0, tl = 0;
+            for (int bt = t0; bt < t1; ++bt, ++tl) {
+                const int buf = tl & 1;
+                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + buf * 256;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int st = it % kBStages;
+                    mbar_wait_role(&full[st], (it / kBStages) & 1);
+                    tc_fence_after();
+                    const uint32_t aBase = smem_u32(sA + kb * kAStage);
+                    const uint32_t bBase = smem_u32(sB + st * kBStage);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint64_t ad = MODE == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
+                                                      : sdesc_sw128(aBase + 2048 * q, 8192, 1024);
+                        const uint64_t bd = sdesc_sw128(bBase + 32 * q, 16, 1024);
+                        mma_bf16(d, ad, bd, idesc, (kb | q) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[buf]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ generators: the resident W_s tile
+        const int rsub = MODE == 0 ? (tid >> 4) : (tid >> 5);
+        const int qd = MODE == 0 ? (tid & 15) : (tid & 31);
+        const int rstep = MODE == 0 ? kGenWarps * 2 : kGenWarps;
+        const uint32_t soff0 =
+            MODE == 0 ? rsub * 128 + ((((qd >> 1) ^ (rsub & 7))) << 4) + ((qd & 1) << 3)
+                      : (qd >> 4) * 8192 + rsub * 128 + (((((qd & 15) >> 1) ^ (rsub & 7))) << 4) + ((qd & 1) << 3);
+        const uint32_t sstep = rstep * 128;
+        const bool vec = a.vec_ok != 0;
+        const uint32_t w3 = (L.t_w << 20) | sg;
+        const bool m_full = MODE == 0 ? (m0 + 128 <= L.N) : (m0 + 128 <= L.K);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const uint32_t tileA = smem_u32(sA + kb * kAStage) + soff0;
+            const bool fullkb = vec && m_full && (MODE == 0 ? (kb * 64 + 64 <= L.K) : (kb * 64 + 64 <= L.N));
+            if (fullkb) {
+                const int n0 = MODE == 0 ? m0 + rsub : kb * 64 + rsub;
+                const int k0 = MODE == 0 ? kb * 64 + 4 * qd : m0 + 4 * qd;
+                const int64_t e0 = L.off_w + (int64_t)n0 * L.K + k0;
+                const int64_t estep = (int64_t)rstep * L.K;
+#pragma unroll 4
+                for (int it = 0; it < kItems; ++it) {
+                    const uint2 w = gen_w4_fast(L.mu + e0 + it * estep, L.sigma + e0 + it * estep, a.kk.key, a.kk.step,
+                                                w3, (uint32_t)(n0 + it * rstep), (uint32_t)(k0 >> 2));
+                    sts64(tileA + it * sstep, w);
+                }
+            } else {
+#pragma unroll 1
+                for (int it = 0; it < kItems; ++it) {
+                    const int n = MODE == 0 ? m0 + rsub + it * rstep : kb * 64 + rsub + it * rstep;
+                    const int k = MODE == 0 ? kb * 64 + 4 * qd : m0 + 4 * qd;
+                    sts64(tileA + it * sstep, gen_w4(L, a.kk, sg, n, k, vec));
+                }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&wfull[kb]);
+        }
+        // ------------------------------------------------ epilogue of every row tile
+        const int q = warp & 3, h = warp >> 2;
+        const int row = 32 * q + lane, m = m0 + row;
+        const int nchunks = (a.nb + 15) / 16;
+        constexpr int kCStep = kGenWarps / 4;
+        const float bias = MODE == 0 ? sbias[row] : 0.0f;
+        int tl = 0;
+        for (int bt = t0; bt < t1; ++bt, ++tl) {
+            const int buf = tl & 1;
+            mbar_wait_suspend(&tfull[buf], (tl >> 1) & 1);
+            tc_fence_after();
+            for (int c = h; c < nchunks; c += kCStep) {
+                const int bc0 = bt * 256 + c * 16;
+                const int nvalid = min(16, a.B - bc0);
+                float v[16];
+                __syncwarp();
+                tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + c * 16, v);
+                if (m >= a.M || nvalid <= 0) continue;
+                const int64_t base = s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
+                if (a.out_f32) {
+                    float* o = reinterpret_cast<float*>(a.out) + base;
+                    float rv[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) rv[j] = 0.0f;
+                    if (MODE == 0 && a.res_f32) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < nvalid) rv[j] = __ldg(a.res_f32 + base + (int64_t)j * a.ldo);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < nvalid) o[(int64_t)j * a.ldo] = v[j] + bias + rv[j];
+                } else {
+                    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + base;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        if (j < nvalid) {
+                            float z = v[j] + bias;
+                            if (MODE == 0 && a.relu) z = fmaxf(z, 0.0f);
+                            o[(int64_t)j * a.ldo] = __float2bfloat16_rn(z);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == WMMA) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // STAGES = 2 (2 CTAs/SM) for the wide layers, whose generation hides the TMA latency; a
 // single-M-tile forward layer (the 10-wide output layer: 10 of 128 rows generated) is
 // TMA-latency-bound instead and gets 4 stages (prefetch distance 3, 1 CTA/SM).
@@ -362,7 +571,24 @@ static void launch_gen_gemm_t(dim3 grid, const CUtensorMap& tmB, const TcGenArgs
 }
 
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st) {
-    dim3 grid((a.M + 127) / 128, S, (a.B + 255) / 256);
+    const int ntb = (a.B + 255) / 256;
+    // W-stationary when a sample has several row tiles, R ≤ 256 and no per-row mask / dropout /
+    // bias partials (the ViT's projections): chunks of row tiles so that ≈ 148 CTAs run
+    if (ntb >= 4 && a.R <= 64 * gws::kMaxKb && !a.mask && !a.dbpart && !a.drop.on && !a.mu_only) {
+        const int mt = (a.M + 127) / 128;
+        const int chunks = std::max(1, std::min(ntb, (kNumSMs + mt * S - 1) / (mt * S)));
+        const int per = (ntb + chunks - 1) / chunks;
+        const dim3 grid(mt, S, (ntb + per - 1) / per);
+        if (a.mode == 0) {
+            ensure_smem_attr(reinterpret_cast<const void*>(gen_gemm_ws_kernel<0>), gws::kSmem);
+            gen_gemm_ws_kernel<0><<<grid, gws::kThreads, gws::kSmem, st>>>(tmB, a, per);
+        } else {
+            ensure_smem_attr(reinterpret_cast<const void*>(gen_gemm_ws_kernel<1>), gws::kSmem);
+            gen_gemm_ws_kernel<1><<<grid, gws::kThreads, gws::kSmem, st>>>(tmB, a, per);
+        }
+        return;
+    }
+    dim3 grid((a.M + 127) / 128, S, ntb);
     if (a.mode == 0 && grid.x == 1)
         launch_gen_gemm_t<0, 4>(grid, tmB, a, st);
     else if (a.mode == 0)
@@ -414,7 +640,11 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
     const int n0 = (tile / W.ktiles) * 128, k0 = (tile % W.ktiles) * kTileK;
     const CUtensorMap* mapG = &maps.g[li];
     const CUtensorMap* mapX = &maps.x[li];
-    const int nbb = (a.B + 63) / 64;
+    const int nbb_all = (a.B + 63) / 64;
+    const int nsp = a.nsplit > 1 ? a.nsplit : 1;
+    const int per = (nbb_all + nsp - 1) / nsp;
+    const int bb0 = blockIdx.y * per;
+    const int nbb = max(0, min(nbb_all, bb0 + per) - bb0);  // this split's 64-row blocks
     const int S = a.S;
 
     if (threadIdx.x == 0) {
@@ -447,11 +677,12 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
                     mbar_wait_suspend(&empty[st], ph ^ 1);
                     mbar_arrive_expect_tx(&full[st], kAStage + kBStage);
                     uint8_t* a_st = sA + st * kAStage;
-                    tma_load_3d(mapG, &full[st], a_st, n0, 64 * bb, s);
-                    tma_load_3d(mapG, &full[st], a_st + 8192, n0 + 64, 64 * bb, s);
+                    const int r0 = 64 * (bb0 + bb);
+                    tma_load_3d(mapG, &full[st], a_st, n0, r0, s);
+                    tma_load_3d(mapG, &full[st], a_st + 8192, n0 + 64, r0, s);
                     uint8_t* b_st = sB + st * kBStage;
-                    tma_load_3d(mapX, &full[st], b_st, k0, 64 * bb, W.b_shared ? 0 : s);
-                    tma_load_3d(mapX, &full[st], b_st + 8192, k0 + 64, 64 * bb, W.b_shared ? 0 : s);
+                    tma_load_3d(mapX, &full[st], b_st, k0, r0, W.b_shared ? 0 : s);
+                    tma_load_3d(mapX, &full[st], b_st + 8192, k0 + 64, r0, W.b_shared ? 0 : s);
                 }
         }
         __syncwarp();
@@ -508,7 +739,7 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
-            if (n < L.N && !a.skip_eps) {
+            if (n < L.N && !a.skip_eps && nbb > 0) {
                 const uint32_t sgw = ((L.t_w << 20) | (a.kk.s0 + s));
                 if (kfull) {
 #pragma unroll
@@ -543,11 +774,21 @@ __global__ void __launch_bounds__(wg::kThreads, 1)
         float am[kCW];
         __syncwarp();
         tmem_ld28(tmem + (static_cast<uint32_t>(32 * q) << 16) + 2 * kTileK + kCW * h, am);
-        if (S == 0) {
+        if (S == 0 || nbb == 0) {
 #pragma unroll
             for (int j = 0; j < kCW; ++j) am[j] = 0.0f;
         }
-        if (n < L.N) {
+        if (nsp > 1 && n < L.N) {  // row split: scaled partials, reduced by launch_wgrad_tc
+            const int64_t nk = (int64_t)L.N * L.K, o = (int64_t)n * L.K + k;
+            float* pm = a.part + a.part_off[li] + (int64_t)blockIdx.y * 2 * nk + o;
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) {
+                if (k + j < kend) {
+                    pm[j] = a.scale * am[j];
+                    pm[nk + j] = a.scale * (nbb == 0 ? 0.0f : ar[j]);
+                }
+            }
+        } else if (n < L.N) {
             const int64_t base = L.off_w + (int64_t)n * L.K + k;
             float* pm = a.acc_mu + base;
             float* pr = a.acc_rho + base;
@@ -587,7 +828,12 @@ void launch_wgrad_tc(const TcWgradMaps& maps, const TcWgradArgs& a, cudaStream_t
     ensure_smem_attr(reinterpret_cast<const void*>(wgrad_tc_kernel), wg::kSmem);
     const WgradLayer& last = a.lay[a.nlayers - 1];
     const int ntiles = last.tile_base + last.mtiles * last.ktiles;
-    wgrad_tc_kernel<<<ntiles, wg::kThreads, wg::kSmem, st>>>(maps, a);
+    const int nsp = a.nsplit > 1 ? a.nsplit : 1;
+    wgrad_tc_kernel<<<dim3(ntiles, nsp), wg::kThreads, wg::kSmem, st>>>(maps, a);
+    if (nsp > 1)
+        for (int l = 0; l < a.nlayers; ++l)
+            launch_wgrad_split_reduce(a.part + a.part_off[l], nsp, (int64_t)a.lay[l].L.N * a.lay[l].L.K,
+                                      a.lay[l].L.off_w, a.acc_mu, a.acc_rho, st);
 }
 
 }  // namespace bnn

@@ -52,6 +52,13 @@ struct TcWgradArgs {
     float* acc_rho;
     int nlayers;
     WgradLayer lay[kMaxWgradLayers];
+    // row splits (many rows per sample, e.g. the ViT's tokens): split z of nsplit owns 64-row
+    // blocks [z·per, …) of every sample and writes its scaled partials to part + part_off[layer]
+    // as [z][μ|ρ][N·K]; launch_wgrad_tc then adds the splits in order (deterministic). nsplit ≤ 1:
+    // the epilogue updates acc in place.
+    int nsplit;
+    float* part;
+    int64_t part_off[kMaxWgradLayers];
 };
 struct TcWgradMaps {
     CUtensorMap g[kMaxWgradLayers];  // G_l: [S][B][N_l], box 64 × 64 × 1
