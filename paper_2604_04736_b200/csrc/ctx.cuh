@@ -222,7 +222,7 @@ struct bnn_ctx {
         __nv_bfloat16 *H1 = nullptr, *O = nullptr, *H2 = nullptr, *A = nullptr;
     };
     struct VitMaps {
-        CUtensorMap fwd, dg, wg_g, wg_x;
+        CUtensorMap fwd, dg, wg_g, wg_x, fwd128, dg128;
     };
     std::vector<VitB> vlb;
     std::vector<VitMaps> vmaps;  // [0] patch, [1 + 4l + {0 qkv, 1 proj, 2 fc1, 3 fc2}], [last] head

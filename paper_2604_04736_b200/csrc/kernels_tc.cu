@@ -364,25 +364,33 @@ __global__ void __launch_bounds__(gen::kThreads, 2)
 // and ε is drawn once per (element, sample, chunk) instead of once per (element, sample, tile).
 // Epilogue features: fwd — fp32 out (+ bias, + res_f32) or bf16 (+ bias, ReLU); dgrad — fp32 or
 // bf16 out, no activation mask (the ViT's projections).
+// Two shapes: NB = 256 rows per tile with R ≤ 256 (4 resident k-blocks, 3 row stages), and
+// NB = 128 with R ≤ 768 (12 resident k-blocks = 192 KB, 2 row stages of 16 KB; N = 128 MMAs).
 namespace gws {
-constexpr int kMaxKb = 4;                          // R ≤ 256
-constexpr int kBStages = 3;
 constexpr int kThreads = (gen::kGenWarps + 2) * 32;  // + MMA warp + TMA warp
-constexpr int kSmem = 1024 + kMaxKb * gen::kAStage + kBStages * gen::kBStage + 256 + 128 * 4;
+template <int NB>
+struct Shape {
+    static constexpr int kMaxKb = NB == 256 ? 4 : 12;
+    static constexpr int kBStages = NB == 256 ? 3 : 2;
+    static constexpr int kBStage = NB * 64 * 2;
+    static constexpr int kSmem = 1024 + kMaxKb * gen::kAStage + kBStages * kBStage + 256 + 128 * 4;
+};
+static_assert(Shape<128>::kSmem <= 227 * 1024, "W-stationary NB=128 shared memory");
 }  // namespace gws
 
-template <int MODE>
+template <int MODE, int NB>
 __global__ void __launch_bounds__(gws::kThreads, 1)
     gen_gemm_ws_kernel(const __grid_constant__ CUtensorMap tmB, const TcGenArgs a, int tiles_per) {
     using namespace gen;
-    using gws::kBStages;
+    constexpr int kBStages = gws::Shape<NB>::kBStages, kMaxKb = gws::Shape<NB>::kMaxKb;
+    constexpr int kBStage = gws::Shape<NB>::kBStage;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;                                   // resident W_s k-blocks
-    uint8_t* sB = smem + gws::kMaxKb * kAStage;            // ring of row-tile k-blocks
+    uint8_t* sB = smem + kMaxKb * kAStage;                 // ring of row-tile k-blocks
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kBStages * kBStage);
     uint64_t* wfull = bars;                                // [kMaxKb] W_s k-block formed
-    uint64_t* full = bars + gws::kMaxKb;                   // [kBStages]
+    uint64_t* full = bars + kMaxKb;                        // [kBStages]
     uint64_t* empty = full + kBStages;                     // [kBStages]
     uint64_t* tfull = empty + kBStages;                    // [2]
     uint64_t* tempty = tfull + 2;                          // [2]
@@ -391,7 +399,7 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     const int m0 = blockIdx.x * 128, s = blockIdx.y;
-    const int ntiles_b = (a.B + 255) / 256;
+    const int ntiles_b = (a.B + NB - 1) / NB;
     const int t0 = blockIdx.z * tiles_per, t1 = min(ntiles_b, t0 + tiles_per);
     const uint32_t sg = a.kk.s0 + s;
     const SampledLayer& L = a.L;
@@ -399,7 +407,7 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
     const int WMMA = kGenWarps, WTMA = kGenWarps + 1;
 
     if (tid == 0) {
-        for (int i = 0; i < gws::kMaxKb; ++i) mbar_init(&wfull[i], kGenWarps);
+        for (int i = 0; i < kMaxKb; ++i) mbar_init(&wfull[i], kGenWarps);
         for (int i = 0; i < kBStages; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
@@ -411,7 +419,7 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
         mbar_fence_init();
         tma_prefetch_desc(&tmB);
     }
-    if (warp == WMMA) tmem_alloc(tslot, 512);
+    if (warp == WMMA) tmem_alloc(tslot, 2 * NB);
     if (MODE == 0 && tid < 128) {
         const int n = m0 + tid;
         sbias[tid] = n < L.N ? __fmaf_rn(L.sigma[L.off_b + n], eps1(a.kk.key, a.kk.step, sg, L.t_b, 0u, (uint32_t)n),
@@ -432,7 +440,7 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
                     const int st = it % kBStages;
                     mbar_wait_role(&empty[st], ((it / kBStages) & 1) ^ 1);
                     mbar_arrive_expect_tx(&full[st], kBStage);
-                    tma_load_3d(&tmB, &full[st], sB + st * kBStage, kb * 64, bt * 256, a.b_shared ? 0 : s);
+                    tma_load_3d(&tmB, &full[st], sB + st * kBStage, kb * 64, bt * NB, a.b_shared ? 0 : s);
                 }
         }
         __syncwarp();
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
                 const int buf = tl & 1;
                 mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + buf * 256;
+                const uint32_t d = tmem + buf * NB;
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % kBStages;
                     mbar_wait_role(&full[st], (it / kBStages) & 1);
@@ -516,11 +524,11 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
             mbar_wait_suspend(&tfull[buf], (tl >> 1) & 1);
             tc_fence_after();
             for (int c = h; c < nchunks; c += kCStep) {
-                const int bc0 = bt * 256 + c * 16;
+                const int bc0 = bt * NB + c * 16;
                 const int nvalid = min(16, a.B - bc0);
                 float v[16];
                 __syncwarp();
-                tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + c * 16, v);
+                tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * NB + c * 16, v);
                 if (m >= a.M || nvalid <= 0) continue;
                 const int64_t base = s * a.out_stride_s + (int64_t)bc0 * a.ldo + m;
                 if (a.out_f32) {
@@ -557,7 +565,7 @@ __global__ void __launch_bounds__(gws::kThreads, 1)
     __syncthreads();
     if (warp == WMMA) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, 2 * NB);
     }
 }
 
@@ -570,24 +578,42 @@ static void launch_gen_gemm_t(dim3 grid, const CUtensorMap& tmB, const TcGenArgs
     gen_gemm_kernel<MODE, STAGES><<<grid, gen::kThreads, gen::smem_bytes(STAGES), st>>>(tmB, a);
 }
 
+template <int MODE, int NB>
+static void launch_ws(const CUtensorMap& tmB, TcGenArgs a, int S, cudaStream_t st) {
+    const int ntb = (a.B + NB - 1) / NB;
+    const int mt = (a.M + 127) / 128;
+    const int chunks = std::max(1, std::min(ntb, (kNumSMs + mt * S - 1) / (mt * S)));
+    const int per = (ntb + chunks - 1) / chunks;
+    a.nb = NB;
+    const dim3 grid(mt, S, (ntb + per - 1) / per);
+    ensure_smem_attr(reinterpret_cast<const void*>(gen_gemm_ws_kernel<MODE, NB>), gws::Shape<NB>::kSmem);
+    gen_gemm_ws_kernel<MODE, NB><<<grid, gws::kThreads, gws::Shape<NB>::kSmem, st>>>(tmB, a, per);
+}
+
+// W-stationary when a sample has several row tiles and no per-row mask / dropout / bias partials
+// (the ViT's projections): R ≤ 256 with 256-row tiles (tmB: box 256 rows), R ≤ 768 with 128-row
+// tiles (tmB128: box 128 rows; only if given). Returns false if not applicable.
+static bool try_ws(const CUtensorMap& tmB, const CUtensorMap* tmB128, const TcGenArgs& a, int S, cudaStream_t st) {
+    if (a.mask || a.dbpart || a.drop.on || a.mu_only || (a.B + 255) / 256 < 4) return false;
+    if (a.R <= 64 * gws::Shape<256>::kMaxKb) {
+        if (a.mode == 0) launch_ws<0, 256>(tmB, a, S, st); else launch_ws<1, 256>(tmB, a, S, st);
+        return true;
+    }
+    if (tmB128 && a.R <= 64 * gws::Shape<128>::kMaxKb) {
+        if (a.mode == 0) launch_ws<0, 128>(*tmB128, a, S, st); else launch_ws<1, 128>(*tmB128, a, S, st);
+        return true;
+    }
+    return false;
+}
+
+void launch_gen_gemm_ws(const CUtensorMap& tmB256, const CUtensorMap& tmB128, const TcGenArgs& a, int S,
+                        cudaStream_t st) {
+    if (!try_ws(tmB256, &tmB128, a, S, st)) launch_gen_gemm(tmB256, a, S, st);
+}
+
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st) {
     const int ntb = (a.B + 255) / 256;
-    // W-stationary when a sample has several row tiles, R ≤ 256 and no per-row mask / dropout /
-    // bias partials (the ViT's projections): chunks of row tiles so that ≈ 148 CTAs run
-    if (ntb >= 4 && a.R <= 64 * gws::kMaxKb && !a.mask && !a.dbpart && !a.drop.on && !a.mu_only) {
-        const int mt = (a.M + 127) / 128;
-        const int chunks = std::max(1, std::min(ntb, (kNumSMs + mt * S - 1) / (mt * S)));
-        const int per = (ntb + chunks - 1) / chunks;
-        const dim3 grid(mt, S, (ntb + per - 1) / per);
-        if (a.mode == 0) {
-            ensure_smem_attr(reinterpret_cast<const void*>(gen_gemm_ws_kernel<0>), gws::kSmem);
-            gen_gemm_ws_kernel<0><<<grid, gws::kThreads, gws::kSmem, st>>>(tmB, a, per);
-        } else {
-            ensure_smem_attr(reinterpret_cast<const void*>(gen_gemm_ws_kernel<1>), gws::kSmem);
-            gen_gemm_ws_kernel<1><<<grid, gws::kThreads, gws::kSmem, st>>>(tmB, a, per);
-        }
-        return;
-    }
+    if (try_ws(tmB, nullptr, a, S, st)) return;
     dim3 grid((a.M + 127) / 128, S, ntb);
     if (a.mode == 0 && grid.x == 1)
         launch_gen_gemm_t<0, 4>(grid, tmB, a, st);

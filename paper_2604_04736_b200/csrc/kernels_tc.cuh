@@ -34,6 +34,10 @@ struct TcGenArgs {
     const float* res_f32;  // fwd, out_f32: added to the output (same layout), or null
 };
 void launch_gen_gemm(const CUtensorMap& tmB, const TcGenArgs& a, int S, cudaStream_t st);
+// the same with a second descriptor of the B operand in 128-row boxes: layers with R ≤ 768 and
+// many rows per sample then run W-stationary with 128-row tiles (kernels_tc.cu)
+void launch_gen_gemm_ws(const CUtensorMap& tmB256, const CUtensorMap& tmB128, const TcGenArgs& a, int S,
+                        cudaStream_t st);
 
 // K5: grouped over up to 4 layers; CTA = 128 n × kWgradTileK k tile, loops over all S samples.
 constexpr int kMaxWgradLayers = 4;

@@ -144,7 +144,8 @@ int alloc_vit(bnn_ctx* c) {
     auto maps = [&](bnn_ctx::VitMaps& m, const void* Xb, int K, int ldK, int rows, int xdepth, const void* Gb, int N,
                     int ldN) {
         return make_map(&m.fwd, Xb, K, rows, xdepth, ldK, 256) && make_map(&m.wg_x, Xb, K, rows, xdepth, ldK, 64) &&
-               make_map(&m.dg, Gb, N, rows, Sc, ldN, 256) && make_map(&m.wg_g, Gb, N, rows, Sc, ldN, 64);
+               make_map(&m.dg, Gb, N, rows, Sc, ldN, 256) && make_map(&m.wg_g, Gb, N, rows, Sc, ldN, 64) &&
+               make_map(&m.fwd128, Xb, K, rows, xdepth, ldK, 128) && make_map(&m.dg128, Gb, N, rows, Sc, ldN, 128);
     };
     ok = maps(c->vmaps[0], c->vPb, PK, PK, B * NP, aug ? Sc : 1, c->vdEb, D, D);
     for (int l = 0; l < L && ok; ++l) {
@@ -162,7 +163,7 @@ int alloc_vit(bnn_ctx* c) {
 
 namespace {
 // Z[s][rows][N] (fp32) = Xb · W_sᵀ + b_s on tcgen05, W_s generated on chip (K2, kernels_tc.cu)
-void proj_fwd(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CUtensorMap& m, int Sc, int rows,
+void proj_fwd(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const bnn_ctx::VitMaps& m, int Sc, int rows,
               bool shared, float* Z, cudaStream_t st, const float* res = nullptr) {
     TcGenArgs a{};
     a.L = Lw;
@@ -180,10 +181,10 @@ void proj_fwd(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CU
     a.relu = 0;
     a.res_f32 = res;
     a.vec_ok = (Lw.K % 4 == 0 && Lw.off_w % 4 == 0) ? 1 : 0;
-    c->launch("fwd", [&] { launch_gen_gemm(m, a, Sc, st); });
+    c->launch("fwd", [&] { launch_gen_gemm_ws(m.fwd, m.fwd128, a, Sc, st); });
 }
 // dX[s][rows][K] (fp32) = G_s · W_s (K4, W_s regenerated on chip; bf16 operands, fp32 result)
-void proj_dgrad(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const CUtensorMap& m, int Sc, int rows,
+void proj_dgrad(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const bnn_ctx::VitMaps& m, int Sc, int rows,
                 float* dXb, cudaStream_t st) {
     TcGenArgs a{};
     a.L = Lw;
@@ -198,7 +199,7 @@ void proj_dgrad(bnn_ctx* c, const SampledLayer& Lw, const SampleKeys& kk, const 
     a.ldo = Lw.K;
     a.out_stride_s = (int64_t)rows * Lw.K;
     a.vec_ok = (Lw.K % 4 == 0 && Lw.off_w % 4 == 0) ? 1 : 0;
-    c->launch("dgrad", [&] { launch_gen_gemm(m, a, Sc, st); });
+    c->launch("dgrad", [&] { launch_gen_gemm_ws(m.dg, m.dg128, a, Sc, st); });
 }
 // weight gradients of up to 4 projections in one K5 launch (ε-weighted sample sums in the epilogue)
 struct WgItem {
@@ -273,7 +274,7 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
             launch_vit_patchify(x, aug ? Sc : 1, B, c->model.in_h, c->model.in_w, c->model.in_c, c->model.patch,
                                 aug ? 1 : 0, seed, step, s0, c->gidx * B, c->vPb, st);
         });
-        proj_fwd(c, lin(c, mu, 0), kk, c->vmaps[0].fwd, Sc, B * NP, !aug, c->vE, st);
+        proj_fwd(c, lin(c, mu, 0), kk, c->vmaps[0], Sc, B * NP, !aug, c->vE, st);
         // the layers' inputs are written in place: the embedding into layer 0's X, each fc2
         // (with its residual fused into the GEMM epilogue) into the next layer's X
         c->launch("elem", [&] { launch_vit_embed(c->vE, c->vvec[2], c->vvec[3], Sc, B, T, D, c->vl[0].X, st); });
@@ -284,22 +285,22 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
             c->launch("ln", [&] {
                 launch_vit_ln_fwd(a.X, Sc, (int)R, D, RD, D, c->vvec[tb], c->vvec[tb + 1], b.H1, D, RD, a.st1, st);
             });
-            proj_fwd(c, lin(c, mu, tb + 2), kk, c->vmaps[1 + 4 * l].fwd, Sc, (int)R, false, a.QKV, st);
+            proj_fwd(c, lin(c, mu, tb + 2), kk, c->vmaps[1 + 4 * l], Sc, (int)R, false, a.QKV, st);
             c->launch("attn", [&] { launch_vit_attn_fwd(a.QKV, Sc, B, T, D, Hh, b.O, a.Att, st); });
-            proj_fwd(c, lin(c, mu, tb + 4), kk, c->vmaps[2 + 4 * l].fwd, Sc, (int)R, false, a.Xmid, st, a.X);
+            proj_fwd(c, lin(c, mu, tb + 4), kk, c->vmaps[2 + 4 * l], Sc, (int)R, false, a.Xmid, st, a.X);
             c->launch("ln", [&] {
                 launch_vit_ln_fwd(a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], c->vvec[tb + 7], b.H2, D, RD, a.st2, st);
             });
-            proj_fwd(c, lin(c, mu, tb + 8), kk, c->vmaps[3 + 4 * l].fwd, Sc, (int)R, false, a.U, st);
+            proj_fwd(c, lin(c, mu, tb + 8), kk, c->vmaps[3 + 4 * l], Sc, (int)R, false, a.U, st);
             c->launch("elem", [&] { launch_vit_gelu(a.U, Sc * R * M, b.A, st); });
             float* Xn = l + 1 < L ? c->vl[l + 1].X : c->vXout;
-            proj_fwd(c, lin(c, mu, tb + 10), kk, c->vmaps[4 + 4 * l].fwd, Sc, (int)R, false, Xn, st, a.Xmid);
+            proj_fwd(c, lin(c, mu, tb + 10), kk, c->vmaps[4 + 4 * l], Sc, (int)R, false, Xn, st, a.Xmid);
         }
         c->launch("ln", [&] {
             launch_vit_ln_fwd(c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4], c->vvec[nt - 3], c->vHcb, D,
                               (int64_t)B * D, c->vstf, st);
         });
-        proj_fwd(c, lin(c, mu, nt - 2), kk, c->vmaps[1 + 4 * L].fwd, Sc, B, false, c->logits, st);
+        proj_fwd(c, lin(c, mu, nt - 2), kk, c->vmaps[1 + 4 * L], Sc, B, false, c->logits, st);
     }
     // the loss head writes the bf16 seed (GEMM operand) and its fp32 copy (bias gradient)
     c->launch("loss", [&] {
@@ -319,7 +320,7 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         const WgItem w{Lh, &c->vmaps[1 + 4 * L], 0};
         proj_wgrad(c, kk, Sc, B, scale, acc_mu, acc_rho, &w, 1, st);
         bias(Lh, c->dz_f32, B, c->O, (int64_t)B * c->O);
-        proj_dgrad(c, Lh, kk, c->vmaps[1 + 4 * L].dg, Sc, B, c->vdHc, st);
+        proj_dgrad(c, Lh, kk, c->vmaps[1 + 4 * L], Sc, B, c->vdHc, st);
         CUDA_TRY(c, cudaMemsetAsync(c->vdX, 0, sizeof(float) * Sc * RD, st));
         c->launch("ln", [&] {
             launch_vit_ln_bwd(c->vdHc, D, (int64_t)B * D, c->vXout, Sc, B, (int64_t)T * D, RD, D, c->vvec[nt - 4],
@@ -338,11 +339,11 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         // fc2: G = dX_out
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb, st); });
         bias(L2, c->vdX, (int)R, D, RD);
-        proj_dgrad(c, L2, kk, m2.dg, Sc, (int)R, c->vdU, st);
+        proj_dgrad(c, L2, kk, m2, Sc, (int)R, c->vdU, st);
         // dU = dA ⊙ GELU'(U), in place (fp32, bias gradient) and as the bf16 GEMM operand
         c->launch("elem", [&] { launch_vit_gelu_bwd_cast(a.U, Sc * R * M, c->vdU, c->vdUb, st); });
         bias(L1, c->vdU, (int)R, M, R * M);
-        proj_dgrad(c, L1, kk, m1.dg, Sc, (int)R, c->vdH, st);
+        proj_dgrad(c, L1, kk, m1, Sc, (int)R, c->vdH, st);
         c->launch("ln", [&] {
             launch_vit_ln_bwd(c->vdH, D, RD, a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], a.st2, c->vdX, c->vdyxh, st);
         });
@@ -351,11 +352,11 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         // proj: G = dX_mid
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb2, st); });
         bias(Lo, c->vdX, (int)R, D, RD);
-        proj_dgrad(c, Lo, kk, mo.dg, Sc, (int)R, c->vdO, st);
+        proj_dgrad(c, Lo, kk, mo, Sc, (int)R, c->vdO, st);
         c->launch("attn", [&] { launch_vit_attn_bwd(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdQKV, Sc * R * 3 * D, c->vdQKVb, st); });
         bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
-        proj_dgrad(c, Lq, kk, mq.dg, Sc, (int)R, c->vdH, st);
+        proj_dgrad(c, Lq, kk, mq, Sc, (int)R, c->vdH, st);
         c->launch("ln", [&] {
             launch_vit_ln_bwd(c->vdH, D, RD, a.X, Sc, (int)R, D, RD, D, c->vvec[tb], a.st1, c->vdX, c->vdyxh, st);
         });
