@@ -275,13 +275,23 @@ static void attn_fwd_t(const float* QKV, int S, int B, int T, int D, int heads, 
     ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_fwd_kernel<TO>), (int)smem);
     vit_attn_fwd_kernel<TO><<<dim3(heads, B, S), 256, smem, st>>>(QKV, B, T, D, D / heads, O, A);
 }
+bool attn_tc_ok(int T, int dh);
+bool attn_fwd_tc_ok(int T, int dh);
+template <class TO>
+static void attn_fwd_tc(const float*, int, int, int, int, int, TO*, float*, cudaStream_t);
+template <class TD>
+static void attn_bwd_tc(const float*, const float*, const TD*, int, int, int, int, int, float*, cudaStream_t);
+
 void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A,
                          cudaStream_t st) {
     attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
 }
 void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, __nv_bfloat16* O, float* A,
                          cudaStream_t st) {
-    attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
+    if (attn_fwd_tc_ok(T, D / heads))
+        attn_fwd_tc(QKV, S, B, T, D, heads, O, A, st);
+    else
+        attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
 }
 
 // dP = dO Vᵀ; dS = A ⊙ (dP − rowsum(A ⊙ dP)) / √dh; dQ = dS K; dK = dSᵀ Q; dV = Aᵀ dO —
@@ -332,9 +342,394 @@ void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int 
                          float* dQKV, cudaStream_t st) {
     attn_bwd_t(QKV, A, dO, S, B, T, D, heads, dQKV, st);
 }
+void launch_vit_attn_bwd_tf32(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D,
+                              int heads, float* dQKV, cudaStream_t st) {
+    if (attn_tc_ok(T, D / heads))
+        attn_bwd_tc(QKV, A, dO, S, B, T, D, heads, dQKV, st);
+    else
+        attn_bwd_t(QKV, A, dO, S, B, T, D, heads, dQKV, st);
+}
 void launch_vit_attn_bwd(const float* QKV, const float* A, const __nv_bfloat16* dO, int S, int B, int T, int D,
                          int heads, float* dQKV, cudaStream_t st) {
-    attn_bwd_t(QKV, A, dO, S, B, T, D, heads, dQKV, st);
+    if (attn_tc_ok(T, D / heads))
+        attn_bwd_tc(QKV, A, dO, S, B, T, D, heads, dQKV, st);
+    else
+        attn_bwd_t(QKV, A, dO, S, B, T, D, heads, dQKV, st);
+}
+
+// ------------------------------------------------------------------------ attention, tensor cores
+// The BF16 step's attention (the FP32 parity mode keeps the SIMT kernels above): the same block
+// per (h, b, s), with each small product on the warp-level tensor-core MMA
+// mma.sync.m16n8k8 in TF32 (fp32 accumulate). Operands are staged once as natural [token][e]
+// tiles of 72 rows (T ≤ 72, zero rows T..71 so every padded reduction index multiplies zeros),
+// pre-rounded to TF32 (cvt.rna); a product reads a tile as A(m, k) = X[m·am + k·ak] so a
+// transposed operand needs no second copy. The pitch decides the bank pattern of the fragment
+// loads: ≡ 4 or 12 (mod 32) makes the row walk (am = pitch) conflict-free, ≡ 8 the column walk.
+// m-tiles run over 80 rows: rows 72..79 read the next tile (finite values) and their results are
+// dropped. TF32 (10-bit mantissa) is finer than the BF16 operands of the surrounding projections.
+constexpr int kTcRows = 72;               // token rows per tile (9 k-steps of 8)
+constexpr int kTcSlack = 8 * 80;          // floats after the last tile (pitch ≤ 80) for the 80-row m-tiles
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// C(m, n) = Σ_{k < 8·Kt} A(m, k)·B(k, n) over m < 16·Mt, n < 8·Nt; A(m, k) = A[m·am + k·ak],
+// B(k, n) = B[k·bk + n·bn] (TF32 bit patterns, or fp32 rounded on load when CVT_A). A warp owns
+// 16 × 16 blocks (two n8 tiles sharing the A fragment); at most kHold blocks per warp are kept
+// and handed to out(m, n, v) — for every m, n — after the whole product (after a block barrier
+// when SYNC, so the output may overwrite an operand). Fragment layout of m16n8k8 (PTX ISA):
+// g = lane/4, q = lane%4; a = (g, q), (g+8, q), (g, q+4), (g+8, q+4); b = (q, g), (q+4, g);
+// c = (g, 2q), (g, 2q+1), (g+8, 2q), (g+8, 2q+1).
+template <bool CVT_A, bool SYNC, int kHold, class F>
+__device__ __forceinline__ void att_mma(const uint32_t* A, int am, int ak, const uint32_t* Bm, int bk, int bn, int Mt,
+                                        int Nt, int Kt, F out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    const int nt2 = (Nt + 1) >> 1, tiles = Mt * nt2;
+    float c[kHold][2][4];
+#pragma unroll
+    for (int h = 0; h < kHold; ++h)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) c[h][u][v] = 0.0f;
+#pragma unroll
+    for (int h = 0; h < kHold; ++h) {
+        const int w = warp + h * nw;
+        if (w < tiles) {
+            const int m0 = (w / nt2) * 16, n0 = (w % nt2) * 16;
+            const bool two = n0 + 8 < Nt * 8;
+            const uint32_t* a0p = A + (m0 + g) * am + q * ak;
+            const uint32_t* b0p = Bm + q * bk + (n0 + g) * bn;
+            for (int k0 = 0; k0 < Kt * 8; k0 += 8) {
+                const uint32_t* ap = a0p + k0 * ak;
+                uint32_t a[4] = {ap[0], ap[8 * am], ap[4 * ak], ap[8 * am + 4 * ak]};
+                if (CVT_A) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) a[v] = to_tf32(__uint_as_float(a[v]));
+                }
+                const uint32_t* bp = b0p + k0 * bk;
+                mma_tf32(c[h][0], a, bp[0], bp[4 * bk]);
+                if (two) mma_tf32(c[h][1], a, bp[8 * bn], bp[4 * bk + 8 * bn]);
+            }
+        }
+    }
+    if (SYNC) __syncthreads();
+#pragma unroll
+    for (int h = 0; h < kHold; ++h) {
+        const int w = warp + h * nw;
+        if (w < tiles) {
+            const int m0 = (w / nt2) * 16, n0 = (w % nt2) * 16;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int n = n0 + 8 * u + 2 * q;
+                if (n < Nt * 8) {
+                    out(m0 + g, n, c[h][u][0]);
+                    out(m0 + g, n + 1, c[h][u][1]);
+                    out(m0 + g + 8, n, c[h][u][2]);
+                    out(m0 + g + 8, n + 1, c[h][u][3]);
+                }
+            }
+        }
+    }
+}
+
+// dst[r][e] = tf32(src[r·ld + c0 + e]) for r < T, e < cols (cols % 4 == 0), zero rows T..71
+__device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+}
+__device__ __forceinline__ void ld4(const __nv_bfloat16* p, float (&v)[4]) {
+    const uint2 x = *reinterpret_cast<const uint2*>(p);
+    const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.x));
+    const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.y));
+    v[0] = lo.x, v[1] = lo.y, v[2] = hi.x, v[3] = hi.y;
+}
+// Staging is latency-bound (one block's tiles are ~50 KB read once): every thread issues all of
+// its global loads before the first shared store, so a block waits about one memory latency per
+// staging phase rather than one per loop trip.
+constexpr int kStageIt = 5;  // ⌈72 rows · 16 float4 / 256 threads⌉ (dh ≤ 64)
+
+// NT tiles dst[t][r][e] = tf32(src[r·ld + c0[t] + e]) for r < T, e < cols (cols % 4 == 0; zero
+// rows T..71), from one row-major source
+template <int NT, int IT = kStageIt, class TI>
+__device__ __forceinline__ void tc_stage(uint32_t* const (&dst)[NT], const int (&pitch)[NT], const TI* src, int T,
+                                         int64_t ld, const int (&c0)[NT], int cols) {
+    const int c4 = cols >> 2, total = kTcRows * c4;
+    float v[IT][NT][4];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+        const int i = threadIdx.x + u * blockDim.x, r = i / c4, e = (i - r * c4) * 4;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            if (i < total && r < T) {
+                ld4(src + (int64_t)r * ld + c0[t] + e, v[u][t]);
+            } else {
+                v[u][t][0] = v[u][t][1] = v[u][t][2] = v[u][t][3] = 0.0f;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+        const int i = threadIdx.x + u * blockDim.x, r = i / c4, e = (i - r * c4) * 4;
+        if (i < total) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                uint4 o;
+                o.x = to_tf32(v[u][t][0]), o.y = to_tf32(v[u][t][1]), o.z = to_tf32(v[u][t][2]),
+                o.w = to_tf32(v[u][t][3]);
+                *reinterpret_cast<uint4*>(dst[t] + r * pitch[t] + e) = o;
+            }
+        }
+    }
+}
+
+bool attn_tc_ok(int T, int dh) { return T >= 1 && T <= kTcRows && dh % 8 == 0 && dh <= 64; }
+
+// Forward, one warp per 16 query rows (FlashAttention-2-style, the whole row in registers): the
+// block (5 warps, rows 16w..16w+15) stages K and V once; each warp loads its Q fragments straight from global
+// memory, forms S = Q Kᵀ for all 72 key columns (9 accumulator tiles), takes the row softmax
+// inside its quads (a row's 72 values live in the 4 lanes of one quad), writes A, and feeds P to
+// P·V as the A operand after moving it from the accumulator layout (g, 2q | 2q+1) to the operand
+// layout (g, q | q+4) with quad shuffles. No block barrier after staging; 40 KB of shared memory.
+constexpr int kFk = 68, kFv = 72;  // K: row walk (B(k = e, n = j) = K[j][e]); V: column walk
+template <int KD, class TO>
+__global__ void __launch_bounds__(160) vit_attn_fwd_tc_kernel(const float* __restrict__ QKV, int B, int T, int D,
+                                                              TO* __restrict__ O, float* __restrict__ A) {
+    constexpr int dh = 8 * KD, NT = kTcRows / 8;
+    extern __shared__ __align__(16) uint32_t smu[];
+    const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    uint32_t* Ks = smu;
+    uint32_t* Vs = Ks + kTcRows * kFk;
+    const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
+    {
+        uint32_t* const dst[2] = {Ks, Vs};
+        const int pitch[2] = {kFk, kFv}, c0[2] = {D + h * dh, 2 * D + h * dh};
+        tc_stage<2, 8>(dst, pitch, base, T, 3 * D, c0, dh);
+    }
+    const int m0 = 16 * warp, r0 = m0 + g, r1 = r0 + 8;
+    uint32_t qa[KD][4];  // Q rows r0, r1 as m16n8k8 A fragments
+#pragma unroll
+    for (int k = 0; k < KD; ++k) {
+        const float* q0 = base + (int64_t)r0 * 3 * D + h * dh + 8 * k + q;
+        const float* q1 = base + (int64_t)r1 * 3 * D + h * dh + 8 * k + q;
+        qa[k][0] = to_tf32(r0 < T ? __ldg(q0) : 0.0f);
+        qa[k][1] = to_tf32(r1 < T ? __ldg(q1) : 0.0f);
+        qa[k][2] = to_tf32(r0 < T ? __ldg(q0 + 4) : 0.0f);
+        qa[k][3] = to_tf32(r1 < T ? __ldg(q1 + 4) : 0.0f);
+    }
+    __syncthreads();
+    if (m0 >= T) return;  // 5 warps cover T ≤ 72 rows (the staging needs all 160 threads)
+    float sa[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        sa[n][0] = sa[n][1] = sa[n][2] = sa[n][3] = 0.0f;
+        const uint32_t* kp = Ks + (8 * n + g) * kFk + q;
+#pragma unroll
+        for (int k = 0; k < KD; ++k) mma_tf32(sa[n], qa[k], kp[8 * k], kp[8 * k + 4]);
+    }
+    // row softmax of S / √dh over the columns < T; rows r0 (elements 0, 1) and r1 (2, 3)
+    const float sc = rsqrtf((float)dh) * 1.4426950408889634f;  // exp(x) = 2^(x·log2 e)
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const bool ok = 8 * n + 2 * q + u < T;
+            sa[n][u] = ok ? sa[n][u] * sc : -INFINITY;
+            sa[n][2 + u] = ok ? sa[n][2 + u] * sc : -INFINITY;
+            mx0 = fmaxf(mx0, sa[n][u]);
+            mx1 = fmaxf(mx1, sa[n][2 + u]);
+        }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    float se0 = 0.0f, se1 = 0.0f;
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            sa[n][u] = exp2f(sa[n][u] - mx0);
+            sa[n][2 + u] = exp2f(sa[n][2 + u] - mx1);
+            se0 += sa[n][u];
+            se1 += sa[n][2 + u];
+        }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        se0 += __shfl_xor_sync(0xffffffffu, se0, o);
+        se1 += __shfl_xor_sync(0xffffffffu, se1, o);
+    }
+    const float inv0 = 1.0f / se0, inv1 = 1.0f / se1;
+    float* ab = A + (((int64_t)s * B + b) * nh + h) * T * T;
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = 8 * n + 2 * q + u;
+            sa[n][u] *= inv0;
+            sa[n][2 + u] *= inv1;
+            if (j < T) {
+                if (r0 < T) ab[(int64_t)r0 * T + j] = sa[n][u];
+                if (r1 < T) ab[(int64_t)r1 * T + j] = sa[n][2 + u];
+            }
+        }
+    // O = P V: the A fragment of k-step kk is columns 8kk + q (+4) of rows r0, r1, held by quad
+    // lanes q/2 and 2 + q/2 as element q % 2
+    float oa[KD][4];
+#pragma unroll
+    for (int n = 0; n < KD; ++n) oa[n][0] = oa[n][1] = oa[n][2] = oa[n][3] = 0.0f;
+    const int srcA = (lane & ~3) | (q >> 1), srcB = srcA + 2;
+    const bool odd = q & 1;
+#pragma unroll
+    for (int kk = 0; kk < NT; ++kk) {
+        float x[4][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            x[0][u] = __shfl_sync(0xffffffffu, sa[kk][u], srcA);
+            x[1][u] = __shfl_sync(0xffffffffu, sa[kk][2 + u], srcA);
+            x[2][u] = __shfl_sync(0xffffffffu, sa[kk][u], srcB);
+            x[3][u] = __shfl_sync(0xffffffffu, sa[kk][2 + u], srcB);
+        }
+        const uint32_t pa[4] = {to_tf32(odd ? x[0][1] : x[0][0]), to_tf32(odd ? x[1][1] : x[1][0]),
+                                to_tf32(odd ? x[2][1] : x[2][0]), to_tf32(odd ? x[3][1] : x[3][0])};
+        const uint32_t* vp = Vs + (8 * kk + q) * kFv + g;
+#pragma unroll
+        for (int n = 0; n < KD; ++n) mma_tf32(oa[n], pa, vp[8 * n], vp[4 * kFv + 8 * n]);
+    }
+    TO* ob = O + ((int64_t)s * B + b) * T * D + h * dh;
+#pragma unroll
+    for (int n = 0; n < KD; ++n) {
+        const int e = 8 * n + 2 * q;
+        if (r0 < T) {
+            stf(ob, (int64_t)r0 * D + e, oa[n][0]);
+            stf(ob, (int64_t)r0 * D + e + 1, oa[n][1]);
+        }
+        if (r1 < T) {
+            stf(ob, (int64_t)r1 * D + e, oa[n][2]);
+            stf(ob, (int64_t)r1 * D + e + 1, oa[n][3]);
+        }
+    }
+}
+
+bool attn_fwd_tc_ok(int T, int dh) { return T >= 1 && T <= kTcRows && (dh == 16 || dh == 32 || dh == 64); }
+
+template <int KD, class TO>
+static void attn_fwd_tc_kd(const float* QKV, int S, int B, int T, int D, int heads, TO* O, float* A,
+                           cudaStream_t st) {
+    const size_t smem = sizeof(uint32_t) * kTcRows * (kFk + kFv);
+    ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_fwd_tc_kernel<KD, TO>), (int)smem);
+    vit_attn_fwd_tc_kernel<KD, TO><<<dim3(heads, B, S), 160, smem, st>>>(QKV, B, T, D, O, A);
+}
+template <class TO>
+static void attn_fwd_tc(const float* QKV, int S, int B, int T, int D, int heads, TO* O, float* A, cudaStream_t st) {
+    switch (D / heads) {
+        case 16: attn_fwd_tc_kd<2>(QKV, S, B, T, D, heads, O, A, st); break;
+        case 32: attn_fwd_tc_kd<4>(QKV, S, B, T, D, heads, O, A, st); break;
+        default: attn_fwd_tc_kd<8>(QKV, S, B, T, D, heads, O, A, st); break;
+    }
+}
+
+// backward tiles: Q, K (column walks in dK / dQ), V (row walk in dP; its slot then holds dS),
+// dO (row walk in dP, column walk in dV), P = A (column walk in dV; fp32, rounded on load)
+constexpr int kBq = 72, kBk = 72, kBv = 76, kBo = 72, kBp = 72;
+template <class TD>
+__global__ void __launch_bounds__(256, 2) vit_attn_bwd_tc_kernel(const float* __restrict__ QKV,
+                                                                 const float* __restrict__ A,
+                                                                 const TD* __restrict__ dO, int B, int T, int D,
+                                                                 int dh, float* __restrict__ dQKV) {
+    extern __shared__ __align__(16) uint32_t smu[];
+    const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t* Qs = smu;
+    uint32_t* Ks = Qs + kTcRows * kBq;
+    uint32_t* Vs = Ks + kTcRows * kBk;  // later dS
+    uint32_t* dOs = Vs + kTcRows * kBv;
+    uint32_t* Ps = dOs + kTcRows * kBo;
+    float* Pf = reinterpret_cast<float*>(Ps);
+    float* dSf = reinterpret_cast<float*>(Vs);
+    const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
+    {
+        // the probabilities first (T·T contiguous floats, all loads in flight), then Q, K, V, dO
+        const float* ab = A + (((int64_t)s * B + b) * nh + h) * T * T;
+        constexpr int kIt = (kTcRows * kTcRows + 255) / 256;
+        float pv[kIt];
+#pragma unroll
+        for (int u = 0; u < kIt; ++u) {
+            const int i = threadIdx.x + u * blockDim.x;
+            pv[u] = i < T * T ? ab[i] : 0.0f;
+        }
+        for (int i = threadIdx.x; i < kTcRows * kTcRows; i += blockDim.x) {  // padding rows / columns
+            const int r = i / kTcRows, c = i - r * kTcRows;
+            if (r >= T || c >= T) Pf[r * kBp + c] = 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < kIt; ++u) {
+            const int i = threadIdx.x + u * blockDim.x;
+            if (i < T * T) {
+                const int r = i / T;
+                Pf[r * kBp + (i - r * T)] = pv[u];
+            }
+        }
+        uint32_t* const dst[3] = {Qs, Ks, Vs};
+        const int pitch[3] = {kBq, kBk, kBv}, c0[3] = {h * dh, D + h * dh, 2 * D + h * dh};
+        tc_stage<3>(dst, pitch, base, T, 3 * D, c0, dh);
+        uint32_t* const dst1[1] = {dOs};
+        const int pitch1[1] = {kBo}, c01[1] = {h * dh};
+        tc_stage<1>(dst1, pitch1, dO + ((int64_t)s * B + b) * T * D, T, D, c01, dh);
+    }
+    __syncthreads();
+    const int Mt = (T + 15) >> 4, Nt = (T + 7) >> 3, Kd = dh >> 3, Kt = kTcRows / 8;
+    // dP = dO Vᵀ (B(k = e, n = j) = V[j][e]), held in registers, then written over V
+    att_mma<false, true, 4>(dOs, kBo, 1, Vs, 1, kBv, Mt, Nt, Kd, [&](int m, int n, float v) {
+        if (m < kTcRows && n < kTcRows) dSf[m * kBv + n] = v;
+    });
+    __syncthreads();
+    const float sc = rsqrtf((float)dh);
+    for (int i = warp; i < kTcRows; i += nw) {  // dS = P ⊙ (dP − rowsum(P ⊙ dP)) / √dh, TF32
+        float rd = 0.f;
+        if (i < T) {
+            for (int j = lane; j < T; j += 32) rd += Pf[i * kBp + j] * dSf[i * kBv + j];
+            rd = warp_sum(rd);
+        }
+        for (int j = lane; j < kTcRows; j += 32)
+            Vs[i * kBv + j] = (i < T && j < T) ? to_tf32(Pf[i * kBp + j] * (dSf[i * kBv + j] - rd) * sc) : 0u;
+    }
+    __syncthreads();
+    float* out = dQKV + ((int64_t)s * B + b) * T * 3 * D;
+    // dQ = dS K: A = dS (row walk, k = j), B(k = j, n = e) = K[j][e]
+    att_mma<false, false, 4>(Vs, kBv, 1, Ks, kBk, 1, Mt, Kd, Kt, [&](int m, int n, float v) {
+        if (m < T) out[(int64_t)m * 3 * D + h * dh + n] = v;
+    });
+    // dK = dSᵀ Q: A(m = j, k = i) = dS[i][j] (column walk), B(k = i, n = e) = Q[i][e]
+    att_mma<false, false, 4>(Vs, 1, kBv, Qs, kBq, 1, Mt, Kd, Kt, [&](int m, int n, float v) {
+        if (m < T) out[(int64_t)m * 3 * D + D + h * dh + n] = v;
+    });
+    // dV = Pᵀ dO: A(m = j, k = i) = P[i][j] (fp32, rounded on load), B(k = i, n = e) = dO[i][e]
+    att_mma<true, false, 4>(Ps, 1, kBp, dOs, kBo, 1, Mt, Kd, Kt, [&](int m, int n, float v) {
+        if (m < T) out[(int64_t)m * 3 * D + 2 * D + h * dh + n] = v;
+    });
+}
+
+template <class TD>
+static void attn_bwd_tc(const float* QKV, const float* A, const TD* dO, int S, int B, int T, int D, int heads,
+                        float* dQKV, cudaStream_t st) {
+    const size_t smem = sizeof(uint32_t) * (kTcRows * (kBq + kBk + kBv + kBo + kBp) + kTcSlack);
+    ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_bwd_tc_kernel<TD>), (int)smem);
+    vit_attn_bwd_tc_kernel<TD><<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, D / heads, dQKV);
 }
 
 // ------------------------------------------------------------------------ elementwise

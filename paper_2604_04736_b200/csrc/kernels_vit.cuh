@@ -43,6 +43,9 @@ void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads
                          cudaStream_t st);
 void launch_vit_attn_bwd(const float* QKV, const float* A, const __nv_bfloat16* dO, int S, int B, int T, int D,
                          int heads, float* dQKV, cudaStream_t st);
+// the BF16 step's backward with an fp32 dO (products in TF32 on the warp MMA, as the bf16 overloads)
+void launch_vit_attn_bwd_tf32(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D,
+                              int heads, float* dQKV, cudaStream_t st);
 void launch_vit_gelu(const float* U, int64_t n, __nv_bfloat16* A, cudaStream_t st);
 void launch_vit_gelu_bwd(const float* U, int64_t n, const __nv_bfloat16* dA, float* dU, __nv_bfloat16* dUb,
                          cudaStream_t st);

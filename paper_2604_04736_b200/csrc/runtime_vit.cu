@@ -353,7 +353,7 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb2, st); });
         bias(Lo, c->vdX, (int)R, D, RD);
         proj_dgrad(c, Lo, kk, mo, Sc, (int)R, c->vdO, st);
-        c->launch("attn", [&] { launch_vit_attn_bwd(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
+        c->launch("attn", [&] { launch_vit_attn_bwd_tf32(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdQKV, Sc * R * 3 * D, c->vdQKVb, st); });
         bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
         proj_dgrad(c, Lq, kk, mq, Sc, (int)R, c->vdH, st);
