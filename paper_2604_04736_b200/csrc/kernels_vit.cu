@@ -276,7 +276,6 @@ static void attn_fwd_t(const float* QKV, int S, int B, int T, int D, int heads, 
     vit_attn_fwd_kernel<TO><<<dim3(heads, B, S), 256, smem, st>>>(QKV, B, T, D, D / heads, O, A);
 }
 bool attn_tc_ok(int T, int dh);
-bool attn_fwd_tc_ok(int T, int dh);
 template <class TO>
 static void attn_fwd_tc(const float*, int, int, int, int, int, TO*, float*, cudaStream_t);
 template <class TD>
@@ -288,7 +287,7 @@ void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads
 }
 void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, __nv_bfloat16* O, float* A,
                          cudaStream_t st) {
-    if (attn_fwd_tc_ok(T, D / heads))
+    if (attn_tc_ok(T, D / heads))
         attn_fwd_tc(QKV, S, B, T, D, heads, O, A, st);
     else
         attn_fwd_t(QKV, S, B, T, D, heads, O, A, st);
@@ -494,7 +493,6 @@ __device__ __forceinline__ void tc_stage(uint32_t* const (&dst)[NT], const int (
     }
 }
 
-bool attn_tc_ok(int T, int dh) { return T >= 1 && T <= kTcRows && dh % 8 == 0 && dh <= 64; }
 
 // Forward, one warp per 16 query rows (FlashAttention-2-style, the whole row in registers): the
 // block (5 warps, rows 16w..16w+15) stages K and V once; each warp loads its Q fragments straight from global
@@ -625,7 +623,7 @@ __global__ void __launch_bounds__(160) vit_attn_fwd_tc_kernel(const float* __res
     }
 }
 
-bool attn_fwd_tc_ok(int T, int dh) { return T >= 1 && T <= kTcRows && (dh == 16 || dh == 32 || dh == 64); }
+bool attn_tc_ok(int T, int dh) { return T >= 1 && T <= kTcRows && (dh == 16 || dh == 32 || dh == 64); }
 
 template <int KD, class TO>
 static void attn_fwd_tc_kd(const float* QKV, int S, int B, int T, int D, int heads, TO* O, float* A,
@@ -643,93 +641,156 @@ static void attn_fwd_tc(const float* QKV, int S, int B, int T, int D, int heads,
     }
 }
 
-// backward tiles: Q, K (column walks in dK / dQ), V (row walk in dP; its slot then holds dS),
-// dO (row walk in dP, column walk in dV), P = A (column walk in dV; fp32, rounded on load)
-constexpr int kBq = 72, kBk = 72, kBv = 76, kBo = 72, kBp = 72;
-template <class TD>
-__global__ void __launch_bounds__(256, 2) vit_attn_bwd_tc_kernel(const float* __restrict__ QKV,
-                                                                 const float* __restrict__ A,
-                                                                 const TD* __restrict__ dO, int B, int T, int D,
-                                                                 int dh, float* __restrict__ dQKV) {
+// Backward, the same warp per 16 query rows i: dP = dO Vᵀ, the row sums Σ_j P ⊙ dP and
+// dS = P ⊙ (dP − rowsum) / √dh stay in registers (P read in the accumulator layout straight from
+// A), and dQ = dS K is formed per warp (dS moved to the operand layout by quad shuffles). dK = dSᵀ Q
+// and dV = Pᵀ dO reduce over i — across the warps — so dS and P are then written into the slots
+// of V and K and both products run block-wide (att_mma, column-walk operands).
+constexpr int kBp = 72;  // every backward tile: K, Q, dO, P are column-walked; V / dS share 72
+template <int KD, class TD>
+__global__ void __launch_bounds__(160, 2) vit_attn_bwd_tc_kernel(const float* __restrict__ QKV,
+                                                              const float* __restrict__ A,
+                                                              const TD* __restrict__ dO, int B, int T, int D,
+                                                              float* __restrict__ dQKV) {
+    constexpr int dh = 8 * KD, NT = kTcRows / 8;
     extern __shared__ __align__(16) uint32_t smu[];
     const int h = blockIdx.x, b = blockIdx.y, s = blockIdx.z, nh = gridDim.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t* Qs = smu;
-    uint32_t* Ks = Qs + kTcRows * kBq;
-    uint32_t* Vs = Ks + kTcRows * kBk;  // later dS
-    uint32_t* dOs = Vs + kTcRows * kBv;
-    uint32_t* Ps = dOs + kTcRows * kBo;
-    float* Pf = reinterpret_cast<float*>(Ps);
-    float* dSf = reinterpret_cast<float*>(Vs);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    constexpr int TILE = kTcRows * kBp;
+    uint32_t* Ks = smu;            // later P
+    uint32_t* Vs = smu + TILE;     // later dS
+    uint32_t* Qs = smu + 2 * TILE;
+    uint32_t* dOs = smu + 3 * TILE;
     const float* base = QKV + ((int64_t)s * B + b) * T * 3 * D;
+    const TD* dOb = dO + ((int64_t)s * B + b) * T * D + h * dh;
     {
-        // the probabilities first (T·T contiguous floats, all loads in flight), then Q, K, V, dO
+        uint32_t* const dst[3] = {Ks, Vs, Qs};
+        const int pitch[3] = {kBp, kBp, kBp}, c0[3] = {D + h * dh, 2 * D + h * dh, h * dh};
+        tc_stage<3, 8>(dst, pitch, base, T, 3 * D, c0, dh);
+        uint32_t* const dst1[1] = {dOs};
+        const int pitch1[1] = {kBp}, c01[1] = {0};
+        tc_stage<1, 8>(dst1, pitch1, dOb, T, D, c01, dh);
+    }
+    const int m0 = 16 * warp, r0 = m0 + g, r1 = r0 + 8;
+    const bool active = m0 < T;
+    float* out = dQKV + ((int64_t)s * B + b) * T * 3 * D + h * dh;
+    float pr[NT][4] = {}, ds[NT][4] = {};
+    if (active) {  // P rows r0, r1 in the accumulator layout, straight from A
         const float* ab = A + (((int64_t)s * B + b) * nh + h) * T * T;
-        constexpr int kIt = (kTcRows * kTcRows + 255) / 256;
-        float pv[kIt];
 #pragma unroll
-        for (int u = 0; u < kIt; ++u) {
-            const int i = threadIdx.x + u * blockDim.x;
-            pv[u] = i < T * T ? ab[i] : 0.0f;
-        }
-        for (int i = threadIdx.x; i < kTcRows * kTcRows; i += blockDim.x) {  // padding rows / columns
-            const int r = i / kTcRows, c = i - r * kTcRows;
-            if (r >= T || c >= T) Pf[r * kBp + c] = 0.0f;
-        }
+        for (int n = 0; n < NT; ++n)
 #pragma unroll
-        for (int u = 0; u < kIt; ++u) {
-            const int i = threadIdx.x + u * blockDim.x;
-            if (i < T * T) {
-                const int r = i / T;
-                Pf[r * kBp + (i - r * T)] = pv[u];
+            for (int u = 0; u < 2; ++u) {
+                const int j = 8 * n + 2 * q + u;
+                pr[n][u] = (r0 < T && j < T) ? __ldg(ab + (int64_t)r0 * T + j) : 0.0f;
+                pr[n][2 + u] = (r1 < T && j < T) ? __ldg(ab + (int64_t)r1 * T + j) : 0.0f;
+            }
+    }
+    __syncthreads();
+    if (active) {
+        // dP = dO Vᵀ: A = the staged dO rows, B(k = e, n = j) = V[j][e]
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            ds[n][0] = ds[n][1] = ds[n][2] = ds[n][3] = 0.0f;
+            const uint32_t* vp = Vs + (8 * n + g) * kBp + q;
+#pragma unroll
+            for (int k = 0; k < KD; ++k) {
+                const uint32_t* ap = dOs + r0 * kBp + 8 * k + q;
+                const uint32_t af[4] = {ap[0], ap[8 * kBp], ap[4], ap[8 * kBp + 4]};
+                mma_tf32(ds[n], af, vp[8 * k], vp[8 * k + 4]);
             }
         }
-        uint32_t* const dst[3] = {Qs, Ks, Vs};
-        const int pitch[3] = {kBq, kBk, kBv}, c0[3] = {h * dh, D + h * dh, 2 * D + h * dh};
-        tc_stage<3>(dst, pitch, base, T, 3 * D, c0, dh);
-        uint32_t* const dst1[1] = {dOs};
-        const int pitch1[1] = {kBo}, c01[1] = {h * dh};
-        tc_stage<1>(dst1, pitch1, dO + ((int64_t)s * B + b) * T * D, T, D, c01, dh);
-    }
-    __syncthreads();
-    const int Mt = (T + 15) >> 4, Nt = (T + 7) >> 3, Kd = dh >> 3, Kt = kTcRows / 8;
-    // dP = dO Vᵀ (B(k = e, n = j) = V[j][e]), held in registers, then written over V
-    att_mma<false, true, 4>(dOs, kBo, 1, Vs, 1, kBv, Mt, Nt, Kd, [&](int m, int n, float v) {
-        if (m < kTcRows && n < kTcRows) dSf[m * kBv + n] = v;
-    });
-    __syncthreads();
-    const float sc = rsqrtf((float)dh);
-    for (int i = warp; i < kTcRows; i += nw) {  // dS = P ⊙ (dP − rowsum(P ⊙ dP)) / √dh, TF32
-        float rd = 0.f;
-        if (i < T) {
-            for (int j = lane; j < T; j += 32) rd += Pf[i * kBp + j] * dSf[i * kBv + j];
-            rd = warp_sum(rd);
+        float rd0 = 0.0f, rd1 = 0.0f;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            rd0 += pr[n][0] * ds[n][0] + pr[n][1] * ds[n][1];
+            rd1 += pr[n][2] * ds[n][2] + pr[n][3] * ds[n][3];
         }
-        for (int j = lane; j < kTcRows; j += 32)
-            Vs[i * kBv + j] = (i < T && j < T) ? to_tf32(Pf[i * kBp + j] * (dSf[i * kBv + j] - rd) * sc) : 0u;
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+            rd0 += __shfl_xor_sync(0xffffffffu, rd0, o);
+            rd1 += __shfl_xor_sync(0xffffffffu, rd1, o);
+        }
+        const float sc = rsqrtf((float)dh);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            ds[n][0] = pr[n][0] * (ds[n][0] - rd0) * sc;
+            ds[n][1] = pr[n][1] * (ds[n][1] - rd0) * sc;
+            ds[n][2] = pr[n][2] * (ds[n][2] - rd1) * sc;
+            ds[n][3] = pr[n][3] * (ds[n][3] - rd1) * sc;
+        }
+        // dQ = dS K: A fragment of k-step kk from quad lanes q/2, 2 + q/2; B(k = j, n = e) = K[j][e]
+        float qa[KD][4];
+#pragma unroll
+        for (int n = 0; n < KD; ++n) qa[n][0] = qa[n][1] = qa[n][2] = qa[n][3] = 0.0f;
+        const int srcA = (lane & ~3) | (q >> 1), srcB = srcA + 2;
+        const bool odd = q & 1;
+#pragma unroll
+        for (int kk = 0; kk < NT; ++kk) {
+            float x[4][2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                x[0][u] = __shfl_sync(0xffffffffu, ds[kk][u], srcA);
+                x[1][u] = __shfl_sync(0xffffffffu, ds[kk][2 + u], srcA);
+                x[2][u] = __shfl_sync(0xffffffffu, ds[kk][u], srcB);
+                x[3][u] = __shfl_sync(0xffffffffu, ds[kk][2 + u], srcB);
+            }
+            const uint32_t af[4] = {to_tf32(odd ? x[0][1] : x[0][0]), to_tf32(odd ? x[1][1] : x[1][0]),
+                                    to_tf32(odd ? x[2][1] : x[2][0]), to_tf32(odd ? x[3][1] : x[3][0])};
+            const uint32_t* kp = Ks + (8 * kk + q) * kBp + g;
+#pragma unroll
+            for (int n = 0; n < KD; ++n) mma_tf32(qa[n], af, kp[8 * n], kp[4 * kBp + 8 * n]);
+        }
+#pragma unroll
+        for (int n = 0; n < KD; ++n) {
+            const int e = 8 * n + 2 * q;
+            if (r0 < T) *reinterpret_cast<float2*>(out + (int64_t)r0 * 3 * D + e) = make_float2(qa[n][0], qa[n][1]);
+            if (r1 < T) *reinterpret_cast<float2*>(out + (int64_t)r1 * 3 * D + e) = make_float2(qa[n][2], qa[n][3]);
+        }
     }
+    __syncthreads();  // V and K are consumed: their slots take dS and P (rows ≥ T zero)
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = 8 * n + 2 * q + u;
+            if (r0 < kTcRows) {
+                Vs[r0 * kBp + j] = active ? to_tf32(ds[n][u]) : 0u;
+                Ks[r0 * kBp + j] = active ? to_tf32(pr[n][u]) : 0u;
+            }
+            if (r1 < kTcRows) {
+                Vs[r1 * kBp + j] = active ? to_tf32(ds[n][2 + u]) : 0u;
+                Ks[r1 * kBp + j] = active ? to_tf32(pr[n][2 + u]) : 0u;
+            }
+        }
     __syncthreads();
-    float* out = dQKV + ((int64_t)s * B + b) * T * 3 * D;
-    // dQ = dS K: A = dS (row walk, k = j), B(k = j, n = e) = K[j][e]
-    att_mma<false, false, 4>(Vs, kBv, 1, Ks, kBk, 1, Mt, Kd, Kt, [&](int m, int n, float v) {
-        if (m < T) out[(int64_t)m * 3 * D + h * dh + n] = v;
+    const int Mt = (T + 15) >> 4, Kt = kTcRows / 8;
+    // dK = dSᵀ Q: A(m = j, k = i) = dS[i][j], B(k = i, n = e) = Q[i][e]
+    att_mma<false, false, 4>(Vs, 1, kBp, Qs, kBp, 1, Mt, KD, Kt, [&](int m, int n, float v) {
+        if (m < T) out[(int64_t)m * 3 * D + D + n] = v;
     });
-    // dK = dSᵀ Q: A(m = j, k = i) = dS[i][j] (column walk), B(k = i, n = e) = Q[i][e]
-    att_mma<false, false, 4>(Vs, 1, kBv, Qs, kBq, 1, Mt, Kd, Kt, [&](int m, int n, float v) {
-        if (m < T) out[(int64_t)m * 3 * D + D + h * dh + n] = v;
-    });
-    // dV = Pᵀ dO: A(m = j, k = i) = P[i][j] (fp32, rounded on load), B(k = i, n = e) = dO[i][e]
-    att_mma<true, false, 4>(Ps, 1, kBp, dOs, kBo, 1, Mt, Kd, Kt, [&](int m, int n, float v) {
-        if (m < T) out[(int64_t)m * 3 * D + 2 * D + h * dh + n] = v;
+    // dV = Pᵀ dO: A(m = j, k = i) = P[i][j], B(k = i, n = e) = dO[i][e]
+    att_mma<false, false, 4>(Ks, 1, kBp, dOs, kBp, 1, Mt, KD, Kt, [&](int m, int n, float v) {
+        if (m < T) out[(int64_t)m * 3 * D + 2 * D + n] = v;
     });
 }
 
+template <int KD, class TD>
+static void attn_bwd_tc_kd(const float* QKV, const float* A, const TD* dO, int S, int B, int T, int D, int heads,
+                           float* dQKV, cudaStream_t st) {
+    const size_t smem = sizeof(uint32_t) * (4 * kTcRows * kBp + kTcSlack);
+    ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_bwd_tc_kernel<KD, TD>), (int)smem);
+    vit_attn_bwd_tc_kernel<KD, TD><<<dim3(heads, B, S), 160, smem, st>>>(QKV, A, dO, B, T, D, dQKV);
+}
 template <class TD>
 static void attn_bwd_tc(const float* QKV, const float* A, const TD* dO, int S, int B, int T, int D, int heads,
                         float* dQKV, cudaStream_t st) {
-    const size_t smem = sizeof(uint32_t) * (kTcRows * (kBq + kBk + kBv + kBo + kBp) + kTcSlack);
-    ensure_smem_attr(reinterpret_cast<const void*>(vit_attn_bwd_tc_kernel<TD>), (int)smem);
-    vit_attn_bwd_tc_kernel<TD><<<dim3(heads, B, S), 256, smem, st>>>(QKV, A, dO, B, T, D, D / heads, dQKV);
+    switch (D / heads) {
+        case 16: attn_bwd_tc_kd<2>(QKV, A, dO, S, B, T, D, heads, dQKV, st); break;
+        case 32: attn_bwd_tc_kd<4>(QKV, A, dO, S, B, T, D, heads, dQKV, st); break;
+        default: attn_bwd_tc_kd<8>(QKV, A, dO, S, B, T, D, heads, dQKV, st); break;
+    }
 }
 
 // ------------------------------------------------------------------------ elementwise
