@@ -226,7 +226,9 @@ struct bnn_ctx {
     };
     std::vector<VitB> vlb;
     std::vector<VitMaps> vmaps;  // [0] patch, [1 + 4l + {0 qkv, 1 proj, 2 fc1, 3 fc2}], [last] head
-    __nv_bfloat16 *vPb = nullptr, *vHcb = nullptr, *vdXb = nullptr, *vdXb2 = nullptr, *vdUb = nullptr,
+    // vdXb / vdXb1: fc2's gradient operand of even / odd layers (layer l's LayerNorm-1 backward
+    // writes layer l−1's while layer l's weight gradients still read its own)
+    __nv_bfloat16 *vPb = nullptr, *vHcb = nullptr, *vdXb = nullptr, *vdXb1 = nullptr, *vdXb2 = nullptr, *vdUb = nullptr,
                   *vdQKVb = nullptr, *vdEb = nullptr, *vdzb = nullptr;
     float* vwpart = nullptr;  // row-split wgrad partials
     int64_t vwpart_cap = 0;

@@ -167,6 +167,85 @@ void launch_vit_ln_bwd(const __nv_bfloat16* dY, int64_t ldy, int64_t sdY, const 
                                                                                 dX, dyxh);
 }
 
+// The same backward over all `rows` token rows of a sample (contiguous, pitch D ≤ 256, D % 32 == 0)
+// with the γ / β gradient sources reduced in place: block (q, s) takes rows 64q … 64q + 63 (warp
+// w: rows 64q + w + 8k, k = 0…7, in that order), and writes the chunk sums
+// part_g[s][q][·] = Σ dY ⊙ x̂ and part_b[s][q][·] = Σ dY (warps added in index order: fixed order,
+// deterministic), the inputs of launch_bias_grad — instead of a dY ⊙ x̂ tensor re-read by a
+// separate chunk pass. dXb (optional): the bf16 copy of the updated dX rows (the next GEMM operand).
+constexpr int kLnMaxC = 8;  // columns per lane (D ≤ 256)
+__global__ void __launch_bounds__(256) vit_ln_bwd_fused_kernel(const float* __restrict__ dY,
+                                                               const float* __restrict__ X, int rows, int D,
+                                                               const float* __restrict__ g,
+                                                               const float* __restrict__ stats,
+                                                               float* __restrict__ dX, __nv_bfloat16* __restrict__ dXb,
+                                                               float* __restrict__ part_g, float* __restrict__ part_b) {
+    __shared__ float red[2][8][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = blockIdx.x, s = blockIdx.y;
+    const int nc = D >> 5, nq = gridDim.x;
+    const int64_t sX = (int64_t)rows * D;
+    float gl[kLnMaxC], ag[kLnMaxC], ab[kLnMaxC];
+#pragma unroll
+    for (int c = 0; c < kLnMaxC; ++c) {
+        gl[c] = c < nc ? g[(int64_t)s * D + lane + 32 * c] : 0.0f;
+        ag[c] = ab[c] = 0.0f;
+    }
+    for (int k = 0; k < 8; ++k) {
+        const int r = 64 * q + warp + 8 * k;
+        if (r >= rows) break;
+        const float mean = stats[((int64_t)s * rows + r) * 2], rstd = stats[((int64_t)s * rows + r) * 2 + 1];
+        const float* x = X + s * sX + (int64_t)r * D;
+        const float* dy = dY + s * sX + (int64_t)r * D;
+        float xv[kLnMaxC], dv[kLnMaxC];
+        float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < kLnMaxC; ++c) {
+            xv[c] = dv[c] = 0.0f;
+            if (c < nc) {
+                xv[c] = (x[lane + 32 * c] - mean) * rstd;
+                dv[c] = dy[lane + 32 * c];
+                const float dxh = dv[c] * gl[c];
+                m1 += dxh;
+                m2 += dxh * xv[c];
+            }
+        }
+        m1 = warp_sum(m1) / D;
+        m2 = warp_sum(m2) / D;
+        float* dx = dX + s * sX + (int64_t)r * D;
+#pragma unroll
+        for (int c = 0; c < kLnMaxC; ++c) {
+            if (c < nc) {
+                const float v = dx[lane + 32 * c] + rstd * (dv[c] * gl[c] - m1 - xv[c] * m2);
+                dx[lane + 32 * c] = v;
+                if (dXb) dXb[s * sX + (int64_t)r * D + lane + 32 * c] = __float2bfloat16_rn(v);
+                ag[c] += dv[c] * xv[c];
+                ab[c] += dv[c];
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kLnMaxC; ++c)
+        if (c < nc) {
+            red[0][warp][lane + 32 * c] = ag[c];
+            red[1][warp][lane + 32 * c] = ab[c];
+        }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
+        const int w = i / D, n = i - w * D;
+        float t = 0.0f;
+        for (int j = 0; j < 8; ++j) t += red[w][j][n];
+        (w ? part_b : part_g)[((int64_t)s * nq + q) * D + n] = t;
+    }
+}
+
+bool vit_ln_bwd_fused_ok(int D) { return D % 32 == 0 && D <= 32 * kLnMaxC; }
+void launch_vit_ln_bwd_fused(const float* dY, const float* X, int S, int rows, int D, const float* g,
+                             const float* stats, float* dX, __nv_bfloat16* dXb, float* part_g, float* part_b,
+                             cudaStream_t st) {
+    vit_ln_bwd_fused_kernel<<<dim3((rows + 63) / 64, S), 256, 0, st>>>(dY, X, rows, D, g, stats, dX, dXb, part_g,
+                                                                       part_b);
+}
+
 // ------------------------------------------------------------------------ attention
 // One block per (head h, example b, sample s), 256 threads. Every operand of the head is staged
 // in shared memory as a [TP][PP] tile (T ≤ TP rows, zero padded; pitch 68) and each of

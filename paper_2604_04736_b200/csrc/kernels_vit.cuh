@@ -23,6 +23,13 @@ void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, 
 // dX (pitch ld, sX) += LayerNorm backward of dY; dyxh[s][row][D] = dY ⊙ x̂ (the g-gradient rows)
 void launch_vit_ln_bwd(const float* dY, int64_t ldy, int64_t sdY, const float* X, int S, int rows, int64_t ld,
                        int64_t sX, int D, const float* g, const float* stats, float* dX, float* dyxh, cudaStream_t st);
+// LayerNorm backward of all `rows` rows of each sample (pitch D) with the γ / β gradient sums of
+// every 64-row chunk written to part_g / part_b [s][⌈rows/64⌉][D] (launch_bias_grad's parts) and,
+// if dXb, a bf16 copy of the updated dX; requires vit_ln_bwd_fused_ok(D)
+bool vit_ln_bwd_fused_ok(int D);
+void launch_vit_ln_bwd_fused(const float* dY, const float* X, int S, int rows, int D, const float* g,
+                             const float* stats, float* dX, __nv_bfloat16* dXb, float* part_g, float* part_b,
+                             cudaStream_t st);
 // softmax attention of every (head, example, sample): QKV [s][b][T][3D] → O [s][b][T][D], A [s][b][h][T][T]
 void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A, cudaStream_t st);
 void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D, int heads,

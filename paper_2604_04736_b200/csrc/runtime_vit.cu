@@ -135,7 +135,8 @@ int alloc_vit(bnn_ctx* c) {
             return c->set_err(BNN_ERR_CUDA, "out of memory (ViT bf16 activations)");
     }
     ok = c->alloc(&c->vPb, (size_t)(aug ? Sc : 1) * B * NP * PK) && c->alloc(&c->vHcb, (size_t)Sc * B * D) &&
-         c->alloc(&c->vdXb, (size_t)Sc * R * D) && c->alloc(&c->vdXb2, (size_t)Sc * R * D) &&
+         c->alloc(&c->vdXb, (size_t)Sc * R * D) && c->alloc(&c->vdXb1, (size_t)Sc * R * D) &&
+         c->alloc(&c->vdXb2, (size_t)Sc * R * D) &&
          c->alloc(&c->vdUb, (size_t)Sc * R * M) && c->alloc(&c->vdQKVb, (size_t)Sc * R * 3 * D) &&
          c->alloc(&c->vdEb, (size_t)Sc * B * NP * D) && c->alloc(&c->vdzb, (size_t)Sc * B * ldO);
     if (!ok) return c->set_err(BNN_ERR_CUDA, "out of memory (ViT bf16 gradients)");
@@ -153,7 +154,7 @@ int alloc_vit(bnn_ctx* c) {
         ok = maps(c->vmaps[1 + 4 * l], b.H1, D, D, (int)R, Sc, c->vdQKVb, 3 * D, 3 * D) &&
              maps(c->vmaps[2 + 4 * l], b.O, D, D, (int)R, Sc, c->vdXb2, D, D) &&
              maps(c->vmaps[3 + 4 * l], b.H2, D, D, (int)R, Sc, c->vdUb, M, M) &&
-             maps(c->vmaps[4 + 4 * l], b.A, M, M, (int)R, Sc, c->vdXb, D, D);
+             maps(c->vmaps[4 + 4 * l], b.A, M, M, (int)R, Sc, (l & 1) ? c->vdXb1 : c->vdXb, D, D);
     }
     ok = ok && maps(c->vmaps[1 + 4 * L], c->vHcb, D, D, B, Sc, c->vdzb, c->O, ldO);
     if (!ok) return c->set_err(BNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (ViT)");
@@ -315,6 +316,31 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
                                   acc_mu, acc_rho, st);
         }, 2);
     };
+    // LayerNorm backward of the token rows: the fused kernel (γ / β chunk sums in place, bf16 copy
+    // of dX) when D allows and the chunk sums fit the scratch, else LayerNorm + two row reductions
+    const int nq = (int)((R + 63) / 64);
+    const bool fused_ln = vit_ln_bwd_fused_ok(D) && 2 * (int64_t)Sc * nq * D <= c->vwpart_cap;
+    auto ln_bwd = [&](const float* dY, const float* Xin, int tv, const float* stats, __nv_bfloat16* dXb) {
+        if (fused_ln) {
+            float *pg = c->vwpart, *pb = c->vwpart + (int64_t)Sc * nq * D;
+            c->launch("ln", [&] {
+                launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, dXb, pg, pb, st);
+            });
+            c->launch("bias", [&] {
+                launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                                 acc_rho, st);
+                launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                                 acc_rho, st);
+            }, 4);
+            return;
+        }
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(dY, D, RD, Xin, Sc, (int)R, D, RD, D, c->vvec[tv], stats, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, tv), c->vdyxh, (int)R, D, RD);
+        bias(vec(c, mu, tv + 1), dY, (int)R, D, RD);
+        if (dXb) c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, dXb, st); });
+    };
     {
         const SampledLayer Lh = lin(c, mu, nt - 2);
         const WgItem w{Lh, &c->vmaps[1 + 4 * L], 0};
@@ -336,32 +362,24 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
                            L2 = lin(c, mu, tb + 10);
         const bnn_ctx::VitMaps &mq = c->vmaps[1 + 4 * l], &mo = c->vmaps[2 + 4 * l], &m1 = c->vmaps[3 + 4 * l],
                                &m2 = c->vmaps[4 + 4 * l];
-        // fc2: G = dX_out
-        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb, st); });
+        // fc2: G = dX_out (its bf16 copy: from the next layer's LayerNorm-1 backward, or cast here
+        // below the final LayerNorm, which touches the cls rows only)
+        __nv_bfloat16* dXb_l = (l & 1) ? c->vdXb1 : c->vdXb;
+        if (l == L - 1 || !fused_ln) c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, dXb_l, st); });
         bias(L2, c->vdX, (int)R, D, RD);
         proj_dgrad(c, L2, kk, m2, Sc, (int)R, c->vdU, st);
         // dU = dA ⊙ GELU'(U), in place (fp32, bias gradient) and as the bf16 GEMM operand
         c->launch("elem", [&] { launch_vit_gelu_bwd_cast(a.U, Sc * R * M, c->vdU, c->vdUb, st); });
         bias(L1, c->vdU, (int)R, M, R * M);
         proj_dgrad(c, L1, kk, m1, Sc, (int)R, c->vdH, st);
-        c->launch("ln", [&] {
-            launch_vit_ln_bwd(c->vdH, D, RD, a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], a.st2, c->vdX, c->vdyxh, st);
-        });
-        bias(vec(c, mu, tb + 6), c->vdyxh, (int)R, D, RD);
-        bias(vec(c, mu, tb + 7), c->vdH, (int)R, D, RD);
-        // proj: G = dX_mid
-        c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, c->vdXb2, st); });
+        ln_bwd(c->vdH, a.Xmid, tb + 6, a.st2, c->vdXb2);  // proj: G = dX_mid (and its bf16 copy)
         bias(Lo, c->vdX, (int)R, D, RD);
         proj_dgrad(c, Lo, kk, mo, Sc, (int)R, c->vdO, st);
         c->launch("attn", [&] { launch_vit_attn_bwd_tf32(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdQKV, Sc * R * 3 * D, c->vdQKVb, st); });
         bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
         proj_dgrad(c, Lq, kk, mq, Sc, (int)R, c->vdH, st);
-        c->launch("ln", [&] {
-            launch_vit_ln_bwd(c->vdH, D, RD, a.X, Sc, (int)R, D, RD, D, c->vvec[tb], a.st1, c->vdX, c->vdyxh, st);
-        });
-        bias(vec(c, mu, tb), c->vdyxh, (int)R, D, RD);
-        bias(vec(c, mu, tb + 1), c->vdH, (int)R, D, RD);
+        ln_bwd(c->vdH, a.X, tb, a.st1, l > 0 ? ((l & 1) ? c->vdXb : c->vdXb1) : nullptr);
         // the four weight gradients of the layer (their G / X operands are still intact here)
         const WgItem w[4] = {{L2, &m2, 0}, {L1, &m1, 0}, {Lo, &mo, 0}, {Lq, &mq, 0}};
         proj_wgrad(c, kk, Sc, (int)R, scale, acc_mu, acc_rho, w, 4, st);
@@ -455,6 +473,28 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
                                   acc_mu, acc_rho, st);
         }, 2);
     };
+    const int nq = (int)((R + 63) / 64);  // LayerNorm backward as in vit_chunk_bf16 (no bf16 copy)
+    const bool fused_ln = vit_ln_bwd_fused_ok(D) && 2 * (int64_t)Sc * nq * D <= c->vwpart_cap;
+    auto ln_bwd = [&](const float* dY, const float* Xin, int tv, const float* stats) {
+        if (fused_ln) {
+            float *pg = c->vwpart, *pb = c->vwpart + (int64_t)Sc * nq * D;
+            c->launch("ln", [&] {
+                launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, nullptr, pg, pb, st);
+            });
+            c->launch("bias", [&] {
+                launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                                 acc_rho, st);
+                launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                                 acc_rho, st);
+            }, 4);
+            return;
+        }
+        c->launch("ln", [&] {
+            launch_vit_ln_bwd(dY, D, RD, Xin, Sc, (int)R, D, RD, D, c->vvec[tv], stats, c->vdX, c->vdyxh, st);
+        });
+        bias(vec(c, mu, tv), c->vdyxh, (int)R, D, RD);
+        bias(vec(c, mu, tv + 1), dY, (int)R, D, RD);
+    };
     {
         const SampledLayer Lh = lin(c, mu, nt - 2);
         c->launch("wgrad", [&] {
@@ -485,11 +525,7 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
         c->launch("wgrad", [&] { launch_wgrad_fp32(L1, kk, Sc, (int)R, c->vdU, R * M, a.H2, RD, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(L1, c->vdU, (int)R, M, R * M);
         c->launch("dgrad", [&] { launch_dgrad_fp32(L1, kk, nod, Sc, (int)R, c->vdU, R * M, nullptr, 0, c->vdH, RD, st); });
-        c->launch("ln", [&] {
-            launch_vit_ln_bwd(c->vdH, D, RD, a.Xmid, Sc, (int)R, D, RD, D, c->vvec[tb + 6], a.st2, c->vdX, c->vdyxh, st);
-        });
-        bias(vec(c, mu, tb + 6), c->vdyxh, (int)R, D, RD);
-        bias(vec(c, mu, tb + 7), c->vdH, (int)R, D, RD);
+        ln_bwd(c->vdH, a.Xmid, tb + 6, a.st2);
         // X_mid = X + proj(attention(LN1(X)))
         c->launch("wgrad", [&] { launch_wgrad_fp32(Lo, kk, Sc, (int)R, c->vdX, RD, a.O, RD, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(Lo, c->vdX, (int)R, D, RD);
@@ -498,11 +534,7 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
         c->launch("wgrad", [&] { launch_wgrad_fp32(Lq, kk, Sc, (int)R, c->vdQKV, 3 * RD, a.H1, RD, scale, acc_mu, acc_rho, st, c->vwpart, c->vwpart_cap); });
         bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
         c->launch("dgrad", [&] { launch_dgrad_fp32(Lq, kk, nod, Sc, (int)R, c->vdQKV, 3 * RD, nullptr, 0, c->vdH, RD, st); });
-        c->launch("ln", [&] {
-            launch_vit_ln_bwd(c->vdH, D, RD, a.X, Sc, (int)R, D, RD, D, c->vvec[tb], a.st1, c->vdX, c->vdyxh, st);
-        });
-        bias(vec(c, mu, tb), c->vdyxh, (int)R, D, RD);
-        bias(vec(c, mu, tb + 1), c->vdH, (int)R, D, RD);
+        ln_bwd(c->vdH, a.X, tb, a.st1);
     }
     // X_0 = [cls; patch·W_pᵀ + b_p] + pos
     bias(vec(c, mu, 2), c->vdX, B, (int64_t)T * D, RD);  // cls: token-0 rows
