@@ -20,6 +20,11 @@ __device__ __forceinline__ float ldf(const float* p, int64_t i) { return p[i]; }
 __device__ __forceinline__ float ldf(const __nv_bfloat16* p, int64_t i) { return __bfloat162float(p[i]); }
 __device__ __forceinline__ void stf(float* p, int64_t i, float v) { p[i] = v; }
 __device__ __forceinline__ void stf(__nv_bfloat16* p, int64_t i, float v) { p[i] = __float2bfloat16_rn(v); }
+// exact-erf GELU and its derivative (R29)
+__device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.0f + erff(u * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_df(float u) {
+    return 0.5f * (1.0f + erff(u * 0.70710678118654752f)) + u * 0.39894228040143268f * __expf(-0.5f * u * u);
+}
 
 // ------------------------------------------------------------------------ sampled vectors
 // w[s][i] = μ[off + i] + σ[off + i]·ε(t, 0, i) for the 1-D tensors (LayerNorm g/b, cls, pos)
@@ -118,8 +123,63 @@ void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, 
                        float* Y, int64_t ldy, int64_t sY, float* stats, cudaStream_t st) {
     vit_ln_fwd_kernel<float><<<dim3((rows + 7) / 8, S), 256, 0, st>>>(X, rows, ld, sX, D, g, b, Y, ldy, sY, stats);
 }
+// the same with D = 32·NC known at compile time and RB rows per warp in flight (all loads of a
+// warp's rows issued before its reductions: the row-per-warp form waits one memory latency per row)
+template <int NC>
+__global__ void __launch_bounds__(256) vit_ln_fwd_rows_kernel(const float* __restrict__ X, int rows, int64_t ld,
+                                                              int64_t sX, const float* __restrict__ g,
+                                                              const float* __restrict__ bb,
+                                                              __nv_bfloat16* __restrict__ Y, int64_t ldy, int64_t sY,
+                                                              float* __restrict__ stats) {
+    constexpr int D = 32 * NC, RB = 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, s = blockIdx.y;
+    const int r0 = (blockIdx.x * 8 + warp) * RB;
+    float xv[RB][NC];
+#pragma unroll
+    for (int k = 0; k < RB; ++k)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) xv[k][c] = r0 + k < rows ? X[s * sX + (r0 + k) * ld + lane + 32 * c] : 0.0f;
+    float gl[NC], bl[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        gl[c] = g[(int64_t)s * D + lane + 32 * c];
+        bl[c] = bb[(int64_t)s * D + lane + 32 * c];
+    }
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+        const int r = r0 + k;
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sum += xv[k][c];
+        const float mean = warp_sum(sum) / D;
+        float sq = 0.f;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sq += (xv[k][c] - mean) * (xv[k][c] - mean);
+        const float rstd = rsqrtf(warp_sum(sq) / D + 1e-6f);
+        if (r >= rows) continue;
+        __nv_bfloat16* y = Y + s * sY + r * ldy;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) y[lane + 32 * c] = __float2bfloat16_rn(gl[c] * ((xv[k][c] - mean) * rstd) + bl[c]);
+        if (lane == 0) {
+            stats[((int64_t)s * rows + r) * 2] = mean;
+            stats[((int64_t)s * rows + r) * 2 + 1] = rstd;
+        }
+    }
+}
+
 void launch_vit_ln_fwd(const float* X, int S, int rows, int64_t ld, int64_t sX, int D, const float* g, const float* b,
                        __nv_bfloat16* Y, int64_t ldy, int64_t sY, float* stats, cudaStream_t st) {
+    const dim3 grid((rows + 31) / 32, S);
+#define BNN_LN_FWD(NC)                                                                                          \
+    case NC:                                                                                                    \
+        vit_ln_fwd_rows_kernel<NC><<<grid, 256, 0, st>>>(X, rows, ld, sX, g, b, Y, ldy, sY, stats);             \
+        return;
+    if (D % 32 == 0) switch (D / 32) {
+            BNN_LN_FWD(1) BNN_LN_FWD(2) BNN_LN_FWD(3) BNN_LN_FWD(4) BNN_LN_FWD(5) BNN_LN_FWD(6) BNN_LN_FWD(7)
+            BNN_LN_FWD(8)
+            default: break;
+        }
+#undef BNN_LN_FWD
     vit_ln_fwd_kernel<__nv_bfloat16><<<dim3((rows + 7) / 8, S), 256, 0, st>>>(X, rows, ld, sX, D, g, b, Y, ldy, sY,
                                                                               stats);
 }
@@ -174,76 +234,142 @@ void launch_vit_ln_bwd(const __nv_bfloat16* dY, int64_t ldy, int64_t sdY, const 
 // deterministic), the inputs of launch_bias_grad — instead of a dY ⊙ x̂ tensor re-read by a
 // separate chunk pass. dXb (optional): the bf16 copy of the updated dX rows (the next GEMM operand).
 constexpr int kLnMaxC = 8;  // columns per lane (D ≤ 256)
+template <int NC>
 __global__ void __launch_bounds__(256) vit_ln_bwd_fused_kernel(const float* __restrict__ dY,
-                                                               const float* __restrict__ X, int rows, int D,
+                                                               const float* __restrict__ X, int rows,
                                                                const float* __restrict__ g,
                                                                const float* __restrict__ stats,
                                                                float* __restrict__ dX, __nv_bfloat16* __restrict__ dXb,
-                                                               float* __restrict__ part_g, float* __restrict__ part_b) {
-    __shared__ float red[2][8][256];
+                                                               float* __restrict__ part_g, float* __restrict__ part_b,
+                                                               float* __restrict__ part_x) {
+    constexpr int D = 32 * NC, RB = 4;  // RB rows of a warp in flight (all their loads first)
+    __shared__ float red[3][8][D];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = blockIdx.x, s = blockIdx.y;
-    const int nc = D >> 5, nq = gridDim.x;
+    const int nq = gridDim.x;
     const int64_t sX = (int64_t)rows * D;
-    float gl[kLnMaxC], ag[kLnMaxC], ab[kLnMaxC];
+    float gl[NC], ag[NC], ab[NC], ax[NC];
 #pragma unroll
-    for (int c = 0; c < kLnMaxC; ++c) {
-        gl[c] = c < nc ? g[(int64_t)s * D + lane + 32 * c] : 0.0f;
-        ag[c] = ab[c] = 0.0f;
+    for (int c = 0; c < NC; ++c) {
+        gl[c] = g[(int64_t)s * D + lane + 32 * c];
+        ag[c] = ab[c] = ax[c] = 0.0f;
     }
-    for (int k = 0; k < 8; ++k) {
-        const int r = 64 * q + warp + 8 * k;
-        if (r >= rows) break;
-        const float mean = stats[((int64_t)s * rows + r) * 2], rstd = stats[((int64_t)s * rows + r) * 2 + 1];
-        const float* x = X + s * sX + (int64_t)r * D;
-        const float* dy = dY + s * sX + (int64_t)r * D;
-        float xv[kLnMaxC], dv[kLnMaxC];
-        float m1 = 0.f, m2 = 0.f;
+#pragma unroll 1
+    for (int k0 = 0; k0 < 8; k0 += RB) {
+        float xv[RB][NC], dv[RB][NC], ov[RB][NC], mean[RB], rstd[RB];
 #pragma unroll
-        for (int c = 0; c < kLnMaxC; ++c) {
-            xv[c] = dv[c] = 0.0f;
-            if (c < nc) {
-                xv[c] = (x[lane + 32 * c] - mean) * rstd;
-                dv[c] = dy[lane + 32 * c];
-                const float dxh = dv[c] * gl[c];
+        for (int k = 0; k < RB; ++k) {
+            const int r = 64 * q + warp + 8 * (k0 + k);
+            const bool ok = r < rows;
+            const int64_t o = s * sX + (int64_t)r * D + lane;
+            mean[k] = ok ? stats[((int64_t)s * rows + r) * 2] : 0.0f;
+            rstd[k] = ok ? stats[((int64_t)s * rows + r) * 2 + 1] : 0.0f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                xv[k][c] = ok ? X[o + 32 * c] : 0.0f;
+                dv[k][c] = ok ? dY[o + 32 * c] : 0.0f;
+                ov[k][c] = ok ? dX[o + 32 * c] : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            const int r = 64 * q + warp + 8 * (k0 + k);
+            float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                xv[k][c] = (xv[k][c] - mean[k]) * rstd[k];
+                const float dxh = dv[k][c] * gl[c];
                 m1 += dxh;
-                m2 += dxh * xv[c];
+                m2 += dxh * xv[k][c];
             }
-        }
-        m1 = warp_sum(m1) / D;
-        m2 = warp_sum(m2) / D;
-        float* dx = dX + s * sX + (int64_t)r * D;
+            m1 = warp_sum(m1) * (1.0f / D);
+            m2 = warp_sum(m2) * (1.0f / D);
+            if (r >= rows) continue;
+            const int64_t o = s * sX + (int64_t)r * D + lane;
 #pragma unroll
-        for (int c = 0; c < kLnMaxC; ++c) {
-            if (c < nc) {
-                const float v = dx[lane + 32 * c] + rstd * (dv[c] * gl[c] - m1 - xv[c] * m2);
-                dx[lane + 32 * c] = v;
-                if (dXb) dXb[s * sX + (int64_t)r * D + lane + 32 * c] = __float2bfloat16_rn(v);
-                ag[c] += dv[c] * xv[c];
-                ab[c] += dv[c];
+            for (int c = 0; c < NC; ++c) {
+                const float v = ov[k][c] + rstd[k] * (dv[k][c] * gl[c] - m1 - xv[k][c] * m2);
+                dX[o + 32 * c] = v;
+                if (dXb) dXb[o + 32 * c] = __float2bfloat16_rn(v);
+                ag[c] += dv[k][c] * xv[k][c];
+                ab[c] += dv[k][c];
+                ax[c] += v;
             }
         }
     }
 #pragma unroll
-    for (int c = 0; c < kLnMaxC; ++c)
-        if (c < nc) {
-            red[0][warp][lane + 32 * c] = ag[c];
-            red[1][warp][lane + 32 * c] = ab[c];
-        }
+    for (int c = 0; c < NC; ++c) {
+        red[0][warp][lane + 32 * c] = ag[c];
+        red[1][warp][lane + 32 * c] = ab[c];
+        red[2][warp][lane + 32 * c] = ax[c];
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < 2 * D; i += blockDim.x) {
+    const int nw = part_x ? 3 : 2;
+    for (int i = threadIdx.x; i < nw * D; i += blockDim.x) {
         const int w = i / D, n = i - w * D;
         float t = 0.0f;
+#pragma unroll
         for (int j = 0; j < 8; ++j) t += red[w][j][n];
-        (w ? part_b : part_g)[((int64_t)s * nq + q) * D + n] = t;
+        (w == 0 ? part_g : w == 1 ? part_b : part_x)[((int64_t)s * nq + q) * D + n] = t;
     }
 }
 
 bool vit_ln_bwd_fused_ok(int D) { return D % 32 == 0 && D <= 32 * kLnMaxC; }
 void launch_vit_ln_bwd_fused(const float* dY, const float* X, int S, int rows, int D, const float* g,
                              const float* stats, float* dX, __nv_bfloat16* dXb, float* part_g, float* part_b,
-                             cudaStream_t st) {
-    vit_ln_bwd_fused_kernel<<<dim3((rows + 63) / 64, S), 256, 0, st>>>(dY, X, rows, D, g, stats, dX, dXb, part_g,
-                                                                       part_b);
+                             float* part_x, cudaStream_t st) {
+    const dim3 grid((rows + 63) / 64, S);
+#define BNN_LN_BWD(NC)                                                                                              \
+    case NC:                                                                                                        \
+        vit_ln_bwd_fused_kernel<NC><<<grid, 256, 0, st>>>(dY, X, rows, g, stats, dX, dXb, part_g, part_b, part_x); \
+        break;
+    switch (D / 32) {
+        BNN_LN_BWD(1) BNN_LN_BWD(2) BNN_LN_BWD(3) BNN_LN_BWD(4) BNN_LN_BWD(5) BNN_LN_BWD(6) BNN_LN_BWD(7)
+        BNN_LN_BWD(8)
+        default: break;
+    }
+#undef BNN_LN_BWD
+}
+
+// dUb = bf16(dA ⊙ GELU'(U)) for the BF16 step's fc1 operand, with the fc1 bias source reduced in
+// place: part[s][q][·] = Σ over rows 64q … 64q + 63 (in row order) of dA ⊙ GELU'(U) in fp32 —
+// the fp32 dU itself is never stored. Block (q, s); thread: 4 adjacent columns (M % 4 == 0).
+__global__ void __launch_bounds__(256) vit_gelu_bwd_fused_kernel(const float* __restrict__ U,
+                                                                 const float* __restrict__ dA, int rows, int M,
+                                                                 __nv_bfloat16* __restrict__ dUb,
+                                                                 float* __restrict__ part) {
+    const int q = blockIdx.x, s = blockIdx.y, nq = gridDim.x;
+    const int r0 = 64 * q, r1 = min(rows, r0 + 64);
+    const int64_t base = (int64_t)s * rows * M;
+    constexpr int kR = 8;  // rows in flight: all loads of a group before the (branchy) erf work
+    for (int c = 4 * threadIdx.x; c < M; c += 4 * blockDim.x) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        for (int rg = r0; rg < r1; rg += kR) {
+            float4 u[kR], d[kR];
+#pragma unroll
+            for (int k = 0; k < kR; ++k) {
+                const int64_t i = base + (int64_t)(rg + k) * M + c;
+                u[k] = rg + k < r1 ? __ldg(reinterpret_cast<const float4*>(U + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                d[k] = rg + k < r1 ? __ldg(reinterpret_cast<const float4*>(dA + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int k = 0; k < kR; ++k) {
+                if (rg + k >= r1) break;
+                const int64_t i = base + (int64_t)(rg + k) * M + c;
+                const float v0 = d[k].x * gelu_df(u[k].x), v1 = d[k].y * gelu_df(u[k].y),
+                            v2 = d[k].z * gelu_df(u[k].z), v3 = d[k].w * gelu_df(u[k].w);
+                uint2 o;
+                o.x = pack_bf16x2(v0, v1);
+                o.y = pack_bf16x2(v2, v3);
+                *reinterpret_cast<uint2*>(dUb + i) = o;
+                a0 += v0, a1 += v1, a2 += v2, a3 += v3;
+            }
+        }
+        *reinterpret_cast<float4*>(part + ((int64_t)s * nq + q) * M + c) = make_float4(a0, a1, a2, a3);
+    }
+}
+void launch_vit_gelu_bwd_fused(const float* U, const float* dA, int S, int rows, int M, __nv_bfloat16* dUb,
+                               float* part, cudaStream_t st) {
+    vit_gelu_bwd_fused_kernel<<<dim3((rows + 63) / 64, S), 256, 0, st>>>(U, dA, rows, M, dUb, part);
 }
 
 // ------------------------------------------------------------------------ attention
@@ -873,10 +999,6 @@ static void attn_bwd_tc(const float* QKV, const float* A, const TD* dO, int S, i
 }
 
 // ------------------------------------------------------------------------ elementwise
-__device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.0f + erff(u * 0.70710678118654752f)); }
-__device__ __forceinline__ float gelu_df(float u) {
-    return 0.5f * (1.0f + erff(u * 0.70710678118654752f)) + u * 0.39894228040143268f * __expf(-0.5f * u * u);
-}
 
 __global__ void vit_gelu_kernel(const float* __restrict__ U, int64_t n, float* __restrict__ Aout) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

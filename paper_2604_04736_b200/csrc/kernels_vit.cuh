@@ -25,11 +25,15 @@ void launch_vit_ln_bwd(const float* dY, int64_t ldy, int64_t sdY, const float* X
                        int64_t sX, int D, const float* g, const float* stats, float* dX, float* dyxh, cudaStream_t st);
 // LayerNorm backward of all `rows` rows of each sample (pitch D) with the γ / β gradient sums of
 // every 64-row chunk written to part_g / part_b [s][⌈rows/64⌉][D] (launch_bias_grad's parts) and,
-// if dXb, a bf16 copy of the updated dX; requires vit_ln_bwd_fused_ok(D)
+// if dXb, a bf16 copy of the updated dX; if part_x, the chunk sums of the updated dX (the bias
+// gradient source of the projection whose output gradient dX is); requires vit_ln_bwd_fused_ok(D)
 bool vit_ln_bwd_fused_ok(int D);
 void launch_vit_ln_bwd_fused(const float* dY, const float* X, int S, int rows, int D, const float* g,
                              const float* stats, float* dX, __nv_bfloat16* dXb, float* part_g, float* part_b,
-                             cudaStream_t st);
+                             float* part_x, cudaStream_t st);
+// dUb = bf16(dA ⊙ GELU'(U)) and part[s][⌈rows/64⌉][M] = its fp32 64-row chunk sums (M % 4 == 0)
+void launch_vit_gelu_bwd_fused(const float* U, const float* dA, int S, int rows, int M, __nv_bfloat16* dUb,
+                               float* part, cudaStream_t st);
 // softmax attention of every (head, example, sample): QKV [s][b][T][3D] → O [s][b][T][D], A [s][b][h][T][T]
 void launch_vit_attn_fwd(const float* QKV, int S, int B, int T, int D, int heads, float* O, float* A, cudaStream_t st);
 void launch_vit_attn_bwd(const float* QKV, const float* A, const float* dO, int S, int B, int T, int D, int heads,

@@ -319,19 +319,24 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
     // LayerNorm backward of the token rows: the fused kernel (γ / β chunk sums in place, bf16 copy
     // of dX) when D allows and the chunk sums fit the scratch, else LayerNorm + two row reductions
     const int nq = (int)((R + 63) / 64);
-    const bool fused_ln = vit_ln_bwd_fused_ok(D) && 2 * (int64_t)Sc * nq * D <= c->vwpart_cap;
-    auto ln_bwd = [&](const float* dY, const float* Xin, int tv, const float* stats, __nv_bfloat16* dXb) {
+    // (xb: the projection whose output gradient the updated dX is — its bias sums come along)
+    const bool fused_ln = vit_ln_bwd_fused_ok(D) && 3 * (int64_t)Sc * nq * D <= c->vwpart_cap;
+    auto ln_bwd = [&](const float* dY, const float* Xin, int tv, const float* stats, __nv_bfloat16* dXb,
+                      const SampledLayer* xb) {
         if (fused_ln) {
-            float *pg = c->vwpart, *pb = c->vwpart + (int64_t)Sc * nq * D;
+            const int64_t n1 = (int64_t)Sc * nq * D;
+            float *pg = c->vwpart, *pb = c->vwpart + n1, *px = xb ? c->vwpart + 2 * n1 : nullptr;
             c->launch("ln", [&] {
-                launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, dXb, pg, pb, st);
+                launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, dXb, pg, pb, px, st);
             });
             c->launch("bias", [&] {
                 launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
                 launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
-            }, 4);
+                if (xb)
+                    launch_bias_grad(*xb, kk, Sc, px, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu, acc_rho, st);
+            }, xb ? 6 : 4);
             return;
         }
         c->launch("ln", [&] {
@@ -339,8 +344,10 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         });
         bias(vec(c, mu, tv), c->vdyxh, (int)R, D, RD);
         bias(vec(c, mu, tv + 1), dY, (int)R, D, RD);
+        if (xb) bias(*xb, c->vdX, (int)R, D, RD);
         if (dXb) c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, dXb, st); });
     };
+    const bool fused_gelu = M % 4 == 0 && (int64_t)Sc * nq * M <= c->vwpart_cap;
     {
         const SampledLayer Lh = lin(c, mu, nt - 2);
         const WgItem w{Lh, &c->vmaps[1 + 4 * L], 0};
@@ -366,20 +373,28 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         // below the final LayerNorm, which touches the cls rows only)
         __nv_bfloat16* dXb_l = (l & 1) ? c->vdXb1 : c->vdXb;
         if (l == L - 1 || !fused_ln) c->launch("elem", [&] { launch_vit_cast_bf16(c->vdX, Sc * RD, dXb_l, st); });
-        bias(L2, c->vdX, (int)R, D, RD);
+        if (l == L - 1) bias(L2, c->vdX, (int)R, D, RD);  // else: summed by layer l+1's LayerNorm-1 backward
         proj_dgrad(c, L2, kk, m2, Sc, (int)R, c->vdU, st);
-        // dU = dA ⊙ GELU'(U), in place (fp32, bias gradient) and as the bf16 GEMM operand
-        c->launch("elem", [&] { launch_vit_gelu_bwd_cast(a.U, Sc * R * M, c->vdU, c->vdUb, st); });
-        bias(L1, c->vdU, (int)R, M, R * M);
+        // dU = dA ⊙ GELU'(U): the bf16 GEMM operand, and its fp32 row sums (fc1's bias gradient)
+        if (fused_gelu) {
+            c->launch("elem", [&] { launch_vit_gelu_bwd_fused(a.U, c->vdU, Sc, (int)R, M, c->vdUb, c->vwpart, st); });
+            c->launch("bias", [&] {
+                launch_bias_grad(L1, kk, Sc, c->vwpart, nq, M, (int64_t)nq * M, scale, c->db_scratch, acc_mu, acc_rho,
+                                 st);
+            }, 2);
+        } else {
+            c->launch("elem", [&] { launch_vit_gelu_bwd_cast(a.U, Sc * R * M, c->vdU, c->vdUb, st); });
+            bias(L1, c->vdU, (int)R, M, R * M);
+        }
         proj_dgrad(c, L1, kk, m1, Sc, (int)R, c->vdH, st);
-        ln_bwd(c->vdH, a.Xmid, tb + 6, a.st2, c->vdXb2);  // proj: G = dX_mid (and its bf16 copy)
-        bias(Lo, c->vdX, (int)R, D, RD);
+        ln_bwd(c->vdH, a.Xmid, tb + 6, a.st2, c->vdXb2, &Lo);  // proj: G = dX_mid (bf16 copy, bias sums)
         proj_dgrad(c, Lo, kk, mo, Sc, (int)R, c->vdO, st);
         c->launch("attn", [&] { launch_vit_attn_bwd_tf32(a.QKV, a.Att, c->vdO, Sc, B, T, D, Hh, c->vdQKV, st); });
         c->launch("elem", [&] { launch_vit_cast_bf16(c->vdQKV, Sc * R * 3 * D, c->vdQKVb, st); });
         bias(Lq, c->vdQKV, (int)R, 3 * D, 3 * RD);
         proj_dgrad(c, Lq, kk, mq, Sc, (int)R, c->vdH, st);
-        ln_bwd(c->vdH, a.X, tb, a.st1, l > 0 ? ((l & 1) ? c->vdXb : c->vdXb1) : nullptr);
+        const SampledLayer L2prev = l > 0 ? lin(c, mu, tb - 12 + 10) : SampledLayer{};  // layer l−1's fc2
+        ln_bwd(c->vdH, a.X, tb, a.st1, l > 0 ? ((l & 1) ? c->vdXb : c->vdXb1) : nullptr, l > 0 ? &L2prev : nullptr);
         // the four weight gradients of the layer (their G / X operands are still intact here)
         const WgItem w[4] = {{L2, &m2, 0}, {L1, &m1, 0}, {Lo, &mo, 0}, {Lq, &mq, 0}};
         proj_wgrad(c, kk, Sc, (int)R, scale, acc_mu, acc_rho, w, 4, st);
@@ -474,12 +489,13 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
         }, 2);
     };
     const int nq = (int)((R + 63) / 64);  // LayerNorm backward as in vit_chunk_bf16 (no bf16 copy)
-    const bool fused_ln = vit_ln_bwd_fused_ok(D) && 2 * (int64_t)Sc * nq * D <= c->vwpart_cap;
+    const bool fused_ln = vit_ln_bwd_fused_ok(D) && 3 * (int64_t)Sc * nq * D <= c->vwpart_cap;
     auto ln_bwd = [&](const float* dY, const float* Xin, int tv, const float* stats) {
         if (fused_ln) {
             float *pg = c->vwpart, *pb = c->vwpart + (int64_t)Sc * nq * D;
             c->launch("ln", [&] {
-                launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, nullptr, pg, pb, st);
+                launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, nullptr, pg, pb, nullptr,
+                                        st);
             });
             c->launch("bias", [&] {
                 launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
