@@ -101,8 +101,10 @@ typedef struct bnn_model_desc {
     float dropout_p;  /* MCD: drop probability of every hidden unit, 0 ≤ p < 1 */
     /* BNN_MODEL_VIT: in_h × in_w × in_c images (NHWC fp32),
      * patch × patch patches, width dim, `heads` attention heads, `depth` pre-norm encoder
-     * layers with an MLP of width mlp, n_classes outputs, loss BNN_LOSS_CE; FP32 (SIMT) or BF16
-     * (projections on tcgen05; patch·patch·in_c, dim, mlp multiples of 8; B_loc == max_B_loc).
+     * layers with an MLP of width mlp, n_classes outputs, loss BNN_LOSS_CE; dim % heads == 0,
+     * dim % 4 == 0, dim ≥ 32, 1 + (in_h/patch)·(in_w/patch) ≤ 68 tokens, dim/heads ≤ 68; FP32
+     * (SIMT) or BF16 (projections on tcgen05, attention on the TF32 warp MMA; patch·patch·in_c,
+     * dim, mlp multiples of 8; B_loc == max_B_loc). Violations: BNN_ERR_CONFIG at bnn_create.
      * bnn_predict and the *_MEAN losses are not available for it (BNN_ERR_CONFIG).
      * Tensor order and shapes: oracle/vit_oracle.c header / DESIGN.md §3 (every tensor,
      * LayerNorm g/b, cls and pos included, is variational). */

@@ -77,20 +77,24 @@ void launch_vit_patchify(const float* x, int S, int B, int H, int W, int C, int 
 }
 
 // X0[s][b][0] = cls_s + pos_s[0];  X0[s][b][t] = E[s][b][t−1] + pos_s[t]
+// one thread per 4 columns of a token row (32-bit index math; D % 4 == 0)
 __global__ void vit_embed_kernel(const float* __restrict__ E, const float* __restrict__ cls,
                                  const float* __restrict__ pos, int B, int T, int D, float* __restrict__ X) {
-    const int64_t n = (int64_t)B * T * D;
-    const int s = blockIdx.y;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int d = (int)(i % D), t = (int)((i / D) % T), b = (int)(i / ((int64_t)T * D));
-        const float v = t == 0 ? cls[(int64_t)s * D + d] : E[(((int64_t)s * B + b) * (T - 1) + t - 1) * D + d];
-        X[(int64_t)s * n + i] = v + pos[(int64_t)s * T * D + (int64_t)t * D + d];
-    }
+    const int D4 = D >> 2, n4 = B * T * D4, s = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    const int row = i / D4, d = (i - row * D4) * 4, b = row / T, t = row - b * T;
+    const float4 v = t == 0 ? *reinterpret_cast<const float4*>(cls + (int64_t)s * D + d)
+                            : *reinterpret_cast<const float4*>(E + (((int64_t)s * B + b) * (T - 1) + t - 1) * D + d);
+    const float4 p = *reinterpret_cast<const float4*>(pos + ((int64_t)s * T + t) * D + d);
+    *reinterpret_cast<float4*>(X + ((int64_t)s * B * T + row) * D + d) =
+        make_float4(v.x + p.x, v.y + p.y, v.z + p.z, v.w + p.w);
 }
 
 void launch_vit_embed(const float* E, const float* cls, const float* pos, int S, int B, int T, int D, float* X,
                       cudaStream_t st) {
-    vit_embed_kernel<<<dim3(256, S), 256, 0, st>>>(E, cls, pos, B, T, D, X);
+    const int n4 = B * T * (D / 4);
+    vit_embed_kernel<<<dim3((n4 + 255) / 256, S), 256, 0, st>>>(E, cls, pos, B, T, D, X);
 }
 
 // ------------------------------------------------------------------------ LayerNorm
@@ -1015,12 +1019,12 @@ __global__ void vit_add_kernel(float* __restrict__ Y, const float* __restrict__ 
 // rows r of [S][rows][D] that are token t0 + (r mod per)… : out[s][b][k][d] = in[s][b][t0 + k][d]
 __global__ void vit_gather_tokens_kernel(const float* __restrict__ in, int B, int T, int t0, int nt, int D,
                                          float* __restrict__ out) {
-    const int64_t n = (int64_t)B * nt * D;
-    const int s = blockIdx.y;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int d = (int)(i % D), k = (int)((i / D) % nt), b = (int)(i / ((int64_t)nt * D));
-        out[(int64_t)s * n + i] = in[(((int64_t)s * B + b) * T + t0 + k) * D + d];
-    }
+    const int D4 = D >> 2, n4 = B * nt * D4, s = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    const int row = i / D4, d = (i - row * D4) * 4, b = row / nt, k = row - b * nt;
+    *reinterpret_cast<float4*>(out + ((int64_t)s * B * nt + row) * D + d) =
+        *reinterpret_cast<const float4*>(in + (((int64_t)s * B + b) * T + t0 + k) * D + d);
 }
 
 __global__ void vit_gelu_bf16_kernel(const float* __restrict__ U, int64_t n, __nv_bfloat16* __restrict__ Aout) {
@@ -1079,7 +1083,8 @@ void launch_vit_add(float* Y, const float* X, int64_t n, cudaStream_t st) {
 }
 void launch_vit_gather_tokens(const float* in, int S, int B, int T, int t0, int nt, int D, float* out,
                               cudaStream_t st) {
-    vit_gather_tokens_kernel<<<dim3(256, S), 256, 0, st>>>(in, B, T, t0, nt, D, out);
+    const int n4 = B * nt * (D / 4);
+    vit_gather_tokens_kernel<<<dim3((n4 + 255) / 256, S), 256, 0, st>>>(in, B, T, t0, nt, D, out);
 }
 
 }  // namespace bnn

@@ -48,8 +48,9 @@ SampledLayer vec(const bnn_ctx* c, const float* mu, int t) {
 int build_vit(bnn_ctx* c) {
     const bnn_model_desc& m = c->model;
     if (m.patch < 1 || m.in_h % m.patch || m.in_w % m.patch || m.dim < 32 || m.heads < 1 || m.dim % m.heads ||
-        m.depth < 1 || m.depth > 64 || m.mlp < 1 || m.n_classes < 1 || m.in_c < 1)
-        return c->set_err(BNN_ERR_CONFIG, "ViT: patch | in_h, in_w; dim %% heads == 0, dim >= 32; 1 <= depth <= 64");
+        m.depth < 1 || m.depth > 64 || m.mlp < 1 || m.n_classes < 1 || m.in_c < 1 || m.dim % 4)
+        return c->set_err(BNN_ERR_CONFIG,
+                          "ViT: patch | in_h, in_w; dim %% heads == 0, dim %% 4 == 0, dim >= 32; 1 <= depth <= 64");
     if (m.dim / m.heads > 128) return c->set_err(BNN_ERR_CONFIG, "ViT: head dimension <= 128");
     c->vNP = (m.in_h / m.patch) * (m.in_w / m.patch);
     c->vT = 1 + c->vNP;
