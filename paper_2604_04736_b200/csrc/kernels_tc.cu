@@ -18,6 +18,7 @@
 //           generated rows of W_s, stored MN-major (k contiguous); B = G_s [b][n], K-major.
 //   wgrad : M = n, N = k (64-wide tiles), K = batch b. A = G_sᵀ, MN-major; B = X_s, MN-major.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 
@@ -582,7 +583,12 @@ template <int MODE, int NB>
 static void launch_ws(const CUtensorMap& tmB, TcGenArgs a, int S, cudaStream_t st) {
     const int ntb = (a.B + NB - 1) / NB;
     const int mt = (a.M + 127) / 128;
-    const int chunks = std::max(1, std::min(ntb, (kNumSMs + mt * S - 1) / (mt * S)));
+    // one wave: at most kNumSMs CTAs (one per SM); a 149th CTA would run as a second wave
+    static const int mode = [] {
+        const char* e = std::getenv("BNN_WS_CHUNKS");  // experiment switch: 1 = round the chunk count up
+        return e ? std::atoi(e) : 0;
+    }();
+    const int chunks = std::max(1, std::min(ntb, mode == 1 ? (kNumSMs + mt * S - 1) / (mt * S) : kNumSMs / (mt * S)));
     const int per = (ntb + chunks - 1) / chunks;
     a.nb = NB;
     const dim3 grid(mt, S, (ntb + per - 1) / per);

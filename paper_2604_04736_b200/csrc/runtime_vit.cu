@@ -232,10 +232,11 @@ void proj_wgrad(bnn_ctx* c, const SampleKeys& kk, int Sc, int rows, float scale,
         maps.x[w.nlayers] = it[i].m->wg_x;
         ++w.nlayers;
     }
-    // row splits so that ≈ 148 CTAs run (the tiles alone are 14–40), within the scratch
+    // row splits so that up to 148 CTAs run in ONE wave (the tiles alone are 14–40; a 149th CTA
+    // would be a second wave), within the scratch
     int64_t need = 0;
     for (int i = 0; i < n; ++i) need += 2 * (int64_t)it[i].L.N * it[i].L.K;
-    w.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({(148 /* SMs */ + base - 1) / base, (rows + 511) / 512,
+    w.nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({148 /* SMs */ / base, (rows + 511) / 512,
                                                             c->vwpart_cap / std::max<int64_t>(need, 1)}));
     w.part = c->vwpart;
     int64_t off = 0;
