@@ -1027,6 +1027,25 @@ __global__ void vit_gather_tokens_kernel(const float* __restrict__ in, int B, in
         *reinterpret_cast<const float4*>(in + (((int64_t)s * B + b) * T + t0 + k) * D + d);
 }
 
+// fp32 → bf16 maps, 4 elements per thread and trip (16-B loads, 8-B stores; n % 4 == 0 and
+// aligned buffers, see vec4_ok), two trips' loads in flight
+template <bool GELU>
+__global__ void vit_to_bf16x4_kernel(const float* __restrict__ x, int64_t n4, __nv_bfloat16* __restrict__ y) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += 2 * stride) {
+        const bool two = i + stride < n4;
+        const float4 a = __ldg(reinterpret_cast<const float4*>(x) + i);
+        const float4 b = two ? __ldg(reinterpret_cast<const float4*>(x) + i + stride) : a;
+        auto f = [](float v) { return GELU ? gelu_f(v) : v; };
+        reinterpret_cast<uint2*>(y)[i] = make_uint2(pack_bf16x2(f(a.x), f(a.y)), pack_bf16x2(f(a.z), f(a.w)));
+        if (two)
+            reinterpret_cast<uint2*>(y)[i + stride] =
+                make_uint2(pack_bf16x2(f(b.x), f(b.y)), pack_bf16x2(f(b.z), f(b.w)));
+    }
+}
+static bool vec4_ok(const void* a, const void* b, int64_t n) {
+    return n % 4 == 0 && (reinterpret_cast<uintptr_t>(a) & 15) == 0 && (reinterpret_cast<uintptr_t>(b) & 7) == 0;
+}
 __global__ void vit_gelu_bf16_kernel(const float* __restrict__ U, int64_t n, __nv_bfloat16* __restrict__ Aout) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         Aout[i] = __float2bfloat16_rn(gelu_f(U[i]));
@@ -1045,6 +1064,10 @@ __global__ void vit_cast_bf16_kernel(const float* __restrict__ x, int64_t n, __n
         y[i] = __float2bfloat16_rn(x[i]);
 }
 void launch_vit_gelu(const float* U, int64_t n, __nv_bfloat16* A, cudaStream_t st) {
+    if (vec4_ok(U, A, n)) {
+        vit_to_bf16x4_kernel<true><<<(int)std::min<int64_t>((n / 4 + 511) / 512, 148 * 8), 256, 0, st>>>(U, n / 4, A);
+        return;
+    }
     vit_gelu_bf16_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, A);
 }
 void launch_vit_gelu_bwd(const float* U, int64_t n, const __nv_bfloat16* dA, float* dU, __nv_bfloat16* dUb,
@@ -1070,6 +1093,10 @@ void launch_vit_gelu_bwd_cast(const float* U, int64_t n, float* dA, __nv_bfloat1
     vit_gelu_bwd_cast_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(U, n, dA, dUb);
 }
 void launch_vit_cast_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
+    if (vec4_ok(x, y, n)) {
+        vit_to_bf16x4_kernel<false><<<(int)std::min<int64_t>((n / 4 + 511) / 512, 148 * 8), 256, 0, st>>>(x, n / 4, y);
+        return;
+    }
     vit_cast_bf16_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(x, n, y);
 }
 void launch_vit_gelu(const float* U, int64_t n, float* A, cudaStream_t st) {
