@@ -1,5 +1,6 @@
 // ctx.cuh — private: the bnn_ctx state shared by the runtime translation units.
 #pragma once
+#include <type_traits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -308,8 +309,12 @@ struct bnn_ctx {
             b = ev_pool[ev_next++];
             cudaEventRecord(a, st);
         }
-        f();
-        launches += kernels;
+        if constexpr (std::is_same_v<decltype(f()), int>)
+            launches += f();  // the launcher reports how many kernels it launched
+        else {
+            f();
+            launches += kernels;
+        }
         if (prof) {
             cudaEventRecord(b, st);
             pending.push_back({c, {a, b}});

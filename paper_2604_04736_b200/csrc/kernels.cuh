@@ -121,11 +121,11 @@ struct BiasGroup {
 };
 void launch_bias_grad_grouped(BiasGroup g, const SampleKeys& k, int S, float scale,
                               float* db_scratch, float* acc_mu, float* acc_rho, cudaStream_t st);
-void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
+int launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
                       int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
                       float* acc_mu, float* acc_rho, cudaStream_t st);
 // the same for many rows (nrows > 512): 64-row chunk sums into `scratch` first (capacity in floats)
-void launch_bias_grad_rows(const SampledLayer& L, const SampleKeys& k, int S, const float* parts, int nrows, int ldp,
+int launch_bias_grad_rows(const SampledLayer& L, const SampleKeys& k, int S, const float* parts, int nrows, int ldp,
                            int64_t strideS, float scale, float* scratch, int64_t scratch_cap, float* db_scratch,
                            float* acc_mu, float* acc_rho, cudaStream_t st);
 

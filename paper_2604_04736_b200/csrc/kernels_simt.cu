@@ -10,6 +10,7 @@
 //   KL = ½ Σ (σ² + μ² − 1 − 2 ln σ)
 #include <algorithm>
 
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include <mutex>
@@ -928,6 +929,55 @@ __global__ void __launch_bounds__(32 * kBiasGroups)
     }
 }
 
+// Both phases in one launch for S ≤ 8 samples: the S blocks of a column block form a
+// thread-block cluster (1 × S), each computes its sample's Σ_p as phase A does and leaves
+// (t_s, t_s·ε_s) in its shared memory; the cluster's block 0 reads them over DSMEM in sample
+// order and updates acc (fixed order ⇒ deterministic). Saves the phase-B launch (the ViT step
+// has 54 bias tensors, each ≈ 4 µs of launch-bound phase B).
+__global__ void __launch_bounds__(32 * kBiasGroups)
+    bias_reduce_acc_cluster_kernel(SampledLayer L, SampleKeys kk, const float* __restrict__ parts, int nparts,
+                                   int ldp, int64_t strideS, float scale, float* __restrict__ acc_mu,
+                                   float* __restrict__ acc_rho) {
+    namespace cg = cooperative_groups;
+    __shared__ float red[kBiasGroups][33];
+    __shared__ float out[2][32];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int G = blockDim.x >> 5;
+    const int tx = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + tx, s = blockIdx.y;
+    float acc = 0.0f;
+    if (n < L.N) {  // group g: parts g, g+G, … (fixed order)
+        const float* p = parts + s * strideS + n;
+        float a0 = 0.0f, a1 = 0.0f;
+        int i = g;
+        for (; i + G < nparts; i += 2 * G) {
+            a0 += __ldg(p + (int64_t)i * ldp);
+            a1 += __ldg(p + (int64_t)(i + G) * ldp);
+        }
+        if (i < nparts) a0 += __ldg(p + (int64_t)i * ldp);
+        acc = a0 + a1;
+    }
+    red[g][tx] = acc;
+    __syncthreads();
+    if (g == 0) {
+        float t = 0.0f;
+        for (int j = 0; j < G; ++j) t += red[j][tx];
+        out[0][tx] = t;
+        out[1][tx] = n < L.N ? t * eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0, n) : 0.0f;
+    }
+    cluster.sync();
+    if (cluster.block_rank() == 0 && g == 0 && n < L.N) {
+        float m = 0.0f, r = 0.0f;
+        for (unsigned b = 0; b < cluster.num_blocks(); ++b) {
+            m += *cluster.map_shared_rank(&out[0][tx], b);
+            r += *cluster.map_shared_rank(&out[1][tx], b);
+        }
+        acc_mu[L.off_b + n] += scale * m;
+        acc_rho[L.off_b + n] += scale * r;
+    }
+    cluster.sync();  // the other blocks' shared memory stays alive until block 0 has read it
+}
+
 // phase B: 32 features × 8 sample groups per block, fixed-order smem combine (deterministic)
 __global__ void bias_acc_kernel(SampledLayer L, int S, const float* __restrict__ db, float scale,
                                 float* __restrict__ acc_mu, float* __restrict__ acc_rho) {
@@ -1036,14 +1086,32 @@ void launch_bias_grad_grouped(BiasGroup g, const SampleKeys& k, int S, float sca
     bias_acc_grouped_kernel<<<blocks, 256, 0, st>>>(g, S, db_scratch, scale, acc_mu, acc_rho);
 }
 
-void launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
-                      int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
-                      float* acc_mu, float* acc_rho, cudaStream_t st) {
+int launch_bias_grad(const SampledLayer& L, const SampleKeys& k, int S, const float* parts,
+                     int nparts, int ldp, int64_t strideS, float scale, float* db_scratch,
+                     float* acc_mu, float* acc_rho, cudaStream_t st) {
     dim3 grid((L.N + 31) / 32, S);
     int G = 1;  // part groups per block: enough for the part count (≤ 32), fewer threads when few parts
     while (G < kBiasGroups && G < nparts) G <<= 1;
+    if (S >= 1 && S <= 8) {  // one launch: the S samples of a column block as a thread-block cluster
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(32 * G);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = (unsigned)S;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, bias_reduce_acc_cluster_kernel, L, k, parts, nparts, ldp, strideS, scale, acc_mu,
+                               acc_rho) == cudaSuccess)
+            return 1;
+        (void)cudaGetLastError();  // cluster launch refused: the two-phase form below
+    }
     bias_reduce_kernel<<<grid, 32 * G, 0, st>>>(L, k, parts, nparts, ldp, strideS, S, db_scratch);
     bias_acc_kernel<<<(L.N + 31) / 32, 256, 0, st>>>(L, S, db_scratch, scale, acc_mu, acc_rho);
+    return 2;
 }
 
 // Many rows (the ViT's token rows): first each 64-row chunk is summed in row order into
@@ -1065,17 +1133,16 @@ __global__ void bias_rows_chunk_kernel(const float* __restrict__ parts, int nrow
     chunk[((int64_t)s * nchunks + q) * N + n] = a0 + a1;
 }
 
-void launch_bias_grad_rows(const SampledLayer& L, const SampleKeys& k, int S, const float* parts, int nrows, int ldp,
-                           int64_t strideS, float scale, float* scratch, int64_t scratch_cap, float* db_scratch,
-                           float* acc_mu, float* acc_rho, cudaStream_t st) {
+int launch_bias_grad_rows(const SampledLayer& L, const SampleKeys& k, int S, const float* parts, int nrows, int ldp,
+                          int64_t strideS, float scale, float* scratch, int64_t scratch_cap, float* db_scratch,
+                          float* acc_mu, float* acc_rho, cudaStream_t st) {
     const int nchunks = (nrows + 63) / 64;
-    if (nrows <= 512 || !scratch || (int64_t)S * nchunks * L.N > scratch_cap) {
-        launch_bias_grad(L, k, S, parts, nrows, ldp, strideS, scale, db_scratch, acc_mu, acc_rho, st);
-        return;
-    }
+    if (nrows <= 512 || !scratch || (int64_t)S * nchunks * L.N > scratch_cap)
+        return launch_bias_grad(L, k, S, parts, nrows, ldp, strideS, scale, db_scratch, acc_mu, acc_rho, st);
     bias_rows_chunk_kernel<<<dim3((L.N + 127) / 128, nchunks, S), 128, 0, st>>>(parts, nrows, ldp, strideS, L.N,
                                                                                nchunks, scratch);
-    launch_bias_grad(L, k, S, scratch, nchunks, L.N, (int64_t)nchunks * L.N, scale, db_scratch, acc_mu, acc_rho, st);
+    return 1 + launch_bias_grad(L, k, S, scratch, nchunks, L.N, (int64_t)nchunks * L.N, scale, db_scratch, acc_mu,
+                                acc_rho, st);
 }
 
 }  // namespace bnn

@@ -207,9 +207,9 @@ int mlp_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls,
                 launch_wgrad_fp32(sl, kk, Sc, B, Gl, sG, A, sA, scale, acc_mu, acc_rho, st);
             });
             c->launch("bias", [&] {
-                launch_bias_grad(sl, kk, Sc, Gl, B, c->ld[l + 1], sG, scale, c->db_scratch, acc_mu,
+                return launch_bias_grad(sl, kk, Sc, Gl, B, c->ld[l + 1], sG, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
-            }, 2);
+            });
             if (l > 0)
                 c->launch("dgrad", [&] {
                     launch_dgrad_fp32(sl, kk, c->drop_for(l - 1, true, B), Sc, B, Gl, sG, (const float*)c->act[l], sA,
@@ -477,8 +477,8 @@ int resnet_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycl
             launch_conv_wgrad_fp32(sl, kk, Sc, cs, D.grad, sD, val(op.src), sval(op.src), scale, acc_mu, acc_rho, st);
         });
         c->launch("bias", [&] {
-            launch_bias_grad(sl, kk, Sc, D.grad, B * D.H * D.W, D.C, sD, scale, c->db_scratch, acc_mu, acc_rho, st);
-        }, 2);
+            return launch_bias_grad(sl, kk, Sc, D.grad, B * D.H * D.W, D.C, sD, scale, c->db_scratch, acc_mu, acc_rho, st);
+        });
         if (op.res >= 0) {
             RBuf& Rb = c->rbufs[op.res];
             if (written[op.res])

@@ -523,8 +523,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         c->launch("wgrad", [&] { launch_wgrad_tc(maps, w, ss); });
         cudaStream_t sb = fork_side2(c);  // every bias launch shares db_scratch: one stream
         c->launch("bias", [&] {
-            launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, sb);
-        }, 2);
+            return launch_bias_grad(sl, kk, Sc, c->dz_f32, B, O, (int64_t)B * O, scale, c->db_scratch, acc_mu, acc_rho, sb);
+        });
         TcGenArgs a{};
         a.L = sl;
         a.kk = kk;
@@ -577,9 +577,9 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         // and the wgrad / ε-combine chain each overlap the data-gradient chain on st)
         cudaStream_t sb = fork_side2(c);
         c->launch("bias", [&] {
-            launch_bias_grad(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale, c->db_scratch,
+            return launch_bias_grad(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale, c->db_scratch,
                              acc_mu, acc_rho, sb);
-        }, 2);
+        });
         cudaStream_t ss = fork_side(c);
         // weight gradient with the sample-accumulating ε epilogue
         if (Ld.cin % 64 == 0 || c->rbf[op.src].C_pad == 8) {

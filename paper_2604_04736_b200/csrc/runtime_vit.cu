@@ -314,9 +314,9 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
     NvtxRange nvb("bnn.backward");
     auto bias = [&](const SampledLayer& Lb, const float* G, int rows, int64_t ldp, int64_t sG) {
         c->launch("bias", [&] {
-            launch_bias_grad_rows(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->vwpart, c->vwpart_cap, c->db_scratch,
+            return launch_bias_grad_rows(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->vwpart, c->vwpart_cap, c->db_scratch,
                                   acc_mu, acc_rho, st);
-        }, 2);
+        });
     };
     // LayerNorm backward of the token rows: the fused kernel (γ / β chunk sums in place, bf16 copy
     // of dX) when D allows and the chunk sums fit the scratch, else LayerNorm + two row reductions
@@ -332,13 +332,15 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
                 launch_vit_ln_bwd_fused(dY, Xin, Sc, (int)R, D, c->vvec[tv], stats, c->vdX, dXb, pg, pb, px, st);
             });
             c->launch("bias", [&] {
-                launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                int nk = 0;
+                nk += launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
-                launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                nk += launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
                 if (xb)
-                    launch_bias_grad(*xb, kk, Sc, px, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu, acc_rho, st);
-            }, xb ? 6 : 4);
+                    nk += launch_bias_grad(*xb, kk, Sc, px, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu, acc_rho, st);
+                return nk;
+            });
             return;
         }
         c->launch("ln", [&] {
@@ -381,9 +383,9 @@ int vit_chunk_bf16(bnn_ctx* c, const float* mu, const float* x, const int32_t* y
         if (fused_gelu) {
             c->launch("elem", [&] { launch_vit_gelu_bwd_fused(a.U, c->vdU, Sc, (int)R, M, c->vdUb, c->vwpart, st); });
             c->launch("bias", [&] {
-                launch_bias_grad(L1, kk, Sc, c->vwpart, nq, M, (int64_t)nq * M, scale, c->db_scratch, acc_mu, acc_rho,
+                return launch_bias_grad(L1, kk, Sc, c->vwpart, nq, M, (int64_t)nq * M, scale, c->db_scratch, acc_mu, acc_rho,
                                  st);
-            }, 2);
+            });
         } else {
             c->launch("elem", [&] { launch_vit_gelu_bwd_cast(a.U, Sc * R * M, c->vdU, c->vdUb, st); });
             bias(L1, c->vdU, (int)R, M, R * M);
@@ -486,9 +488,9 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
     NvtxRange nvb("bnn.backward");
     auto bias = [&](const SampledLayer& Lb, const float* G, int rows, int64_t ldp, int64_t sG) {
         c->launch("bias", [&] {
-            launch_bias_grad_rows(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->vwpart, c->vwpart_cap, c->db_scratch,
+            return launch_bias_grad_rows(Lb, kk, Sc, G, rows, (int)ldp, sG, scale, c->vwpart, c->vwpart_cap, c->db_scratch,
                                   acc_mu, acc_rho, st);
-        }, 2);
+        });
     };
     const int nq = (int)((R + 63) / 64);  // LayerNorm backward as in vit_chunk_bf16 (no bf16 copy)
     const bool fused_ln = vit_ln_bwd_fused_ok(D) && 3 * (int64_t)Sc * nq * D <= c->vwpart_cap;
@@ -500,11 +502,13 @@ int vit_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t* ycls, 
                                         st);
             });
             c->launch("bias", [&] {
-                launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                int nk = 0;
+                nk += launch_bias_grad(vec(c, mu, tv), kk, Sc, pg, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
-                launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
+                nk += launch_bias_grad(vec(c, mu, tv + 1), kk, Sc, pb, nq, D, (int64_t)nq * D, scale, c->db_scratch, acc_mu,
                                  acc_rho, st);
-            }, 4);
+                return nk;
+            });
             return;
         }
         c->launch("ln", [&] {
