@@ -83,6 +83,14 @@ void launch_conv3_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Co
 void launch_conv3_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 int conv3_dgrad_parts(const Conv2Args& a);
 int conv3_halo_ok(int H, int W);
+// conv64 (kernels_conv64.cu): stride-1 3×3 64 → 64-channel convs, W-stationary (the sample's 9
+// tap blocks resident in shared memory, loaded once per CTA and sample) and tap-paired (6 MMA
+// groups per 255-pixel tile of the padded stream); wmap = the 64-row K-major W map (fwd) or the
+// transposed map (dgrad), bmap = the HALO window map. Bias partials: conv64_parts per sample.
+void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
+void launch_conv64_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
+int conv64_parts(const Conv2Args& a);
+int conv64_ok(int H, int W);
 
 
 struct ConvWgradArgs {

@@ -227,8 +227,11 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->cmap_hd.resize(L);
     c->halo_fwd.assign(L, 0);
     c->halo_dgrad.assign(L, 0);
+    c->conv64.assign(L, 0);
     const char* he = getenv("BNN_CONV_HALO");
     const bool halo_on = !(he && atoi(he) == 0);
+    const char* c64e = getenv("BNN_CONV64");  // 0: the 64 → 64 layers on conv3's HALO tile instead
+    const bool c64_on = !(c64e && atoi(c64e) == 0);
     for (const ROp& op : c->rops) {
         if (!halo_on || op.type != 0 || is_fc(c, op) || op.src == 0) continue;
         const LayerDesc& Ld = c->layers[op.layer];
@@ -253,6 +256,9 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                 return c->set_err(BNN_ERR_CUDA, "tensor map (conv3 halo dY window) failed");
             c->halo_dgrad[op.layer] = 1;
         }
+        // both directions 64 → 64 (stage 1): the W-stationary tap-paired kernel (kernels_conv64.cu)
+        if (c64_on && Sb.C == 64 && Db.C == 64 && c->rbf[op.src].C_pad == 64 && Ld.cin == 64 && conv64_ok(Db.H, Db.W))
+            c->conv64[op.layer] = 1;
     }
     // stride-2 forward: the input window of a 2-strided conv is a TMA box with element stride 2
     // in W and H (box = 2·extent raw elements, every other one loaded); conv3 256-pixel and
@@ -453,7 +459,10 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
             a.tma_a = c->tma_fwd[op.layer];
             a.halo = c->halo_fwd[op.layer];
             const CUtensorMap& bm = a.halo ? c->cmap_hf[op.layer] : c->cmap_bf[op.layer];
-            c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], bm, a, st); });
+            if (a.halo && c->conv64[op.layer])
+                c->launch("fwd", [&] { launch_conv64_fwd(c->cmap_w64[op.layer], bm, a, st); });
+            else
+                c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], bm, a, st); });
         } else {
             c->launch("fwd", [&] { launch_conv2_fwd(c->cmap_a2f[op.layer], c->cmap_w2[op.layer], a, st); });
         }
@@ -682,7 +691,8 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         if (m_chan) a.tma_a = c->tma_dgrad[op.layer];
         if (m_chan) a.halo = c->halo_dgrad[op.layer];
         if (final) {
-            const int np = m_chan ? conv3_dgrad_parts(a) : conv2_dgrad_parts(a);
+            const int np = (m_chan && a.halo && c->conv64[op.layer]) ? conv64_parts(a)
+                           : m_chan ? conv3_dgrad_parts(a) : conv2_dgrad_parts(a);
             a.addsrc = pending[op.src];
             a.mbits = c->rbf[op.src].mbits;  // written by the producer's forward epilogue
             a.mask = a.mbits ? nullptr : c->rbf[op.src].val;
@@ -696,7 +706,10 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         }
         if (m_chan) {
             const CUtensorMap& bm = a.halo ? c->cmap_hd[op.layer] : c->cmap_bd[op.layer];
-            c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], bm, a, st); });
+            if (a.halo && c->conv64[op.layer])
+                c->launch("dgrad", [&] { launch_conv64_dgrad(c->cmap_wT[op.layer], bm, a, st); });
+            else
+                c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], bm, a, st); });
         } else {
             c->launch("dgrad", [&] { launch_conv2_dgrad(c->cmap_a2d[op.layer], c->cmap_wT[op.layer], a, st); });
         }

@@ -1163,3 +1163,31 @@ def test_out_of_range_label_is_a_numeric_error(precision):
     ctx = native.Context(RAGGED, precision=precision, max_B_loc=8, max_S_loc=2, dataset_size=1.0)
     with pytest.raises(native.BnnError, match="non-finite"):
         ctx.elbo_step(_dev(mu), _dev(rho), _dev(x), _dev(bad), 8, 2, 1, 0)
+
+
+@pytest.mark.parametrize("hw,B", [(16, 3), (32, 2)])
+def test_cnn_bf16_conv64_equals_conv3_halo(hw, B, monkeypatch):
+    """The stage-1 (64 → 64) layers on the W-stationary tap-paired kernel (kernels_conv64.cu)
+    against the same step with those layers on conv3's HALO tile (BNN_CONV64=0): every stored
+    activation and gradient of every layer, and acc_μ / acc_ρ. The two differ only in fp32
+    summation order before the bf16 rounding of each stored value (a rounding tie can flip one
+    bf16 ulp, 2^-8 relative), so the bound is 1e-2 elementwise of each layer's max."""
+    native = _native()
+    model, S = dict(BF16_CNN, in_h=hw, in_w=hw), 2
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    res = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BNN_CONV64", flag)
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=1e4, aug="per_sample")
+        acc = ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0xBEEF, 5).cpu().numpy()
+        torch.cuda.synchronize()
+        n_layers = len(ctx.tensors) // 2
+        lay = [(ctx.layer_output(l, 0).cpu().numpy(),
+                ctx.layer_output(l, 1).cpu().numpy() if l < n_layers - 1 else None) for l in range(n_layers)]
+        res.append((acc, lay))
+    (a0, l0), (a1, l1) = res
+    for l, ((o0, g0), (o1, g1)) in enumerate(zip(l0, l1)):
+        assert np.abs(o1 - o0).max() <= 1e-2 * max(np.abs(o0).max(), 1e-30), ("out", l)
+        if g0 is not None:
+            assert np.abs(g1 - g0).max() <= 1e-2 * max(np.abs(g0).max(), 1e-30), ("grad", l)
+    assert np.abs(a1 - a0).max() <= 1e-2 * np.abs(a0).max()
