@@ -1,29 +1,30 @@
-// kernels_conv64.cu — W-stationary, tap-paired tcgen05 convolution for the stride-1 3×3
+// kernels_conv64.cu — W-stationary, row-packed tcgen05 convolution for the stride-1 3×3
 // 64 → 64-channel layers (the ResNet's stage 1), forward (K3) and data gradient (K4):
 //
 //   fwd   Y[p][co]  = Σ_{kh,kw,ci} X[p ⊕ (kh−1, kw−1)][ci] · W_s[co][kh,kw,ci]
 //   dgrad dX[p][ci] = Σ_{kh,kw,co} dY[p ⊖ (kh−1, kw−1)][co] · W_s[co][kh,kw,ci]
 //
 // Why a separate kernel: with 64 output channels the conv3 tile (M = 128
-// channels × N = 256 pixels) duplicates its 64 weight rows, so half of every MMA is wasted, and
-// the 16 KB weight k-blocks are re-read from L2 for every pixel tile (≈ 646 MB of the 877 MB
-// L2→SM traffic of a stage-1 dgrad launch, profiles/r02/ncu).
+// channels × N = 256 pixels) duplicates its 64 weight rows, so half of every MMA is wasted, the
+// 16 KB weight k-blocks are re-read from L2 for every pixel tile (≈ 646 MB of the 877 MB L2→SM
+// traffic of a stage-1 dgrad launch, profiles/r02/ncu), and its channel-major accumulator needs
+// a shared-memory transpose per 32 × 32 block before the NHWC epilogue.
 //
 //  * W-stationary: the sample's 9 tap blocks (64 × 64 bf16 each, 72 KB) are loaded ONCE per CTA
 //    into resident shared memory; a CTA walks a contiguous range of (sample, pixel tile), so it
 //    reloads them at most once (when its range crosses a sample boundary). Only the halo
-//    windows stream (one ≈ 47 KB window of whole padded rows per tile, as conv3's HALO tile).
-//  * Tap pairing: an M = 128 MMA whose rows 0–63 hold tap a = (dh, −1) and rows 64–127 tap
-//    b = (dh, 0) of the same kernel row, run against the window at tap a's offset, puts tap
-//    b's contribution to pixel n − 1 in TMEM lane 64 + co, column n (tap b's window offset is
-//    tap a's + 1). Three such pairs plus three single taps (dw = +1, rows 64–127 zero) cover
-//    the 9 taps in 6 MMA groups instead of 9. A tile computes 256 columns and outputs the 255
-//    pixels whose upper contribution it holds: out[n] = L[n] + U[n + 1].
-//  * Epilogue: warp q of the TMEM lane quarters (q = 0, 1: lower channels 0–31 / 32–63;
-//    q = 2, 3: upper) transposes its 32 channels × 32 columns through shared memory (the upper
-//    warps shifted by one column), then each lower/upper warp pair sums the two and finishes
-//    the NHWC rows thread = pixel, 16 channels each (+ bias, + residual, ReLU, ReLU bitmask /
-//    + other contribution, input ReLU mask, bias-gradient partials), 32-byte stores.
+//    windows stream (≤ 30 KB of whole padded rows per 128-pixel tile, a ring of 4).
+//  * Row packing: pixels on M (128 consecutive positions of the padded pixel stream, one halo
+//    window), and the three taps of one kernel row (dh, dw = −1, 0, +1) side by side on
+//    N = 192 (3 × 64 output channels). One MMA group per kernel row, run against the window at
+//    the dw = −1 offset, puts tap (dh, dw)'s contribution to pixel n − (dw + 1) in TMEM lane n,
+//    columns 64(dw + 1) + co: 3 groups × 4 K-steps per tile, all 192 columns useful.
+//  * Epilogue (thread = pixel = TMEM lane): out[n] = D[n][0:64] + D[n+1][64:128] + D[n+2][128:192]
+//    — two warp shuffles per value; the 2 lanes at each warp boundary take their neighbours'
+//    values from a 96-float shared exchange (one named barrier per tile and channel half); a
+//    tile outputs 126 of its 128 rows. Then the NHWC row in place: + bias, + residual, ReLU,
+//    ReLU bitmask (fwd) / + other contribution, input ReLU mask, bias-gradient partials (dgrad),
+//    32 channels = 64 contiguous bytes per thread.
 #include <algorithm>
 
 #include <cuda_bf16.h>
@@ -37,17 +38,23 @@ namespace bnn {
 using namespace ptx;
 
 namespace c64 {
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = (kEpiWarps + 2) * 32;  // + the TMA warp + the MMA warp
+// epilogue warps: groups of 8 (4 lane quarters × 2 channel halves); the forward runs two groups
+// (even / odd tiles: two MMA tile-times per epilogue), the dgrad one (its bias-gradient butterfly
+// does not fit the 96-register budget of 18 warps)
+template <int MODE> constexpr int groups() { return MODE == 0 ? 2 : 1; }
+template <int MODE> constexpr int threads() { return (8 * groups<MODE>() + 2) * 32; }  // + TMA, MMA warps
 constexpr int kBlk = 64 * 128;                  // one tap block: 64 rows × 64 bf16 (SWIZZLE_128B)
-constexpr int kWres = 12 * kBlk;                // 6 groups of two blocks (3 pairs, 3 singles + zeros)
-constexpr int kWin = 374 * 128;                 // one halo window (11 padded rows × 34 px at 32 × 32)
-constexpr int kTransPitch = 33;                 // floats per transposed row (conflict-free)
-constexpr int kTrans = kEpiWarps * 32 * kTransPitch * 4;
-constexpr int kTileN = 255;                     // output pixels per tile (256 MMA columns)
+constexpr int kWres = 9 * kBlk;                 // 3 kernel rows × 3 taps (72 KB)
+constexpr int kNWin = 4;                        // halo window ring
+constexpr int kWin = 240 * 128;                 // one window (7 padded rows × 34 px at 32 × 32)
+constexpr int kTileM = 128;                     // MMA rows (pixels of the padded stream)
+constexpr int kTileP = 126;                     // output pixels per tile (rows 126, 127: neighbours only)
+constexpr int kN = 192;                         // 3 taps × 64 channels
+constexpr int kCh = 32;                         // channels per epilogue warp
+constexpr int kXb = 2 * 2 * 2 * 4 * 3 * kCh * 4;  // [group][tile parity][channel half][lane quarter][3 × 32]
+constexpr int kBred = 2 * 2 * 2 * 4 * kCh * 4;   // [group][tile parity][channel half][lane quarter][32]
 constexpr int kBars = 256;
-constexpr int kBred = 2 * kEpiWarps * 16 * 4;
-constexpr int kSmem = 1024 + kWres + 2 * kWin + kTrans + kBars + kBred;
+constexpr int kSmem = 1024 + kWres + kNWin * kWin + kXb + kBred + kBars;
 static_assert(kSmem <= 227 * 1024, "conv64 shared memory");
 }  // namespace c64
 
@@ -56,47 +63,91 @@ __host__ __device__ __forceinline__ int c64_floor_div(int a, int b) {  // b > 0
     return (a % b != 0 && a < 0) ? q - 1 : q;
 }
 
-// resident slot of tap (dh, dw) (window offsets dh·(W+2) + dw): pairs [(dh,−1), (dh,0)] in
-// slots 2(dh+1), 2(dh+1)+1; singles (dh,+1) in slot 6 + 2(dh+1), its upper slot zero
-__host__ __device__ __forceinline__ int c64_slot(int dh, int dw) {
-    return dw == 1 ? 6 + 2 * (dh + 1) : 2 * (dh + 1) + dw + 1;
-}
-
-// 32 lanes × 32 columns plus the column after them (one wait)
-__device__ __forceinline__ void tmem_ld33(uint32_t taddr, float* v, float& e) {
-    uint32_t r[33];
+// 32 lanes × 32 columns at three column offsets 64 apart (one wait)
+__device__ __forceinline__ void tmem_ld32x3(uint32_t ta, float* a, float* b, float* c) {
+    uint32_t r[96];
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {%32}, [%34];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31]), "=r"(r[32])
-        : "r"(taddr), "r"(taddr + 32)
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%96];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%97];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%64,%65,%66,%67,%68,%69,%70,%71,%72,%73,%74,%75,%76,%77,%78,%79,%80,%81,%82,%83,%84,%85,%86,%87,%88,%89,%90,%91,%92,%93,%94,%95}, [%98];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63]), "=r"(r[64]), "=r"(r[65]), "=r"(r[66]), "=r"(r[67]), "=r"(r[68]), "=r"(r[69]), "=r"(r[70]), "=r"(r[71]), "=r"(r[72]), "=r"(r[73]), "=r"(r[74]), "=r"(r[75]), "=r"(r[76]), "=r"(r[77]), "=r"(r[78]), "=r"(r[79]), "=r"(r[80]), "=r"(r[81]), "=r"(r[82]), "=r"(r[83]), "=r"(r[84]), "=r"(r[85]), "=r"(r[86]), "=r"(r[87]), "=r"(r[88]), "=r"(r[89]), "=r"(r[90]), "=r"(r[91]), "=r"(r[92]), "=r"(r[93]), "=r"(r[94]), "=r"(r[95])
+        : "r"(ta), "r"(ta + 64), "r"(ta + 128)
         : "memory");
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-    e = __uint_as_float(r[32]);
+    for (int i = 0; i < 32; ++i) {
+        a[i] = __uint_as_float(r[i]);
+        b[i] = __uint_as_float(r[32 + i]);
+        c[i] = __uint_as_float(r[64 + i]);
+    }
+}
+
+// v of lane + d, or `other` where lane + d is past the warp (shfl's in-range predicate selects)
+__device__ __forceinline__ float shfl_down_or(float v, int d, float other) {
+    float r;
+    asm(
+        "{\n\t.reg .pred p;\n\t.reg .f32 t;\n\t"
+        "shfl.sync.down.b32 t|p, %1, %2, 0x1f, 0xffffffff;\n\t"
+        "selp.f32 %0, t, %3, p;\n\t}"
+        : "=f"(r)
+        : "f"(v), "r"(d), "f"(other));
+    return r;
+}
+
+// 32 lanes × 32 columns at two column offsets (one wait)
+__device__ __forceinline__ void tmem_ld32x2(uint32_t ta, uint32_t tb, float* a, float* b) {
+    uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(ta), "r"(tb)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        a[i] = __uint_as_float(r[i]);
+        b[i] = __uint_as_float(r[32 + i]);
+    }
+}
+
+// 32-byte global load / store (LDG.256 / STG.256: one full sector per lane)
+template <bool NC>
+__device__ __forceinline__ void ld256(const void* p, uint32_t* r) {
+    if (NC)
+        asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "l"(p));
+    else
+        asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st256(void* p, const uint32_t* r) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                 "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__device__ __forceinline__ void add_bf16x16(float* z, uint4 a, uint4 b) {
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+// lane j ends with Σ over the warp's 32 lanes of v[j] (fixed butterfly order)
+__device__ __forceinline__ float c64_transpose_sum(float* v, int lane) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        z[2 * e] += __uint_as_float(w[e] << 16);
-        z[2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool hi = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const float send = hi ? v[i] : v[i + off];
+            const float keep = hi ? v[i + off] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
     }
+    return v[0];
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(c64::kThreads, 1)
+__global__ void __launch_bounds__(c64::threads<MODE>(), 1)
     conv64_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
                   const Conv2Args a) {
     using namespace c64;
@@ -104,39 +155,36 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sW = smem;
     uint8_t* sWin = sW + kWres;
-    float* trans = reinterpret_cast<float*>(sWin + 2 * kWin);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(trans) + kTrans);
+    float* xb = reinterpret_cast<float*>(sWin + kNWin * kWin);
+    float* bred = xb + kXb / 4;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bred + kBred / 4);
     uint64_t* wres_full = bars;
     uint64_t* wres_empty = bars + 1;
-    uint64_t* wfull = bars + 2;   // [2] halo windows
-    uint64_t* wempty = bars + 4;  // [2]
-    uint64_t* tfull = bars + 6;   // [2] TMEM accumulators
-    uint64_t* tempty = bars + 8;  // [2]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
-    float* bred = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBars);  // [2][8 warps][16]
+    uint64_t* wfull = bars + 2;            // [kNWin] halo windows
+    uint64_t* wempty = bars + 2 + kNWin;   // [kNWin]
+    uint64_t* tfull = bars + 2 + 2 * kNWin;  // [2] TMEM accumulators
+    uint64_t* tempty = tfull + 2;          // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    constexpr int WTMA = kEpiWarps, WMMA = kEpiWarps + 1;
+    constexpr int NG = groups<MODE>();
+    constexpr int WTMA = 8 * NG, WMMA = WTMA + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int PH = a.H, PW = a.W;  // stride 1, pad 1: the output grid is the input grid
     const int PWp = PW + 2, PHp = PH + 1;
-    const int ptiles = (a.B * PHp * PWp + kTileN - 1) / kTileN;
+    const int ptiles = (a.B * PHp * PWp + kTileP - 1) / kTileP;
     const int64_t T = (int64_t)a.S * ptiles;
     const int t0 = (int)(T * blockIdx.x / gridDim.x), t1 = (int)(T * (blockIdx.x + 1) / gridDim.x);
 
-    // the zero upper halves of the single-tap groups (slots 7, 9, 11): written once
-    for (int i = threadIdx.x; i < 3 * kBlk / 16; i += blockDim.x) {
-        const int z = i / (kBlk / 16), o = i - z * (kBlk / 16);
-        reinterpret_cast<uint4*>(sW + (7 + 2 * z) * kBlk)[o] = make_uint4(0u, 0u, 0u, 0u);
-    }
-    fence_proxy_async_smem();
     if (threadIdx.x == 0) {
         mbar_init(wres_full, 1);
         mbar_init(wres_empty, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNWin; ++i) {
             mbar_init(&wfull[i], 1);
             mbar_init(&wempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], kEpiWarps);
+            mbar_init(&tempty[i], 8);
         }
         mbar_fence_init();
     }
@@ -160,19 +208,19 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
                     for (int tap = 0; tap < 9; ++tap) {
                         const int kh = tap / 3, kw = tap - 3 * kh;
                         const int dh = MODE == 0 ? kh - 1 : 1 - kh, dw = MODE == 0 ? kw - 1 : 1 - kw;
-                        uint8_t* dst = sW + c64_slot(dh, dw) * kBlk;
+                        uint8_t* dst = sW + (3 * (dh + 1) + dw + 1) * kBlk;  // kernel row dh: dw = −1, 0, +1
                         if (MODE == 0)
-                            tma_load_3d(&wmap, wres_full, dst, tap * 64, 0, s);  // [co][ci] K-major
+                            tma_load_3d(&wmap, wres_full, dst, tap * 64, 0, s);  // [co][ci]: K-major B
                         else
-                            tma_load_5d(&wmap, wres_full, dst, 0, tap, 0, 0, s);  // [co][ci]: MN-major A
+                            tma_load_5d(&wmap, wres_full, dst, 0, tap, 0, 0, s);  // [co][ci]: MN-major B
                     }
                     cur_s = s;
                     ++seg;
                 }
-                const int ws = tl & 1;
-                mbar_wait_role(&wempty[ws], ((tl >> 1) & 1) ^ 1);
-                const int p0 = pt * kTileN;
-                const int rs = c64_floor_div(p0 - PWp - 1, PWp), re = c64_floor_div(p0 + 256 + PWp, PWp);
+                const int ws = tl % kNWin;
+                mbar_wait_role(&wempty[ws], ((tl / kNWin) & 1) ^ 1);
+                const int p0 = pt * kTileP;
+                const int rs = c64_floor_div(p0 - PWp - 1, PWp), re = c64_floor_div(p0 + kTileM + PWp, PWp);
                 uint8_t* win = sWin + ws * kWin;
                 mbar_arrive_expect_tx(&wfull[ws], (uint32_t)((re - rs + 1) * PWp * 128));
                 for (int r = rs; r <= re; ++r) {
@@ -183,9 +231,9 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
         }
         __syncwarp();
     } else if (warp == WMMA) {
-        // ------------------------------------------------ MMA issuer: 6 groups × 4 K-steps per tile
+        // ------------------------------------------------ MMA issuer: 3 kernel rows × 4 K-steps per tile
         if (lane == 0) {
-            const uint32_t idesc = idesc_bf16(128, 256, MODE == 1 ? 1 : 0, 0);
+            const uint32_t idesc = idesc_bf16(kTileM, kN, 0, MODE == 1 ? 1 : 0);
             int cur_s = -1, seg = 0, tl = 0;
             for (int t = t0; t < t1; ++t, ++tl) {
                 const int s = t / ptiles, pt = t - s * ptiles;
@@ -194,162 +242,187 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
                     cur_s = s;
                     ++seg;
                 }
-                const int buf = tl & 1;
+                const int buf = tl & 1, ws = tl % kNWin;
                 mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
-                mbar_wait_role(&wfull[buf], (tl >> 1) & 1);
+                mbar_wait_role(&wfull[ws], (tl / kNWin) & 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
-                const int p0 = pt * kTileN;
+                const int p0 = pt * kTileP;
                 const int wrow0 = p0 - c64_floor_div(p0 - PWp - 1, PWp) * PWp;  // window row of pixel p0
-                const uint32_t winb = smem_u32(sWin + buf * kWin);
+                const uint32_t winb = smem_u32(sWin + ws * kWin);
 #pragma unroll
-                for (int g = 0; g < 6; ++g) {
-                    const int dh = (g < 3 ? g : g - 3) - 1, dw = g < 3 ? -1 : 1;  // the lower tap
-                    const uint32_t aBase = smem_u32(sW + 2 * g * kBlk);
-                    const uint32_t bBase = winb + (uint32_t)(wrow0 + dh * PWp + dw) * 128u;
+                for (int g = 0; g < 3; ++g) {  // kernel row dh = g − 1, window at its dw = −1 tap
+                    const uint32_t aBase = winb + (uint32_t)(wrow0 + (g - 1) * PWp - 1) * 128u;
+                    const uint32_t bBase = smem_u32(sW + 3 * g * kBlk);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint64_t ad = MODE == 0 ? sdesc_sw128(aBase + 32 * q, 16, 1024)
-                                                      : sdesc_sw128(aBase + 2048 * q, kBlk, 1024);
-                        const uint64_t bd = sdesc_sw128(bBase + 32 * q, 16, 1024);
+                        const uint64_t ad = sdesc_sw128(aBase + 32 * q, 16, 1024);
+                        const uint64_t bd = MODE == 0 ? sdesc_sw128(bBase + 32 * q, 16, 1024)
+                                                      : sdesc_sw128(bBase + 2048 * q, kBlk, 1024);
                         mma_bf16(d, ad, bd, idesc, (g | q) != 0 ? 1u : 0u);
                     }
                 }
-                mma_commit(&wempty[buf]);
+                mma_commit(&wempty[ws]);
                 mma_commit(&tfull[buf]);
                 if (t + 1 < t1 && (t + 1) / ptiles != s) mma_commit(wres_empty);  // W free for the next sample
             }
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------ epilogue
-        const int q = warp & 3, h = warp >> 2;
-        const bool upper = q >= 2;
-        const int cg = q & 1;             // channel group of 32
-        const int pair = 1 + cg + 2 * h;  // named barrier of the lower/upper warp pair
-        float* tr_self = trans + warp * 32 * kTransPitch;
-        const float* tr_lo = trans + (upper ? warp - 2 : warp) * 32 * kTransPitch;
-        const float* tr_up = trans + (upper ? warp : warp + 2) * 32 * kTransPitch;
-        const int cl = upper ? 16 : 0;      // this thread's 16 channels within the group
-        const int chq = cg * 32 + cl;       // … within the 64
-        int tl = 0;
-        for (int t = t0; t < t1; ++t, ++tl) {
+        // ------------------------------------------------ epilogue: group g = warp / 8 takes the tiles
+        // of TMEM buffer g (every other tile of the CTA: each group has two MMA tile-times per
+        // epilogue); warp (q, h) = TMEM lane quarter q (pixels 32q … 32q+31), channels 32h … 32h+31
+        const int g = warp >> 3, q = warp & 3, h = (warp >> 2) & 1;
+        const int bar_id = 1 + 2 * g + h;
+        const int ch0 = kCh * h;
+        const int m = 32 * q + lane;  // tile row = pixel offset
+        // x / PWp and x / PHp as a multiply-shift (x < 2^24: exact with a 40-bit reciprocal)
+        const uint64_t mW = ((1ull << 40) + PWp - 1) / PWp, mH = ((1ull << 40) + PHp - 1) / PHp;
+        int prev_s = 0, prev_pt = 0;
+        int tl = g;
+        for (int t = t0 + g; t < t1; t += NG, tl += NG) {
             const int s = t / ptiles, pt = t - s * ptiles;
-            const int buf = tl & 1;
-            const int p0 = pt * kTileN;
+            const int buf = tl & 1, par = (tl / NG) & 1;
             const int64_t so = (int64_t)s * a.out_stride_s;
-            float bias16[16], bacc[16];
+            const int pix = pt * kTileP + m;
+            const int r = (int)(((uint64_t)pix * mW) >> 40), cx = pix - r * PWp;
+            const int b = (int)(((uint64_t)r * mH) >> 40), y = r - b * PHp;
+            const bool pv = m < kTileP && b < a.B && y < PH && cx >= 1 && cx <= PW;
+            const int64_t ro = pv ? (((int64_t)b * PH + y) * PW + cx - 1) * 64 + ch0 : 0;
+            uint32_t xw[16];  // 32 bf16 of the residual / other contribution: two 32-byte loads
 #pragma unroll
-            for (int k = 0; k < 16; ++k) bacc[k] = 0.0f;
-            if (MODE == 0) {
-                const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO + chq);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float4 b4 = __ldg(bs + k);
-                    bias16[4 * k] = b4.x;
-                    bias16[4 * k + 1] = b4.y;
-                    bias16[4 * k + 2] = b4.z;
-                    bias16[4 * k + 3] = b4.w;
-                }
+            for (int i = 0; i < 16; ++i) xw[i] = 0u;
+            uint32_t mw = 0xFFFFFFFFu;
+            const __nv_bfloat16* opnd = MODE == 0 ? a.res : a.addsrc;
+            if (pv && opnd) {  // the row's residual / other contribution, in flight during the wait
+                ld256<MODE == 0>(opnd + so + ro, xw);  // dgrad: the contribution may be the output buffer
+                ld256<MODE == 0>(opnd + so + ro + 16, xw + 8);
             }
+            if (MODE == 1 && pv && a.mbits) mw = __ldg(a.mbits + ((so + ro) >> 5));
             mbar_wait(&tfull[buf], (tl >> 1) & 1);
             tc_fence_after();
-#pragma unroll 1
-            for (int i = 0; i < 4; ++i) {
-                const int c = 4 * h + i;
-                // the pass's pixel (thread = pixel after the transpose) and its operand rows: in
-                // flight while the accumulator is read and transposed
-                const int m = 32 * c + lane;
-                const int pix = p0 + m;
-                const int r = pix / PWp, cx = pix - r * PWp, b = r / PHp, y = r - b * PHp;
-                const bool pv = m < kTileN && b < a.B && y < PH && cx >= 1 && cx <= PW;
-                const int64_t rowoff = pv ? (((int64_t)b * PH + y) * PW + cx - 1) * 64 : 0;
-                uint4 x0 = make_uint4(0u, 0u, 0u, 0u), x1 = x0;
-                uint32_t mw = 0xFFFFFFFFu;
-                const __nv_bfloat16* opnd = MODE == 0 ? a.res : a.addsrc;
-                if (pv && opnd) {
-                    const uint4* p = reinterpret_cast<const uint4*>(opnd + so + rowoff + chq);
-                    x0 = MODE == 0 ? __ldg(p) : p[0];
-                    x1 = MODE == 0 ? __ldg(p + 1) : p[1];
+            const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + ch0;
+            float z[kCh], v[16];
+            float* xq = xb + (((g * 2 + par) * 2 + h) * 4 + q) * 3 * kCh;
+            // xq: [0] row 0's dw = +1 block, [1] row 0's dw = 0 block, [2] row 1's dw = +1 block —
+            // what the previous quarter's rows 30, 31 need from this one. 16 channels at a time
+            // (register budget of 18 warps).
+#pragma unroll
+            for (int c = 0; c < kCh; c += 16) {
+                tmem_ld16(ta + c, z + c);       // block dw = −1 (this pixel)
+                tmem_ld16(ta + 64 + c, v);      // dw = 0 (pixel − 1)
+                if (q > 0 && lane == 0) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(xq + kCh + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 }
-                if (MODE == 1 && pv && a.mbits) mw = __ldg(a.mbits + ((so + rowoff + cg * 32) >> 5));
-                float v[32], e = 0.0f;
-                const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + 32 * c;
-                if (upper && c < 7)
-                    tmem_ld33(ta, v, e);
-                else
-                    tmem_ld32(ta, v);
-                if (i == 3) {  // this warp's last TMEM read of the tile
+#pragma unroll
+                for (int j = 0; j < 16; ++j) z[c + j] += shfl_down_or(v[j], 1, 0.0f);
+                tmem_ld16(ta + 128 + c, v);     // dw = +1 (pixel − 2)
+                if (c + 16 == kCh) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[buf]);
                 }
-                if (!upper) {
+                if (q > 0 && lane < 2) {
+                    float* d = xq + (lane == 0 ? 0 : 2 * kCh) + c;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) tr_self[j * kTransPitch + lane] = v[j];
-                } else {  // upper column n + 1 holds pixel n
-#pragma unroll
-                    for (int j = 0; j < 31; ++j) tr_self[j * kTransPitch + lane] = v[j + 1];
-                    tr_self[31 * kTransPitch + lane] = e;
+                    for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 }
-                named_bar(pair, 64);
-                float z[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    z[k] = tr_lo[lane * kTransPitch + cl + k] + tr_up[lane * kTransPitch + cl + k];
-                named_bar(pair, 64);  // both halves read before the next chunk overwrites them
-                if (!pv) continue;
-                if (MODE == 0) {
+                for (int j = 0; j < 16; ++j) z[c + j] += shfl_down_or(v[j], 2, 0.0f);
+            }
+            named_bar(bar_id, 4 * 32);  // the exchange of this tile is written
+            if (q < 3 && lane >= 30) {  // rows 30, 31: the next quarter's rows 0, 1 (same summation order)
+                const float* xn = xb + (((g * 2 + par) * 2 + h) * 4 + q + 1) * 3 * kCh;
+                if (lane == 31) {
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) z[k] += bias16[k];
-                    if (a.res) add_bf16x16(z, x0, x1);
-                    if (a.relu) {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) z[k] = fmaxf(z[k], 0.0f);
+                    for (int j = 0; j < kCh; j += 4) {
+                        const float4 fb = *reinterpret_cast<const float4*>(xn + kCh + j);
+                        const float4 fc = *reinterpret_cast<const float4*>(xn + 2 * kCh + j);
+                        z[j] = (z[j] + fb.x) + fc.x;
+                        z[j + 1] = (z[j + 1] + fb.y) + fc.y;
+                        z[j + 2] = (z[j + 2] + fb.z) + fc.z;
+                        z[j + 3] = (z[j + 3] + fb.w) + fc.w;
                     }
                 } else {
-                    if (a.addsrc) add_bf16x16(z, x0, x1);
-                    const uint32_t mb = mw >> cl;
 #pragma unroll
-                    for (int k = 0; k < 16; ++k)
-                        if (!((mb >> k) & 1u)) z[k] = 0.0f;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) bacc[k] += z[k];
-                }
-                uint32_t pk[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) pk[k] = pack_bf16x2(z[2 * k], z[2 * k + 1]);
-                uint4* op = reinterpret_cast<uint4*>(a.out + so + rowoff + chq);
-                op[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                op[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                if (MODE == 0 && a.mbits_out) {  // bits of the stored bf16 values (> 0), 16 per thread
-                    uint32_t bits = 0;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t lo = pk[k] & 0xFFFFu, hi = pk[k] >> 16;
-                        bits |= (uint32_t)((lo & 0x7FFFu) != 0 && (lo & 0x8000u) == 0) << (2 * k);
-                        bits |= (uint32_t)((hi & 0x7FFFu) != 0 && (hi & 0x8000u) == 0) << (2 * k + 1);
+                    for (int j = 0; j < kCh; j += 4) {
+                        const float4 fc = *reinterpret_cast<const float4*>(xn + j);
+                        z[j] += fc.x;
+                        z[j + 1] += fc.y;
+                        z[j + 2] += fc.z;
+                        z[j + 3] += fc.w;
                     }
-                    reinterpret_cast<uint16_t*>(a.mbits_out)[((so + rowoff + cg * 32) >> 4) + (upper ? 1 : 0)] =
-                        (uint16_t)bits;
                 }
             }
-            if (MODE == 1 && a.bpart) {  // Σ over the tile's pixels per channel, fixed order
+            if (MODE == 1 && a.bpart && t > t0 + g && q == 0) {  // this group's previous tile's bias partials
+                const float* rb = bred + ((g * 2 + (par ^ 1)) * 2 + h) * 4 * kCh;
+                a.bpart[(int64_t)prev_s * a.bpart_stride_s + (int64_t)prev_pt * a.C + ch0 + lane] =
+                    ((rb[lane] + rb[kCh + lane]) + rb[2 * kCh + lane]) + rb[3 * kCh + lane];
+            }
+            if (pv) {
+                if (MODE == 0) {
+                    const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO + ch0);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) tr_self[lane * kTransPitch + k] = bacc[k];
-                __syncwarp();
-                float sum = 0.0f;
-                if (lane < 16) {
-#pragma unroll 8
-                    for (int r = 0; r < 32; ++r) sum += tr_self[r * kTransPitch + lane];
+                    for (int k = 0; k < kCh / 4; ++k) {
+                        const float4 b4 = __ldg(bs + k);
+                        z[4 * k] += b4.x;
+                        z[4 * k + 1] += b4.y;
+                        z[4 * k + 2] += b4.z;
+                        z[4 * k + 3] += b4.w;
+                    }
                 }
-                __syncwarp();
-                float* red = bred + (tl & 1) * kEpiWarps * 16;
-                if (lane < 16) red[warp * 16 + lane] = sum;
-                named_bar(5, kEpiWarps * 32);
-                if (h == 0 && lane < 16)
-                    a.bpart[(int64_t)s * a.bpart_stride_s + (int64_t)pt * a.C + chq + lane] =
-                        red[warp * 16 + lane] + red[(warp + 4) * 16 + lane];
+                if (opnd) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        z[2 * e] += __uint_as_float(xw[e] << 16);
+                        z[2 * e + 1] += __uint_as_float(xw[e] & 0xFFFF0000u);
+                    }
+                }
+                if (MODE == 0) {
+                    if (a.relu) {
+#pragma unroll
+                        for (int j = 0; j < kCh; ++j) z[j] = fmaxf(z[j], 0.0f);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kCh; ++j)
+                        if (!((mw >> j) & 1u)) z[j] = 0.0f;
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) pk[k] = pack_bf16x2(z[2 * k], z[2 * k + 1]);
+                st256(a.out + so + ro, pk);  // one full 32-byte sector per store
+                st256(a.out + so + ro + 16, pk + 8);
+                if (MODE == 0 && a.mbits_out) {
+                    // bit j = (stored bf16 of channel ch0 + j > 0); after the ReLU no stored value is
+                    // negative, so > 0 ⟺ magnitude bits ≠ 0: (x & 0x7FFF) + 0x7FFF carries into bit 15
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t c = ((pk[k] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x80008000u;
+                        bits |= (((c >> 15) & 1u) | (c >> 30)) << (2 * k);  // bit 0: low half, bit 1: high half
+                    }
+                    a.mbits_out[(so + ro) >> 5] = bits;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kCh; ++j) z[j] = 0.0f;
+            }
+            if (MODE == 1 && a.bpart) {  // Σ over the quarter's 32 pixels per channel (fixed order)
+                const float bsum = c64_transpose_sum(z, lane);  // lane j: channel ch0 + j
+                bred[(((g * 2 + par) * 2 + h) * 4 + q) * kCh + lane] = bsum;
+            }
+            prev_s = s;
+            prev_pt = pt;
+        }
+        if (MODE == 1 && a.bpart && t1 > t0 + g) {  // flush the group's last tile's partials
+            named_bar(bar_id, 4 * 32);
+            if (q == 0) {
+                const float* rb = bred + ((g * 2 + (((tl - NG) / NG) & 1)) * 2 + h) * 4 * kCh;
+                a.bpart[(int64_t)prev_s * a.bpart_stride_s + (int64_t)prev_pt * a.C + ch0 + lane] =
+                    ((rb[lane] + rb[kCh + lane]) + rb[2 * kCh + lane]) + rb[3 * kCh + lane];
             }
         }
     }
@@ -361,19 +434,19 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
     }
 }
 
-int conv64_ok(int H, int W) {  // the padded window of a 255-pixel tile fits one window stage
+int conv64_ok(int H, int W) {  // the padded window of a 128-row tile fits one window stage
     const int PWp = W + 2;
-    const int rows = (256 + 2 * PWp + 1 + PWp - 1) / PWp + 1;
+    const int rows = (c64::kTileM + 3 * PWp) / PWp + 1;
     return H >= 1 && rows * PWp * 128 <= c64::kWin ? 1 : 0;
 }
 
-int conv64_parts(const Conv2Args& a) { return (a.B * (a.H + 1) * (a.W + 2) + c64::kTileN - 1) / c64::kTileN; }
+int conv64_parts(const Conv2Args& a) { return (a.B * (a.H + 1) * (a.W + 2) + c64::kTileP - 1) / c64::kTileP; }
 
 template <int MODE>
 static void launch_conv64(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(conv64_kernel<MODE>), c64::kSmem);
     const int64_t T = (int64_t)a.S * conv64_parts(a);
-    conv64_kernel<MODE><<<(int)std::min<int64_t>(T, kNumSMs), c64::kThreads, c64::kSmem, st>>>(wmap, bmap, a);
+    conv64_kernel<MODE><<<(int)std::min<int64_t>(T, kNumSMs), c64::threads<MODE>(), c64::kSmem, st>>>(wmap, bmap, a);
 }
 
 void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
