@@ -91,6 +91,13 @@ void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const C
 void launch_conv64_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 int conv64_parts(const Conv2Args& a);
 int conv64_ok(int H, int W);
+// conv64 weight gradient: the fp32 per-sample partials part[s][split][64][576] of the ε combine,
+// one CTA per (sample, split) (nsplit = conv64_wgrad_nsplit(S)); ymap / xmap = the HALO window
+// maps of dY and of the layer input.
+struct ConvWgradArgs;
+void launch_conv64_wgrad(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st);
+int conv64_wgrad_ok(int H, int W);
+int conv64_wgrad_nsplit(int S);
 
 
 struct ConvWgradArgs {

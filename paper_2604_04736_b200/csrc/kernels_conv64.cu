@@ -434,6 +434,167 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
     }
 }
 
+// ============================================================================ weight gradient
+// dW_s[co][kh,kw][ci] = Σ_p dY_s[p][co] · X_s[p ⊕ (kh−1, kw−1)][ci]   (per sample)
+// over the padded pixel stream (pad columns and separator rows of dY and X are zero), split into
+// contiguous pixel ranges, one (sample, split) per CTA. Both operands come straight out of halo
+// windows as MN-major SWIZZLE_128B views (scripts/mn_desc_test.cu, profiles/r02/mn_desc_test.txt):
+//   A (M = 128): rows 0–63 = dY[p][co], rows 64–127 = dY[p + 1][co] (second M block one 128-B row
+//     later: LBO = 128 B);
+//   B (N = 192): X[p + o + j·(W+2)][ci], j = 0, 1, 2 (N blocks one padded row apart).
+// With o = −(W+2) + 1 the lower rows give the taps (dh, +1) of the three kernel rows and the upper
+// rows, whose dY is one pixel later, the taps (dh, 0); with o = −(W+2) − 1 the lower rows give
+// (dh, −1) (upper rows unused). Two N = 192 MMAs per 16 pixels cover all 9 taps (the generic
+// conv2 wgrad: three MMAs, N = 256, 256, 64, half of M idle). Output: the fp32 per-sample
+// partials part[s][split][co][tap·64 + ci] of the ε combine (kernels_conv2.cu).
+namespace c64w {
+constexpr int kKpx = 128;                 // pixels per k-block
+constexpr int kXw = 240 * 128;            // X window: ≤ 240 padded pixels (7 rows of 34)
+constexpr int kYw = 176 * 128;            // dY window: ≤ 176 padded pixels (5 rows of 34)
+constexpr int kStages = 4;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (kEpiWarps + 2) * 32;
+constexpr int kSmem = 1024 + kStages * (kXw + kYw) + 256;
+static_assert(kSmem <= 227 * 1024, "conv64 wgrad shared memory");
+}  // namespace c64w
+
+__global__ void __launch_bounds__(c64w::kThreads, 1)
+    conv64_wgrad_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
+                        const ConvWgradArgs a) {
+    using namespace c64w;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * (kXw + kYw));
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
+    constexpr int WTMA = kEpiWarps, WMMA = kEpiWarps + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int PH = a.H, PW = a.W, PWp = PW + 2, PHp = PH + 1;
+    const int s = blockIdx.x / a.nsplit, u = blockIdx.x - s * a.nsplit;
+    const int nkb_all = (a.B * PHp * PWp + kKpx - 1) / kKpx;
+    const int kb0 = (int)((int64_t)nkb_all * u / a.nsplit), kb1 = (int)((int64_t)nkb_all * (u + 1) / a.nsplit);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_fence_init();
+    }
+    if (warp == WMMA) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == WTMA) {
+        if (lane == 0) {
+            tma_prefetch_desc(&ymap);
+            tma_prefetch_desc(&xmap);
+            for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+                const int st = it % kStages;
+                mbar_wait_role(&empty[st], ((it / kStages) & 1) ^ 1);
+                const int p0 = kb * kKpx;
+                const int xs = c64_floor_div(p0 - PWp - 1, PWp), xe = c64_floor_div(p0 + kKpx + PWp, PWp);
+                const int ys = c64_floor_div(p0, PWp), ye = c64_floor_div(p0 + kKpx, PWp);
+                uint8_t* xw = smem + st * (kXw + kYw);
+                uint8_t* yw = xw + kXw;
+                mbar_arrive_expect_tx(&full[st], (uint32_t)((xe - xs + 1 + ye - ys + 1) * PWp * 128));
+                for (int r = xs; r <= xe; ++r) {
+                    const int b = c64_floor_div(r, PHp), y = r - b * PHp;  // y == PH, b ∉ [0, B): zeros
+                    tma_load_5d(&xmap, &full[st], xw + (r - xs) * PWp * 128, 0, -1, y, b, s);
+                }
+                for (int r = ys; r <= ye; ++r) {
+                    const int b = c64_floor_div(r, PHp), y = r - b * PHp;
+                    tma_load_5d(&ymap, &full[st], yw + (r - ys) * PWp * 128, 0, -1, y, b, s);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == WMMA) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_bf16(128, 192, 1, 1);
+            for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+                const int st = it % kStages;
+                mbar_wait_role(&full[st], (it / kStages) & 1);
+                tc_fence_after();
+                const int p0 = kb * kKpx;
+                const int xs = c64_floor_div(p0 - PWp - 1, PWp), ys = c64_floor_div(p0, PWp);
+                const uint32_t xb0 = smem_u32(smem + st * (kXw + kYw)) + (uint32_t)(p0 - xs * PWp) * 128u;
+                const uint32_t yb0 = smem_u32(smem + st * (kXw + kYw) + kXw) + (uint32_t)(p0 - ys * PWp) * 128u;
+#pragma unroll
+                for (int q = 0; q < kKpx / 16; ++q) {
+                    const uint64_t ad = sdesc_sw128(yb0 + 2048 * q, 128, 1024);
+                    const uint64_t bA = sdesc_sw128(xb0 + 2048 * q + (uint32_t)(1 - PWp) * 128u, PWp * 128, 1024);
+                    const uint64_t bB = sdesc_sw128(xb0 + 2048 * q - (uint32_t)(1 + PWp) * 128u, PWp * 128, 1024);
+                    const uint32_t acc = (it | q) != 0 ? 1u : 0u;
+                    mma_bf16(tmem, ad, bA, idesc, acc);        // taps (dh, +1) | (dh, 0)
+                    mma_bf16(tmem + 256, ad, bB, idesc, acc);  // taps (dh, −1) | unused
+                }
+                mma_commit(&empty[st]);
+            }
+            mma_commit(tfull);
+        }
+        __syncwarp();
+    } else {
+        // epilogue: warp (q, hh) — TMEM lane quarter q (lower rows: co = 32q + lane; upper rows:
+        // co = 32(q − 2) + lane), column blocks split between hh = 0, 1
+        const int q = warp & 3, hh = warp >> 2;
+        const bool upper = q >= 2;
+        const int co = 32 * (q & 1) + lane;
+        const bool any = kb1 > kb0;
+        if (any) {
+            mbar_wait(tfull, 0);
+            tc_fence_after();
+        }
+        float* outrow = a.part + ((int64_t)(s * a.nsplit + u) * 64 + co) * 576;
+        // (accumulator column block, tap) pairs of this warp: lower rows: A blocks j → tap 3j + 2,
+        // B blocks j → tap 3j; upper rows: A blocks j → tap 3j + 1
+        const int nblk = upper ? 3 : 6;
+        for (int i = hh; i < nblk; i += 2) {
+            const int j = i % 3;
+            const bool tileB = i >= 3;
+            const int tap = upper ? 3 * j + 1 : (tileB ? 3 * j : 3 * j + 2);
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < 64; c += 32) {
+                __syncwarp();
+                if (any) {
+                    tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + (tileB ? 256 : 0) + 64 * j + c, v);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+                }
+                float4* o4 = reinterpret_cast<float4*>(outrow + tap * 64 + c);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == WMMA) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+int conv64_wgrad_ok(int H, int W) {  // both halo windows of a 128-pixel k-block fit their stages
+    const int PWp = W + 2;
+    const int rx = (c64w::kKpx + 3 * PWp) / PWp + 1, ry = (c64w::kKpx + PWp) / PWp + 1;
+    return H >= 1 && rx * PWp * 128 <= c64w::kXw && ry * PWp * 128 <= c64w::kYw ? 1 : 0;
+}
+
+int conv64_wgrad_nsplit(int S) { return std::max(1, kNumSMs / std::max(S, 1)); }
+
+void launch_conv64_wgrad(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st) {
+    ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel), c64w::kSmem);
+    conv64_wgrad_kernel<<<a.S * a.nsplit, c64w::kThreads, c64w::kSmem, st>>>(ymap, xmap, a);
+}
+
 int conv64_ok(int H, int W) {  // the padded window of a 128-row tile fits one window stage
     const int PWp = W + 2;
     const int rows = (c64::kTileM + 3 * PWp) / PWp + 1;

@@ -26,6 +26,25 @@ bool is_proj_output(const bnn_ctx* c, int buf) {
 
 // buffer whose gradient is "dL/d(this op's pre-activation output)": the op's own output,
 // except for a projection, whose output sc is summed into the block output y
+// stage-1 64 → 64 stride-1 3×3 convs on the W-stationary row-packed kernels (kernels_conv64.cu);
+// BNN_CONV_HALO=0 or BNN_CONV64=0 puts them back on conv3's tiles, BNN_CONV64W=0 their weight
+// gradients back on the generic conv2 wgrad
+static bool env_on(const char* name) {
+    const char* e = getenv(name);
+    return !(e && atoi(e) == 0);
+}
+bool conv64_layer(const bnn_ctx* c, const ROp& op) {
+    if (op.type != 0 || is_fc(c, op) || op.src == 0 || !env_on("BNN_CONV_HALO") || !env_on("BNN_CONV64")) return false;
+    const LayerDesc& Ld = c->layers[op.layer];
+    const RBuf& Sb = c->rbufs[op.src];
+    const RBuf& Db = c->rbufs[op.dst];
+    return Ld.stride == 1 && Ld.k == 3 && Ld.pad == 1 && Ld.cin == 64 && Ld.cout == 64 && Sb.C == 64 &&
+           Db.C == 64 && c->rbf[op.src].C_pad == 64 && Db.H == Sb.H && Db.W == Sb.W && conv64_ok(Db.H, Db.W);
+}
+bool conv64w_layer(const bnn_ctx* c, const ROp& op) {
+    return conv64_layer(c, op) && env_on("BNN_CONV64W") && conv64_wgrad_ok(c->rbufs[op.dst].H, c->rbufs[op.dst].W);
+}
+
 int grad_src_buffer(const bnn_ctx* c, int dst) {
     if (is_proj_output(c, dst))
         for (const ROp& op : c->rops)
@@ -115,7 +134,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                     c->wkpx[op.layer] = kp;
             }
             const int blocks = (int)((npix + c->wkpx[op.layer] - 1) / c->wkpx[op.layer]);
-            c->nsplit[op.layer] = conv2_wgrad_nsplit(base, blocks);
+            c->nsplit[op.layer] = conv64w_layer(c, op) ? conv64_wgrad_nsplit(Sc) : conv2_wgrad_nsplit(base, blocks);
             if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
             pmax = std::max(pmax, (size_t)Sc * c->nsplit[op.layer] * Ld.cout * Kt);
             continue;
@@ -230,8 +249,6 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->conv64.assign(L, 0);
     const char* he = getenv("BNN_CONV_HALO");
     const bool halo_on = !(he && atoi(he) == 0);
-    const char* c64e = getenv("BNN_CONV64");  // 0: the 64 → 64 layers on conv3's HALO tile instead
-    const bool c64_on = !(c64e && atoi(c64e) == 0);
     for (const ROp& op : c->rops) {
         if (!halo_on || op.type != 0 || is_fc(c, op) || op.src == 0) continue;
         const LayerDesc& Ld = c->layers[op.layer];
@@ -256,9 +273,8 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                 return c->set_err(BNN_ERR_CUDA, "tensor map (conv3 halo dY window) failed");
             c->halo_dgrad[op.layer] = 1;
         }
-        // both directions 64 → 64 (stage 1): the W-stationary tap-paired kernel (kernels_conv64.cu)
-        if (c64_on && Sb.C == 64 && Db.C == 64 && c->rbf[op.src].C_pad == 64 && Ld.cin == 64 && conv64_ok(Db.H, Db.W))
-            c->conv64[op.layer] = 1;
+        // both directions 64 → 64 (stage 1): the W-stationary row-packed kernel (kernels_conv64.cu)
+        if (conv64_layer(c, op) && c->halo_fwd[op.layer] && c->halo_dgrad[op.layer]) c->conv64[op.layer] = 1;
     }
     // stride-2 forward: the input window of a 2-strided conv is a TMA box with element stride 2
     // in W and H (box = 2·extent raw elements, every other one loaded); conv3 256-pixel and
@@ -620,7 +636,10 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             if (w.kpx != c->wkpx[op.layer]) return c->set_err(BNN_ERR_CONFIG, "wgrad k-step / operand path mismatch");
             // the buffer is free once the ε combine that last read it (two layers back) is done
             if (split3) cudaStreamWaitEvent(ss, c->ev_comb[wbuf], 0);
-            c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, ss); });
+            if (c->conv64[op.layer] && conv64w_layer(c, op))  // both halo window maps exist for conv64 layers
+                c->launch("wgrad", [&] { launch_conv64_wgrad(c->cmap_hd[op.layer], c->cmap_hf[op.layer], w, ss); });
+            else
+                c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, ss); });
             cudaStream_t sc = ss;
             if (split3) {  // ε combine on the third stream, overlapping the next layer's wgrad GEMM
                 cudaEventRecord(c->ev_wg[wbuf], ss);

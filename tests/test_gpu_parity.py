@@ -1191,3 +1191,27 @@ def test_cnn_bf16_conv64_equals_conv3_halo(hw, B, monkeypatch):
         if g0 is not None:
             assert np.abs(g1 - g0).max() <= 1e-2 * max(np.abs(g0).max(), 1e-30), ("grad", l)
     assert np.abs(a1 - a0).max() <= 1e-2 * np.abs(a0).max()
+
+
+@pytest.mark.parametrize("hw,B,S", [(16, 3, 2), (32, 2, 3)])
+def test_cnn_bf16_conv64_wgrad_equals_conv2_wgrad(hw, B, S, monkeypatch):
+    """The stage-1 weight gradients on the row-packed kernel (conv64_wgrad_kernel: MN-major views of
+    two halo windows, 2 MMAs of N = 192 per 16 pixels) against the generic conv2 wgrad
+    (BNN_CONV64W=0) on the same step: acc_μ and acc_ρ of every tensor. Both accumulate the same
+    bf16 products in fp32, in a different split / pixel order, so they agree to fp32 summation
+    error (1e-4 of each tensor's max; a wrong tap, channel or pixel is O(1))."""
+    native = _native()
+    model = dict(BF16_CNN, in_h=hw, in_w=hw)
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    accs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BNN_CONV64W", flag)
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=1e4, aug="per_sample")
+        accs.append(_acc_parts(ctx, ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0xBEEF, 5)))
+        torch.cuda.synchronize()
+    (m0, r0, l0), (m1, r1, l1) = accs
+    for t in ctx.tensors:
+        sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
+        for name, u, ref in (("acc_mu", m1[sl], m0[sl]), ("acc_rho", r1[sl], r0[sl])):
+            assert np.abs(u - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
+    assert l1 == l0
