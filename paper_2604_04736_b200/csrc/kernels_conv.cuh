@@ -98,6 +98,12 @@ struct ConvWgradArgs;
 void launch_conv64_wgrad(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st);
 int conv64_wgrad_ok(int H, int W);
 int conv64_wgrad_nsplit(int S);
+// ε-fused form (clusters of the S ≤ 8 samples of a split): writes scale·Σ_s (D_s, ε_s ⊙ D_s) to
+// split partials part[split][μ | ρ][64·576] for launch_wgrad_split_reduce; nsplit =
+// conv64_wgrad_eps_nsplit(S) (co-resident clusters, 0 = not available). Returns 0 or -1 (launch refused).
+int conv64_wgrad_eps_nsplit(int S, int Gc);
+int conv64_wgrad_eps_cluster(int S);  // default cluster size (BNN_WGRAD_EPS_CLUSTER overrides)
+int launch_conv64_wgrad_eps(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st);
 
 
 struct ConvWgradArgs {
@@ -115,6 +121,7 @@ struct ConvWgradArgs {
     int n_tile;              // conv2 wgrad: column-tile width (256; the last tile may be narrower)
     int kpx;                 // pixels per k-step: 128 on the TMA path where the window fits, else 64
     int dbg;                 // timing experiments only (BNN_CONV_DEBUG); 0 in production
+    int eps_cluster;         // ε-fused conv64 wgrad: samples per thread-block cluster (divides S, ≤ 8)
 };
 void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off,
                                float* acc_mu, float* acc_rho, cudaStream_t st);

@@ -26,7 +26,9 @@
 //    ReLU bitmask (fwd) / + other contribution, input ReLU mask, bias-gradient partials (dgrad),
 //    32 channels = 64 contiguous bytes per thread.
 #include <algorithm>
+#include <cstdlib>
 
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -458,6 +460,27 @@ constexpr int kSmem = 1024 + kStages * (kXw + kYw) + 256;
 static_assert(kSmem <= 227 * 1024, "conv64 wgrad shared memory");
 }  // namespace c64w
 
+// cluster size of the ε-fused form (a.eps_cluster): by default 2 samples when S is even
+// (measured, one B200 with this kernel's 214 KB of shared memory: 15 co-resident clusters of 8 =
+// 120 CTAs, 32 of 4 = 128, pairs fill the chip: 156 / 149 / 133 µs per C3 layer), else 1; the
+// groups of a split are summed by the split reduce in (split, group) order.
+// BNN_WGRAD_EPS_CLUSTER=S (S ≤ 8) sums all samples of a split over DSMEM (no per-group partials).
+int conv64_wgrad_eps_cluster(int S) {
+    const char* e = getenv("BNN_WGRAD_EPS_CLUSTER");
+    if (e) {
+        const int g = atoi(e);
+        if (g >= 1 && g <= 8 && S % g == 0) return g;
+    }
+    return S % 2 == 0 ? 2 : 1;
+}
+
+// EPS (ε-fused, sample-accumulating): the S samples of one pixel split form a thread-block
+// cluster (rank = sample). Each CTA turns its D_s into (D_s, ε_s ⊙ D_s) — ε regenerated, the same
+// EPS-v1 draw as the forward's W_s — and leaves them in its shared memory; after a cluster barrier
+// CTA j sums rows [j·64/S, (j+1)·64/S) over the S samples in sample order (DSMEM reads) and writes
+// scale·Σ to the split partials part[split][μ | ρ][64·576] (wgrad_split_reduce adds the splits in
+// order). No per-sample partials, no separate ε combine (north_star (3)); deterministic.
+template <bool EPS>
 __global__ void __launch_bounds__(c64w::kThreads, 1)
     conv64_wgrad_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
                         const ConvWgradArgs a) {
@@ -472,9 +495,14 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
     constexpr int WTMA = kEpiWarps, WMMA = kEpiWarps + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int PH = a.H, PW = a.W, PWp = PW + 2, PHp = PH + 1;
-    const int s = blockIdx.x / a.nsplit, u = blockIdx.x - s * a.nsplit;
+    // EPS: blockIdx = (partial index u = split·groups + group)·Gc + rank, sample = group·Gc + rank;
+    // pixel split = u / groups (a.nsplit counts the partials, splits × groups)
+    const int Gc = EPS ? a.eps_cluster : 1, groups = a.S / Gc;
+    const int s = EPS ? (int)((blockIdx.x / Gc) % groups) * Gc + (int)(blockIdx.x % Gc) : (int)(blockIdx.x / a.nsplit);
+    const int u = EPS ? (int)(blockIdx.x / Gc) : (int)(blockIdx.x - s * a.nsplit);
+    const int usplit = EPS ? u / groups : u, nsplit_px = EPS ? a.nsplit / groups : a.nsplit;
     const int nkb_all = (a.B * PHp * PWp + kKpx - 1) / kKpx;
-    const int kb0 = (int)((int64_t)nkb_all * u / a.nsplit), kb1 = (int)((int64_t)nkb_all * (u + 1) / a.nsplit);
+    const int kb0 = (int)((int64_t)nkb_all * usplit / nsplit_px), kb1 = (int)((int64_t)nkb_all * (usplit + 1) / nsplit_px);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) {
@@ -539,7 +567,7 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
             mma_commit(tfull);
         }
         __syncwarp();
-    } else {
+    } else if (!EPS) {
         // epilogue: warp (q, hh) — TMEM lane quarter q (lower rows: co = 32q + lane; upper rows:
         // co = 32(q − 2) + lane), column blocks split between hh = 0, 1
         const int q = warp & 3, hh = warp >> 2;
@@ -574,6 +602,79 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
             }
         }
     }
+    if (EPS) {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        constexpr int kPitch = 196;  // floats per exchange row (conflict-free float4 stores)
+        float* xch = reinterpret_cast<float*>(smem);  // [2: D, ε⊙D][64 co][kPitch]: the stage memory, free now
+        const bool any = kb1 > kb0;
+        const int q = warp & 3, hh = warp >> 2;
+        if (warp < kEpiWarps && any) {
+            mbar_wait(tfull, 0);
+            tc_fence_after();
+        }
+        const int S = Gc;  // the cluster's samples
+        const int rank = (int)cluster.block_rank();
+        const int rows = (64 + S - 1) / S, r0 = rank * rows, r1 = min(64, r0 + rows);
+        const int n = 64 * 576;
+        for (int j = 0; j < 3; ++j) {  // kernel row j: taps 3j (tile B lower), 3j+1 (tile A upper), 3j+2 (tile A lower)
+            if (warp < kEpiWarps) {
+                const bool upper = q >= 2;
+                const int co = 32 * (q & 1) + lane;
+                const int loc = upper ? 1 : (hh == 0 ? 2 : 0);         // tap 3j + loc
+                const uint32_t col0 = (upper ? 0u : (hh == 0 ? 0u : 256u)) + 64 * j;  // accumulator columns
+                const int c_lo = upper ? 32 * hh : 0, c_hi = upper ? c_lo + 32 : 64;
+                for (int c = c_lo; c < c_hi; c += 32) {
+                    float v[32];
+                    __syncwarp();
+                    if (any) {
+                        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + col0 + c, v);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) v[k] = 0.0f;
+                    }
+                    const uint32_t quad0 = (uint32_t)((3 * j + loc) * 64 + c) / 4;
+                    float* xm = xch + co * kPitch + loc * 64 + c;
+                    float* xr = xm + 64 * kPitch;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float4 e = eps4(a.kk.key, a.kk.step, a.kk.s0 + s, a.L.t_w, (uint32_t)co, quad0 + k);
+                        *reinterpret_cast<float4*>(xm + 4 * k) = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                        *reinterpret_cast<float4*>(xr + 4 * k) =
+                            make_float4(v[4 * k] * e.x, v[4 * k + 1] * e.y, v[4 * k + 2] * e.z, v[4 * k + 3] * e.w);
+                    }
+                }
+            }
+            cluster.sync();  // every sample's (D, ε ⊙ D) for kernel row j is in its CTA's shared memory
+            for (int e = threadIdx.x; e < (r1 - r0) * 48; e += blockDim.x) {  // 4 columns per task
+                const int co = r0 + e / 48, cc = 4 * (e - (e / 48) * 48);
+                float4 xm[8], xr[8];  // every sample's values in flight at once (S ≤ 8)
+#pragma unroll
+                for (int rr = 0; rr < 8; ++rr) {
+                    if (rr < S) {
+                        const float* src = cluster.map_shared_rank(xch, rr);
+                        xm[rr] = *reinterpret_cast<const float4*>(src + co * kPitch + cc);
+                        xr[rr] = *reinterpret_cast<const float4*>(src + (64 + co) * kPitch + cc);
+                    }
+                }
+                float4 m = make_float4(0.f, 0.f, 0.f, 0.f), r = m;
+#pragma unroll
+                for (int rr = 0; rr < 8; ++rr) {  // sample order ⇒ deterministic
+                    if (rr < S) {
+                        m.x += xm[rr].x; m.y += xm[rr].y; m.z += xm[rr].z; m.w += xm[rr].w;
+                        r.x += xr[rr].x; r.y += xr[rr].y; r.z += xr[rr].z; r.w += xr[rr].w;
+                    }
+                }
+                const int col = (3 * j + cc / 64) * 64 + (cc & 63);
+                const float k = a.scale;
+                *reinterpret_cast<float4*>(a.part + (int64_t)u * 2 * n + co * 576 + col) =
+                    make_float4(k * m.x, k * m.y, k * m.z, k * m.w);
+                *reinterpret_cast<float4*>(a.part + (int64_t)u * 2 * n + n + co * 576 + col) =
+                    make_float4(k * r.x, k * r.y, k * r.z, k * r.w);
+            }
+            cluster.sync();  // the exchange is read before the next row overwrites it
+        }
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == WMMA) {
@@ -591,8 +692,45 @@ int conv64_wgrad_ok(int H, int W) {  // both halo windows of a 128-pixel k-block
 int conv64_wgrad_nsplit(int S) { return std::max(1, kNumSMs / std::max(S, 1)); }
 
 void launch_conv64_wgrad(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st) {
-    ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel), c64w::kSmem);
-    conv64_wgrad_kernel<<<a.S * a.nsplit, c64w::kThreads, c64w::kSmem, st>>>(ymap, xmap, a);
+    ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel<false>), c64w::kSmem);
+    conv64_wgrad_kernel<false><<<a.S * a.nsplit, c64w::kThreads, c64w::kSmem, st>>>(ymap, xmap, a);
+}
+
+static cudaLaunchConfig_t eps_cfg(int Gc, int nparts, cudaStream_t st, cudaLaunchAttribute* attr) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(Gc * nparts), 1, 1);
+    cfg.blockDim = dim3(c64w::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = c64w::kSmem;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)Gc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+int conv64_wgrad_eps_nsplit(int S, int Gc) {  // partials (splits × sample groups) of one co-resident wave, 0 if none
+    if (S < 1 || Gc < 1 || S % Gc != 0) return 0;
+    ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel<true>), c64w::kSmem);
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = eps_cfg(Gc, 1, nullptr, attr);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, conv64_wgrad_kernel<true>, &cfg) != cudaSuccess || n < 1) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    const int groups = S / Gc;
+    return std::max(1, n / groups) * groups;  // whole pixel splits: every split has all sample groups
+}
+
+int launch_conv64_wgrad_eps(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st) {
+    ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel<true>), c64w::kSmem);
+    cudaLaunchAttribute attr[1];
+    if (a.eps_cluster < 1 || a.S % a.eps_cluster != 0 || a.nsplit % (a.S / a.eps_cluster) != 0) return -1;
+    cudaLaunchConfig_t cfg = eps_cfg(a.eps_cluster, a.nsplit, st, attr);
+    return cudaLaunchKernelEx(&cfg, conv64_wgrad_kernel<true>, ymap, xmap, a) == cudaSuccess ? 0 : -1;
 }
 
 int conv64_ok(int H, int W) {  // the padded window of a 128-row tile fits one window stage

@@ -44,6 +44,13 @@ bool conv64_layer(const bnn_ctx* c, const ROp& op) {
 bool conv64w_layer(const bnn_ctx* c, const ROp& op) {
     return conv64_layer(c, op) && env_on("BNN_CONV64W") && conv64_wgrad_ok(c->rbufs[op.dst].H, c->rbufs[op.dst].W);
 }
+// ε-fused sample accumulation in the weight-gradient kernel (clusters of the chunk's samples):
+// the number of pixel splits (co-resident clusters), or 0 for the per-sample partials + ε combine
+int eps_fused_nsplit(const bnn_ctx* c, const ROp& op, int Sc) {
+    if (!conv64w_layer(c, op) || !env_on("BNN_WGRAD_EPS")) return 0;
+    const int Gc = conv64_wgrad_eps_cluster(Sc);
+    return conv64_wgrad_eps_nsplit(Sc, Gc) / (Sc / Gc);  // pixel splits (partials = splits × sample groups)
+}
 
 int grad_src_buffer(const bnn_ctx* c, int dst) {
     if (is_proj_output(c, dst))
@@ -90,6 +97,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->kpad.assign(L, 0);
     c->wscr_off.assign(L, 0);
     c->nsplit.assign(L, 1);
+    c->wgrad_eps.assign(L, 0);
     c->wkpx.assign(L, 64);
     c->cmap_w.resize(L);
     c->cmap_wT.resize(L);
@@ -134,9 +142,13 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                     c->wkpx[op.layer] = kp;
             }
             const int blocks = (int)((npix + c->wkpx[op.layer] - 1) / c->wkpx[op.layer]);
-            c->nsplit[op.layer] = conv64w_layer(c, op) ? conv64_wgrad_nsplit(Sc) : conv2_wgrad_nsplit(base, blocks);
+            const int epsn = eps_fused_nsplit(c, op, Sc);
+            c->wgrad_eps[op.layer] = epsn > 0 ? 1 : 0;
+            c->nsplit[op.layer] = epsn > 0 ? epsn : conv64w_layer(c, op) ? conv64_wgrad_nsplit(Sc) : conv2_wgrad_nsplit(base, blocks);
             if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
-            pmax = std::max(pmax, (size_t)Sc * c->nsplit[op.layer] * Ld.cout * Kt);
+            // per-sample partials [s][split][co][cols], or (ε-fused) partials [split·group][μ | ρ][co·cols]
+            // (≤ Sc sample groups for any chunk size)
+            pmax = std::max(pmax, (size_t)(epsn > 0 ? 2 * Sc : Sc) * c->nsplit[op.layer] * Ld.cout * Kt);
             continue;
         } else {  // SIMT wgrad (the stem): split pixels so ≥ 2 waves of CTAs exist
             const int tiles = (int)(((int64_t)taps * Ld.cin + 63) / 64) * ((Ld.cout + 63) / 64);
@@ -636,7 +648,14 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             if (w.kpx != c->wkpx[op.layer]) return c->set_err(BNN_ERR_CONFIG, "wgrad k-step / operand path mismatch");
             // the buffer is free once the ε combine that last read it (two layers back) is done
             if (split3) cudaStreamWaitEvent(ss, c->ev_comb[wbuf], 0);
-            if (c->conv64[op.layer] && conv64w_layer(c, op))  // both halo window maps exist for conv64 layers
+            const bool epsf = c->wgrad_eps[op.layer] && c->conv64[op.layer];
+            if (epsf) {  // ε and the sample sum in the GEMM's epilogue (clusters), then the ordered split sum
+                w.eps_cluster = conv64_wgrad_eps_cluster(Sc);
+                w.nsplit = c->nsplit[op.layer] * (Sc / w.eps_cluster);  // partials: pixel splits × sample groups
+                int lrc = 0;
+                c->launch("wgrad", [&] { lrc = launch_conv64_wgrad_eps(c->cmap_hd[op.layer], c->cmap_hf[op.layer], w, ss); });
+                if (lrc) return c->set_err(BNN_ERR_CUDA, "cluster launch of the ε-fused weight gradient refused");
+            } else if (c->conv64[op.layer] && conv64w_layer(c, op))  // both halo window maps exist for conv64 layers
                 c->launch("wgrad", [&] { launch_conv64_wgrad(c->cmap_hd[op.layer], c->cmap_hf[op.layer], w, ss); });
             else
                 c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, ss); });
@@ -646,7 +665,11 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
                 cudaStreamWaitEvent(c->side3, c->ev_wg[wbuf], 0);
                 sc = c->side3;
             }
-            if (w.C_pad < 64) {
+            if (epsf) {
+                c->launch("wgrad", [&] {
+                    launch_wgrad_split_reduce(wp, w.nsplit, (int64_t)Ld.cout * Kt, Ld.off_w, acc_mu, acc_rho, sc);
+                });
+            } else if (w.C_pad < 64) {
                 c->launch("wcomb", [&] {
                     launch_wgrad_eps_combine_stem(sl, kk, Sc, w.nsplit, Ld.cout, taps, Ld.cin, Kt, wp, scale,
                                                   acc_mu, acc_rho, sc);

@@ -1215,3 +1215,31 @@ def test_cnn_bf16_conv64_wgrad_equals_conv2_wgrad(hw, B, S, monkeypatch):
         for name, u, ref in (("acc_mu", m1[sl], m0[sl]), ("acc_rho", r1[sl], r0[sl])):
             assert np.abs(u - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
     assert l1 == l0
+
+
+@pytest.mark.parametrize("hw,B,S,chunk,cl", [(16, 3, 2, 0, None), (32, 2, 3, 0, None), (16, 2, 8, 0, None),
+                                             (16, 2, 8, 0, "8"), (16, 2, 8, 0, "4"), (16, 2, 5, 2, None)])
+def test_cnn_bf16_eps_fused_wgrad_equals_combine(hw, B, S, chunk, cl, monkeypatch):
+    """ε-fused, sample-accumulating stage-1 weight gradient (ε regenerated in the GEMM epilogue,
+    samples summed over DSMEM in sample order within a cluster, north_star (3)) against the
+    per-sample partials + separate ε combine (BNN_WGRAD_EPS=0): acc_μ, acc_ρ of every tensor within
+    fp32 summation error (1e-4 of each tensor's max; a wrong ε, sample or column is O(1)); default
+    pairs, clusters of 8 and 4, and a ragged sample chunk (5 samples in chunks of 2)."""
+    native = _native()
+    model = dict(BF16_CNN, in_h=hw, in_w=hw)
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    accs = []
+    if cl is not None:  # clusters of all 8 samples / of 4 (no per-pair partials)
+        monkeypatch.setenv("BNN_WGRAD_EPS_CLUSTER", cl)
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BNN_WGRAD_EPS", flag)
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, sample_chunk=chunk, dataset_size=1e4,
+                             aug="per_sample")
+        accs.append(_acc_parts(ctx, ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0xBEEF, 5)))
+        torch.cuda.synchronize()
+    (m0, r0, l0), (m1, r1, l1) = accs
+    for t in ctx.tensors:
+        sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
+        for name, u, ref in (("acc_mu", m1[sl], m0[sl]), ("acc_rho", r1[sl], r0[sl])):
+            assert np.abs(u - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
+    assert l1 == l0
