@@ -236,6 +236,8 @@ struct bnn_ctx {
     std::vector<float*> vvec;  // sampled 1-D tensors [chunk][n] (LayerNorm g/b, cls, pos), else null
     std::vector<CUtensorMap> cmap_hf, cmap_hd;  // conv3 HALO: 1-row (W + 2)-pixel boxes of the input / dY
     std::vector<char> halo_fwd, halo_dgrad;
+    float* bias_rows_scr = nullptr;  // chunk sums of many bias partials (launch_bias_grad_rows)
+    int64_t bias_rows_cap = 0;
     std::vector<char> wgrad_eps;  // ε-fused, sample-accumulating weight gradient (no per-sample partials)
     std::vector<char> conv64;  // stage-1 64 → 64 layers on the W-stationary tap-paired kernel (both passes)
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]

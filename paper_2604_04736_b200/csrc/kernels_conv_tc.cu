@@ -103,8 +103,59 @@ __global__ void wgrad_split_reduce_kernel(const float* __restrict__ part, int ns
     }
 }
 
+// float4 form (n, off multiples of 4): block = 32 column quads × 8 split groups; group g sums the
+// splits g, g + 8, … in order (loads of 4 splits in flight), the 8 groups are added in group order
+// through shared memory ⇒ deterministic, and 288 blocks for a stage-1 layer instead of 36
+__global__ void __launch_bounds__(256) wgrad_split_reduce4_kernel(const float* __restrict__ part, int nsplit, int64_t n,
+                                                                  int64_t off, float* __restrict__ acc_mu,
+                                                                  float* __restrict__ acc_rho) {
+    __shared__ float4 red[2][8][33];
+    const int64_t n4 = n / 4;
+    const int tx = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + tx;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f), r = m;
+    if (i < n4) {
+        const float4* pm = reinterpret_cast<const float4*>(part) + i;
+        for (int sp0 = g; sp0 < nsplit; sp0 += 32) {
+            float4 xm[4], xr[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (sp0 + 8 * j < nsplit) {
+                    xm[j] = __ldcs(pm + (int64_t)(sp0 + 8 * j) * 2 * n4);
+                    xr[j] = __ldcs(pm + (int64_t)(sp0 + 8 * j) * 2 * n4 + n4);
+                }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (sp0 + 8 * j < nsplit) {
+                    m.x += xm[j].x; m.y += xm[j].y; m.z += xm[j].z; m.w += xm[j].w;
+                    r.x += xr[j].x; r.y += xr[j].y; r.z += xr[j].z; r.w += xr[j].w;
+                }
+        }
+    }
+    red[0][g][tx] = m;
+    red[1][g][tx] = r;
+    __syncthreads();
+    if (g == 0 && i < n4) {
+        for (int k = 1; k < 8; ++k) {
+            const float4 a = red[0][k][tx], b = red[1][k][tx];
+            m.x += a.x; m.y += a.y; m.z += a.z; m.w += a.w;
+            r.x += b.x; r.y += b.y; r.z += b.z; r.w += b.w;
+        }
+        float4* am = reinterpret_cast<float4*>(acc_mu + off) + i;
+        float4* ar = reinterpret_cast<float4*>(acc_rho + off) + i;
+        const float4 a0 = *am, b0 = *ar;
+        *am = make_float4(a0.x + m.x, a0.y + m.y, a0.z + m.z, a0.w + m.w);
+        *ar = make_float4(b0.x + r.x, b0.y + r.y, b0.z + r.z, b0.w + r.w);
+    }
+}
+
 void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off, float* acc_mu,
                                float* acc_rho, cudaStream_t st) {
+    if (n % 4 == 0 && off % 4 == 0) {
+        wgrad_split_reduce4_kernel<<<(int)std::max<int64_t>(1, (n / 4 + 31) / 32), 256, 0, st>>>(part, nsplit, n, off,
+                                                                                              acc_mu, acc_rho);
+        return;
+    }
     const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8);
     wgrad_split_reduce_kernel<<<std::max(grid, 1), 256, 0, st>>>(part, nsplit, n, off, acc_mu, acc_rho);
 }

@@ -157,10 +157,12 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         }
         pmax = std::max(pmax, (size_t)c->nsplit[op.layer] * 2 * Ld.cout * taps * Ld.cin);
     }
+    c->bias_rows_cap = (int64_t)Sc * 64 * std::max(maxN, O);
     if (!c->alloc(&c->wscr, wmax) || !c->alloc(&c->wpart, std::max<size_t>(pmax, 1)) ||
         !c->alloc(&c->wpart2, std::max<size_t>(pmax, 1)) ||
         !c->alloc(&c->bias_scr, (size_t)Sc * 512 * c->layers.size()) ||  // one slot per layer
-        !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)))
+        !c->alloc(&c->db_scratch, (size_t)2 * Sc * std::max(maxN, O)) ||
+        !c->alloc(&c->bias_rows_scr, (size_t)Sc * 64 * std::max(maxN, O)))
         return c->set_err(BNN_ERR_CUDA, "out of memory (scratch)");
     for (const ROp& op : c->rops) {
         if (op.type != 0 || is_fc(c, op)) continue;
@@ -614,7 +616,9 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         // and the wgrad / ε-combine chain each overlap the data-gradient chain on st)
         cudaStream_t sb = fork_side2(c);
         c->launch("bias", [&] {
-            return launch_bias_grad(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale, c->db_scratch,
+            // many partials (the stage-1 dgrad tiles): 64-part chunks summed in parallel first
+            return launch_bias_grad_rows(sl, kk, Sc, G.bpart, G.nparts, Db.C, (int64_t)G.nparts * Db.C, scale,
+                                         c->bias_rows_scr, c->bias_rows_cap, c->db_scratch,
                              acc_mu, acc_rho, sb);
         });
         cudaStream_t ss = fork_side(c);
