@@ -40,10 +40,10 @@ namespace bnn {
 using namespace ptx;
 
 namespace c64 {
-// epilogue warps: groups of 8 (4 lane quarters × 2 channel halves); the forward runs two groups
-// (even / odd tiles: two MMA tile-times per epilogue), the dgrad one (its bias-gradient butterfly
-// does not fit the 96-register budget of 18 warps)
-template <int MODE> constexpr int groups() { return MODE == 0 ? 2 : 1; }
+// epilogue warps: two groups of 8 (4 lane quarters × 2 channel halves) taking even / odd tiles, so
+// each group has two MMA tile-times per epilogue (C64_PROF: a group's epilogue of a tile takes
+// ≈ 4.7 K cycles, the MMAs ≈ 2.2 K)
+template <int MODE> constexpr int groups() { return 2; }
 template <int MODE> constexpr int threads() { return (8 * groups<MODE>() + 2) * 32; }  // + TMA, MMA warps
 constexpr int kBlk = 64 * 128;                  // one tap block: 64 rows × 64 bf16 (SWIZZLE_128B)
 constexpr int kWres = 9 * kBlk;                 // 3 kernel rows × 3 taps (72 KB)
@@ -133,6 +133,22 @@ __device__ __forceinline__ void st256(void* p, const uint32_t* r) {
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// 16 values whose lanes l and l ^ 16 are equal: lane j (j < 16) ends with Σ over a 16-lane half
+// of v[j] (fixed butterfly order)
+__device__ __forceinline__ float c64_transpose_sum16(float* v, int lane) {
+#pragma unroll
+    for (int off = 8; off >= 1; off >>= 1) {
+        const bool hi = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < off; ++i) {
+            const float send = hi ? v[i] : v[i + off];
+            const float keep = hi ? v[i + off] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
 // lane j ends with Σ over the warp's 32 lanes of v[j] (fixed butterfly order)
 __device__ __forceinline__ float c64_transpose_sum(float* v, int lane) {
 #pragma unroll
@@ -148,6 +164,13 @@ __device__ __forceinline__ float c64_transpose_sum(float* v, int lane) {
     return v[0];
 }
 
+// C64_PROF (experiment builds, BNN_NVCC_FLAGS=-DC64_PROF): per-role phase cycle sums printed by
+// CTA 0 at exit — where a tile's time goes
+#ifdef C64_PROF
+#define C64_T(x) const long long x = clock64()
+#else
+#define C64_T(x)
+#endif
 template <int MODE>
 __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
     conv64_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
@@ -195,6 +218,11 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+#ifdef C64_PROF
+    long long p_tma_wait = 0, p_mma_tempty = 0, p_mma_wfull = 0, p_e_wait = 0, p_e_tmem = 0, p_e_bar = 0, p_e_post = 0;
+    int p_tiles = 0;
+    const long long p_start = clock64();
+#endif
 
     if (warp == WTMA) {
         // ------------------------------------------------ TMA producer: resident W, windows
@@ -220,7 +248,12 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
                     ++seg;
                 }
                 const int ws = tl % kNWin;
+                C64_T(pa0);
                 mbar_wait_role(&wempty[ws], ((tl / kNWin) & 1) ^ 1);
+                C64_T(pa1);
+#ifdef C64_PROF
+                p_tma_wait += pa1 - pa0;
+#endif
                 const int p0 = pt * kTileP;
                 const int rs = c64_floor_div(p0 - PWp - 1, PWp), re = c64_floor_div(p0 + kTileM + PWp, PWp);
                 uint8_t* win = sWin + ws * kWin;
@@ -245,8 +278,15 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
                     ++seg;
                 }
                 const int buf = tl & 1, ws = tl % kNWin;
+                C64_T(pm0);
                 mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                C64_T(pm1);
                 mbar_wait_role(&wfull[ws], (tl / kNWin) & 1);
+                C64_T(pm2);
+#ifdef C64_PROF
+                p_mma_tempty += pm1 - pm0;
+                p_mma_wfull += pm2 - pm1;
+#endif
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 const int p0 = pt * kTileP;
@@ -301,123 +341,152 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
                 ld256<MODE == 0>(opnd + so + ro + 16, xw + 8);
             }
             if (MODE == 1 && pv && a.mbits) mw = __ldg(a.mbits + ((so + ro) >> 5));
+            C64_T(pe0);
             mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            C64_T(pe1);
             tc_fence_after();
             const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + ch0;
-            float z[kCh], v[16];
+            // Passes of CH channels (dgrad: 16, the register budget of 18 warps with the bias-gradient
+            // butterfly; fwd: 32). xq: [0] row 0's dw = +1 block, [1] row 0's dw = 0 block, [2] row 1's
+            // dw = +1 block — what the previous quarter's rows 30, 31 need from this one.
+            constexpr int CH = MODE == 1 ? 16 : 32;
             float* xq = xb + (((g * 2 + par) * 2 + h) * 4 + q) * 3 * kCh;
-            // xq: [0] row 0's dw = +1 block, [1] row 0's dw = 0 block, [2] row 1's dw = +1 block —
-            // what the previous quarter's rows 30, 31 need from this one. 16 channels at a time
-            // (register budget of 18 warps).
 #pragma unroll
-            for (int c = 0; c < kCh; c += 16) {
-                tmem_ld16(ta + c, z + c);       // block dw = −1 (this pixel)
-                tmem_ld16(ta + 64 + c, v);      // dw = 0 (pixel − 1)
-                if (q > 0 && lane == 0) {
+            for (int c0 = 0; c0 < kCh; c0 += CH) {
+                float z[CH], v[16];
 #pragma unroll
-                    for (int j = 0; j < 16; j += 4)
-                        *reinterpret_cast<float4*>(xq + kCh + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                for (int c = c0; c < c0 + CH; c += 16) {
+                    tmem_ld16(ta + c, z + (c - c0));  // block dw = −1 (this pixel)
+                    tmem_ld16(ta + 64 + c, v);         // dw = 0 (pixel − 1)
+                    if (q > 0 && lane == 0) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4*>(xq + kCh + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) z[c - c0 + j] += shfl_down_or(v[j], 1, 0.0f);
+                    tmem_ld16(ta + 128 + c, v);        // dw = +1 (pixel − 2)
+                    if (c + 16 == kCh) {  // the tile's last accumulator read
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);
+                    }
+                    if (q > 0 && lane < 2) {
+                        float* d = xq + (lane == 0 ? 0 : 2 * kCh) + c;
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) z[c - c0 + j] += shfl_down_or(v[j], 2, 0.0f);
                 }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) z[c + j] += shfl_down_or(v[j], 1, 0.0f);
-                tmem_ld16(ta + 128 + c, v);     // dw = +1 (pixel − 2)
-                if (c + 16 == kCh) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[buf]);
+                C64_T(pe2);
+                named_bar(bar_id, 4 * 32);  // the exchange of this pass is written
+                C64_T(pe3);
+#ifdef C64_PROF
+                if (c0 == 0) {
+                    p_e_tmem += pe2 - pe1;
+                    p_e_bar += pe3 - pe2;
                 }
-                if (q > 0 && lane < 2) {
-                    float* d = xq + (lane == 0 ? 0 : 2 * kCh) + c;
+#endif
+                if (q < 3 && lane >= 30) {  // rows 30, 31: the next quarter's rows 0, 1 (same summation order)
+                    const float* xn = xb + (((g * 2 + par) * 2 + h) * 4 + q + 1) * 3 * kCh + c0;
+                    if (lane == 31) {
 #pragma unroll
-                    for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(d + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        for (int j = 0; j < CH; j += 4) {
+                            const float4 fb = *reinterpret_cast<const float4*>(xn + kCh + j);
+                            const float4 fc = *reinterpret_cast<const float4*>(xn + 2 * kCh + j);
+                            z[j] = (z[j] + fb.x) + fc.x;
+                            z[j + 1] = (z[j + 1] + fb.y) + fc.y;
+                            z[j + 2] = (z[j + 2] + fb.z) + fc.z;
+                            z[j + 3] = (z[j + 3] + fb.w) + fc.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < CH; j += 4) {
+                            const float4 fc = *reinterpret_cast<const float4*>(xn + j);
+                            z[j] += fc.x;
+                            z[j + 1] += fc.y;
+                            z[j + 2] += fc.z;
+                            z[j + 3] += fc.w;
+                        }
+                    }
                 }
+                if (MODE == 1 && a.bpart && c0 == 0 && t > t0 + g && q == 0) {  // this group's previous tile
+                    const float* rb = bred + ((g * 2 + (par ^ 1)) * 2 + h) * 4 * kCh;
+                    a.bpart[(int64_t)prev_s * a.bpart_stride_s + (int64_t)prev_pt * a.C + ch0 + lane] =
+                        ((rb[lane] + rb[kCh + lane]) + rb[2 * kCh + lane]) + rb[3 * kCh + lane];
+                }
+                if (pv) {
+                    if (MODE == 0) {
+                        const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO + ch0 + c0);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) z[c + j] += shfl_down_or(v[j], 2, 0.0f);
-            }
-            named_bar(bar_id, 4 * 32);  // the exchange of this tile is written
-            if (q < 3 && lane >= 30) {  // rows 30, 31: the next quarter's rows 0, 1 (same summation order)
-                const float* xn = xb + (((g * 2 + par) * 2 + h) * 4 + q + 1) * 3 * kCh;
-                if (lane == 31) {
+                        for (int k = 0; k < CH / 4; ++k) {
+                            const float4 b4 = __ldg(bs + k);
+                            z[4 * k] += b4.x;
+                            z[4 * k + 1] += b4.y;
+                            z[4 * k + 2] += b4.z;
+                            z[4 * k + 3] += b4.w;
+                        }
+                    }
+                    if (opnd) {
 #pragma unroll
-                    for (int j = 0; j < kCh; j += 4) {
-                        const float4 fb = *reinterpret_cast<const float4*>(xn + kCh + j);
-                        const float4 fc = *reinterpret_cast<const float4*>(xn + 2 * kCh + j);
-                        z[j] = (z[j] + fb.x) + fc.x;
-                        z[j + 1] = (z[j + 1] + fb.y) + fc.y;
-                        z[j + 2] = (z[j + 2] + fb.z) + fc.z;
-                        z[j + 3] = (z[j + 3] + fb.w) + fc.w;
+                        for (int e = 0; e < CH / 2; ++e) {
+                            const uint32_t wv = xw[c0 / 2 + e];
+                            z[2 * e] += __uint_as_float(wv << 16);
+                            z[2 * e + 1] += __uint_as_float(wv & 0xFFFF0000u);
+                        }
+                    }
+                    if (MODE == 0) {
+                        if (a.relu) {
+#pragma unroll
+                            for (int j = 0; j < CH; ++j) z[j] = fmaxf(z[j], 0.0f);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < CH; ++j)
+                            if (!((mw >> (c0 + j)) & 1u)) z[j] = 0.0f;
+                    }
+                    uint32_t pk[CH / 2];
+#pragma unroll
+                    for (int k = 0; k < CH / 2; ++k) pk[k] = pack_bf16x2(z[2 * k], z[2 * k + 1]);
+#pragma unroll
+                    for (int k = 0; k < CH / 16; ++k) st256(a.out + so + ro + c0 + 16 * k, pk + 8 * k);  // full sectors
+                    if (MODE == 0 && a.mbits_out) {
+                        // bit j = (stored bf16 of channel ch0 + j > 0); after the ReLU no stored value is
+                        // negative, so > 0 ⟺ magnitude bits ≠ 0: (x & 0x7FFF) + 0x7FFF carries into bit 15
+                        uint32_t bits = 0;
+#pragma unroll
+                        for (int k = 0; k < CH / 2; ++k) {
+                            const uint32_t cb = ((pk[k] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x80008000u;
+                            bits |= (((cb >> 15) & 1u) | (cb >> 30)) << (2 * k);  // bit 0: low half, bit 1: high half
+                        }
+                        a.mbits_out[(so + ro) >> 5] = bits;  // CH = 32: the whole word
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < kCh; j += 4) {
-                        const float4 fc = *reinterpret_cast<const float4*>(xn + j);
-                        z[j] += fc.x;
-                        z[j + 1] += fc.y;
-                        z[j + 2] += fc.z;
-                        z[j + 3] += fc.w;
+                    for (int j = 0; j < CH; ++j) z[j] = 0.0f;
+                }
+                if (MODE == 1 && a.bpart) {  // Σ over the quarter's 32 pixels per channel (fixed order)
+                    float* rb = bred + (((g * 2 + par) * 2 + h) * 4 + q) * kCh + c0;
+                    if (CH == 32) {
+                        const float bsum = c64_transpose_sum(z, lane);  // lane j: channel j of the pass
+                        rb[lane] = bsum;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < CH; ++j) z[j] += __shfl_xor_sync(0xffffffffu, z[j], 16);
+                        const float bsum = c64_transpose_sum16(z, lane);  // lanes l, l + 16: channel l & 15
+                        if (lane < 16) rb[lane] = bsum;
                     }
                 }
-            }
-            if (MODE == 1 && a.bpart && t > t0 + g && q == 0) {  // this group's previous tile's bias partials
-                const float* rb = bred + ((g * 2 + (par ^ 1)) * 2 + h) * 4 * kCh;
-                a.bpart[(int64_t)prev_s * a.bpart_stride_s + (int64_t)prev_pt * a.C + ch0 + lane] =
-                    ((rb[lane] + rb[kCh + lane]) + rb[2 * kCh + lane]) + rb[3 * kCh + lane];
-            }
-            if (pv) {
-                if (MODE == 0) {
-                    const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO + ch0);
-#pragma unroll
-                    for (int k = 0; k < kCh / 4; ++k) {
-                        const float4 b4 = __ldg(bs + k);
-                        z[4 * k] += b4.x;
-                        z[4 * k + 1] += b4.y;
-                        z[4 * k + 2] += b4.z;
-                        z[4 * k + 3] += b4.w;
-                    }
-                }
-                if (opnd) {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        z[2 * e] += __uint_as_float(xw[e] << 16);
-                        z[2 * e + 1] += __uint_as_float(xw[e] & 0xFFFF0000u);
-                    }
-                }
-                if (MODE == 0) {
-                    if (a.relu) {
-#pragma unroll
-                        for (int j = 0; j < kCh; ++j) z[j] = fmaxf(z[j], 0.0f);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < kCh; ++j)
-                        if (!((mw >> j) & 1u)) z[j] = 0.0f;
-                }
-                uint32_t pk[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) pk[k] = pack_bf16x2(z[2 * k], z[2 * k + 1]);
-                st256(a.out + so + ro, pk);  // one full 32-byte sector per store
-                st256(a.out + so + ro + 16, pk + 8);
-                if (MODE == 0 && a.mbits_out) {
-                    // bit j = (stored bf16 of channel ch0 + j > 0); after the ReLU no stored value is
-                    // negative, so > 0 ⟺ magnitude bits ≠ 0: (x & 0x7FFF) + 0x7FFF carries into bit 15
-                    uint32_t bits = 0;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t c = ((pk[k] & 0x7FFF7FFFu) + 0x7FFF7FFFu) & 0x80008000u;
-                        bits |= (((c >> 15) & 1u) | (c >> 30)) << (2 * k);  // bit 0: low half, bit 1: high half
-                    }
-                    a.mbits_out[(so + ro) >> 5] = bits;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < kCh; ++j) z[j] = 0.0f;
-            }
-            if (MODE == 1 && a.bpart) {  // Σ over the quarter's 32 pixels per channel (fixed order)
-                const float bsum = c64_transpose_sum(z, lane);  // lane j: channel ch0 + j
-                bred[(((g * 2 + par) * 2 + h) * 4 + q) * kCh + lane] = bsum;
             }
             prev_s = s;
             prev_pt = pt;
+#ifdef C64_PROF
+            C64_T(pe4);
+            p_e_wait += pe1 - pe0;
+            p_e_post += pe4 - pe1;
+            ++p_tiles;
+#endif
         }
         if (MODE == 1 && a.bpart && t1 > t0 + g) {  // flush the group's last tile's partials
             named_bar(bar_id, 4 * 32);
@@ -428,6 +497,15 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
             }
         }
     }
+#ifdef C64_PROF
+    if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0) {
+        const long long tot = clock64() - p_start;
+        if (warp == WTMA) printf("c64<%d> cta %d TMA: total %lld wait_wempty %lld\n", MODE, blockIdx.x, tot, p_tma_wait);
+        else if (warp == WMMA) printf("c64<%d> cta %d MMA: total %lld wait_tempty %lld wait_wfull %lld\n", MODE, blockIdx.x, tot, p_mma_tempty, p_mma_wfull);
+        else if ((warp & 3) == 0) printf("c64<%d> cta %d epi warp %d: tiles %d total %lld wait_tfull %lld tmem+shfl %lld bar %lld post %lld\n",
+                                      MODE, blockIdx.x, warp, p_tiles, tot, p_e_wait, p_e_tmem, p_e_bar, p_e_post);
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == WMMA) {
