@@ -238,6 +238,7 @@ struct bnn_ctx {
     std::vector<char> halo_fwd, halo_dgrad;
     float* bias_rows_scr = nullptr;  // chunk sums of many bias partials (launch_bias_grad_rows)
     int64_t bias_rows_cap = 0;
+    std::vector<char> wcps;  // conv2 weight gradient: CTAs per SM (1 or 2)
     std::vector<char> wgrad_eps;  // ε-fused, sample-accumulating weight gradient (no per-sample partials)
     std::vector<char> conv64;  // stage-1 64 → 64 layers on the W-stationary tap-paired kernel (both passes)
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]

@@ -122,6 +122,7 @@ struct ConvWgradArgs {
     int kpx;                 // pixels per k-step: 128 on the TMA path where the window fits, else 64
     int dbg;                 // timing experiments only (BNN_CONV_DEBUG); 0 in production
     int eps_cluster;         // ε-fused conv64 wgrad: samples per thread-block cluster (divides S, ≤ 8)
+    int cps;                 // conv2 wgrad: CTAs per SM (2 needs kpx = 64)
 };
 void launch_wgrad_split_reduce(const float* part, int nsplit, int64_t n, int64_t off,
                                float* acc_mu, float* acc_rho, cudaStream_t st);
@@ -137,6 +138,7 @@ void launch_wgrad_eps_combine_stem(const SampledLayer& L, const SampleKeys& kk, 
                                    int C, int Ktp, const float* part, float scale, float* acc_mu, float* acc_rho,
                                    cudaStream_t st);
 int conv2_wgrad_ntile(int Kt);
+int conv2_wgrad_cps();
 int conv2_wgrad_nsplit(int base, int blocks);
 // partial columns: taps·C, or (stem, C_pad < 64) ⌈taps/8⌉·64
 inline int conv2_wgrad_cols(int taps, int C, int C_pad) { return C_pad < 64 ? ((taps + 7) / 8) * 64 : taps * C; }

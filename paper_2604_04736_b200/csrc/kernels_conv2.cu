@@ -998,10 +998,16 @@ constexpr int kSmem = 1024 + kData + 512;
 // Persistent: unit u = (((s·nsplit + split)·co_tiles + ct)·ntiles + nt); neighbouring CTAs share
 // (s, split) so the dY and X blocks they read are L2 hits. D[co][col] accumulates in TMEM
 // (two 256-column buffers: unit i's store overlaps unit i+1's main loop).
-__global__ void __launch_bounds__(w2::kThreads, 1)
+// CPS CTAs per SM: 1 (216 KB of stages, two TMEM accumulators) or 2 (100 KB, one accumulator each:
+// two MMA issue streams per SM — one issuing thread sustains ≈ 185 cycles per MMA whatever N,
+// profiles/r02/mma_bench*.txt)
+template <int CPS>
+__global__ void __launch_bounds__(w2::kThreads, CPS)
     conv2_wgrad_kernel(const __grid_constant__ CUtensorMap gmap, const __grid_constant__ CUtensorMap xmap,
                        const ConvWgradArgs a, const int g_max_stages_arg) {
     using namespace w2;
+    constexpr int NB = CPS == 1 ? 2 : 1;                      // TMEM accumulators of 256 columns
+    constexpr int DATA = CPS == 1 ? kData : 100 * 1024;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
     // address space, so plain loads/stores through it compile to LDS/STS
@@ -1013,7 +1019,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     const int blkB = kpx * 128;
     const int kAStage = 2 * blkB;  // dYᵀ: up to 2 co blocks
     const int kBStage = 4 * blkB;  // X windows: up to 256 parameter columns
-    const int kStages = min(g_max_stages_arg, kData / (kAStage + kBStage));
+    const int kStages = min(g_max_stages_arg, DATA / (kAStage + kBStage));
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
     uint64_t* full = bars;
@@ -1058,7 +1064,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         }
         mbar_fence_init();
     }
-    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, 512);
+    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, NB * 256);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1108,8 +1114,8 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const U u = unit(t);
                 const uint32_t idesc = idesc_bf16(128, u.w, 1, 1);
-                const int buf = tl & 1;
-                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                const int buf = tl % NB;
+                mbar_wait_role(&tempty[buf], ((tl / NB) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 for (int b = 0; b < u.nblk; ++b, ++it) {
@@ -1198,8 +1204,8 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         int tl = 0;
         for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
             const U u = unit(t);
-            const int buf = tl & 1;
-            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            const int buf = tl % NB;
+            mbar_wait(&tfull[buf], (tl / NB) & 1);
             tc_fence_after();
             const int co = u.ct * 128 + 32 * q + lane;
             const int half = u.w / 2;
@@ -1228,20 +1234,35 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     __syncthreads();
     if (warp == kEpiWarps + kGatherWarps + 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, NB * 256);
     }
+}
+
+int conv2_wgrad_cps() {  // BNN_WGRAD_CPS=1|2 forces the CTAs per SM of the conv2 weight gradient, 0 = per layer
+    static int v = [] {
+        const char* e = getenv("BNN_WGRAD_CPS");
+        const int x = e ? atoi(e) : 0;
+        return x == 1 || x == 2 ? x : 0;
+    }();
+    return v;
 }
 
 int conv2_wgrad_ntile(int Kt) { return Kt >= 64 ? 256 : 0; }  // column-tile width (the last may be narrower)
 
 void launch_conv2_wgrad(const CUtensorMap& gmap, const CUtensorMap& xmap, const ConvWgradArgs& a,
                         cudaStream_t st) {
-    ensure_smem_attr(reinterpret_cast<const void*>(conv2_wgrad_kernel), w2::kSmem);
     const int Kt = conv2_wgrad_cols(a);
     const int T = a.S * a.nsplit * ((a.CO + 127) / 128) * ((Kt + 255) / 256);
     ConvWgradArgs b = a;
     b.dbg = conv_debug();
-    conv2_wgrad_kernel<<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, b, conv_stage_cap());
+    if (a.kpx == 64 && a.cps == 2) {  // two CTAs per SM (64-pixel k-steps: two 48 KB stages each)
+        constexpr int smem = 1024 + 100 * 1024 + 512;
+        ensure_smem_attr(reinterpret_cast<const void*>(conv2_wgrad_kernel<2>), smem);
+        conv2_wgrad_kernel<2><<<std::min(T, 2 * kNumSMs), w2::kThreads, smem, st>>>(gmap, xmap, b, conv_stage_cap());
+        return;
+    }
+    ensure_smem_attr(reinterpret_cast<const void*>(conv2_wgrad_kernel<1>), w2::kSmem);
+    conv2_wgrad_kernel<1><<<std::min(T, kNumSMs), w2::kThreads, w2::kSmem, st>>>(gmap, xmap, b, conv_stage_cap());
 }
 
 // Phase 2: thread = four consecutive parameter columns of one row. The partials of up to 8

@@ -98,6 +98,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->wscr_off.assign(L, 0);
     c->nsplit.assign(L, 1);
     c->wgrad_eps.assign(L, 0);
+    c->wcps.assign(L, 1);
     c->wkpx.assign(L, 64);
     c->cmap_w.resize(L);
     c->cmap_wT.resize(L);
@@ -140,6 +141,16 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                 if (Ld.stride == 1 && Ld.cout <= 512 && Ld.cin % 64 == 0 && !shared && Sb0.W == PW &&
                     kp % PW == 0 && PH % wh == 0 && (kp / (PW * wh)) * PW * wh == kp)
                     c->wkpx[op.layer] = kp;
+            }
+            // CTAs per SM of the conv2 weight gradient (measured per stage, C3): two (64-pixel k-steps)
+            // for the gather-path layers (stride 2, the stem) and the ≤ 2048-pixel-per-sample layers
+            // (stage 4: 91 → 85 µs, the stride-2 ones 102 → 82, 135 → 124); one with 128-pixel k-steps
+            // for stages 2 and 3 (two CTAs there: 77 → 108, 92 → 100)
+            {
+                const int forced = conv2_wgrad_cps();
+                const bool two = forced ? forced == 2 : (c->wkpx[op.layer] == 64 || npix <= 2048);
+                c->wcps[op.layer] = two ? 2 : 1;
+                if (two) c->wkpx[op.layer] = 64;
             }
             const int blocks = (int)((npix + c->wkpx[op.layer] - 1) / c->wkpx[op.layer]);
             const int epsn = eps_fused_nsplit(c, op, Sc);
@@ -649,6 +660,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
             const int taps = Ld.k * Ld.k, Kt = conv2_wgrad_cols(taps, Ld.cin, w.C_pad);
             w.n_tile = conv2_wgrad_ntile(Kt);
             w.kpx = w.tma_b ? c->wkpx[op.layer] : 64;
+            w.cps = c->wcps[op.layer];
             if (w.kpx != c->wkpx[op.layer]) return c->set_err(BNN_ERR_CONFIG, "wgrad k-step / operand path mismatch");
             // the buffer is free once the ε combine that last read it (two layers back) is done
             if (split3) cudaStreamWaitEvent(ss, c->ev_comb[wbuf], 0);
