@@ -67,7 +67,8 @@ inline bool make_map(CUtensorMap* m, const void* base, int inner, int rows, int 
 
 // generic bf16 tensor map: rank ≤ 5, dims[0] contiguous, strides in bytes for dims 1..rank-1
 inline bool make_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                        const uint64_t* strides, const uint32_t* box, const uint32_t* estr = nullptr) {
+                        const uint64_t* strides, const uint32_t* box, const uint32_t* estr = nullptr,
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t d[5], st[4];
@@ -79,7 +80,7 @@ inline bool make_map_nd(CUtensorMap* m, const void* base, int rank, const uint64
         if (i > 0) st[i - 1] = strides[i - 1];
     }
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, bx, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -240,6 +241,8 @@ struct bnn_ctx {
     int64_t bias_rows_cap = 0;
     std::vector<char> wcps;  // conv2 weight gradient: CTAs per SM (1 or 2)
     std::vector<char> wgrad_eps;  // ε-fused, sample-accumulating weight gradient (no per-sample partials)
+    CUtensorMap cmap_stem;      // the stem input: 1-row (W + 2)-pixel boxes, 8 channels, no swizzle
+    int stem_layer = -1;       // the layer on stem_fwd_kernel (-1: none)
     std::vector<char> conv64;  // stage-1 64 → 64 layers on the W-stationary tap-paired kernel (both passes)
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
     // TMA descriptors (BF16)

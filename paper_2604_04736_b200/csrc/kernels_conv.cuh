@@ -70,6 +70,7 @@ struct Conv2Args {
     uint32_t* mbits_out;       // fwd (relu): ReLU bitmask of the stored output, bit j of word
                                //   [pixel][c/32] = (stored bf16 of channel c > 0); or null
     const uint32_t* mbits;     // dgrad: bitmask of the layer input (replaces `mask` when set)
+    const __nv_bfloat16* wsrc; // stem kernel: the layer's W scratch slot [s][CO][K_pad]
     int halo;                  // conv3, stride-1 3×3, 64-channel B operand: padded-stream tiles with
                                //   one halo window per tile (bmap = 1-row box of W + 2 pixels)
 };
@@ -91,6 +92,12 @@ void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const C
 void launch_conv64_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
 int conv64_parts(const Conv2Args& a);
 int conv64_ok(int H, int W);
+// stem (kernels_stem.cu): 3×3 stride-1 conv of the 8-channel input to 64 channels, pixels on M and two
+// taps per MMA (SWIZZLE_NONE K-major operands, the taps' distance as the leading byte offset);
+// xmap = 1-row (W + 2)-pixel boxes of the input, no swizzle; a.wsrc = the W scratch slot
+void launch_stem_fwd(const CUtensorMap& xmap, const Conv2Args& a, cudaStream_t st);
+int stem_fwd_ok(const Conv2Args& a);
+int stem_row_pitch(int W);  // padded-row length of the stem window (the map box width)
 // conv64 weight gradient: the fp32 per-sample partials part[s][split][64][576] of the ε combine,
 // one CTA per (sample, split) (nsplit = conv64_wgrad_nsplit(S)); ymap / xmap = the HALO window
 // maps of dY and of the layer input.

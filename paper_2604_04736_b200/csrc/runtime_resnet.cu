@@ -301,6 +301,24 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         // both directions 64 → 64 (stage 1): the W-stationary row-packed kernel (kernels_conv64.cu)
         if (conv64_layer(c, op) && c->halo_fwd[op.layer] && c->halo_dgrad[op.layer]) c->conv64[op.layer] = 1;
     }
+    // the stem (kernels_stem.cu): the 8-channel input as 1-row boxes of W + 2 pixels (OOB zero
+    // columns), no swizzle (16-byte rows: the MMA's two K core matrices are two taps)
+    c->stem_layer = -1;
+    for (const ROp& op : c->rops) {
+        if (op.type != 0 || is_fc(c, op) || op.src != 0 || !env_on("BNN_STEM")) continue;
+        const LayerDesc& Ld = c->layers[op.layer];
+        const RBuf& Sb = c->rbufs[op.src];
+        const RBuf& Db = c->rbufs[op.dst];
+        if (Ld.k != 3 || Ld.stride != 1 || Ld.pad != 1 || c->rbf[0].C_pad != 8 || Ld.cout != 64 || op.res >= 0 ||
+            !op.relu || Db.H != Sb.H || Db.W != Sb.W)
+            continue;
+        const bool shared = c->cfg.aug != BNN_AUG_PER_SAMPLE;
+        const uint64_t dims[5] = {8, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B, (uint64_t)(shared ? 1 : Sc)};
+        const uint64_t str[4] = {16, (uint64_t)Sb.W * 16, (uint64_t)Sb.H * Sb.W * 16, (uint64_t)B * Sb.H * Sb.W * 16};
+        const uint32_t box[5] = {8, (uint32_t)stem_row_pitch(Sb.W), 1, 1, 1};
+        if (make_map_nd(&c->cmap_stem, c->rbf[0].val, 5, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_NONE))
+            c->stem_layer = op.layer;
+    }
     // stride-2 forward: the input window of a 2-strided conv is a TMA box with element stride 2
     // in W and H (box = 2·extent raw elements, every other one loaded); conv3 256-pixel and
     // conv2 128-pixel tiles of the output grid
@@ -496,7 +514,9 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
         a.res = op.res >= 0 ? c->rbf[op.res].val : nullptr;
         a.relu = op.relu;
         a.mbits_out = op.relu ? c->rbf[op.dst].mbits : nullptr;
-        if (Db.C <= 128) {  // channels on M, 256 pixels on N (full-width MMA)
+        if (op.layer == c->stem_layer && (a.wsrc = c->wscr + c->wscr_off[op.layer], stem_fwd_ok(a))) {
+            c->launch("fwd", [&] { launch_stem_fwd(c->cmap_stem, a, st); });  // two taps per MMA, pixels on M
+        } else if (Db.C <= 128) {  // channels on M, 256 pixels on N (full-width MMA)
             a.tma_a = c->tma_fwd[op.layer];
             a.halo = c->halo_fwd[op.layer];
             const CUtensorMap& bm = a.halo ? c->cmap_hf[op.layer] : c->cmap_bf[op.layer];

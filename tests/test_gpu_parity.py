@@ -1243,3 +1243,30 @@ def test_cnn_bf16_eps_fused_wgrad_equals_combine(hw, B, S, chunk, cl, monkeypatc
         for name, u, ref in (("acc_mu", m1[sl], m0[sl]), ("acc_rho", r1[sl], r0[sl])):
             assert np.abs(u - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
     assert l1 == l0
+
+
+@pytest.mark.parametrize("hw,B,S,aug", [(16, 3, 2, "per_sample"), (32, 2, 3, "per_sample"), (16, 4, 2, "none")])
+def test_cnn_bf16_stem_kernel_equals_conv3(hw, B, S, aug, monkeypatch):
+    """The stem on stem_fwd_kernel (two taps per MMA through SWIZZLE_NONE core-matrix descriptors,
+    pixels on M) against the conv3 gather path (BNN_STEM=0): the stem's stored output, its ReLU
+    bitmask's effect on every later layer, and acc_μ / acc_ρ. Same bf16 products, fp32 sums in a
+    different order: 1e-2 of each layer's max elementwise (one bf16 ulp), 1e-3 for the accumulators."""
+    native = _native()
+    model = dict(BF16_CNN, in_h=hw, in_w=hw)
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    res = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BNN_STEM", flag)
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=1e4, aug=aug)
+        acc = _acc_parts(ctx, ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0xBEEF, 5))
+        torch.cuda.synchronize()
+        n_layers = len(ctx.tensors) // 2
+        lay = [ctx.layer_output(l, 0).cpu().numpy() for l in range(n_layers)]
+        res.append((acc, lay))
+    (a0, l0), (a1, l1) = res
+    for l, (o0, o1) in enumerate(zip(l0, l1)):
+        assert np.abs(o1 - o0).max() <= 1e-2 * max(np.abs(o0).max(), 1e-30), ("out", l)
+    for t in ctx.tensors:
+        sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
+        for name, u, ref in (("acc_mu", a1[0][sl], a0[0][sl]), ("acc_rho", a1[1][sl], a0[1][sl])):
+            assert np.abs(u - ref).max() <= 1e-3 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
