@@ -11,6 +11,8 @@
 // ReLU, RN-bf16, ReLU bitmask, 32-byte stores). W_s of every sample of the chunk (10 × 1 KB core-
 // matrix blocks each) is staged in shared memory once per CTA from the layer's W scratch slot.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 
@@ -23,7 +25,8 @@ namespace bnn {
 using namespace ptx;
 
 namespace stem {
-constexpr int kEpiWarps = 8;                  // two groups of 4 (one per TMEM lane quarter), alternate tiles
+constexpr int kGroups = 4;                     // epilogue groups of 4 warps (one per TMEM lane quarter), tiles round-robin
+constexpr int kEpiWarps = 4 * kGroups;
 constexpr int kThreads = (kEpiWarps + 2) * 32;
 constexpr int kTile = 128;                    // padded-stream positions per tile (all 128 rows are outputs)
 constexpr int kWBlk = 1024;                   // one tap: 8 co-groups × (8 rows × 16 B) core matrices
@@ -68,9 +71,9 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sWin + kNWin * kWin);
     uint64_t* wfull = bars;                  // [kNWin]
     uint64_t* wempty = bars + kNWin;         // [kNWin]
-    uint64_t* tfull = bars + 2 * kNWin;      // [2]
-    uint64_t* tempty = tfull + 2;            // [2]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tfull = bars + 2 * kNWin;      // [kGroups] TMEM accumulators of 64 columns
+    uint64_t* tempty = tfull + kGroups;      // [kGroups]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + kGroups);
     constexpr int WTMA = kEpiWarps, WMMA = kEpiWarps + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // padded rows of round_up(W + 2, 8) pixels = a multiple of 128 B (TMA destinations stay 128-B aligned)
@@ -94,13 +97,13 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
             mbar_init(&wfull[i], 1);
             mbar_init(&wempty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kGroups; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
         mbar_fence_init();
     }
-    if (warp == WMMA) tmem_alloc(tslot, 128);
+    if (warp == WMMA) tmem_alloc(tslot, 64 * kGroups);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -129,8 +132,8 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
             const uint32_t idesc = idesc_bf16(128, 64, 0, 0);
             for (int t = t0, tl = 0; t < t1; ++t, ++tl) {
                 const int s = t / ptiles, pt = t - s * ptiles;
-                const int buf = tl & 1, ws = tl % kNWin;
-                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                const int buf = tl % kGroups, ws = tl % kNWin;
+                mbar_wait_role(&tempty[buf], ((tl / kGroups) & 1) ^ 1);
                 mbar_wait_role(&wfull[ws], (tl / kNWin) & 1);
                 tc_fence_after();
                 const int p0 = pt * kTile;
@@ -156,36 +159,37 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
         // (pixels 32q … 32q + 31), thread = pixel with its 64 channels (two passes of 32)
         const int g = warp >> 2, q = warp & 3;
         const int m = 32 * q + lane;
-        for (int t = t0 + g, tl = g; t < t1; t += 2, tl += 2) {
+        for (int t = t0 + g, tl = g; t < t1; t += kGroups, tl += kGroups) {
             const int s = t / ptiles, pt = t - s * ptiles;
             const int pix = pt * kTile + m;
             const int r = pix / PWp, cx = pix - r * PWp, b = r / PHp, y = r - b * PHp;
             const bool pv = b < a.B && y < PH && cx >= 1 && cx <= PW;
             const int64_t ro = pv ? (((int64_t)b * PH + y) * PW + cx - 1) * 64 : 0;
             const int64_t so = (int64_t)s * a.out_stride_s;
-            mbar_wait(&tfull[g], (tl >> 1) & 1);
+            mbar_wait(&tfull[g], (tl / kGroups) & 1);
             tc_fence_after();
-            float v[64];
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + g * 64, v);
-            tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + g * 64 + 32, v + 32);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[g]);
-            if (!pv) continue;
             const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO);
 #pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 32) {
+            for (int c0 = 0; c0 < 64; c0 += 32) {  // two passes of 32 channels (96-register budget of 18 warps)
+                float v[32];
+                tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + g * 64 + c0, v);
+                if (c0 == 32) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[g]);
+                }
+                if (!pv) continue;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const float4 b4 = __ldg(bs + c0 / 4 + k);
-                    v[c0 + 4 * k] = fmaxf(v[c0 + 4 * k] + b4.x, 0.0f);
-                    v[c0 + 4 * k + 1] = fmaxf(v[c0 + 4 * k + 1] + b4.y, 0.0f);
-                    v[c0 + 4 * k + 2] = fmaxf(v[c0 + 4 * k + 2] + b4.z, 0.0f);
-                    v[c0 + 4 * k + 3] = fmaxf(v[c0 + 4 * k + 3] + b4.w, 0.0f);
+                    v[4 * k] = fmaxf(v[4 * k] + b4.x, 0.0f);
+                    v[4 * k + 1] = fmaxf(v[4 * k + 1] + b4.y, 0.0f);
+                    v[4 * k + 2] = fmaxf(v[4 * k + 2] + b4.z, 0.0f);
+                    v[4 * k + 3] = fmaxf(v[4 * k + 3] + b4.w, 0.0f);
                 }
                 uint32_t pk[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) pk[k] = pack_bf16x2(v[c0 + 2 * k], v[c0 + 2 * k + 1]);
+                for (int k = 0; k < 16; ++k) pk[k] = pack_bf16x2(v[2 * k], v[2 * k + 1]);
                 st256s(a.out + so + ro + c0, pk);
                 st256s(a.out + so + ro + c0 + 16, pk + 8);
                 if (a.mbits_out) {  // bit j = stored bf16 of channel c0 + j > 0 (no negative values after the ReLU)
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
     __syncthreads();
     if (warp == WMMA) {
         tc_fence_after();
-        tmem_dealloc(tmem, 128);
+        tmem_dealloc(tmem, 64 * kGroups);
     }
 }
 
@@ -224,6 +228,11 @@ void launch_stem_fwd(const CUtensorMap& xmap, const Conv2Args& a, cudaStream_t s
     const int ptiles = (a.B * (a.H + 1) * stem_pitch(a.W) + stem::kTile - 1) / stem::kTile;
     const int64_t T = (int64_t)a.S * ptiles;
     stem_fwd_kernel<<<(int)std::min<int64_t>(T, kNumSMs), stem::kThreads, stem::kSmem, st>>>(xmap, a);
+    if (getenv("BNN_DEBUG_SYNC")) {
+        cudaError_t e1 = cudaGetLastError(), e2 = cudaStreamSynchronize(st);
+        fprintf(stderr, "stem_fwd_kernel: launch %s, sync %s (smem %d, threads %d)\n", cudaGetErrorString(e1),
+                cudaGetErrorString(e2), stem::kSmem, stem::kThreads);
+    }
 }
 
 }  // namespace bnn
