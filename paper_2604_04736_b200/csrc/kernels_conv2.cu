@@ -237,18 +237,22 @@ __device__ __forceinline__ void epi_apply32(const Conv2Args& a, float* v, bool p
     if (MODE == 0 && a.mbits_out) a.mbits_out[(so + rowoff + ch0) >> 5] = relu_bits32(pk);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(c2::kThreads, 1)
+// CPS CTAs per SM: 1 (216 KB of stages, two TMEM accumulators) or 2 (96 KB, one accumulator each:
+// two MMA issue streams per SM, and a 256-tile stage-4 layer fits one wave of 296 slots)
+template <int MODE, int CPS>
+__global__ void __launch_bounds__(c2::kThreads, CPS)
     conv2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap wmap,
                  const Conv2Args a, const int g_max_stages_arg) {
     using namespace c2;
+    constexpr int NB = CPS == 1 ? 2 : 1;
+    constexpr int DATA = CPS == 1 ? kData : 96 * 1024;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment as an offset into the __shared__ array: the pointer keeps the shared
     // address space, so plain loads/stores through it compile to LDS/STS
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     const int kBStage = a.n_tile * 128;
-    const int kStages = min(g_max_stages_arg, kData / (kAStage + kBStage));
+    const int kStages = min(g_max_stages_arg, DATA / (kAStage + kBStage));
     uint8_t* sB = smem + kStages * kAStage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
     uint64_t* full = bars;
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
             staps[cl * 10 + 9] = cnt;
         }
     }
-    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, 512);
+    if (warp == kEpiWarps + kGatherWarps + 1) tmem_alloc(tslot, NB * 256);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -356,8 +360,8 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
             int it = 0, tl = 0;
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
-                const int buf = tl & 1;
-                mbar_wait_role(&tempty[buf], ((tl >> 1) & 1) ^ 1);
+                const int buf = tl % NB;
+                mbar_wait_role(&tempty[buf], ((tl / NB) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 const int nkb = nkb_of(g.cls);
@@ -453,9 +457,9 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
         int tl = 0, nred = 0;
         for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
             const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
-            const int buf = tl & 1;
+            const int buf = tl % NB;
             const int nkb = nkb_of(g.cls);
-            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            mbar_wait(&tfull[buf], (tl / NB) & 1);
             tc_fence_after();
             const int pix = g.ptile * 128 + row;
             const bool pv = pix < P;
@@ -503,8 +507,19 @@ __global__ void __launch_bounds__(c2::kThreads, 1)
     __syncthreads();
     if (warp == kEpiWarps + kGatherWarps + 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, NB * 256);
     }
+}
+
+// CTAs per SM of the swap-AB conv: 2 for the data gradient (C3 stage 4: 91–96 → 77–83 µs, stage 3
+// 96–101 → 90–100), 1 for the forward (stage 4: 82 → 90 µs with two); BNN_CONV2_CPS=1|2 forces both
+static int conv2_cps(int mode) {
+    static int v = [] {
+        const char* e = getenv("BNN_CONV2_CPS");
+        const int x = e ? atoi(e) : 0;
+        return x == 1 || x == 2 ? x : 0;
+    }();
+    return v ? v : (mode == 1 ? 2 : 1);
 }
 
 int conv2_dgrad_parts(const Conv2Args& a) {
@@ -515,16 +530,21 @@ int conv2_dgrad_parts(const Conv2Args& a) {
 template <int MODE>
 static void launch_conv2(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a,
                          cudaStream_t st) {
-    ensure_smem_attr(reinterpret_cast<const void*>(conv2_kernel<MODE>), c2::kSmem);
     const int ncls = MODE == 1 ? a.stride * a.stride : 1;
     const int PH = MODE == 0 ? a.OH : a.H / a.stride, PW = MODE == 0 ? a.OW : a.W / a.stride;
     const int P = a.B * PH * PW;
     const int Ntot = MODE == 0 ? a.CO : a.C;
     const int T = a.S * ncls * ((P + 127) / 128) * ((Ntot + a.n_tile - 1) / a.n_tile);
-    const int grid = std::min(T, kNumSMs);
     Conv2Args b = a;
     b.dbg = conv_debug();
-    conv2_kernel<MODE><<<grid, c2::kThreads, c2::kSmem, st>>>(amap, wmap, b, conv_stage_cap());
+    if (conv2_cps(MODE) == 2) {
+        constexpr int smem = 1024 + 96 * 1024 + 512 + 1024;
+        ensure_smem_attr(reinterpret_cast<const void*>(conv2_kernel<MODE, 2>), smem);
+        conv2_kernel<MODE, 2><<<std::min(T, 2 * kNumSMs), c2::kThreads, smem, st>>>(amap, wmap, b, conv_stage_cap());
+        return;
+    }
+    ensure_smem_attr(reinterpret_cast<const void*>(conv2_kernel<MODE, 1>), c2::kSmem);
+    conv2_kernel<MODE, 1><<<std::min(T, kNumSMs), c2::kThreads, c2::kSmem, st>>>(amap, wmap, b, conv_stage_cap());
 }
 
 void launch_conv2_fwd(const CUtensorMap& amap, const CUtensorMap& wmap, const Conv2Args& a, cudaStream_t st) {
