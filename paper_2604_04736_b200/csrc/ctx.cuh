@@ -299,8 +299,13 @@ struct bnn_ctx {
         pending.clear();
         ev_next = 0;
     }
+    static bool skip_class(const char* cls) {
+        static const char* e = getenv("BNN_EXP_SKIP");
+        return e && strstr(e, cls) != nullptr;
+    }
     template <class F>
     void launch(const char* cls, F&& f, int kernels = 1) {
+        if (skip_class(cls)) return;  // timing experiments only (BNN_EXP_SKIP=class[,class]): wrong results
         int c = -1;
         cudaEvent_t a = nullptr, b = nullptr;
         if (prof) {

@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(256)
     gen_wscratch_kernel(SampledLayer L, SampleKeys kk, int S, int C, int C_pad, int taps, int K_pad,
                         __nv_bfloat16* __restrict__ out, float* __restrict__ bias_out) {
     const int co = blockIdx.x;
-    for (int s = threadIdx.x; bias_out && s < S; s += blockDim.x) {  // sampled biases b_s, fp32 [S][N]
+    // blockIdx.y: a group of samples [s_lo, s_hi) (more blocks for layers with few rows)
+    const int sg = (S + gridDim.y - 1) / gridDim.y, s_lo = blockIdx.y * sg, s_hi = min(S, s_lo + sg);
+    for (int s = s_lo + threadIdx.x; bias_out && s < s_hi; s += blockDim.x) {  // sampled biases b_s, fp32 [S][N]
         bias_out[(int64_t)s * L.N + co] = __fmaf_rn(
             L.sigma[L.off_b + co], eps1(kk.key, kk.step, kk.s0 + s, L.t_b, 0u, (uint32_t)co), L.mu[L.off_b + co]);
     }
@@ -50,7 +52,7 @@ __global__ void __launch_bounds__(256)
                 g = __ldg(reinterpret_cast<const float4*>(L.sigma + i));
             }
 #pragma unroll 4
-            for (int s = 0; s < S; ++s) {  // independent Philox chains: unrolled for ILP
+            for (int s = s_lo; s < s_hi; ++s) {  // independent Philox chains: unrolled for ILP
                 uint2 v = make_uint2(0u, 0u);
                 if (ok) {
                     const float4 e = eps4(kk.key, kk.step, kk.s0 + s, L.t_w, (uint32_t)co, (uint32_t)qd);
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(256)
                 *reinterpret_cast<uint2*>(orow + s * srow + kp) = v;
             }
         } else {
-            for (int s = 0; s < S; ++s) {
+            for (int s = s_lo; s < s_hi; ++s) {
                 float w[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -83,7 +85,10 @@ void launch_gen_wscratch(const SampledLayer& L, const SampleKeys& kk, int S, int
                          int taps, int K_pad, __nv_bfloat16* out, float* bias_out, cudaStream_t st) {
     const int kq = K_pad / 4;
     const int threads = kq >= 256 ? 256 : ((kq + 31) / 32) * 32;
-    gen_wscratch_kernel<<<L.N, std::max(threads, 32), 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out, bias_out);
+    // sample groups so that a layer with few rows still fills the GPU (≥ 8 blocks per SM)
+    const int groups = std::max(1, std::min(S, (8 * kNumSMs + L.N - 1) / L.N));
+    gen_wscratch_kernel<<<dim3(L.N, groups), std::max(threads, 32), 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out,
+                                                                           bias_out);
 }
 
 // ============================================================================ split reduce
