@@ -8,10 +8,12 @@ import sys
 CLASSES = {
     "mlp": {"fwd": ["gen_gemm_kernel<0, 2>", "gen_gemm_kernel<0, 4>"], "dgrad": ["gen_gemm_kernel<1, 2>"],
             "wgrad": ["wgrad_tc_kernel"]},
-    "cnn": {"fwd": ["conv2_kernel<0>", "conv3_kernel<0, 0>", "conv3_kernel<0, 1>", "conv64_kernel<0>"],
-            "dgrad": ["conv2_kernel<1>", "conv3_kernel<1, 0>", "conv3_kernel<1, 1>", "conv64_kernel<1>"],
-            "wgrad": ["conv2_wgrad_kernel", "conv64_wgrad_kernel<0>", "conv64_wgrad_kernel<1>",
-                      "wgrad_split_reduce_kernel", "wgrad_eps_combine_kernel", "wgrad_eps_combine_lanes_kernel"]},
+    "cnn": {"fwd": ["conv2_kernel<0, 1>", "conv2_kernel<0, 2>", "conv3_kernel<0, 0>", "conv3_kernel<0, 1>",
+                    "conv64_kernel<0>", "stem_fwd_kernel"],
+            "dgrad": ["conv2_kernel<1, 1>", "conv2_kernel<1, 2>", "conv3_kernel<1, 0>", "conv3_kernel<1, 1>",
+                      "conv64_kernel<1>"],
+            "wgrad": ["conv2_wgrad_kernel<1>", "conv2_wgrad_kernel<2>", "conv64_wgrad_kernel<0>", "conv64_wgrad_kernel<1>",
+                      "wgrad_split_reduce4_kernel", "wgrad_eps_combine_kernel", "wgrad_eps_combine_lanes_kernel"]},
 }
 
 
