@@ -1270,3 +1270,43 @@ def test_cnn_bf16_stem_kernel_equals_conv3(hw, B, S, aug, monkeypatch):
         sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
         for name, u, ref in (("acc_mu", a1[0][sl], a0[0][sl]), ("acc_rho", a1[1][sl], a0[1][sl])):
             assert np.abs(u - ref).max() <= 1e-3 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
+
+
+_OLD_PATHS = {"BNN_CONV64": "0", "BNN_STEM": "0", "BNN_WGRAD_EPS": "0", "BNN_CONV2_CPS": "1", "BNN_WGRAD_CPS": "1"}
+
+
+@pytest.mark.parametrize("hw,B,S", [(8, 1, 1), (24, 2, 1), (16, 1, 3), (8, 3, 8)])
+def test_cnn_bf16_session4_kernels_edge_shapes(hw, B, S, monkeypatch):
+    """Edge shapes (one image, one sample, 8×8 inputs where one tile spans several images, 24×24
+    (rows not a power of two), S = 8 with B = 3) through the round-2 session-4
+    kernels (conv64 fwd / dgrad / ε-fused wgrad, the stem kernel, two CTAs per SM) against the
+    same step on the earlier paths: every stored activation and gradient within one bf16 ulp of
+    each layer's max (1e-2), acc_μ / acc_ρ within 1e-2 of each tensor's max (their inputs are those
+    stored bf16 values, so a rounding tie flipped upstream moves a weight gradient by up to ≈ 2^-8
+    of a product: measured 1.6e-3 at 24×24)."""
+    native = _native()
+    model = dict(BF16_CNN, in_h=hw, in_w=hw)
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    res = []
+    for old in (True, False):
+        for k, v in _OLD_PATHS.items():
+            if old:
+                monkeypatch.setenv(k, v)
+            else:
+                monkeypatch.delenv(k, raising=False)
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=1e4, aug="per_sample")
+        acc = _acc_parts(ctx, ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0xBEEF, 5))
+        torch.cuda.synchronize()
+        n_layers = len(ctx.tensors) // 2
+        lay = [(ctx.layer_output(l, 0).cpu().numpy(),
+                ctx.layer_output(l, 1).cpu().numpy() if l < n_layers - 1 else None) for l in range(n_layers)]
+        res.append((acc, lay))
+    (a0, l0), (a1, l1) = res
+    for l, ((o0, g0), (o1, g1)) in enumerate(zip(l0, l1)):
+        assert np.abs(o1 - o0).max() <= 1e-2 * max(np.abs(o0).max(), 1e-30), ("out", l)
+        if g0 is not None:
+            assert np.abs(g1 - g0).max() <= 1e-2 * max(np.abs(g0).max(), 1e-30), ("grad", l)
+    for t in ctx.tensors:
+        sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
+        for name, u, ref in (("acc_mu", a1[0][sl], a0[0][sl]), ("acc_rho", a1[1][sl], a0[1][sl])):
+            assert np.abs(u - ref).max() <= 1e-2 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
