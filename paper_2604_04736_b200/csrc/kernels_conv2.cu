@@ -668,6 +668,10 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+#ifdef C3_PROF
+    long long p_full = 0, p_tempty = 0, p_tfull = 0, p_empty = 0;
+    const long long p_start = clock64();
+#endif
     auto nkb_of = [&](int cls) { return MODE == 0 ? a.K_pad / 64 : staps[cls * 10 + 9] * cblocks; };
 
     if (warp == WTMA) {
@@ -701,7 +705,13 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % NST;
                     const uint32_t ph = (it / NST) & 1;
+#ifdef C3_PROF
+                    const long long q0 = clock64();
+#endif
                     mbar_wait_role(&empty[st], ph ^ 1);
+#ifdef C3_PROF
+                    p_empty += clock64() - q0;
+#endif
                     if (a.dbg & 2) {  // feed-rate experiment: no loads
                         mbar_arrive_expect_tx(&full[st], 0);
                         continue;
@@ -742,7 +752,13 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
             for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
                 const TileGeo g = tile_of<MODE>(t, mtiles, ptiles, ncls);
                 const int buf = tl % NBUF;
+#ifdef C3_PROF
+                const long long q1 = clock64();
+#endif
                 mbar_wait_role(&tempty[buf], ((tl / NBUF) & 1) ^ 1);
+#ifdef C3_PROF
+                p_tempty += clock64() - q1;
+#endif
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 const int nkb = nkb_of(g.cls);
@@ -753,7 +769,13 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % NST;
                     const uint32_t ph = (it / NST) & 1;
+#ifdef C3_PROF
+                    const long long q2 = clock64();
+#endif
                     mbar_wait_role(&full[st], ph);
+#ifdef C3_PROF
+                    p_full += clock64() - q2;
+#endif
                     fence_proxy_async_smem();
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
@@ -910,7 +932,13 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
                 if (MODE == 1 && a.mbits) x2 = __ldg(a.mbits + ((so + ro + ch0) >> 5));
             };
             load_ops(c_first, o1, o2);  // independent of the accumulator: in flight while the MMAs finish
+#ifdef C3_PROF
+            const long long q3 = clock64();
+#endif
             mbar_wait(&tfull[buf], (tl / NBUF) & 1);
+#ifdef C3_PROF
+            p_tfull += clock64() - q3;
+#endif
             tc_fence_after();
             for (int c = c_first; c < 8; c += c_step) {  // 32 pixels per chunk
                 float v[32];
@@ -951,6 +979,11 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
             if (lane == 0) mbar_arrive(&tempty[buf]);
         }
     }
+#ifdef C3_PROF
+    if ((blockIdx.x == 0 || blockIdx.x == 77) && lane == 0 && (warp == WMMA || warp == WTMA || warp == 0 || warp == 4))
+        printf("c3<%d,%d> cta %d warp %d total %lld wait_empty %lld wait_tempty %lld wait_full %lld wait_tfull %lld\n", MODE,
+               (int)HALO, blockIdx.x, warp, clock64() - p_start, p_empty, p_tempty, p_full, p_tfull);
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == WMMA) {
