@@ -181,6 +181,20 @@ __global__ void input_bf16_kernel(const float* __restrict__ x, int B, int H, int
     }
     const float* src = x + (int64_t)b * H * W * C;
     __nv_bfloat16* dst = out + ((int64_t)s * B + b) * H * W * C_pad;
+    if (C_pad == 8 && C <= 8) {  // thread = pixel: its 8 (padded) channels as one 16-byte store
+        for (int pix = threadIdx.x; pix < H * W; pix += blockDim.x) {
+            const int r = pix / W, cc = pix - r * W;
+            const int jj = flip ? W - 1 - cc : cc;
+            const int si = r + dy - 4, sj = jj + dx - 4;
+            const bool in = si >= 0 && si < H && sj >= 0 && sj < W;
+            float v[8];
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) v[ch] = (in && ch < C) ? src[((int64_t)si * W + sj) * C + ch] : 0.0f;
+            *reinterpret_cast<uint4*>(dst + (int64_t)pix * 8) =
+                make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < H * W * C_pad; i += blockDim.x) {
         const int ch = i % C_pad, pix = i / C_pad, r = pix / W, cc = pix % W;
         const int jj = flip ? W - 1 - cc : cc;
