@@ -26,7 +26,7 @@ using namespace ptx;
 // ============================================================================ W scratch
 // Block = one output-channel row co (blockIdx.x) of every sample; thread = column quads of the
 // row; μ and σ are loaded once per quad and reused for the S samples.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     gen_wscratch_kernel(SampledLayer L, SampleKeys kk, int S, int C, int C_pad, int taps, int K_pad,
                         __nv_bfloat16* __restrict__ out, float* __restrict__ bias_out) {
     const int co = blockIdx.x;
@@ -84,9 +84,17 @@ __global__ void __launch_bounds__(256)
 void launch_gen_wscratch(const SampledLayer& L, const SampleKeys& kk, int S, int C, int C_pad,
                          int taps, int K_pad, __nv_bfloat16* out, float* bias_out, cudaStream_t st) {
     const int kq = K_pad / 4;
-    const int threads = kq >= 256 ? 256 : ((kq + 31) / 32) * 32;
-    // sample groups so that a layer with few rows still fills the GPU (≥ 8 blocks per SM)
-    const int groups = std::max(1, std::min(S, (8 * kNumSMs + L.N - 1) / L.N));
+    // balanced blocks: a thread count (multiple of 32, ≤ 512) that divides the row's quads when one
+    // exists (a 4608-column row: 384 threads × 3 quads instead of 256 × 4.5), and sample groups that
+    // divide S, enough of them for a layer with few rows to fill the GPU (≥ 8 blocks per SM)
+    int threads = kq >= 256 ? 256 : ((kq + 31) / 32) * 32;
+    for (int t = 512; t >= 128; t -= 32)
+        if (kq % t == 0) {
+            threads = t;
+            break;
+        }
+    int groups = std::max(1, std::min(S, (8 * kNumSMs + L.N - 1) / L.N));
+    while (groups > 1 && S % groups != 0) --groups;
     gen_wscratch_kernel<<<dim3(L.N, groups), std::max(threads, 32), 0, st>>>(L, kk, S, C, C_pad, taps, K_pad, out,
                                                                            bias_out);
 }
