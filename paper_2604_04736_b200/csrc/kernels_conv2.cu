@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(c2::kThreads, CPS)
             const TileGeo g = tile_of<MODE>(t, ntiles, ptiles, ncls);
             const int buf = tl % NB;
             const int nkb = nkb_of(g.cls);
-            mbar_wait(&tfull[buf], (tl / NB) & 1);
+            epi_wait(&tfull[buf], (tl / NB) & 1);
             tc_fence_after();
             const int pix = g.ptile * 128 + row;
             const bool pv = pix < P;
@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
 #ifdef C3_PROF
             const long long q3 = clock64();
 #endif
-            mbar_wait(&tfull[buf], (tl / NBUF) & 1);
+            epi_wait(&tfull[buf], (tl / NBUF) & 1);
 #ifdef C3_PROF
             p_tfull += clock64() - q3;
 #endif
@@ -1258,7 +1258,7 @@ __global__ void __launch_bounds__(w2::kThreads, CPS)
         for (int t = blockIdx.x; t < T; t += gridDim.x, ++tl) {
             const U u = unit(t);
             const int buf = tl % NB;
-            mbar_wait(&tfull[buf], (tl / NB) & 1);
+            epi_wait(&tfull[buf], (tl / NB) & 1);
             tc_fence_after();
             const int co = u.ct * 128 + 32 * q + lane;
             const int half = u.w / 2;

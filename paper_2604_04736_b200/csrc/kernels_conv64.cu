@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
             }
             if (MODE == 1 && pv && a.mbits) mw = __ldg(a.mbits + ((so + ro) >> 5));
             C64_T(pe0);
-            mbar_wait(&tfull[buf], (tl >> 1) & 1);
+            epi_wait(&tfull[buf], (tl >> 1) & 1);  // the other group works meanwhile
             C64_T(pe1);
             tc_fence_after();
             const uint32_t ta = tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 256 + ch0;
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
         const int co = 32 * (q & 1) + lane;
         const bool any = kb1 > kb0;
         if (any) {
-            mbar_wait(tfull, 0);
+            epi_wait(tfull, 0);
             tc_fence_after();
         }
         float* outrow = a.part + ((int64_t)(s * a.nsplit + u) * 64 + co) * 576;
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
         const bool any = kb1 > kb0;
         const int q = warp & 3, hh = warp >> 2;
         if (warp < kEpiWarps && any) {
-            mbar_wait(tfull, 0);
+            epi_wait(tfull, 0);
             tc_fence_after();
         }
         const int S = Gc;  // the cluster's samples

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
             const bool pv = b < a.B && y < PH && cx >= 1 && cx <= PW;
             const int64_t ro = pv ? (((int64_t)b * PH + y) * PW + cx - 1) * 64 : 0;
             const int64_t so = (int64_t)s * a.out_stride_s;
-            mbar_wait(&tfull[g], (tl / kGroups) & 1);
+            epi_wait(&tfull[g], (tl / kGroups) & 1);
             tc_fence_after();
             const float4* bs = reinterpret_cast<const float4*>(a.bias + (int64_t)s * a.CO);
 #pragma unroll

@@ -119,6 +119,17 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity
 #endif
 }
 
+// Epilogue warps waiting for an accumulator: the suspend-hint form (the waiting warps would
+// otherwise poll and take issue slots from the working ones — the other epilogue group, the
+// gather warps); BNN_EPI_POLL builds poll (A/B)
+__device__ __forceinline__ void epi_wait(uint64_t* bar, uint32_t parity) {
+#ifdef BNN_EPI_POLL
+    mbar_wait(bar, parity);
+#else
+    mbar_wait_suspend(bar, parity);
+#endif
+}
+
 // ------------------------------------------------------------------ proxy fences
 // generic-proxy smem writes → visible to the async proxy (tensor core operand reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
