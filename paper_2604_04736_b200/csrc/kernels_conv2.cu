@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(c2::kThreads, CPS)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % kStages;
                     const uint32_t phs = (it / kStages) & 1;
-                    mbar_wait(&empty[st], phs ^ 1);
+                    gather_wait(&empty[st], phs ^ 1);
                     const uint32_t base = smem_u32(sA + st * kAStage) + r * 128;
                     if (MODE == 0 && cpb == 0) {  // stem: 8 taps × 8 channels per K block
 #pragma unroll
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int st = it % NST;
                     const uint32_t phs = (it / NST) & 1;
-                    mbar_wait(&empty[st], phs ^ 1);
+                    gather_wait(&empty[st], phs ^ 1);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int r = gt + 128 * h;
@@ -1235,7 +1235,7 @@ __global__ void __launch_bounds__(w2::kThreads, CPS)
                         ix0[i] = (rem - oy * a.OW) * a.stride;
                         nb0[i] = (int64_t)n * a.H;
                     }
-                    mbar_wait(&empty[st], ph ^ 1);
+                    gather_wait(&empty[st], ph ^ 1);
                     const uint32_t base = smem_u32(sB + st * kBStage) + ((ch ^ (r0 & 7)) << 4) + r0 * 128;
                     for (int j = 0; j < nb; ++j) {
 #pragma unroll

@@ -130,6 +130,16 @@ __device__ __forceinline__ void epi_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Gather warps (cp.async producers) waiting for a free stage: the suspend-hint form unless a
+// BNN_GATHER_POLL build (A/B)
+__device__ __forceinline__ void gather_wait(uint64_t* bar, uint32_t parity) {
+#ifdef BNN_GATHER_POLL
+    mbar_wait(bar, parity);
+#else
+    mbar_wait_suspend(bar, parity);
+#endif
+}
+
 // ------------------------------------------------------------------ proxy fences
 // generic-proxy smem writes → visible to the async proxy (tensor core operand reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
