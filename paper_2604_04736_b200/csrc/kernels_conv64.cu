@@ -24,7 +24,10 @@
 //    values from a 96-float shared exchange (one named barrier per tile and channel half); a
 //    tile outputs 126 of its 128 rows. Then the NHWC row in place: + bias, + residual, ReLU,
 //    ReLU bitmask (fwd) / + other contribution, input ReLU mask, bias-gradient partials (dgrad),
-//    32 channels = 64 contiguous bytes per thread.
+//    32 channels = 64 contiguous bytes per thread (the dgrad in passes of 16 channels). Two groups
+//    of epilogue warps take alternate tiles.
+//  * The weight gradient (below): MN-major views of two halo windows, ε fused in the epilogue and
+//    the samples of a thread-block cluster summed over DSMEM.
 #include <algorithm>
 #include <cstdlib>
 
@@ -43,8 +46,8 @@ namespace c64 {
 // epilogue warps: two groups of 8 (4 lane quarters × 2 channel halves) taking even / odd tiles, so
 // each group has two MMA tile-times per epilogue (C64_PROF: a group's epilogue of a tile takes
 // ≈ 4.7 K cycles, the MMAs ≈ 2.2 K)
-template <int MODE> constexpr int groups() { return 2; }
-template <int MODE> constexpr int threads() { return (8 * groups<MODE>() + 2) * 32; }  // + TMA, MMA warps
+constexpr int kGroups = 2;
+constexpr int kThreads = (8 * kGroups + 2) * 32;  // + the TMA warp + the MMA warp
 constexpr int kBlk = 64 * 128;                  // one tap block: 64 rows × 64 bf16 (SWIZZLE_128B)
 constexpr int kWres = 9 * kBlk;                 // 3 kernel rows × 3 taps (72 KB)
 constexpr int kNWin = 4;                        // halo window ring
@@ -65,25 +68,6 @@ __host__ __device__ __forceinline__ int c64_floor_div(int a, int b) {  // b > 0
     return (a % b != 0 && a < 0) ? q - 1 : q;
 }
 
-// 32 lanes × 32 columns at three column offsets 64 apart (one wait)
-__device__ __forceinline__ void tmem_ld32x3(uint32_t ta, float* a, float* b, float* c) {
-    uint32_t r[96];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%96];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%97];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%64,%65,%66,%67,%68,%69,%70,%71,%72,%73,%74,%75,%76,%77,%78,%79,%80,%81,%82,%83,%84,%85,%86,%87,%88,%89,%90,%91,%92,%93,%94,%95}, [%98];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63]), "=r"(r[64]), "=r"(r[65]), "=r"(r[66]), "=r"(r[67]), "=r"(r[68]), "=r"(r[69]), "=r"(r[70]), "=r"(r[71]), "=r"(r[72]), "=r"(r[73]), "=r"(r[74]), "=r"(r[75]), "=r"(r[76]), "=r"(r[77]), "=r"(r[78]), "=r"(r[79]), "=r"(r[80]), "=r"(r[81]), "=r"(r[82]), "=r"(r[83]), "=r"(r[84]), "=r"(r[85]), "=r"(r[86]), "=r"(r[87]), "=r"(r[88]), "=r"(r[89]), "=r"(r[90]), "=r"(r[91]), "=r"(r[92]), "=r"(r[93]), "=r"(r[94]), "=r"(r[95])
-        : "r"(ta), "r"(ta + 64), "r"(ta + 128)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        a[i] = __uint_as_float(r[i]);
-        b[i] = __uint_as_float(r[32 + i]);
-        c[i] = __uint_as_float(r[64 + i]);
-    }
-}
-
 // v of lane + d, or `other` where lane + d is past the warp (shfl's in-range predicate selects)
 __device__ __forceinline__ float shfl_down_or(float v, int d, float other) {
     float r;
@@ -94,23 +78,6 @@ __device__ __forceinline__ float shfl_down_or(float v, int d, float other) {
         : "=f"(r)
         : "f"(v), "r"(d), "f"(other));
     return r;
-}
-
-// 32 lanes × 32 columns at two column offsets (one wait)
-__device__ __forceinline__ void tmem_ld32x2(uint32_t ta, uint32_t tb, float* a, float* b) {
-    uint32_t r[64];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%64];\n\t"
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%65];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
-        : "r"(ta), "r"(tb)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        a[i] = __uint_as_float(r[i]);
-        b[i] = __uint_as_float(r[32 + i]);
-    }
 }
 
 // 32-byte global load / store (LDG.256 / STG.256: one full sector per lane)
@@ -172,7 +139,7 @@ __device__ __forceinline__ float c64_transpose_sum(float* v, int lane) {
 #define C64_T(x)
 #endif
 template <int MODE>
-__global__ void __launch_bounds__(c64::threads<MODE>(), 1)
+__global__ void __launch_bounds__(c64::kThreads, 1)
     conv64_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
                   const Conv2Args a) {
     using namespace c64;
@@ -191,7 +158,7 @@ __global__ void __launch_bounds__(c64::threads<MODE>(), 1)
     uint64_t* tempty = tfull + 2;          // [2]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    constexpr int NG = groups<MODE>();
+    constexpr int NG = kGroups;
     constexpr int WTMA = 8 * NG, WMMA = WTMA + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int PH = a.H, PW = a.W;  // stride 1, pad 1: the output grid is the input grid
@@ -823,7 +790,7 @@ template <int MODE>
 static void launch_conv64(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(conv64_kernel<MODE>), c64::kSmem);
     const int64_t T = (int64_t)a.S * conv64_parts(a);
-    conv64_kernel<MODE><<<(int)std::min<int64_t>(T, kNumSMs), c64::threads<MODE>(), c64::kSmem, st>>>(wmap, bmap, a);
+    conv64_kernel<MODE><<<(int)std::min<int64_t>(T, kNumSMs), c64::kThreads, c64::kSmem, st>>>(wmap, bmap, a);
 }
 
 void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
