@@ -243,6 +243,7 @@ struct bnn_ctx {
     std::vector<char> wgrad_eps;  // ε-fused, sample-accumulating weight gradient (no per-sample partials)
     CUtensorMap cmap_stem;      // the stem input: 1-row (W + 2)-pixel boxes, 8 channels, no swizzle
     int stem_layer = -1;       // the layer on stem_fwd_kernel (-1: none)
+    std::vector<Conv64RowMaps> rowmaps;  // conv64 weight gradient: multi-row TMA boxes
     std::vector<char> conv64;  // stage-1 64 → 64 layers on the W-stationary tap-paired kernel (both passes)
     __nv_bfloat16* fcG = nullptr;   // FC output gradient, [S][B][round8(O)]
     // TMA descriptors (BF16)

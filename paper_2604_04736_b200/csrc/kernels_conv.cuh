@@ -102,7 +102,12 @@ int stem_row_pitch(int W);  // padded-row length of the stem window (the map box
 // one CTA per (sample, split) (nsplit = conv64_wgrad_nsplit(S)); ymap / xmap = the HALO window
 // maps of dY and of the layer input.
 struct ConvWgradArgs;
-void launch_conv64_wgrad(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st);
+// Runs of padded rows loaded by one TMA op each: maps of box height h + 1 (h < 8) over dY and X
+// (a run never crosses an image: its separator row is the box's out-of-range row).
+struct Conv64RowMaps {
+    CUtensorMap y[8], x[8];
+};
+void launch_conv64_wgrad(const Conv64RowMaps& maps, const ConvWgradArgs& a, cudaStream_t st);
 int conv64_wgrad_ok(int H, int W);
 int conv64_wgrad_nsplit(int S);
 // ε-fused form (clusters of the S ≤ 8 samples of a split): writes scale·Σ_s (D_s, ε_s ⊙ D_s) to
@@ -110,7 +115,7 @@ int conv64_wgrad_nsplit(int S);
 // conv64_wgrad_eps_nsplit(S) (co-resident clusters, 0 = not available). Returns 0 or -1 (launch refused).
 int conv64_wgrad_eps_nsplit(int S, int Gc);
 int conv64_wgrad_eps_cluster(int S);  // default cluster size (BNN_WGRAD_EPS_CLUSTER overrides)
-int launch_conv64_wgrad_eps(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st);
+int launch_conv64_wgrad_eps(const Conv64RowMaps& maps, const ConvWgradArgs& a, cudaStream_t st);
 
 
 struct ConvWgradArgs {

@@ -527,8 +527,7 @@ int conv64_wgrad_eps_cluster(int S) {
 // order). No per-sample partials, no separate ε combine (north_star (3)); deterministic.
 template <bool EPS>
 __global__ void __launch_bounds__(c64w::kThreads, 1)
-    conv64_wgrad_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
-                        const ConvWgradArgs a) {
+    conv64_wgrad_kernel(const __grid_constant__ Conv64RowMaps maps, const ConvWgradArgs a) {
     using namespace c64w;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -565,8 +564,16 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
 
     if (warp == WTMA) {
         if (lane == 0) {
-            tma_prefetch_desc(&ymap);
-            tma_prefetch_desc(&xmap);
+            // padded rows r0 … r1 to dst: one TMA op per run of rows inside one image (its separator
+            // row y = PH and rows of images outside [0, B) are out of range: zeros)
+            auto load_rows = [&](const CUtensorMap* m, uint64_t* bar, uint8_t* dst, int r0, int r1) {
+                for (int r = r0; r <= r1;) {
+                    const int b = c64_floor_div(r, PHp), y = r - b * PHp;
+                    const int run = min(min(r1, b * PHp + PH) - r + 1, min(8, PH));  // the maps: 1 … min(8, H) rows
+                    tma_load_5d(&m[run - 1], bar, dst + (r - r0) * PWp * 128, 0, -1, y, b, s);
+                    r += run;
+                }
+            };
             for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
                 const int st = it % kStages;
                 mbar_wait_role(&empty[st], ((it / kStages) & 1) ^ 1);
@@ -575,20 +582,19 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
                 const int ys = c64_floor_div(p0, PWp), ye = c64_floor_div(p0 + kKpx, PWp);
                 uint8_t* xw = smem + st * (kXw + kYw);
                 uint8_t* yw = xw + kXw;
+                if (a.dbg & 2) {  // timing experiment (BNN_CONV_DEBUG=2): no operand loads
+                    mbar_arrive_expect_tx(&full[st], 0);
+                    continue;
+                }
                 mbar_arrive_expect_tx(&full[st], (uint32_t)((xe - xs + 1 + ye - ys + 1) * PWp * 128));
-                for (int r = xs; r <= xe; ++r) {
-                    const int b = c64_floor_div(r, PHp), y = r - b * PHp;  // y == PH, b ∉ [0, B): zeros
-                    tma_load_5d(&xmap, &full[st], xw + (r - xs) * PWp * 128, 0, -1, y, b, s);
-                }
-                for (int r = ys; r <= ye; ++r) {
-                    const int b = c64_floor_div(r, PHp), y = r - b * PHp;
-                    tma_load_5d(&ymap, &full[st], yw + (r - ys) * PWp * 128, 0, -1, y, b, s);
-                }
+                load_rows(maps.x, &full[st], xw, xs, xe);
+                load_rows(maps.y, &full[st], yw, ys, ye);
             }
         }
         __syncwarp();
     } else if (warp == WMMA) {
-        if (lane == 0) {
+        // the whole warp runs the loop (warp-uniform descriptor arithmetic), one lane issues
+        {
             const uint32_t idesc = idesc_bf16(128, 192, 1, 1);
             for (int kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
                 const int st = it % kStages;
@@ -598,18 +604,19 @@ __global__ void __launch_bounds__(c64w::kThreads, 1)
                 const int xs = c64_floor_div(p0 - PWp - 1, PWp), ys = c64_floor_div(p0, PWp);
                 const uint32_t xb0 = smem_u32(smem + st * (kXw + kYw)) + (uint32_t)(p0 - xs * PWp) * 128u;
                 const uint32_t yb0 = smem_u32(smem + st * (kXw + kYw) + kXw) + (uint32_t)(p0 - ys * PWp) * 128u;
+                const uint64_t ad0 = sdesc_sw128(yb0, 128, 1024);
+                const uint64_t bA0 = sdesc_sw128(xb0 + (uint32_t)(1 - PWp) * 128u, PWp * 128, 1024);
+                const uint64_t bB0 = sdesc_sw128(xb0 - (uint32_t)(1 + PWp) * 128u, PWp * 128, 1024);
 #pragma unroll
-                for (int q = 0; q < kKpx / 16; ++q) {
-                    const uint64_t ad = sdesc_sw128(yb0 + 2048 * q, 128, 1024);
-                    const uint64_t bA = sdesc_sw128(xb0 + 2048 * q + (uint32_t)(1 - PWp) * 128u, PWp * 128, 1024);
-                    const uint64_t bB = sdesc_sw128(xb0 + 2048 * q - (uint32_t)(1 + PWp) * 128u, PWp * 128, 1024);
+                for (int q = 0; q < kKpx / 16; ++q) {  // + 2048 B per K-step: + 128 in the address field
                     const uint32_t acc = (it | q) != 0 ? 1u : 0u;
-                    mma_bf16(tmem, ad, bA, idesc, acc);        // taps (dh, +1) | (dh, 0)
-                    mma_bf16(tmem + 256, ad, bB, idesc, acc);  // taps (dh, −1) | unused
+                    if (a.dbg & 1) continue;  // timing experiment (BNN_CONV_DEBUG=1): no MMAs
+                    mma_bf16_warp(tmem, ad0 + 128u * q, bA0 + 128u * q, idesc, acc);        // taps (dh, +1) | (dh, 0)
+                    mma_bf16_warp(tmem + 256, ad0 + 128u * q, bB0 + 128u * q, idesc, acc);  // taps (dh, −1) | unused
                 }
-                mma_commit(&empty[st]);
+                mma_commit_warp(&empty[st]);
             }
-            mma_commit(tfull);
+            mma_commit_warp(tfull);
         }
         __syncwarp();
     } else if (!EPS) {
@@ -736,9 +743,9 @@ int conv64_wgrad_ok(int H, int W) {  // both halo windows of a 128-pixel k-block
 
 int conv64_wgrad_nsplit(int S) { return std::max(1, kNumSMs / std::max(S, 1)); }
 
-void launch_conv64_wgrad(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st) {
+void launch_conv64_wgrad(const Conv64RowMaps& maps, const ConvWgradArgs& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel<false>), c64w::kSmem);
-    conv64_wgrad_kernel<false><<<a.S * a.nsplit, c64w::kThreads, c64w::kSmem, st>>>(ymap, xmap, a);
+    conv64_wgrad_kernel<false><<<a.S * a.nsplit, c64w::kThreads, c64w::kSmem, st>>>(maps, a);
 }
 
 static cudaLaunchConfig_t eps_cfg(int Gc, int nparts, cudaStream_t st, cudaLaunchAttribute* attr) {
@@ -770,12 +777,18 @@ int conv64_wgrad_eps_nsplit(int S, int Gc) {  // partials (splits × sample grou
     return std::max(1, n / groups) * groups;  // whole pixel splits: every split has all sample groups
 }
 
-int launch_conv64_wgrad_eps(const CUtensorMap& ymap, const CUtensorMap& xmap, const ConvWgradArgs& a, cudaStream_t st) {
+int launch_conv64_wgrad_eps(const Conv64RowMaps& maps, const ConvWgradArgs& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(conv64_wgrad_kernel<true>), c64w::kSmem);
     cudaLaunchAttribute attr[1];
     if (a.eps_cluster < 1 || a.S % a.eps_cluster != 0 || a.nsplit % (a.S / a.eps_cluster) != 0) return -1;
     cudaLaunchConfig_t cfg = eps_cfg(a.eps_cluster, a.nsplit, st, attr);
-    return cudaLaunchKernelEx(&cfg, conv64_wgrad_kernel<true>, ymap, xmap, a) == cudaSuccess ? 0 : -1;
+    ConvWgradArgs b = a;
+    static const int dbg = [] {  // BNN_CONV_DEBUG (timing experiments): 1 = no MMAs, 2 = no operand loads
+        const char* e = getenv("BNN_CONV_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    b.dbg = dbg;
+    return cudaLaunchKernelEx(&cfg, conv64_wgrad_kernel<true>, maps, b) == cudaSuccess ? 0 : -1;
 }
 
 int conv64_ok(int H, int W) {  // the padded window of a 128-row tile fits one window stage

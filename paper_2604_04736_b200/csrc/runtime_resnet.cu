@@ -272,6 +272,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
     c->halo_fwd.assign(L, 0);
     c->halo_dgrad.assign(L, 0);
     c->conv64.assign(L, 0);
+    c->rowmaps.resize(L);
     const char* he = getenv("BNN_CONV_HALO");
     const bool halo_on = !(he && atoi(he) == 0);
     for (const ROp& op : c->rops) {
@@ -299,7 +300,20 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             c->halo_dgrad[op.layer] = 1;
         }
         // both directions 64 → 64 (stage 1): the W-stationary row-packed kernel (kernels_conv64.cu)
-        if (conv64_layer(c, op) && c->halo_fwd[op.layer] && c->halo_dgrad[op.layer]) c->conv64[op.layer] = 1;
+        if (conv64_layer(c, op) && c->halo_fwd[op.layer] && c->halo_dgrad[op.layer]) {
+            c->conv64[op.layer] = 1;
+            // the weight gradient's dY / X row runs: boxes of 1 … 8 padded rows (W + 2 pixels each)
+            const int gb = grad_src_buffer(c, op.dst);
+            const uint64_t dims[5] = {64, (uint64_t)Db.W, (uint64_t)Db.H, (uint64_t)B, (uint64_t)Sc};
+            const uint64_t str[4] = {128, (uint64_t)Db.W * 128, (uint64_t)Db.H * Db.W * 128,
+                                     (uint64_t)B * Db.H * Db.W * 128};
+            for (int h = 1; h <= 8; ++h) {
+                const uint32_t bx[5] = {64, (uint32_t)(Db.W + 2), (uint32_t)std::min(h, Db.H), 1, 1};
+                if (!make_map_nd(&c->rowmaps[op.layer].y[h - 1], c->rbf[gb].grad, 5, dims, str, bx) ||
+                    !make_map_nd(&c->rowmaps[op.layer].x[h - 1], c->rbf[op.src].val, 5, dims, str, bx))
+                    return c->set_err(BNN_ERR_CUDA, "tensor map (conv64 weight-gradient rows) failed");
+            }
+        }
     }
     // the stem (kernels_stem.cu): the 8-channel input as 1-row boxes of W + 2 pixels (OOB zero
     // columns), no swizzle (16-byte rows: the MMA's two K core matrices are two taps)
@@ -689,10 +703,10 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
                 w.eps_cluster = conv64_wgrad_eps_cluster(Sc);
                 w.nsplit = c->nsplit[op.layer] * (Sc / w.eps_cluster);  // partials: pixel splits × sample groups
                 int lrc = 0;
-                c->launch("wgrad", [&] { lrc = launch_conv64_wgrad_eps(c->cmap_hd[op.layer], c->cmap_hf[op.layer], w, ss); });
+                c->launch("wgrad", [&] { lrc = launch_conv64_wgrad_eps(c->rowmaps[op.layer], w, ss); });
                 if (lrc) return c->set_err(BNN_ERR_CUDA, "cluster launch of the ε-fused weight gradient refused");
             } else if (c->conv64[op.layer] && conv64w_layer(c, op))  // both halo window maps exist for conv64 layers
-                c->launch("wgrad", [&] { launch_conv64_wgrad(c->cmap_hd[op.layer], c->cmap_hf[op.layer], w, ss); });
+                c->launch("wgrad", [&] { launch_conv64_wgrad(c->rowmaps[op.layer], w, ss); });
             else
                 c->launch("wgrad", [&] { launch_conv2_wgrad(c->cmap_g[op.layer], c->cmap_xw[op.layer], w, ss); });
             cudaStream_t sc = ss;
