@@ -241,7 +241,7 @@ struct bnn_ctx {
     int64_t bias_rows_cap = 0;
     std::vector<char> wcps;  // conv2 weight gradient: CTAs per SM (1 or 2)
     std::vector<char> wgrad_eps;  // ε-fused, sample-accumulating weight gradient (no per-sample partials)
-    CUtensorMap cmap_stem;      // the stem input: 1-row (W + 2)-pixel boxes, 8 channels, no swizzle
+    StemRowMaps cmap_stem;      // the stem input: 1 … 8-row boxes of padded rows, 8 channels, no swizzle
     int stem_layer = -1;       // the layer on stem_fwd_kernel (-1: none)
     std::vector<Conv64RowMaps> rowmaps;  // conv64 weight gradient: multi-row TMA boxes
     std::vector<char> conv64;  // stage-1 64 → 64 layers on the W-stationary tap-paired kernel (both passes)

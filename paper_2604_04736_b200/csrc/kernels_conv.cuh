@@ -88,14 +88,18 @@ int conv3_halo_ok(int H, int W);
 // tap blocks resident in shared memory, loaded once per CTA and sample) and tap-paired (6 MMA
 // groups per 255-pixel tile of the padded stream); wmap = the 64-row K-major W map (fwd) or the
 // transposed map (dgrad), bmap = the HALO window map. Bias partials: conv64_parts per sample.
-void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
-void launch_conv64_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st);
+struct Conv64RowMaps;
+void launch_conv64_fwd(const CUtensorMap& wmap, const Conv64RowMaps& rows, const Conv2Args& a, cudaStream_t st);
+void launch_conv64_dgrad(const CUtensorMap& wmapT, const Conv64RowMaps& rows, const Conv2Args& a, cudaStream_t st);
 int conv64_parts(const Conv2Args& a);
 int conv64_ok(int H, int W);
 // stem (kernels_stem.cu): 3×3 stride-1 conv of the 8-channel input to 64 channels, pixels on M and two
 // taps per MMA (SWIZZLE_NONE K-major operands, the taps' distance as the leading byte offset);
 // xmap = 1-row (W + 2)-pixel boxes of the input, no swizzle; a.wsrc = the W scratch slot
-void launch_stem_fwd(const CUtensorMap& xmap, const Conv2Args& a, cudaStream_t st);
+struct StemRowMaps {  // boxes of 1 … 8 padded rows of the stem input
+    CUtensorMap x[8];
+};
+void launch_stem_fwd(const StemRowMaps& xmaps, const Conv2Args& a, cudaStream_t st);
 int stem_fwd_ok(const Conv2Args& a);
 int stem_row_pitch(int W);  // padded-row length of the stem window (the map box width)
 // conv64 weight gradient: the fp32 per-sample partials part[s][split][64][576] of the ε combine,

@@ -140,7 +140,7 @@ __device__ __forceinline__ float c64_transpose_sum(float* v, int lane) {
 #endif
 template <int MODE>
 __global__ void __launch_bounds__(c64::kThreads, 1)
-    conv64_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap bmap,
+    conv64_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ Conv64RowMaps rows,
                   const Conv2Args a) {
     using namespace c64;
     extern __shared__ uint8_t smem_raw[];
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
         // ------------------------------------------------ TMA producer: resident W, windows
         if (lane == 0) {
             tma_prefetch_desc(&wmap);
-            tma_prefetch_desc(&bmap);
+            const CUtensorMap* bm = MODE == 0 ? rows.x : rows.y;  // the window operand: X (fwd) / dY (dgrad)
             int cur_s = -1, seg = 0, tl = 0;
             for (int t = t0; t < t1; ++t, ++tl) {
                 const int s = t / ptiles, pt = t - s * ptiles;
@@ -225,9 +225,15 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
                 const int rs = c64_floor_div(p0 - PWp - 1, PWp), re = c64_floor_div(p0 + kTileM + PWp, PWp);
                 uint8_t* win = sWin + ws * kWin;
                 mbar_arrive_expect_tx(&wfull[ws], (uint32_t)((re - rs + 1) * PWp * 128));
-                for (int r = rs; r <= re; ++r) {
+                for (int r = rs; r <= re;) {  // one op per run of padded rows inside one image
                     const int b = c64_floor_div(r, PHp), y = r - b * PHp;  // y == PH: separator (OOB: zeros)
-                    tma_load_5d(&bmap, &wfull[ws], win + (r - rs) * PWp * 128, 0, -1, y, b, s);
+#ifdef C64_ROWS1  // A/B: one op per row
+                    const int run = 1;
+#else
+                    const int run = min(min(re, b * PHp + PH) - r + 1, min(8, PH));
+#endif
+                    tma_load_5d(&bm[run - 1], &wfull[ws], win + (r - rs) * PWp * 128, 0, -1, y, b, s);
+                    r += run;
                 }
             }
         }
@@ -800,17 +806,17 @@ int conv64_ok(int H, int W) {  // the padded window of a 128-row tile fits one w
 int conv64_parts(const Conv2Args& a) { return (a.B * (a.H + 1) * (a.W + 2) + c64::kTileP - 1) / c64::kTileP; }
 
 template <int MODE>
-static void launch_conv64(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
+static void launch_conv64(const CUtensorMap& wmap, const Conv64RowMaps& rows, const Conv2Args& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(conv64_kernel<MODE>), c64::kSmem);
     const int64_t T = (int64_t)a.S * conv64_parts(a);
-    conv64_kernel<MODE><<<(int)std::min<int64_t>(T, kNumSMs), c64::kThreads, c64::kSmem, st>>>(wmap, bmap, a);
+    conv64_kernel<MODE><<<(int)std::min<int64_t>(T, kNumSMs), c64::kThreads, c64::kSmem, st>>>(wmap, rows, a);
 }
 
-void launch_conv64_fwd(const CUtensorMap& wmap, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
-    launch_conv64<0>(wmap, bmap, a, st);
+void launch_conv64_fwd(const CUtensorMap& wmap, const Conv64RowMaps& rows, const Conv2Args& a, cudaStream_t st) {
+    launch_conv64<0>(wmap, rows, a, st);
 }
-void launch_conv64_dgrad(const CUtensorMap& wmapT, const CUtensorMap& bmap, const Conv2Args& a, cudaStream_t st) {
-    launch_conv64<1>(wmapT, bmap, a, st);
+void launch_conv64_dgrad(const CUtensorMap& wmapT, const Conv64RowMaps& rows, const Conv2Args& a, cudaStream_t st) {
+    launch_conv64<1>(wmapT, rows, a, st);
 }
 
 }  // namespace bnn

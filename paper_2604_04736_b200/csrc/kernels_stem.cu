@@ -62,7 +62,7 @@ __device__ __forceinline__ void st256s(void* p, const uint32_t* r) {
 }
 
 __global__ void __launch_bounds__(stem::kThreads, 1)
-    stem_fwd_kernel(const __grid_constant__ CUtensorMap xmap, const Conv2Args a) {
+    stem_fwd_kernel(const __grid_constant__ StemRowMaps xmaps, const Conv2Args a) {
     using namespace stem;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
 
     if (warp == WTMA) {
         if (lane == 0) {
-            tma_prefetch_desc(&xmap);
+
             for (int t = t0, tl = 0; t < t1; ++t, ++tl) {
                 const int s = t / ptiles, pt = t - s * ptiles;
                 const int ws = tl % kNWin;
@@ -119,10 +119,12 @@ __global__ void __launch_bounds__(stem::kThreads, 1)
                 const int p0 = pt * kTile;
                 const int rs = stem_floor_div(p0 - PWp - 1, PWp), re = stem_floor_div(p0 + kTile + PWp, PWp);
                 mbar_arrive_expect_tx(&wfull[ws], (uint32_t)((re - rs + 1) * PWp * 16));
-                for (int r = rs; r <= re; ++r) {
+                for (int r = rs; r <= re;) {  // one op per run of padded rows inside one image
                     const int b = stem_floor_div(r, PHp), y = r - b * PHp;  // y == PH, b ∉ [0, B): zeros
-                    tma_load_5d(&xmap, &wfull[ws], sWin + ws * kWin + (r - rs) * PWp * 16, 0, -1, y, b,
+                    const int run = min(min(re, b * PHp + PH) - r + 1, min(8, PH));
+                    tma_load_5d(&xmaps.x[run - 1], &wfull[ws], sWin + ws * kWin + (r - rs) * PWp * 16, 0, -1, y, b,
                                 a.src_stride_s == 0 ? 0 : s);
+                    r += run;
                 }
             }
         }
@@ -223,11 +225,11 @@ int stem_fwd_ok(const Conv2Args& a) {  // 3×3 stride-1 pad-1, 8 padded input ch
 
 int stem_row_pitch(int W) { return stem_pitch(W); }
 
-void launch_stem_fwd(const CUtensorMap& xmap, const Conv2Args& a, cudaStream_t st) {
+void launch_stem_fwd(const StemRowMaps& xmaps, const Conv2Args& a, cudaStream_t st) {
     ensure_smem_attr(reinterpret_cast<const void*>(stem_fwd_kernel), stem::kSmem);
     const int ptiles = (a.B * (a.H + 1) * stem_pitch(a.W) + stem::kTile - 1) / stem::kTile;
     const int64_t T = (int64_t)a.S * ptiles;
-    stem_fwd_kernel<<<(int)std::min<int64_t>(T, kNumSMs), stem::kThreads, stem::kSmem, st>>>(xmap, a);
+    stem_fwd_kernel<<<(int)std::min<int64_t>(T, kNumSMs), stem::kThreads, stem::kSmem, st>>>(xmaps, a);
     if (getenv("BNN_DEBUG_SYNC")) {
         cudaError_t e1 = cudaGetLastError(), e2 = cudaStreamSynchronize(st);
         fprintf(stderr, "stem_fwd_kernel: launch %s, sync %s (smem %d, threads %d)\n", cudaGetErrorString(e1),

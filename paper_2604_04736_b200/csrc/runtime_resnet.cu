@@ -329,9 +329,13 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         const bool shared = c->cfg.aug != BNN_AUG_PER_SAMPLE;
         const uint64_t dims[5] = {8, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B, (uint64_t)(shared ? 1 : Sc)};
         const uint64_t str[4] = {16, (uint64_t)Sb.W * 16, (uint64_t)Sb.H * Sb.W * 16, (uint64_t)B * Sb.H * Sb.W * 16};
-        const uint32_t box[5] = {8, (uint32_t)stem_row_pitch(Sb.W), 1, 1, 1};
-        if (make_map_nd(&c->cmap_stem, c->rbf[0].val, 5, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_NONE))
-            c->stem_layer = op.layer;
+        bool ok = true;
+        for (int h = 1; h <= 8; ++h) {
+            const uint32_t box[5] = {8, (uint32_t)stem_row_pitch(Sb.W), (uint32_t)std::min(h, Sb.H), 1, 1};
+            ok = ok && make_map_nd(&c->cmap_stem.x[h - 1], c->rbf[0].val, 5, dims, str, box, nullptr,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE);
+        }
+        if (ok) c->stem_layer = op.layer;
     }
     // stride-2 forward: the input window of a 2-strided conv is a TMA box with element stride 2
     // in W and H (box = 2·extent raw elements, every other one loaded); conv3 256-pixel and
@@ -535,7 +539,7 @@ void resnet_bf16_forward(bnn_ctx* c, const float* mu, const float* x, int Sc, in
             a.halo = c->halo_fwd[op.layer];
             const CUtensorMap& bm = a.halo ? c->cmap_hf[op.layer] : c->cmap_bf[op.layer];
             if (a.halo && c->conv64[op.layer])
-                c->launch("fwd", [&] { launch_conv64_fwd(c->cmap_w64[op.layer], bm, a, st); });
+                c->launch("fwd", [&] { launch_conv64_fwd(c->cmap_w64[op.layer], c->rowmaps[op.layer], a, st); });
             else
                 c->launch("fwd", [&] { launch_conv3_fwd(Db.C >= 128 ? c->cmap_w[op.layer] : c->cmap_w64[op.layer], bm, a, st); });
         } else {
@@ -799,7 +803,7 @@ int resnet_bf16_chunk(bnn_ctx* c, const float* mu, const float* x, const int32_t
         if (m_chan) {
             const CUtensorMap& bm = a.halo ? c->cmap_hd[op.layer] : c->cmap_bd[op.layer];
             if (a.halo && c->conv64[op.layer])
-                c->launch("dgrad", [&] { launch_conv64_dgrad(c->cmap_wT[op.layer], bm, a, st); });
+                c->launch("dgrad", [&] { launch_conv64_dgrad(c->cmap_wT[op.layer], c->rowmaps[op.layer], a, st); });
             else
                 c->launch("dgrad", [&] { launch_conv3_dgrad(c->cmap_wT[op.layer], bm, a, st); });
         } else {
