@@ -155,7 +155,7 @@ void launch_wgrad_eps_combine_stem(const SampledLayer& L, const SampleKeys& kk, 
                                    cudaStream_t st);
 int conv2_wgrad_ntile(int Kt);
 int conv2_wgrad_cps();
-int conv2_wgrad_nsplit(int base, int blocks);
+int conv2_wgrad_nsplit(int base, int blocks, int cps = 1);
 // partial columns: taps·C, or (stem, C_pad < 64) ⌈taps/8⌉·64
 inline int conv2_wgrad_cols(int taps, int C, int C_pad) { return C_pad < 64 ? ((taps + 7) / 8) * 64 : taps * C; }
 

@@ -1487,15 +1487,16 @@ void launch_wgrad_eps_combine_stem(const SampledLayer& L, const SampleKeys& kk, 
 
 // nsplit for `base` units per split: fewest waves per split (persistent grid of 148), and among
 // choices within 3 % of the best, the fewest splits (each split adds partial traffic)
-int conv2_wgrad_nsplit(int base, int blocks) {
+int conv2_wgrad_nsplit(int base, int blocks, int cps) {  // slots = cps CTAs per SM
+    const int slots = std::max(1, cps) * kNumSMs;
     double best = 1e30;
-    const int hi = std::max(1, std::min(blocks, 256));
+    const int hi = std::max(1, std::min(blocks, 512));
     for (int ns = 1; ns <= hi; ++ns) {
-        const int waves = (base * ns + kNumSMs - 1) / kNumSMs;
+        const int waves = (base * ns + slots - 1) / slots;
         best = std::min(best, (double)waves / ns);
     }
     for (int ns = 1; ns <= hi; ++ns) {
-        const int waves = (base * ns + kNumSMs - 1) / kNumSMs;
+        const int waves = (base * ns + slots - 1) / slots;
         if ((double)waves / ns <= best * 1.03) return ns;
     }
     return hi;

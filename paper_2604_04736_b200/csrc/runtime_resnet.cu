@@ -155,7 +155,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
             const int blocks = (int)((npix + c->wkpx[op.layer] - 1) / c->wkpx[op.layer]);
             const int epsn = eps_fused_nsplit(c, op, Sc);
             c->wgrad_eps[op.layer] = epsn > 0 ? 1 : 0;
-            c->nsplit[op.layer] = epsn > 0 ? epsn : conv64w_layer(c, op) ? conv64_wgrad_nsplit(Sc) : conv2_wgrad_nsplit(base, blocks);
+            c->nsplit[op.layer] = epsn > 0 ? epsn : conv64w_layer(c, op) ? conv64_wgrad_nsplit(Sc) : conv2_wgrad_nsplit(base, blocks, c->wcps[op.layer]);
             if (Ld.off_w % 4 != 0) return c->set_err(BNN_ERR_CONFIG, "conv weight offset not 16-byte aligned");
             // per-sample partials [s][split][co][cols], or (ε-fused) partials [split·group][μ | ρ][co·cols]
             // (≤ Sc sample groups for any chunk size)
