@@ -138,6 +138,14 @@ __device__ __forceinline__ float c64_transpose_sum(float* v, int lane) {
 #else
 #define C64_T(x)
 #endif
+#ifdef C64_LANE0_MMA
+#define C64_MMA mma_bf16
+#define C64_COMMIT mma_commit
+#else
+#define C64_MMA mma_bf16_warp
+#define C64_COMMIT mma_commit_warp
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(c64::kThreads, 1)
     conv64_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ Conv64RowMaps rows,
@@ -240,7 +248,10 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
         __syncwarp();
     } else if (warp == WMMA) {
         // ------------------------------------------------ MMA issuer: 3 kernel rows × 4 K-steps per tile
-        if (lane == 0) {
+#ifdef C64_LANE0_MMA  // A/B switch: lane 0 alone runs the loop
+        if (lane == 0)
+#endif
+        {  // the whole warp runs the loop (warp-uniform descriptor arithmetic), one lane issues
             const uint32_t idesc = idesc_bf16(kTileM, kN, 0, MODE == 1 ? 1 : 0);
             int cur_s = -1, seg = 0, tl = 0;
             for (int t = t0; t < t1; ++t, ++tl) {
@@ -265,21 +276,22 @@ __global__ void __launch_bounds__(c64::kThreads, 1)
                 const int p0 = pt * kTileP;
                 const int wrow0 = p0 - c64_floor_div(p0 - PWp - 1, PWp) * PWp;  // window row of pixel p0
                 const uint32_t winb = smem_u32(sWin + ws * kWin);
+                // descriptors of the (g, q) = (0, 0) operands; the others add their byte offset ÷ 16 to the
+                // start-address field (the smem addresses stay below 256 KB: no carry out of the field)
+                const uint64_t ad0 = sdesc_sw128(winb + (uint32_t)(wrow0 - PWp - 1) * 128u, 16, 1024);
+                const uint64_t bd0 = MODE == 0 ? sdesc_sw128(smem_u32(sW), 16, 1024) : sdesc_sw128(smem_u32(sW), kBlk, 1024);
 #pragma unroll
                 for (int g = 0; g < 3; ++g) {  // kernel row dh = g − 1, window at its dw = −1 tap
-                    const uint32_t aBase = winb + (uint32_t)(wrow0 + (g - 1) * PWp - 1) * 128u;
-                    const uint32_t bBase = smem_u32(sW + 3 * g * kBlk);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint64_t ad = sdesc_sw128(aBase + 32 * q, 16, 1024);
-                        const uint64_t bd = MODE == 0 ? sdesc_sw128(bBase + 32 * q, 16, 1024)
-                                                      : sdesc_sw128(bBase + 2048 * q, kBlk, 1024);
-                        mma_bf16(d, ad, bd, idesc, (g | q) != 0 ? 1u : 0u);
+                        const uint64_t ad = ad0 + (uint64_t)(g * PWp * 8 + 2 * q);
+                        const uint64_t bd = bd0 + (uint64_t)((3 * g * kBlk) / 16 + (MODE == 0 ? 2 * q : 128 * q));
+                        C64_MMA(d, ad, bd, idesc, (g | q) != 0 ? 1u : 0u);
                     }
                 }
-                mma_commit(&wempty[ws]);
-                mma_commit(&tfull[buf]);
-                if (t + 1 < t1 && (t + 1) / ptiles != s) mma_commit(wres_empty);  // W free for the next sample
+                C64_COMMIT(&wempty[ws]);
+                C64_COMMIT(&tfull[buf]);
+                if (t + 1 < t1 && (t + 1) / ptiles != s) C64_COMMIT(wres_empty);  // W free for the next sample
             }
         }
         __syncwarp();
