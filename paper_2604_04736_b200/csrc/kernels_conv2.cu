@@ -1152,8 +1152,9 @@ __global__ void __launch_bounds__(w2::kThreads, CPS)
                         for (int j = 0; j < nb; j += cbx) {
                             const int col = u.nt * 256 + 64 * j, tap = col / a.C, ci0 = col - tap * a.C;
                             const int kh = tap / a.k, kw = tap - kh * a.k;
+                            // stride 2: the map's W / H element stride is 2 (box = whole output rows)
                             tma_load_5d(&xmap, &full[st], sB + st * kBStage + j * blkB, 0, kw - a.pad,
-                                        y0 + kh - a.pad, u.s * a.B + n0, ci0 / 64);
+                                        a.stride * y0 + kh - a.pad, u.s * a.B + n0, ci0 / 64);
                         }
                     }
                 }

@@ -362,6 +362,23 @@ int alloc_resnet_bf16(bnn_ctx* c) {
                 return c->set_err(BNN_ERR_CUDA, "tensor map (stride-2 activation window) failed");
             (px == 256 ? c->tma_fwd : c->tma_a2f)[op.layer] = 1;
         }
+        // weight gradient: the X window of a 64-pixel k-step (whole output rows) with the same
+        // element stride 2, one op per run of channel blocks of a tap (as the stride-1 map above)
+        const int kp = c->wkpx[op.layer];
+        const int wh = PW >= kp ? 1 : std::min(PH, kp / PW);
+        const int wn = kp / (std::min(PW, kp) * wh);
+        if (env_on("BNN_WGRAD_S2_TMA") && kp == 64 && PW <= 64 && 64 % PW == 0 && PH % wh == 0 && wn >= 1 &&
+            Ld.cin % 64 == 0 && Cp == Ld.cin) {
+            const int cbx = std::min(4, Ld.cin / 64);
+            const uint64_t xd[5] = {64, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B * Sc, (uint64_t)(Cp / 64)};
+            const uint64_t xs[4] = {(uint64_t)Cp * 2, (uint64_t)Sb.W * Cp * 2, (uint64_t)Sb.H * Sb.W * Cp * 2, 128};
+            const uint32_t wbox[5] = {64, (uint32_t)(2 * std::min(PW, kp)), (uint32_t)(2 * wh), (uint32_t)wn,
+                                      (uint32_t)cbx};
+            const uint32_t wes[5] = {1, 2, 2, 1, 1};
+            if (!make_map_nd(&c->cmap_xw[op.layer], c->rbf[op.src].val, 5, xd, xs, wbox, wes))
+                return c->set_err(BNN_ERR_CUDA, "tensor map (stride-2 wgrad window) failed");
+            c->tma_wgrad[op.layer] = 1;
+        }
     }
     // stride-2 dgrad: each input-pixel parity class reads a plain shifted window of dY over the
     // output grid, so dY windows by TMA too (conv3: 256-pixel box; conv2: 128-pixel box below)

@@ -1217,6 +1217,31 @@ def test_cnn_bf16_conv64_wgrad_equals_conv2_wgrad(hw, B, S, monkeypatch):
     assert l1 == l0
 
 
+@pytest.mark.parametrize("hw,B,S", [(32, 2, 2), (16, 3, 3), (8, 5, 2), (32, 1, 8)])
+def test_cnn_bf16_stride2_wgrad_tma_equals_gather(hw, B, S, monkeypatch):
+    """Weight gradients of the stride-2 convs (3×3 and the 1×1 shortcuts) with the X window loaded
+    by TMA with element stride 2 in W and H against the cp.async gather of the same operand
+    (BNN_WGRAD_S2_TMA=0): the same bf16 operands in the same shared-memory layout, summed in the
+    same order, so acc_μ and acc_ρ of every tensor agree to 1e-6 of the tensor's max (a wrong
+    tap, row parity or image is O(1)); 8×8 inputs put several images in one box, B = 5 leaves a
+    ragged last k-step."""
+    native = _native()
+    model = dict(BF16_CNN, in_h=hw, in_w=hw)
+    mu, rho, x, yc, _ = _inputs(model, B, regime="positive")
+    accs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("BNN_WGRAD_S2_TMA", flag)
+        ctx = native.Context(model, precision="bf16", max_B_loc=B, max_S_loc=S, dataset_size=1e4, aug="per_sample")
+        accs.append(_acc_parts(ctx, ctx.elbo_partial(_dev(mu), _dev(rho), _dev(x), _dev(yc), B, S, 0xBEEF, 5)))
+        torch.cuda.synchronize()
+    (m0, r0, l0), (m1, r1, l1) = accs
+    for t in ctx.tensors:
+        sl = slice(t["offset"], t["offset"] + t["rows"] * t["cols"])
+        for name, u, ref in (("acc_mu", m1[sl], m0[sl]), ("acc_rho", r1[sl], r0[sl])):
+            assert np.abs(u - ref).max() <= 1e-6 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
+    assert l1 == l0
+
+
 @pytest.mark.parametrize("hw,B,S,chunk,cl", [(16, 3, 2, 0, None), (32, 2, 3, 0, None), (16, 2, 8, 0, None),
                                              (16, 2, 8, 0, "8"), (16, 2, 8, 0, "4"), (16, 2, 5, 2, None)])
 def test_cnn_bf16_eps_fused_wgrad_equals_combine(hw, B, S, chunk, cl, monkeypatch):
@@ -1272,7 +1297,8 @@ def test_cnn_bf16_stem_kernel_equals_conv3(hw, B, S, aug, monkeypatch):
             assert np.abs(u - ref).max() <= 1e-3 * max(np.abs(ref).max(), 1e-30), (t["t"], name)
 
 
-_OLD_PATHS = {"BNN_CONV64": "0", "BNN_STEM": "0", "BNN_WGRAD_EPS": "0", "BNN_CONV2_CPS": "1", "BNN_WGRAD_CPS": "1"}
+_OLD_PATHS = {"BNN_CONV64": "0", "BNN_STEM": "0", "BNN_WGRAD_EPS": "0", "BNN_CONV2_CPS": "1", "BNN_WGRAD_CPS": "1",
+              "BNN_WGRAD_S2_TMA": "0"}
 
 
 @pytest.mark.parametrize("hw,B,S", [(8, 1, 1), (24, 2, 1), (16, 1, 3), (8, 3, 8)])
