@@ -132,13 +132,17 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         if (Ld.cin % 64 == 0 || Cp_src == 8) {  // conv2 wgrad: units = samples × splits × co tiles × column tiles
             const int Kt = conv2_wgrad_cols(taps, Ld.cin, Cp_src);
             const int base = Sc * ((Ld.cout + 127) / 128) * ((Kt + 255) / 256);
-            // 64-channel stride-1 layers (TMA operand path): 128-pixel k-steps halve the TMA ops
+            // 64-channel layers on the TMA operand path: 128-pixel k-steps halve the TMA ops
             {
                 const RBuf& Sb0 = c->rbufs[op.src];
                 const int PW = D.W, PH = D.H, kp = 128;
                 const int wh = PW >= kp ? 1 : std::min(PH, kp / PW);
                 const bool shared = op.src == 0 && c->cfg.aug != BNN_AUG_PER_SAMPLE;
-                if (Ld.stride == 1 && Ld.cout <= 512 && Ld.cin % 64 == 0 && !shared && Sb0.W == PW &&
+                // stride 2: the same with the element-stride-2 X window (stage-3 stride-2 wgrad 85 → 76 µs;
+                // BNN_WGRAD_S2_KP128=0 keeps 64-pixel k-steps there)
+                const bool s2 = Ld.stride == 2 && Sb0.W == 2 * PW && op.src != 0 && Cp_src == Ld.cin &&
+                                env_on("BNN_WGRAD_S2_TMA") && env_on("BNN_WGRAD_S2_KP128");
+                if ((Ld.stride == 1 && Sb0.W == PW || s2) && Ld.cout <= 512 && Ld.cin % 64 == 0 && !shared &&
                     kp % PW == 0 && PH % wh == 0 && (kp / (PW * wh)) * PW * wh == kp)
                     c->wkpx[op.layer] = kp;
             }
@@ -367,7 +371,7 @@ int alloc_resnet_bf16(bnn_ctx* c) {
         const int kp = c->wkpx[op.layer];
         const int wh = PW >= kp ? 1 : std::min(PH, kp / PW);
         const int wn = kp / (std::min(PW, kp) * wh);
-        if (env_on("BNN_WGRAD_S2_TMA") && kp == 64 && PW <= 64 && 64 % PW == 0 && PH % wh == 0 && wn >= 1 &&
+        if (env_on("BNN_WGRAD_S2_TMA") && (kp == 64 || kp == 128) && PW <= 64 && kp % PW == 0 && PH % wh == 0 && wn >= 1 &&
             Ld.cin % 64 == 0 && Cp == Ld.cin) {
             const int cbx = std::min(4, Ld.cin / 64);
             const uint64_t xd[5] = {64, (uint64_t)Sb.W, (uint64_t)Sb.H, (uint64_t)B * Sc, (uint64_t)(Cp / 64)};
