@@ -23,6 +23,14 @@
 
 namespace bnn {
 
+// The MMA issuers fence the async proxy after a stage fills only when gather warps wrote it with
+// generic-proxy stores; TMA-filled stages need no fence (-DBNN_ALWAYS_PROXY_FENCE restores it).
+#ifdef BNN_ALWAYS_PROXY_FENCE
+constexpr bool kAlwaysFence = true;
+#else
+constexpr bool kAlwaysFence = false;
+#endif
+
 using namespace ptx;
 
 // pipeline depth cap (BNN_CONV_STAGES, default 4; ≤ 12), passed as a launch argument
@@ -369,7 +377,7 @@ __global__ void __launch_bounds__(c2::kThreads, CPS)
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
                     mbar_wait_role(&full[st], ph);
-                    fence_proxy_async_smem();
+                    if (kAlwaysFence || !(a.tma_a)) fence_proxy_async_smem();  // gathered (generic-proxy) operands only
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
                     const uint32_t bBase = smem_u32(sB + st * kBStage);
@@ -776,7 +784,7 @@ __global__ void __launch_bounds__(HALO ? c3::kThreadsH : c3::kThreads, 1)
 #ifdef C3_PROF
                     p_full += clock64() - q2;
 #endif
-                    fence_proxy_async_smem();
+                    if (kAlwaysFence || !(a.tma_a || HALO)) fence_proxy_async_smem();  // gathered (generic-proxy) operands only
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
                     uint32_t bBase = smem_u32(sB + st * kBStage);
@@ -1176,7 +1184,7 @@ __global__ void __launch_bounds__(w2::kThreads, CPS)
                     const int st = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
                     mbar_wait_role(&full[st], ph);
-                    fence_proxy_async_smem();
+                    if (kAlwaysFence || !(a.tma_b)) fence_proxy_async_smem();  // gathered (generic-proxy) operands only
                     tc_fence_after();
                     const uint32_t aBase = smem_u32(sA + st * kAStage);
                     const uint32_t bBase = smem_u32(sB + st * kBStage);
